@@ -1,0 +1,151 @@
+"""CPU oracle for the AMG-PCG solve phase — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product library
+(``paper_2406_19754_b200``) never does, and shares no code with it.
+
+Thin ctypes marshalling over ``oracle/psc_oracle.c`` (plain C, fp64,
+single-threaded, no fast-math, no FMA contraction).  Each C function cites the
+PAPER.md passage it implements.  Pins (tests that tie the oracle to the paper
+and to mathematics rather than to itself) live in ``tests/test_oracle_pins.py``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+STATUS = {0: "converged", 1: "not converged", -6: "breakdown"}
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "psc_oracle.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-fPIC",
+                               "-shared", "-o", tmp, src, "-lm"])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+class _CSR(ctypes.Structure):
+    _fields_ = [("nrows", ctypes.c_int64), ("ncols", ctypes.c_int64), ("ptr", ctypes.c_void_p),
+                ("col", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
+class _Hier(ctypes.Structure):
+    _fields_ = [("nlevels", ctypes.c_int), ("A", ctypes.POINTER(_CSR)), ("P", ctypes.POINTER(_CSR)),
+                ("R", ctypes.POINTER(_CSR)), ("pre", ctypes.c_int), ("post", ctypes.c_int),
+                ("coarse", ctypes.c_int)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        vp = ctypes.c_void_p
+        L.or_spmv.argtypes = [vp, vp, vp]
+        L.or_l1_diag.argtypes = [vp, vp]
+        L.or_l1_sweep.argtypes = [vp, vp, vp, vp, vp]
+        L.or_l1_sweeps_from_zero.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp]
+        L.or_vcycle.argtypes = [vp, vp, vp]
+        L.or_pcg.argtypes = [vp, vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int)]
+        L.or_pcg.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _arr(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+class _CsrHolder:
+    """Keeps the numpy buffers alive for the lifetime of the C struct."""
+
+    def __init__(self, m):
+        if hasattr(m, "indptr"):  # scipy.sparse
+            m = m.tocsr()
+            m.sort_indices()
+            shape, ptr, col, val = m.shape, m.indptr, m.indices, m.data
+        else:  # pscgen.CSR duck type
+            shape, ptr, col, val = m.shape, m.ptr, m.col, m.val
+        self.ptr = _arr(ptr, np.int64)
+        self.col = _arr(col, np.int64)
+        self.val = _arr(val, np.float64)
+        self.c = _CSR(shape[0], shape[1], self.ptr.ctypes.data, self.col.ctypes.data, self.val.ctypes.data)
+
+
+class _HierHolder:
+    def __init__(self, hier, pre=4, post=4, coarse=30):
+        L = hier.nlevels
+        self.A = [_CsrHolder(hier.levels[l].A) for l in range(L)]
+        self.P = [_CsrHolder(hier.levels[l].P) for l in range(L - 1)]
+        self.R = [_CsrHolder(hier.levels[l].R) for l in range(L - 1)]
+        self.Aa = (_CSR * L)(*[h.c for h in self.A])
+        self.Pa = (_CSR * max(L - 1, 1))(*[h.c for h in self.P])
+        self.Ra = (_CSR * max(L - 1, 1))(*[h.c for h in self.R])
+        self.c = _Hier(L, self.Aa, self.Pa, self.Ra, pre, post, coarse)
+
+
+def spmv(A, x) -> np.ndarray:
+    h = _CsrHolder(A)
+    x = _arr(x, np.float64)
+    y = np.empty(h.c.nrows, np.float64)
+    lib().or_spmv(ctypes.byref(h.c), x.ctypes.data, y.ctypes.data)
+    return y
+
+
+def l1_diag(A) -> np.ndarray:
+    h = _CsrHolder(A)
+    m = np.empty(h.c.nrows, np.float64)
+    lib().or_l1_diag(ctypes.byref(h.c), m.ctypes.data)
+    return m
+
+
+def l1_sweep(A, b, x) -> np.ndarray:
+    """One sweep x + M^{-1}(b - A x) (Eq. (2) right factor)."""
+    h = _CsrHolder(A)
+    m = l1_diag(A)
+    b, x = _arr(b, np.float64), _arr(x, np.float64)
+    out = np.empty_like(x)
+    lib().or_l1_sweep(ctypes.byref(h.c), m.ctypes.data, b.ctypes.data, x.ctypes.data, out.ctypes.data)
+    return out
+
+
+def l1_sweeps_from_zero(A, b, nsweeps: int) -> np.ndarray:
+    h = _CsrHolder(A)
+    m = l1_diag(A)
+    b = _arr(b, np.float64)
+    x = np.empty(h.c.nrows, np.float64)
+    w = np.empty(h.c.nrows, np.float64)
+    lib().or_l1_sweeps_from_zero(ctypes.byref(h.c), m.ctypes.data, b.ctypes.data, int(nsweeps), x.ctypes.data,
+                                 w.ctypes.data)
+    return x
+
+
+def vcycle(hier, r, pre=4, post=4, coarse=30) -> np.ndarray:
+    """z = B_0 r, Eq. (2)."""
+    hh = _HierHolder(hier, pre, post, coarse)
+    r = _arr(r, np.float64)
+    z = np.empty_like(r)
+    lib().or_vcycle(ctypes.byref(hh.c), r.ctypes.data, z.ctypes.data)
+    return z
+
+
+def pcg(hier, b, x0=None, tol=1e-8, maxit=200, pre=4, post=4, coarse=30):
+    """PCG preconditioned by one V-cycle per iteration.  Returns (x, iters, status, hist)."""
+    hh = _HierHolder(hier, pre, post, coarse)
+    b = _arr(b, np.float64)
+    x = np.zeros_like(b) if x0 is None else _arr(x0, np.float64).copy()
+    hist = np.full(maxit + 1, np.nan)
+    it = ctypes.c_int(0)
+    st = lib().or_pcg(ctypes.byref(hh.c), b.ctypes.data, x.ctypes.data, float(tol), int(maxit), hist.ctypes.data,
+                      ctypes.byref(it))
+    return x, it.value, st, hist[: it.value + 1]

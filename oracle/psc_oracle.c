@@ -1,0 +1,199 @@
+/* psc_oracle.c — CPU ORACLE for the AMG-PCG solve phase.  TEST INFRASTRUCTURE.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may load
+ * this.  It shares no code with the CUDA library (paper_2406_19754_b200/): no
+ * headers, no helpers, no constants.  Plain, slow, single-threaded, IEEE-754
+ * binary64, compiled without fast-math and with -ffp-contract=off so every
+ * a*b+c below is a rounded multiply followed by a rounded add.
+ *
+ * Every function follows PAPER.md (arXiv 2406.19754) step by step; `P:n` is a
+ * PAPER.md line, with its section / equation.  Readings of silent or garbled
+ * points are DESIGN.md §3 R1..R22.
+ *
+ * Matrices are global CSR (int64 row_ptr, int64 column, f64 value).  The
+ * hierarchy {A_l, P_l, R_l} is GIVEN (BASELINE.json north_star).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  int64_t nrows, ncols;
+  const int64_t* ptr;
+  const int64_t* col;
+  const double* val;
+} or_csr;
+
+typedef struct {
+  int nlevels;      /* L: level 0 finest, L-1 coarsest */
+  const or_csr* A;  /* A[0..L-1] */
+  const or_csr* P;  /* P[0..L-2], n_l x n_{l+1} */
+  const or_csr* R;  /* R[0..L-2], n_{l+1} x n_l, R_l = P_l^T given explicitly */
+  int pre, post;    /* smoothing sweeps before/after the coarse correction (R4: 4 and 4) */
+  int coarse;       /* l1-Jacobi sweeps at the coarsest level (30) */
+} or_hier;
+
+/* y = A x.  Row sums in stored column order. */
+void or_spmv(const or_csr* A, const double* x, double* y) {
+  for (int64_t i = 0; i < A->nrows; ++i) {
+    double s = 0.0;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) s += A->val[k] * x[A->col[k]];
+    y[i] = s;
+  }
+}
+
+/* l1-Jacobi smoother matrix, P:269-272 (Sec. 2.3.2):
+ *   M_l = diag(A_l) + diag( { sum_{j=1, j!=i}^{N} |a_ij| }_i )
+ * over the whole row (reading R7).  m[i] is the i-th diagonal entry of M_l. */
+void or_l1_diag(const or_csr* A, double* m) {
+  for (int64_t i = 0; i < A->nrows; ++i) {
+    double aii = 0.0, off = 0.0;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) {
+      if (A->col[k] == i) aii = A->val[k];
+      else off += fabs(A->val[k]);
+    }
+    m[i] = aii + off;
+  }
+}
+
+/* One smoothing sweep x_new = x + M^{-1} (b - A x) (the factor (I - M^{-1}A)
+ * of Eq. (2)), Jacobi: every row reads the old x (reading R8). */
+void or_l1_sweep(const or_csr* A, const double* m, const double* b, const double* x, double* xnew) {
+  for (int64_t i = 0; i < A->nrows; ++i) {
+    double s = 0.0;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) s += A->val[k] * x[A->col[k]];
+    xnew[i] = x[i] + (b[i] - s) / m[i];
+  }
+}
+
+/* nsweeps sweeps starting from x = 0 (reading R6: smoothers start from zero).
+ * Result in x.  work: n doubles. */
+void or_l1_sweeps_from_zero(const or_csr* A, const double* m, const double* b, int nsweeps, double* x,
+                            double* work) {
+  const int64_t n = A->nrows;
+  memset(x, 0, sizeof(double) * (size_t)n);
+  for (int s = 0; s < nsweeps; ++s) {
+    or_l1_sweep(A, m, b, x, work);
+    memcpy(x, work, sizeof(double) * (size_t)n);
+  }
+}
+
+static double* dalloc(int64_t n) { return (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double)); }
+
+/* x = B_l b, the V-cycle of Eq. (2) (Sec. 2.3):
+ *   I - B_l A_l = (I - M_l^{-T} A_l)(I - P_l B_{l+1} P_l^T A_l)(I - M_l^{-1} A_l),
+ * applied to b with x = 0 on entry, i.e. right to left:
+ *   pre:    x <- x + M^{-1}(b - A x), `pre` times                 (rightmost factor)
+ *   coarse: x <- x + P B_{l+1} R (b - A x), R = P^T              (middle factor)
+ *   post:   x <- x + M^{-T}(b - A x), `post` times; M diagonal so M^{-T} = M^{-1} (R9)
+ * and B_ell at the coarsest level = `coarse` sweeps from zero. */
+static void vcycle_level(const or_hier* h, double* const* m, int l, const double* b, double* x) {
+  const or_csr* A = &h->A[l];
+  const int64_t n = A->nrows;
+  double* w = dalloc(n);
+  if (l == h->nlevels - 1) {
+    or_l1_sweeps_from_zero(A, m[l], b, h->coarse, x, w);
+    free(w);
+    return;
+  }
+  or_l1_sweeps_from_zero(A, m[l], b, h->pre, x, w);
+  /* coarse-grid correction */
+  const or_csr* R = &h->R[l];
+  const or_csr* P = &h->P[l];
+  const int64_t nc = R->nrows;
+  double* r = dalloc(n);
+  double* bc = dalloc(nc);
+  double* xc = dalloc(nc);
+  or_spmv(A, x, r);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
+  or_spmv(R, r, bc);
+  vcycle_level(h, m, l + 1, bc, xc);
+  or_spmv(P, xc, r);
+  for (int64_t i = 0; i < n; ++i) x[i] = x[i] + r[i];
+  free(r);
+  free(bc);
+  free(xc);
+  for (int s = 0; s < h->post; ++s) {
+    or_l1_sweep(A, m[l], b, x, w);
+    memcpy(x, w, sizeof(double) * (size_t)n);
+  }
+  free(w);
+}
+
+static double** make_m(const or_hier* h) {
+  double** m = (double**)calloc((size_t)h->nlevels, sizeof(double*));
+  for (int l = 0; l < h->nlevels; ++l) {
+    m[l] = dalloc(h->A[l].nrows);
+    or_l1_diag(&h->A[l], m[l]);
+  }
+  return m;
+}
+static void free_m(const or_hier* h, double** m) {
+  for (int l = 0; l < h->nlevels; ++l) free(m[l]);
+  free(m);
+}
+
+/* z = B_0 r (one V-cycle from x = 0). */
+void or_vcycle(const or_hier* h, const double* r, double* z) {
+  double** m = make_m(h);
+  vcycle_level(h, m, 0, r, z);
+  free_m(h, m);
+}
+
+static double dot(int64_t n, const double* a, const double* b) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+/* Preconditioned CG (reading R1: PCG, equal to FCG(1) for a fixed SPD B;
+ * P:113-117) with B = one V-cycle per iteration.
+ * Stopping rule hist[k] = ||r_k||_2/||b||_2 <= tol on the recurrence residual
+ * (reading R2).  x holds x_0 on entry (Fig. 6 caption), the solution on exit.
+ * hist: maxit+1 doubles.  Returns 0 converged, 1 not converged, -6 breakdown
+ * (p^T A p <= 0 or not finite).  *iters = iterations performed. */
+int or_pcg(const or_hier* h, const double* b, double* x, double tol, int maxit, double* hist, int* iters) {
+  const or_csr* A = &h->A[0];
+  const int64_t n = A->nrows;
+  *iters = 0;
+  const double nb = sqrt(dot(n, b, b));
+  if (nb == 0.0) { /* b = 0 -> x = 0, no iterations (R10) */
+    memset(x, 0, sizeof(double) * (size_t)n);
+    hist[0] = 0.0;
+    return 0;
+  }
+  double** m = make_m(h);
+  double* r = dalloc(n);
+  double* z = dalloc(n);
+  double* p = dalloc(n);
+  double* q = dalloc(n);
+  int status = 1;
+  or_spmv(A, x, r);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
+  hist[0] = sqrt(dot(n, r, r)) / nb;
+  if (hist[0] <= tol) { status = 0; goto done; }
+  vcycle_level(h, m, 0, r, z);
+  memcpy(p, z, sizeof(double) * (size_t)n);
+  double rz = dot(n, r, z);
+  for (int k = 1; k <= maxit; ++k) {
+    or_spmv(A, p, q);
+    const double pq = dot(n, p, q);
+    if (!(pq > 0.0) || !isfinite(pq)) { status = -6; *iters = k; goto done; }
+    const double alpha = rz / pq;
+    for (int64_t i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
+    for (int64_t i = 0; i < n; ++i) r[i] = r[i] - alpha * q[i];
+    hist[k] = sqrt(dot(n, r, r)) / nb;
+    *iters = k;
+    if (hist[k] <= tol) { status = 0; goto done; }
+    vcycle_level(h, m, 0, r, z);
+    const double rz_new = dot(n, r, z);
+    const double beta = rz_new / rz;
+    rz = rz_new;
+    for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+  }
+done:
+  free(r); free(z); free(p); free(q);
+  free_m(h, m);
+  return status;
+}

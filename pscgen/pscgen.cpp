@@ -1,0 +1,521 @@
+// pscgen.cpp — seeded input generator for the AMG-PCG solve phase.
+//
+// INPUT GENERATOR, NOT THE METHOD'S SOLVE PATH.  The north star (BASELINE.json)
+// takes the aggregation hierarchy {A_l, P_l, R_l = P_l^T} as a *given* input;
+// this file builds that input the way PSCToolkit's VBM set-up describes it, so
+// that both the CUDA library (paper_2406_19754_b200/) and the CPU oracle
+// (oracle/) can be fed the same matrices.  It contains none of the solve-phase
+// arithmetic (no l1 diagonal, no smoothing sweep, no V-cycle, no CG); those live
+// separately in the oracle and in the CUDA library and share no code.
+//
+// What is built (citations are PAPER.md line numbers + section):
+//   * A_0: 7-point finite-difference 3D Poisson, -lap u = 1 on [0,1]^3 with
+//     homogeneous Dirichlet boundary (Sec. 3), unscaled stencil
+//     (6, -1) (reading R15); or the variable-coefficient diffusion of
+//     BASELINE.json config 5 (reading R22).
+//   * Row-block distribution by boxes: rank r owns a box of the grid and a
+//     contiguous block of global rows (Sec. 2.1 "partitioning the index
+//     space among processes"); numbering is rank-major, x-fastest in the box.
+//   * Decoupled Vanek-Mandel-Brezina aggregation (Sec. 2.3.1): strong
+//     set N_i(theta) = { j : |a_ij| >= theta sqrt(a_ii a_jj) }; aggregates never
+//     cross a rank boundary ("decoupled").  Classical three phases (reading R18).
+//   * Tentative prolongator Eq. (3) with near-kernel w = 1.
+//   * Smoothed prolongator P = (I - omega D^-1 A) P^ with omega = 1/||D^-1 A||_inf
+//     (P:240).
+//   * Explicit restriction R = P^T (BASELINE.json north_star).
+//   * Galerkin coarse operator A_{l+1} = P_l^T A_l P_l.
+//
+// Everything is computed for all ranks inside one process (logical ranks), with
+// OpenMP over rows.  The global CSR of each level is the concatenation of the
+// rank blocks, so rank r's piece is a contiguous row range.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <vector>
+#include <omp.h>
+
+namespace {
+
+template <class T>
+struct Buf {  // uninitialised heap array (avoids zero-filling multi-GB vectors)
+  std::unique_ptr<T[]> p;
+  int64_t n = 0;
+  void alloc(int64_t m) { p.reset(m ? new T[m] : nullptr); n = m; }
+  T& operator[](int64_t i) { return p[i]; }
+  const T& operator[](int64_t i) const { return p[i]; }
+  T* data() { return p.get(); }
+};
+
+struct CSR {
+  int64_t nrows = 0, ncols = 0;
+  Buf<int64_t> ptr;  // nrows+1
+  Buf<int64_t> col;  // nnz, strictly increasing per row
+  Buf<double> val;   // nnz
+  int64_t nnz() const { return nrows ? ptr[nrows] : 0; }
+};
+
+struct Level {
+  int64_t n = 0;
+  std::vector<int64_t> row_start;  // nranks+1
+  CSR A, P, R;                     // P: n x n_next, R: n_next x n (absent at coarsest)
+  std::vector<int64_t> agg;        // fine node -> global coarse id (absent at coarsest)
+};
+
+struct Hier {
+  int nranks = 1;
+  std::vector<Level> lv;
+  double omega_last = 0.0;
+  std::vector<double> omega;  // per level (l < L-1)
+};
+
+// Chunked parallel CSR builder: rows [0, nrows) are cut into chunks; each chunk
+// is filled by one thread into private vectors, then concatenated in row order.
+struct ChunkOut {
+  std::vector<int64_t> len;  // per row
+  std::vector<int64_t> col;
+  std::vector<double> val;
+};
+
+template <class RowFn>
+void build_csr_chunked(CSR& out, int64_t nrows, int64_t ncols, RowFn&& row_fn) {
+  const int64_t CH = 8192;
+  const int64_t nch = (nrows + CH - 1) / CH;
+  std::vector<ChunkOut> chunks(nch);
+#pragma omp parallel
+  {
+    auto st = row_fn.make_state();
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nch; ++c) {
+      ChunkOut& co = chunks[c];
+      const int64_t r0 = c * CH, r1 = std::min(nrows, r0 + CH);
+      co.len.resize(r1 - r0);
+      for (int64_t i = r0; i < r1; ++i) {
+        size_t before = co.col.size();
+        row_fn(st, i, co.col, co.val);
+        co.len[i - r0] = (int64_t)(co.col.size() - before);
+      }
+    }
+  }
+  std::vector<int64_t> coff(nch + 1, 0);
+  for (int64_t c = 0; c < nch; ++c) coff[c + 1] = coff[c] + (int64_t)chunks[c].col.size();
+  out.nrows = nrows;
+  out.ncols = ncols;
+  out.ptr.alloc(nrows + 1);
+  out.col.alloc(coff[nch]);
+  out.val.alloc(coff[nch]);
+  out.ptr[0] = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t c = 0; c < nch; ++c) {
+    ChunkOut& co = chunks[c];
+    const int64_t r0 = c * CH;
+    int64_t o = coff[c];
+    for (size_t k = 0; k < co.len.size(); ++k) {
+      o += co.len[k];
+      out.ptr[r0 + (int64_t)k + 1] = o;
+    }
+    std::memcpy(out.col.data() + coff[c], co.col.data(), co.col.size() * sizeof(int64_t));
+    std::memcpy(out.val.data() + coff[c], co.val.data(), co.val.size() * sizeof(double));
+    std::vector<int64_t>().swap(co.col);
+    std::vector<double>().swap(co.val);
+  }
+}
+
+// ---------------------------------------------------------------- A_0 (grid)
+struct Grid {
+  int64_t nx, ny, nz;  // global grid points
+  int px, py, pz;      // process grid
+  int64_t bx, by, bz;  // box per rank
+  int64_t box_n() const { return bx * by * bz; }
+  int64_t gidx(int64_t gx, int64_t gy, int64_t gz) const {
+    int64_t rx = gx / bx, ry = gy / by, rz = gz / bz;
+    int64_t r = rx + px * (ry + py * rz);
+    int64_t lx = gx - rx * bx, ly = gy - ry * by, lz = gz - rz * bz;
+    return r * box_n() + lx + bx * (ly + by * lz);
+  }
+  void coords(int64_t g, int64_t& gx, int64_t& gy, int64_t& gz) const {
+    int64_t r = g / box_n(), li = g - r * box_n();
+    int64_t rx = r % px, ry = (r / px) % py, rz = r / ((int64_t)px * py);
+    int64_t lx = li % bx, ly = (li / bx) % by, lz = li / (bx * by);
+    gx = rx * bx + lx;
+    gy = ry * by + ly;
+    gz = rz * bz + lz;
+  }
+};
+
+// Variable-coefficient diffusion (reading R22): kappa = jump on a checkerboard
+// of `cube`^3-cell cubes in global coordinates, else 1; face coefficient is the
+// harmonic mean 2 k_i k_j/(k_i + k_j); a Dirichlet face contributes k_i.
+struct Coef {
+  int problem;  // 0 = Poisson, 1 = jump
+  double jump;
+  int64_t cube;
+  double kappa(int64_t gx, int64_t gy, int64_t gz) const {
+    if (problem == 0) return 1.0;
+    int64_t s = gx / cube + gy / cube + gz / cube;
+    return (s & 1) ? jump : 1.0;
+  }
+};
+
+struct StencilRow {
+  const Grid* g;
+  const Coef* cf;
+  int make_state() const { return 0; }
+  void operator()(int&, int64_t i, std::vector<int64_t>& col, std::vector<double>& val) const {
+    int64_t gx, gy, gz;
+    g->coords(i, gx, gy, gz);
+    const double ki = cf->kappa(gx, gy, gz);
+    int64_t c[7];
+    double v[7];
+    int m = 0;
+    double diag = 0.0;
+    const int64_t d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+    for (int f = 0; f < 6; ++f) {
+      int64_t x = gx + d[f][0], y = gy + d[f][1], z = gz + d[f][2];
+      if (x < 0 || y < 0 || z < 0 || x >= g->nx || y >= g->ny || z >= g->nz) {
+        diag += ki;  // Dirichlet face
+        continue;
+      }
+      double kj = cf->kappa(x, y, z);
+      double t = (cf->problem == 0) ? 1.0 : 2.0 * ki * kj / (ki + kj);
+      diag += t;
+      c[m] = g->gidx(x, y, z);
+      v[m] = -t;
+      ++m;
+    }
+    c[m] = i;
+    v[m] = diag;
+    ++m;
+    // insertion sort by column
+    for (int a = 1; a < m; ++a) {
+      int64_t cc = c[a];
+      double vv = v[a];
+      int b = a - 1;
+      while (b >= 0 && c[b] > cc) { c[b + 1] = c[b]; v[b + 1] = v[b]; --b; }
+      c[b + 1] = cc;
+      v[b + 1] = vv;
+    }
+    for (int a = 0; a < m; ++a) { col.push_back(c[a]); val.push_back(v[a]); }
+  }
+};
+
+// ------------------------------------------------------------- aggregation
+// Decoupled VMB on one rank's block [r0, r1) of level matrix A (global CSR).
+// Returns the number of aggregates; agg_local[i - r0] = local aggregate id.
+int64_t vmb_aggregate_rank(const CSR& A, const double* diag, int64_t r0, int64_t r1, double theta,
+                           int64_t* agg_local) {
+  const int64_t nloc = r1 - r0;
+  // strong sets (owned, j != i)
+  std::vector<int64_t> sptr(nloc + 1, 0);
+  std::vector<int64_t> sidx;
+  std::vector<double> sstr;
+  sidx.reserve((size_t)(A.ptr[r1] - A.ptr[r0]));
+  sstr.reserve((size_t)(A.ptr[r1] - A.ptr[r0]));
+  for (int64_t i = r0; i < r1; ++i) {
+    for (int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+      int64_t j = A.col[k];
+      if (j == i || j < r0 || j >= r1) continue;
+      double s = std::sqrt(diag[i] * diag[j]);
+      double a = std::fabs(A.val[k]);
+      if (a >= theta * s) {
+        sidx.push_back(j - r0);
+        sstr.push_back(a / s);
+      }
+    }
+    sptr[i - r0 + 1] = (int64_t)sidx.size();
+  }
+  for (int64_t i = 0; i < nloc; ++i) agg_local[i] = -1;
+  int64_t nagg = 0;
+  // Phase 1: i and all its strong neighbours unaggregated -> new aggregate.
+  for (int64_t i = 0; i < nloc; ++i) {
+    if (agg_local[i] != -1) continue;
+    bool free_nb = true;
+    for (int64_t k = sptr[i]; k < sptr[i + 1]; ++k)
+      if (agg_local[sidx[k]] != -1) { free_nb = false; break; }
+    if (!free_nb) continue;
+    agg_local[i] = nagg;
+    for (int64_t k = sptr[i]; k < sptr[i + 1]; ++k) agg_local[sidx[k]] = nagg;
+    ++nagg;
+  }
+  // Phase 2: join the phase-1 aggregate of the strongest strong neighbour
+  // (snapshot of phase 1; ties -> lowest aggregate id).
+  std::vector<int64_t> snap(agg_local, agg_local + nloc);
+  for (int64_t i = 0; i < nloc; ++i) {
+    if (snap[i] != -1) continue;
+    double best = -1.0;
+    int64_t bagg = -1;
+    for (int64_t k = sptr[i]; k < sptr[i + 1]; ++k) {
+      int64_t a = snap[sidx[k]];
+      if (a == -1) continue;
+      if (sstr[k] > best || (sstr[k] == best && a < bagg)) { best = sstr[k]; bagg = a; }
+    }
+    if (bagg != -1) agg_local[i] = bagg;
+  }
+  // Phase 3: leftovers form aggregates with their unaggregated strong neighbours.
+  for (int64_t i = 0; i < nloc; ++i) {
+    if (agg_local[i] != -1) continue;
+    agg_local[i] = nagg;
+    for (int64_t k = sptr[i]; k < sptr[i + 1]; ++k)
+      if (agg_local[sidx[k]] == -1) agg_local[sidx[k]] = nagg;
+    ++nagg;
+  }
+  return nagg;
+}
+
+// ---------------------------------------------------------- prolongator
+struct SmoothedPRow {
+  const CSR* A;
+  const double* diag;
+  const int64_t* agg;
+  double omega;
+  bool smooth;
+  int make_state() const { return 0; }
+  void operator()(int&, int64_t i, std::vector<int64_t>& col, std::vector<double>& val) const {
+    if (!smooth) {  // tentative prolongator, Eq. (3) with w = 1
+      col.push_back(agg[i]);
+      val.push_back(1.0);
+      return;
+    }
+    // P_i. = e_{agg(i)} - (omega / a_ii) * sum_k a_ik e_{agg(k)}
+    const int64_t k0 = A->ptr[i], k1 = A->ptr[i + 1];
+    const size_t base = col.size();
+    for (int64_t k = k0; k < k1; ++k) {
+      int64_t J = agg[A->col[k]];
+      double a = A->val[k];
+      size_t t = base;
+      while (t < col.size() && col[t] != J) ++t;
+      if (t == col.size()) { col.push_back(J); val.push_back(a); }
+      else val[t] += a;
+    }
+    const double s = omega / diag[i];
+    bool have_own = false;
+    for (size_t t = base; t < col.size(); ++t) {
+      double v = -s * val[t];
+      if (col[t] == agg[i]) { v = 1.0 + v; have_own = true; }
+      val[t] = v;
+    }
+    if (!have_own) { col.push_back(agg[i]); val.push_back(1.0); }
+    // sort the row by column
+    const size_t m = col.size() - base;
+    for (size_t a = 1; a < m; ++a) {
+      int64_t cc = col[base + a];
+      double vv = val[base + a];
+      size_t b = a;
+      while (b > 0 && col[base + b - 1] > cc) { col[base + b] = col[base + b - 1]; val[base + b] = val[base + b - 1]; --b; }
+      col[base + b] = cc;
+      val[base + b] = vv;
+    }
+  }
+};
+
+void transpose(const CSR& P, CSR& R) {
+  const int64_t n = P.nrows, nc = P.ncols, nnz = P.nnz();
+  R.nrows = nc;
+  R.ncols = n;
+  R.ptr.alloc(nc + 1);
+  R.col.alloc(nnz);
+  R.val.alloc(nnz);
+  std::vector<int64_t> cnt(nc + 1, 0);
+  for (int64_t k = 0; k < nnz; ++k) cnt[P.col[k] + 1]++;
+  for (int64_t c = 0; c < nc; ++c) cnt[c + 1] += cnt[c];
+  for (int64_t c = 0; c <= nc; ++c) R.ptr[c] = cnt[c];
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = P.ptr[i]; k < P.ptr[i + 1]; ++k) {
+      int64_t c = P.col[k];
+      int64_t o = cnt[c]++;
+      R.col[o] = i;
+      R.val[o] = P.val[k];
+    }
+}
+
+// Galerkin product rows: A_c[J,:] = sum_i R[J,i] sum_k A[i,k] P[k,:]
+struct RAPRow {
+  const CSR *R, *A, *P;
+  int64_t nc;
+  struct State {
+    std::vector<double> acc;
+    std::vector<int64_t> mark;
+    std::vector<int64_t> touched;
+  };
+  State make_state() const {
+    State s;
+    s.acc.assign(nc, 0.0);
+    s.mark.assign(nc, -1);
+    return s;
+  }
+  void operator()(State& s, int64_t J, std::vector<int64_t>& col, std::vector<double>& val) const {
+    s.touched.clear();
+    for (int64_t a = R->ptr[J]; a < R->ptr[J + 1]; ++a) {
+      const int64_t i = R->col[a];
+      const double rv = R->val[a];
+      for (int64_t b = A->ptr[i]; b < A->ptr[i + 1]; ++b) {
+        const int64_t k = A->col[b];
+        const double ra = rv * A->val[b];
+        for (int64_t c = P->ptr[k]; c < P->ptr[k + 1]; ++c) {
+          const int64_t K = P->col[c];
+          if (s.mark[K] != J) { s.mark[K] = J; s.acc[K] = 0.0; s.touched.push_back(K); }
+          s.acc[K] += ra * P->val[c];
+        }
+      }
+    }
+    std::sort(s.touched.begin(), s.touched.end());
+    for (int64_t K : s.touched) { col.push_back(K); val.push_back(s.acc[K]); }
+  }
+};
+
+struct Params {
+  double theta = 0.01;
+  int max_levels = 20;
+  int64_t coarse_target = 200;
+  double stall_ratio = 0.75;
+  int smooth = 1;
+};
+
+void diag_of(const CSR& A, std::vector<double>& d) {
+  d.assign(A.nrows, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < A.nrows; ++i)
+    for (int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
+      if (A.col[k] == i) d[i] = A.val[k];
+}
+
+void build_levels(Hier* h, const Params& prm) {
+  for (;;) {
+    Level& L = h->lv.back();
+    const int l = (int)h->lv.size() - 1;
+    if (L.n <= prm.coarse_target || l + 1 >= prm.max_levels) break;
+    std::vector<double> diag;
+    diag_of(L.A, diag);
+    // decoupled aggregation, independently per rank
+    std::vector<int64_t> agg_local(L.n);
+    std::vector<int64_t> nagg(h->nranks);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = 0; r < h->nranks; ++r)
+      nagg[r] = vmb_aggregate_rank(L.A, diag.data(), L.row_start[r], L.row_start[r + 1], prm.theta,
+                                   agg_local.data() + L.row_start[r]);
+    std::vector<int64_t> crs(h->nranks + 1, 0);
+    for (int r = 0; r < h->nranks; ++r) crs[r + 1] = crs[r] + nagg[r];
+    const int64_t nc = crs[h->nranks];
+    if ((double)nc > prm.stall_ratio * (double)L.n || nc >= L.n) break;
+    L.agg.resize(L.n);
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < h->nranks; ++r)
+      for (int64_t i = L.row_start[r]; i < L.row_start[r + 1]; ++i) L.agg[i] = agg_local[i] + crs[r];
+    std::vector<int64_t>().swap(agg_local);
+    // omega = 1/||D^-1 A||_inf over the whole (global) matrix
+    double nrm = 0.0;
+#pragma omp parallel for reduction(max : nrm) schedule(static)
+    for (int64_t i = 0; i < L.n; ++i) {
+      double s = 0.0;
+      for (int64_t k = L.A.ptr[i]; k < L.A.ptr[i + 1]; ++k) s += std::fabs(L.A.val[k]);
+      s /= std::fabs(diag[i]);
+      nrm = std::max(nrm, s);
+    }
+    const double omega = 1.0 / nrm;
+    h->omega.push_back(prm.smooth ? omega : 0.0);
+    SmoothedPRow prow{&L.A, diag.data(), L.agg.data(), omega, prm.smooth != 0};
+    build_csr_chunked(L.P, L.n, nc, prow);
+    transpose(L.P, L.R);
+    Level NL;
+    NL.n = nc;
+    NL.row_start = crs;
+    RAPRow rrow{&L.R, &L.A, &L.P, nc};
+    build_csr_chunked(NL.A, nc, nc, rrow);
+    h->lv.push_back(std::move(NL));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// Build a hierarchy for the 7-point problem on an nx*ny*nz grid split into
+// px*py*pz rank boxes.  problem: 0 = Poisson, 1 = jump diffusion.
+void* pscgen_build_grid(int64_t nx, int64_t ny, int64_t nz, int px, int py, int pz, int problem,
+                        double jump, int64_t cube, double theta, int max_levels, int64_t coarse_target,
+                        double stall_ratio, int smooth) {
+  if (nx % px || ny % py || nz % pz) return nullptr;
+  Grid g{nx, ny, nz, px, py, pz, nx / px, ny / py, nz / pz};
+  Coef cf{problem, jump, cube};
+  Hier* h = new Hier();
+  h->nranks = px * py * pz;
+  Level L0;
+  L0.n = nx * ny * nz;
+  L0.row_start.resize(h->nranks + 1);
+  for (int r = 0; r <= h->nranks; ++r) L0.row_start[r] = (int64_t)r * g.box_n();
+  StencilRow srow{&g, &cf};
+  build_csr_chunked(L0.A, L0.n, L0.n, srow);
+  h->lv.push_back(std::move(L0));
+  Params prm;
+  prm.theta = theta;
+  prm.max_levels = max_levels;
+  prm.coarse_target = coarse_target;
+  prm.stall_ratio = stall_ratio;
+  prm.smooth = smooth;
+  build_levels(h, prm);
+  return h;
+}
+
+// Build a hierarchy from a user-supplied global CSR A_0 (copied) and a
+// contiguous row partition row_start[0..nranks].
+void* pscgen_build_csr(int64_t n, const int64_t* ptr, const int64_t* col, const double* val, int nranks,
+                       const int64_t* row_start, double theta, int max_levels, int64_t coarse_target,
+                       double stall_ratio, int smooth) {
+  Hier* h = new Hier();
+  h->nranks = nranks;
+  Level L0;
+  L0.n = n;
+  L0.row_start.assign(row_start, row_start + nranks + 1);
+  L0.A.nrows = n;
+  L0.A.ncols = n;
+  L0.A.ptr.alloc(n + 1);
+  std::memcpy(L0.A.ptr.data(), ptr, (n + 1) * sizeof(int64_t));
+  const int64_t nnz = ptr[n];
+  L0.A.col.alloc(nnz);
+  L0.A.val.alloc(nnz);
+  std::memcpy(L0.A.col.data(), col, nnz * sizeof(int64_t));
+  std::memcpy(L0.A.val.data(), val, nnz * sizeof(double));
+  h->lv.push_back(std::move(L0));
+  Params prm;
+  prm.theta = theta;
+  prm.max_levels = max_levels;
+  prm.coarse_target = coarse_target;
+  prm.stall_ratio = stall_ratio;
+  prm.smooth = smooth;
+  build_levels(h, prm);
+  return h;
+}
+
+int pscgen_nlevels(void* hp) { return (int)((Hier*)hp)->lv.size(); }
+int pscgen_nranks(void* hp) { return ((Hier*)hp)->nranks; }
+int64_t pscgen_level_n(void* hp, int l) { return ((Hier*)hp)->lv[l].n; }
+double pscgen_omega(void* hp, int l) { return ((Hier*)hp)->omega[l]; }
+void pscgen_row_start(void* hp, int l, int64_t* out) {
+  Level& L = ((Hier*)hp)->lv[l];
+  std::copy(L.row_start.begin(), L.row_start.end(), out);
+}
+static CSR* pick(void* hp, int l, int kind) {
+  Level& L = ((Hier*)hp)->lv[l];
+  return kind == 0 ? &L.A : (kind == 1 ? &L.P : &L.R);
+}
+// kind: 0 = A_l, 1 = P_l, 2 = R_l.  Returns the global CSR arrays (borrowed).
+int pscgen_csr(void* hp, int l, int kind, int64_t* nrows, int64_t* ncols, int64_t** ptr, int64_t** col,
+               double** val) {
+  Hier* h = (Hier*)hp;
+  if (l < 0 || l >= (int)h->lv.size()) return -1;
+  if (kind != 0 && l == (int)h->lv.size() - 1) return -1;
+  CSR* m = pick(hp, l, kind);
+  *nrows = m->nrows;
+  *ncols = m->ncols;
+  *ptr = m->ptr.data();
+  *col = m->col.data();
+  *val = m->val.data();
+  return 0;
+}
+const int64_t* pscgen_agg(void* hp, int l) { return ((Hier*)hp)->lv[l].agg.data(); }
+void pscgen_free(void* hp) { delete (Hier*)hp; }
+void pscgen_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
+
+}  // extern "C"
