@@ -1,0 +1,202 @@
+/* psc.h — C ABI of the B200-native AMG-PCG solve phase (libpsc.so).
+ *
+ * The method is the solve phase of PSCToolkit (arXiv 2406.19754, PAPER.md):
+ * FP64 preconditioned conjugate gradient on a row-block-distributed SPD sparse
+ * matrix, preconditioned by one AMG V-cycle per iteration (Eq. (2), P:202-207,
+ * Sec. 2.3) over a GIVEN aggregation hierarchy {A_l, P_l, R_l = P_l^T}, with
+ * l1-Jacobi pre/post-smoothing (Sec. 2.3.2) and a fixed number of
+ * l1-Jacobi sweeps at the coarsest level (Fig. 5 caption).
+ *
+ * The call order follows the paper's statement of a PSBLAS application
+ * (Sec. 2.1): initialise the parallel + accelerator environment
+ * (psb_init / psb_cuda_init), create the index-space descriptors (psb_cdall),
+ * insert the matrices in GLOBAL numbering (psb_spall / psb_spins), assemble the
+ * descriptors (psb_cdasb: halo lists) and the matrices (psb_spasb with the GPU
+ * "mold": here a device sliced-ELL), build the preconditioner (the smoother
+ * build of P:164-166: the l1 diagonals), and call the Krylov solver
+ * (psb_krylov, Fig. 6) with x holding the initial guess on entry.
+ *
+ *   psc_init -> psc_desc_create (one per level index space)
+ *            -> psc_mat_create_csr (A_l: rows l, cols l; P_l: rows l, cols l+1;
+ *                                   R_l: rows l+1, cols l)
+ *            -> psc_desc_assemble (each) -> psc_mat_assemble (each)
+ *            -> psc_hier_create -> psc_pcg_solve ... -> destroy in reverse order.
+ *
+ * CONVENTIONS
+ *  - Return value: int status.  PSC_OK (0); PSC_NOT_CONVERGED (1, psc_pcg_solve*
+ *    only; outputs are valid); negative = error (mirrors PSBLAS `info`,
+ *    P:105-107).  psc_last_error(ctx) gives a message for the last error.
+ *  - Global indices are int64 ("8-byte integers for extreme-scale problems",
+ *    P:62-63).  Device-local indices are int32 (owned first, then halo).
+ *  - Ownership is a contiguous block partition: rank r owns global rows
+ *    [row_start[r], row_start[r+1]) of an index space; row_start is identical on
+ *    all ranks, starts at 0, is non-decreasing and ends at n_global.
+ *  - CSR input: row_ptr[0] = 0, non-decreasing; columns strictly increasing
+ *    within a row; 0 <= column < n_global(col space).  Violations: PSC_ERR_ARG.
+ *  - Memory: the library copies every host array it is given at *_create*; the
+ *    caller keeps its arrays.  Vector arguments named *_dev are device pointers to
+ *    contiguous FP64 arrays on the context's GPU (e.g. torch.Tensor.data_ptr()),
+ *    of length n_owned of the relevant index space; they belong to the caller.
+ *    Arguments named *_host are host pointers.
+ *  - Streams: all work runs on the library's own stream, ordered after the work
+ *    already submitted to the `user_stream` given at psc_init (NULL = legacy
+ *    default stream); every call returns after its GPU work is complete.
+ *  - Collective: calls marked [collective] must be issued by every rank in the
+ *    same order.  One host thread per context.
+ *  - No CPU fallback: every numerical step runs in this library's CUDA kernels
+ *    (sm_100a) and NCCL; a missing GPU is PSC_ERR_CUDA.
+ */
+#ifndef PSC_H
+#define PSC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSC_OK 0
+#define PSC_NOT_CONVERGED 1
+#define PSC_ERR_ARG (-1)       /* bad argument / dimension mismatch / malformed CSR */
+#define PSC_ERR_STATE (-2)     /* wrong call order: unassembled object, missing level */
+#define PSC_ERR_CUDA (-3)      /* CUDA runtime error (including: no device) */
+#define PSC_ERR_NCCL (-4)      /* NCCL error */
+#define PSC_ERR_NOMEM (-5)     /* device or host allocation failed */
+#define PSC_ERR_BREAKDOWN (-6) /* PCG: p^T A p <= 0 or not finite */
+
+typedef struct psc_ctx_s psc_ctx;
+typedef struct psc_desc_s psc_desc;
+typedef struct psc_mat_s psc_mat;
+typedef struct psc_hier_s psc_hier;
+
+/* ------------------------------------------------------------------ context */
+
+/* Fill id[128] with a fresh NCCL unique id.  Call on rank 0 only and broadcast
+ * the bytes to the other ranks (e.g. with torch.distributed) before psc_init. */
+int psc_get_unique_id(unsigned char id[128]);
+
+/* Parallel + accelerator environment (psb_init + psb_cuda_init).
+ * [collective when nranks > 1]  rank in [0, nranks); cuda_device = device
+ * ordinal; id = 128 bytes from psc_get_unique_id (ignored, may be NULL, when
+ * nranks == 1); user_stream = cudaStream_t the caller's producers/consumers use
+ * (may be NULL).  On success *ctx owns a CUDA stream and (nranks > 1) an NCCL
+ * communicator. */
+int psc_init(int rank, int nranks, int cuda_device, const unsigned char* id, void* user_stream, psc_ctx** ctx);
+void psc_finalize(psc_ctx* ctx);
+const char* psc_status_string(int status);
+const char* psc_last_error(psc_ctx* ctx);
+/* Library build string (compiler, arch). */
+const char* psc_version(void);
+
+/* --------------------------------------------------------------- descriptor */
+
+/* Index space of n_global entries split in contiguous row blocks (psb_cdall,
+ * P:81-86; Fig. 1).  row_start: host, nranks+1 entries, copied. */
+int psc_desc_create(psc_ctx* ctx, int64_t n_global, const int64_t* row_start, psc_desc** d);
+
+/* [collective] Build halo lists (psb_cdasb): the halo of this index space is
+ * the sorted set of off-rank global indices referenced by the columns of every
+ * matrix created with this descriptor as `cols`; local numbering is owned
+ * [0, n_owned) then halo [n_owned, n_owned + n_halo) ordered by global index
+ * (hence grouped by owner).  Send lists are negotiated with the owners.  All
+ * matrices whose columns live in this space must be created before this call. */
+int psc_desc_assemble(psc_desc* d);
+
+/* After assembly: n_owned, n_halo, first owned global index (any may be NULL). */
+int psc_desc_info(psc_desc* d, int64_t* n_owned, int64_t* n_halo, int64_t* own_begin);
+/* Test hook: halo_globals_host[n_halo] = global index of each halo slot. */
+int psc_desc_halo(psc_desc* d, int64_t* halo_globals_host);
+void psc_desc_destroy(psc_desc* d);
+
+/* ------------------------------------------------------------------- matrix */
+
+/* Insert this rank's rows of a distributed matrix in GLOBAL numbering (psb_spall
+ * + psb_spins).  rows/cols: descriptors of the row and column index
+ * spaces; n_local_rows must equal rows' owned count; row_ptr[n_local_rows+1]
+ * (int64, local rows), col_global[nnz] (int64), val[nnz] (f64): host arrays,
+ * copied to the device.  Off-rank columns are registered as halo of `cols`. */
+int psc_mat_create_csr(psc_ctx* ctx, psc_desc* rows, psc_desc* cols, int64_t n_local_rows, const int64_t* row_ptr,
+                       const int64_t* col_global, const double* val, psc_mat** m);
+
+/* Renumber columns to local (owned then halo) and convert the device CSR into the
+ * device sliced-ELL format (Hacked ELLPACK of P:168-183: 32-row slices, each its
+ * own column-major ELLPACK block, padding value 0.0 with the row's last valid
+ * column).  Needs both descriptors assembled. */
+int psc_mat_assemble(psc_mat* m);
+
+/* nnz (stored), padded slots (total sliced-ELL slots), slices, local rows (any may be NULL). */
+int psc_mat_info(psc_mat* m, int64_t* nnz, int64_t* padded_slots, int64_t* n_slices, int64_t* n_rows);
+
+/* [collective] y_dev = alpha * A * x_dev + beta * y_dev (test hook; includes the
+ * halo exchange of x).  x_dev: n_owned(cols); y_dev: n_owned(rows). */
+int psc_mat_spmv(psc_mat* m, double alpha, const double* x_dev, double beta, double* y_dev);
+void psc_mat_destroy(psc_mat* m);
+
+/* -------------------------------------------------------------- hierarchy */
+
+/* Smoothing sweeps before / after the coarse correction and l1-Jacobi sweeps at
+ * the coarsest level (defaults 4 / 4 / 30: Fig. 5 caption). */
+typedef struct {
+  int pre_sweeps;
+  int post_sweeps;
+  int coarse_sweeps;
+} psc_cycle_opts;
+
+/* [collective] AMG hierarchy handle over given level matrices (D10/D11 in
+ * SURVEY.md): A[0..nlevels-1], P[0..nlevels-2], R[0..nlevels-2] (R_l = P_l^T given
+ * explicitly).  Builds the l1-Jacobi smoothers M_l = diag(A_l) + diag(sum_{j!=i}
+ * |a_ij|) (the smoother-build step of P:164-166) and the device
+ * workspace.  opts NULL = defaults.  Matrices must stay alive until
+ * psc_hier_destroy. */
+int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const* P, psc_mat* const* R,
+                    const psc_cycle_opts* opts, psc_hier** h);
+
+/* Local sizes: n_owned[l], nnz of A_l, P_l, R_l on this rank (arrays of nlevels; any may be NULL). */
+int psc_hier_info(psc_hier* h, int* nlevels, int64_t* n_owned, int64_t* nnz_A, int64_t* nnz_P, int64_t* nnz_R);
+
+/* [collective] z_dev = B_0 r_dev: one V-cycle (Eq. (2)) from zero. */
+int psc_hier_vcycle(psc_hier* h, const double* r_dev, double* z_dev);
+
+/* Test hook: dinv_dev[n_owned(level)] = 1 / M_level (the stored reciprocal l1 diagonal). */
+int psc_hier_dinv(psc_hier* h, int level, double* dinv_dev);
+
+/* [collective] Test hook: x_dev = nsweeps l1-Jacobi sweeps x <- x + M^{-1}(b - A_l x)
+ * from x = 0 at `level` (the coarsest-level solver when level = nlevels-1). */
+int psc_hier_smooth(psc_hier* h, int level, const double* b_dev, double* x_dev, int nsweeps);
+
+/* Solve statistics. */
+typedef struct {
+  int iters;                    /* PCG iterations performed */
+  int status;                   /* same as the return value */
+  double rel_res;               /* ||r_k||_2 / ||b||_2 at exit (recurrence residual) */
+  double solve_seconds;         /* device time of the solve (CUDA events on the library stream) */
+  int64_t kernel_launches;      /* library kernels launched during the solve */
+  int64_t collectives;          /* NCCL calls issued during the solve */
+  double dom_kernel_seconds;    /* summed device time of the level-0 l1-Jacobi sweep launches */
+  int64_t dom_kernel_launches;  /* number of those launches */
+  double dom_kernel_bytes;      /* algorithmic bytes per launch: 12 nnz(A_0) + 32 n_0 */
+  int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by psc_pcg_solve_host */
+} psc_stats;
+
+/* [collective] PCG (reading R1 of DESIGN.md) preconditioned by one
+ * V-cycle per iteration.  b_dev: RHS; x_dev: initial guess on entry, solution on
+ * exit (Fig. 6 caption); both n_owned(level 0), device.  Stops when
+ * ||r_k||_2/||b||_2 <= tol (recurrence residual) or after maxit iterations.
+ * res_hist_host: NULL or >= maxit+1 doubles, receives ||r_k||/||b|| for k = 0..iters.
+ * st: NULL or receives statistics.  Returns PSC_OK, PSC_NOT_CONVERGED or an error
+ * (PSC_ERR_BREAKDOWN when p^T A p <= 0 or non-finite).  b = 0 gives x = 0 and 0
+ * iterations. */
+int psc_pcg_solve(psc_hier* h, const double* b_dev, double* x_dev, double tol, int maxit, double* res_hist_host,
+                  psc_stats* st);
+
+/* [collective] Same, with HOST b and x (n_owned(0) each): the host->device copy of b
+ * and x0 and the device->host copy of x are inside the call (end-to-end path). */
+int psc_pcg_solve_host(psc_hier* h, const double* b_host, double* x_host, double tol, int maxit,
+                       double* res_hist_host, psc_stats* st);
+
+void psc_hier_destroy(psc_hier* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSC_H */

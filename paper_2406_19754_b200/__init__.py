@@ -1,0 +1,310 @@
+"""B200-native AMG-PCG solve phase of PSCToolkit (arXiv 2406.19754).
+
+Thin ctypes binding over ``libpsc.so`` (C ABI declared in ``include/psc.h``).
+Argument marshalling only: every numerical step runs in the library's sm_100a
+CUDA kernels and NCCL.  There is no CPU fallback: if the shared library is
+missing this module raises ImportError, and on a machine without a B200 every
+compute call fails with PscError(PSC_ERR_CUDA).
+
+Device vectors are passed as torch CUDA float64 tensors (torch is used only for
+device memory, streams and process groups); host vectors as numpy float64.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpsc.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2406_19754_b200.build` "
+                      "(or __graft_entry__.build()); there is no fallback path")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+PSC_OK, PSC_NOT_CONVERGED = 0, 1
+PSC_ERR_ARG, PSC_ERR_STATE, PSC_ERR_CUDA, PSC_ERR_NCCL, PSC_ERR_NOMEM, PSC_ERR_BREAKDOWN = -1, -2, -3, -4, -5, -6
+
+_vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+
+
+class CycleOpts(ctypes.Structure):
+    _fields_ = [("pre_sweeps", _i32), ("post_sweeps", _i32), ("coarse_sweeps", _i32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("iters", _i32), ("status", _i32), ("rel_res", _f64), ("solve_seconds", _f64),
+                ("kernel_launches", _i64), ("collectives", _i64), ("dom_kernel_seconds", _f64),
+                ("dom_kernel_launches", _i64), ("dom_kernel_bytes", _f64), ("h2d_bytes", _i64),
+                ("d2h_bytes", _i64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_P = ctypes.POINTER
+_sig("psc_get_unique_id", _i32, [ctypes.c_char_p])
+_sig("psc_init", _i32, [_i32, _i32, _i32, ctypes.c_char_p, _vp, _P(_vp)])
+_sig("psc_finalize", None, [_vp])
+_sig("psc_status_string", ctypes.c_char_p, [_i32])
+_sig("psc_last_error", ctypes.c_char_p, [_vp])
+_sig("psc_version", ctypes.c_char_p, [])
+_sig("psc_desc_create", _i32, [_vp, _i64, _vp, _P(_vp)])
+_sig("psc_desc_assemble", _i32, [_vp])
+_sig("psc_desc_info", _i32, [_vp, _P(_i64), _P(_i64), _P(_i64)])
+_sig("psc_desc_halo", _i32, [_vp, _vp])
+_sig("psc_desc_destroy", None, [_vp])
+_sig("psc_mat_create_csr", _i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _P(_vp)])
+_sig("psc_mat_assemble", _i32, [_vp])
+_sig("psc_mat_info", _i32, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)])
+_sig("psc_mat_spmv", _i32, [_vp, _f64, _vp, _f64, _vp])
+_sig("psc_mat_destroy", None, [_vp])
+_sig("psc_hier_create", _i32, [_vp, _i32, _vp, _vp, _vp, _P(CycleOpts), _P(_vp)])
+_sig("psc_hier_info", _i32, [_vp, _P(_i32), _vp, _vp, _vp, _vp])
+_sig("psc_hier_vcycle", _i32, [_vp, _vp, _vp])
+_sig("psc_hier_dinv", _i32, [_vp, _i32, _vp])
+_sig("psc_hier_smooth", _i32, [_vp, _i32, _vp, _vp, _i32])
+_sig("psc_pcg_solve", _i32, [_vp, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
+_sig("psc_pcg_solve_host", _i32, [_vp, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
+_sig("psc_hier_destroy", None, [_vp])
+
+
+class PscError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_lib.psc_status_string(code).decode()}: {msg}")
+        self.code = code
+
+
+def version() -> str:
+    return _lib.psc_version().decode()
+
+
+def _check(rc, ctx=None, ok=(PSC_OK,)):
+    if rc in ok:
+        return rc
+    msg = _lib.psc_last_error(ctx.handle if ctx is not None else None).decode()
+    raise PscError(rc, msg)
+
+
+def _dev_ptr(t, n, name):
+    """torch CUDA float64 contiguous tensor of n elements -> raw pointer."""
+    if t is None:
+        if n == 0:
+            return None
+        raise ValueError(f"{name} is None")
+    if not (getattr(t, "is_cuda", False) and str(t.dtype) == "torch.float64" and t.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous CUDA float64 tensor")
+    if t.numel() != n:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {n}")
+    return t.data_ptr()
+
+
+def _host(a, dtype, name):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.psc_get_unique_id(buf))
+    return buf.raw
+
+
+class Context:
+    """psc_init: rank/nranks/device; unique_id (128 bytes from rank 0) when nranks > 1."""
+
+    def __init__(self, rank=0, nranks=1, device=0, unique_id: bytes | None = None, stream=None):
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream(device).cuda_stream
+            except Exception:
+                stream = None
+        h = _vp()
+        _check(_lib.psc_init(rank, nranks, device, unique_id, stream, ctypes.byref(h)))
+        self.handle = h.value
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self._children = []
+
+    def close(self):
+        if self.handle:
+            for c in reversed(self._children):
+                c.close()
+            self._children = []
+            _lib.psc_finalize(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Descriptor:
+    def __init__(self, ctx: Context, n_global: int, row_start):
+        rs = _host(row_start, np.int64, "row_start")
+        if len(rs) != ctx.nranks + 1:
+            raise ValueError("row_start must have nranks+1 entries")
+        h = _vp()
+        _check(_lib.psc_desc_create(ctx.handle, int(n_global), rs.ctypes.data, ctypes.byref(h)), ctx)
+        self.ctx, self.handle = ctx, h.value
+        self.n_global = int(n_global)
+        self.row_start = rs
+        ctx._children.append(self)
+
+    def assemble(self):
+        _check(_lib.psc_desc_assemble(self.handle), self.ctx)
+        return self
+
+    def info(self):
+        a, b, c = _i64(), _i64(), _i64()
+        _check(_lib.psc_desc_info(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), self.ctx)
+        return dict(n_owned=a.value, n_halo=b.value, own_begin=c.value)
+
+    def halo(self) -> np.ndarray:
+        out = np.zeros(self.info()["n_halo"], dtype=np.int64)
+        _check(_lib.psc_desc_halo(self.handle, out.ctypes.data), self.ctx)
+        return out
+
+    @property
+    def n_owned(self):
+        return int(self.row_start[self.ctx.rank + 1] - self.row_start[self.ctx.rank])
+
+    def close(self):
+        if self.handle:
+            _lib.psc_desc_destroy(self.handle)
+            self.handle = None
+
+
+class Matrix:
+    """This rank's rows in CSR with GLOBAL int64 columns (psc_mat_create_csr)."""
+
+    def __init__(self, ctx: Context, rows: Descriptor, cols: Descriptor, row_ptr, col_global, val):
+        rp = _host(row_ptr, np.int64, "row_ptr")
+        cg = _host(col_global, np.int64, "col_global")
+        v = _host(val, np.float64, "val")
+        h = _vp()
+        _check(_lib.psc_mat_create_csr(ctx.handle, rows.handle, cols.handle, len(rp) - 1, rp.ctypes.data,
+                                       cg.ctypes.data, v.ctypes.data, ctypes.byref(h)), ctx)
+        self.ctx, self.rows, self.cols, self.handle = ctx, rows, cols, h.value
+        ctx._children.append(self)
+
+    def assemble(self):
+        _check(_lib.psc_mat_assemble(self.handle), self.ctx)
+        return self
+
+    def info(self):
+        a, b, c, d = _i64(), _i64(), _i64(), _i64()
+        _check(_lib.psc_mat_info(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
+               self.ctx)
+        return dict(nnz=a.value, padded=b.value, n_slices=c.value, n_rows=d.value)
+
+    def spmv(self, x, y, alpha=1.0, beta=0.0):
+        """y = alpha A x + beta y (device tensors; owned parts)."""
+        _check(_lib.psc_mat_spmv(self.handle, float(alpha), _dev_ptr(x, self.cols.n_owned, "x"), float(beta),
+                                 _dev_ptr(y, self.rows.n_owned, "y")), self.ctx)
+        return y
+
+    def close(self):
+        if self.handle:
+            _lib.psc_mat_destroy(self.handle)
+            self.handle = None
+
+
+class Hierarchy:
+    """psc_hier_create over given level matrices A[l], P[l], R[l]; V-cycle + PCG."""
+
+    def __init__(self, ctx: Context, A, P, R, pre=4, post=4, coarse=30):
+        L = len(A)
+        Aa = (_vp * L)(*[m.handle for m in A])
+        Pa = (_vp * max(L - 1, 1))(*[m.handle for m in P])
+        Ra = (_vp * max(L - 1, 1))(*[m.handle for m in R])
+        opts = CycleOpts(pre, post, coarse)
+        h = _vp()
+        _check(_lib.psc_hier_create(ctx.handle, L, Aa, Pa, Ra, ctypes.byref(opts), ctypes.byref(h)), ctx)
+        self.ctx, self.handle, self.nlevels = ctx, h.value, L
+        self.A, self.P, self.R = list(A), list(P), list(R)
+        self.n0 = A[0].rows.n_owned
+        ctx._children.append(self)
+
+    def info(self):
+        L = self.nlevels
+        nl = _i32()
+        arrs = [np.zeros(L, np.int64) for _ in range(4)]
+        _check(_lib.psc_hier_info(self.handle, ctypes.byref(nl), *[a.ctypes.data for a in arrs]), self.ctx)
+        return dict(nlevels=nl.value, n_owned=arrs[0].tolist(), nnz_A=arrs[1].tolist(), nnz_P=arrs[2].tolist(),
+                    nnz_R=arrs[3].tolist())
+
+    def vcycle(self, r, z):
+        _check(_lib.psc_hier_vcycle(self.handle, _dev_ptr(r, self.n0, "r"), _dev_ptr(z, self.n0, "z")), self.ctx)
+        return z
+
+    def dinv(self, level, out):
+        n = self.A[level].rows.n_owned
+        _check(_lib.psc_hier_dinv(self.handle, level, _dev_ptr(out, n, "out")), self.ctx)
+        return out
+
+    def smooth(self, level, b, x, nsweeps):
+        n = self.A[level].rows.n_owned
+        _check(_lib.psc_hier_smooth(self.handle, level, _dev_ptr(b, n, "b"), _dev_ptr(x, n, "x"), int(nsweeps)),
+               self.ctx)
+        return x
+
+    def solve(self, b, x, tol=1e-8, maxit=200):
+        """PCG on device tensors.  Returns (status, stats dict, residual history ndarray)."""
+        hist = np.full(maxit + 1, np.nan)
+        st = Stats()
+        rc = _lib.psc_pcg_solve(self.handle, _dev_ptr(b, self.n0, "b"), _dev_ptr(x, self.n0, "x"), float(tol),
+                                int(maxit), hist.ctypes.data, ctypes.byref(st))
+        _check(rc, self.ctx, ok=(PSC_OK, PSC_NOT_CONVERGED))
+        return rc, st.as_dict(), hist[: st.iters + 1]
+
+    def solve_host(self, b, x, tol=1e-8, maxit=200):
+        """PCG on host numpy arrays (end-to-end path: copies inside the call). x updated in place."""
+        if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous):
+            raise TypeError("x must be a C-contiguous float64 numpy array")
+        b = _host(b, np.float64, "b")
+        if len(b) != self.n0 or len(x) != self.n0:
+            raise ValueError("b/x size mismatch")
+        hist = np.full(maxit + 1, np.nan)
+        st = Stats()
+        rc = _lib.psc_pcg_solve_host(self.handle, b.ctypes.data, x.ctypes.data, float(tol), int(maxit),
+                                     hist.ctypes.data, ctypes.byref(st))
+        _check(rc, self.ctx, ok=(PSC_OK, PSC_NOT_CONVERGED))
+        return rc, st.as_dict(), hist[: st.iters + 1]
+
+    def close(self):
+        if self.handle:
+            _lib.psc_hier_destroy(self.handle)
+            self.handle = None
+
+
+def build_hierarchy(ctx: Context, levels, pre=4, post=4, coarse=30):
+    """Create descriptors + matrices for this rank and assemble them, in the
+    PSBLAS order.  `levels[l]` is a dict with
+      n_global, row_start (nranks+1), A=(row_ptr, col_global, val) for this rank's rows,
+      and for l < L-1: P=(...) (rows of space l), R=(...) (rows of space l+1).
+    Returns (Hierarchy, descs, A, P, R)."""
+    L = len(levels)
+    descs = [Descriptor(ctx, lv["n_global"], lv["row_start"]) for lv in levels]
+    A = [Matrix(ctx, descs[l], descs[l], *levels[l]["A"]) for l in range(L)]
+    P = [Matrix(ctx, descs[l], descs[l + 1], *levels[l]["P"]) for l in range(L - 1)]
+    R = [Matrix(ctx, descs[l + 1], descs[l], *levels[l]["R"]) for l in range(L - 1)]
+    for d in descs:
+        d.assemble()
+    for m in A + P + R:
+        m.assemble()
+    h = Hierarchy(ctx, A, P, R, pre, post, coarse)
+    return h, descs, A, P, R

@@ -1,0 +1,697 @@
+// hier.cu — AMG hierarchy handle, V-cycle (Eq. (2)) and PCG driver of libpsc.so.
+//
+// One PCG iteration = one CUDA Graph launch (V-cycle + p update + q = A p +
+// x/r update + the 2-scalar device->host copy); the host waits once per
+// iteration for the stopping test (P:314 relative residual), so the only
+// per-iteration host<->device traffic is 2*nranks doubles.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "kernels.h"
+
+using namespace psc;
+
+namespace {
+
+enum Slot { S_PQ = 0, S_RR = 1, S_RZ = 2, S_BB = 3, NSLOT = 4 };
+
+struct LevelWS {
+  psc_mat *A = nullptr, *P = nullptr, *R = nullptr;
+  psc_desc* d = nullptr;
+  int64_t n = 0, nh = 0;
+  double* dinv = nullptr;     // n
+  double* x[2] = {nullptr, nullptr};  // n + nh
+  double* r = nullptr;        // n + nh
+  double* b = nullptr;        // n (level >= 1: R_{l-1} r_{l-1})
+};
+
+// replicated coarsest level (nranks > 1): every rank holds the whole A_coarse
+struct Replica {
+  bool on = false;
+  int64_t N = 0, maxcnt = 0;
+  Sell S;                       // global rows, columns = global indices
+  double* dinv = nullptr;       // N
+  double* sendbuf = nullptr;    // maxcnt
+  double* gbuf = nullptr;       // nranks * maxcnt
+  int64_t* map_full = nullptr;  // N: global g -> position in gbuf
+  double* bfull = nullptr;      // N
+  double* xfull = nullptr;      // N
+  int64_t* map_loc = nullptr;   // n + nh: local slot -> global index
+};
+
+}  // namespace
+
+struct psc_hier_s {
+  psc_ctx* ctx = nullptr;
+  int L = 0;
+  psc_cycle_opts opt{4, 4, 30};
+  std::vector<LevelWS> lv;
+  Replica rep;
+  bool coarse_one_cta = false;
+  // CG state (level 0)
+  double* x_int = nullptr;  // n0 + nh0
+  double* r_cg = nullptr;   // n0
+  double* p = nullptr;      // n0 + nh0
+  double* q = nullptr;      // n0
+  double* d_scal = nullptr; // NSLOT * nranks gathered partial scalars, then rz_old
+  double* h_scal = nullptr; // pinned mirror
+  double* d_bhost = nullptr;  // device staging for psc_pcg_solve_host
+  double* d_xhost = nullptr;
+  RedSite red1, red2;
+  // graph of one PCG iteration
+  cudaGraphExec_t iter_exec = nullptr;
+  int64_t iter_launches = 0, iter_collectives = 0;
+  double* z_ptr = nullptr;
+  // dominant-kernel timing (level-0 l1-Jacobi sweep) inside the graph
+  std::vector<cudaEvent_t> ev_dom;  // pairs (start, end)
+  int dom_used = 0;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_herr;
+
+int hfail(psc_ctx* ctx, const Error& e) {
+  if (ctx) ctx->err = e.what();
+  g_herr = e.what();
+  return e.code;
+}
+
+void enter(psc_ctx* ctx) {
+  PSC_CUDA(cudaSetDevice(ctx->device));
+  PSC_CUDA(cudaEventRecord(ctx->ev_user, ctx->user_stream));
+  PSC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_user, 0));
+}
+
+double* scal(psc_hier* h, Slot s) { return h->d_scal + (size_t)s * h->ctx->nranks; }
+double* scal_mine(psc_hier* h, Slot s) { return scal(h, s) + h->ctx->rank; }
+double* rz_old(psc_hier* h) { return h->d_scal + (size_t)NSLOT * h->ctx->nranks; }
+
+void allgather_slot(psc_hier* h, Slot s, cudaStream_t st) {
+  psc_ctx* ctx = h->ctx;
+  if (ctx->nranks == 1) return;
+  PSC_NCCL(ncclAllGather(scal_mine(h, s), scal(h, s), 1, ncclDouble, ctx->comm, st));
+  ctx->collectives++;
+}
+
+// ------------------------------------------------------------ coarsest level
+// B_ell = `nsweeps` l1-Jacobi sweeps from zero.  Returns the
+// owned+halo iterate of the coarsest index space.
+double* coarse_solve(psc_hier* h, const double* b, int nsweeps, cudaStream_t s) {
+  psc_ctx* ctx = h->ctx;
+  LevelWS& W = h->lv[h->L - 1];
+  if (h->rep.on) {
+    Replica& R = h->rep;
+    // gather b_coarse on every rank, solve the whole coarse system redundantly
+    // (bit-identical per row to the distributed sweeps), scatter to owned+halo.
+    if (W.n) PSC_CUDA(cudaMemcpyAsync(R.sendbuf, b, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+    PSC_NCCL(ncclAllGather(R.sendbuf, R.gbuf, R.maxcnt, ncclDouble, ctx->comm, s));
+    ctx->collectives++;
+    launch_gather(ctx, R.N, R.map_full, R.gbuf, R.bfull, s);
+    launch_coarse_solve(ctx, R.S, R.dinv, R.bfull, R.xfull, nsweeps, s);
+    launch_gather(ctx, W.n + W.nh, R.map_loc, R.xfull, W.x[0], s);
+    return W.x[0];
+  }
+  if (h->coarse_one_cta) {
+    launch_coarse_solve(ctx, W.A->S, W.dinv, b, W.x[0], nsweeps, s);
+    return W.x[0];
+  }
+  // general path: distributed sweeps, one halo exchange each
+  int cur = 0;
+  if (nsweeps <= 0) {
+    PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
+    return W.x[0];
+  }
+  launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
+  for (int k = 1; k < nsweeps; ++k) {
+    halo_exchange(ctx, W.d, W.x[cur], s);
+    RowArgs a;
+    a.x = W.x[cur];
+    a.b = b;
+    a.dinv = W.dinv;
+    a.y = W.x[cur ^ 1];
+    launch_rows(ctx, W.A->S, RowOp::Sweep, a, s);
+    cur ^= 1;
+  }
+  return W.x[cur];
+}
+
+bool coarse_has_halo(psc_hier* h) { return h->rep.on; }
+
+// nsweeps l1-Jacobi sweeps from zero at level l < L-1 (pre-smoothing: the
+// rightmost factor of Eq. (2) applied `pre` times).  The first sweep is
+// x = M^{-1} b exactly.  Returns the index of the buffer holding x.
+int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s, bool timing) {
+  psc_ctx* ctx = h->ctx;
+  LevelWS& W = h->lv[l];
+  if (nsweeps <= 0) {
+    PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
+    return 0;
+  }
+  launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
+  int cur = 0;
+  for (int k = 1; k < nsweeps; ++k) {
+    halo_exchange(ctx, W.d, W.x[cur], s);
+    RowArgs a;
+    a.x = W.x[cur];
+    a.b = b;
+    a.dinv = W.dinv;
+    a.y = W.x[cur ^ 1];
+    const bool t = timing && l == 0 && h->dom_used + 2 <= (int)h->ev_dom.size();
+    if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
+    launch_rows(ctx, W.A->S, RowOp::Sweep, a, s);
+    if (t) {
+      PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
+      h->dom_used += 2;
+    }
+    cur ^= 1;
+  }
+  return cur;
+}
+
+// z = B_l b  (Eq. (2)), recursively.  At level 0 the last
+// post-sweep also accumulates (b, z) = (r, z) into slot S_RZ.
+double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool timing) {
+  psc_ctx* ctx = h->ctx;
+  if (l == h->L - 1) return coarse_solve(h, b, h->opt.coarse_sweeps, s);
+  LevelWS& W = h->lv[l];
+  LevelWS& C = h->lv[l + 1];
+  // (I - M^-1 A)^pre
+  int cur = pre_smooth(h, l, b, h->opt.pre_sweeps, s, timing);
+  // coarse-grid correction (I - P B_{l+1} P^T A): r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
+  halo_exchange(ctx, W.d, W.x[cur], s);
+  {
+    RowArgs a;
+    a.x = W.x[cur];
+    a.b = b;
+    a.y = W.r;
+    launch_rows(ctx, W.A->S, RowOp::Resid, a, s);
+  }
+  halo_exchange(ctx, W.d, W.r, s);
+  {
+    RowArgs a;
+    a.x = W.r;
+    a.y = C.b;
+    launch_rows(ctx, W.R->S, RowOp::Spmv, a, s);
+  }
+  double* xc = vcycle_level(h, l + 1, C.b, s, timing);
+  if (!(l + 1 == h->L - 1 && coarse_has_halo(h))) halo_exchange(ctx, C.d, xc, s);
+  {
+    RowArgs a;
+    a.x = xc;
+    a.y = W.x[cur];
+    launch_rows(ctx, W.P->S, RowOp::PAdd, a, s);
+  }
+  // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
+  const int post = h->opt.post_sweeps;
+  for (int k = 0; k < post; ++k) {
+    halo_exchange(ctx, W.d, W.x[cur], s);
+    const bool last0 = (l == 0 && k == post - 1);
+    RowArgs a;
+    a.x = W.x[cur];
+    a.b = b;
+    a.dinv = W.dinv;
+    a.y = W.x[cur ^ 1];
+    if (last0) {
+      a.red = &h->red1;
+      a.red_out = scal_mine(h, S_RZ);
+    }
+    const bool t = timing && l == 0 && h->dom_used + 2 <= (int)h->ev_dom.size();
+    if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
+    launch_rows(ctx, W.A->S, last0 ? RowOp::SweepDot : RowOp::Sweep, a, s);
+    if (t) {
+      PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
+      h->dom_used += 2;
+    }
+    cur ^= 1;
+  }
+  if (l == 0 && post == 0) launch_dot(ctx, W.n, b, W.x[cur], &h->red1, scal_mine(h, S_RZ), s);
+  return W.x[cur];
+}
+
+// One PCG iteration k >= 1 (P:113-117 with B = V-cycle; reading R1):
+//   z = B r ; rz = (r, z) ; beta = rz / rz_old ; p = z + beta p ; rz_old = rz
+//   q = A p ; pq = (p, q) ; alpha = rz_old / pq ; x += alpha p ; r -= alpha q ; rr = (r, r)
+// (at k = 1, p = 0 and rz_old = 1 so p = z exactly)
+void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
+  psc_ctx* ctx = h->ctx;
+  LevelWS& W = h->lv[0];
+  const int R = ctx->nranks;
+  h->dom_used = 0;
+  double* z = vcycle_level(h, 0, h->r_cg, s, timing);
+  h->z_ptr = z;
+  allgather_slot(h, S_RZ, s);
+  launch_xpby(ctx, W.n, z, h->p, scal(h, S_RZ), rz_old(h), R, &h->red2, s);
+  halo_exchange(ctx, W.d, h->p, s);
+  {
+    RowArgs a;
+    a.x = h->p;
+    a.y = h->q;
+    a.red = &h->red1;
+    a.red_out = scal_mine(h, S_PQ);
+    launch_rows(ctx, W.A->S, RowOp::SpmvDot, a, s);
+  }
+  allgather_slot(h, S_PQ, s);
+  launch_cg_update(ctx, W.n, h->x_int, h->p, h->r_cg, h->q, scal(h, S_PQ), rz_old(h), R, &h->red1,
+                   scal_mine(h, S_RR), s);
+  allgather_slot(h, S_RR, s);
+  PSC_CUDA(cudaMemcpyAsync(h->h_scal, h->d_scal, sizeof(double) * NSLOT * R, cudaMemcpyDeviceToHost, s));
+}
+
+void capture_iteration(psc_hier* h) {
+  psc_ctx* ctx = h->ctx;
+  cudaStream_t s = ctx->stream;
+  const int64_t l0 = ctx->launches, c0 = ctx->collectives;
+  cudaGraph_t g = nullptr;
+  PSC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    record_iteration(h, s, true);
+  } catch (...) {
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  PSC_CUDA(cudaStreamEndCapture(s, &g));
+  PSC_CUDA(cudaGraphInstantiate(&h->iter_exec, g, 0));
+  PSC_CUDA(cudaGraphDestroy(g));
+  h->iter_launches = ctx->launches - l0;
+  h->iter_collectives = ctx->collectives - c0;
+  ctx->launches = l0;
+  ctx->collectives = c0;
+}
+
+double sum_ranks(const double* v, int R) {
+  double s = 0.0;
+  for (int r = 0; r < R; ++r) s += v[r];
+  return s;
+}
+
+void build_replica(psc_hier* h) {
+  psc_ctx* ctx = h->ctx;
+  const int R = ctx->nranks;
+  LevelWS& W = h->lv[h->L - 1];
+  psc_mat* A = W.A;
+  psc_desc* d = W.d;
+  Replica& rp = h->rep;
+  rp.N = d->n_global;
+  if (rp.N > coarse_smem_rows()) return;
+  PSC_REQUIRE((int64_t)A->h_rowptr.size() == A->n_rows + 1, PSC_ERR_STATE, "coarsest matrix has no host copy");
+  cudaStream_t s = ctx->stream;
+  // allgather (n_r, nnz_r), then broadcast each rank's rows
+  int64_t* dcnt = dalloc<int64_t>(2 * R + 2);
+  int64_t mine[2] = {A->n_rows, A->nnz};
+  PSC_CUDA(cudaMemcpy(dcnt + 2 * R, mine, sizeof(mine), cudaMemcpyHostToDevice));
+  PSC_NCCL(ncclAllGather(dcnt + 2 * R, dcnt, 2, ncclInt64, ctx->comm, s));
+  std::vector<int64_t> cnt(2 * R);
+  PSC_CUDA(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(int64_t) * 2 * R, cudaMemcpyDeviceToHost, s));
+  PSC_CUDA(cudaStreamSynchronize(s));
+  dfree(dcnt);
+  int64_t totnnz = 0;
+  for (int r = 0; r < R; ++r) totnnz += cnt[2 * r + 1];
+  std::vector<int64_t> rp_all(rp.N + 1, 0), col_all(totnnz);
+  std::vector<double> val_all(totnnz);
+  int64_t row0 = 0, nz0 = 0;
+  for (int r = 0; r < R; ++r) {
+    const int64_t nr = cnt[2 * r], nz = cnt[2 * r + 1];
+    int64_t* dp = dalloc<int64_t>(nr + 1 + nz);
+    double* dv = dalloc<double>(nz);
+    if (r == ctx->rank) {
+      PSC_CUDA(cudaMemcpy(dp, A->h_rowptr.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice));
+      if (nz) {
+        PSC_CUDA(cudaMemcpy(dp + nr + 1, A->h_colg.data(), sizeof(int64_t) * nz, cudaMemcpyHostToDevice));
+        PSC_CUDA(cudaMemcpy(dv, A->h_val.data(), sizeof(double) * nz, cudaMemcpyHostToDevice));
+      }
+    }
+    PSC_NCCL(ncclBroadcast(dp, dp, nr + 1 + nz, ncclInt64, r, ctx->comm, s));
+    if (nz) PSC_NCCL(ncclBroadcast(dv, dv, nz, ncclDouble, r, ctx->comm, s));
+    std::vector<int64_t> hp(nr + 1 + nz);
+    PSC_CUDA(cudaMemcpyAsync(hp.data(), dp, sizeof(int64_t) * (nr + 1 + nz), cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaMemcpyAsync(val_all.data() + nz0, dv, sizeof(double) * nz, cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    dfree(dp);
+    dfree(dv);
+    for (int64_t i = 0; i < nr; ++i) rp_all[row0 + i + 1] = nz0 + hp[i + 1];
+    std::copy(hp.begin() + nr + 1, hp.end(), col_all.begin() + nz0);
+    row0 += nr;
+    nz0 += nz;
+  }
+  PSC_REQUIRE(row0 == rp.N, PSC_ERR_STATE, "coarsest rows do not add up");
+  int64_t* drp = dalloc<int64_t>(rp.N + 1);
+  int64_t* dcol = dalloc<int64_t>(totnnz);
+  double* dval = dalloc<double>(totnnz);
+  PSC_CUDA(cudaMemcpy(drp, rp_all.data(), sizeof(int64_t) * (rp.N + 1), cudaMemcpyHostToDevice));
+  PSC_CUDA(cudaMemcpy(dcol, col_all.data(), sizeof(int64_t) * totnnz, cudaMemcpyHostToDevice));
+  PSC_CUDA(cudaMemcpy(dval, val_all.data(), sizeof(double) * totnnz, cudaMemcpyHostToDevice));
+  sell_from_csr(ctx, rp.N, drp, dcol, dval, totnnz, 0, rp.N, nullptr, 0, rp.S, s);
+  dfree(drp);
+  dfree(dcol);
+  dfree(dval);
+  rp.dinv = dalloc<double>(rp.N);
+  launch_l1_dinv(ctx, rp.S, rp.dinv, s);
+  // b gather map: padded allgather buffer -> global index
+  for (int r = 0; r < R; ++r) rp.maxcnt = std::max(rp.maxcnt, d->row_start[r + 1] - d->row_start[r]);
+  rp.maxcnt = std::max<int64_t>(rp.maxcnt, 1);
+  std::vector<int64_t> mf(rp.N);
+  for (int r = 0; r < R; ++r)
+    for (int64_t g = d->row_start[r]; g < d->row_start[r + 1]; ++g) mf[g] = r * rp.maxcnt + (g - d->row_start[r]);
+  std::vector<int64_t> ml(W.n + W.nh);
+  for (int64_t i = 0; i < W.n; ++i) ml[i] = d->own_begin + i;
+  for (int64_t i = 0; i < W.nh; ++i) ml[W.n + i] = d->halo[i];
+  rp.map_full = dalloc<int64_t>(rp.N);
+  rp.map_loc = dalloc<int64_t>(ml.size());
+  PSC_CUDA(cudaMemcpy(rp.map_full, mf.data(), sizeof(int64_t) * rp.N, cudaMemcpyHostToDevice));
+  if (!ml.empty()) PSC_CUDA(cudaMemcpy(rp.map_loc, ml.data(), sizeof(int64_t) * ml.size(), cudaMemcpyHostToDevice));
+  rp.sendbuf = dalloc<double>(rp.maxcnt);
+  rp.gbuf = dalloc<double>((size_t)R * rp.maxcnt);
+  rp.bfull = dalloc<double>(rp.N);
+  rp.xfull = dalloc<double>(rp.N);
+  PSC_CUDA(cudaMemset(rp.sendbuf, 0, sizeof(double) * rp.maxcnt));
+  PSC_CUDA(cudaStreamSynchronize(s));
+  rp.on = true;
+}
+
+void free_hier(psc_hier* h) {
+  if (!h) return;
+  cudaSetDevice(h->ctx->device);
+  if (h->ctx->stream) cudaStreamSynchronize(h->ctx->stream);
+  for (auto& W : h->lv) {
+    dfree(W.dinv);
+    dfree(W.x[0]);
+    dfree(W.x[1]);
+    dfree(W.r);
+    if (&W != &h->lv[0]) dfree(W.b);
+  }
+  Replica& rp = h->rep;
+  sell_free(rp.S);
+  dfree(rp.dinv);
+  dfree(rp.sendbuf);
+  dfree(rp.gbuf);
+  dfree(rp.map_full);
+  dfree(rp.bfull);
+  dfree(rp.xfull);
+  dfree(rp.map_loc);
+  dfree(h->x_int);
+  dfree(h->r_cg);
+  dfree(h->p);
+  dfree(h->q);
+  dfree(h->d_scal);
+  dfree(h->d_bhost);
+  dfree(h->d_xhost);
+  if (h->h_scal) cudaFreeHost(h->h_scal);
+  red_free(h->red1);
+  red_free(h->red2);
+  if (h->iter_exec) cudaGraphExecDestroy(h->iter_exec);
+  for (auto e : h->ev_dom) cudaEventDestroy(e);
+  if (h->ev_t0) cudaEventDestroy(h->ev_t0);
+  if (h->ev_t1) cudaEventDestroy(h->ev_t1);
+  delete h;
+}
+
+int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, double* hist, psc_stats* st,
+               double extra_h2d) {
+  psc_ctx* ctx = h->ctx;
+  cudaStream_t s = ctx->stream;
+  const int R = ctx->nranks;
+  LevelWS& W = h->lv[0];
+  const int64_t l0 = ctx->launches, c0 = ctx->collectives;
+  psc_stats S{};
+  PSC_CUDA(cudaEventRecord(h->ev_t0, s));
+  if (W.n) PSC_CUDA(cudaMemcpyAsync(h->x_int, x, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+  halo_exchange(ctx, W.d, h->x_int, s);
+  {
+    RowArgs a;
+    a.x = h->x_int;
+    a.b = b;
+    a.y = h->r_cg;
+    a.red = &h->red2;
+    a.red_out = scal_mine(h, S_RR);
+    a.red_stride = (int)((size_t)(S_BB - S_RR) * R);
+    launch_rows(ctx, W.A->S, RowOp::ResidDot2, a, s);
+  }
+  allgather_slot(h, S_RR, s);
+  allgather_slot(h, S_BB, s);
+  PSC_CUDA(cudaMemcpyAsync(h->h_scal, h->d_scal, sizeof(double) * NSLOT * R, cudaMemcpyDeviceToHost, s));
+  PSC_CUDA(cudaStreamSynchronize(s));
+  const double bb = sum_ranks(h->h_scal + S_BB * R, R);
+  const double rr0 = sum_ranks(h->h_scal + S_RR * R, R);
+  const double nb = std::sqrt(bb);
+  int status = PSC_NOT_CONVERGED;
+  int iters = 0;
+  double rel = 0.0;
+  double dom_ms = 0.0;
+  int64_t dom_n = 0;
+  if (nb == 0.0) {  // b = 0 -> x = 0 and no iteration
+    if (W.n) PSC_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * W.n, s));
+    status = PSC_OK;
+    rel = 0.0;
+    if (hist) hist[0] = 0.0;
+  } else {
+    rel = std::sqrt(rr0) / nb;
+    if (hist) hist[0] = rel;
+    if (rel <= tol) {
+      status = PSC_OK;
+    } else {
+      PSC_CUDA(cudaMemsetAsync(h->p, 0, sizeof(double) * (W.n + W.nh), s));
+      const double one = 1.0;
+      PSC_CUDA(cudaMemcpyAsync(rz_old(h), &one, sizeof(double), cudaMemcpyHostToDevice, s));
+      if (!h->iter_exec) capture_iteration(h);
+      for (int k = 1; k <= maxit; ++k) {
+        PSC_CUDA(cudaGraphLaunch(h->iter_exec, s));
+        PSC_CUDA(cudaStreamSynchronize(s));
+        ctx->launches += h->iter_launches;
+        ctx->collectives += h->iter_collectives;
+        for (int e = 0; e + 1 < h->dom_used; e += 2) {
+          float ms = 0.f;
+          PSC_CUDA(cudaEventElapsedTime(&ms, h->ev_dom[e], h->ev_dom[e + 1]));
+          dom_ms += ms;
+          dom_n++;
+        }
+        const double pq = sum_ranks(h->h_scal + S_PQ * R, R);
+        const double rr = sum_ranks(h->h_scal + S_RR * R, R);
+        iters = k;
+        if (!(pq > 0.0) || !std::isfinite(pq)) {
+          status = PSC_ERR_BREAKDOWN;
+          break;
+        }
+        rel = std::sqrt(rr) / nb;
+        if (hist) hist[k] = rel;
+        if (rel <= tol) {
+          status = PSC_OK;
+          break;
+        }
+      }
+    }
+    if (W.n && status != PSC_ERR_BREAKDOWN)
+      PSC_CUDA(cudaMemcpyAsync(x, h->x_int, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+  }
+  PSC_CUDA(cudaEventRecord(h->ev_t1, s));
+  PSC_CUDA(cudaStreamSynchronize(s));
+  float tot = 0.f;
+  PSC_CUDA(cudaEventElapsedTime(&tot, h->ev_t0, h->ev_t1));
+  S.iters = iters;
+  S.status = status;
+  S.rel_res = rel;
+  S.solve_seconds = tot * 1e-3;
+  S.kernel_launches = ctx->launches - l0;
+  S.collectives = ctx->collectives - c0;
+  S.dom_kernel_seconds = dom_ms * 1e-3;
+  S.dom_kernel_launches = dom_n;
+  S.dom_kernel_bytes = 12.0 * (double)W.A->nnz + 32.0 * (double)W.n;
+  S.h2d_bytes = (int64_t)extra_h2d;
+  if (st) *st = S;
+  if (status == PSC_ERR_BREAKDOWN) throw Error(PSC_ERR_BREAKDOWN, "PCG breakdown: p^T A p <= 0 or not finite");
+  return status;
+}
+
+}  // namespace
+
+extern "C" {
+
+int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const* P, psc_mat* const* R,
+                    const psc_cycle_opts* opts, psc_hier** out) {
+  psc_hier* h = nullptr;
+  try {
+    PSC_REQUIRE(ctx && out && A && nlevels >= 1, PSC_ERR_ARG, "bad argument");
+    PSC_REQUIRE(nlevels == 1 || (P && R), PSC_ERR_ARG, "P and R required for nlevels > 1");
+    *out = nullptr;
+    enter(ctx);
+    h = new psc_hier();
+    h->ctx = ctx;
+    h->L = nlevels;
+    if (opts) h->opt = *opts;
+    PSC_REQUIRE(h->opt.pre_sweeps >= 0 && h->opt.post_sweeps >= 0 && h->opt.coarse_sweeps >= 0, PSC_ERR_ARG,
+                "negative sweep count");
+    h->lv.resize(nlevels);
+    for (int l = 0; l < nlevels; ++l) {
+      LevelWS& W = h->lv[l];
+      W.A = A[l];
+      PSC_REQUIRE(W.A && W.A->assembled, PSC_ERR_STATE, "A_l missing or not assembled");
+      PSC_REQUIRE(W.A->rows == W.A->cols, PSC_ERR_ARG, "A_l must map its index space to itself");
+      W.d = W.A->rows;
+      W.n = W.d->n_own;
+      W.nh = W.d->n_halo();
+      if (l + 1 < nlevels) {
+        W.P = P[l];
+        W.R = R[l];
+        PSC_REQUIRE(W.P && W.R && W.P->assembled && W.R->assembled, PSC_ERR_STATE, "P_l/R_l missing or not assembled");
+        PSC_REQUIRE(W.P->rows == W.d && W.P->cols == A[l + 1]->rows, PSC_ERR_ARG, "P_l: rows space l, cols space l+1");
+        PSC_REQUIRE(W.R->rows == A[l + 1]->rows && W.R->cols == W.d, PSC_ERR_ARG, "R_l: rows space l+1, cols space l");
+      }
+    }
+    cudaStream_t s = ctx->stream;
+    for (int l = 0; l < nlevels; ++l) {
+      LevelWS& W = h->lv[l];
+      W.dinv = dalloc<double>(W.n);
+      launch_l1_dinv(ctx, W.A->S, W.dinv, s);  // smoother build
+      W.x[0] = dalloc<double>(W.n + W.nh);
+      W.x[1] = dalloc<double>(W.n + W.nh);
+      W.r = dalloc<double>(W.n + W.nh);
+      PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
+      PSC_CUDA(cudaMemsetAsync(W.x[1], 0, sizeof(double) * (W.n + W.nh), s));
+      PSC_CUDA(cudaMemsetAsync(W.r, 0, sizeof(double) * (W.n + W.nh), s));
+      if (l > 0) W.b = dalloc<double>(W.n);
+    }
+    LevelWS& W0 = h->lv[0];
+    h->x_int = dalloc<double>(W0.n + W0.nh);
+    h->r_cg = dalloc<double>(W0.n);
+    h->p = dalloc<double>(W0.n + W0.nh);
+    h->q = dalloc<double>(W0.n);
+    W0.b = h->r_cg;
+    h->d_scal = dalloc<double>((size_t)NSLOT * ctx->nranks + 1);
+    PSC_CUDA(cudaMemsetAsync(h->d_scal, 0, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1), s));
+    PSC_CUDA(cudaMallocHost(&h->h_scal, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1)));
+    h->red1 = red_alloc(ctx->num_sms, 1);
+    h->red2 = red_alloc(ctx->num_sms, 2);
+    const int ndom = 2 * (std::max(h->opt.pre_sweeps - 1, 0) + h->opt.post_sweeps);
+    h->ev_dom.resize(ndom);
+    for (auto& e : h->ev_dom) PSC_CUDA(cudaEventCreate(&e));
+    PSC_CUDA(cudaEventCreate(&h->ev_t0));
+    PSC_CUDA(cudaEventCreate(&h->ev_t1));
+    // coarsest solver: one CTA when the level is small enough; replicated on
+    // every rank when distributed
+    LevelWS& Wc = h->lv[nlevels - 1];
+    if (ctx->nranks > 1) build_replica(h);
+    else h->coarse_one_cta = (Wc.n <= coarse_smem_rows() && Wc.nh == 0);
+    PSC_CUDA(cudaStreamSynchronize(s));
+    *out = h;
+    return PSC_OK;
+  } catch (const Error& e) {
+    free_hier(h);
+    return hfail(ctx, e);
+  } catch (const std::exception& e) {
+    free_hier(h);
+    return hfail(ctx, Error(PSC_ERR_ARG, e.what()));
+  }
+}
+
+int psc_hier_info(psc_hier* h, int* nlevels, int64_t* n_owned, int64_t* nnz_A, int64_t* nnz_P, int64_t* nnz_R) {
+  if (!h) return PSC_ERR_ARG;
+  if (nlevels) *nlevels = h->L;
+  for (int l = 0; l < h->L; ++l) {
+    const LevelWS& W = h->lv[l];
+    if (n_owned) n_owned[l] = W.n;
+    if (nnz_A) nnz_A[l] = W.A->nnz;
+    if (nnz_P) nnz_P[l] = W.P ? W.P->nnz : 0;
+    if (nnz_R) nnz_R[l] = W.R ? W.R->nnz : 0;
+  }
+  return PSC_OK;
+}
+
+int psc_hier_vcycle(psc_hier* h, const double* r, double* z) {
+  psc_ctx* ctx = h ? h->ctx : nullptr;
+  try {
+    PSC_REQUIRE(h && (r || h->lv[0].n == 0) && (z || h->lv[0].n == 0), PSC_ERR_ARG, "null argument");
+    enter(ctx);
+    cudaStream_t s = ctx->stream;
+    LevelWS& W = h->lv[0];
+    if (W.n) PSC_CUDA(cudaMemcpyAsync(h->r_cg, r, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+    double* zz = vcycle_level(h, 0, h->r_cg, s, false);
+    if (W.n) PSC_CUDA(cudaMemcpyAsync(z, zz, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    return PSC_OK;
+  } catch (const Error& e) {
+    return hfail(ctx, e);
+  }
+}
+
+int psc_hier_dinv(psc_hier* h, int level, double* dinv) {
+  psc_ctx* ctx = h ? h->ctx : nullptr;
+  try {
+    PSC_REQUIRE(h && level >= 0 && level < h->L, PSC_ERR_ARG, "bad level");
+    enter(ctx);
+    LevelWS& W = h->lv[level];
+    if (W.n) PSC_CUDA(cudaMemcpyAsync(dinv, W.dinv, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, ctx->stream));
+    PSC_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PSC_OK;
+  } catch (const Error& e) {
+    return hfail(ctx, e);
+  }
+}
+
+int psc_hier_smooth(psc_hier* h, int level, const double* b, double* x, int nsweeps) {
+  psc_ctx* ctx = h ? h->ctx : nullptr;
+  try {
+    PSC_REQUIRE(h && level >= 0 && level < h->L && nsweeps >= 0, PSC_ERR_ARG, "bad argument");
+    enter(ctx);
+    cudaStream_t s = ctx->stream;
+    LevelWS& W = h->lv[level];
+    double* bl = W.b;
+    if (W.n) PSC_CUDA(cudaMemcpyAsync(bl, b, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+    double* res;
+    if (level == h->L - 1) res = coarse_solve(h, bl, nsweeps, s);
+    else res = W.x[pre_smooth(h, level, bl, nsweeps, s, false)];
+    if (W.n) PSC_CUDA(cudaMemcpyAsync(x, res, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    return PSC_OK;
+  } catch (const Error& e) {
+    return hfail(ctx, e);
+  }
+}
+
+int psc_pcg_solve(psc_hier* h, const double* b, double* x, double tol, int maxit, double* hist, psc_stats* st) {
+  psc_ctx* ctx = h ? h->ctx : nullptr;
+  try {
+    PSC_REQUIRE(h && maxit >= 0 && tol >= 0.0, PSC_ERR_ARG, "bad argument");
+    PSC_REQUIRE((b && x) || h->lv[0].n == 0, PSC_ERR_ARG, "null b/x");
+    enter(ctx);
+    return solve_impl(h, b, x, tol, maxit, hist, st, 0.0);
+  } catch (const Error& e) {
+    return hfail(ctx, e);
+  }
+}
+
+int psc_pcg_solve_host(psc_hier* h, const double* b_host, double* x_host, double tol, int maxit, double* hist,
+                       psc_stats* st) {
+  psc_ctx* ctx = h ? h->ctx : nullptr;
+  try {
+    PSC_REQUIRE(h && maxit >= 0 && tol >= 0.0, PSC_ERR_ARG, "bad argument");
+    const int64_t n = h->lv[0].n;
+    PSC_REQUIRE((b_host && x_host) || n == 0, PSC_ERR_ARG, "null b/x");
+    enter(ctx);
+    cudaStream_t s = ctx->stream;
+    if (!h->d_bhost) {
+      h->d_bhost = dalloc<double>(n);
+      h->d_xhost = dalloc<double>(n);
+    }
+    if (n) {
+      PSC_CUDA(cudaMemcpyAsync(h->d_bhost, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      PSC_CUDA(cudaMemcpyAsync(h->d_xhost, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    }
+    psc_stats S{};
+    int rc = solve_impl(h, h->d_bhost, h->d_xhost, tol, maxit, hist, &S, 16.0 * (double)n);
+    if (n) PSC_CUDA(cudaMemcpyAsync(x_host, h->d_xhost, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    S.d2h_bytes = 8 * n;
+    if (st) *st = S;
+    return rc;
+  } catch (const Error& e) {
+    return hfail(ctx, e);
+  }
+}
+
+void psc_hier_destroy(psc_hier* h) { free_hier(h); }
+
+}  // extern "C"

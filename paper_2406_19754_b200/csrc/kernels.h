@@ -1,0 +1,73 @@
+// kernels.h — launchers of the sm_100a kernels of the solve path.
+#pragma once
+#include "psc_internal.h"
+
+namespace psc {
+
+// Row-wise sliced-ELL kernels: s_i = sum_k val * x[col] over row i (stored order,
+// fused multiply-add), then an epilogue.  `x` is an owned+halo vector of the
+// column space.  Reductions are deterministic: fixed warp-shuffle tree, fixed
+// block order, finalised by the last CTA to finish (ticket), written to `red_out`.
+enum class RowOp {
+  Spmv,       // y = alpha s + beta y           (beta == 0: y not read)
+  SpmvDot,    // y = s;  red0 += x_i * s        (q = A p and (p, q))
+  Sweep,      // y = x_i + dinv_i (b_i - s)     (l1-Jacobi sweep, Jacobi: reads old x)
+  SweepDot,   // Sweep, red0 += b_i * y_i       (last level-0 post-sweep: (r, z))
+  Resid,      // y = b_i - s
+  ResidDot2,  // y = b_i - s; red0 += y_i^2; red1 += b_i^2
+  PAdd,       // y += s                         (prolongation x_l += P x_{l+1})
+};
+
+struct RowArgs {
+  double alpha = 1.0, beta = 0.0;
+  const double* x = nullptr;
+  const double* b = nullptr;
+  const double* dinv = nullptr;
+  double* y = nullptr;
+  const RedSite* red = nullptr;
+  double* red_out = nullptr;   // red0 -> red_out[0], red1 -> red_out[red_stride]
+  int red_stride = 1;
+};
+
+// Which slices: all, interior only (no halo column), boundary only.
+enum class SliceSet { All, Interior, Boundary };
+
+int row_grid(const Sell& A, RowOp op, int num_sms, SliceSet set = SliceSet::All);
+void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& a, cudaStream_t s,
+                 SliceSet set = SliceSet::All);
+
+// x = dinv .* b  (first sweep from x = 0: x + M^-1 (b - A 0) = M^-1 b)
+void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, double* x, cudaStream_t s);
+// m_i = a_ii + sum_{j != i} |a_ij| over the stored row;  dinv_i = 1 / m_i
+void launch_l1_dinv(psc_ctx* ctx, const Sell& A, double* dinv, cudaStream_t s);
+// gathered scalars: value of slot = sum over ranks of g[slot*nranks + r], in rank order
+// CG: alpha = rz_old / pq ; x += alpha p ; r -= alpha q ; red(r.r)
+void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
+                      const double* g_pq, const double* rz_old, int nranks, const RedSite* red, double* red_out,
+                      cudaStream_t s);
+// beta = rz / rz_old ; p = z + beta p ; then rz_old := rz (by the last CTA)
+void launch_xpby(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rz, double* rz_old,
+                 int nranks, const RedSite* red, cudaStream_t s);
+// red(a . b)
+void launch_dot(psc_ctx* ctx, int64_t n, const double* a, const double* b, const RedSite* red, double* red_out,
+                cudaStream_t s);
+// sendbuf[i] = x[idx[i]]
+void launch_pack(psc_ctx* ctx, int64_t n, const int32_t* idx, const double* x, double* sendbuf, cudaStream_t s);
+// out[i] = in[map[i]]  (gather from a replicated vector into owned+halo layout)
+void launch_gather(psc_ctx* ctx, int64_t n, const int64_t* map, const double* in, double* out, cudaStream_t s);
+// Coarsest solver in ONE CTA: x = dinv .* b, then nsweeps-1 l1-Jacobi sweeps in shared memory.
+// Requires n <= coarse_smem_rows().
+int64_t coarse_smem_rows();
+void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const double* b, double* x, int nsweeps,
+                         cudaStream_t s);
+
+// CSR (global int64 columns) -> sliced ELL with local int32 columns.
+void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg,
+                   const double* d_val, int64_t nnz, int64_t own_begin, int64_t n_own, const int64_t* d_halo,
+                   int64_t n_halo, Sell& S, cudaStream_t s);
+void sell_free(Sell& S);
+
+RedSite red_alloc(int num_sms, int nred);
+void red_free(RedSite& r);
+
+}  // namespace psc

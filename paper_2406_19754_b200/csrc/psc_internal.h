@@ -1,0 +1,139 @@
+// psc_internal.h — internal types of libpsc.so (B200 / sm_100a).
+// Nothing here is part of the ABI (see include/psc.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "psc.h"
+
+namespace psc {
+
+constexpr int kSlice = 32;        // rows per sliced-ELL slice = warp size ("based on the size of a warp")
+constexpr int kBlock = 256;       // threads per CTA for the row kernels (8 slices per CTA pass)
+constexpr int kWarpsPerBlock = kBlock / 32;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PSC_CUDA(call)                                                                                  \
+  do {                                                                                                  \
+    cudaError_t e_ = (call);                                                                            \
+    if (e_ != cudaSuccess)                                                                              \
+      throw ::psc::Error(e_ == cudaErrorMemoryAllocation ? PSC_ERR_NOMEM : PSC_ERR_CUDA,                \
+                         std::string(#call) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + ":" + \
+                             std::to_string(__LINE__));                                                 \
+  } while (0)
+
+#define PSC_NCCL(call)                                                                                    \
+  do {                                                                                                    \
+    ncclResult_t r_ = (call);                                                                             \
+    if (r_ != ncclSuccess)                                                                                \
+      throw ::psc::Error(PSC_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_) + " @" + __FILE__ + \
+                                           ":" + std::to_string(__LINE__));                               \
+  } while (0)
+
+#define PSC_REQUIRE(cond, code, msg)                 \
+  do {                                               \
+    if (!(cond)) throw ::psc::Error((code), (msg)); \
+  } while (0)
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  PSC_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+inline void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+// Device sliced-ELL (Hacked ELLPACK): rows grouped in 32-row slices;
+// slice s stores its width w_s = max row length of its rows as a column-major
+// w_s x 32 block at element offset slice_ptr[s]; row (32 s + lane), entry k is at
+// slice_ptr[s] + 32 k + lane.  Padding: value 0.0, column = the row's last valid
+// column (0 for empty rows / rows past n_rows).  Width = (slice_ptr[s+1]-slice_ptr[s])/32.
+struct Sell {
+  int64_t n_rows = 0, n_cols_local = 0, n_slices = 0, nnz = 0, padded = 0;
+  int64_t* slice_ptr = nullptr;  // n_slices + 1
+  int32_t* col = nullptr;        // padded
+  double* val = nullptr;         // padded
+  // slices whose columns are all owned (interior) and the others (boundary):
+  // the interior ones can run while the halo exchange is in flight.
+  int32_t* interior = nullptr;
+  int32_t* boundary = nullptr;
+  int64_t n_interior = 0, n_boundary = 0;
+  int max_width = 0;
+};
+
+// Per-reduction-site scratch: block partials, a ticket counter, and the slot of
+// the gathered-scalar array the finalising block writes (fixed-order sums).
+struct RedSite {
+  double* partials = nullptr;  // [nred][grid]
+  unsigned int* ticket = nullptr;
+  int grid = 0;
+};
+
+}  // namespace psc
+
+struct psc_ctx_s {
+  int rank = 0, nranks = 1, device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;       // library stream (all work)
+  cudaStream_t comm_stream = nullptr;  // halo exchange stream (overlap)
+  cudaStream_t user_stream = nullptr;
+  cudaEvent_t ev_user = nullptr;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  int64_t launches = 0;     // kernel launch counter (incremented by every launcher)
+  int64_t collectives = 0;  // NCCL call counter
+};
+
+struct psc_desc_s {
+  psc_ctx* ctx = nullptr;
+  int64_t n_global = 0;
+  std::vector<int64_t> row_start;
+  int64_t own_begin = 0, n_own = 0;
+  std::vector<int64_t> halo_req;  // registrations (unsorted, duplicates) until assembly
+  bool assembled = false;
+  std::vector<int64_t> halo;              // sorted unique off-rank globals
+  std::vector<int64_t> rcount, roff;      // per peer: received halo entries / offset in the halo region
+  std::vector<int64_t> scount, soff;      // per peer: entries sent / offset in the send list
+  int64_t n_send = 0;
+  int32_t* d_send_idx = nullptr;          // local owned indices to send, grouped by peer
+  double* d_sendbuf = nullptr;
+  int64_t* d_halo = nullptr;              // halo globals on the device (column renumbering)
+  int64_t n_halo() const { return (int64_t)halo.size(); }
+};
+
+struct psc_mat_s {
+  psc_ctx* ctx = nullptr;
+  psc_desc* rows = nullptr;
+  psc_desc* cols = nullptr;
+  int64_t n_rows = 0, nnz = 0;
+  // staged device CSR (global columns) until assembly
+  int64_t* d_rowptr = nullptr;
+  int64_t* d_colg = nullptr;
+  double* d_valcsr = nullptr;
+  bool assembled = false;
+  psc::Sell S;
+  // host copy of this rank's rows (global columns), kept for small matrices only:
+  // used to replicate the coarsest level on every rank.
+  std::vector<int64_t> h_rowptr, h_colg;
+  std::vector<double> h_val;
+};
+
+namespace psc {
+// ctx_desc.cu
+void halo_exchange(psc_ctx* ctx, psc_desc* d, double* x, cudaStream_t s);
+void desc_assemble(psc_desc* d);
+// mat.cu
+void mat_assemble(psc_mat* m);
+}  // namespace psc

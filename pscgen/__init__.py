@@ -234,3 +234,21 @@ def rhs_poisson(grid, start: int, count: int) -> np.ndarray:
     """b = h^2 * f with f = 1 and h = 1/(nx_global + 1) (reading R15)."""
     h = 1.0 / (grid[0] + 1)
     return np.full(count, h * h, dtype=np.float64)
+
+
+def rank_levels(h: Hierarchy, r: int) -> list:
+    """Per-level inputs of rank r for the C ABI (psc_desc_create / psc_mat_create_csr):
+    n_global, row_start, and this rank's CSR rows (row_ptr, int64 global cols, values)
+    of A_l, P_l (rows in space l) and R_l (rows in space l+1)."""
+    out = []
+    for l, L in enumerate(h.levels):
+        d = dict(n_global=L.n, row_start=L.row_start)
+        A = h.rank_piece(l, "A", r)
+        d["A"] = (A.ptr, A.col, A.val)
+        if l < h.nlevels - 1:
+            P = h.rank_piece(l, "P", r)
+            R = h.rank_piece(l, "R", r)
+            d["P"] = (P.ptr, P.col, P.val)
+            d["R"] = (R.ptr, R.col, R.val)
+        out.append(d)
+    return out
