@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py — AMG-PCG solve phase (PSCToolkit, arXiv 2406.19754) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl psc|reference] [--grid 256]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload: BASELINE.json configs[2], 3D Poisson 7-point, 256^3
+unknowns PER GPU (weak scaling; rank boxes (1,1,1), (1,1,2), (1,2,2), (2,2,2)),
+decoupled-VMB smoothed-aggregation hierarchy, V-cycle 4/4 l1-Jacobi sweeps,
+30 coarsest sweeps, PCG to tol 1e-8 from x0 = 0.  One step = one full PCG
+solve (every row of SURVEY.md §8(a)), right-hand side b_k = (k+1) h^2 1.
+Metric: Mdof*iters/s = N_global * iterations / solve seconds / 1e6 (whole job).
+
+--impl reference runs the CPU oracle (oracle/, single thread) on rank 0 only,
+each step one PCG iteration on a 256^3 single-box sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PROCS = {1: (1, 1, 1), 2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}
+
+
+def procs_for(n):
+    """Rank-box grid (px, py, pz) for n GPUs: split z first, then y, then x."""
+    if n in PROCS:
+        return PROCS[n]
+    f = [1, 1, 1]
+    k, p = n, 2
+    while k > 1:
+        while k % p == 0:
+            i = min((2, 1, 0), key=lambda j: f[j])  # smallest extent, z preferred on ties
+            f[i] *= p
+            k //= p
+        p += 1
+    return tuple(f)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(key):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        v = d.get(key)
+        if isinstance(v, dict):
+            return v.get("dram_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self, gpus):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            c = [x.strip() for x in line.split(",")]
+            if len(c) < 9 or not c[0].isdigit() or int(c[0]) not in gpus:
+                continue
+            try:
+                sm.append(float(c[1]))
+                mx = max(mx, float(c[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, c[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- inputs
+def save_rank_levels(d, h, nranks):
+    import pscgen
+    os.makedirs(d, exist_ok=True)
+    meta = {"nlevels": h.nlevels, "nranks": nranks, "n": [L.n for L in h.levels],
+            "row_start": [L.row_start.tolist() for L in h.levels], "oc": h.operator_complexity()}
+    for r in range(nranks):
+        for l, lv in enumerate(pscgen.rank_levels(h, r)):
+            for k in ("A", "P", "R"):
+                if k in lv:
+                    for nm, arr in zip(("ptr", "col", "val"), lv[k]):
+                        np.save(os.path.join(d, f"r{r}_l{l}_{k}_{nm}.npy"), np.ascontiguousarray(arr))
+    with open(os.path.join(d, "meta.json.tmp"), "w") as f:
+        json.dump(meta, f)
+    os.replace(os.path.join(d, "meta.json.tmp"), os.path.join(d, "meta.json"))
+
+
+def load_rank_levels(d, r):
+    with open(os.path.join(d, "meta.json")) as f:
+        meta = json.load(f)
+    out = []
+    for l in range(meta["nlevels"]):
+        lv = dict(n_global=meta["n"][l], row_start=np.array(meta["row_start"][l], np.int64))
+        for k in ("A", "P", "R"):
+            p = os.path.join(d, f"r{r}_l{l}_{k}_ptr.npy")
+            if os.path.exists(p):
+                lv[k] = tuple(np.load(os.path.join(d, f"r{r}_l{l}_{k}_{nm}.npy"), mmap_mode="r")
+                              for nm in ("ptr", "col", "val"))
+        out.append(lv)
+    return out, meta
+
+
+# -------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    """CPU oracle arm: rank 0 only; each step = 1 PCG iteration on a 256^3 sample."""
+    if rank != 0:
+        return
+    import oracle
+    import pscgen
+    g = args.grid
+    h = pscgen.poisson_hierarchy(g, g, g, (1, 1, 1))
+    n = h.levels[0].n
+    b = pscgen.rhs_poisson((g, g, g), 0, n)
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        x, it, st, hist = oracle.pcg(h, b * (k + 1), tol=0.0, maxit=1)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+    t = sum(times)
+    value = n * args.steps / t / 1e6
+    line = {
+        "impl": "reference", "metric": "AMG-PCG Mdof*iters/s", "value": value, "unit": "Mdof*iters/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"3D Poisson 7-point {g}^3 single-box sample of the {g}^3-per-GPU weak-scaling "
+                               "workload (BASELINE.json configs[2]); step = 1 PCG iteration of the CPU oracle",
+                   "levels": h.nlevels, "n_dof": n},
+        "cpu_baseline": {"value": value, "unit": "Mdof*iters/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} steps x 1 PCG iteration (incl. its V-cycles) on {g}^3"},
+        "e2e": {"value": value, "unit": "Mdof*iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="psc", choices=["psc", "reference"])
+    ap.add_argument("--grid", type=int, default=256, help="box edge per GPU")
+    ap.add_argument("--problem", default="poisson", choices=["poisson", "jump"])
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--maxit", type=int, default=200)
+    ap.add_argument("--cpu-iters", type=int, default=2, help="oracle PCG iterations in the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
+    N = max(world, 1) if world > 1 else 1
+    if args.gpus > 1 and world == 1:
+        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+
+    if args.impl == "reference":
+        run_reference(args, rank, N)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_19754_b200 as psc
+    import pscgen
+
+    torch.cuda.set_device(local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    px, py, pz = procs_for(N)
+    g = args.grid
+    grid = (g * px, g * py, g * pz)
+    t_setup0 = time.perf_counter()
+    h = None
+    if N == 1:
+        h = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem)
+        levels = pscgen.rank_levels(h, 0)
+        oc = h.operator_complexity()
+    else:
+        shm = f"/dev/shm/psc_bench_{args.problem}_{grid[0]}x{grid[1]}x{grid[2]}_{px}{py}{pz}"
+        if rank == 0 and not os.path.exists(os.path.join(shm, "meta.json")):
+            hh = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem)
+            save_rank_levels(shm, hh, N)
+            del hh
+        dist.barrier()
+        levels, meta = load_rank_levels(shm, rank)
+        oc = meta["oc"]
+    t_gen = time.perf_counter() - t_setup0
+
+    uid = None
+    if N > 1:
+        obj = [psc.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = psc.Context(rank=rank, nranks=N, device=local, unique_id=uid)
+    t1 = time.perf_counter()
+    H, descs, A, P, R = psc.build_hierarchy(ctx, levels)
+    t_build = time.perf_counter() - t1
+    info = H.info()
+    n_loc = info["n_owned"][0]
+    r0 = int(levels[0]["row_start"][rank])
+    n_global = int(levels[0]["n_global"])
+    b_base = pscgen.rhs_poisson(grid, r0, n_loc)
+    nsteps = args.warmup + args.steps
+    bs = [torch.from_numpy(b_base * (k + 1)).cuda() for k in range(nsteps)]
+    xs = [torch.zeros(n_loc, dtype=torch.float64, device="cuda") for _ in range(nsteps)]
+    lib_stream = torch.cuda.ExternalStream(ctx.stream)
+
+    def barrier():
+        if N > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def maxover(v):
+        if N == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for k in range(args.warmup):
+        H.solve(bs[k], xs[k], tol=args.tol, maxit=args.maxit)
+
+    barrier()
+    clocks = ClockSampler() if local == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    e0.record(lib_stream)
+    for k in range(args.warmup, nsteps):
+        rc, st, hist = H.solve(bs[k], xs[k], tol=args.tol, maxit=args.maxit)
+        stats.append(st)
+    e1.record(lib_stream)
+    barrier()
+    clk = clocks.stop(list(range(N))) if clocks else None
+    t = maxover(e0.elapsed_time(e1) * 1e-3)
+    iters = [s["iters"] for s in stats]
+    value = n_global * sum(iters) / t / 1e6
+
+    # dominant kernel: level-0 fused l1-Jacobi sweep (events inside the graph, library stream)
+    dom_s = sum(s["dom_kernel_seconds"] for s in stats)
+    dom_n = sum(s["dom_kernel_launches"] for s in stats)
+    dom_b = stats[0]["dom_kernel_bytes"]
+    peak, peak_src = load_peaks()
+    achieved = dom_b * dom_n / dom_s / 1e9 if dom_s > 0 else None
+    roof = {"bound": "hbm", "kernel": "row_kernel<Sweep> (level-0 fused l1-Jacobi sweep)",
+            "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+            "frac": achieved / peak if achieved else None,
+            "traffic": load_traffic(f"sweep_l0_{g}"), "algorithmic_bytes_per_launch": dom_b,
+            "launches": dom_n, "avg_launch_us": 1e6 * dom_s / dom_n if dom_n else None,
+            "share_of_step": dom_s / sum(s["solve_seconds"] for s in stats)}
+
+    # end to end: host b / x through psc_pcg_solve_host, pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        bh = [torch.from_numpy(b_base * (k + 1)).pin_memory().numpy() for k in range(args.steps)]
+        xh = [torch.zeros(n_loc, dtype=torch.float64).pin_memory().numpy() for _ in range(args.steps)]
+        H.solve_host(bh[0], xh[0].copy(), tol=args.tol, maxit=args.maxit)  # warm
+        barrier()
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        it_h, h2d, d2h = 0, 0, 0
+        e2.record(lib_stream)
+        for k in range(args.steps):
+            rc, st, hist = H.solve_host(bh[k], xh[k], tol=args.tol, maxit=args.maxit)
+            it_h += st["iters"]
+            h2d += st["h2d_bytes"]
+            d2h += st["d2h_bytes"]
+        e3.record(lib_stream)
+        barrier()
+        te = maxover(e2.elapsed_time(e3) * 1e-3)
+        e2e = {"value": n_global * it_h / te / 1e6, "unit": "Mdof*iters/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "api": "psc_pcg_solve_host"}
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        import oracle
+        bcpu = pscgen.rhs_poisson(grid, 0, n_global)
+        t0 = time.perf_counter()
+        oracle.pcg(h, bcpu, tol=0.0, maxit=args.cpu_iters)
+        tc = time.perf_counter() - t0
+        cpu = {"value": n_global * args.cpu_iters / tc / 1e6, "unit": "Mdof*iters/s", "cores": 1, "kind": "oracle",
+               "sample": f"{args.cpu_iters} PCG iterations (tol 0) of the same {grid[0]}x{grid[1]}x{grid[2]} "
+                         f"workload, single thread, {tc:.1f} s"}
+
+    if rank == 0:
+        solve_s = [s["solve_seconds"] for s in stats]
+        line = {
+            "metric": "AMG-PCG Mdof*iters/s (3D Poisson, 256^3 dof per GPU, tol 1e-8)",
+            "value": value, "unit": "Mdof*iters/s", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"3D {args.problem} 7-point {g}^3 dof per GPU, weak scaling (BASELINE.json configs[2])",
+                "global_grid": list(grid), "procs": [px, py, pz], "n_global": n_global, "levels": info["nlevels"],
+                "rows_rank0": info["n_owned"], "nnz_A_rank0": info["nnz_A"], "operator_complexity": oc,
+                "cycle": "V(4,4) l1-Jacobi, 30 coarsest sweeps", "tol": args.tol, "iters": iters,
+                "solve_s_median": statistics.median(solve_s), "solve_s_per_step": solve_s,
+                "rhs": "b_k = (k+1) h^2 1, x0 = 0", "parallelism": f"dp{N} row-block",
+                "l2": "inputs larger than L2 (A_0 alone ~1.4 GB/GPU vs 126 MB L2)",
+                "setup_s": {"generate": round(t_gen, 2), "create_assemble_hier": round(t_build, 2)},
+                "model": "none (sparse solver)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": sum(s["kernel_launches"] for s in stats),
+            "collectives": sum(s["collectives"] for s in stats),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if N > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -87,6 +87,9 @@ const char* psc_status_string(int status);
 const char* psc_last_error(psc_ctx* ctx);
 /* Library build string (compiler, arch). */
 const char* psc_version(void);
+/* The cudaStream_t all of this context's work runs on (for callers that bracket
+ * library calls with their own CUDA events).  Owned by the context. */
+void* psc_ctx_stream(psc_ctx* ctx);
 
 /* --------------------------------------------------------------- descriptor */
 
@@ -124,8 +127,12 @@ int psc_mat_create_csr(psc_ctx* ctx, psc_desc* rows, psc_desc* cols, int64_t n_l
  * column).  Needs both descriptors assembled. */
 int psc_mat_assemble(psc_mat* m);
 
-/* nnz (stored), padded slots (total sliced-ELL slots), slices, local rows (any may be NULL). */
-int psc_mat_info(psc_mat* m, int64_t* nnz, int64_t* padded_slots, int64_t* n_slices, int64_t* n_rows);
+/* After assembly (any pointer may be NULL): nnz stored; padded = total device slots
+ * including padding; n_units = warp work units (32-row slices, or 32/lanes-row
+ * blocks); n_rows local rows; lanes = 1 for the sliced-ELL layout (one thread per
+ * row), or G in {4, 8, 16, 32} for the row-group layout (G lanes per row, rows
+ * padded to multiples of G) chosen for long rows. */
+int psc_mat_info(psc_mat* m, int64_t* nnz, int64_t* padded, int64_t* n_units, int64_t* n_rows, int* lanes);
 
 /* [collective] y_dev = alpha * A * x_dev + beta * y_dev (test hook; includes the
  * halo exchange of x).  x_dev: n_owned(cols); y_dev: n_owned(rows). */

@@ -59,6 +59,7 @@ _sig("psc_finalize", None, [_vp])
 _sig("psc_status_string", ctypes.c_char_p, [_i32])
 _sig("psc_last_error", ctypes.c_char_p, [_vp])
 _sig("psc_version", ctypes.c_char_p, [])
+_sig("psc_ctx_stream", _vp, [_vp])
 _sig("psc_desc_create", _i32, [_vp, _i64, _vp, _P(_vp)])
 _sig("psc_desc_assemble", _i32, [_vp])
 _sig("psc_desc_info", _i32, [_vp, _P(_i64), _P(_i64), _P(_i64)])
@@ -66,7 +67,7 @@ _sig("psc_desc_halo", _i32, [_vp, _vp])
 _sig("psc_desc_destroy", None, [_vp])
 _sig("psc_mat_create_csr", _i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _P(_vp)])
 _sig("psc_mat_assemble", _i32, [_vp])
-_sig("psc_mat_info", _i32, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)])
+_sig("psc_mat_info", _i32, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64), _P(_i32)])
 _sig("psc_mat_spmv", _i32, [_vp, _f64, _vp, _f64, _vp])
 _sig("psc_mat_destroy", None, [_vp])
 _sig("psc_hier_create", _i32, [_vp, _i32, _vp, _vp, _vp, _P(CycleOpts), _P(_vp)])
@@ -137,6 +138,11 @@ class Context:
         self.rank, self.nranks, self.device = rank, nranks, device
         self._children = []
 
+    @property
+    def stream(self) -> int:
+        """cudaStream_t (as int) of the library stream; wrap with torch.cuda.ExternalStream."""
+        return _lib.psc_ctx_stream(self.handle)
+
     def close(self):
         if self.handle:
             for c in reversed(self._children):
@@ -206,10 +212,10 @@ class Matrix:
         return self
 
     def info(self):
-        a, b, c, d = _i64(), _i64(), _i64(), _i64()
-        _check(_lib.psc_mat_info(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
-               self.ctx)
-        return dict(nnz=a.value, padded=b.value, n_slices=c.value, n_rows=d.value)
+        a, b, c, d, e = _i64(), _i64(), _i64(), _i64(), _i32()
+        _check(_lib.psc_mat_info(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d),
+                                 ctypes.byref(e)), self.ctx)
+        return dict(nnz=a.value, padded=b.value, n_units=c.value, n_rows=d.value, lanes=e.value)
 
     def spmv(self, x, y, alpha=1.0, beta=0.0):
         """y = alpha A x + beta y (device tensors; owned parts)."""

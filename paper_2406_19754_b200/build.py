@@ -1,6 +1,6 @@
 """Build libpsc.so in-tree: nvcc for sm_100a (B200), NCCL from the torch-bundled wheel.
 
-    python -m paper_2406_19754_b200.build [--force]
+    python paper_2406_19754_b200/build.py [--force]     (or __graft_entry__.build())
 """
 from __future__ import annotations
 

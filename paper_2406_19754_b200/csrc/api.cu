@@ -161,6 +161,8 @@ const char* psc_status_string(int st) {
   return "PSC_UNKNOWN_STATUS";
 }
 
+void* psc_ctx_stream(psc_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
 const char* psc_last_error(psc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
 int psc_get_unique_id(unsigned char id[128]) {
@@ -359,15 +361,16 @@ int psc_mat_assemble(psc_mat* m) {
   API_END(ctx)
 }
 
-int psc_mat_info(psc_mat* m, int64_t* nnz, int64_t* padded, int64_t* n_slices, int64_t* n_rows) {
+int psc_mat_info(psc_mat* m, int64_t* nnz, int64_t* padded, int64_t* n_units, int64_t* n_rows, int* lanes) {
   psc_ctx* ctx = m ? m->ctx : nullptr;
   API_BEGIN
   PSC_REQUIRE(m, PSC_ERR_ARG, "null matrix");
   PSC_REQUIRE(m->assembled, PSC_ERR_STATE, "matrix not assembled");
   if (nnz) *nnz = m->nnz;
   if (padded) *padded = m->S.padded;
-  if (n_slices) *n_slices = m->S.n_slices;
+  if (n_units) *n_units = m->S.n_units;
   if (n_rows) *n_rows = m->n_rows;
+  if (lanes) *lanes = m->S.lanes;
   return PSC_OK;
   API_END(ctx)
 }
@@ -389,7 +392,7 @@ int psc_mat_spmv(psc_mat* m, double alpha, const double* x, double beta, double*
   a.beta = beta;
   a.x = xh;
   a.y = y;
-  if (m->S.n_slices) launch_rows(ctx, m->S, RowOp::Spmv, a, s);
+  if (m->S.n_units) launch_rows(ctx, m->S, RowOp::Spmv, a, s);
   PSC_CUDA(cudaStreamSynchronize(s));
   dfree(xh);
   return PSC_OK;

@@ -62,9 +62,11 @@ void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const 
                          cudaStream_t s);
 
 // CSR (global int64 columns) -> sliced ELL with local int32 columns.
+// lanes: 0 = choose from the mean row length (choose_lanes), else 1 / 4 / 8 / 16 / 32.
+int choose_lanes(int64_t n_rows, int64_t nnz);
 void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg,
                    const double* d_val, int64_t nnz, int64_t own_begin, int64_t n_own, const int64_t* d_halo,
-                   int64_t n_halo, Sell& S, cudaStream_t s);
+                   int64_t n_halo, Sell& S, cudaStream_t s, int lanes = 0);
 void sell_free(Sell& S);
 
 RedSite red_alloc(int num_sms, int nred);

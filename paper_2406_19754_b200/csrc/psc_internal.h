@@ -55,22 +55,31 @@ inline void dfree(void* p) {
   if (p) cudaFree(p);
 }
 
-// Device sliced-ELL (Hacked ELLPACK): rows grouped in 32-row slices;
-// slice s stores its width w_s = max row length of its rows as a column-major
-// w_s x 32 block at element offset slice_ptr[s]; row (32 s + lane), entry k is at
-// slice_ptr[s] + 32 k + lane.  Padding: value 0.0, column = the row's last valid
-// column (0 for empty rows / rows past n_rows).  Width = (slice_ptr[s+1]-slice_ptr[s])/32.
+// Device matrix, one of two layouts chosen at assembly from the mean row length
+// (DESIGN.md §5):
+//  lanes == 1  sliced ELL (Hacked ELLPACK): rows grouped in 32-row
+//              slices; slice s stores its width w_s = max row length of its rows
+//              as a column-major w_s x 32 block at element offset ptr[s]; entry k
+//              of row (32 s + lane) is at ptr[s] + 32 k + lane.  One thread per row.
+//  lanes == G  row groups (G in {4,8,16,32}): rows stored contiguously, each padded
+//              to a multiple of G entries, ptr[i] = start of row i; G lanes of a
+//              warp share one row (long rows of coarse A_l and R_l).
+// Padding: value 0.0, column = the row's last valid column (0 for empty rows).
+// A warp processes one "unit": a slice (lanes == 1) or 32/G consecutive rows.
 struct Sell {
-  int64_t n_rows = 0, n_cols_local = 0, n_slices = 0, nnz = 0, padded = 0;
-  int64_t* slice_ptr = nullptr;  // n_slices + 1
-  int32_t* col = nullptr;        // padded
-  double* val = nullptr;         // padded
-  // slices whose columns are all owned (interior) and the others (boundary):
+  int64_t n_rows = 0, n_cols_local = 0, nnz = 0, padded = 0;
+  int lanes = 1;
+  int64_t n_units = 0;
+  int64_t* ptr = nullptr;  // lanes == 1: n_units + 1 slice offsets; else n_rows + 1 row offsets
+  int32_t* col = nullptr;  // padded
+  double* val = nullptr;   // padded
+  // units whose columns are all owned (interior) and the others (boundary):
   // the interior ones can run while the halo exchange is in flight.
   int32_t* interior = nullptr;
   int32_t* boundary = nullptr;
   int64_t n_interior = 0, n_boundary = 0;
-  int max_width = 0;
+  int max_width = 0;  // longest (padded) row
+  int rows_per_unit() const { return lanes == 1 ? 32 : 32 / lanes; }
 };
 
 // Per-reduction-site scratch: block partials, a ticket counter, and the slot of

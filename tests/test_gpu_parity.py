@@ -75,19 +75,32 @@ def test_spmv_all_level_matrices(psc, grid):
             assert np.all(err <= tol), (name, l, float((err / tol).max()))
 
 
-def test_sliced_ell_layout_info(psc):
-    h, ctx, H, A, P, R, _ = setup(psc, (13, 11, 7), coarse_target=20)
-    for l in range(h.nlevels):
-        info = A[l].info()
-        ptr = h.levels[l].A.ptr
-        lens = np.diff(ptr)
-        nsl = (len(lens) + 31) // 32
+def _check_layout(M, info):
+    lens = np.diff(M.ptr)
+    n = len(lens)
+    G = info["lanes"]
+    assert info["nnz"] == M.nnz and info["n_rows"] == n
+    if G == 1:  # sliced ELL, 32-row slices padded to the slice's longest row
+        nsl = (n + 31) // 32
         pad = np.zeros(nsl * 32, np.int64)
-        pad[: len(lens)] = lens
-        widths = pad.reshape(nsl, 32).max(axis=1)
-        assert info["n_slices"] == nsl
-        assert info["padded"] == int(widths.sum()) * 32
-        assert info["nnz"] == h.levels[l].A.nnz
+        pad[:n] = lens
+        assert info["n_units"] == nsl
+        assert info["padded"] == int(pad.reshape(nsl, 32).max(axis=1).sum()) * 32
+    else:  # row groups: rows padded to multiples of G, 32/G rows per warp
+        assert G in (4, 8, 16, 32)
+        assert info["n_units"] == (n + 32 // G - 1) // (32 // G)
+        assert info["padded"] == int((((lens + G - 1) // G) * G).sum())
+    mean = M.nnz / max(n, 1)
+    assert (G == 1) == (mean < 10)
+
+
+def test_device_layout_info(psc):
+    h, ctx, H, A, P, R, _ = setup(psc, 32)
+    for l in range(h.nlevels):
+        _check_layout(h.levels[l].A, A[l].info())
+        if l < h.nlevels - 1:
+            _check_layout(h.levels[l].P, P[l].info())
+            _check_layout(h.levels[l].R, R[l].info())
 
 
 # ---------------------------------------------------------- l1 diag / sweeps
