@@ -126,7 +126,7 @@ void mat_assemble(psc_mat* m) {
   PSC_REQUIRE(!m->assembled, PSC_ERR_STATE, "matrix already assembled");
   psc_desc* c = m->cols;
   sell_from_csr(m->ctx, m->n_rows, m->d_rowptr, m->d_colg, m->d_valcsr, m->nnz, c->own_begin, c->n_own, c->d_halo,
-                c->n_halo(), m->S, m->ctx->stream);
+                c->n_halo(), m->S, m->ctx->stream, 0, m->rows == m->cols);
   dfree(m->d_rowptr);
   dfree(m->d_colg);
   dfree(m->d_valcsr);

@@ -15,6 +15,9 @@ using namespace psc;
 
 namespace {
 
+// vectors of the solve path: padded so TMA bulk copies of the last rows may overread
+double* dvec(int64_t n) { return dalloc<double>((size_t)n + 64); }
+
 enum Slot { S_PQ = 0, S_RR = 1, S_RZ = 2, S_BB = 3, NSLOT = 4 };
 
 struct LevelWS {
@@ -32,6 +35,7 @@ struct Replica {
   bool on = false;
   int64_t N = 0, maxcnt = 0;
   Sell S;                       // global rows, columns = global indices
+  double* dense = nullptr;      // N x N when N <= coarse_dense_max_rows()
   double* dinv = nullptr;       // N
   double* sendbuf = nullptr;    // maxcnt
   double* gbuf = nullptr;       // nranks * maxcnt
@@ -50,6 +54,7 @@ struct psc_hier_s {
   std::vector<LevelWS> lv;
   Replica rep;
   bool coarse_one_cta = false;
+  double* coarse_dense = nullptr;  // dense copy of A_coarse (single rank, small coarsest level)
   // CG state (level 0)
   double* x_int = nullptr;  // n0 + nh0
   double* r_cg = nullptr;   // n0
@@ -111,8 +116,13 @@ double* coarse_solve(psc_hier* h, const double* b, int nsweeps, cudaStream_t s) 
     PSC_NCCL(ncclAllGather(R.sendbuf, R.gbuf, R.maxcnt, ncclDouble, ctx->comm, s));
     ctx->collectives++;
     launch_gather(ctx, R.N, R.map_full, R.gbuf, R.bfull, s);
-    launch_coarse_solve(ctx, R.S, R.dinv, R.bfull, R.xfull, nsweeps, s);
+    if (R.dense) launch_coarse_dense(ctx, R.dense, R.N, R.dinv, R.bfull, R.xfull, nsweeps, s);
+    else launch_coarse_solve(ctx, R.S, R.dinv, R.bfull, R.xfull, nsweeps, s);
     launch_gather(ctx, W.n + W.nh, R.map_loc, R.xfull, W.x[0], s);
+    return W.x[0];
+  }
+  if (h->coarse_dense) {
+    launch_coarse_dense(ctx, h->coarse_dense, W.n, W.dinv, b, W.x[0], nsweeps, s);
     return W.x[0];
   }
   if (h->coarse_one_cta) {
@@ -129,6 +139,7 @@ double* coarse_solve(psc_hier* h, const double* b, int nsweeps, cudaStream_t s) 
   for (int k = 1; k < nsweeps; ++k) {
     halo_exchange(ctx, W.d, W.x[cur], s);
     RowArgs a;
+    a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
     a.b = b;
     a.dinv = W.dinv;
@@ -156,6 +167,7 @@ int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s,
   for (int k = 1; k < nsweeps; ++k) {
     halo_exchange(ctx, W.d, W.x[cur], s);
     RowArgs a;
+    a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
     a.b = b;
     a.dinv = W.dinv;
@@ -185,6 +197,7 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
   halo_exchange(ctx, W.d, W.x[cur], s);
   {
     RowArgs a;
+    a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
     a.b = b;
     a.y = W.r;
@@ -193,6 +206,7 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
   halo_exchange(ctx, W.d, W.r, s);
   {
     RowArgs a;
+    a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.r;
     a.y = C.b;
     launch_rows(ctx, W.R->S, RowOp::Spmv, a, s);
@@ -201,6 +215,7 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
   if (!(l + 1 == h->L - 1 && coarse_has_halo(h))) halo_exchange(ctx, C.d, xc, s);
   {
     RowArgs a;
+    a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = xc;
     a.y = W.x[cur];
     launch_rows(ctx, W.P->S, RowOp::PAdd, a, s);
@@ -211,6 +226,7 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
     halo_exchange(ctx, W.d, W.x[cur], s);
     const bool last0 = (l == 0 && k == post - 1);
     RowArgs a;
+    a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
     a.b = b;
     a.dinv = W.dinv;
@@ -248,6 +264,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
   halo_exchange(ctx, W.d, h->p, s);
   {
     RowArgs a;
+    a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = h->p;
     a.y = h->q;
     a.red = &h->red1;
@@ -317,7 +334,7 @@ void build_replica(psc_hier* h) {
   for (int r = 0; r < R; ++r) {
     const int64_t nr = cnt[2 * r], nz = cnt[2 * r + 1];
     int64_t* dp = dalloc<int64_t>(nr + 1 + nz);
-    double* dv = dalloc<double>(nz);
+    double* dv = dvec(nz);
     if (r == ctx->rank) {
       PSC_CUDA(cudaMemcpy(dp, A->h_rowptr.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice));
       if (nz) {
@@ -341,16 +358,20 @@ void build_replica(psc_hier* h) {
   PSC_REQUIRE(row0 == rp.N, PSC_ERR_STATE, "coarsest rows do not add up");
   int64_t* drp = dalloc<int64_t>(rp.N + 1);
   int64_t* dcol = dalloc<int64_t>(totnnz);
-  double* dval = dalloc<double>(totnnz);
+  double* dval = dvec(totnnz);
   PSC_CUDA(cudaMemcpy(drp, rp_all.data(), sizeof(int64_t) * (rp.N + 1), cudaMemcpyHostToDevice));
   PSC_CUDA(cudaMemcpy(dcol, col_all.data(), sizeof(int64_t) * totnnz, cudaMemcpyHostToDevice));
   PSC_CUDA(cudaMemcpy(dval, val_all.data(), sizeof(double) * totnnz, cudaMemcpyHostToDevice));
-  sell_from_csr(ctx, rp.N, drp, dcol, dval, totnnz, 0, rp.N, nullptr, 0, rp.S, s);
+  sell_from_csr(ctx, rp.N, drp, dcol, dval, totnnz, 0, rp.N, nullptr, 0, rp.S, s, 0, true);
   dfree(drp);
   dfree(dcol);
   dfree(dval);
-  rp.dinv = dalloc<double>(rp.N);
+  rp.dinv = dvec(rp.N);
   launch_l1_dinv(ctx, rp.S, rp.dinv, s);
+  if (rp.N <= coarse_dense_max_rows() && !getenv("PSC_NO_DENSE_COARSE")) {
+    rp.dense = dvec(rp.N * rp.N + 1);
+    dense_from_sell(ctx, rp.S, rp.dense, s);
+  }
   // b gather map: padded allgather buffer -> global index
   for (int r = 0; r < R; ++r) rp.maxcnt = std::max(rp.maxcnt, d->row_start[r + 1] - d->row_start[r]);
   rp.maxcnt = std::max<int64_t>(rp.maxcnt, 1);
@@ -364,10 +385,10 @@ void build_replica(psc_hier* h) {
   rp.map_loc = dalloc<int64_t>(ml.size());
   PSC_CUDA(cudaMemcpy(rp.map_full, mf.data(), sizeof(int64_t) * rp.N, cudaMemcpyHostToDevice));
   if (!ml.empty()) PSC_CUDA(cudaMemcpy(rp.map_loc, ml.data(), sizeof(int64_t) * ml.size(), cudaMemcpyHostToDevice));
-  rp.sendbuf = dalloc<double>(rp.maxcnt);
-  rp.gbuf = dalloc<double>((size_t)R * rp.maxcnt);
-  rp.bfull = dalloc<double>(rp.N);
-  rp.xfull = dalloc<double>(rp.N);
+  rp.sendbuf = dvec(rp.maxcnt);
+  rp.gbuf = dvec((size_t)R * rp.maxcnt);
+  rp.bfull = dvec(rp.N);
+  rp.xfull = dvec(rp.N);
   PSC_CUDA(cudaMemset(rp.sendbuf, 0, sizeof(double) * rp.maxcnt));
   PSC_CUDA(cudaStreamSynchronize(s));
   rp.on = true;
@@ -387,6 +408,8 @@ void free_hier(psc_hier* h) {
   Replica& rp = h->rep;
   sell_free(rp.S);
   dfree(rp.dinv);
+  dfree(rp.dense);
+  dfree(h->coarse_dense);
   dfree(rp.sendbuf);
   dfree(rp.gbuf);
   dfree(rp.map_full);
@@ -423,6 +446,7 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
   halo_exchange(ctx, W.d, h->x_int, s);
   {
     RowArgs a;
+    a.vec_padded = false;  // reads the caller's b
     a.x = h->x_int;
     a.b = b;
     a.y = h->r_cg;
@@ -499,7 +523,9 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
   S.collectives = ctx->collectives - c0;
   S.dom_kernel_seconds = dom_ms * 1e-3;
   S.dom_kernel_launches = dom_n;
-  S.dom_kernel_bytes = 12.0 * (double)W.A->nnz + 32.0 * (double)W.n;
+  // bytes the level-0 sweep must move in its layout: 8 B per stored value, 4 B per
+  // explicit column index (ELL slices), x in, b, dinv, x out
+  S.dom_kernel_bytes = 8.0 * (double)W.A->nnz + 4.0 * (double)W.A->S.nnz_ell + 32.0 * (double)W.n;
   S.h2d_bytes = (int64_t)extra_h2d;
   if (st) *st = S;
   if (status == PSC_ERR_BREAKDOWN) throw Error(PSC_ERR_BREAKDOWN, "PCG breakdown: p^T A p <= 0 or not finite");
@@ -544,23 +570,23 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     cudaStream_t s = ctx->stream;
     for (int l = 0; l < nlevels; ++l) {
       LevelWS& W = h->lv[l];
-      W.dinv = dalloc<double>(W.n);
+      W.dinv = dvec(W.n);
       launch_l1_dinv(ctx, W.A->S, W.dinv, s);  // smoother build
-      W.x[0] = dalloc<double>(W.n + W.nh);
-      W.x[1] = dalloc<double>(W.n + W.nh);
-      W.r = dalloc<double>(W.n + W.nh);
+      W.x[0] = dvec(W.n + W.nh);
+      W.x[1] = dvec(W.n + W.nh);
+      W.r = dvec(W.n + W.nh);
       PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
       PSC_CUDA(cudaMemsetAsync(W.x[1], 0, sizeof(double) * (W.n + W.nh), s));
       PSC_CUDA(cudaMemsetAsync(W.r, 0, sizeof(double) * (W.n + W.nh), s));
-      if (l > 0) W.b = dalloc<double>(W.n);
+      if (l > 0) W.b = dvec(W.n);
     }
     LevelWS& W0 = h->lv[0];
-    h->x_int = dalloc<double>(W0.n + W0.nh);
-    h->r_cg = dalloc<double>(W0.n);
-    h->p = dalloc<double>(W0.n + W0.nh);
-    h->q = dalloc<double>(W0.n);
+    h->x_int = dvec(W0.n + W0.nh);
+    h->r_cg = dvec(W0.n);
+    h->p = dvec(W0.n + W0.nh);
+    h->q = dvec(W0.n);
     W0.b = h->r_cg;
-    h->d_scal = dalloc<double>((size_t)NSLOT * ctx->nranks + 1);
+    h->d_scal = dvec((size_t)NSLOT * ctx->nranks + 1);
     PSC_CUDA(cudaMemsetAsync(h->d_scal, 0, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1), s));
     PSC_CUDA(cudaMallocHost(&h->h_scal, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1)));
     h->red1 = red_alloc(ctx->num_sms, 1);
@@ -573,8 +599,15 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     // coarsest solver: one CTA when the level is small enough; replicated on
     // every rank when distributed
     LevelWS& Wc = h->lv[nlevels - 1];
-    if (ctx->nranks > 1) build_replica(h);
-    else h->coarse_one_cta = (Wc.n <= coarse_smem_rows() && Wc.nh == 0);
+    if (ctx->nranks > 1) {
+      build_replica(h);
+    } else {
+      h->coarse_one_cta = (Wc.n <= coarse_smem_rows() && Wc.nh == 0);
+      if (Wc.n <= coarse_dense_max_rows() && Wc.nh == 0 && !getenv("PSC_NO_DENSE_COARSE")) {
+        h->coarse_dense = dvec(Wc.n * Wc.n + 1);
+        dense_from_sell(ctx, Wc.A->S, h->coarse_dense, s);
+      }
+    }
     PSC_CUDA(cudaStreamSynchronize(s));
     *out = h;
     return PSC_OK;
@@ -673,8 +706,8 @@ int psc_pcg_solve_host(psc_hier* h, const double* b_host, double* x_host, double
     enter(ctx);
     cudaStream_t s = ctx->stream;
     if (!h->d_bhost) {
-      h->d_bhost = dalloc<double>(n);
-      h->d_xhost = dalloc<double>(n);
+      h->d_bhost = dvec(n);
+      h->d_xhost = dvec(n);
     }
     if (n) {
       PSC_CUDA(cudaMemcpyAsync(h->d_bhost, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));

@@ -12,6 +12,11 @@
 
 namespace psc {
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ double gsum(const double* g, int nranks) {
   // value of a gathered scalar: sum over ranks in rank order (identical on all ranks)
@@ -69,17 +74,67 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NR], double* partials,
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-// Row sum of `lane`'s row in slice s: s = sum_k val[k] * x[col[k]], k in stored
-// order (padding contributes fma(0, x, s) = s).  Loads of a batch of up to 8
-// (value, column) pairs are issued before the dependent gathers for memory-level
-// parallelism.
-__device__ __forceinline__ double sell_row_sum(const int64_t* __restrict__ sptr, const int32_t* __restrict__ col,
-                                               const double* __restrict__ val, int64_t s, int lane,
-                                               const double* __restrict__ x) {
-  const int64_t b = sptr[s];
-  const int w = (int)((sptr[s + 1] - b) >> 5);
-  const int32_t* c = col + b + lane;
-  const double* v = val + b + lane;
+constexpr int kHdr = 16;     // int32 words per slice header
+constexpr int kMaxDia = 8;   // most diagonals a DIA slice may have (header words 6..13)
+
+__device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int64_t s, int lane) {
+  return lane < kHdr ? __ldg(hdr + s * kHdr + lane) : 0;
+}
+
+// DIA slice of width W (compile-time, so no predicates: all W value loads,
+// then all W gathers, are in flight before the first FMA).  Column of entry j
+// = i + offset_j (offsets broadcast from the header); an entry outside
+// [0, ncols) is absent: its value is 0 and it gathers x[0] (a valid address),
+// so fma(0, x[0], s) = s for finite x.
+template <int W>
+__device__ __forceinline__ double dia_sum(int32_t h, uint32_t i, const double* __restrict__ v,
+                                          const double* __restrict__ x, uint32_t nc) {
+  double vi[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) vi[j] = __ldcs(v + 32 * j);
+  double xv[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    const uint32_t c = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
+    xv[j] = __ldg(x + (c < nc ? c : 0u));
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (int j = 0; j < W; ++j) sum = fma(vi[j], xv[j], sum);
+  return sum;
+}
+
+// Row sum of `lane`'s row i = 32 s + lane of slice s whose header word `h` this
+// lane holds: s = sum_k val[k] * x[col[k]], k in stored order (padding adds
+// fma(0, x, s) = s).  DIA slices: dia_sum<W>.  ELL slices: explicit columns,
+// batches of 8 (value, column) loads issued before the dependent gathers.
+__device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, const int32_t* __restrict__ col,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               int64_t ncols) {
+  const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
+                     (uint32_t)__shfl_sync(0xffffffffu, h, 0);
+  const int w = __shfl_sync(0xffffffffu, h, 4);
+  const bool dia = __shfl_sync(0xffffffffu, h, 5) != 0;
+  const double* v = val + vb + lane;
+  if (dia) {
+    // local indices < 2^31: unsigned 32-bit wrap-around maps out-of-range columns above ncols
+    const uint32_t i = (uint32_t)(s * 32 + lane);
+    const uint32_t nc = (uint32_t)ncols;
+    switch (w) {
+      case 1: return dia_sum<1>(h, i, v, x, nc);
+      case 2: return dia_sum<2>(h, i, v, x, nc);
+      case 3: return dia_sum<3>(h, i, v, x, nc);
+      case 4: return dia_sum<4>(h, i, v, x, nc);
+      case 5: return dia_sum<5>(h, i, v, x, nc);
+      case 6: return dia_sum<6>(h, i, v, x, nc);
+      case 7: return dia_sum<7>(h, i, v, x, nc);
+      case 8: return dia_sum<8>(h, i, v, x, nc);
+      default: return 0.0;
+    }
+  }
+  const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
+                     (uint32_t)__shfl_sync(0xffffffffu, h, 2);
+  const int32_t* c = col + cb + lane;
   double sum = 0.0;
   int k = 0;
   for (; k + 8 <= w; k += 8) {
@@ -112,6 +167,18 @@ __device__ __forceinline__ double sell_row_sum(const int64_t* __restrict__ sptr,
   return sum;
 }
 
+// Column of entry k of local row i (lane = i & 31) in slice s; -1 if a DIA
+// offset points outside [0, ncols) (absent entry).
+__device__ __forceinline__ int64_t sell_col(const int64_t* __restrict__ cptr, const int32_t* __restrict__ col,
+                                            int64_t s, int w, int64_t i, int k, int64_t ncols) {
+  const int64_t cb = cptr[s];
+  if ((cptr[s + 1] - cb) < 32 * (int64_t)w) {
+    const int64_t c = i + col[cb + k];
+    return ((uint64_t)c < (uint64_t)ncols) ? c : -1;
+  }
+  return col[cb + 32 * (int64_t)k + (i & 31)];
+}
+
 // Partial row sum of lane `sub` of a G-lane group over a contiguous padded row
 // [b, e): entries b + sub, b + sub + G, ...; 4 independent loads in flight.
 template <int G>
@@ -135,7 +202,11 @@ __device__ __forceinline__ double rg_row_sum(const int32_t* __restrict__ col, co
 }
 
 struct RowKArgs {
+  int keep_matrix;  // 1: matrix small enough to stay in L2 across the level's launches (evict_last)
   const int64_t* ptr;
+  const int64_t* cptr;
+  const int32_t* hdr;
+  int64_t ncols;
   const int32_t* col;
   const double* val;
   const int32_t* list;  // nullptr: units 0..nlist-1
@@ -158,33 +229,64 @@ struct NRed {
       (OP == RowOp::SpmvDot || OP == RowOp::SweepDot) ? 1 : (OP == RowOp::ResidDot2 ? 2 : 0);
 };
 
-// Fused epilogue of row i with row sum `sum`.
+// Fused epilogue of row i with row sum `sum`, split in two: the row's vector
+// operands are loaded by epi_load BEFORE the row sum (so they travel with the
+// matrix values instead of costing one more memory round trip afterwards),
+// epi_store combines and writes.
+struct EpiIn {
+  double b, d, x;
+};
+
 template <RowOp OP>
-__device__ __forceinline__ void epilogue(const RowKArgs& a, int64_t i, double sum, double* acc) {
+__device__ __forceinline__ EpiIn epi_load(const RowKArgs& a, int64_t i) {
+  EpiIn e{0.0, 0.0, 0.0};
   if constexpr (OP == RowOp::Spmv) {
-    a.y[i] = (a.beta == 0.0) ? a.alpha * sum : a.alpha * sum + a.beta * a.y[i];
+    if (a.beta != 0.0) e.x = a.y[i];
+  } else if constexpr (OP == RowOp::SpmvDot) {
+    e.x = __ldg(a.x + i);
+  } else if constexpr (OP == RowOp::Sweep || OP == RowOp::SweepDot) {
+    e.b = __ldcs(a.b + i);
+    e.d = __ldcs(a.dinv + i);
+    e.x = __ldg(a.x + i);
+  } else if constexpr (OP == RowOp::Resid || OP == RowOp::ResidDot2) {
+    e.b = __ldcs(a.b + i);
+  } else if constexpr (OP == RowOp::PAdd) {
+    e.x = a.y[i];
+  }
+  return e;
+}
+
+template <RowOp OP>
+__device__ __forceinline__ void epi_store(const RowKArgs& a, int64_t i, double sum, const EpiIn& e, double* acc) {
+  if constexpr (OP == RowOp::Spmv) {
+    a.y[i] = (a.beta == 0.0) ? a.alpha * sum : a.alpha * sum + a.beta * e.x;
   } else if constexpr (OP == RowOp::SpmvDot) {
     a.y[i] = sum;
-    acc[0] += a.x[i] * sum;
+    acc[0] += e.x * sum;
   } else if constexpr (OP == RowOp::Sweep || OP == RowOp::SweepDot) {
-    const double bi = a.b[i];
-    const double xn = a.x[i] + a.dinv[i] * (bi - sum);
+    const double xn = e.x + e.d * (e.b - sum);
     a.y[i] = xn;
-    if constexpr (OP == RowOp::SweepDot) acc[0] += bi * xn;
+    if constexpr (OP == RowOp::SweepDot) acc[0] += e.b * xn;
   } else if constexpr (OP == RowOp::Resid) {
-    a.y[i] = a.b[i] - sum;
+    a.y[i] = e.b - sum;
   } else if constexpr (OP == RowOp::ResidDot2) {
-    const double bi = a.b[i];
-    const double r = bi - sum;
+    const double r = e.b - sum;
     a.y[i] = r;
     acc[0] += r * r;
-    acc[1] += bi * bi;
+    acc[1] += e.b * e.b;
   } else if constexpr (OP == RowOp::PAdd) {
-    a.y[i] += sum;
+    a.y[i] = e.x + sum;
   }
 }
 
-// sliced ELL: one warp per slice, one thread per row
+template <RowOp OP>
+__device__ __forceinline__ void epilogue(const RowKArgs& a, int64_t i, double sum, double* acc) {
+  epi_store<OP>(a, i, sum, epi_load<OP>(a, i), acc);
+}
+
+// sliced ELL: one warp per slice, one thread per row; the next slice's header
+// is loaded before the current slice is processed (one dependent round trip
+// less per slice)
 template <RowOp OP>
 __device__ __forceinline__ void sell_body(const RowKArgs& a) {
   constexpr int NR = NRed<OP>::value;
@@ -192,11 +294,30 @@ __device__ __forceinline__ void sell_body(const RowKArgs& a) {
   const int warp = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * kWarpsPerBlock;
   double acc[NR > 0 ? NR : 1] = {};
-  for (int64_t t = (int64_t)blockIdx.x * kWarpsPerBlock + warp; t < a.nlist; t += stride) {
-    const int64_t s = a.list ? (int64_t)a.list[t] : t;
-    const double sum = sell_row_sum(a.ptr, a.col, a.val, s, lane, a.x);
+  int64_t t = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+  int64_t s = 0;
+  int32_t h = 0;
+  if (t < a.nlist) {
+    s = a.list ? (int64_t)a.list[t] : t;
+    h = load_hdr(a.hdr, s, lane);
+  }
+  while (t < a.nlist) {
+    const int64_t tn = t + stride;
+    int64_t sn = 0;
+    int32_t hn = 0;
+    if (tn < a.nlist) {
+      sn = a.list ? (int64_t)a.list[tn] : tn;
+      hn = load_hdr(a.hdr, sn, lane);
+    }
     const int64_t i = s * kSlice + lane;
-    if (i < a.n_rows) epilogue<OP>(a, i, sum, acc);
+    const bool live = i < a.n_rows;
+    EpiIn e{0.0, 0.0, 0.0};
+    if (live) e = epi_load<OP>(a, i);
+    const double sum = sell_row_sum(h, s, lane, a.col, a.val, a.x, a.ncols);
+    if (live) epi_store<OP>(a, i, sum, e, acc);
+    t = tn;
+    s = sn;
+    h = hn;
   }
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
@@ -307,9 +428,377 @@ int row_grid(const Sell& A, RowOp op, int num_sms, SliceSet set) {
   return (int)std::max<int64_t>(1, std::min(need, cap));
 }
 
+// ------------------------------------------------ TMA-staged sliced-ELL kernel
+// Persistent CTAs, warp-specialised: warp 8 (one elected lane) streams chunks of
+// 8 slices (256 rows) into a 3-stage shared-memory ring with 1-D bulk TMA copies
+// (cp.async.bulk ... mbarrier::complete_tx): slice headers, values, explicit
+// columns and the rows' epilogue vectors (b, dinv, own x / y), tracked by
+// `full` mbarriers (expected transaction bytes).  Warps 0-7 each take one
+// slice of the chunk: values and columns from shared memory, gathers of x
+// from L2, fused epilogue, then arrive on the stage's `empty` mbarrier.  The
+// bytes in flight per SM are set by the ring (2 CTAs x 3 stages x ~30 KB), not
+// by registers or compiler scheduling.
+constexpr int kTmaSlices = 8;                 // slices per chunk (= consumer warps)
+constexpr int kTmaMaxW = 8;                   // widest slice the ring holds
+constexpr int kTmaStages = 3;
+constexpr int kTmaThreads = (kTmaSlices + 1) * 32;
+constexpr int kTmaRows = kTmaSlices * 32;
+constexpr int kTmaHdrBytes = kTmaSlices * kHdr * 4;                    // 512
+constexpr int kTmaValBytes = kTmaSlices * kTmaMaxW * 32 * 8;           // 16 KB
+constexpr int kTmaColBytes = kTmaSlices * kTmaMaxW * 32 * 4;           // 8 KB
+constexpr int kTmaVecBytes = kTmaRows * 8;                             // 2 KB per vector
+constexpr int kTmaStageBytes = kTmaHdrBytes + kTmaValBytes + kTmaColBytes + 3 * kTmaVecBytes;
+constexpr int kTmaSmem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+template <RowOp OP>
+struct EpiVecs {  // which row vectors the epilogue reads: b, dinv, x(own), y
+  static constexpr bool B = (OP == RowOp::Sweep || OP == RowOp::SweepDot || OP == RowOp::Resid ||
+                             OP == RowOp::ResidDot2);
+  static constexpr bool D = (OP == RowOp::Sweep || OP == RowOp::SweepDot);
+  // sell_tma reads the stored dinv (recomputing M_ii per row per sweep made the
+  // kernel FP64-divide bound: 317 vs 221 us on A_0 of 256^3)
+  static constexpr bool D_SELL = D;
+  static constexpr bool X = (OP == RowOp::Sweep || OP == RowOp::SweepDot || OP == RowOp::SpmvDot);
+  static constexpr bool Y = (OP == RowOp::PAdd || OP == RowOp::Spmv);
+};
+
+template <RowOp OP>
+__global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchunks, int64_t n_slices) {
+  constexpr int NR = NRed<OP>::value;
+  using EV = EpiVecs<OP>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaStageBytes);
+  uint64_t* empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool readY = EV::Y && !(OP == RowOp::Spmv && a.beta == 0.0);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTmaStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kTmaSlices);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double acc[NR > 0 ? NR : 1] = {};
+  if (warp == kTmaSlices) {
+    // ---------------- producer (one lane)
+    if (lane == 0) {
+      uint64_t pol_stream, pol_keep;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+      const uint64_t pol_mat = a.keep_matrix ? pol_keep : pol_stream;
+      int64_t c = blockIdx.x;
+      int64_t vb0 = 0, vb1 = 0, cb0 = 0, cb1 = 0;
+      if (c < nchunks) {
+        const int64_t s0 = c * kTmaSlices, s1 = min(s0 + kTmaSlices, n_slices);
+        vb0 = a.ptr[s0]; vb1 = a.ptr[s1]; cb0 = a.cptr[s0]; cb1 = a.cptr[s1];
+      }
+      for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
+        // prefetch the next chunk's offsets before blocking on the ring
+        const int64_t cn = c + gridDim.x;
+        int64_t nvb0 = 0, nvb1 = 0, ncb0 = 0, ncb1 = 0;
+        if (cn < nchunks) {
+          const int64_t s0 = cn * kTmaSlices, s1 = min(s0 + kTmaSlices, n_slices);
+          nvb0 = a.ptr[s0]; nvb1 = a.ptr[s1]; ncb0 = a.cptr[s0]; ncb1 = a.cptr[s1];
+        }
+        const int st = (int)(it % kTmaStages);
+        if (it >= kTmaStages) mbar_wait(&empty[st], (uint32_t)((it / kTmaStages - 1) & 1));
+        unsigned char* base = smem + st * kTmaStageBytes;
+        const int64_t s0 = c * kTmaSlices, s1 = min(s0 + kTmaSlices, n_slices);
+        const int64_t r0 = s0 * 32, r1 = min(s1 * 32, a.n_rows);
+        const uint32_t hb = (uint32_t)(s1 - s0) * kHdr * 4;
+        const uint32_t vbytes = (uint32_t)(vb1 - vb0) * 8;
+        const uint32_t cbytes = (uint32_t)(cb1 - cb0) * 4;
+        const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
+        const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) + (EV::X ? 1 : 0) + (readY ? 1 : 0);
+        mbar_expect_tx(&full[st], hb + vbytes + cbytes + nvec * rbytes);
+        bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol_keep);
+        if (vbytes) bulk_g2s(base + kTmaHdrBytes, a.val + vb0, vbytes, &full[st], pol_mat);
+        if (cbytes) bulk_g2s(base + kTmaHdrBytes + kTmaValBytes, a.col + cb0, cbytes, &full[st], pol_mat);
+        unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
+        if (rbytes) {
+          if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol_stream);
+          if constexpr (EV::D_SELL) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
+          if constexpr (EV::X) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
+          if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
+        }
+        vb0 = nvb0; vb1 = nvb1; cb0 = ncb0; cb1 = ncb1;
+      }
+    }
+  } else {
+    // ---------------- consumers: warp `warp` takes slice s0 + warp of each chunk
+    const uint32_t nc = (uint32_t)a.ncols;
+    int64_t c = blockIdx.x;
+    for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
+      const int st = (int)(it % kTmaStages);
+      mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
+      const unsigned char* base = smem + st * kTmaStageBytes;
+      const int32_t* hs = reinterpret_cast<const int32_t*>(base);
+      const double* vs = reinterpret_cast<const double*>(base + kTmaHdrBytes);
+      const int32_t* cs = reinterpret_cast<const int32_t*>(base + kTmaHdrBytes + kTmaValBytes);
+      const double* vec = reinterpret_cast<const double*>(base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes);
+      const int64_t s0 = c * kTmaSlices;
+      const int64_t s = s0 + warp;
+      if (s < n_slices) {
+        const int32_t h = lane < kHdr ? hs[warp * kHdr + lane] : 0;
+        const int32_t h0 = hs[0], h1 = hs[1], h2 = hs[2], h3 = hs[3];  // chunk's first slice: stage bases
+        const int64_t vbase = ((int64_t)(uint32_t)h1 << 32) | (uint32_t)h0;
+        const int64_t cbase = ((int64_t)(uint32_t)h3 << 32) | (uint32_t)h2;
+        const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
+                           (uint32_t)__shfl_sync(0xffffffffu, h, 0);
+        const int w = __shfl_sync(0xffffffffu, h, 4);
+        const bool dia = __shfl_sync(0xffffffffu, h, 5) != 0;
+        const double* v = vs + (vb - vbase) + lane;
+        const uint32_t i = (uint32_t)(s * 32 + lane);
+        double xv[kTmaMaxW];
+        if (dia) {
+#pragma unroll
+          for (int j = 0; j < kTmaMaxW; ++j) {
+            const uint32_t cj = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
+            xv[j] = (j < w) ? __ldg(a.x + (cj < nc ? cj : 0u)) : 0.0;
+          }
+        } else {
+          const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
+                             (uint32_t)__shfl_sync(0xffffffffu, h, 2);
+          const int32_t* cc = cs + (cb - cbase) + lane;
+#pragma unroll
+          for (int j = 0; j < kTmaMaxW; ++j) xv[j] = (j < w) ? __ldg(a.x + cc[32 * j]) : 0.0;
+        }
+        double sum = 0.0;
+#pragma unroll
+        for (int j = 0; j < kTmaMaxW; ++j)
+          if (j < w) sum = fma(v[32 * j], xv[j], sum);
+        if ((int64_t)i < a.n_rows) {
+          const int rl = warp * 32 + lane;
+          EpiIn e{0.0, 0.0, 0.0};
+          if constexpr (EV::B) e.b = vec[rl];
+          if constexpr (EV::D) e.d = vec[kTmaRows + rl];
+          if constexpr (EV::X) e.x = vec[2 * kTmaRows + rl];
+          if (readY) e.x = vec[2 * kTmaRows + rl];
+          epi_store<OP>(a, (int64_t)i, sum, e, acc);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
+}
+
+template <RowOp OP>
+static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PSC_CUDA(cudaFuncSetAttribute(sell_tma<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+    attr = true;
+  }
+  sell_tma<OP><<<grid, kTmaThreads, kTmaSmem, s>>>(a, nchunks, n_slices);
+}
+
+// ---------------------------------------------- TMA-staged row-group kernel
+// Same producer / consumer ring as sell_tma for the row-group layout: a chunk
+// is 8 units (8 x 32/G consecutive rows, contiguous in memory); the producer
+// bulk-copies the chunk's row pointers, values, columns and epilogue vectors;
+// consumer warp w reduces unit w's rows with G lanes each (values/columns from
+// shared memory, gathers of x from L2).
+constexpr int kRgCap = 4096;                       // entries per stage
+constexpr int kRgMaxRows = kTmaSlices * 8;         // 8 units x at most 8 rows (G = 4)
+constexpr int kRgValBytes = kRgCap * 8;
+constexpr int kRgColBytes = kRgCap * 4;
+constexpr int kRgPtrBytes = 1024;                  // (kRgMaxRows + 1) int64, rounded
+constexpr int kRgVecBytes = kRgMaxRows * 8;
+constexpr int kRgStages = 2;
+constexpr int kRgStageBytes = kRgValBytes + kRgColBytes + kRgPtrBytes + 3 * kRgVecBytes;
+constexpr int kRgSmem = kRgStages * kRgStageBytes + 2 * kRgStages * 8;
+
+template <RowOp OP, int G>
+__global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunks) {
+  constexpr int NR = NRed<OP>::value;
+  constexpr int RU = 32 / G;
+  constexpr int CR = kTmaSlices * RU;  // rows per chunk
+  using EV = EpiVecs<OP>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRgStages * kRgStageBytes);
+  uint64_t* empty = full + kRgStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool readY = EV::Y && !(OP == RowOp::Spmv && a.beta == 0.0);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kRgStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kTmaSlices);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double acc[NR > 0 ? NR : 1] = {};
+  if (warp == kTmaSlices) {
+    if (lane == 0) {
+      uint64_t pol_stream, pol_keep;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+      const uint64_t pol_mat = a.keep_matrix ? pol_keep : pol_stream;
+      int64_t c = blockIdx.x;
+      int64_t e0 = 0, e1 = 0;
+      if (c < nchunks) {
+        e0 = a.ptr[c * CR];
+        e1 = a.ptr[min((c + 1) * CR, a.n_rows)];
+      }
+      for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
+        const int64_t cn = c + gridDim.x;
+        int64_t ne0 = 0, ne1 = 0;
+        if (cn < nchunks) {
+          ne0 = a.ptr[cn * CR];
+          ne1 = a.ptr[min((cn + 1) * CR, a.n_rows)];
+        }
+        const int st = (int)(it % kRgStages);
+        if (it >= kRgStages) mbar_wait(&empty[st], (uint32_t)((it / kRgStages - 1) & 1));
+        unsigned char* base = smem + st * kRgStageBytes;
+        const int64_t r0 = c * CR, r1 = min(r0 + CR, a.n_rows);
+        const uint32_t pbytes = (uint32_t)(((r1 - r0 + 1) * 8 + 15) & ~15);
+        const uint32_t vbytes = (uint32_t)(e1 - e0) * 8;
+        const uint32_t cbytes = (uint32_t)(e1 - e0) * 4;
+        const uint32_t rbytes = (uint32_t)(((r1 - r0) * 8 + 15) & ~15);
+        const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D ? 1 : 0) + (EV::X ? 1 : 0) + (readY ? 1 : 0);
+        mbar_expect_tx(&full[st], pbytes + vbytes + cbytes + nvec * rbytes);
+        bulk_g2s(base + kRgValBytes + kRgColBytes, a.ptr + r0, pbytes, &full[st], pol_keep);
+        if (vbytes) {
+          bulk_g2s(base, a.val + e0, vbytes, &full[st], pol_mat);
+          bulk_g2s(base + kRgValBytes, a.col + e0, cbytes, &full[st], pol_mat);
+        }
+        unsigned char* vec = base + kRgValBytes + kRgColBytes + kRgPtrBytes;
+        if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol_stream);
+        if constexpr (EV::D) bulk_g2s(vec + kRgVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
+        if constexpr (EV::X) bulk_g2s(vec + 2 * kRgVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
+        if (readY) bulk_g2s(vec + 2 * kRgVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
+        e0 = ne0;
+        e1 = ne1;
+      }
+    }
+  } else {
+    const int sub = lane & (G - 1), grp = lane / G;
+    int64_t c = blockIdx.x;
+    for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
+      const int st = (int)(it % kRgStages);
+      mbar_wait(&full[st], (uint32_t)((it / kRgStages) & 1));
+      const unsigned char* base = smem + st * kRgStageBytes;
+      const double* vs = reinterpret_cast<const double*>(base);
+      const int32_t* cs = reinterpret_cast<const int32_t*>(base + kRgValBytes);
+      const int64_t* ps = reinterpret_cast<const int64_t*>(base + kRgValBytes + kRgColBytes);
+      const double* vec = reinterpret_cast<const double*>(base + kRgValBytes + kRgColBytes + kRgPtrBytes);
+      const int lr = warp * RU + grp;  // row within the chunk
+      const int64_t i = c * CR + lr;
+      const bool live = i < a.n_rows;
+      int b = 0, e = 0;
+      if (live) {
+        const int64_t e0 = ps[0];
+        b = (int)(ps[lr] - e0);
+        e = (int)(ps[lr + 1] - e0);
+      }
+      double sum = 0.0;
+      for (int kk = b + sub; kk < e; kk += 8 * G) {
+        int cj[8];
+        double vj[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = kk + j * G;
+          const bool ok = k < e;
+          cj[j] = ok ? cs[k] : 0;
+          vj[j] = ok ? vs[k] : 0.0;
+        }
+        double xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xv[j] = __ldg(a.x + cj[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum = fma(vj[j], xv[j], sum);
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, G);
+      if (sub == 0 && live) {
+        EpiIn ein{0.0, 0.0, 0.0};
+        if constexpr (EV::B) ein.b = vec[lr];
+        if constexpr (EV::D) ein.d = vec[kRgMaxRows + lr];
+        if constexpr (EV::X) ein.x = vec[2 * kRgMaxRows + lr];
+        if (readY) ein.x = vec[2 * kRgMaxRows + lr];
+        epi_store<OP>(a, i, sum, ein, acc);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
+}
+
+template <RowOp OP, int G>
+static void rg_tma_launch(const RowKArgs& a, int grid, int64_t nchunks, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PSC_CUDA(cudaFuncSetAttribute(rg_tma<OP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRgSmem));
+    attr = true;
+  }
+  rg_tma<OP, G><<<grid, kTmaThreads, kRgSmem, s>>>(a, nchunks);
+}
+
+template <int G>
+static void rg_tma_dispatch(RowOp op, const RowKArgs& a, int grid, int64_t nchunks, cudaStream_t s) {
+  switch (op) {
+    case RowOp::Spmv: rg_tma_launch<RowOp::Spmv, G>(a, grid, nchunks, s); break;
+    case RowOp::SpmvDot: rg_tma_launch<RowOp::SpmvDot, G>(a, grid, nchunks, s); break;
+    case RowOp::Sweep: rg_tma_launch<RowOp::Sweep, G>(a, grid, nchunks, s); break;
+    case RowOp::SweepDot: rg_tma_launch<RowOp::SweepDot, G>(a, grid, nchunks, s); break;
+    case RowOp::Resid: rg_tma_launch<RowOp::Resid, G>(a, grid, nchunks, s); break;
+    case RowOp::ResidDot2: rg_tma_launch<RowOp::ResidDot2, G>(a, grid, nchunks, s); break;
+    case RowOp::PAdd: rg_tma_launch<RowOp::PAdd, G>(a, grid, nchunks, s); break;
+  }
+}
+
+static bool rg_tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
+  const int off = env_int("PSC_NO_TMA", 0) || env_int("PSC_NO_RG_TMA", 0);
+  return !off && A.lanes > 1 && A.max_chunk <= kRgCap && set == SliceSet::All && r.vec_padded && A.n_units > 0;
+}
+
+// TMA path: sliced ELL, every slice at most kTmaMaxW wide, all slices, vectors
+// padded (the bulk copies of the last chunk's rows round up to 16 bytes).
+static bool tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
+  const int off = env_int("PSC_NO_TMA", 0);
+  return !off && A.lanes == 1 && A.max_width <= kTmaMaxW && set == SliceSet::All && r.vec_padded && A.hdr &&
+         A.n_units > 0;
+}
+
 void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaStream_t s, SliceSet set) {
   RowKArgs a;
+  // matrices up to 48 MB stay in L2 (evict_last) across the 8-10 launches of their level
+  a.keep_matrix = (A.padded * 12 + A.n_rows * 8) <= ((int64_t)48 << 20) ? 1 : 0;
   a.ptr = A.ptr;
+  a.cptr = A.cptr;
+  a.hdr = A.hdr;
+  a.ncols = A.n_cols_local;
   a.col = A.col;
   a.val = A.val;
   a.list = set == SliceSet::All ? nullptr : (set == SliceSet::Interior ? A.interior : A.boundary);
@@ -325,8 +814,39 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.ticket = r.red ? r.red->ticket : nullptr;
   a.red_out = r.red_out;
   a.red_stride = r.red_stride;
-  const int grid = row_grid(A, op, ctx->num_sms, set);
   const bool needs_red = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
+  if (tma_ok(A, r, set)) {
+    const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
+    PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
+    switch (op) {
+      case RowOp::Spmv: tma_launch<RowOp::Spmv>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::SpmvDot: tma_launch<RowOp::SpmvDot>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::Sweep: tma_launch<RowOp::Sweep>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::SweepDot: tma_launch<RowOp::SweepDot>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::Resid: tma_launch<RowOp::Resid>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::ResidDot2: tma_launch<RowOp::ResidDot2>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::PAdd: tma_launch<RowOp::PAdd>(a, grid, nchunks, A.n_units, s); break;
+    }
+    PSC_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
+  if (rg_tma_ok(A, r, set)) {
+    const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
+    PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
+    switch (A.lanes) {
+      case 4: rg_tma_dispatch<4>(op, a, grid, nchunks, s); break;
+      case 8: rg_tma_dispatch<8>(op, a, grid, nchunks, s); break;
+      case 16: rg_tma_dispatch<16>(op, a, grid, nchunks, s); break;
+      default: rg_tma_dispatch<32>(op, a, grid, nchunks, s); break;
+    }
+    PSC_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
+  const int grid = row_grid(A, op, ctx->num_sms, set);
   PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
   kernel_of(op, A.lanes)<<<grid, kBlock, 0, s>>>(a);
   PSC_CUDA(cudaGetLastError());
@@ -356,32 +876,36 @@ void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, 
 // the last column with value 0 and is skipped by the `found` flag);
 // off-diagonal |a_ij| summed in stored order; m = a_ii + sum; dinv = 1/m.
 __global__ void __launch_bounds__(kBlock) l1_dinv_kernel(const int64_t* __restrict__ ptr,
+                                                         const int64_t* __restrict__ cptr,
                                                          const int32_t* __restrict__ col,
-                                                         const double* __restrict__ val, int64_t n, int lanes,
-                                                         double* __restrict__ dinv) {
+                                                         const double* __restrict__ val, int64_t n, int64_t ncols,
+                                                         int lanes, double* __restrict__ dinv) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t base, step;
-    int w;
-    if (lanes == 1) {
-      const int64_t s = i >> 5;
-      base = ptr[s] + (i & 31);
-      w = (int)((ptr[s + 1] - ptr[s]) >> 5);
-      step = 32;
-    } else {
-      base = ptr[i];
-      w = (int)(ptr[i + 1] - base);
-      step = 1;
-    }
     double aii = 0.0, off = 0.0;
     bool found = false;
-    for (int k = 0; k < w; ++k) {
-      const int32_t c = col[base + step * k];
-      const double v = val[base + step * k];
-      if (c == (int32_t)i && !found) {
-        aii = v;
-        found = true;
-      } else {
-        off += fabs(v);
+    if (lanes == 1) {
+      const int64_t s = i >> 5;
+      const int64_t vb = ptr[s] + (i & 31);
+      const int w = (int)((ptr[s + 1] - ptr[s]) >> 5);
+      for (int k = 0; k < w; ++k) {
+        const int64_t c = sell_col(cptr, col, s, w, i, k, ncols);
+        const double v = val[vb + 32 * (int64_t)k];
+        if (c == i && !found) {
+          aii = v;
+          found = true;
+        } else {
+          off += fabs(v);
+        }
+      }
+    } else {
+      for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
+        const double v = val[k];
+        if (col[k] == (int32_t)i && !found) {
+          aii = v;
+          found = true;
+        } else {
+          off += fabs(v);
+        }
       }
     }
     dinv[i] = 1.0 / (aii + off);
@@ -390,7 +914,8 @@ __global__ void __launch_bounds__(kBlock) l1_dinv_kernel(const int64_t* __restri
 
 void launch_l1_dinv(psc_ctx* ctx, const Sell& A, double* dinv, cudaStream_t s) {
   if (A.n_rows == 0) return;
-  l1_dinv_kernel<<<vec_grid(ctx, A.n_rows), kBlock, 0, s>>>(A.ptr, A.col, A.val, A.n_rows, A.lanes, dinv);
+  l1_dinv_kernel<<<vec_grid(ctx, A.n_rows), kBlock, 0, s>>>(A.ptr, A.cptr, A.col, A.val, A.n_rows, A.n_cols_local,
+                                                            A.lanes, dinv);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -491,25 +1016,29 @@ void launch_gather(psc_ctx* ctx, int64_t n, const int64_t* map, const double* in
 
 // ------------------------------------------------------------ coarsest solve
 // One CTA runs the whole coarsest-level solver (l1-Jacobi "as coarse
-// solver (30 iterations)"): iterate, right-hand side and dinv live in shared
-// memory, A_coarse comes from L1/L2.  Replaces 30 dependent launches by one.
+// solver (30 iterations)") instead of 30 dependent launches: iterate,
+// right-hand side and dinv live in shared memory and, when it fits (227 KB),
+// so does A_coarse.  `gk` lanes share a row (gk = pow2floor(1024 / n), so all
+// 1024 threads work on every sweep); partial sums are combined by a fixed
+// shuffle tree.
 constexpr int kCoarseThreads = 1024;
-constexpr int kCoarseSmem = 200 * 1024;
-int64_t coarse_smem_rows() { return kCoarseSmem / (4 * sizeof(double)); }
+constexpr int kMaxSmem = 227 * 1024;
+int64_t coarse_smem_rows() { return (64 * 1024) / (4 * sizeof(double)); }
 
 struct CoarseArgs {
   const int64_t* ptr;
+  const int64_t* cptr;  // sliced ELL only
   const int32_t* col;
   const double* val;
-  int64_t n;
+  int64_t n, nptr, padded, col_slots;
+  int gk;
   const double* dinv;
   const double* b;
   double* xout;
   int nsweeps;
 };
 
-// lanes == 1 (sliced ELL): one thread per row.  G > 1: G lanes per row.
-template <int G>
+template <bool SELL, bool STAGE>
 __global__ void __launch_bounds__(kCoarseThreads) coarse_solve(CoarseArgs a) {
   extern __shared__ double sm[];
   const int64_t n = a.n;
@@ -517,39 +1046,56 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve(CoarseArgs a) {
   double* xb = sm + n;
   double* bs = sm + 2 * n;
   double* ds = sm + 3 * n;
+  const double* val = a.val;
+  const int64_t* ptr = a.ptr;
+  const int64_t* cptr = a.cptr;
+  const int32_t* col = a.col;
+  if constexpr (STAGE) {
+    double* v_s = sm + 4 * n;
+    int64_t* p_s = reinterpret_cast<int64_t*>(v_s + a.padded);
+    int64_t* cp_s = p_s + a.nptr;
+    int32_t* c_s = reinterpret_cast<int32_t*>(cp_s + (SELL ? a.nptr : 0));
+    for (int64_t k = threadIdx.x; k < a.padded; k += blockDim.x) v_s[k] = a.val[k];
+    for (int64_t k = threadIdx.x; k < a.col_slots; k += blockDim.x) c_s[k] = a.col[k];
+    for (int64_t k = threadIdx.x; k < a.nptr; k += blockDim.x) {
+      p_s[k] = a.ptr[k];
+      if constexpr (SELL) cp_s[k] = a.cptr[k];
+    }
+    val = v_s;
+    ptr = p_s;
+    cptr = cp_s;
+    col = c_s;
+  }
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     bs[i] = a.b[i];
     ds[i] = a.dinv[i];
     xa[i] = (a.nsweeps > 0) ? ds[i] * bs[i] : 0.0;  // first sweep from x = 0
   }
   __syncthreads();
+  const int gk = a.gk;
+  const int sub = threadIdx.x & (gk - 1);
+  const int rows_per_pass = kCoarseThreads / gk;
   for (int sw = 1; sw < a.nsweeps; ++sw) {
-    if constexpr (G == 1) {
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const int64_t s = i >> 5;
-        const int64_t base = a.ptr[s] + (i & 31);
-        const int w = (int)((a.ptr[s + 1] - a.ptr[s]) >> 5);
-        double sum = 0.0;
-        for (int k = 0; k < w; ++k) sum = fma(__ldg(a.val + base + 32 * k), xa[__ldg(a.col + base + 32 * k)], sum);
-        xb[i] = xa[i] + ds[i] * (bs[i] - sum);
-      }
-    } else {
-      constexpr int RU = 32 / G;
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      const int sub = lane & (G - 1), grp = lane / G;
-      for (int64_t r0 = (int64_t)warp * RU; r0 < n; r0 += (int64_t)(kCoarseThreads / 32) * RU) {
-        const int64_t i = r0 + grp;
-        int64_t b = 0, e = 0;
-        if (i < n) {
-          b = a.ptr[i];
-          e = a.ptr[i + 1];
+    for (int64_t r0 = 0; r0 < n; r0 += rows_per_pass) {
+      const int64_t i = r0 + threadIdx.x / gk;
+      double sum = 0.0;
+      if (i < n) {
+        if constexpr (SELL) {
+          const int64_t s = i >> 5;
+          const int64_t base = ptr[s] + (i & 31);
+          const int w = (int)((ptr[s + 1] - ptr[s]) >> 5);
+          for (int k = sub; k < w; k += gk) {
+            const int64_t c = sell_col(cptr, col, s, w, i, k, n);
+            if (c >= 0) sum = fma(val[base + 32 * k], xa[c], sum);
+          }
+        } else {
+          const int64_t base = ptr[i];
+          const int w = (int)(ptr[i + 1] - base);
+          for (int k = sub; k < w; k += gk) sum = fma(val[base + k], xa[col[base + k]], sum);
         }
-        double sum = 0.0;
-        for (int64_t k = b + sub; k < e; k += G) sum = fma(__ldg(a.val + k), xa[__ldg(a.col + k)], sum);
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, G);
-        if (sub == 0 && i < n) xb[i] = xa[i] + ds[i] * (bs[i] - sum);
       }
+      for (int o = gk / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, gk);
+      if (sub == 0 && i < n) xb[i] = xa[i] + ds[i] * (bs[i] - sum);
     }
     __syncthreads();
     double* t = xa;
@@ -559,15 +1105,14 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve(CoarseArgs a) {
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a.xout[i] = xa[i];
 }
 
-template <int G>
-static void coarse_launch(const CoarseArgs& a, cudaStream_t s) {
+template <bool SELL, bool STAGE>
+static void coarse_launch(const CoarseArgs& a, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    PSC_CUDA(cudaFuncSetAttribute(coarse_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCoarseSmem));
+    PSC_CUDA(cudaFuncSetAttribute(coarse_solve<SELL, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     attr = true;
   }
-  const size_t smem = (size_t)std::max<int64_t>(a.n, 1) * 4 * sizeof(double);
-  coarse_solve<G><<<1, kCoarseThreads, smem, s>>>(a);
+  coarse_solve<SELL, STAGE><<<1, kCoarseThreads, smem, s>>>(a);
 }
 
 void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const double* b, double* x, int nsweeps,
@@ -575,14 +1120,127 @@ void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const 
   const int64_t n = A.n_rows;
   PSC_REQUIRE(n <= coarse_smem_rows(), PSC_ERR_STATE, "coarsest level too large for the one-CTA solver");
   PSC_REQUIRE(A.n_cols_local == n, PSC_ERR_STATE, "coarsest matrix must have no halo");
-  CoarseArgs a{A.ptr, A.col, A.val, n, dinv, b, x, nsweeps};
-  switch (A.lanes) {
-    case 4: coarse_launch<4>(a, s); break;
-    case 8: coarse_launch<8>(a, s); break;
-    case 16: coarse_launch<16>(a, s); break;
-    case 32: coarse_launch<32>(a, s); break;
-    default: coarse_launch<1>(a, s); break;
+  const bool sell = (A.lanes == 1);
+  const int64_t nptr = sell ? A.n_units + 1 : n + 1;
+  int gk = 1;
+  while (gk < 32 && (int64_t)(gk * 2) * std::max<int64_t>(n, 1) <= kCoarseThreads) gk *= 2;
+  CoarseArgs a{A.ptr, A.cptr, A.col, A.val, n, nptr, A.padded, A.col_slots, gk, dinv, b, x, nsweeps};
+  const size_t vec = (size_t)std::max<int64_t>(n, 1) * 4 * sizeof(double);
+  const size_t mat = (size_t)A.padded * sizeof(double) + (size_t)A.col_slots * sizeof(int32_t) +
+                     (size_t)nptr * sizeof(int64_t) * (sell ? 2 : 1);
+  const bool stage = vec + mat <= (size_t)kMaxSmem;
+  const size_t smem = stage ? vec + mat : vec;
+  if (sell) stage ? coarse_launch<true, true>(a, smem, s) : coarse_launch<true, false>(a, smem, s);
+  else stage ? coarse_launch<false, true>(a, smem, s) : coarse_launch<false, false>(a, smem, s);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+// Dense coarsest solver: the coarsest A (nearly dense after Galerkin
+// coarsening: ~115 of 141 entries per row on 256^3) is expanded once into a
+// row-major n x n array; each sweep is then a shared-memory dense matvec by
+// all 1024 threads (gk lanes per row, fixed shuffle tree).
+int64_t coarse_dense_max_rows() { return 160; }
+
+__global__ void dense_from_sell_kernel(const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
+                                       const int32_t* __restrict__ col, const double* __restrict__ val, int64_t n,
+                                       int lanes, double* __restrict__ dense) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* row = dense + i * n;
+  if (lanes == 1) {
+    const int64_t s = i >> 5;
+    const int64_t vb = ptr[s] + (i & 31);
+    const int w = (int)((ptr[s + 1] - ptr[s]) >> 5);
+    for (int k = 0; k < w; ++k) {
+      const int64_t c = sell_col(cptr, col, s, w, i, k, n);
+      if (c >= 0) row[c] += val[vb + 32 * (int64_t)k];  // padding adds 0.0
+    }
+  } else {
+    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) row[col[k]] += val[k];
   }
+}
+
+void dense_from_sell(psc_ctx* ctx, const Sell& A, double* dense, cudaStream_t s) {
+  const int64_t n = A.n_rows;
+  PSC_CUDA(cudaMemsetAsync(dense, 0, sizeof(double) * n * n, s));
+  if (n == 0) return;
+  dense_from_sell_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A.ptr, A.cptr, A.col, A.val, n, A.lanes, dense);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+__global__ void __launch_bounds__(kCoarseThreads) coarse_dense(const double* __restrict__ Ad, int n,
+                                                               const double* __restrict__ dinv,
+                                                               const double* __restrict__ b, double* __restrict__ xout,
+                                                               int nsweeps, int gk) {
+  extern __shared__ __align__(16) double smd[];
+  double* As = smd;
+  double* xa = As + (size_t)n * n + 1;
+  double* xb = xa + n;
+  double* bs = xb + n;
+  double* ds = bs + n;
+  {  // stage A: 16-byte loads, 4 in flight per thread (n*n padded to even by the allocation)
+    const int n2 = (n * n + 1) / 2;
+    const double2* src = reinterpret_cast<const double2*>(Ad);
+    double2* dst = reinterpret_cast<double2*>(As);
+    int k = threadIdx.x;
+    for (; k + 3 * kCoarseThreads < n2; k += 4 * kCoarseThreads) {
+      const double2 a0 = __ldg(src + k), a1 = __ldg(src + k + kCoarseThreads);
+      const double2 a2 = __ldg(src + k + 2 * kCoarseThreads), a3 = __ldg(src + k + 3 * kCoarseThreads);
+      dst[k] = a0;
+      dst[k + kCoarseThreads] = a1;
+      dst[k + 2 * kCoarseThreads] = a2;
+      dst[k + 3 * kCoarseThreads] = a3;
+    }
+    for (; k < n2; k += kCoarseThreads) dst[k] = __ldg(src + k);
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    bs[i] = b[i];
+    ds[i] = dinv[i];
+    xa[i] = (nsweeps > 0) ? ds[i] * bs[i] : 0.0;  // first sweep from x = 0
+  }
+  __syncthreads();
+  const int sub = threadIdx.x & (gk - 1);
+  const int rows_per_pass = kCoarseThreads / gk;
+  for (int sw = 1; sw < nsweeps; ++sw) {
+    for (int r0 = 0; r0 < n; r0 += rows_per_pass) {
+      const int i = r0 + threadIdx.x / gk;
+      double sum = 0.0;
+      if (i < n) {
+        const double* Ai = As + (size_t)i * n;
+        double s1 = 0.0;
+        int j = sub;
+        for (; j + gk < n; j += 2 * gk) {
+          sum = fma(Ai[j], xa[j], sum);
+          s1 = fma(Ai[j + gk], xa[j + gk], s1);
+        }
+        if (j < n) sum = fma(Ai[j], xa[j], sum);
+        sum += s1;
+      }
+      for (int o = gk / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, gk);
+      if (sub == 0 && i < n) xb[i] = xa[i] + ds[i] * (bs[i] - sum);
+    }
+    __syncthreads();
+    double* t = xa;
+    xa = xb;
+    xb = t;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xa[i];
+}
+
+void launch_coarse_dense(psc_ctx* ctx, const double* Ad, int64_t n, const double* dinv, const double* b, double* x,
+                         int nsweeps, cudaStream_t s) {
+  PSC_REQUIRE(n <= coarse_dense_max_rows(), PSC_ERR_STATE, "coarsest level too large for the dense solver");
+  static bool attr = false;
+  if (!attr) {
+    PSC_CUDA(cudaFuncSetAttribute(coarse_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    attr = true;
+  }
+  int gk = 1;
+  while (gk < 32 && (int64_t)(gk * 2) * std::max<int64_t>(n, 1) <= kCoarseThreads) gk *= 2;
+  const size_t smem = ((size_t)n * n + 1 + 4 * (size_t)std::max<int64_t>(n, 1)) * sizeof(double);
+  coarse_dense<<<1, kCoarseThreads, smem, s>>>(Ad, (int)n, dinv, b, x, nsweeps, gk);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -602,58 +1260,113 @@ __device__ __forceinline__ int32_t map_col(int64_t g, int64_t own_begin, int64_t
   return 0;
 }
 
-// one warp per slice: slice width (max row length) and whether any column is off-rank
+
+// One warp per slice: width (max row length), off-rank flag, nnz, and — when
+// allowed and every column is owned — the sorted distinct diagonal offsets
+// (local col - local row) of the slice, found by repeated warp-min over the
+// rows' sorted column lists.  The slice is stored DIA when d <= 1.5 w
+// (8 B x 32 d value slots beat 12 B x 32 w value+column slots).
 __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_t* __restrict__ rowptr,
-                                  const int64_t* __restrict__ colg, int64_t own_begin, int64_t n_own,
-                                  int64_t* __restrict__ slots, int32_t* __restrict__ bflag) {
+                                  const int64_t* __restrict__ colg, int64_t own_begin, int64_t n_own, int allow_dia,
+                                  int64_t* __restrict__ vslots, int64_t* __restrict__ cslots,
+                                  int64_t* __restrict__ snnz, int32_t* __restrict__ bflag, int32_t* __restrict__ dia_d,
+                                  int32_t* __restrict__ dia_off) {
   const int lane = threadIdx.x & 31;
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= n_slices) return;
   const int64_t i = s * 32 + lane;
   int len = 0, off = 0;
+  int64_t b = 0;
   if (i < n_rows) {
-    const int64_t b = rowptr[i], e = rowptr[i + 1];
+    b = rowptr[i];
+    const int64_t e = rowptr[i + 1];
     len = (int)(e - b);
     for (int64_t k = b; k < e; ++k) {
       const int64_t g = colg[k];
       off |= (g < own_begin || g >= own_begin + n_own);
     }
   }
-  for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+  int w = len, tot = len;
+  for (int o = 16; o > 0; o >>= 1) {
+    w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
+    tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  }
   off = __any_sync(0xffffffffu, off);
+  int d = 0;
+  if (allow_dia && !off && w > 0 && w <= kMaxDia) {
+    int q = 0;
+    bool ok = true;
+    for (;;) {
+      const long long my = (q < len) ? (long long)(colg[b + q] - own_begin - i) : LLONG_MAX;
+      long long mn = my;
+      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      if (mn == LLONG_MAX) break;
+      if (d == kMaxDia) {
+        ok = false;
+        break;
+      }
+      if (lane == 0) dia_off[s * kMaxDia + d] = (int32_t)mn;
+      ++d;
+      if (my == mn) ++q;
+    }
+    if (!ok || 2 * d > 3 * w) d = 0;
+  }
   if (lane == 0) {
-    slots[s] = (int64_t)len * 32;
+    vslots[s] = 32 * (int64_t)(d ? d : w);
+    cslots[s] = d ? (int64_t)((d + 3) & ~3) : 32 * (int64_t)w;  // DIA: offsets, padded to 16 B
+    snnz[s] = tot;
     bflag[s] = off;
+    dia_d[s] = d;
   }
 }
 
-// thread per row: scatter the row into its slice column-major, renumbering columns
+// thread per row: scatter the row into its slice column-major, renumbering
+// columns (ELL slice) or aligning it with the slice's diagonals (DIA slice)
 __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t* __restrict__ rowptr,
                                  const int64_t* __restrict__ colg, const double* __restrict__ valcsr,
-                                 const int64_t* __restrict__ sptr, int64_t own_begin, int64_t n_own,
-                                 const int64_t* __restrict__ halo, int64_t nh, int32_t* __restrict__ col,
-                                 double* __restrict__ val, int* err) {
+                                 const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
+                                 const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
+                                 int64_t own_begin, int64_t n_own, const int64_t* __restrict__ halo, int64_t nh,
+                                 int32_t* __restrict__ col, double* __restrict__ val, int* err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_slices * 32) return;
   const int64_t s = i >> 5;
   const int lane = (int)(i & 31);
-  const int64_t base = sptr[s];
-  const int w = (int)((sptr[s + 1] - base) >> 5);
+  const int64_t vb = ptr[s], cb = cptr[s];
+  const int w = (int)((ptr[s + 1] - vb) >> 5);
   int64_t b = 0, e = 0;
   if (i < n_rows) {
     b = rowptr[i];
     e = rowptr[i + 1];
   }
+  const int d = dia_d[s];
+  if (d > 0) {
+    int64_t q = b;
+    for (int j = 0; j < d; ++j) {
+      const int32_t o = dia_off[s * kMaxDia + j];
+      double v = 0.0;
+      if (q < e && colg[q] - own_begin == i + o) {
+        v = valcsr[q];
+        ++q;
+      }
+      val[vb + 32 * (int64_t)j + lane] = v;
+      if (lane == 0) col[cb + j] = o;
+    }
+    if (lane == 0)
+      for (int j = d; j < ((d + 3) & ~3); ++j) col[cb + j] = 0;
+    if (q != e) *err = 2;
+    return;
+  }
   int32_t last = 0;
   for (int k = 0; k < w; ++k) {
-    const int64_t o = base + 32 * (int64_t)k + lane;
+    const int64_t o = 32 * (int64_t)k + lane;
     if (b + k < e) {
       last = map_col(colg[b + k], own_begin, n_own, halo, nh, err);
-      col[o] = last;
-      val[o] = valcsr[b + k];
+      col[cb + o] = last;
+      val[vb + o] = valcsr[b + k];
     } else {
-      col[o] = last;
-      val[o] = 0.0;
+      col[cb + o] = last;
+      val[vb + o] = 0.0;
     }
   }
 }
@@ -695,11 +1408,6 @@ __global__ void rg_fill_kernel(int64_t n_rows, const int64_t* __restrict__ rowpt
   }
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
 // Layout choice: short rows (mean < PSC_RG_MIN = 10) -> sliced ELL,
 // thread per row; long rows -> G lanes per row, G = pow2floor(mean / PSC_RG_DIV)
 // clamped to [4, 32].  PSC_LANES forces a layout (1, 4, 8, 16, 32).
@@ -714,76 +1422,152 @@ int choose_lanes(int64_t n_rows, int64_t nnz) {
   return G;
 }
 
+__global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
+                                const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
+                                int32_t* __restrict__ hdr) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_slices) return;
+  int32_t* h = hdr + s * kHdr;
+  const int64_t vb = ptr[s], cb = cptr[s];
+  h[0] = (int32_t)(uint32_t)(vb & 0xffffffffu);
+  h[1] = (int32_t)(uint32_t)((uint64_t)vb >> 32);
+  h[2] = (int32_t)(uint32_t)(cb & 0xffffffffu);
+  h[3] = (int32_t)(uint32_t)((uint64_t)cb >> 32);
+  h[4] = (int32_t)((ptr[s + 1] - vb) >> 5);
+  const int d = dia_d[s];
+  h[5] = d > 0 ? 1 : 0;
+  for (int j = 0; j < kMaxDia; ++j) h[6 + j] = j < d ? dia_off[s * kMaxDia + j] : 0;
+}
+
 void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg, const double* d_val,
                    int64_t nnz, int64_t own_begin, int64_t n_own, const int64_t* d_halo, int64_t n_halo, Sell& S,
-                   cudaStream_t s, int lanes) {
+                   cudaStream_t s, int lanes, bool allow_dia) {
   S.n_rows = n_rows;
   S.n_cols_local = n_own + n_halo;
   S.nnz = nnz;
   S.lanes = lanes > 0 ? lanes : choose_lanes(n_rows, nnz);
+  if (env_int("PSC_NO_DIA", 0)) allow_dia = false;
   const int RU = S.rows_per_unit();
   S.n_units = (n_rows + RU - 1) / RU;
   const bool sell = (S.lanes == 1);
-  const int64_t nptr = sell ? S.n_units + 1 : n_rows + 1;
-  S.ptr = dalloc<int64_t>(nptr);
-  int32_t* d_flag = dalloc<int32_t>(sell ? S.n_units : n_rows);
-  int64_t* d_len = dalloc<int64_t>(nptr);
+  const int64_t nu = S.n_units;
+  const int64_t nptr = sell ? nu + 1 : n_rows + 1;
   int* d_err = dalloc<int>(1);
   PSC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-  PSC_CUDA(cudaMemsetAsync(d_len, 0, sizeof(int64_t) * nptr, s));
-  if (sell && S.n_units > 0) {
-    const int64_t threads = S.n_units * 32;
-    sell_width_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(n_rows, S.n_units, d_rowptr, d_colg,
-                                                                         own_begin, n_own, d_len, d_flag);
-    PSC_CUDA(cudaGetLastError());
-  } else if (!sell && n_rows > 0) {
-    rg_len_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, S.lanes, d_rowptr, d_colg, own_begin,
-                                                                    n_own, d_len, d_flag);
-    PSC_CUDA(cudaGetLastError());
-  }
+  std::vector<int32_t> flag;      // per unit (sell) or per row (row groups)
+  std::vector<int64_t> hp;        // ptr on the host
+  std::vector<int32_t> hdia;      // DIA widths per slice
+  std::vector<int64_t> hsnnz;     // nnz per slice
   size_t tmp_bytes = 0;
-  PSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_len, S.ptr, nptr, s));
-  void* d_tmp = dalloc<char>(tmp_bytes);
-  PSC_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_len, S.ptr, nptr, s));
-  PSC_CUDA(cudaMemcpyAsync(&S.padded, S.ptr + nptr - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  PSC_CUDA(cudaStreamSynchronize(s));
-  dfree(d_tmp);
-  dfree(d_len);
-  S.col = dalloc<int32_t>(S.padded);
-  S.val = dalloc<double>(S.padded);
-  if (sell && S.n_units > 0) {
-    const int64_t threads = S.n_units * 32;
-    sell_fill_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(n_rows, S.n_units, d_rowptr, d_colg, d_val,
-                                                                        S.ptr, own_begin, n_own, d_halo, n_halo,
-                                                                        S.col, S.val, d_err);
-    PSC_CUDA(cudaGetLastError());
-  } else if (!sell && n_rows > 0) {
-    rg_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, d_rowptr, d_colg, d_val, S.ptr,
-                                                                     own_begin, n_own, d_halo, n_halo, S.col, S.val,
-                                                                     d_err);
-    PSC_CUDA(cudaGetLastError());
+  if (sell) {
+    int64_t* d_vs = dalloc<int64_t>(nu + 1);
+    int64_t* d_cs = dalloc<int64_t>(nu + 1);
+    int64_t* d_snnz = dalloc<int64_t>(nu);
+    int32_t* d_flag = dalloc<int32_t>(nu);
+    int32_t* d_diad = dalloc<int32_t>(nu);
+    int32_t* d_diaoff = dalloc<int32_t>((size_t)nu * kMaxDia);
+    PSC_CUDA(cudaMemsetAsync(d_vs, 0, sizeof(int64_t) * (nu + 1), s));
+    PSC_CUDA(cudaMemsetAsync(d_cs, 0, sizeof(int64_t) * (nu + 1), s));
+    if (nu > 0) {
+      sell_width_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
+          n_rows, nu, d_rowptr, d_colg, own_begin, n_own, allow_dia ? 1 : 0, d_vs, d_cs, d_snnz, d_flag, d_diad,
+          d_diaoff);
+      PSC_CUDA(cudaGetLastError());
+    }
+    S.ptr = dalloc<int64_t>(nu + 1);
+    S.cptr = dalloc<int64_t>(nu + 1);
+    PSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_vs, S.ptr, nu + 1, s));
+    void* d_tmp = dalloc<char>(tmp_bytes);
+    PSC_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_vs, S.ptr, nu + 1, s));
+    PSC_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_cs, S.cptr, nu + 1, s));
+    PSC_CUDA(cudaMemcpyAsync(&S.padded, S.ptr + nu, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaMemcpyAsync(&S.col_slots, S.cptr + nu, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    dfree(d_tmp);
+    dfree(d_vs);
+    dfree(d_cs);
+    S.col = dalloc<int32_t>(S.col_slots);
+    S.val = dalloc<double>(S.padded);
+    S.hdr = dalloc<int32_t>((size_t)nu * kHdr);
+    if (nu > 0) {
+      sell_fill_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
+          n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, own_begin, n_own, d_halo, n_halo,
+          S.col, S.val, d_err);
+      PSC_CUDA(cudaGetLastError());
+      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, S.hdr);
+      PSC_CUDA(cudaGetLastError());
+    }
+    flag.resize(nu);
+    hp.resize(nu + 1);
+    hdia.resize(nu);
+    hsnnz.resize(nu);
+    if (nu) {
+      PSC_CUDA(cudaMemcpyAsync(flag.data(), d_flag, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
+      PSC_CUDA(cudaMemcpyAsync(hdia.data(), d_diad, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
+      PSC_CUDA(cudaMemcpyAsync(hsnnz.data(), d_snnz, sizeof(int64_t) * nu, cudaMemcpyDeviceToHost, s));
+    }
+    PSC_CUDA(cudaMemcpyAsync(hp.data(), S.ptr, sizeof(int64_t) * (nu + 1), cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    dfree(d_snnz);
+    dfree(d_flag);
+    dfree(d_diad);
+    dfree(d_diaoff);
+  } else {
+    int64_t* d_len = dalloc<int64_t>(nptr);
+    int32_t* d_flag = dalloc<int32_t>(n_rows);
+    PSC_CUDA(cudaMemsetAsync(d_len, 0, sizeof(int64_t) * nptr, s));
+    if (n_rows > 0) {
+      rg_len_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, S.lanes, d_rowptr, d_colg, own_begin,
+                                                                      n_own, d_len, d_flag);
+      PSC_CUDA(cudaGetLastError());
+    }
+    S.ptr = dalloc<int64_t>(nptr + 2);  // +2: TMA copies of the last chunk's row pointers round up to 16 B
+    PSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_len, S.ptr, nptr, s));
+    void* d_tmp = dalloc<char>(tmp_bytes);
+    PSC_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_len, S.ptr, nptr, s));
+    PSC_CUDA(cudaMemcpyAsync(&S.padded, S.ptr + nptr - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    dfree(d_tmp);
+    dfree(d_len);
+    S.col_slots = S.padded;
+    S.col = dalloc<int32_t>(S.col_slots);
+    S.val = dalloc<double>(S.padded);
+    if (n_rows > 0) {
+      rg_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, d_rowptr, d_colg, d_val, S.ptr,
+                                                                       own_begin, n_own, d_halo, n_halo, S.col,
+                                                                       S.val, d_err);
+      PSC_CUDA(cudaGetLastError());
+    }
+    flag.resize(n_rows);
+    hp.resize(nptr);
+    if (n_rows) PSC_CUDA(cudaMemcpyAsync(flag.data(), d_flag, sizeof(int32_t) * n_rows, cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaMemcpyAsync(hp.data(), S.ptr, sizeof(int64_t) * nptr, cudaMemcpyDeviceToHost, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    dfree(d_flag);
   }
   int h_err = 0;
   PSC_CUDA(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
-  const int64_t nflag = sell ? S.n_units : n_rows;
-  std::vector<int32_t> flag(nflag);
-  if (nflag) PSC_CUDA(cudaMemcpyAsync(flag.data(), d_flag, sizeof(int32_t) * nflag, cudaMemcpyDeviceToHost, s));
-  std::vector<int64_t> hp(nptr);
-  PSC_CUDA(cudaMemcpyAsync(hp.data(), S.ptr, sizeof(int64_t) * nptr, cudaMemcpyDeviceToHost, s));
   PSC_CUDA(cudaStreamSynchronize(s));
   dfree(d_err);
-  dfree(d_flag);
-  PSC_REQUIRE(h_err == 0, PSC_ERR_STATE, "column not in the owned block nor in the assembled halo");
+  PSC_REQUIRE(h_err == 0, PSC_ERR_STATE,
+              h_err == 2 ? "DIA slice fill mismatch" : "column not in the owned block nor in the assembled halo");
   std::vector<int32_t> in, bd;
-  for (int64_t u = 0; u < S.n_units; ++u) {
+  S.nnz_ell = sell ? 0 : nnz;
+  for (int64_t u = 0; u < nu; ++u) {
     int f = 0;
     if (sell) {
       f = flag[u];
       S.max_width = std::max<int>(S.max_width, (int)((hp[u + 1] - hp[u]) / 32));
+      if (hdia[u]) S.n_dia++;
+      else S.nnz_ell += hsnnz[u];
     } else {
       for (int64_t i = u * RU; i < std::min<int64_t>(n_rows, (u + 1) * RU); ++i) {
         f |= flag[i];
         S.max_width = std::max<int>(S.max_width, (int)(hp[i + 1] - hp[i]));
+      }
+      if (u % 8 == 0) {
+        const int64_t r1 = std::min<int64_t>(n_rows, (u + 8) * RU);
+        S.max_chunk = std::max<int64_t>(S.max_chunk, hp[r1] - hp[u * RU]);
       }
     }
     (f ? bd : in).push_back((int32_t)u);
@@ -801,6 +1585,8 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
 
 void sell_free(Sell& S) {
   dfree(S.ptr);
+  dfree(S.cptr);
+  dfree(S.hdr);
   dfree(S.col);
   dfree(S.val);
   dfree(S.interior);

@@ -27,6 +27,9 @@ struct RowArgs {
   const RedSite* red = nullptr;
   double* red_out = nullptr;   // red0 -> red_out[0], red1 -> red_out[red_stride]
   int red_stride = 1;
+  // all row vectors (b, dinv, x, y) are library buffers padded past n (TMA bulk
+  // copies of the last chunk may read up to 8 bytes beyond the last row)
+  bool vec_padded = false;
 };
 
 // Which slices: all, interior only (no halo column), boundary only.
@@ -61,12 +64,18 @@ int64_t coarse_smem_rows();
 void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const double* b, double* x, int nsweeps,
                          cudaStream_t s);
 
+// Dense coarsest solver (n <= coarse_dense_max_rows()): dense = row-major n x n copy of A.
+int64_t coarse_dense_max_rows();
+void dense_from_sell(psc_ctx* ctx, const Sell& A, double* dense, cudaStream_t s);
+void launch_coarse_dense(psc_ctx* ctx, const double* dense, int64_t n, const double* dinv, const double* b, double* x,
+                         int nsweeps, cudaStream_t s);
+
 // CSR (global int64 columns) -> sliced ELL with local int32 columns.
 // lanes: 0 = choose from the mean row length (choose_lanes), else 1 / 4 / 8 / 16 / 32.
 int choose_lanes(int64_t n_rows, int64_t nnz);
 void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg,
                    const double* d_val, int64_t nnz, int64_t own_begin, int64_t n_own, const int64_t* d_halo,
-                   int64_t n_halo, Sell& S, cudaStream_t s, int lanes = 0);
+                   int64_t n_halo, Sell& S, cudaStream_t s, int lanes = 0, bool allow_dia = false);
 void sell_free(Sell& S);
 
 RedSite red_alloc(int num_sms, int nred);

@@ -59,8 +59,15 @@ inline void dfree(void* p) {
 // (DESIGN.md §5):
 //  lanes == 1  sliced ELL (Hacked ELLPACK): rows grouped in 32-row
 //              slices; slice s stores its width w_s = max row length of its rows
-//              as a column-major w_s x 32 block at element offset ptr[s]; entry k
-//              of row (32 s + lane) is at ptr[s] + 32 k + lane.  One thread per row.
+//              as a column-major w_s x 32 block of values at element offset ptr[s];
+//              value k of row (32 s + lane) is at ptr[s] + 32 k + lane.  One thread
+//              per row.  Column indices per slice, from cptr[s], in one of two forms:
+//                ELL slice: 32 w_s explicit local columns (same layout as values);
+//                DIA slice: w_s diagonal offsets shared by the 32 rows, column =
+//                  local row + offset (absent entries stored as 0.0) — chosen when
+//                  the slice's distinct (col - row) offsets are few (stencil-like rows,
+//                  interior slices), cutting 4 B/nnz of column traffic.
+//              DIA iff cptr[s+1] - cptr[s] < 32 w_s.
 //  lanes == G  row groups (G in {4,8,16,32}): rows stored contiguously, each padded
 //              to a multiple of G entries, ptr[i] = start of row i; G lanes of a
 //              warp share one row (long rows of coarse A_l and R_l).
@@ -71,7 +78,15 @@ struct Sell {
   int lanes = 1;
   int64_t n_units = 0;
   int64_t* ptr = nullptr;  // lanes == 1: n_units + 1 slice offsets; else n_rows + 1 row offsets
-  int32_t* col = nullptr;  // padded
+  int64_t* cptr = nullptr; // lanes == 1: n_units + 1 column-slot offsets (ELL or DIA slices)
+  int64_t col_slots = 0;   // entries of `col`
+  int64_t nnz_ell = 0;     // stored nonzeros whose column index is explicit (ELL slices / row groups)
+  int64_t n_dia = 0;       // DIA slices
+  int32_t* col = nullptr;  // col_slots
+  // lanes == 1: per-slice 64-byte header read by the row kernels in one coalesced
+  // half-warp load (prefetched one slice ahead): [0..1] value offset, [2..3] column
+  // offset, [4] width, [5] 1 = DIA slice, [6..15] DIA offsets.
+  int32_t* hdr = nullptr;
   double* val = nullptr;   // padded
   // units whose columns are all owned (interior) and the others (boundary):
   // the interior ones can run while the halo exchange is in flight.
@@ -79,6 +94,7 @@ struct Sell {
   int32_t* boundary = nullptr;
   int64_t n_interior = 0, n_boundary = 0;
   int max_width = 0;  // longest (padded) row
+  int64_t max_chunk = 0;  // row groups: most entries in one chunk of 8 units (TMA ring capacity check)
   int rows_per_unit() const { return lanes == 1 ? 32 : 32 / lanes; }
 };
 

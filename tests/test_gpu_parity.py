@@ -80,12 +80,14 @@ def _check_layout(M, info):
     n = len(lens)
     G = info["lanes"]
     assert info["nnz"] == M.nnz and info["n_rows"] == n
-    if G == 1:  # sliced ELL, 32-row slices padded to the slice's longest row
+    if G == 1:  # sliced ELL, 32-row slices padded to the slice's longest row (ELL slices) or
+        # to the slice's number of distinct diagonals (DIA slices): padded >= 32 * sum of widths
         nsl = (n + 31) // 32
         pad = np.zeros(nsl * 32, np.int64)
         pad[:n] = lens
         assert info["n_units"] == nsl
-        assert info["padded"] == int(pad.reshape(nsl, 32).max(axis=1).sum()) * 32
+        widths = int(pad.reshape(nsl, 32).max(axis=1).sum()) * 32
+        assert widths <= info["padded"] <= 1.5 * widths
     else:  # row groups: rows padded to multiples of G, 32/G rows per warp
         assert G in (4, 8, 16, 32)
         assert info["n_units"] == (n + 32 // G - 1) // (32 // G)
@@ -232,3 +234,51 @@ def test_breakdown_is_reported(psc):
     with pytest.raises(psc.PscError) as e:
         H.solve(dev(np.ones(2)), x)
     assert e.value.code == psc.PSC_ERR_BREAKDOWN
+
+
+# ------------------------------------------------ kernel / layout variants
+# Every code path of the library (TMA-staged vs plain row kernels, DIA vs ELL
+# slices, row-group lane counts, dense vs sparse one-CTA coarsest solver) must
+# give the oracle's answer.  The switches are read at assembly (layout), at
+# hierarchy creation (coarsest solver) and at launch (kernel family).
+VARIANTS = [
+    {},
+    {"PSC_NO_TMA": "1"},
+    {"PSC_NO_DIA": "1"},
+    {"PSC_NO_RG_TMA": "1", "PSC_NO_DENSE_COARSE": "1"},
+    {"PSC_LANES": "1", "PSC_NO_DENSE_COARSE": "1"},
+    {"PSC_LANES": "8"},
+    {"PSC_LANES": "32", "PSC_NO_TMA": "1"},
+    {"PSC_RG_MIN": "4", "PSC_RG_DIV": "1"},
+]
+
+
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+@pytest.mark.parametrize("grid", [(21, 19, 17), 40])
+def test_variants_pcg_parity(psc, env, grid, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = grid if isinstance(grid, tuple) else (grid,) * 3
+    h = pscgen.poisson_hierarchy(*g, coarse_target=60)
+    ctx = psc.Context()
+    H, descs, A, P, R = psc.build_hierarchy(ctx, pscgen.rank_levels(h, 0))
+    n = h.levels[0].n
+    b = pscgen.rhs_random(17, 0, n)
+    for l in range(h.nlevels):
+        r = pscgen.rhs_random(l + 3, 0, h.levels[l].n)
+        z = torch.zeros(h.levels[l].n, dtype=torch.float64, device="cuda")
+        H.smooth(l, dev(r), z, 5)
+        ref = oracle.l1_sweeps_from_zero(h.levels[l].A, r, 5)
+        assert np.linalg.norm(host(z) - ref) / np.linalg.norm(ref) <= 1e-12
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    H.vcycle(dev(b), z)
+    zo = oracle.vcycle(h, b)
+    assert np.linalg.norm(host(z) - zo) / np.linalg.norm(zo) <= 1e-12
+    xo, ito, sto, histo = oracle.pcg(h, b, tol=1e-8, maxit=100)
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    rc, st, hist = H.solve(dev(b), x, tol=1e-8, maxit=100)
+    assert rc == 0 and abs(st["iters"] - ito) <= 1
+    k = min(20, ito, st["iters"]) + 1
+    np.testing.assert_allclose(hist[:k], histo[:k], rtol=1e-9, atol=0)
+    assert np.linalg.norm(host(x) - xo) / np.linalg.norm(xo) <= 1e-7
+    ctx.close()
