@@ -111,6 +111,21 @@ int psc_desc_info(psc_desc* d, int64_t* n_owned, int64_t* n_halo, int64_t* own_b
 int psc_desc_halo(psc_desc* d, int64_t* halo_globals_host);
 void psc_desc_destroy(psc_desc* d);
 
+/* Host-only halo planning (no GPU, no NCCL), the arithmetic of psc_desc_assemble:
+ * refs[n_refs] = global columns referenced by this rank's rows (any order,
+ * duplicates allowed).  Writes the sorted unique off-rank ones to halo (capacity
+ * n_refs) and their count to *n_halo, and recv_count[nranks] = halo entries owned
+ * by each rank (the requests this rank sends to each owner, in halo order).
+ * Errors: PSC_ERR_ARG for a malformed partition or an out-of-range column. */
+int psc_halo_plan(int nranks, int rank, const int64_t* row_start, int64_t n_refs, const int64_t* refs, int64_t* halo,
+                  int64_t* n_halo, int64_t* recv_count);
+/* Host-only: local (owned) indices to send, for the requests received from the
+ * peers: requests = the peers' halo lists for this rank, concatenated in peer
+ * order, send_count[nranks] their lengths.  send_idx[sum send_count] (int32).
+ * PSC_ERR_STATE if a request is not owned by this rank. */
+int psc_send_plan(int nranks, int rank, const int64_t* row_start, const int64_t* send_count, const int64_t* requests,
+                  int32_t* send_idx);
+
 /* ------------------------------------------------------------------- matrix */
 
 /* Insert this rank's rows of a distributed matrix in GLOBAL numbering (psb_spall

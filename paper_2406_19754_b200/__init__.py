@@ -60,6 +60,8 @@ _sig("psc_status_string", ctypes.c_char_p, [_i32])
 _sig("psc_last_error", ctypes.c_char_p, [_vp])
 _sig("psc_version", ctypes.c_char_p, [])
 _sig("psc_ctx_stream", _vp, [_vp])
+_sig("psc_halo_plan", _i32, [_i32, _i32, _vp, _i64, _vp, _vp, _P(_i64), _vp])
+_sig("psc_send_plan", _i32, [_i32, _i32, _vp, _vp, _vp, _vp])
 _sig("psc_desc_create", _i32, [_vp, _i64, _vp, _P(_vp)])
 _sig("psc_desc_assemble", _i32, [_vp])
 _sig("psc_desc_info", _i32, [_vp, _P(_i64), _P(_i64), _P(_i64)])
@@ -113,6 +115,28 @@ def _dev_ptr(t, n, name):
 def _host(a, dtype, name):
     a = np.ascontiguousarray(a, dtype=dtype)
     return a
+
+
+def halo_plan(nranks: int, rank: int, row_start, refs):
+    """Host-only halo plan (psc_halo_plan): sorted unique off-rank columns and per-owner counts."""
+    rs = _host(row_start, np.int64, "row_start")
+    refs = _host(refs, np.int64, "refs")
+    halo = np.zeros(max(len(refs), 1), np.int64)
+    nh = _i64()
+    rc = np.zeros(nranks, np.int64)
+    _check(_lib.psc_halo_plan(nranks, rank, rs.ctypes.data, len(refs), refs.ctypes.data, halo.ctypes.data,
+                              ctypes.byref(nh), rc.ctypes.data))
+    return halo[: nh.value].copy(), rc
+
+
+def send_plan(nranks: int, rank: int, row_start, send_count, requests):
+    """Host-only send plan (psc_send_plan): local owned indices for the peers' requests."""
+    rs = _host(row_start, np.int64, "row_start")
+    sc = _host(send_count, np.int64, "send_count")
+    rq = _host(requests, np.int64, "requests")
+    out = np.zeros(max(int(sc.sum()), 1), np.int32)
+    _check(_lib.psc_send_plan(nranks, rank, rs.ctypes.data, sc.ctypes.data, rq.ctypes.data, out.ctypes.data))
+    return out[: int(sc.sum())].copy()
 
 
 def get_unique_id() -> bytes:

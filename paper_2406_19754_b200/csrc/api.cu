@@ -44,17 +44,39 @@ int64_t owner_of(const std::vector<int64_t>& rs, int64_t g) {
 
 namespace psc {
 
+// sorted unique off-rank halo + per-owner counts (host arithmetic of psb_cdasb)
+void halo_plan(const std::vector<int64_t>& row_start, int rank, std::vector<int64_t>& refs,
+               std::vector<int64_t>& rcount) {
+  const int R = (int)row_start.size() - 1;
+  const int64_t ob = row_start[rank], oe = row_start[rank + 1];
+  refs.erase(std::remove_if(refs.begin(), refs.end(), [&](int64_t g) { return g >= ob && g < oe; }), refs.end());
+  std::sort(refs.begin(), refs.end());
+  refs.erase(std::unique(refs.begin(), refs.end()), refs.end());
+  rcount.assign(R, 0);
+  for (int64_t g : refs) {
+    PSC_REQUIRE(g >= 0 && g < row_start[R], PSC_ERR_ARG, "halo column out of range");
+    rcount[owner_of(row_start, g)]++;
+  }
+}
+
+// requests of the peers (global, grouped by peer) -> local owned indices
+void send_plan(const std::vector<int64_t>& row_start, int rank, const int64_t* req, int64_t n, int32_t* idx) {
+  const int64_t ob = row_start[rank], no = row_start[rank + 1] - ob;
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t li = req[k] - ob;
+    PSC_REQUIRE(li >= 0 && li < no, PSC_ERR_STATE, "halo request for a non-owned index");
+    idx[k] = (int32_t)li;
+  }
+}
+
 void desc_assemble(psc_desc* d) {
   psc_ctx* ctx = d->ctx;
   const int R = ctx->nranks;
-  std::sort(d->halo_req.begin(), d->halo_req.end());
-  d->halo_req.erase(std::unique(d->halo_req.begin(), d->halo_req.end()), d->halo_req.end());
+  halo_plan(d->row_start, ctx->rank, d->halo_req, d->rcount);
   d->halo.swap(d->halo_req);
   std::vector<int64_t>().swap(d->halo_req);
   PSC_REQUIRE(d->n_own + d->n_halo() < (int64_t)INT32_MAX, PSC_ERR_ARG, "local index space exceeds int32");
-  d->rcount.assign(R, 0);
   d->roff.assign(R + 1, 0);
-  for (int64_t g : d->halo) d->rcount[owner_of(d->row_start, g)]++;
   for (int p = 0; p < R; ++p) d->roff[p + 1] = d->roff[p] + d->rcount[p];
   d->scount.assign(R, 0);
   d->soff.assign(R + 1, 0);
@@ -90,11 +112,7 @@ void desc_assemble(psc_desc* d) {
     PSC_CUDA(cudaStreamSynchronize(s));
     dfree(d_req);
     std::vector<int32_t> idx(d->n_send);
-    for (int64_t k = 0; k < d->n_send; ++k) {
-      const int64_t li = req[k] - d->own_begin;
-      PSC_REQUIRE(li >= 0 && li < d->n_own, PSC_ERR_STATE, "halo request for a non-owned index");
-      idx[k] = (int32_t)li;
-    }
+    send_plan(d->row_start, ctx->rank, req.data(), d->n_send, idx.data());
     d->d_send_idx = dalloc<int32_t>(idx.size());
     d->d_sendbuf = dalloc<double>(idx.size());
     if (!idx.empty())
@@ -226,6 +244,38 @@ void psc_finalize(psc_ctx* ctx) {
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   delete ctx;
+}
+
+int psc_halo_plan(int nranks, int rank, const int64_t* row_start, int64_t n_refs, const int64_t* refs, int64_t* halo,
+                  int64_t* n_halo, int64_t* recv_count) {
+  API_BEGIN
+  PSC_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks && row_start && (refs || n_refs == 0) && n_halo &&
+                  recv_count && (halo || n_refs == 0),
+              PSC_ERR_ARG, "bad argument");
+  std::vector<int64_t> rs(row_start, row_start + nranks + 1);
+  PSC_REQUIRE(rs[0] == 0, PSC_ERR_ARG, "row_start[0] != 0");
+  for (int r = 0; r < nranks; ++r) PSC_REQUIRE(rs[r] <= rs[r + 1], PSC_ERR_ARG, "row_start decreasing");
+  std::vector<int64_t> v(refs, refs + n_refs);
+  std::vector<int64_t> rc;
+  halo_plan(rs, rank, v, rc);
+  std::copy(v.begin(), v.end(), halo);
+  *n_halo = (int64_t)v.size();
+  std::copy(rc.begin(), rc.end(), recv_count);
+  return PSC_OK;
+  API_END(nullptr)
+}
+
+int psc_send_plan(int nranks, int rank, const int64_t* row_start, const int64_t* send_count, const int64_t* requests,
+                  int32_t* send_idx) {
+  API_BEGIN
+  PSC_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks && row_start && send_count, PSC_ERR_ARG, "bad argument");
+  std::vector<int64_t> rs(row_start, row_start + nranks + 1);
+  int64_t n = 0;
+  for (int p = 0; p < nranks; ++p) n += send_count[p];
+  PSC_REQUIRE(n == 0 || (requests && send_idx), PSC_ERR_ARG, "null requests/send_idx");
+  send_plan(rs, rank, requests, n, send_idx);
+  return PSC_OK;
+  API_END(nullptr)
 }
 
 int psc_desc_create(psc_ctx* ctx, int64_t n_global, const int64_t* row_start, psc_desc** out) {

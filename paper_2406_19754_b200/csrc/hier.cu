@@ -591,7 +591,12 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     PSC_CUDA(cudaMallocHost(&h->h_scal, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1)));
     h->red1 = red_alloc(ctx->num_sms, 1);
     h->red2 = red_alloc(ctx->num_sms, 2);
-    const int ndom = 2 * (std::max(h->opt.pre_sweeps - 1, 0) + h->opt.post_sweeps);
+    // live timing of the dominant kernel: one event pair around one level-0
+    // sweep per iteration (each event-record node costs ~0.1% of an iteration);
+    // PSC_DOM_TIMING=k times k of the 7 sweeps, 0 disables
+    const char* dt = getenv("PSC_DOM_TIMING");
+    const int nt = std::min(dt ? atoi(dt) : 1, std::max(h->opt.pre_sweeps - 1, 0) + h->opt.post_sweeps);
+    const int ndom = 2 * std::max(nt, 0);
     h->ev_dom.resize(ndom);
     for (auto& e : h->ev_dom) PSC_CUDA(cudaEventCreate(&e));
     PSC_CUDA(cudaEventCreate(&h->ev_t0));

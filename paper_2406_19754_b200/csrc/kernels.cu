@@ -17,6 +17,38 @@ static int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
+// ---------------------------------------------- programmatic dependent launch
+// Every solve-path kernel starts with griddepcontrol.wait (all prior grids
+// complete and visible; a no-op without PDL) followed by
+// griddepcontrol.launch_dependents, and is launched with programmatic stream
+// serialization: inside the captured iteration graph the next kernel's CTAs
+// are staged while the current one drains, hiding launch latency between the
+// ~50 dependent kernels of a PCG iteration.  The trigger is issued when a CTA
+// has finished its work (an entry-time trigger let waiting dependent CTAs take
+// SM resources from the running grid: 3080 vs 3634 Mdof*it/s).  Measured
+// slower even with the end-of-work trigger (3523 vs 3645), so it is off unless
+// PSC_PDL=1.
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// a CTA is done with its share: the dependent grid may be scheduled once every CTA got here
+__device__ __forceinline__ void pdl_exit() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  static const bool pdl = env_int("PSC_PDL", 0) != 0;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = pdl ? attr : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  PSC_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ double gsum(const double* g, int nranks) {
   // value of a gathered scalar: sum over ranks in rank order (identical on all ranks)
@@ -86,12 +118,16 @@ __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int
 // = i + offset_j (offsets broadcast from the header); an entry outside
 // [0, ncols) is absent: its value is 0 and it gathers x[0] (a valid address),
 // so fma(0, x[0], s) = s for finite x.
+// matrix-stream load: evict-first unless the matrix is small enough to stay in L2
+__device__ __forceinline__ double ldm(const double* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
+__device__ __forceinline__ int32_t ldm(const int32_t* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
+
 template <int W>
 __device__ __forceinline__ double dia_sum(int32_t h, uint32_t i, const double* __restrict__ v,
-                                          const double* __restrict__ x, uint32_t nc) {
+                                          const double* __restrict__ x, uint32_t nc, bool keep) {
   double vi[W];
 #pragma unroll
-  for (int j = 0; j < W; ++j) vi[j] = __ldcs(v + 32 * j);
+  for (int j = 0; j < W; ++j) vi[j] = ldm(v + 32 * j, keep);
   double xv[W];
 #pragma unroll
   for (int j = 0; j < W; ++j) {
@@ -110,7 +146,7 @@ __device__ __forceinline__ double dia_sum(int32_t h, uint32_t i, const double* _
 // batches of 8 (value, column) loads issued before the dependent gathers.
 __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, const int32_t* __restrict__ col,
                                                const double* __restrict__ val, const double* __restrict__ x,
-                                               int64_t ncols) {
+                                               int64_t ncols, bool keep) {
   const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
                      (uint32_t)__shfl_sync(0xffffffffu, h, 0);
   const int w = __shfl_sync(0xffffffffu, h, 4);
@@ -121,14 +157,14 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
     const uint32_t i = (uint32_t)(s * 32 + lane);
     const uint32_t nc = (uint32_t)ncols;
     switch (w) {
-      case 1: return dia_sum<1>(h, i, v, x, nc);
-      case 2: return dia_sum<2>(h, i, v, x, nc);
-      case 3: return dia_sum<3>(h, i, v, x, nc);
-      case 4: return dia_sum<4>(h, i, v, x, nc);
-      case 5: return dia_sum<5>(h, i, v, x, nc);
-      case 6: return dia_sum<6>(h, i, v, x, nc);
-      case 7: return dia_sum<7>(h, i, v, x, nc);
-      case 8: return dia_sum<8>(h, i, v, x, nc);
+      case 1: return dia_sum<1>(h, i, v, x, nc, keep);
+      case 2: return dia_sum<2>(h, i, v, x, nc, keep);
+      case 3: return dia_sum<3>(h, i, v, x, nc, keep);
+      case 4: return dia_sum<4>(h, i, v, x, nc, keep);
+      case 5: return dia_sum<5>(h, i, v, x, nc, keep);
+      case 6: return dia_sum<6>(h, i, v, x, nc, keep);
+      case 7: return dia_sum<7>(h, i, v, x, nc, keep);
+      case 8: return dia_sum<8>(h, i, v, x, nc, keep);
       default: return 0.0;
     }
   }
@@ -142,8 +178,8 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
     double vi[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      ci[j] = __ldcs(c + 32 * j);
-      vi[j] = __ldcs(v + 32 * j);
+      ci[j] = ldm(c + 32 * j, keep);
+      vi[j] = ldm(v + 32 * j, keep);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) sum = fma(vi[j], __ldg(x + ci[j]), sum);
@@ -157,8 +193,8 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (j < rem) {
-        ci[j] = __ldcs(c + 32 * j);
-        vi[j] = __ldcs(v + 32 * j);
+        ci[j] = ldm(c + 32 * j, keep);
+        vi[j] = ldm(v + 32 * j, keep);
       }
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -183,7 +219,8 @@ __device__ __forceinline__ int64_t sell_col(const int64_t* __restrict__ cptr, co
 // [b, e): entries b + sub, b + sub + G, ...; 4 independent loads in flight.
 template <int G>
 __device__ __forceinline__ double rg_row_sum(const int32_t* __restrict__ col, const double* __restrict__ val,
-                                             int64_t b, int64_t e, int sub, const double* __restrict__ x) {
+                                             int64_t b, int64_t e, int sub, const double* __restrict__ x,
+                                             bool keep) {
   double sum = 0.0;
   int64_t k = b + sub;
   for (; k + 3 * G < e; k += 4 * G) {
@@ -191,13 +228,13 @@ __device__ __forceinline__ double rg_row_sum(const int32_t* __restrict__ col, co
     double vi[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      ci[j] = __ldcs(col + k + j * G);
-      vi[j] = __ldcs(val + k + j * G);
+      ci[j] = ldm(col + k + j * G, keep);
+      vi[j] = ldm(val + k + j * G, keep);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) sum = fma(vi[j], __ldg(x + ci[j]), sum);
   }
-  for (; k < e; k += G) sum = fma(__ldcs(val + k), __ldg(x + __ldcs(col + k)), sum);
+  for (; k < e; k += G) sum = fma(ldm(val + k, keep), __ldg(x + ldm(col + k, keep)), sum);
   return sum;
 }
 
@@ -289,6 +326,7 @@ __device__ __forceinline__ void epilogue(const RowKArgs& a, int64_t i, double su
 // less per slice)
 template <RowOp OP>
 __device__ __forceinline__ void sell_body(const RowKArgs& a) {
+  pdl_enter();
   constexpr int NR = NRed<OP>::value;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -313,18 +351,20 @@ __device__ __forceinline__ void sell_body(const RowKArgs& a) {
     const bool live = i < a.n_rows;
     EpiIn e{0.0, 0.0, 0.0};
     if (live) e = epi_load<OP>(a, i);
-    const double sum = sell_row_sum(h, s, lane, a.col, a.val, a.x, a.ncols);
+    const double sum = sell_row_sum(h, s, lane, a.col, a.val, a.x, a.ncols, a.keep_matrix != 0);
     if (live) epi_store<OP>(a, i, sum, e, acc);
     t = tn;
     s = sn;
     h = hn;
   }
+  pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
 // row groups: one warp per unit of 32/G rows, G lanes per row, fixed shuffle tree
 template <RowOp OP, int G>
 __device__ __forceinline__ void rg_body(const RowKArgs& a) {
+  pdl_enter();
   constexpr int NR = NRed<OP>::value;
   constexpr int RU = 32 / G;
   const int lane = threadIdx.x & 31;
@@ -341,11 +381,12 @@ __device__ __forceinline__ void rg_body(const RowKArgs& a) {
       b = a.ptr[i];
       e = a.ptr[i + 1];
     }
-    double sum = rg_row_sum<G>(a.col, a.val, b, e, sub, a.x);
+    double sum = rg_row_sum<G>(a.col, a.val, b, e, sub, a.x, a.keep_matrix != 0);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, G);
     if (sub == 0 && i < a.n_rows) epilogue<OP>(a, i, sum, acc);
   }
+  pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
@@ -491,6 +532,7 @@ struct EpiVecs {  // which row vectors the epilogue reads: b, dinv, x(own), y
 
 template <RowOp OP>
 __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchunks, int64_t n_slices) {
+  pdl_enter();
   constexpr int NR = NRed<OP>::value;
   using EV = EpiVecs<OP>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -609,6 +651,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
+  pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
@@ -619,7 +662,7 @@ static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_s
     PSC_CUDA(cudaFuncSetAttribute(sell_tma<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
     attr = true;
   }
-  sell_tma<OP><<<grid, kTmaThreads, kTmaSmem, s>>>(a, nchunks, n_slices);
+  launch_k(sell_tma<OP>, grid, kTmaThreads, kTmaSmem, s, a, nchunks, n_slices);
 }
 
 // ---------------------------------------------- TMA-staged row-group kernel
@@ -640,6 +683,7 @@ constexpr int kRgSmem = kRgStages * kRgStageBytes + 2 * kRgStages * 8;
 
 template <RowOp OP, int G>
 __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunks) {
+  pdl_enter();
   constexpr int NR = NRed<OP>::value;
   constexpr int RU = 32 / G;
   constexpr int CR = kTmaSlices * RU;  // rows per chunk
@@ -752,6 +796,7 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
+  pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
@@ -762,7 +807,7 @@ static void rg_tma_launch(const RowKArgs& a, int grid, int64_t nchunks, cudaStre
     PSC_CUDA(cudaFuncSetAttribute(rg_tma<OP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRgSmem));
     attr = true;
   }
-  rg_tma<OP, G><<<grid, kTmaThreads, kRgSmem, s>>>(a, nchunks);
+  launch_k(rg_tma<OP, G>, grid, kTmaThreads, kRgSmem, s, a, nchunks);
 }
 
 template <int G>
@@ -794,7 +839,7 @@ static bool tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
 void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaStream_t s, SliceSet set) {
   RowKArgs a;
   // matrices up to 48 MB stay in L2 (evict_last) across the 8-10 launches of their level
-  a.keep_matrix = (A.padded * 12 + A.n_rows * 8) <= ((int64_t)48 << 20) ? 1 : 0;
+  a.keep_matrix = (A.padded * 12 + A.n_rows * 8) <= ((int64_t)env_int("PSC_KEEP_MB", 96) << 20) ? 1 : 0;
   a.ptr = A.ptr;
   a.cptr = A.cptr;
   a.hdr = A.hdr;
@@ -848,7 +893,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   }
   const int grid = row_grid(A, op, ctx->num_sms, set);
   PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
-  kernel_of(op, A.lanes)<<<grid, kBlock, 0, s>>>(a);
+  launch_k(kernel_of(op, A.lanes), grid, kBlock, 0, s, a);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -861,12 +906,14 @@ static int vec_grid(psc_ctx* ctx, int64_t n) {
 
 __global__ void __launch_bounds__(kBlock) scale_kernel(int64_t n, const double* __restrict__ dinv,
                                                        const double* __restrict__ b, double* __restrict__ x) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = dinv[i] * b[i];
+  pdl_exit();
 }
 
 void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, double* x, cudaStream_t s) {
-  scale_kernel<<<vec_grid(ctx, n), kBlock, 0, s>>>(n, dinv, b, x);
+  launch_k(scale_kernel, vec_grid(ctx, n), kBlock, 0, s, n, dinv, b, x);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -925,6 +972,7 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
                                                            const double* __restrict__ q, const double* g_pq,
                                                            const double* rz_old, int nranks, double* partials,
                                                            unsigned int* ticket, double* out) {
+  pdl_enter();
   const double alpha = __ldcg(rz_old) / gsum(g_pq, nranks);
   double acc[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -933,6 +981,7 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
     r[i] = ri;
     acc[0] += ri * ri;
   }
+  pdl_exit();
   grid_reduce<1>(acc, partials, ticket, out, 1);
 }
 
@@ -940,7 +989,8 @@ void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, doubl
                       const double* g_pq, const double* rz_old, int nranks, const RedSite* red, double* red_out,
                       cudaStream_t s) {
   const int g = std::min(vec_grid(ctx, n), red->grid);
-  cg_update_kernel<<<g, kBlock, 0, s>>>(n, x, p, r, q, g_pq, rz_old, nranks, red->partials, red->ticket, red_out);
+  launch_k(cg_update_kernel, g, kBlock, 0, s, n, x, p, r, q, g_pq, rz_old, nranks, red->partials, red->ticket,
+           red_out);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -948,10 +998,12 @@ void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, doubl
 __global__ void __launch_bounds__(kBlock) xpby_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ p,
                                                       const double* g_rz, double* rz_old, int nranks,
                                                       unsigned int* ticket) {
+  pdl_enter();
   const double rz = gsum(g_rz, nranks);
   const double beta = rz / __ldcg(rz_old);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
+  pdl_exit();
   // rz_old := rz once every CTA has read the old value
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -966,7 +1018,7 @@ __global__ void __launch_bounds__(kBlock) xpby_kernel(int64_t n, const double* _
 
 void launch_xpby(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rz, double* rz_old, int nranks,
                  const RedSite* red, cudaStream_t s) {
-  xpby_kernel<<<vec_grid(ctx, n), kBlock, 0, s>>>(n, z, p, g_rz, rz_old, nranks, red->ticket);
+  launch_k(xpby_kernel, vec_grid(ctx, n), kBlock, 0, s, n, z, p, g_rz, rz_old, nranks, red->ticket);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -974,42 +1026,48 @@ void launch_xpby(psc_ctx* ctx, int64_t n, const double* z, double* p, const doub
 __global__ void __launch_bounds__(kBlock) dot_kernel(int64_t n, const double* __restrict__ a,
                                                      const double* __restrict__ b, double* partials,
                                                      unsigned int* ticket, double* out) {
+  pdl_enter();
   double acc[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     acc[0] += a[i] * b[i];
+  pdl_exit();
   grid_reduce<1>(acc, partials, ticket, out, 1);
 }
 
 void launch_dot(psc_ctx* ctx, int64_t n, const double* a, const double* b, const RedSite* red, double* red_out,
                 cudaStream_t s) {
   const int g = std::min(vec_grid(ctx, n), red->grid);
-  dot_kernel<<<g, kBlock, 0, s>>>(n, a, b, red->partials, red->ticket, red_out);
+  launch_k(dot_kernel, g, kBlock, 0, s, n, a, b, red->partials, red->ticket, red_out);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
 
 __global__ void pack_kernel(int64_t n, const int32_t* __restrict__ idx, const double* __restrict__ x,
                             double* __restrict__ out) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = x[idx[i]];
+  pdl_exit();
 }
 
 void launch_pack(psc_ctx* ctx, int64_t n, const int32_t* idx, const double* x, double* sendbuf, cudaStream_t s) {
   if (n == 0) return;
-  pack_kernel<<<vec_grid(ctx, n), kBlock, 0, s>>>(n, idx, x, sendbuf);
+  launch_k(pack_kernel, vec_grid(ctx, n), kBlock, 0, s, n, idx, x, sendbuf);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
 
 __global__ void gather_kernel(int64_t n, const int64_t* __restrict__ map, const double* __restrict__ in,
                               double* __restrict__ out) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = in[map[i]];
+  pdl_exit();
 }
 
 void launch_gather(psc_ctx* ctx, int64_t n, const int64_t* map, const double* in, double* out, cudaStream_t s) {
   if (n == 0) return;
-  gather_kernel<<<vec_grid(ctx, n), kBlock, 0, s>>>(n, map, in, out);
+  launch_k(gather_kernel, vec_grid(ctx, n), kBlock, 0, s, n, map, in, out);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -1040,6 +1098,7 @@ struct CoarseArgs {
 
 template <bool SELL, bool STAGE>
 __global__ void __launch_bounds__(kCoarseThreads) coarse_solve(CoarseArgs a) {
+  pdl_enter();
   extern __shared__ double sm[];
   const int64_t n = a.n;
   double* xa = sm;
@@ -1103,6 +1162,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve(CoarseArgs a) {
     xb = t;
   }
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a.xout[i] = xa[i];
+  pdl_exit();
 }
 
 template <bool SELL, bool STAGE>
@@ -1112,7 +1172,7 @@ static void coarse_launch(const CoarseArgs& a, size_t smem, cudaStream_t s) {
     PSC_CUDA(cudaFuncSetAttribute(coarse_solve<SELL, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     attr = true;
   }
-  coarse_solve<SELL, STAGE><<<1, kCoarseThreads, smem, s>>>(a);
+  launch_k(coarse_solve<SELL, STAGE>, 1, kCoarseThreads, smem, s, a);
 }
 
 void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const double* b, double* x, int nsweeps,
@@ -1174,6 +1234,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_dense(const double* __r
                                                                const double* __restrict__ dinv,
                                                                const double* __restrict__ b, double* __restrict__ xout,
                                                                int nsweeps, int gk) {
+  pdl_enter();
   extern __shared__ __align__(16) double smd[];
   double* As = smd;
   double* xa = As + (size_t)n * n + 1;
@@ -1227,6 +1288,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_dense(const double* __r
     xb = t;
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xa[i];
+  pdl_exit();
 }
 
 void launch_coarse_dense(psc_ctx* ctx, const double* Ad, int64_t n, const double* dinv, const double* b, double* x,
@@ -1240,7 +1302,7 @@ void launch_coarse_dense(psc_ctx* ctx, const double* Ad, int64_t n, const double
   int gk = 1;
   while (gk < 32 && (int64_t)(gk * 2) * std::max<int64_t>(n, 1) <= kCoarseThreads) gk *= 2;
   const size_t smem = ((size_t)n * n + 1 + 4 * (size_t)std::max<int64_t>(n, 1)) * sizeof(double);
-  coarse_dense<<<1, kCoarseThreads, smem, s>>>(Ad, (int)n, dinv, b, x, nsweeps, gk);
+  launch_k(coarse_dense, 1, kCoarseThreads, smem, s, Ad, (int)n, dinv, b, x, nsweeps, gk);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -1408,15 +1470,17 @@ __global__ void rg_fill_kernel(int64_t n_rows, const int64_t* __restrict__ rowpt
   }
 }
 
-// Layout choice: short rows (mean < PSC_RG_MIN = 10) -> sliced ELL,
-// thread per row; long rows -> G lanes per row, G = pow2floor(mean / PSC_RG_DIV)
-// clamped to [4, 32].  PSC_LANES forces a layout (1, 4, 8, 16, 32).
+// Layout choice: rows shorter than PSC_RG_MIN = 100 on average ->
+// sliced ELL, thread per row (measured faster than row groups on the 31-nnz/row
+// level-1 operator of 256^3: 150 vs 179 us per sweep); long rows -> G lanes per
+// row, G = pow2floor(mean / PSC_RG_DIV) clamped to [4, 32].  PSC_LANES forces a
+// layout (1, 4, 8, 16, 32).
 int choose_lanes(int64_t n_rows, int64_t nnz) {
   const int forced = env_int("PSC_LANES", 0);
   if (forced == 1 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
   const double mu = n_rows ? (double)nnz / (double)n_rows : 0.0;
-  if (mu < env_int("PSC_RG_MIN", 10)) return 1;
-  const double t = mu / std::max(1, env_int("PSC_RG_DIV", 4));
+  if (mu < env_int("PSC_RG_MIN", 100)) return 1;
+  const double t = mu / std::max(1, env_int("PSC_RG_DIV", 1));
   int G = 4;
   while (G * 2 <= t && G < 32) G *= 2;
   return G;

@@ -1,0 +1,110 @@
+"""Worker for tests/test_gpu_dist.py (launched by torchrun, one process per GPU).
+
+Rank 0 generates the global hierarchy for the rank-box grid, every rank maps its
+rows, the distributed CUDA path (NCCL halo exchange, replicated coarsest level)
+runs SpMV / V-cycle / PCG, and rank 0 compares with the CPU oracle on the global
+hierarchy.  Prints one JSON line on rank 0; exit code 0 on success.
+"""
+import json
+import os
+import sys
+import tempfile
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import bench
+    import paper_2406_19754_b200 as psc
+    import pscgen
+
+    grid = tuple(int(v) for v in os.environ.get("PSC_TEST_GRID", "32,32,64").split(","))
+    procs = tuple(int(v) for v in os.environ.get("PSC_TEST_PROCS", "1,1,2").split(","))
+    problem = os.environ.get("PSC_TEST_PROBLEM", "poisson")
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    shm = os.environ.get("PSC_TEST_SHM") or tempfile.gettempdir()
+    d = os.path.join(shm, f"psc_dist_{grid[0]}x{grid[1]}x{grid[2]}_{procs}_{problem}".replace(" ", ""))
+    h = None
+    if rank == 0:
+        h = pscgen.poisson_hierarchy(*grid, procs=procs, problem=problem, cube=8, coarse_target=60)
+        bench.save_rank_levels(d, h, world)
+    dist.barrier()
+    levels, meta = bench.load_rank_levels(d, rank)
+    obj = [psc.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx = psc.Context(rank=rank, nranks=world, device=local, unique_id=obj[0])
+    H, descs, A, P, R = psc.build_hierarchy(ctx, levels)
+    rs = levels[0]["row_start"]
+    r0, r1 = int(rs[rank]), int(rs[rank + 1])
+    N = int(levels[0]["n_global"])
+    out = {}
+    # SpMV of every level matrix
+    spmv = []
+    for l in range(meta["nlevels"]):
+        mats = [("A", A[l], l, l)] + ([("P", P[l], l, l + 1), ("R", R[l], l + 1, l)] if l < meta["nlevels"] - 1 else [])
+        for name, M, rsp, csp in mats:
+            crs = levels[csp]["row_start"]
+            rrs = levels[rsp]["row_start"]
+            xg = pscgen.rhs_random(31 + l, 0, int(levels[csp]["n_global"]))
+            x = torch.from_numpy(xg[int(crs[rank]):int(crs[rank + 1])].copy()).cuda()
+            y = torch.zeros(int(rrs[rank + 1] - rrs[rank]), dtype=torch.float64, device="cuda")
+            M.spmv(x, y)
+            spmv.append((name, l, y.cpu().numpy()))
+    allspmv = [None] * world
+    dist.all_gather_object(allspmv, spmv)
+    # V-cycle and PCG on the global RHS
+    b = pscgen.rhs_random(7, 0, N)
+    z = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+    H.vcycle(torch.from_numpy(b[r0:r1].copy()).cuda(), z)
+    x = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+    rc, st, hist = H.solve(torch.from_numpy(b[r0:r1].copy()).cuda(), x, tol=1e-8, maxit=200)
+    parts = [None] * world
+    dist.all_gather_object(parts, (z.cpu().numpy(), x.cpu().numpy(), rc, st["iters"], hist))
+    ok = True
+    if rank == 0:
+        import oracle
+        for k, (name, l, _) in enumerate(spmv):
+            M = getattr(h.levels[l], name)
+            rsp = l if name != "R" else l + 1
+            csp = l if name != "P" else l + 1
+            xg = pscgen.rhs_random(31 + l, 0, M.shape[1])
+            ref = oracle.spmv(M, xg)
+            got = np.concatenate([allspmv[p][k][2] for p in range(world)])
+            scale = abs(M.to_scipy()) @ np.abs(xg)
+            e = float((np.abs(got - ref) / (scale + 1e-300)).max())
+            out[f"spmv_{name}{l}"] = e
+            ok &= e <= 1e-14
+        zg = np.concatenate([p[0] for p in parts])
+        zo = oracle.vcycle(h, b)
+        out["vcycle_rel"] = float(np.linalg.norm(zg - zo) / np.linalg.norm(zo))
+        ok &= out["vcycle_rel"] <= 1e-12
+        xg = np.concatenate([p[1] for p in parts])
+        xo, ito, sto, histo = oracle.pcg(h, b, tol=1e-8, maxit=200)
+        its = {p[3] for p in parts}
+        out.update(iters_gpu=sorted(its), iters_oracle=ito, rc=[p[2] for p in parts])
+        k = min(20, ito, parts[0][3]) + 1
+        out["hist_rel"] = float(np.max(np.abs(parts[0][4][:k] - histo[:k]) / histo[:k]))
+        out["x_rel"] = float(np.linalg.norm(xg - xo) / np.linalg.norm(xo))
+        same_hist = all(np.array_equal(parts[0][4], p[4]) for p in parts)
+        out["hist_identical_across_ranks"] = same_hist
+        ok &= (len(its) == 1 and abs(parts[0][3] - ito) <= 1 and all(p[2] == 0 for p in parts)
+               and out["hist_rel"] <= 1e-9 and out["x_rel"] <= 1e-7 and same_hist)
+        out["ok"] = bool(ok)
+        print(json.dumps(out), flush=True)
+    flag = [ok]
+    dist.broadcast_object_list(flag, src=0)
+    ctx.close()
+    dist.destroy_process_group()
+    sys.exit(0 if flag[0] else 1)
+
+
+if __name__ == "__main__":
+    main()
