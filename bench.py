@@ -147,7 +147,7 @@ def load_rank_levels(d, r):
 
 
 # -------------------------------------------------------------- reference
-def run_reference(args, rank, world):
+def run_reference(args, rank, world, out=sys.stdout):
     """CPU oracle arm: rank 0 only; each step = 1 PCG iteration on a 256^3 sample."""
     if rank != 0:
         return
@@ -177,11 +177,22 @@ def run_reference(args, rank, world):
                          "sample": f"{args.steps} steps x 1 PCG iteration (incl. its V-cycles) on {g}^3"},
         "e2e": {"value": value, "unit": "Mdof*iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=out, flush=True)
 
 
 # ------------------------------------------------------------------- main
+def _json_out():
+    """The driver reads ONE JSON line from stdout: send everything else (NCCL's version
+    banner, library prints) to stderr by pointing fd 1 at fd 2; keep a handle on the
+    real stdout for the result line."""
+    sys.stdout.flush()
+    real = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    return real
+
+
 def main():
+    out = _json_out()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -206,7 +217,7 @@ def main():
         raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
 
     if args.impl == "reference":
-        run_reference(args, rank, N)
+        run_reference(args, rank, N, out)
         return
 
     import torch
@@ -354,10 +365,12 @@ def main():
                 "model": "none (sparse solver)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": sum(s["kernel_launches"] for s in stats),
+            "launches_per_iteration": stats[0]["iter_graph_nodes"],
+            "halo_path": {0: "single rank", 1: "NVLink peer stores (CUDA IPC)", 2: "NCCL"}[stats[0]["halo_path"]],
             "collectives": sum(s["collectives"] for s in stats),
             "clocks": clk,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=out, flush=True)
     ctx.close()
     if N > 1:
         dist.barrier()

@@ -198,6 +198,8 @@ typedef struct {
   int64_t dom_kernel_launches;  /* number of those launches */
   double dom_kernel_bytes;      /* algorithmic bytes per launch: 12 nnz(A_0) + 32 n_0 */
   int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by psc_pcg_solve_host */
+  int halo_path;                /* 0 single rank, 1 NVLink peer stores (CUDA IPC), 2 NCCL */
+  int iter_graph_nodes;         /* kernel launches per PCG iteration (captured graph) */
 } psc_stats;
 
 /* [collective] PCG (reading R1 of DESIGN.md) preconditioned by one

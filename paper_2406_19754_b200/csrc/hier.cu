@@ -10,6 +10,7 @@
 #include <cstring>
 
 #include "kernels.h"
+#include "p2p.h"
 
 using namespace psc;
 
@@ -73,6 +74,10 @@ struct psc_hier_s {
   std::vector<cudaEvent_t> ev_dom;  // pairs (start, end)
   int dom_used = 0;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+  // buffers peers write into (halo-bearing vectors, gathered scalars, coarse
+  // gather buffer, P2P flags) live in one arena: one CUDA IPC handle maps them
+  char* arena = nullptr;
+  P2P p2p;
 };
 
 namespace {
@@ -98,8 +103,17 @@ double* rz_old(psc_hier* h) { return h->d_scal + (size_t)NSLOT * h->ctx->nranks;
 void allgather_slot(psc_hier* h, Slot s, cudaStream_t st) {
   psc_ctx* ctx = h->ctx;
   if (ctx->nranks == 1) return;
+  if (p2p_allgather(ctx, h->p2p, scal_mine(h, s), 1, scal(h, s), st)) return;
   PSC_NCCL(ncclAllGather(scal_mine(h, s), scal(h, s), 1, ncclDouble, ctx->comm, st));
   ctx->collectives++;
+}
+
+// halo exchange of a level vector: NVLink peer stores when available, else NCCL
+void exchange(psc_hier* h, psc_desc* d, double* x, cudaStream_t s) {
+  psc_ctx* ctx = h->ctx;
+  if (ctx->nranks == 1) return;
+  if (p2p_halo(ctx, h->p2p, d, x, s)) return;
+  halo_exchange(ctx, d, x, s);
 }
 
 // ------------------------------------------------------------ coarsest level
@@ -112,9 +126,11 @@ double* coarse_solve(psc_hier* h, const double* b, int nsweeps, cudaStream_t s) 
     Replica& R = h->rep;
     // gather b_coarse on every rank, solve the whole coarse system redundantly
     // (bit-identical per row to the distributed sweeps), scatter to owned+halo.
-    if (W.n) PSC_CUDA(cudaMemcpyAsync(R.sendbuf, b, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
-    PSC_NCCL(ncclAllGather(R.sendbuf, R.gbuf, R.maxcnt, ncclDouble, ctx->comm, s));
-    ctx->collectives++;
+    if (!p2p_allgather(ctx, h->p2p, b, W.n, R.gbuf, s)) {
+      if (W.n) PSC_CUDA(cudaMemcpyAsync(R.sendbuf, b, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+      PSC_NCCL(ncclAllGather(R.sendbuf, R.gbuf, R.maxcnt, ncclDouble, ctx->comm, s));
+      ctx->collectives++;
+    }
     launch_gather(ctx, R.N, R.map_full, R.gbuf, R.bfull, s);
     if (R.dense) launch_coarse_dense(ctx, R.dense, R.N, R.dinv, R.bfull, R.xfull, nsweeps, s);
     else launch_coarse_solve(ctx, R.S, R.dinv, R.bfull, R.xfull, nsweeps, s);
@@ -137,7 +153,7 @@ double* coarse_solve(psc_hier* h, const double* b, int nsweeps, cudaStream_t s) 
   }
   launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
   for (int k = 1; k < nsweeps; ++k) {
-    halo_exchange(ctx, W.d, W.x[cur], s);
+    exchange(h, W.d, W.x[cur], s);
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
@@ -165,7 +181,7 @@ int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s,
   launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
   int cur = 0;
   for (int k = 1; k < nsweeps; ++k) {
-    halo_exchange(ctx, W.d, W.x[cur], s);
+    exchange(h, W.d, W.x[cur], s);
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
@@ -194,7 +210,7 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
   // (I - M^-1 A)^pre
   int cur = pre_smooth(h, l, b, h->opt.pre_sweeps, s, timing);
   // coarse-grid correction (I - P B_{l+1} P^T A): r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
-  halo_exchange(ctx, W.d, W.x[cur], s);
+  exchange(h, W.d, W.x[cur], s);
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -203,7 +219,7 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
     a.y = W.r;
     launch_rows(ctx, W.A->S, RowOp::Resid, a, s);
   }
-  halo_exchange(ctx, W.d, W.r, s);
+  exchange(h, W.d, W.r, s);
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -212,7 +228,7 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
     launch_rows(ctx, W.R->S, RowOp::Spmv, a, s);
   }
   double* xc = vcycle_level(h, l + 1, C.b, s, timing);
-  if (!(l + 1 == h->L - 1 && coarse_has_halo(h))) halo_exchange(ctx, C.d, xc, s);
+  if (!(l + 1 == h->L - 1 && coarse_has_halo(h))) exchange(h, C.d, xc, s);
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -223,7 +239,7 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
   const int post = h->opt.post_sweeps;
   for (int k = 0; k < post; ++k) {
-    halo_exchange(ctx, W.d, W.x[cur], s);
+    exchange(h, W.d, W.x[cur], s);
     const bool last0 = (l == 0 && k == post - 1);
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -261,7 +277,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
   h->z_ptr = z;
   allgather_slot(h, S_RZ, s);
   launch_xpby(ctx, W.n, z, h->p, scal(h, S_RZ), rz_old(h), R, &h->red2, s);
-  halo_exchange(ctx, W.d, h->p, s);
+  exchange(h, W.d, h->p, s);
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -372,9 +388,7 @@ void build_replica(psc_hier* h) {
     rp.dense = dvec(rp.N * rp.N + 1);
     dense_from_sell(ctx, rp.S, rp.dense, s);
   }
-  // b gather map: padded allgather buffer -> global index
-  for (int r = 0; r < R; ++r) rp.maxcnt = std::max(rp.maxcnt, d->row_start[r + 1] - d->row_start[r]);
-  rp.maxcnt = std::max<int64_t>(rp.maxcnt, 1);
+  // b gather map: padded allgather buffer (allocated in the arena) -> global index
   std::vector<int64_t> mf(rp.N);
   for (int r = 0; r < R; ++r)
     for (int64_t g = d->row_start[r]; g < d->row_start[r + 1]; ++g) mf[g] = r * rp.maxcnt + (g - d->row_start[r]);
@@ -386,7 +400,6 @@ void build_replica(psc_hier* h) {
   PSC_CUDA(cudaMemcpy(rp.map_full, mf.data(), sizeof(int64_t) * rp.N, cudaMemcpyHostToDevice));
   if (!ml.empty()) PSC_CUDA(cudaMemcpy(rp.map_loc, ml.data(), sizeof(int64_t) * ml.size(), cudaMemcpyHostToDevice));
   rp.sendbuf = dvec(rp.maxcnt);
-  rp.gbuf = dvec((size_t)R * rp.maxcnt);
   rp.bfull = dvec(rp.N);
   rp.xfull = dvec(rp.N);
   PSC_CUDA(cudaMemset(rp.sendbuf, 0, sizeof(double) * rp.maxcnt));
@@ -398,11 +411,9 @@ void free_hier(psc_hier* h) {
   if (!h) return;
   cudaSetDevice(h->ctx->device);
   if (h->ctx->stream) cudaStreamSynchronize(h->ctx->stream);
+  p2p_free(h->ctx, h->p2p);
   for (auto& W : h->lv) {
     dfree(W.dinv);
-    dfree(W.x[0]);
-    dfree(W.x[1]);
-    dfree(W.r);
     if (&W != &h->lv[0]) dfree(W.b);
   }
   Replica& rp = h->rep;
@@ -411,16 +422,13 @@ void free_hier(psc_hier* h) {
   dfree(rp.dense);
   dfree(h->coarse_dense);
   dfree(rp.sendbuf);
-  dfree(rp.gbuf);
   dfree(rp.map_full);
   dfree(rp.bfull);
   dfree(rp.xfull);
   dfree(rp.map_loc);
-  dfree(h->x_int);
   dfree(h->r_cg);
-  dfree(h->p);
   dfree(h->q);
-  dfree(h->d_scal);
+  dfree(h->arena);  // x[0], x[1], r of every level, x_int, p, d_scal, coarse gather buffer, flags
   dfree(h->d_bhost);
   dfree(h->d_xhost);
   if (h->h_scal) cudaFreeHost(h->h_scal);
@@ -443,7 +451,7 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
   psc_stats S{};
   PSC_CUDA(cudaEventRecord(h->ev_t0, s));
   if (W.n) PSC_CUDA(cudaMemcpyAsync(h->x_int, x, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
-  halo_exchange(ctx, W.d, h->x_int, s);
+  exchange(h, W.d, h->x_int, s);
   {
     RowArgs a;
     a.vec_padded = false;  // reads the caller's b
@@ -527,6 +535,8 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
   // explicit column index (ELL slices), x in, b, dinv, x out
   S.dom_kernel_bytes = 8.0 * (double)W.A->nnz + 4.0 * (double)W.A->S.nnz_ell + 32.0 * (double)W.n;
   S.h2d_bytes = (int64_t)extra_h2d;
+  S.halo_path = R == 1 ? 0 : (h->p2p.on ? 1 : 2);
+  S.iter_graph_nodes = (int)h->iter_launches;
   if (st) *st = S;
   if (status == PSC_ERR_BREAKDOWN) throw Error(PSC_ERR_BREAKDOWN, "PCG breakdown: p^T A p <= 0 or not finite");
   return status;
@@ -568,26 +578,47 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       }
     }
     cudaStream_t s = ctx->stream;
+    const int NR = ctx->nranks;
+    LevelWS& W0 = h->lv[0];
+    // the arena: every buffer a peer writes into (halo-bearing vectors, gathered
+    // scalars, the coarsest level's gather buffer, P2P flags), zero-initialised
+    psc_desc* dc = h->lv[nlevels - 1].d;
+    int64_t maxcnt = 1;
+    for (int r = 0; r < NR; ++r) maxcnt = std::max(maxcnt, dc->row_start[r + 1] - dc->row_start[r]);
+    double* gbuf = nullptr;
+    double* flagbuf = nullptr;
+    std::vector<std::pair<double**, size_t>> plan;
+    for (int l = 0; l < nlevels; ++l) {
+      LevelWS& W = h->lv[l];
+      for (double** b : {&W.x[0], &W.x[1], &W.r}) plan.push_back({b, (size_t)(W.n + W.nh) + 64});
+    }
+    plan.push_back({&h->x_int, (size_t)(W0.n + W0.nh) + 64});
+    plan.push_back({&h->p, (size_t)(W0.n + W0.nh) + 64});
+    plan.push_back({&h->d_scal, (size_t)NSLOT * NR + 1 + 64});
+    if (NR > 1) plan.push_back({&gbuf, (size_t)NR * maxcnt + 64});
+    plan.push_back({&flagbuf, (size_t)NR + 8});
+    size_t total = 0;
+    for (auto& pl : plan) total += (pl.second * sizeof(double) + 255) & ~(size_t)255;
+    h->arena = dalloc<char>(total);
+    PSC_CUDA(cudaMemset(h->arena, 0, total));
+    size_t off = 0;
+    for (auto& pl : plan) {
+      *pl.first = reinterpret_cast<double*>(h->arena + off);
+      off += (pl.second * sizeof(double) + 255) & ~(size_t)255;
+    }
     for (int l = 0; l < nlevels; ++l) {
       LevelWS& W = h->lv[l];
       W.dinv = dvec(W.n);
       launch_l1_dinv(ctx, W.A->S, W.dinv, s);  // smoother build
-      W.x[0] = dvec(W.n + W.nh);
-      W.x[1] = dvec(W.n + W.nh);
-      W.r = dvec(W.n + W.nh);
-      PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
-      PSC_CUDA(cudaMemsetAsync(W.x[1], 0, sizeof(double) * (W.n + W.nh), s));
-      PSC_CUDA(cudaMemsetAsync(W.r, 0, sizeof(double) * (W.n + W.nh), s));
       if (l > 0) W.b = dvec(W.n);
     }
-    LevelWS& W0 = h->lv[0];
-    h->x_int = dvec(W0.n + W0.nh);
     h->r_cg = dvec(W0.n);
-    h->p = dvec(W0.n + W0.nh);
     h->q = dvec(W0.n);
     W0.b = h->r_cg;
-    h->d_scal = dvec((size_t)NSLOT * ctx->nranks + 1);
-    PSC_CUDA(cudaMemsetAsync(h->d_scal, 0, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1), s));
+    if (NR > 1) {
+      h->rep.gbuf = gbuf;
+      h->rep.maxcnt = maxcnt;
+    }
     PSC_CUDA(cudaMallocHost(&h->h_scal, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1)));
     h->red1 = red_alloc(ctx->num_sms, 1);
     h->red2 = red_alloc(ctx->num_sms, 2);
@@ -606,6 +637,20 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     LevelWS& Wc = h->lv[nlevels - 1];
     if (ctx->nranks > 1) {
       build_replica(h);
+      std::vector<P2PBufSpec> hb;
+      std::vector<psc_desc*> ld;
+      for (int l = 0; l < nlevels; ++l) {
+        LevelWS& W = h->lv[l];
+        ld.push_back(W.d);
+        for (double* b : {W.x[0], W.x[1], W.r}) hb.push_back({b, l});
+      }
+      hb.push_back({h->x_int, 0});
+      hb.push_back({h->p, 0});
+      std::vector<P2PGatherSpec> gs;
+      for (int sl = 0; sl < NSLOT; ++sl) gs.push_back({scal(h, (Slot)sl), ctx->rank});
+      if (h->rep.on) gs.push_back({h->rep.gbuf, (int64_t)ctx->rank * h->rep.maxcnt});
+      h->p2p.arena = h->arena;
+      p2p_setup(ctx, h->p2p, hb, gs, ld, (char*)flagbuf - h->arena);
     } else {
       h->coarse_one_cta = (Wc.n <= coarse_smem_rows() && Wc.nh == 0);
       if (Wc.n <= coarse_dense_max_rows() && Wc.nh == 0 && !getenv("PSC_NO_DENSE_COARSE")) {

@@ -1,0 +1,52 @@
+// p2p.h — NVLink peer-memory exchanges (see p2p.cu).
+#pragma once
+#include <map>
+#include <vector>
+
+#include "psc_internal.h"
+
+namespace psc {
+
+struct P2PBufSpec {  // a halo-bearing vector in the arena, exchanged at `level`
+  double* local;
+  int level;
+};
+struct P2PGatherSpec {  // an all-gather target in the arena; my block starts at local + my_block
+  double* local;
+  int64_t my_block;
+};
+struct P2PBufDev {
+  int level = -1;
+  double** d_dst = nullptr;  // [R] device pointers into peer memory
+};
+struct P2PLevel {
+  bool any = false;
+  int64_t max_send = 0;
+  int32_t* d_nbr = nullptr;
+  int64_t* d_soff = nullptr;
+};
+struct P2P {
+  bool on = false;
+  char* arena = nullptr;  // this rank's IPC-shared allocation (owned by the hierarchy)
+  std::vector<char*> peer_arena;
+  uint64_t* flags = nullptr;  // [R] in the arena
+  uint64_t** d_pflag = nullptr;
+  uint64_t* d_gen = nullptr;
+  unsigned int* d_ticket = nullptr;
+  int32_t* d_all = nullptr;
+  std::vector<P2PLevel> levels;
+  std::map<const double*, P2PBufDev> bufs;
+  std::map<const double*, P2PBufDev> gathers;
+};
+
+// collective; P.arena must be set and the flags region zeroed
+void p2p_setup(psc_ctx* ctx, P2P& P, const std::vector<P2PBufSpec>& halo_bufs,
+               const std::vector<P2PGatherSpec>& gathers, const std::vector<psc_desc*>& level_desc,
+               int64_t flags_off);
+void p2p_free(psc_ctx* ctx, P2P& P);
+// false: not handled (caller falls back to NCCL)
+bool p2p_halo(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, cudaStream_t s);
+bool p2p_allgather(psc_ctx* ctx, P2P& P, const double* src, int64_t n, const double* dst_base_local,
+                   cudaStream_t s);
+
+}  // namespace psc
