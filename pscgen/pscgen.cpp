@@ -36,6 +36,7 @@
 #include <memory>
 #include <vector>
 #include <omp.h>
+#include <cstdio>
 
 namespace {
 
@@ -310,6 +311,8 @@ struct SmoothedPRow {
   }
 };
 
+// R = P^T.  Parallel: column counts and slot claims with atomics, then every
+// row of R is sorted by column, so the result is deterministic.
 void transpose(const CSR& P, CSR& R) {
   const int64_t n = P.nrows, nc = P.ncols, nnz = P.nnz();
   R.nrows = nc;
@@ -318,19 +321,72 @@ void transpose(const CSR& P, CSR& R) {
   R.col.alloc(nnz);
   R.val.alloc(nnz);
   std::vector<int64_t> cnt(nc + 1, 0);
-  for (int64_t k = 0; k < nnz; ++k) cnt[P.col[k] + 1]++;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < nnz; ++k) {
+#pragma omp atomic
+    cnt[P.col[k] + 1]++;
+  }
   for (int64_t c = 0; c < nc; ++c) cnt[c + 1] += cnt[c];
   for (int64_t c = 0; c <= nc; ++c) R.ptr[c] = cnt[c];
+#pragma omp parallel for schedule(dynamic, 4096)
   for (int64_t i = 0; i < n; ++i)
     for (int64_t k = P.ptr[i]; k < P.ptr[i + 1]; ++k) {
-      int64_t c = P.col[k];
-      int64_t o = cnt[c]++;
+      const int64_t c = P.col[k];
+      int64_t o;
+#pragma omp atomic capture
+      o = cnt[c]++;
       R.col[o] = i;
       R.val[o] = P.val[k];
     }
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t c = 0; c < nc; ++c) {
+    const int64_t b = R.ptr[c], e = R.ptr[c + 1];
+    for (int64_t x = b + 1; x < e; ++x) {  // insertion sort by row index (rows are short)
+      const int64_t cc = R.col[x];
+      const double vv = R.val[x];
+      int64_t y = x - 1;
+      while (y >= b && R.col[y] > cc) { R.col[y + 1] = R.col[y]; R.val[y + 1] = R.val[y]; --y; }
+      R.col[y + 1] = cc;
+      R.val[y + 1] = vv;
+    }
+  }
 }
 
-// Galerkin product rows: A_c[J,:] = sum_i R[J,i] sum_k A[i,k] P[k,:]
+// Sparse product rows (Gustavson): C[i,:] = sum_k X[i,k] Y[k,:], accumulated in
+// X's stored order, output columns sorted.  Used twice for the Galerkin
+// operator A_{l+1} = R (A P): first AP = A P, then R (AP).
+struct SpGEMMRow {
+  const CSR *X, *Y;
+  int64_t ncols;
+  struct State {
+    std::vector<double> acc;
+    std::vector<int64_t> mark;
+    std::vector<int64_t> touched;
+  };
+  State make_state() const {
+    State s;
+    s.acc.assign(ncols, 0.0);
+    s.mark.assign(ncols, -1);
+    return s;
+  }
+  void operator()(State& s, int64_t i, std::vector<int64_t>& col, std::vector<double>& val) const {
+    s.touched.clear();
+    for (int64_t a = X->ptr[i]; a < X->ptr[i + 1]; ++a) {
+      const int64_t k = X->col[a];
+      const double xv = X->val[a];
+      for (int64_t c = Y->ptr[k]; c < Y->ptr[k + 1]; ++c) {
+        const int64_t K = Y->col[c];
+        if (s.mark[K] != i) { s.mark[K] = i; s.acc[K] = 0.0; s.touched.push_back(K); }
+        s.acc[K] += xv * Y->val[c];
+      }
+    }
+    std::sort(s.touched.begin(), s.touched.end());
+    for (int64_t K : s.touched) { col.push_back(K); val.push_back(s.acc[K]); }
+  }
+};
+
+// Direct Galerkin rows: A_c[J,:] = sum_i R[J,i] sum_k A[i,k] P[k,:] (cheapest when
+// A is a short-row stencil: no intermediate AP).
 struct RAPRow {
   const CSR *R, *A, *P;
   int64_t nc;
@@ -381,13 +437,25 @@ void diag_of(const CSR& A, std::vector<double>& d) {
       if (A.col[k] == i) d[i] = A.val[k];
 }
 
+static bool verbose() { return getenv("PSCGEN_VERBOSE") != nullptr; }
+#define TLOG(name)                                                                        \
+  do {                                                                                    \
+    if (verbose()) {                                                                      \
+      double t1 = omp_get_wtime();                                                        \
+      fprintf(stderr, "[pscgen] level %d %-12s %.2f s\n", l, name, t1 - t0);             \
+      t0 = t1;                                                                            \
+    }                                                                                     \
+  } while (0)
+
 void build_levels(Hier* h, const Params& prm) {
   for (;;) {
+    double t0 = omp_get_wtime();
     Level& L = h->lv.back();
     const int l = (int)h->lv.size() - 1;
     if (L.n <= prm.coarse_target || l + 1 >= prm.max_levels) break;
     std::vector<double> diag;
     diag_of(L.A, diag);
+    TLOG("diag");
     // decoupled aggregation, independently per rank
     std::vector<int64_t> agg_local(L.n);
     std::vector<int64_t> nagg(h->nranks);
@@ -395,6 +463,7 @@ void build_levels(Hier* h, const Params& prm) {
     for (int r = 0; r < h->nranks; ++r)
       nagg[r] = vmb_aggregate_rank(L.A, diag.data(), L.row_start[r], L.row_start[r + 1], prm.theta,
                                    agg_local.data() + L.row_start[r]);
+    TLOG("aggregate");
     std::vector<int64_t> crs(h->nranks + 1, 0);
     for (int r = 0; r < h->nranks; ++r) crs[r + 1] = crs[r] + nagg[r];
     const int64_t nc = crs[h->nranks];
@@ -417,12 +486,23 @@ void build_levels(Hier* h, const Params& prm) {
     h->omega.push_back(prm.smooth ? omega : 0.0);
     SmoothedPRow prow{&L.A, diag.data(), L.agg.data(), omega, prm.smooth != 0};
     build_csr_chunked(L.P, L.n, nc, prow);
+    TLOG("prolongator");
     transpose(L.P, L.R);
+    TLOG("transpose");
     Level NL;
     NL.n = nc;
     NL.row_start = crs;
-    RAPRow rrow{&L.R, &L.A, &L.P, nc};
-    build_csr_chunked(NL.A, nc, nc, rrow);
+    if (L.A.nnz() <= 8 * L.n) {  // stencil-like A: direct triple product
+      RAPRow rrow{&L.R, &L.A, &L.P, nc};
+      build_csr_chunked(NL.A, nc, nc, rrow);
+    } else {  // denser A: AP first, then R (AP)
+      CSR AP;
+      SpGEMMRow aprow{&L.A, &L.P, nc};
+      build_csr_chunked(AP, L.n, nc, aprow);
+      SpGEMMRow raprow{&L.R, &AP, nc};
+      build_csr_chunked(NL.A, nc, nc, raprow);
+    }
+    TLOG("galerkin");
     h->lv.push_back(std::move(NL));
   }
 }
