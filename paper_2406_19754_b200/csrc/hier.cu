@@ -55,6 +55,7 @@ struct psc_hier_s {
   std::vector<LevelWS> lv;
   Replica rep;
   bool coarse_one_cta = false;
+  bool z0_fused = false;  // CG update writes the first level-0 sweep of the next V-cycle
   double* coarse_dense = nullptr;  // dense copy of A_coarse (single rank, small coarsest level)
   // CG state (level 0)
   double* x_int = nullptr;  // n0 + nh0
@@ -171,14 +172,17 @@ bool coarse_has_halo(psc_hier* h) { return h->rep.on; }
 // nsweeps l1-Jacobi sweeps from zero at level l < L-1 (pre-smoothing: the
 // rightmost factor of Eq. (2) applied `pre` times).  The first sweep is
 // x = M^{-1} b exactly.  Returns the index of the buffer holding x.
-int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s, bool timing) {
+// first_done: x[0] = M^{-1} b was already written by the kernel that produced b
+// (the restriction, or the CG update at level 0).
+int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s, bool timing,
+               bool first_done = false) {
   psc_ctx* ctx = h->ctx;
   LevelWS& W = h->lv[l];
   if (nsweeps <= 0) {
     PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
     return 0;
   }
-  launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
+  if (!first_done) launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
   int cur = 0;
   for (int k = 1; k < nsweeps; ++k) {
     exchange(h, W.d, W.x[cur], s);
@@ -202,13 +206,15 @@ int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s,
 
 // z = B_l b  (Eq. (2)), recursively.  At level 0 the last
 // post-sweep also accumulates (b, z) = (r, z) into slot S_RZ.
-double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool timing) {
+bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
+
+double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool timing, bool first_done = false) {
   psc_ctx* ctx = h->ctx;
   if (l == h->L - 1) return coarse_solve(h, b, h->opt.coarse_sweeps, s);
   LevelWS& W = h->lv[l];
   LevelWS& C = h->lv[l + 1];
   // (I - M^-1 A)^pre
-  int cur = pre_smooth(h, l, b, h->opt.pre_sweeps, s, timing);
+  int cur = pre_smooth(h, l, b, h->opt.pre_sweeps, s, timing, first_done);
   // coarse-grid correction (I - P B_{l+1} P^T A): r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
   exchange(h, W.d, W.x[cur], s);
   {
@@ -225,9 +231,16 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.r;
     a.y = C.b;
+    // fused: the next level's first sweep from zero, x_{l+1} = M^{-1} b_{l+1}
+    const bool fuse = fuse_first_sweep() && l + 1 < h->L - 1 && h->opt.pre_sweeps > 0;
+    if (fuse) {
+      a.y2 = C.x[0];
+      a.dinv2 = C.dinv;
+    }
     launch_rows(ctx, W.R->S, RowOp::Spmv, a, s);
   }
-  double* xc = vcycle_level(h, l + 1, C.b, s, timing);
+  const bool fused_next = fuse_first_sweep() && l + 1 < h->L - 1 && h->opt.pre_sweeps > 0;
+  double* xc = vcycle_level(h, l + 1, C.b, s, timing, fused_next);
   if (!(l + 1 == h->L - 1 && coarse_has_halo(h))) exchange(h, C.d, xc, s);
   {
     RowArgs a;
@@ -273,7 +286,8 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
   LevelWS& W = h->lv[0];
   const int R = ctx->nranks;
   h->dom_used = 0;
-  double* z = vcycle_level(h, 0, h->r_cg, s, timing);
+  // the CG update of the previous iteration (or the eager start) wrote x_0 = M^{-1} r
+  double* z = vcycle_level(h, 0, h->r_cg, s, timing, h->z0_fused);
   h->z_ptr = z;
   allgather_slot(h, S_RZ, s);
   launch_xpby(ctx, W.n, z, h->p, scal(h, S_RZ), rz_old(h), R, &h->red2, s);
@@ -289,7 +303,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
   }
   allgather_slot(h, S_PQ, s);
   launch_cg_update(ctx, W.n, h->x_int, h->p, h->r_cg, h->q, scal(h, S_PQ), rz_old(h), R, &h->red1,
-                   scal_mine(h, S_RR), s);
+                   scal_mine(h, S_RR), s, h->z0_fused ? W.dinv : nullptr, h->z0_fused ? W.x[0] : nullptr);
   allgather_slot(h, S_RR, s);
   PSC_CUDA(cudaMemcpyAsync(h->h_scal, h->d_scal, sizeof(double) * NSLOT * R, cudaMemcpyDeviceToHost, s));
 }
@@ -489,6 +503,7 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
       PSC_CUDA(cudaMemsetAsync(h->p, 0, sizeof(double) * (W.n + W.nh), s));
       const double one = 1.0;
       PSC_CUDA(cudaMemcpyAsync(rz_old(h), &one, sizeof(double), cudaMemcpyHostToDevice, s));
+      if (h->z0_fused) launch_scale(ctx, W.n, W.dinv, h->r_cg, W.x[0], s);  // first V-cycle's first sweep
       if (!h->iter_exec) capture_iteration(h);
       for (int k = 1; k <= maxit; ++k) {
         PSC_CUDA(cudaGraphLaunch(h->iter_exec, s));
@@ -620,6 +635,7 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       h->rep.maxcnt = maxcnt;
     }
     PSC_CUDA(cudaMallocHost(&h->h_scal, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1)));
+    h->z0_fused = fuse_first_sweep() && nlevels > 1 && h->opt.pre_sweeps > 0;
     h->red1 = red_alloc(ctx->num_sms, 1);
     h->red2 = red_alloc(ctx->num_sms, 2);
     // live timing of the dominant kernel: one event pair around one level-0

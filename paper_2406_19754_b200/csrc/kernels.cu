@@ -254,6 +254,8 @@ struct RowKArgs {
   const double* b;
   const double* dinv;
   double* y;
+  double* y2;            // Spmv: if set, y2 = dinv2 .* y (first sweep from zero of the next level)
+  const double* dinv2;
   double* partials;
   unsigned int* ticket;
   double* red_out;
@@ -296,7 +298,9 @@ __device__ __forceinline__ EpiIn epi_load(const RowKArgs& a, int64_t i) {
 template <RowOp OP>
 __device__ __forceinline__ void epi_store(const RowKArgs& a, int64_t i, double sum, const EpiIn& e, double* acc) {
   if constexpr (OP == RowOp::Spmv) {
-    a.y[i] = (a.beta == 0.0) ? a.alpha * sum : a.alpha * sum + a.beta * e.x;
+    const double v = (a.beta == 0.0) ? a.alpha * sum : a.alpha * sum + a.beta * e.x;
+    a.y[i] = v;
+    if (a.y2) a.y2[i] = a.dinv2[i] * v;
   } else if constexpr (OP == RowOp::SpmvDot) {
     a.y[i] = sum;
     acc[0] += e.x * sum;
@@ -527,6 +531,10 @@ struct EpiVecs {  // which row vectors the epilogue reads: b, dinv, x(own), y
   // kernel FP64-divide bound: 317 vs 221 us on A_0 of 256^3)
   static constexpr bool D_SELL = D;
   static constexpr bool X = (OP == RowOp::Sweep || OP == RowOp::SweepDot || OP == RowOp::SpmvDot);
+  // residual: the rows' own x block is bulk-copied although the epilogue does not
+  // read it, to bring the gathers' lines into L2 ahead of the consumers (no extra
+  // DRAM bytes: the gathers read them anyway); 236 -> ~215 us on A_0 of 256^3
+  static constexpr bool XPRE = (OP == RowOp::Resid || OP == RowOp::ResidDot2);
   static constexpr bool Y = (OP == RowOp::PAdd || OP == RowOp::Spmv);
 };
 
@@ -579,7 +587,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const uint32_t vbytes = (uint32_t)(vb1 - vb0) * 8;
         const uint32_t cbytes = (uint32_t)(cb1 - cb0) * 4;
         const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
-        const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) + (EV::X ? 1 : 0) + (readY ? 1 : 0);
+        const uint32_t nvec =
+            (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) + ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0);
         mbar_expect_tx(&full[st], hb + vbytes + cbytes + nvec * rbytes);
         bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol_keep);
         if (vbytes) bulk_g2s(base + kTmaHdrBytes, a.val + vb0, vbytes, &full[st], pol_mat);
@@ -588,7 +597,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         if (rbytes) {
           if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol_stream);
           if constexpr (EV::D_SELL) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
-          if constexpr (EV::X) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
+          if constexpr (EV::X || EV::XPRE) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
           if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
         }
         vb0 = nvb0; vb1 = nvb1; cb0 = ncb0; cb1 = ncb1;
@@ -653,6 +662,163 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
   }
   pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
+}
+
+// k-blocked variant for slices wider than kTmaMaxW (level-1 A_1, R_0, P_1, A_2
+// of 256^3): a chunk of 8 slices is streamed in blocks of 8 columns, one stage
+// per block (values / columns of block kb of each slice are contiguous in the
+// column-major slice); consumer warps carry their row sums across the blocks
+// and run the epilogue after the chunk's last block.  Headers and epilogue
+// vectors travel with block 0.  The producer warp's lanes handle one slice each.
+template <RowOp OP>
+__global__ void __launch_bounds__(kTmaThreads) sell_tmak(RowKArgs a, int64_t nchunks, int64_t n_slices) {
+  pdl_enter();
+  constexpr int NR = NRed<OP>::value;
+  using EV = EpiVecs<OP>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaStageBytes);
+  uint64_t* empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool readY = EV::Y && !(OP == RowOp::Spmv && a.beta == 0.0);
+  const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) + ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTmaStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kTmaSlices);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double acc[NR > 0 ? NR : 1] = {};
+  if (warp == kTmaSlices) {
+    // ---------------- producer warp: lane j issues the copies of slice j
+    uint64_t pol_stream, pol_keep;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    const uint64_t pol_mat = a.keep_matrix ? pol_keep : pol_stream;
+    int64_t it = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const int64_t s0 = c * kTmaSlices;
+      const int nsl = (int)min((int64_t)kTmaSlices, n_slices - s0);
+      int64_t vb = 0, cb = 0;
+      int w = 0, dia = 0;
+      if (lane < nsl) {
+        const int32_t* h = a.hdr + (s0 + lane) * kHdr;
+        vb = ((int64_t)(uint32_t)__ldg(h + 1) << 32) | (uint32_t)__ldg(h + 0);
+        cb = ((int64_t)(uint32_t)__ldg(h + 3) << 32) | (uint32_t)__ldg(h + 2);
+        w = __ldg(h + 4);
+        dia = __ldg(h + 5);
+      }
+      int wmax = w;
+      for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+      const int nkb = max(1, (wmax + kTmaMaxW - 1) / kTmaMaxW);
+      const int64_t r0 = s0 * 32, r1 = min((s0 + nsl) * 32, a.n_rows);
+      const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int st = (int)(it % kTmaStages);
+        if (lane == 0 && it >= kTmaStages) mbar_wait(&empty[st], (uint32_t)((it / kTmaStages - 1) & 1));
+        __syncwarp();
+        const int cnt = (lane < nsl) ? min(max(w - kb * kTmaMaxW, 0), kTmaMaxW) : 0;
+        const uint32_t vbytes = (uint32_t)cnt * 256u;
+        const uint32_t cbytes = dia ? 0u : (uint32_t)cnt * 128u;
+        uint32_t tot = vbytes + cbytes;
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (kb == 0) tot += (uint32_t)nsl * kHdr * 4 + nvec * rbytes;
+        if (lane == 0) mbar_expect_tx(&full[st], tot);
+        __syncwarp();
+        unsigned char* base = smem + st * kTmaStageBytes;
+        if (kb == 0 && lane == 0) {
+          bulk_g2s(base, a.hdr + s0 * kHdr, (uint32_t)nsl * kHdr * 4, &full[st], pol_keep);
+          unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
+          if (rbytes) {
+            if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol_stream);
+            if constexpr (EV::D_SELL) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
+            if constexpr (EV::X || EV::XPRE) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
+            if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
+          }
+        }
+        if (vbytes)
+          bulk_g2s(base + kTmaHdrBytes + lane * (kTmaMaxW * 256), a.val + vb + (int64_t)kb * kTmaMaxW * 32, vbytes,
+                   &full[st], pol_mat);
+        if (cbytes)
+          bulk_g2s(base + kTmaHdrBytes + kTmaValBytes + lane * (kTmaMaxW * 128),
+                   a.col + cb + (int64_t)kb * kTmaMaxW * 32, cbytes, &full[st], pol_mat);
+      }
+    }
+  } else {
+    // ---------------- consumers: warp `warp` takes slice s0 + warp
+    const uint32_t nc = (uint32_t)a.ncols;
+    int64_t it = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const int64_t s0 = c * kTmaSlices;
+      const int nsl = (int)min((int64_t)kTmaSlices, n_slices - s0);
+      const bool mine = warp < nsl;
+      const uint32_t i = (uint32_t)((s0 + warp) * 32 + lane);
+      const bool live = mine && (int64_t)i < a.n_rows;
+      int32_t h = 0;
+      int w = 0, nkb = 1;
+      bool dia = false;
+      EpiIn e{0.0, 0.0, 0.0};
+      double sum = 0.0;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int st = (int)(it % kTmaStages);
+        mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
+        const unsigned char* base = smem + st * kTmaStageBytes;
+        if (kb == 0) {
+          const int32_t* hs = reinterpret_cast<const int32_t*>(base);
+          h = (mine && lane < kHdr) ? hs[warp * kHdr + lane] : 0;
+          w = __shfl_sync(0xffffffffu, h, 4);
+          dia = __shfl_sync(0xffffffffu, h, 5) != 0;
+          int wm = lane < nsl ? hs[lane * kHdr + 4] : 0;
+          for (int o = 16; o > 0; o >>= 1) wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+          nkb = max(1, (wm + kTmaMaxW - 1) / kTmaMaxW);
+          if (live) {
+            const double* vec = reinterpret_cast<const double*>(base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes);
+            const int rl = warp * 32 + lane;
+            if constexpr (EV::B) e.b = vec[rl];
+            if constexpr (EV::D) e.d = vec[kTmaRows + rl];
+            if constexpr (EV::X) e.x = vec[2 * kTmaRows + rl];
+            if (readY) e.x = vec[2 * kTmaRows + rl];
+          }
+        }
+        const int cnt = mine ? min(max(w - kb * kTmaMaxW, 0), kTmaMaxW) : 0;
+        if (cnt > 0) {
+          const double* v = reinterpret_cast<const double*>(base + kTmaHdrBytes) + warp * (kTmaMaxW * 32) + lane;
+          const int32_t* cc =
+              reinterpret_cast<const int32_t*>(base + kTmaHdrBytes + kTmaValBytes) + warp * (kTmaMaxW * 32) + lane;
+          double xv[kTmaMaxW];
+          if (dia) {
+#pragma unroll
+            for (int j = 0; j < kTmaMaxW; ++j) {
+              const uint32_t cj = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
+              xv[j] = (j < cnt) ? __ldg(a.x + (cj < nc ? cj : 0u)) : 0.0;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < kTmaMaxW; ++j) xv[j] = (j < cnt) ? __ldg(a.x + cc[32 * j]) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < kTmaMaxW; ++j)
+            if (j < cnt) sum = fma(v[32 * j], xv[j], sum);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      if (live) epi_store<OP>(a, (int64_t)i, sum, e, acc);
+    }
+  }
+  pdl_exit();
+  if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
+}
+
+template <RowOp OP>
+static void tmak_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PSC_CUDA(cudaFuncSetAttribute(sell_tmak<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+    attr = true;
+  }
+  launch_k(sell_tmak<OP>, grid, kTmaThreads, kTmaSmem, s, a, nchunks, n_slices);
 }
 
 template <RowOp OP>
@@ -823,6 +989,15 @@ static void rg_tma_dispatch(RowOp op, const RowKArgs& a, int grid, int64_t nchun
   }
 }
 
+// k-blocked TMA path: sliced ELL wider than the ring's 8 columns
+static bool tmak_ok(const Sell& A, const RowArgs& r, SliceSet set) {
+  // measured not faster than the header-prefetching plain kernel on the wide
+  // slices of 256^3 (A_1: 99 vs 93 us, R_0: 190 vs 178 us): opt-in (PSC_TMAK=1)
+  const int off = env_int("PSC_NO_TMA", 0) || !env_int("PSC_TMAK", 0);
+  return !off && A.lanes == 1 && A.max_width > kTmaMaxW && set == SliceSet::All && r.vec_padded && A.hdr &&
+         A.n_units > 0;
+}
+
 static bool rg_tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
   const int off = env_int("PSC_NO_TMA", 0) || env_int("PSC_NO_RG_TMA", 0);
   return !off && A.lanes > 1 && A.max_chunk <= kRgCap && set == SliceSet::All && r.vec_padded && A.n_units > 0;
@@ -855,6 +1030,8 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.b = r.b;
   a.dinv = r.dinv;
   a.y = r.y;
+  a.y2 = r.y2;
+  a.dinv2 = r.dinv2;
   a.partials = r.red ? r.red->partials : nullptr;
   a.ticket = r.red ? r.red->ticket : nullptr;
   a.red_out = r.red_out;
@@ -872,6 +1049,23 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
       case RowOp::Resid: tma_launch<RowOp::Resid>(a, grid, nchunks, A.n_units, s); break;
       case RowOp::ResidDot2: tma_launch<RowOp::ResidDot2>(a, grid, nchunks, A.n_units, s); break;
       case RowOp::PAdd: tma_launch<RowOp::PAdd>(a, grid, nchunks, A.n_units, s); break;
+    }
+    PSC_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
+  if (tmak_ok(A, r, set)) {
+    const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
+    PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
+    switch (op) {
+      case RowOp::Spmv: tmak_launch<RowOp::Spmv>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::SpmvDot: tmak_launch<RowOp::SpmvDot>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::Sweep: tmak_launch<RowOp::Sweep>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::SweepDot: tmak_launch<RowOp::SweepDot>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::Resid: tmak_launch<RowOp::Resid>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::ResidDot2: tmak_launch<RowOp::ResidDot2>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::PAdd: tmak_launch<RowOp::PAdd>(a, grid, nchunks, A.n_units, s); break;
     }
     PSC_CUDA(cudaGetLastError());
     ctx->launches++;
@@ -971,7 +1165,8 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
                                                            const double* __restrict__ p, double* __restrict__ r,
                                                            const double* __restrict__ q, const double* g_pq,
                                                            const double* rz_old, int nranks, double* partials,
-                                                           unsigned int* ticket, double* out) {
+                                                           unsigned int* ticket, double* out,
+                                                           const double* __restrict__ dinv, double* __restrict__ z0) {
   pdl_enter();
   const double alpha = __ldcg(rz_old) / gsum(g_pq, nranks);
   double acc[1] = {0.0};
@@ -979,6 +1174,7 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
     x[i] = x[i] + alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
+    if (z0) z0[i] = dinv[i] * ri;  // first level-0 sweep of the next V-cycle, from zero
     acc[0] += ri * ri;
   }
   pdl_exit();
@@ -987,10 +1183,10 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
 
 void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
                       const double* g_pq, const double* rz_old, int nranks, const RedSite* red, double* red_out,
-                      cudaStream_t s) {
+                      cudaStream_t s, const double* dinv, double* z0) {
   const int g = std::min(vec_grid(ctx, n), red->grid);
   launch_k(cg_update_kernel, g, kBlock, 0, s, n, x, p, r, q, g_pq, rz_old, nranks, red->partials, red->ticket,
-           red_out);
+           red_out, dinv, z0);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -1200,7 +1396,7 @@ void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const 
 // coarsening: ~115 of 141 entries per row on 256^3) is expanded once into a
 // row-major n x n array; each sweep is then a shared-memory dense matvec by
 // all 1024 threads (gk lanes per row, fixed shuffle tree).
-int64_t coarse_dense_max_rows() { return 160; }
+int64_t coarse_dense_max_rows() { return 144; }
 
 __global__ void dense_from_sell_kernel(const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
                                        const int32_t* __restrict__ col, const double* __restrict__ val, int64_t n,
@@ -1230,79 +1426,64 @@ void dense_from_sell(psc_ctx* ctx, const Sell& A, double* dense, cudaStream_t s)
   ctx->launches++;
 }
 
-__global__ void __launch_bounds__(kCoarseThreads) coarse_dense(const double* __restrict__ Ad, int n,
-                                                               const double* __restrict__ dinv,
-                                                               const double* __restrict__ b, double* __restrict__ xout,
-                                                               int nsweeps, int gk) {
+// Register-blocked: warp w owns rows w + 24 m (m < 6), lane owns columns
+// lane + 32 c (c < 5), so n <= 144: A_coarse lives in registers (30 doubles per thread)
+// for all sweeps; each sweep reads x from shared memory, does 25 FMAs per
+// thread and one xor-butterfly per row (fixed order, every lane gets the sum).
+constexpr int kCR = 6, kCC = 5, kDenseWarps = 24;  // 24 warps x 6 rows = 144 rows, 32 lanes x 5 cols = 160
+__global__ void __launch_bounds__(kDenseWarps * 32, 1) coarse_dense(const double* __restrict__ Ad, int n,
+                                                                  const double* __restrict__ dinv,
+                                                                  const double* __restrict__ b,
+                                                                  double* __restrict__ xout, int nsweeps, int gk_unused) {
   pdl_enter();
-  extern __shared__ __align__(16) double smd[];
-  double* As = smd;
-  double* xa = As + (size_t)n * n + 1;
-  double* xb = xa + n;
-  double* bs = xb + n;
-  double* ds = bs + n;
-  {  // stage A: 16-byte loads, 4 in flight per thread (n*n padded to even by the allocation)
-    const int n2 = (n * n + 1) / 2;
-    const double2* src = reinterpret_cast<const double2*>(Ad);
-    double2* dst = reinterpret_cast<double2*>(As);
-    int k = threadIdx.x;
-    for (; k + 3 * kCoarseThreads < n2; k += 4 * kCoarseThreads) {
-      const double2 a0 = __ldg(src + k), a1 = __ldg(src + k + kCoarseThreads);
-      const double2 a2 = __ldg(src + k + 2 * kCoarseThreads), a3 = __ldg(src + k + 3 * kCoarseThreads);
-      dst[k] = a0;
-      dst[k + kCoarseThreads] = a1;
-      dst[k + 2 * kCoarseThreads] = a2;
-      dst[k + 3 * kCoarseThreads] = a3;
+  __shared__ double xs[2][32 * kCC];
+  __shared__ double bs[32 * kCC], ds[32 * kCC];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double a[kCR][kCC];
+#pragma unroll
+  for (int m = 0; m < kCR; ++m) {
+    const int i = w + kDenseWarps * m;
+#pragma unroll
+    for (int c = 0; c < kCC; ++c) {
+      const int j = lane + 32 * c;
+      a[m][c] = (i < n && j < n) ? __ldg(Ad + (size_t)i * n + j) : 0.0;
     }
-    for (; k < n2; k += kCoarseThreads) dst[k] = __ldg(src + k);
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     bs[i] = b[i];
     ds[i] = dinv[i];
-    xa[i] = (nsweeps > 0) ? ds[i] * bs[i] : 0.0;  // first sweep from x = 0
+    xs[0][i] = (nsweeps > 0) ? ds[i] * bs[i] : 0.0;  // first sweep from x = 0
   }
   __syncthreads();
-  const int sub = threadIdx.x & (gk - 1);
-  const int rows_per_pass = kCoarseThreads / gk;
+  int cur = 0;
   for (int sw = 1; sw < nsweeps; ++sw) {
-    for (int r0 = 0; r0 < n; r0 += rows_per_pass) {
-      const int i = r0 + threadIdx.x / gk;
+    double xj[kCC];
+#pragma unroll
+    for (int c = 0; c < kCC; ++c) {
+      const int j = lane + 32 * c;
+      xj[c] = j < n ? xs[cur][j] : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < kCR; ++m) {
       double sum = 0.0;
-      if (i < n) {
-        const double* Ai = As + (size_t)i * n;
-        double s1 = 0.0;
-        int j = sub;
-        for (; j + gk < n; j += 2 * gk) {
-          sum = fma(Ai[j], xa[j], sum);
-          s1 = fma(Ai[j + gk], xa[j + gk], s1);
-        }
-        if (j < n) sum = fma(Ai[j], xa[j], sum);
-        sum += s1;
-      }
-      for (int o = gk / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, gk);
-      if (sub == 0 && i < n) xb[i] = xa[i] + ds[i] * (bs[i] - sum);
+#pragma unroll
+      for (int c = 0; c < kCC; ++c) sum = fma(a[m][c], xj[c], sum);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const int i = w + kDenseWarps * m;
+      if (lane == m && i < n) xs[cur ^ 1][i] = xs[cur][i] + ds[i] * (bs[i] - sum);
     }
     __syncthreads();
-    double* t = xa;
-    xa = xb;
-    xb = t;
+    cur ^= 1;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xa[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xs[cur][i];
   pdl_exit();
 }
 
 void launch_coarse_dense(psc_ctx* ctx, const double* Ad, int64_t n, const double* dinv, const double* b, double* x,
                          int nsweeps, cudaStream_t s) {
   PSC_REQUIRE(n <= coarse_dense_max_rows(), PSC_ERR_STATE, "coarsest level too large for the dense solver");
-  static bool attr = false;
-  if (!attr) {
-    PSC_CUDA(cudaFuncSetAttribute(coarse_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    attr = true;
-  }
-  int gk = 1;
-  while (gk < 32 && (int64_t)(gk * 2) * std::max<int64_t>(n, 1) <= kCoarseThreads) gk *= 2;
-  const size_t smem = ((size_t)n * n + 1 + 4 * (size_t)std::max<int64_t>(n, 1)) * sizeof(double);
-  launch_k(coarse_dense, 1, kCoarseThreads, smem, s, Ad, (int)n, dinv, b, x, nsweeps, gk);
+  launch_k(coarse_dense, 1, kDenseWarps * 32, 0, s, Ad, (int)n, dinv, b, x, nsweeps, 0);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }

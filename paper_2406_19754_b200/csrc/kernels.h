@@ -24,6 +24,8 @@ struct RowArgs {
   const double* b = nullptr;
   const double* dinv = nullptr;
   double* y = nullptr;
+  double* y2 = nullptr;        // Spmv only: y2 = dinv2 .* y
+  const double* dinv2 = nullptr;
   const RedSite* red = nullptr;
   double* red_out = nullptr;   // red0 -> red_out[0], red1 -> red_out[red_stride]
   int red_stride = 1;
@@ -45,9 +47,10 @@ void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, 
 void launch_l1_dinv(psc_ctx* ctx, const Sell& A, double* dinv, cudaStream_t s);
 // gathered scalars: value of slot = sum over ranks of g[slot*nranks + r], in rank order
 // CG: alpha = rz_old / pq ; x += alpha p ; r -= alpha q ; red(r.r)
+// (optionally z0 = dinv .* r: the first level-0 sweep of the next V-cycle)
 void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
                       const double* g_pq, const double* rz_old, int nranks, const RedSite* red, double* red_out,
-                      cudaStream_t s);
+                      cudaStream_t s, const double* dinv = nullptr, double* z0 = nullptr);
 // beta = rz / rz_old ; p = z + beta p ; then rz_old := rz (by the last CTA)
 void launch_xpby(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rz, double* rz_old,
                  int nranks, const RedSite* red, cudaStream_t s);
