@@ -218,6 +218,10 @@ int psc_pcg_solve(psc_hier* h, const double* b_dev, double* x_dev, double tol, i
 int psc_pcg_solve_host(psc_hier* h, const double* b_host, double* x_host, double tol, int maxit,
                        double* res_hist_host, psc_stats* st);
 
+/* [collective] Timing hook: *us_per_exchange = device time of one halo exchange of a
+ * level-`level` vector, averaged over `reps` back-to-back exchanges (eager launches). */
+int psc_hier_exchange_bench(psc_hier* h, int level, int reps, double* us_per_exchange);
+
 void psc_hier_destroy(psc_hier* h);
 
 #ifdef __cplusplus

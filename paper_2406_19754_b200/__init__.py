@@ -79,6 +79,7 @@ _sig("psc_hier_dinv", _i32, [_vp, _i32, _vp])
 _sig("psc_hier_smooth", _i32, [_vp, _i32, _vp, _vp, _i32])
 _sig("psc_pcg_solve", _i32, [_vp, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
 _sig("psc_pcg_solve_host", _i32, [_vp, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
+_sig("psc_hier_exchange_bench", _i32, [_vp, _i32, _i32, _P(_f64)])
 _sig("psc_hier_destroy", None, [_vp])
 
 
@@ -314,6 +315,12 @@ class Hierarchy:
                                      hist.ctypes.data, ctypes.byref(st))
         _check(rc, self.ctx, ok=(PSC_OK, PSC_NOT_CONVERGED))
         return rc, st.as_dict(), hist[: st.iters + 1]
+
+    def exchange_bench(self, level, reps=200):
+        """Device microseconds per halo exchange of a level vector (collective)."""
+        us = _f64()
+        _check(_lib.psc_hier_exchange_bench(self.handle, level, reps, ctypes.byref(us)), self.ctx)
+        return us.value
 
     def close(self):
         if self.handle:

@@ -382,8 +382,8 @@ int psc_mat_create_csr(psc_ctx* ctx, psc_desc* rows, psc_desc* cols, int64_t n_l
     PSC_CUDA(cudaMemcpy(m->d_colg, col_global, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice));
     PSC_CUDA(cudaMemcpy(m->d_valcsr, val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
   }
-  // small matrices keep a host copy (coarsest-level replication)
-  if (nnz <= (int64_t)4 << 20) {
+  // small matrices keep a host copy (replicated coarse levels)
+  if (nnz <= (int64_t)8 << 20) {
     m->h_rowptr.assign(row_ptr, row_ptr + n_local_rows + 1);
     m->h_colg.assign(col_global, col_global + nnz);
     m->h_val.assign(val, val + nnz);

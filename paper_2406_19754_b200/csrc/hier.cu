@@ -23,27 +23,34 @@ enum Slot { S_PQ = 0, S_RR = 1, S_RZ = 2, S_BB = 3, NSLOT = 4 };
 
 struct LevelWS {
   psc_mat *A = nullptr, *P = nullptr, *R = nullptr;
-  psc_desc* d = nullptr;
+  psc_desc* d = nullptr;      // nullptr: replicated level (no halo, no exchange)
   int64_t n = 0, nh = 0;
   double* dinv = nullptr;     // n
   double* x[2] = {nullptr, nullptr};  // n + nh
   double* r = nullptr;        // n + nh
   double* b = nullptr;        // n (level >= 1: R_{l-1} r_{l-1})
+  // coarsest-level solver data (last level of a level array)
+  double* dense = nullptr;    // n x n row-major copy of A when n <= coarse_dense_max_rows()
+  bool one_cta = false;       // sparse one-CTA solver applies
 };
 
-// replicated coarsest level (nranks > 1): every rank holds the whole A_coarse
+// Replicated suffix (nranks > 1): levels first..L-1 are held whole on every
+// rank.  The V-cycle gathers b at level `first` once (all-gather), runs the
+// rest of the cycle redundantly with no halo exchange (row results are the same
+// arithmetic as the distributed sweeps), and scatters x to the owned+halo slots
+// of level `first`.  The coarse levels are latency-bound (one exchange costs
+// ~10 us, about a whole coarse kernel), so this removes ~2 x 10 exchanges per
+// V-cycle at the price of kernels over a few thousand more rows.
 struct Replica {
   bool on = false;
-  int64_t N = 0, maxcnt = 0;
-  Sell S;                       // global rows, columns = global indices
-  double* dense = nullptr;      // N x N when N <= coarse_dense_max_rows()
-  double* dinv = nullptr;       // N
+  int first = -1;
+  int64_t N = 0, maxcnt = 0;    // global rows of level `first`; all-gather block per rank
+  std::vector<LevelWS> lv;      // replicated levels first..L-1 (global numbering, internal matrices)
+  std::vector<psc_mat*> mats;   // owned internal matrices
   double* sendbuf = nullptr;    // maxcnt
-  double* gbuf = nullptr;       // nranks * maxcnt
+  double* gbuf = nullptr;       // nranks * maxcnt (in the arena: peers write it)
   int64_t* map_full = nullptr;  // N: global g -> position in gbuf
-  double* bfull = nullptr;      // N
-  double* xfull = nullptr;      // N
-  int64_t* map_loc = nullptr;   // n + nh: local slot -> global index
+  int64_t* map_loc = nullptr;   // n + nh of level `first`: local slot -> global index
 };
 
 }  // namespace
@@ -54,9 +61,7 @@ struct psc_hier_s {
   psc_cycle_opts opt{4, 4, 30};
   std::vector<LevelWS> lv;
   Replica rep;
-  bool coarse_one_cta = false;
   bool z0_fused = false;  // CG update writes the first level-0 sweep of the next V-cycle
-  double* coarse_dense = nullptr;  // dense copy of A_coarse (single rank, small coarsest level)
   // CG state (level 0)
   double* x_int = nullptr;  // n0 + nh0
   double* r_cg = nullptr;   // n0
@@ -117,36 +122,42 @@ void exchange(psc_hier* h, psc_desc* d, double* x, cudaStream_t s) {
   halo_exchange(ctx, d, x, s);
 }
 
-// ------------------------------------------------------------ coarsest level
-// B_ell = `nsweeps` l1-Jacobi sweeps from zero.  Returns the
-// owned+halo iterate of the coarsest index space.
-double* coarse_solve(psc_hier* h, const double* b, int nsweeps, cudaStream_t s) {
+// Halo exchange of a.x before the row kernel `a` is launched: folded into that
+// kernel's prologue when the NVLink path is on (no separate launch), else a
+// standalone exchange.  PSC_NO_FUSED_EXCHANGE=1 keeps the standalone kernel.
+void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
   psc_ctx* ctx = h->ctx;
-  LevelWS& W = h->lv[h->L - 1];
-  if (h->rep.on) {
-    Replica& R = h->rep;
-    // gather b_coarse on every rank, solve the whole coarse system redundantly
-    // (bit-identical per row to the distributed sweeps), scatter to owned+halo.
-    if (!p2p_allgather(ctx, h->p2p, b, W.n, R.gbuf, s)) {
-      if (W.n) PSC_CUDA(cudaMemcpyAsync(R.sendbuf, b, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
-      PSC_NCCL(ncclAllGather(R.sendbuf, R.gbuf, R.maxcnt, ncclDouble, ctx->comm, s));
-      ctx->collectives++;
-    }
-    launch_gather(ctx, R.N, R.map_full, R.gbuf, R.bfull, s);
-    if (R.dense) launch_coarse_dense(ctx, R.dense, R.N, R.dinv, R.bfull, R.xfull, nsweeps, s);
-    else launch_coarse_solve(ctx, R.S, R.dinv, R.bfull, R.xfull, nsweeps, s);
-    launch_gather(ctx, W.n + W.nh, R.map_loc, R.xfull, W.x[0], s);
+  if (ctx->nranks == 1 || !d) return;
+  // TIMING EXPERIMENTS ONLY (wrong results): PSC_DEBUG_SKIP_HALO=1 skips halo exchanges
+  static const bool skip = getenv("PSC_DEBUG_SKIP_HALO") != nullptr;
+  static const int skip_from = getenv("PSC_DEBUG_SKIP_HALO_FROM") ? atoi(getenv("PSC_DEBUG_SKIP_HALO_FROM")) : 1 << 30;
+  if (skip) return;
+  for (int l = skip_from; l < h->L; ++l)
+    if (h->lv[l].d == d) return;
+  // measured slower than the standalone exchange kernel on 2 B200 (5.51 vs 5.40
+  // ms per iteration at 256^3/GPU): opt-in with PSC_FUSED_EXCHANGE=1
+  static const bool nofuse = getenv("PSC_FUSED_EXCHANGE") == nullptr;
+  // TIMING EXPERIMENTS ONLY: PSC_DEBUG_DOUBLE_HALO=1 adds a second, standalone exchange
+  static const bool twice = getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr;
+  if (twice) exchange(h, d, const_cast<double*>(a.x), s);
+  if (!nofuse && p2p_fused(ctx, h->p2p, d, a.x, a.ex)) return;
+  exchange(h, d, const_cast<double*>(a.x), s);
+}
+
+// ------------------------------------------------------------ coarsest level
+// B_ell = `nsweeps` l1-Jacobi sweeps from zero on the last
+// level of a level array.  Returns its iterate.
+double* coarse_solve(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream_t s) {
+  psc_ctx* ctx = h->ctx;
+  if (W.dense) {
+    launch_coarse_dense(ctx, W.dense, W.n, W.dinv, b, W.x[0], nsweeps, s);
     return W.x[0];
   }
-  if (h->coarse_dense) {
-    launch_coarse_dense(ctx, h->coarse_dense, W.n, W.dinv, b, W.x[0], nsweeps, s);
-    return W.x[0];
-  }
-  if (h->coarse_one_cta) {
+  if (W.one_cta) {
     launch_coarse_solve(ctx, W.A->S, W.dinv, b, W.x[0], nsweeps, s);
     return W.x[0];
   }
-  // general path: distributed sweeps, one halo exchange each
+  // general path: sweeps, one halo exchange each when distributed
   int cur = 0;
   if (nsweeps <= 0) {
     PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
@@ -154,30 +165,27 @@ double* coarse_solve(psc_hier* h, const double* b, int nsweeps, cudaStream_t s) 
   }
   launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
   for (int k = 1; k < nsweeps; ++k) {
-    exchange(h, W.d, W.x[cur], s);
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
     a.b = b;
     a.dinv = W.dinv;
     a.y = W.x[cur ^ 1];
+    prep(h, W.d, a, s);
     launch_rows(ctx, W.A->S, RowOp::Sweep, a, s);
     cur ^= 1;
   }
   return W.x[cur];
 }
 
-bool coarse_has_halo(psc_hier* h) { return h->rep.on; }
-
-// nsweeps l1-Jacobi sweeps from zero at level l < L-1 (pre-smoothing: the
-// rightmost factor of Eq. (2) applied `pre` times).  The first sweep is
-// x = M^{-1} b exactly.  Returns the index of the buffer holding x.
+// nsweeps l1-Jacobi sweeps from zero on W (pre-smoothing: the rightmost factor
+// of Eq. (2) applied `pre` times).  The first sweep is x = M^{-1} b exactly;
 // first_done: x[0] = M^{-1} b was already written by the kernel that produced b
-// (the restriction, or the CG update at level 0).
-int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s, bool timing,
+// (the restriction, or the CG update at level 0).  Returns the buffer index of x.
+// timing: event pairs around level-0 sweeps (dominant kernel, measured live).
+int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream_t s, bool timing,
                bool first_done = false) {
   psc_ctx* ctx = h->ctx;
-  LevelWS& W = h->lv[l];
   if (nsweeps <= 0) {
     PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
     return 0;
@@ -185,14 +193,14 @@ int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s,
   if (!first_done) launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
   int cur = 0;
   for (int k = 1; k < nsweeps; ++k) {
-    exchange(h, W.d, W.x[cur], s);
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
     a.b = b;
     a.dinv = W.dinv;
     a.y = W.x[cur ^ 1];
-    const bool t = timing && l == 0 && h->dom_used + 2 <= (int)h->ev_dom.size();
+    prep(h, W.d, a, s);
+    const bool t = timing && h->dom_used + 2 <= (int)h->ev_dom.size();
     if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
     launch_rows(ctx, W.A->S, RowOp::Sweep, a, s);
     if (t) {
@@ -204,56 +212,81 @@ int pre_smooth(psc_hier* h, int l, const double* b, int nsweeps, cudaStream_t s,
   return cur;
 }
 
-// z = B_l b  (Eq. (2)), recursively.  At level 0 the last
-// post-sweep also accumulates (b, z) = (r, z) into slot S_RZ.
 bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
 
-double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool timing, bool first_done = false) {
+double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b, cudaStream_t s, bool timing,
+                   bool first_done, bool dist);
+
+// The replicated suffix: gather b of level `first`, cycle on the whole coarse
+// hierarchy, scatter x to the owned+halo slots of level `first`.
+double* replicated_cycle(psc_hier* h, const double* b, cudaStream_t s) {
   psc_ctx* ctx = h->ctx;
-  if (l == h->L - 1) return coarse_solve(h, b, h->opt.coarse_sweeps, s);
-  LevelWS& W = h->lv[l];
-  LevelWS& C = h->lv[l + 1];
+  Replica& R = h->rep;
+  LevelWS& W = h->lv[R.first];
+  if (!p2p_allgather(ctx, h->p2p, b, W.n, R.gbuf, s)) {
+    if (W.n) PSC_CUDA(cudaMemcpyAsync(R.sendbuf, b, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
+    PSC_NCCL(ncclAllGather(R.sendbuf, R.gbuf, R.maxcnt, ncclDouble, ctx->comm, s));
+    ctx->collectives++;
+  }
+  launch_gather(ctx, R.N, R.map_full, R.gbuf, R.lv[0].b, s);
+  double* xf = vcycle_rec(h, R.lv, 0, R.lv[0].b, s, false, false, false);
+  launch_gather(ctx, W.n + W.nh, R.map_loc, xf, W.x[0], s);
+  return W.x[0];
+}
+
+// z = B_l b  (Eq. (2)), recursively over the level array LV (the
+// distributed levels, or the replicated suffix when dist == false).  At level
+// 0 the last post-sweep also accumulates (b, z) = (r, z) into slot S_RZ.
+double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b, cudaStream_t s, bool timing,
+                   bool first_done, bool dist) {
+  psc_ctx* ctx = h->ctx;
+  const int Lend = (int)LV.size();
+  if (dist && h->rep.on && l == h->rep.first) return replicated_cycle(h, b, s);
+  if (l == Lend - 1) return coarse_solve(h, LV[l], b, h->opt.coarse_sweeps, s);
+  LevelWS& W = LV[l];
+  LevelWS& C = LV[l + 1];
+  const bool time_here = timing && dist && l == 0;
+  const bool next_replicated = dist && h->rep.on && l + 1 == h->rep.first;
   // (I - M^-1 A)^pre
-  int cur = pre_smooth(h, l, b, h->opt.pre_sweeps, s, timing, first_done);
+  int cur = pre_smooth(h, W, b, h->opt.pre_sweeps, s, time_here, first_done);
   // coarse-grid correction (I - P B_{l+1} P^T A): r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
-  exchange(h, W.d, W.x[cur], s);
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
     a.b = b;
     a.y = W.r;
+    prep(h, W.d, a, s);
     launch_rows(ctx, W.A->S, RowOp::Resid, a, s);
   }
-  exchange(h, W.d, W.r, s);
+  // fused: the next level's first sweep from zero, x_{l+1} = M^{-1} b_{l+1}
+  const bool fuse = fuse_first_sweep() && l + 1 < Lend - 1 && h->opt.pre_sweeps > 0 && !next_replicated;
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.r;
     a.y = C.b;
-    // fused: the next level's first sweep from zero, x_{l+1} = M^{-1} b_{l+1}
-    const bool fuse = fuse_first_sweep() && l + 1 < h->L - 1 && h->opt.pre_sweeps > 0;
     if (fuse) {
       a.y2 = C.x[0];
       a.dinv2 = C.dinv;
     }
+    prep(h, W.d, a, s);
     launch_rows(ctx, W.R->S, RowOp::Spmv, a, s);
   }
-  const bool fused_next = fuse_first_sweep() && l + 1 < h->L - 1 && h->opt.pre_sweeps > 0;
-  double* xc = vcycle_level(h, l + 1, C.b, s, timing, fused_next);
-  if (!(l + 1 == h->L - 1 && coarse_has_halo(h))) exchange(h, C.d, xc, s);
+  double* xc = vcycle_rec(h, LV, l + 1, C.b, s, timing, fuse, dist);
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = xc;
     a.y = W.x[cur];
+    if (!next_replicated) prep(h, C.d, a, s);  // the replicated cycle filled xc's halo
     launch_rows(ctx, W.P->S, RowOp::PAdd, a, s);
   }
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
   const int post = h->opt.post_sweeps;
+  const bool level0 = dist && l == 0;
   for (int k = 0; k < post; ++k) {
-    exchange(h, W.d, W.x[cur], s);
-    const bool last0 = (l == 0 && k == post - 1);
+    const bool last0 = (level0 && k == post - 1);
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
@@ -264,7 +297,8 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
       a.red = &h->red1;
       a.red_out = scal_mine(h, S_RZ);
     }
-    const bool t = timing && l == 0 && h->dom_used + 2 <= (int)h->ev_dom.size();
+    prep(h, W.d, a, s);
+    const bool t = time_here && h->dom_used + 2 <= (int)h->ev_dom.size();
     if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
     launch_rows(ctx, W.A->S, last0 ? RowOp::SweepDot : RowOp::Sweep, a, s);
     if (t) {
@@ -273,8 +307,12 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
     }
     cur ^= 1;
   }
-  if (l == 0 && post == 0) launch_dot(ctx, W.n, b, W.x[cur], &h->red1, scal_mine(h, S_RZ), s);
+  if (level0 && post == 0) launch_dot(ctx, W.n, b, W.x[cur], &h->red1, scal_mine(h, S_RZ), s);
   return W.x[cur];
+}
+
+double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool timing, bool first_done = false) {
+  return vcycle_rec(h, h->lv, l, b, s, timing, first_done, true);
 }
 
 // One PCG iteration k >= 1 (P:113-117 with B = V-cycle; reading R1):
@@ -291,7 +329,6 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
   h->z_ptr = z;
   allgather_slot(h, S_RZ, s);
   launch_xpby(ctx, W.n, z, h->p, scal(h, S_RZ), rz_old(h), R, &h->red2, s);
-  exchange(h, W.d, h->p, s);
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -299,6 +336,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
     a.y = h->q;
     a.red = &h->red1;
     a.red_out = scal_mine(h, S_PQ);
+    prep(h, W.d, a, s);
     launch_rows(ctx, W.A->S, RowOp::SpmvDot, a, s);
   }
   allgather_slot(h, S_PQ, s);
@@ -336,18 +374,13 @@ double sum_ranks(const double* v, int R) {
   return s;
 }
 
-void build_replica(psc_hier* h) {
-  psc_ctx* ctx = h->ctx;
+// Gather every rank's rows of a distributed matrix (host copies kept at
+// psc_mat_create_csr for small matrices) and build a device layout of the whole
+// matrix with global row and column numbering.
+psc_mat* replicate_matrix(psc_ctx* ctx, psc_mat* A, int64_t n_rows_global, int64_t n_cols_global, bool allow_dia) {
   const int R = ctx->nranks;
-  LevelWS& W = h->lv[h->L - 1];
-  psc_mat* A = W.A;
-  psc_desc* d = W.d;
-  Replica& rp = h->rep;
-  rp.N = d->n_global;
-  if (rp.N > coarse_smem_rows()) return;
-  PSC_REQUIRE((int64_t)A->h_rowptr.size() == A->n_rows + 1, PSC_ERR_STATE, "coarsest matrix has no host copy");
   cudaStream_t s = ctx->stream;
-  // allgather (n_r, nnz_r), then broadcast each rank's rows
+  PSC_REQUIRE((int64_t)A->h_rowptr.size() == A->n_rows + 1, PSC_ERR_STATE, "replicated level matrix has no host copy");
   int64_t* dcnt = dalloc<int64_t>(2 * R + 2);
   int64_t mine[2] = {A->n_rows, A->nnz};
   PSC_CUDA(cudaMemcpy(dcnt + 2 * R, mine, sizeof(mine), cudaMemcpyHostToDevice));
@@ -358,7 +391,7 @@ void build_replica(psc_hier* h) {
   dfree(dcnt);
   int64_t totnnz = 0;
   for (int r = 0; r < R; ++r) totnnz += cnt[2 * r + 1];
-  std::vector<int64_t> rp_all(rp.N + 1, 0), col_all(totnnz);
+  std::vector<int64_t> rp_all(n_rows_global + 1, 0), col_all(totnnz);
   std::vector<double> val_all(totnnz);
   int64_t row0 = 0, nz0 = 0;
   for (int r = 0; r < R; ++r) {
@@ -385,24 +418,92 @@ void build_replica(psc_hier* h) {
     row0 += nr;
     nz0 += nz;
   }
-  PSC_REQUIRE(row0 == rp.N, PSC_ERR_STATE, "coarsest rows do not add up");
-  int64_t* drp = dalloc<int64_t>(rp.N + 1);
+  PSC_REQUIRE(row0 == n_rows_global, PSC_ERR_STATE, "replicated rows do not add up");
+  int64_t* drp = dalloc<int64_t>(n_rows_global + 1);
   int64_t* dcol = dalloc<int64_t>(totnnz);
   double* dval = dvec(totnnz);
-  PSC_CUDA(cudaMemcpy(drp, rp_all.data(), sizeof(int64_t) * (rp.N + 1), cudaMemcpyHostToDevice));
+  PSC_CUDA(cudaMemcpy(drp, rp_all.data(), sizeof(int64_t) * (n_rows_global + 1), cudaMemcpyHostToDevice));
   PSC_CUDA(cudaMemcpy(dcol, col_all.data(), sizeof(int64_t) * totnnz, cudaMemcpyHostToDevice));
   PSC_CUDA(cudaMemcpy(dval, val_all.data(), sizeof(double) * totnnz, cudaMemcpyHostToDevice));
-  sell_from_csr(ctx, rp.N, drp, dcol, dval, totnnz, 0, rp.N, nullptr, 0, rp.S, s, 0, true);
+  psc_mat* m = new psc_mat();
+  m->ctx = ctx;
+  m->n_rows = n_rows_global;
+  m->nnz = totnnz;
+  try {
+    sell_from_csr(ctx, n_rows_global, drp, dcol, dval, totnnz, 0, n_cols_global, nullptr, 0, m->S, s, 0, allow_dia);
+  } catch (...) {
+    dfree(drp);
+    dfree(dcol);
+    dfree(dval);
+    delete m;
+    throw;
+  }
+  m->assembled = true;
   dfree(drp);
   dfree(dcol);
   dfree(dval);
-  rp.dinv = dvec(rp.N);
-  launch_l1_dinv(ctx, rp.S, rp.dinv, s);
-  if (rp.N <= coarse_dense_max_rows() && !getenv("PSC_NO_DENSE_COARSE")) {
-    rp.dense = dvec(rp.N * rp.N + 1);
-    dense_from_sell(ctx, rp.S, rp.dense, s);
+  return m;
+}
+
+// first replicated level: the first level >= 1 whose global size is at most
+// PSC_REPL_ROWS (default 50000); -1 when none (or PSC_REPL_ROWS=0)
+int replica_first(psc_hier* h) {
+  if (h->ctx->nranks == 1 || h->L < 2) return -1;
+  const char* e = getenv("PSC_REPL_ROWS");
+  const int64_t lim = e ? atoll(e) : 50000;
+  auto has_host = [&](int l) {  // every matrix of levels l.. has its host copy on this rank
+    for (int k = l; k < h->L; ++k)
+      for (psc_mat* m : {h->lv[k].A, h->lv[k].P, h->lv[k].R})
+        if (m && (int64_t)m->h_rowptr.size() != m->n_rows + 1) return false;
+    return true;
+  };
+  for (int l = 1; l < h->L; ++l)
+    if (h->lv[l].d->n_global <= lim) return has_host(l) ? l : -1;
+  return (h->lv[h->L - 1].d->n_global <= coarse_smem_rows() && has_host(h->L - 1)) ? h->L - 1 : -1;
+}
+
+void level_coarse_solver(psc_hier* h, LevelWS& W) {
+  W.one_cta = (W.n <= coarse_smem_rows() && W.nh == 0);
+  if (W.n <= coarse_dense_max_rows() && W.nh == 0 && !getenv("PSC_NO_DENSE_COARSE")) {
+    W.dense = dvec(W.n * W.n + 1);
+    dense_from_sell(h->ctx, W.A->S, W.dense, h->ctx->stream);
   }
-  // b gather map: padded allgather buffer (allocated in the arena) -> global index
+}
+
+void build_replica(psc_hier* h, int first) {
+  psc_ctx* ctx = h->ctx;
+  const int R = ctx->nranks;
+  const int L = h->L;
+  Replica& rp = h->rep;
+  cudaStream_t s = ctx->stream;
+  rp.first = first;
+  rp.N = h->lv[first].d->n_global;
+  for (int k = first; k < L; ++k) {
+    LevelWS& D = h->lv[k];
+    LevelWS W;
+    W.n = D.d->n_global;
+    W.A = replicate_matrix(ctx, D.A, W.n, W.n, true);
+    rp.mats.push_back(W.A);
+    if (k + 1 < L) {
+      const int64_t nc = h->lv[k + 1].d->n_global;
+      W.P = replicate_matrix(ctx, D.P, W.n, nc, false);
+      W.R = replicate_matrix(ctx, D.R, nc, W.n, false);
+      rp.mats.push_back(W.P);
+      rp.mats.push_back(W.R);
+    }
+    W.dinv = dvec(W.n);
+    launch_l1_dinv(ctx, W.A->S, W.dinv, s);
+    for (double** b : {&W.x[0], &W.x[1], &W.r, &W.b}) {
+      *b = dvec(W.n);
+      PSC_CUDA(cudaMemsetAsync(*b, 0, sizeof(double) * W.n, s));
+    }
+    if (k == L - 1) level_coarse_solver(h, W);
+    rp.lv.push_back(W);
+  }
+  // b gather map: padded all-gather buffer (in the arena) -> global index; and
+  // the owned+halo slots of level `first` -> global index
+  LevelWS& W = h->lv[first];
+  psc_desc* d = W.d;
   std::vector<int64_t> mf(rp.N);
   for (int r = 0; r < R; ++r)
     for (int64_t g = d->row_start[r]; g < d->row_start[r + 1]; ++g) mf[g] = r * rp.maxcnt + (g - d->row_start[r]);
@@ -414,8 +515,6 @@ void build_replica(psc_hier* h) {
   PSC_CUDA(cudaMemcpy(rp.map_full, mf.data(), sizeof(int64_t) * rp.N, cudaMemcpyHostToDevice));
   if (!ml.empty()) PSC_CUDA(cudaMemcpy(rp.map_loc, ml.data(), sizeof(int64_t) * ml.size(), cudaMemcpyHostToDevice));
   rp.sendbuf = dvec(rp.maxcnt);
-  rp.bfull = dvec(rp.N);
-  rp.xfull = dvec(rp.N);
   PSC_CUDA(cudaMemset(rp.sendbuf, 0, sizeof(double) * rp.maxcnt));
   PSC_CUDA(cudaStreamSynchronize(s));
   rp.on = true;
@@ -431,15 +530,22 @@ void free_hier(psc_hier* h) {
     if (&W != &h->lv[0]) dfree(W.b);
   }
   Replica& rp = h->rep;
-  sell_free(rp.S);
-  dfree(rp.dinv);
-  dfree(rp.dense);
-  dfree(h->coarse_dense);
+  for (auto& W : rp.lv) {
+    dfree(W.dinv);
+    dfree(W.x[0]);
+    dfree(W.x[1]);
+    dfree(W.r);
+    dfree(W.b);
+    dfree(W.dense);
+  }
+  for (psc_mat* m : rp.mats) {
+    sell_free(m->S);
+    delete m;
+  }
   dfree(rp.sendbuf);
   dfree(rp.map_full);
-  dfree(rp.bfull);
-  dfree(rp.xfull);
   dfree(rp.map_loc);
+  for (auto& W : h->lv) dfree(W.dense);
   dfree(h->r_cg);
   dfree(h->q);
   dfree(h->arena);  // x[0], x[1], r of every level, x_int, p, d_scal, coarse gather buffer, flags
@@ -465,7 +571,6 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
   psc_stats S{};
   PSC_CUDA(cudaEventRecord(h->ev_t0, s));
   if (W.n) PSC_CUDA(cudaMemcpyAsync(h->x_int, x, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
-  exchange(h, W.d, h->x_int, s);
   {
     RowArgs a;
     a.vec_padded = false;  // reads the caller's b
@@ -475,6 +580,7 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
     a.red = &h->red2;
     a.red_out = scal_mine(h, S_RR);
     a.red_stride = (int)((size_t)(S_BB - S_RR) * R);
+    prep(h, W.d, a, s);
     launch_rows(ctx, W.A->S, RowOp::ResidDot2, a, s);
   }
   allgather_slot(h, S_RR, s);
@@ -597,7 +703,8 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     LevelWS& W0 = h->lv[0];
     // the arena: every buffer a peer writes into (halo-bearing vectors, gathered
     // scalars, the coarsest level's gather buffer, P2P flags), zero-initialised
-    psc_desc* dc = h->lv[nlevels - 1].d;
+    const int first = replica_first(h);
+    psc_desc* dc = h->lv[first >= 0 ? first : nlevels - 1].d;
     int64_t maxcnt = 1;
     for (int r = 0; r < NR; ++r) maxcnt = std::max(maxcnt, dc->row_start[r + 1] - dc->row_start[r]);
     double* gbuf = nullptr;
@@ -652,7 +759,7 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     // every rank when distributed
     LevelWS& Wc = h->lv[nlevels - 1];
     if (ctx->nranks > 1) {
-      build_replica(h);
+      if (first >= 0) build_replica(h, first);
       std::vector<P2PBufSpec> hb;
       std::vector<psc_desc*> ld;
       for (int l = 0; l < nlevels; ++l) {
@@ -668,11 +775,7 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       h->p2p.arena = h->arena;
       p2p_setup(ctx, h->p2p, hb, gs, ld, (char*)flagbuf - h->arena);
     } else {
-      h->coarse_one_cta = (Wc.n <= coarse_smem_rows() && Wc.nh == 0);
-      if (Wc.n <= coarse_dense_max_rows() && Wc.nh == 0 && !getenv("PSC_NO_DENSE_COARSE")) {
-        h->coarse_dense = dvec(Wc.n * Wc.n + 1);
-        dense_from_sell(ctx, Wc.A->S, h->coarse_dense, s);
-      }
+      level_coarse_solver(h, Wc);
     }
     PSC_CUDA(cudaStreamSynchronize(s));
     *out = h;
@@ -740,8 +843,8 @@ int psc_hier_smooth(psc_hier* h, int level, const double* b, double* x, int nswe
     double* bl = W.b;
     if (W.n) PSC_CUDA(cudaMemcpyAsync(bl, b, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
     double* res;
-    if (level == h->L - 1) res = coarse_solve(h, bl, nsweeps, s);
-    else res = W.x[pre_smooth(h, level, bl, nsweeps, s, false)];
+    if (level == h->L - 1) res = coarse_solve(h, W, bl, nsweeps, s);
+    else res = W.x[pre_smooth(h, W, bl, nsweeps, s, false)];
     if (W.n) PSC_CUDA(cudaMemcpyAsync(x, res, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
     PSC_CUDA(cudaStreamSynchronize(s));
     return PSC_OK;
@@ -786,6 +889,28 @@ int psc_pcg_solve_host(psc_hier* h, const double* b_host, double* x_host, double
     S.d2h_bytes = 8 * n;
     if (st) *st = S;
     return rc;
+  } catch (const Error& e) {
+    return hfail(ctx, e);
+  }
+}
+
+int psc_hier_exchange_bench(psc_hier* h, int level, int reps, double* us_per_exchange) {
+  psc_ctx* ctx = h ? h->ctx : nullptr;
+  try {
+    PSC_REQUIRE(h && level >= 0 && level < h->L && reps > 0 && us_per_exchange, PSC_ERR_ARG, "bad argument");
+    enter(ctx);
+    cudaStream_t s = ctx->stream;
+    LevelWS& W = h->lv[level];
+    for (int k = 0; k < 3; ++k) exchange(h, W.d, W.x[0], s);  // warm
+    PSC_CUDA(cudaStreamSynchronize(s));
+    PSC_CUDA(cudaEventRecord(h->ev_t0, s));
+    for (int k = 0; k < reps; ++k) exchange(h, W.d, W.x[0], s);
+    PSC_CUDA(cudaEventRecord(h->ev_t1, s));
+    PSC_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    PSC_CUDA(cudaEventElapsedTime(&ms, h->ev_t0, h->ev_t1));
+    *us_per_exchange = 1e3 * ms / reps;
+    return PSC_OK;
   } catch (const Error& e) {
     return hfail(ctx, e);
   }

@@ -260,6 +260,7 @@ struct RowKArgs {
   unsigned int* ticket;
   double* red_out;
   int red_stride;
+  FusedExchange ex;
 };
 
 template <RowOp OP>
@@ -267,6 +268,77 @@ struct NRed {
   static constexpr int value =
       (OP == RowOp::SpmvDot || OP == RowOp::SweepDot) ? 1 : (OP == RowOp::ResidDot2 ? 2 : 0);
 };
+
+// ----------------------------------------------------- fused halo exchange
+constexpr int kMaxExRanks = 64;
+static __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+static __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Prologue of a row kernel whose input x is halo-exchanged (see FusedExchange).
+// Must be reached by every thread of every CTA before x's halo is read.
+__device__ __noinline__ void fused_exchange(const FusedExchange& e, const double* __restrict__ x) {
+  __shared__ uint64_t tgt[kMaxExRanks];
+  __shared__ bool last;
+  if (threadIdx.x < e.R) tgt[threadIdx.x] = e.gen[e.R + threadIdx.x] + 1;  // this exchange's generation
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e.nsend; k += nthr) {
+    int p = 0;
+    while (k >= e.soff[p + 1]) ++p;
+    e.dst[p][k - e.soff[p]] = x[e.send_idx[k]];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = (atomicAdd(e.ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (e.mode == 1) {
+      // the signalling CTA alone polls the peers, then releases the others on the GPU
+      const uint64_t goal = __ldcg(e.go) + 1;  // read before this CTA's ticket (program order)
+      if (last) {
+        __threadfence_system();
+        for (int q = 0; q < e.R; ++q)
+          if (e.nbr[q]) st_release_sys(e.pflag[q], ++e.gen[q]);
+        for (int q = 0; q < e.R; ++q)
+          if (e.nbr[q]) e.gen[e.R + q] = tgt[q];
+        *e.ticket = 0u;
+        for (int q = 0; q < e.R; ++q)
+          if (e.nbr[q])
+            while (ld_acquire_sys(e.myflag + q) < tgt[q]) {
+            }
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(e.go), "l"(goal) : "memory");
+      } else {
+        uint64_t v;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(e.go) : "memory");
+          if (v >= goal) break;
+          __nanosleep(64);
+        }
+      }
+    } else {
+      if (last) {
+        __threadfence_system();
+        for (int q = 0; q < e.R; ++q)
+          if (e.nbr[q]) st_release_sys(e.pflag[q], ++e.gen[q]);
+        for (int q = 0; q < e.R; ++q)
+          if (e.nbr[q]) e.gen[e.R + q] = tgt[q];
+        *e.ticket = 0u;
+      }
+      for (int q = 0; q < e.R; ++q)
+        if (e.nbr[q])
+          while (ld_acquire_sys(e.myflag + q) < tgt[q]) {
+          }
+    }
+  }
+  __syncthreads();
+}
 
 // Fused epilogue of row i with row sum `sum`, split in two: the row's vector
 // operands are loaded by epi_load BEFORE the row sum (so they travel with the
@@ -331,6 +403,7 @@ __device__ __forceinline__ void epilogue(const RowKArgs& a, int64_t i, double su
 template <RowOp OP>
 __device__ __forceinline__ void sell_body(const RowKArgs& a) {
   pdl_enter();
+  if (a.ex.on) fused_exchange(a.ex, a.x);
   constexpr int NR = NRed<OP>::value;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -369,6 +442,7 @@ __device__ __forceinline__ void sell_body(const RowKArgs& a) {
 template <RowOp OP, int G>
 __device__ __forceinline__ void rg_body(const RowKArgs& a) {
   pdl_enter();
+  if (a.ex.on) fused_exchange(a.ex, a.x);
   constexpr int NR = NRed<OP>::value;
   constexpr int RU = 32 / G;
   const int lane = threadIdx.x & 31;
@@ -556,6 +630,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (a.ex.on) fused_exchange(a.ex, a.x);
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     // ---------------- producer (one lane)
@@ -689,6 +764,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tmak(RowKArgs a, int64_t nch
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (a.ex.on) fused_exchange(a.ex, a.x);
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     // ---------------- producer warp: lane j issues the copies of slice j
@@ -867,6 +943,7 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (a.ex.on) fused_exchange(a.ex, a.x);
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     if (lane == 0) {
@@ -1036,6 +1113,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.ticket = r.red ? r.red->ticket : nullptr;
   a.red_out = r.red_out;
   a.red_stride = r.red_stride;
+  a.ex = r.ex;
   const bool needs_red = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
   if (tma_ok(A, r, set)) {
     const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;

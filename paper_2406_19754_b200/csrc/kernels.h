@@ -18,6 +18,31 @@ enum class RowOp {
   PAdd,       // y += s                         (prolongation x_l += P x_{l+1})
 };
 
+// Halo exchange fused into the prologue of the row kernel that consumes the
+// exchanged vector (NVLink peer stores through CUDA IPC mappings, see p2p.cu):
+// every CTA stores its share of x[send_idx] into the neighbours' halo slots,
+// the last CTA (ticket) signals each neighbour with a per-pair generation
+// counter (st.release.sys), then every CTA waits for the neighbours' counters
+// (ld.acquire.sys) before the main loop reads halo values.  Row-kernel grids
+// are persistent (all CTAs resident), so waiting CTAs cannot starve a pusher.
+struct FusedExchange {
+  int on = 0;
+  int R = 0;
+  int64_t nsend = 0;
+  const int32_t* send_idx = nullptr;  // local owned indices, grouped by peer
+  const int64_t* soff = nullptr;      // [R+1]
+  double* const* dst = nullptr;       // [R] peer p's halo slots for this rank
+  const int32_t* nbr = nullptr;       // [R] exchange partners at this level
+  uint64_t* const* pflag = nullptr;   // [R] &flags_p[me]
+  const uint64_t* myflag = nullptr;   // [R]
+  uint64_t* gen = nullptr;            // [2R] sgen, rgen
+  unsigned int* ticket = nullptr;
+  // mode 1: only the signalling CTA polls the peers' flags (system scope) and then
+  // publishes the exchange's generation in `go` (GPU scope) for the other CTAs
+  int mode = 1;
+  uint64_t* go = nullptr;
+};
+
 struct RowArgs {
   double alpha = 1.0, beta = 0.0;
   const double* x = nullptr;
@@ -32,6 +57,7 @@ struct RowArgs {
   // all row vectors (b, dinv, x, y) are library buffers padded past n (TMA bulk
   // copies of the last chunk may read up to 8 bytes beyond the last row)
   bool vec_padded = false;
+  FusedExchange ex;  // halo exchange of x done by this kernel's prologue (ex.on)
 };
 
 // Which slices: all, interior only (no halo column), boundary only.

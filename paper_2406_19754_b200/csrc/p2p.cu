@@ -20,10 +20,10 @@
 
 namespace psc {
 
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+static __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+static __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
@@ -41,6 +41,7 @@ struct PushArgs {
   uint64_t* gen;          // [2R] sgen[p], rgen[p]
   unsigned int* ticket;
   int R;
+  int dbg;  // timing experiments (PSC_DEBUG_EX): 1 gpu fence, 2 relaxed flags + one fence, 4 no wait
 };
 
 __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
@@ -55,19 +56,35 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (!(a.dbg & 1)) __threadfence_system();
+    else __threadfence();
     const unsigned int t = atomicAdd(a.ticket, 1u);
     last = (t == gridDim.x * gridDim.y - 1);
   }
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
-  __threadfence_system();
+  if (!(a.dbg & 1)) __threadfence_system();
   for (int q = 0; q < a.R; ++q)
-    if (a.nbr[q]) st_release_sys(a.pflag[q], ++a.gen[q]);
+    if (a.nbr[q]) {
+      if (a.dbg & 2) {
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(a.pflag[q]), "l"(++a.gen[q]) : "memory");
+      } else {
+        st_release_sys(a.pflag[q], ++a.gen[q]);
+      }
+    }
   for (int q = 0; q < a.R; ++q)
     if (a.nbr[q]) {
       const uint64_t target = ++a.gen[a.R + q];
-      while (ld_acquire_sys(a.myflag + q) < target) {
+      if (a.dbg & 4) continue;  // timing only: do not wait
+      if (a.dbg & 2) {
+        uint64_t v;
+        do {
+          asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.myflag + q) : "memory");
+        } while (v < target);
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+      } else {
+        while (ld_acquire_sys(a.myflag + q) < target) {
+        }
       }
     }
   __threadfence();
@@ -76,7 +93,8 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
 
 static void push(psc_ctx* ctx, P2P& P, const double* x, const int32_t* idx, const int64_t* soff, int64_t n,
                  int64_t max_per_peer, double* const* dst, const int32_t* nbr, cudaStream_t s) {
-  PushArgs a{x, idx, soff, n, dst, nbr, P.d_pflag, P.flags, P.d_gen, P.d_ticket, ctx->nranks};
+  static const int dbg = getenv("PSC_DEBUG_EX") ? atoi(getenv("PSC_DEBUG_EX")) : 0;
+  PushArgs a{x, idx, soff, n, dst, nbr, P.d_pflag, P.flags, P.d_gen, P.d_ticket, ctx->nranks, dbg};
   const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((max_per_peer + 255) / 256, 64));
   p2p_push_kernel<<<dim3((unsigned)bx, (unsigned)ctx->nranks), 256, 0, s>>>(a);
   PSC_CUDA(cudaGetLastError());
@@ -91,6 +109,32 @@ bool p2p_halo(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, cudaStream_t s
   const P2PLevel& L = P.levels[it->second.level];
   if (!L.any) return true;  // no neighbour at this level: nothing to exchange
   push(ctx, P, x, d->d_send_idx, L.d_soff, 0, L.max_send, it->second.d_dst, L.d_nbr, s);
+  return true;
+}
+
+bool p2p_fused(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, FusedExchange& ex) {
+  if (!P.on) return false;
+  auto it = P.bufs.find(x);
+  if (it == P.bufs.end()) return false;
+  const P2PLevel& L = P.levels[it->second.level];
+  ex = FusedExchange();
+  if (!L.any) return true;
+  PSC_REQUIRE(ctx->nranks <= 64, PSC_ERR_STATE, "fused exchange supports at most 64 ranks");
+  ex.on = 1;
+  ex.R = ctx->nranks;
+  ex.nsend = d->n_send;
+  ex.send_idx = d->d_send_idx;
+  ex.soff = L.d_soff;
+  ex.dst = it->second.d_dst;
+  ex.nbr = L.d_nbr;
+  ex.pflag = P.d_pflag;
+  ex.myflag = P.flags;
+  ex.gen = P.d_gen;
+  ex.ticket = P.d_ticket2;
+  ex.go = P.d_go;
+  static const int mode = getenv("PSC_EX_MODE") ? atoi(getenv("PSC_EX_MODE")) : 1;
+  ex.mode = mode;
+  ctx->collectives++;
   return true;
 }
 
@@ -238,6 +282,10 @@ void p2p_setup(psc_ctx* ctx, P2P& P, const std::vector<P2PBufSpec>& halo_bufs,
   PSC_CUDA(cudaMemset(P.d_gen, 0, sizeof(uint64_t) * 2 * R));
   P.d_ticket = dalloc<unsigned int>(1);
   PSC_CUDA(cudaMemset(P.d_ticket, 0, sizeof(unsigned int)));
+  P.d_ticket2 = dalloc<unsigned int>(1);
+  PSC_CUDA(cudaMemset(P.d_ticket2, 0, sizeof(unsigned int)));
+  P.d_go = dalloc<uint64_t>(1);
+  PSC_CUDA(cudaMemset(P.d_go, 0, sizeof(uint64_t)));
   PSC_CUDA(cudaDeviceSynchronize());
   allreduce_min(ctx, 1);  // nobody signals before everybody is set up
   P.on = true;
@@ -256,6 +304,8 @@ void p2p_free(psc_ctx* ctx, P2P& P) {
   dfree(P.d_pflag);
   dfree(P.d_gen);
   dfree(P.d_ticket);
+  dfree(P.d_ticket2);
+  dfree(P.d_go);
   P = P2P();
 }
 

@@ -3,6 +3,7 @@
 #include <map>
 #include <vector>
 
+#include "kernels.h"
 #include "psc_internal.h"
 
 namespace psc {
@@ -33,6 +34,8 @@ struct P2P {
   uint64_t** d_pflag = nullptr;
   uint64_t* d_gen = nullptr;
   unsigned int* d_ticket = nullptr;
+  unsigned int* d_ticket2 = nullptr;  // fused exchanges (row-kernel prologues)
+  uint64_t* d_go = nullptr;           // fused exchanges: GPU-scope release word (mode 1)
   int32_t* d_all = nullptr;
   std::vector<P2PLevel> levels;
   std::map<const double*, P2PBufDev> bufs;
@@ -46,6 +49,9 @@ void p2p_setup(psc_ctx* ctx, P2P& P, const std::vector<P2PBufSpec>& halo_bufs,
 void p2p_free(psc_ctx* ctx, P2P& P);
 // false: not handled (caller falls back to NCCL)
 bool p2p_halo(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, cudaStream_t s);
+// Fill a row kernel's FusedExchange for the halo exchange of x (level buffer);
+// false: not handled (caller uses the standalone exchange).
+bool p2p_fused(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, FusedExchange& ex);
 bool p2p_allgather(psc_ctx* ctx, P2P& P, const double* src, int64_t n, const double* dst_base_local,
                    cudaStream_t s);
 

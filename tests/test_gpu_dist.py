@@ -14,11 +14,11 @@ torch = pytest.importorskip("torch")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(nproc, grid, procs, problem="poisson", timeout=600):
+def _run(nproc, grid, procs, problem="poisson", timeout=600, env_extra=None):
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     env = dict(os.environ, PSC_TEST_GRID=",".join(map(str, grid)), PSC_TEST_PROCS=",".join(map(str, procs)),
-               PSC_TEST_PROBLEM=problem)
+               PSC_TEST_PROBLEM=problem, **(env_extra or {}))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + nproc * 7 + sum(grid) % 97),
            os.path.join(ROOT, "tests", "dist_worker.py")]
@@ -41,3 +41,12 @@ def test_two_gpu_jump_problem():
 
 def test_four_gpu_parity():
     _run(4, (32, 32, 32), (1, 2, 2))
+
+
+@pytest.mark.parametrize("env", [{"PSC_REPL_ROWS": "0"}, {"PSC_REPL_ROWS": "100000000"}, {"PSC_FUSED_EXCHANGE": "1"},
+                                 {"PSC_NO_P2P": "1"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_two_gpu_exchange_and_replication_variants(env):
+    """Replicated suffix from the coarsest level only / from level 1; fused and
+    NCCL halo exchanges: all must match the oracle."""
+    _run(2, (32, 32, 64), (1, 1, 2), env_extra=env)
