@@ -198,7 +198,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="psc", choices=["psc", "reference"])
-    ap.add_argument("--grid", type=int, default=256, help="box edge per GPU")
+    ap.add_argument("--grid", type=int, default=256, help="box edge per GPU (weak scaling)")
+    ap.add_argument("--global-grid", type=int, default=0,
+                    help="strong scaling: fixed global cube edge split over the GPUs (BASELINE.json configs[3]: 512)")
     ap.add_argument("--problem", default="poisson", choices=["poisson", "jump"])
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--maxit", type=int, default=200)
@@ -232,6 +234,12 @@ def main():
     px, py, pz = procs_for(N)
     g = args.grid
     grid = (g * px, g * py, g * pz)
+    strong = args.global_grid > 0
+    if strong:
+        G = args.global_grid
+        if G % px or G % py or G % pz:
+            raise SystemExit(f"--global-grid {G} not divisible by the rank grid {(px, py, pz)}")
+        grid = (G, G, G)
     t_setup0 = time.perf_counter()
     h = None
     if N == 1:
@@ -262,7 +270,7 @@ def main():
     n_loc = info["n_owned"][0]
     r0 = int(levels[0]["row_start"][rank])
     n_global = int(levels[0]["n_global"])
-    b_base = pscgen.rhs_poisson(grid, r0, n_loc)
+    b_base = pscgen.rhs_poisson(grid, r0, n_loc)  # f = 1 also for the jump problem (R22)
     nsteps = args.warmup + args.steps
     bs = [torch.from_numpy(b_base * (k + 1)).cuda() for k in range(nsteps)]
     xs = [torch.zeros(n_loc, dtype=torch.float64, device="cuda") for _ in range(nsteps)]
@@ -307,7 +315,7 @@ def main():
     roof = {"bound": "hbm", "kernel": "sell_tma<Sweep> (level-0 fused l1-Jacobi sweep, TMA-staged)",
             "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": achieved / peak if achieved else None,
-            "traffic": load_traffic(f"sweep_l0_{g}"), "algorithmic_bytes_per_launch": dom_b,
+            "traffic": None if strong else load_traffic(f"sweep_l0_{g}"), "algorithmic_bytes_per_launch": dom_b,
             "launches_timed": dom_n, "avg_launch_us": 1e6 * dom_s / dom_n if dom_n else None,
             # 7 level-0 sweep launches per iteration (3 pre + 4 post, R4); one is timed per iteration
             "share_of_step": (dom_s / dom_n * 7 * sum(iters) / sum(s["solve_seconds"] for s in stats)
@@ -348,13 +356,21 @@ def main():
 
     if rank == 0:
         solve_s = [s["solve_seconds"] for s in stats]
+        if strong:
+            workload = f"3D {args.problem} 7-point {grid[0]}^3 global, strong scaling over {N} GPUs (BASELINE.json configs[3])"
+        elif args.problem == "jump":
+            workload = (f"3D variable-coefficient diffusion, 1e4 jumps on 32^3 cubes, {g}^3 dof per GPU "
+                        "(BASELINE.json configs[4])")
+        else:
+            workload = f"3D {args.problem} 7-point {g}^3 dof per GPU, weak scaling (BASELINE.json configs[2])"
         line = {
-            "metric": "AMG-PCG Mdof*iters/s (3D Poisson, 256^3 dof per GPU, tol 1e-8)",
+            "metric": f"AMG-PCG Mdof*iters/s (3D {args.problem}, "
+                      + (f"{grid[0]}^3 global" if strong else f"{g}^3 dof per GPU") + ", tol 1e-8)",
             "value": value, "unit": "Mdof*iters/s", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
-                "workload": f"3D {args.problem} 7-point {g}^3 dof per GPU, weak scaling (BASELINE.json configs[2])",
+                "workload": workload,
                 "global_grid": list(grid), "procs": [px, py, pz], "n_global": n_global, "levels": info["nlevels"],
                 "rows_rank0": info["n_owned"], "nnz_A_rank0": info["nnz_A"], "operator_complexity": oc,
                 "cycle": "V(4,4) l1-Jacobi, 30 coarsest sweeps", "tol": args.tol, "iters": iters,

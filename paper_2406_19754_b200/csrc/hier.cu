@@ -463,7 +463,7 @@ int replica_first(psc_hier* h) {
 }
 
 void level_coarse_solver(psc_hier* h, LevelWS& W) {
-  W.one_cta = (W.n <= coarse_smem_rows() && W.nh == 0);
+  W.one_cta = (W.nh == 0 && coarse_one_cta_fits(W.A->S));
   if (W.n <= coarse_dense_max_rows() && W.nh == 0 && !getenv("PSC_NO_DENSE_COARSE")) {
     W.dense = dvec(W.n * W.n + 1);
     dense_from_sell(h->ctx, W.A->S, W.dense, h->ctx->stream);
@@ -742,7 +742,9 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       h->rep.maxcnt = maxcnt;
     }
     PSC_CUDA(cudaMallocHost(&h->h_scal, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1)));
-    h->z0_fused = fuse_first_sweep() && nlevels > 1 && h->opt.pre_sweeps > 0;
+    // level 0: writing z0 = M^{-1} r from the CG update measured slower than the
+    // separate scale kernel (201 us vs 123 + 57 us at 256^3): opt-in PSC_Z0_FUSED=1
+    h->z0_fused = getenv("PSC_Z0_FUSED") && fuse_first_sweep() && nlevels > 1 && h->opt.pre_sweeps > 0;
     h->red1 = red_alloc(ctx->num_sms, 1);
     h->red2 = red_alloc(ctx->num_sms, 2);
     // live timing of the dominant kernel: one event pair around one level-0

@@ -1449,6 +1449,18 @@ static void coarse_launch(const CoarseArgs& a, size_t smem, cudaStream_t s) {
   launch_k(coarse_solve<SELL, STAGE>, 1, kCoarseThreads, smem, s, a);
 }
 
+// The one-CTA solver pays off only when A_coarse is staged in shared memory; a
+// larger coarsest level (e.g. 602 rows x ~600 nnz on the 1e4-jump problem:
+// 11 ms per call from L2 in one CTA) runs as full-grid sweep launches instead.
+bool coarse_one_cta_fits(const Sell& A) {
+  const int64_t n = A.n_rows;
+  const int64_t nptr = A.lanes == 1 ? A.n_units + 1 : n + 1;
+  const size_t vec = (size_t)std::max<int64_t>(n, 1) * 4 * sizeof(double);
+  const size_t mat = (size_t)A.padded * sizeof(double) + (size_t)A.col_slots * sizeof(int32_t) +
+                     (size_t)nptr * sizeof(int64_t) * (A.lanes == 1 ? 2 : 1);
+  return n <= coarse_smem_rows() && vec + mat <= (size_t)kMaxSmem;
+}
+
 void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const double* b, double* x, int nsweeps,
                          cudaStream_t s) {
   const int64_t n = A.n_rows;

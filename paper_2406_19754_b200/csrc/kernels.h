@@ -90,6 +90,7 @@ void launch_gather(psc_ctx* ctx, int64_t n, const int64_t* map, const double* in
 // Coarsest solver in ONE CTA: x = dinv .* b, then nsweeps-1 l1-Jacobi sweeps in shared memory.
 // Requires n <= coarse_smem_rows().
 int64_t coarse_smem_rows();
+bool coarse_one_cta_fits(const Sell& A);  // A_coarse fits the one-CTA solver's shared memory
 void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const double* b, double* x, int nsweeps,
                          cudaStream_t s);
 
