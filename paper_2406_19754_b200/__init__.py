@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsc.so")
+# PSC_LIB: alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("PSC_LIB") or os.path.join(_HERE, "libpsc.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2406_19754_b200.build` "

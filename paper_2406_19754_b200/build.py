@@ -36,25 +36,38 @@ def flags():
                    "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
 
 
-def _compile(src):
+def _compile(src, defines=()):
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
     deps = [src] + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "psc.h")]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj, ""
-    r = subprocess.run([NVCC] + flags() + ["-c", src, "-o", obj], capture_output=True, text=True)
+    r = subprocess.run([NVCC] + flags() + list(defines) + ["-c", src, "-o", obj], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Build libpsc.so (or, for experiments, `out` with extra -D defines in a separate object dir)."""
+    global BUILD
+    lib = out or LIB
+    build_dir = BUILD if not out else os.path.join(HERE, "_build_" + os.path.basename(out).replace(".so", ""))
+    saved = BUILD
+    BUILD = build_dir
+    try:
+        return _build(force, verbose, lib, list(defines))
+    finally:
+        BUILD = saved
+
+
+def _build(force, verbose, LIB, defines):
     os.makedirs(BUILD, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     if force:
         for o in glob.glob(os.path.join(BUILD, "*.o")):
             os.remove(o)
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        res = list(ex.map(_compile, srcs))
+        res = list(ex.map(lambda f: _compile(f, defines), srcs))
     objs = [o for o, _ in res]
     if verbose:
         for _, log in res:

@@ -49,6 +49,12 @@ static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   PSC_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+// plain sliced-ELL kernels: minimum resident CTAs per SM requested from ptxas
+// (2: ~116 registers; 3: 80; 4: 64 with spills: 3550 / 3523 / 3262 Mdof*it/s)
+#ifndef PSC_SELL_MINB
+#define PSC_SELL_MINB 2
+#endif
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ double gsum(const double* g, int nranks) {
   // value of a gathered scalar: sum over ranks in rank order (identical on all ranks)
@@ -240,6 +246,7 @@ __device__ __forceinline__ double rg_row_sum(const int32_t* __restrict__ col, co
 
 struct RowKArgs {
   int keep_matrix;  // 1: matrix small enough to stay in L2 across the level's launches (evict_last)
+  int dinv_fly;     // sell_tma sweeps on all-DIA matrices: 1/M_ii from the row's values, no dinv stream
   const int64_t* ptr;
   const int64_t* cptr;
   const int32_t* hdr;
@@ -282,7 +289,7 @@ static __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 
 // Prologue of a row kernel whose input x is halo-exchanged (see FusedExchange).
 // Must be reached by every thread of every CTA before x's halo is read.
-__device__ __noinline__ void fused_exchange(const FusedExchange& e, const double* __restrict__ x) {
+__device__ __forceinline__ void fused_exchange(const FusedExchange& e, const double* __restrict__ x) {
   __shared__ uint64_t tgt[kMaxExRanks];
   __shared__ bool last;
   if (threadIdx.x < e.R) tgt[threadIdx.x] = e.gen[e.R + threadIdx.x] + 1;  // this exchange's generation
@@ -403,7 +410,9 @@ __device__ __forceinline__ void epilogue(const RowKArgs& a, int64_t i, double su
 template <RowOp OP>
 __device__ __forceinline__ void sell_body(const RowKArgs& a) {
   pdl_enter();
+#ifndef PSC_NO_FUSED_EX_CODE
   if (a.ex.on) fused_exchange(a.ex, a.x);
+#endif
   constexpr int NR = NRed<OP>::value;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -442,7 +451,9 @@ __device__ __forceinline__ void sell_body(const RowKArgs& a) {
 template <RowOp OP, int G>
 __device__ __forceinline__ void rg_body(const RowKArgs& a) {
   pdl_enter();
+#ifndef PSC_NO_FUSED_EX_CODE
   if (a.ex.on) fused_exchange(a.ex, a.x);
+#endif
   constexpr int NR = NRed<OP>::value;
   constexpr int RU = 32 / G;
   const int lane = threadIdx.x & 31;
@@ -470,7 +481,7 @@ __device__ __forceinline__ void rg_body(const RowKArgs& a) {
 
 // One named kernel per (layout, epilogue): readable launch lists and ncu filters.
 #define PSC_ROW_KERNELS(name, OP)                                                                         \
-  __global__ void __launch_bounds__(kBlock) sell_##name(RowKArgs a) { sell_body<OP>(a); }               \
+  __global__ void __launch_bounds__(kBlock, PSC_SELL_MINB) sell_##name(RowKArgs a) { sell_body<OP>(a); }  \
   template <int G>                                                                                        \
   __global__ void __launch_bounds__(kBlock) rg_##name(RowKArgs a) {                                      \
     rg_body<OP, G>(a);                                                                                    \
@@ -630,7 +641,9 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+#ifndef PSC_NO_FUSED_EX_CODE
   if (a.ex.on) fused_exchange(a.ex, a.x);
+#endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     // ---------------- producer (one lane)
@@ -662,8 +675,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const uint32_t vbytes = (uint32_t)(vb1 - vb0) * 8;
         const uint32_t cbytes = (uint32_t)(cb1 - cb0) * 4;
         const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
-        const uint32_t nvec =
-            (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) + ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0);
+        const uint32_t nvec = (EV::B ? 1 : 0) + ((EV::D_SELL && !a.dinv_fly) ? 1 : 0) +
+                              ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0);
         mbar_expect_tx(&full[st], hb + vbytes + cbytes + nvec * rbytes);
         bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol_keep);
         if (vbytes) bulk_g2s(base + kTmaHdrBytes, a.val + vb0, vbytes, &full[st], pol_mat);
@@ -671,7 +684,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
         if (rbytes) {
           if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol_stream);
-          if constexpr (EV::D_SELL) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
+          if constexpr (EV::D_SELL)
+            if (!a.dinv_fly) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
           if constexpr (EV::X || EV::XPRE) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
           if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
         }
@@ -721,11 +735,29 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
 #pragma unroll
         for (int j = 0; j < kTmaMaxW; ++j)
           if (j < w) sum = fma(v[32 * j], xv[j], sum);
+        double dfly = 0.0;
+        if constexpr (EV::D) {
+          if (a.dinv_fly) {
+            // l1 diagonal M_ii = a_ii + sum_{j != i} |a_ij| from the slice in
+            // shared memory, same order as l1_dinv_kernel; __drcp_rn is the correctly
+            // rounded 1/M_ii, i.e. bit-identical to the stored dinv
+            const int j0 = __shfl_sync(0xffffffffu, h, 14);
+            double aii = 0.0, off = 0.0;
+#pragma unroll
+            for (int j = 0; j < kTmaMaxW; ++j)
+              if (j < w) {
+                const double vj = v[32 * j];
+                if (j == j0) aii = vj;
+                else off += fabs(vj);
+              }
+            dfly = __drcp_rn(aii + off);
+          }
+        }
         if ((int64_t)i < a.n_rows) {
           const int rl = warp * 32 + lane;
           EpiIn e{0.0, 0.0, 0.0};
           if constexpr (EV::B) e.b = vec[rl];
-          if constexpr (EV::D) e.d = vec[kTmaRows + rl];
+          if constexpr (EV::D) e.d = a.dinv_fly ? dfly : vec[kTmaRows + rl];
           if constexpr (EV::X) e.x = vec[2 * kTmaRows + rl];
           if (readY) e.x = vec[2 * kTmaRows + rl];
           epi_store<OP>(a, (int64_t)i, sum, e, acc);
@@ -764,7 +796,9 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tmak(RowKArgs a, int64_t nch
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+#ifndef PSC_NO_FUSED_EX_CODE
   if (a.ex.on) fused_exchange(a.ex, a.x);
+#endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     // ---------------- producer warp: lane j issues the copies of slice j
@@ -943,7 +977,9 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+#ifndef PSC_NO_FUSED_EX_CODE
   if (a.ex.on) fused_exchange(a.ex, a.x);
+#endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     if (lane == 0) {
@@ -1092,6 +1128,10 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   RowKArgs a;
   // matrices up to 48 MB stay in L2 (evict_last) across the 8-10 launches of their level
   a.keep_matrix = (A.padded * 12 + A.n_rows * 8) <= ((int64_t)env_int("PSC_KEEP_MB", 96) << 20) ? 1 : 0;
+  // on-the-fly 1/M_ii (no dinv stream) measured slower: 287 vs 242 us per level-0 sweep
+  // (FP64 reciprocal + |a_ij| sums in the consumer warps); opt-in PSC_DINV_FLY=1
+  a.dinv_fly = (A.all_dia_diag && (op == RowOp::Sweep || op == RowOp::SweepDot) && env_int("PSC_DINV_FLY", 0))
+                   ? 1 : 0;
   a.ptr = A.ptr;
   a.cptr = A.cptr;
   a.hdr = A.hdr;
@@ -1759,7 +1799,7 @@ int choose_lanes(int64_t n_rows, int64_t nnz) {
 
 __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
                                 const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
-                                int32_t* __restrict__ hdr) {
+                                int32_t* __restrict__ hdr, int* all_dia_diag) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_slices) return;
   int32_t* h = hdr + s * kHdr;
@@ -1771,7 +1811,14 @@ __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ pt
   h[4] = (int32_t)((ptr[s + 1] - vb) >> 5);
   const int d = dia_d[s];
   h[5] = d > 0 ? 1 : 0;
-  for (int j = 0; j < kMaxDia; ++j) h[6 + j] = j < d ? dia_off[s * kMaxDia + j] : 0;
+  int j0 = -1;
+  for (int j = 0; j < kMaxDia; ++j) {
+    h[6 + j] = j < d ? dia_off[s * kMaxDia + j] : 0;
+    if (j < d && dia_off[s * kMaxDia + j] == 0) j0 = j;
+  }
+  h[14] = j0;  // DIA: slot of the diagonal (offset 0), -1 if none
+  h[15] = 0;
+  if (j0 < 0) atomicAnd(all_dia_diag, 0);
 }
 
 void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg, const double* d_val,
@@ -1829,8 +1876,16 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
           n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, own_begin, n_own, d_halo, n_halo,
           S.col, S.val, d_err);
       PSC_CUDA(cudaGetLastError());
-      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, S.hdr);
+      int* d_all = dalloc<int>(1);
+      const int one = 1;
+      PSC_CUDA(cudaMemcpyAsync(d_all, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, S.hdr, d_all);
       PSC_CUDA(cudaGetLastError());
+      int h_all = 0;
+      PSC_CUDA(cudaMemcpyAsync(&h_all, d_all, sizeof(int), cudaMemcpyDeviceToHost, s));
+      PSC_CUDA(cudaStreamSynchronize(s));
+      dfree(d_all);
+      S.all_dia_diag = (h_all != 0);
     }
     flag.resize(nu);
     hp.resize(nu + 1);

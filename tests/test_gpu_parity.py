@@ -247,6 +247,7 @@ VARIANTS = [
     {"PSC_TMAK": "1"},
     {"PSC_NO_FUSED_SCALE": "1"},
     {"PSC_Z0_FUSED": "1"},
+    {"PSC_DINV_FLY": "1"},
     {"PSC_FUSED_EXCHANGE": "1"},
     {"PSC_NO_DIA": "1"},
     {"PSC_NO_RG_TMA": "1", "PSC_NO_DENSE_COARSE": "1"},
