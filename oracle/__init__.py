@@ -42,7 +42,8 @@ class _CSR(ctypes.Structure):
 class _Hier(ctypes.Structure):
     _fields_ = [("nlevels", ctypes.c_int), ("A", ctypes.POINTER(_CSR)), ("P", ctypes.POINTER(_CSR)),
                 ("R", ctypes.POINTER(_CSR)), ("pre", ctypes.c_int), ("post", ctypes.c_int),
-                ("coarse", ctypes.c_int)]
+                ("coarse", ctypes.c_int), ("coarse_pcg", ctypes.c_int), ("coarse_maxit", ctypes.c_int),
+                ("coarse_tol", ctypes.c_double)]
 
 
 def lib():
@@ -58,6 +59,10 @@ def lib():
         L.or_vcycle.argtypes = [vp, vp, vp]
         L.or_pcg.argtypes = [vp, vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int)]
         L.or_pcg.restype = ctypes.c_int
+        L.or_fcg.argtypes = [vp, vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int)]
+        L.or_fcg.restype = ctypes.c_int
+        L.or_coarse_pcg.argtypes = [vp, vp, vp, vp, ctypes.c_int, ctypes.c_double]
+        L.or_coarse_pcg.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -83,7 +88,7 @@ class _CsrHolder:
 
 
 class _HierHolder:
-    def __init__(self, hier, pre=4, post=4, coarse=30):
+    def __init__(self, hier, pre=4, post=4, coarse=30, coarse_pcg=False, coarse_maxit=40, coarse_tol=1e-10):
         L = hier.nlevels
         self.A = [_CsrHolder(hier.levels[l].A) for l in range(L)]
         self.P = [_CsrHolder(hier.levels[l].P) for l in range(L - 1)]
@@ -91,7 +96,8 @@ class _HierHolder:
         self.Aa = (_CSR * L)(*[h.c for h in self.A])
         self.Pa = (_CSR * max(L - 1, 1))(*[h.c for h in self.P])
         self.Ra = (_CSR * max(L - 1, 1))(*[h.c for h in self.R])
-        self.c = _Hier(L, self.Aa, self.Pa, self.Ra, pre, post, coarse)
+        self.c = _Hier(L, self.Aa, self.Pa, self.Ra, pre, post, coarse, 1 if coarse_pcg else 0, coarse_maxit,
+                       coarse_tol)
 
 
 def spmv(A, x) -> np.ndarray:
@@ -130,18 +136,40 @@ def l1_sweeps_from_zero(A, b, nsweeps: int) -> np.ndarray:
     return x
 
 
-def vcycle(hier, r, pre=4, post=4, coarse=30) -> np.ndarray:
-    """z = B_0 r, Eq. (2)."""
-    hh = _HierHolder(hier, pre, post, coarse)
+def vcycle(hier, r, pre=4, post=4, coarse=30, **coarse_kw) -> np.ndarray:
+    """z = B_0 r, Eq. (2).  coarse_kw: coarse_pcg, coarse_maxit, coarse_tol."""
+    hh = _HierHolder(hier, pre, post, coarse, **coarse_kw)
     r = _arr(r, np.float64)
     z = np.empty_like(r)
     lib().or_vcycle(ctypes.byref(hh.c), r.ctypes.data, z.ctypes.data)
     return z
 
 
-def pcg(hier, b, x0=None, tol=1e-8, maxit=200, pre=4, post=4, coarse=30):
+def coarse_pcg(A, b, maxit=40, tol=1e-10):
+    """Coarsest-level PCG with the l1-Jacobi preconditioner.  Returns (x, iterations)."""
+    h = _CsrHolder(A)
+    m = l1_diag(A)
+    b = _arr(b, np.float64)
+    x = np.empty(h.c.nrows, np.float64)
+    it = lib().or_coarse_pcg(ctypes.byref(h.c), m.ctypes.data, b.ctypes.data, x.ctypes.data, int(maxit), float(tol))
+    return x, it
+
+
+def fcg(hier, b, x0=None, tol=1e-8, maxit=200, pre=4, post=4, coarse=30, **coarse_kw):
+    """Flexible CG, FCG(1), one V-cycle per iteration.  Returns (x, iters, status, hist)."""
+    hh = _HierHolder(hier, pre, post, coarse, **coarse_kw)
+    b = _arr(b, np.float64)
+    x = np.zeros_like(b) if x0 is None else _arr(x0, np.float64).copy()
+    hist = np.full(maxit + 1, np.nan)
+    it = ctypes.c_int(0)
+    st = lib().or_fcg(ctypes.byref(hh.c), b.ctypes.data, x.ctypes.data, float(tol), int(maxit), hist.ctypes.data,
+                      ctypes.byref(it))
+    return x, it.value, st, hist[: it.value + 1]
+
+
+def pcg(hier, b, x0=None, tol=1e-8, maxit=200, pre=4, post=4, coarse=30, **coarse_kw):
     """PCG preconditioned by one V-cycle per iteration.  Returns (x, iters, status, hist)."""
-    hh = _HierHolder(hier, pre, post, coarse)
+    hh = _HierHolder(hier, pre, post, coarse, **coarse_kw)
     b = _arr(b, np.float64)
     x = np.zeros_like(b) if x0 is None else _arr(x0, np.float64).copy()
     hist = np.full(maxit + 1, np.nan)

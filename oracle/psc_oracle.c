@@ -32,6 +32,9 @@ typedef struct {
   const or_csr* R;  /* R[0..L-2], n_{l+1} x n_l, R_l = P_l^T given explicitly */
   int pre, post;    /* smoothing sweeps before/after the coarse correction (R4: 4 and 4) */
   int coarse;       /* l1-Jacobi sweeps at the coarsest level (30) */
+  int coarse_pcg;   /* 1: coarsest solver = PCG with l1-Jacobi preconditioner (VBM) */
+  int coarse_maxit; /* its iteration cap ("at most 40 iterations") */
+  double coarse_tol;/* its relative-residual tolerance (reading R23) */
 } or_hier;
 
 /* y = A x.  Row sums in stored column order. */
@@ -81,6 +84,51 @@ void or_l1_sweeps_from_zero(const or_csr* A, const double* m, const double* b, i
 
 static double* dalloc(int64_t n) { return (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double)); }
 
+static double dot(int64_t n, const double* a, const double* b) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+/* Coarsest solver of the paper's VBM configuration: "at most 40
+ * iterations of the Preconditioned CG coupled to l1-Jacobi preconditioner".
+ * PCG from x = 0 with M = diag(m) (m from or_l1_diag); stops after maxit
+ * iterations or when ||r_k||_2 <= tol ||b||_2 (reading R23).  Returns the
+ * number of iterations. */
+int or_coarse_pcg(const or_csr* A, const double* m, const double* b, double* x, int maxit, double tol) {
+  const int64_t n = A->nrows;
+  double* r = dalloc(n);
+  double* z = dalloc(n);
+  double* p = dalloc(n);
+  double* q = dalloc(n);
+  memset(x, 0, sizeof(double) * (size_t)n);
+  memcpy(r, b, sizeof(double) * (size_t)n);
+  const double nb = sqrt(dot(n, b, b));
+  int k = 0;
+  if (nb > 0.0) {
+    for (int64_t i = 0; i < n; ++i) z[i] = r[i] / m[i];
+    memcpy(p, z, sizeof(double) * (size_t)n);
+    double rz = dot(n, r, z);
+    for (k = 1; k <= maxit; ++k) {
+      or_spmv(A, p, q);
+      const double pq = dot(n, p, q);
+      if (!(pq > 0.0)) { k -= 1; break; }
+      const double alpha = rz / pq;
+      for (int64_t i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
+      for (int64_t i = 0; i < n; ++i) r[i] = r[i] - alpha * q[i];
+      if (sqrt(dot(n, r, r)) <= tol * nb) break;
+      for (int64_t i = 0; i < n; ++i) z[i] = r[i] / m[i];
+      const double rz_new = dot(n, r, z);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    }
+    if (k > maxit) k = maxit;
+  }
+  free(r); free(z); free(p); free(q);
+  return k;
+}
+
 /* x = B_l b, the V-cycle of Eq. (2) (Sec. 2.3):
  *   I - B_l A_l = (I - M_l^{-T} A_l)(I - P_l B_{l+1} P_l^T A_l)(I - M_l^{-1} A_l),
  * applied to b with x = 0 on entry, i.e. right to left:
@@ -93,7 +141,8 @@ static void vcycle_level(const or_hier* h, double* const* m, int l, const double
   const int64_t n = A->nrows;
   double* w = dalloc(n);
   if (l == h->nlevels - 1) {
-    or_l1_sweeps_from_zero(A, m[l], b, h->coarse, x, w);
+    if (h->coarse_pcg) or_coarse_pcg(A, m[l], b, x, h->coarse_maxit, h->coarse_tol);
+    else or_l1_sweeps_from_zero(A, m[l], b, h->coarse, x, w);
     free(w);
     return;
   }
@@ -141,12 +190,6 @@ void or_vcycle(const or_hier* h, const double* r, double* z) {
   free_m(h, m);
 }
 
-static double dot(int64_t n, const double* a, const double* b) {
-  double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
-  return s;
-}
-
 /* Preconditioned CG (reading R1: PCG, equal to FCG(1) for a fixed SPD B;
  * P:113-117) with B = one V-cycle per iteration.
  * Stopping rule hist[k] = ||r_k||_2/||b||_2 <= tol on the recurrence residual
@@ -191,6 +234,58 @@ int or_pcg(const or_hier* h, const double* b, double* x, double tol, int maxit, 
     const double beta = rz_new / rz;
     rz = rz_new;
     for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+  }
+done:
+  free(r); free(z); free(p); free(q);
+  free_m(h, m);
+  return status;
+}
+
+/* Flexible CG, FCG(1) of Notay (the paper's Krylov method, Fig. 6;
+ * its reference [MR1797890]): the preconditioner may vary between iterations
+ * (e.g. the coarsest PCG solve makes B nonlinear), so each new direction is
+ * explicitly A-orthogonalised against the previous one:
+ *   z_k = B(r_k);  p_k = z_k - ((z_k, A p_{k-1}) / (p_{k-1}, A p_{k-1})) p_{k-1}
+ *   alpha_k = (p_k, r_k) / (p_k, A p_k);  x += alpha_k p_k;  r -= alpha_k A p_k
+ * Same stopping rule, history and status codes as or_pcg. */
+int or_fcg(const or_hier* h, const double* b, double* x, double tol, int maxit, double* hist, int* iters) {
+  const or_csr* A = &h->A[0];
+  const int64_t n = A->nrows;
+  *iters = 0;
+  const double nb = sqrt(dot(n, b, b));
+  if (nb == 0.0) {
+    memset(x, 0, sizeof(double) * (size_t)n);
+    hist[0] = 0.0;
+    return 0;
+  }
+  double** m = make_m(h);
+  double* r = dalloc(n);
+  double* z = dalloc(n);
+  double* p = dalloc(n);
+  double* q = dalloc(n);
+  int status = 1;
+  double delta = 0.0;
+  or_spmv(A, x, r);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
+  hist[0] = sqrt(dot(n, r, r)) / nb;
+  if (hist[0] <= tol) { status = 0; goto done; }
+  for (int k = 1; k <= maxit; ++k) {
+    vcycle_level(h, m, 0, r, z);
+    if (k == 1) {
+      memcpy(p, z, sizeof(double) * (size_t)n);
+    } else {
+      const double beta = dot(n, z, q) / delta; /* q = A p_{k-1} */
+      for (int64_t i = 0; i < n; ++i) p[i] = z[i] - beta * p[i];
+    }
+    or_spmv(A, p, q);
+    delta = dot(n, p, q);
+    if (!(delta > 0.0) || !isfinite(delta)) { status = -6; *iters = k; goto done; }
+    const double alpha = dot(n, p, r) / delta;
+    for (int64_t i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
+    for (int64_t i = 0; i < n; ++i) r[i] = r[i] - alpha * q[i];
+    hist[k] = sqrt(dot(n, r, r)) / nb;
+    *iters = k;
+    if (hist[k] <= tol) { status = 0; goto done; }
   }
 done:
   free(r); free(z); free(p); free(q);

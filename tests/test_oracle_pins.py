@@ -14,6 +14,10 @@ sign or index, transposed operand) fails at least one test here:
   or_pcg             -> Cholesky / DST exact solve, scipy's CG with the same B,
                         A = I, diag(1..10), b = 0, A-norm error monotone,
                         true vs recurrence residual, paper Fig. 2 loose pin
+  or_coarse_pcg      -> S:417-418 examples, scipy CG with M = diag(1/m) iterate by
+                        iterate, exact-coarse V-cycle = dense Eq. (2) with A^-1
+  or_fcg             -> PCG iterates for a fixed SPD B (Notay FCG(1)), Cholesky,
+                        A = I, b = 0, variable-B convergence, VBM loose pin
 """
 import numpy as np
 import pytest
@@ -291,5 +295,104 @@ def test_paper_fig2_iterations_loose():
     h = pscgen.poisson_hierarchy(128)
     b = pscgen.rhs_poisson((128, 128, 128), 0, h.levels[0].n)
     x, it, st, hist = oracle.pcg(h, b, tol=1e-6, maxit=100)
+    assert st == 0
+    assert abs(it - golden("vbm_iterations_1gpu_tol1e-6")) <= 4
+
+
+# ------------------------------------------- NEXT-2: coarse PCG(40) and FCG(1)
+def test_coarse_pcg_spec_examples():
+    # [2] x = 4 -> x = 2 ; diag(1..5) exact within 5 iterations
+    x, it = oracle.coarse_pcg(sp.csr_matrix(np.array([[2.0]])), np.array([4.0]), maxit=40, tol=1e-12)
+    assert it == 1 and x[0] == 2.0
+    x, it = oracle.coarse_pcg(sp.diags(np.arange(1.0, 6.0), format="csr"), np.ones(5), maxit=40, tol=1e-12)
+    assert it <= 5
+    np.testing.assert_allclose(x, 1.0 / np.arange(1.0, 6.0), rtol=1e-14)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_coarse_pcg_iterates_equal_scipy_cg(seed):
+    """P:328 "PCG coupled to l1-Jacobi preconditioner": iterates equal scipy's CG with
+    M^{-1} = diag(1/m), m = a_ii + sum_{j!=i} |a_ij| (S:374 values pinned above)."""
+    from scipy.sparse.linalg import LinearOperator, cg
+    A = random_spd_mixed(40, 0.08, seed)
+    b = np.random.default_rng(seed).standard_normal(40)
+    m = oracle.l1_diag(A)
+    M = LinearOperator((40, 40), matvec=lambda r: np.asarray(r).ravel() / m)
+    for k in (1, 2, 5, 9):
+        xo, it = oracle.coarse_pcg(A, b, maxit=k, tol=0.0)
+        assert it == k
+        xs, _ = cg(A, b, x0=np.zeros(40), rtol=0.0, atol=0.0, maxiter=k, M=M)
+        np.testing.assert_allclose(xo, xs, rtol=0, atol=1e-11 * np.abs(xs).max())
+    xo, it = oracle.coarse_pcg(A, b, maxit=400, tol=1e-13)
+    np.testing.assert_allclose(xo, np.linalg.solve(A.toarray(), b), rtol=1e-10, atol=1e-12)
+
+
+def test_vcycle_with_exact_coarse_pcg_equals_dense_eq2():
+    """Coarse PCG run to exactness (maxit >= n_coarse, tiny tol) is B_ell = A_ell^{-1} in Eq. (2)."""
+    h = pscgen.poisson_hierarchy(6, max_levels=3, coarse_target=1)
+    n = h.levels[0].n
+    L = h.nlevels
+    # dense Eq. (2) with an exact coarsest solve
+    def Bl(l):
+        A = h.levels[l].A.to_scipy().toarray()
+        if l == L - 1:
+            return np.linalg.inv(A)
+        G = np.eye(A.shape[0]) - A / _M(A)[:, None]
+        P = h.levels[l].P.to_scipy().toarray()
+        R = h.levels[l].R.to_scipy().toarray()
+        E = np.linalg.matrix_power(G, 4) @ (np.eye(A.shape[0]) - P @ Bl(l + 1) @ R @ A) @ np.linalg.matrix_power(G, 4)
+        return (np.eye(A.shape[0]) - E) @ np.linalg.inv(A)
+    Bd = Bl(0)
+    r = pscgen.rhs_random(3, 0, n)
+    z = oracle.vcycle(h, r, coarse_pcg=True, coarse_maxit=1000, coarse_tol=1e-15)
+    np.testing.assert_allclose(z, Bd @ r, rtol=0, atol=1e-10 * np.abs(Bd @ r).max())
+
+
+def test_fcg_equals_pcg_for_fixed_spd_preconditioner():
+    """Notay's FCG(1) and PCG build the same iterates for a fixed SPD B (exact arithmetic;
+    S:476): compare x_k for every k with the pinned PCG."""
+    h = pscgen.poisson_hierarchy(12, coarse_target=30)
+    b = pscgen.rhs_random(21, 0, h.levels[0].n)
+    for k in (1, 2, 3, 5, 8):
+        xp, ip, sp_, _ = oracle.pcg(h, b, tol=0.0, maxit=k)
+        xf, if_, sf, _ = oracle.fcg(h, b, tol=0.0, maxit=k)
+        assert ip == if_ == k
+        np.testing.assert_allclose(xf, xp, rtol=0, atol=1e-10 * np.abs(xp).max())
+
+
+def test_fcg_cholesky_identity_zero_rhs():
+    h = pscgen.poisson_hierarchy(6, coarse_target=20)
+    A = h.levels[0].A.to_scipy().toarray()
+    b = pscgen.rhs_random(8, 0, h.levels[0].n)
+    x, it, st, hist = oracle.fcg(h, b, tol=1e-13, maxit=216)
+    assert st == 0
+    xc = sla.cho_solve(sla.cho_factor(A), b)
+    assert np.linalg.norm(x - xc) / np.linalg.norm(xc) < 1e-11
+    hI = pscgen.csr_hierarchy(sp.eye(20, format="csr"))
+    x, it, st, _ = oracle.fcg(hI, np.arange(1.0, 21.0), tol=1e-12)
+    assert st == 0 and it == 1
+    x, it, st, _ = oracle.fcg(h, np.zeros(h.levels[0].n), x0=np.ones(h.levels[0].n))
+    assert st == 0 and it == 0 and not x.any()
+
+
+def test_fcg_with_variable_coarse_pcg_converges():
+    """A loose coarse PCG (tol 1e-2) makes B vary between applications: FCG still
+    converges and its recurrence residual matches the true residual."""
+    h = pscgen.poisson_hierarchy(16, coarse_target=60)
+    b = pscgen.rhs_poisson((16, 16, 16), 0, h.levels[0].n)
+    x, it, st, hist = oracle.fcg(h, b, tol=1e-10, maxit=100, coarse_pcg=True, coarse_maxit=40, coarse_tol=1e-2)
+    assert st == 0
+    A = h.levels[0].A.to_scipy()
+    true = np.linalg.norm(b - A @ x) / np.linalg.norm(b)
+    assert true <= 1e-9
+
+
+@pytest.mark.slow
+def test_paper_vbm_configuration_iterations_loose():
+    """The paper's VBM solve: FCG, l1-Jacobi V-cycle, coarsest PCG(<= 40)
+    with l1-Jacobi; Fig. 2: 18 iterations to 1e-6 on 8e6 dof (loose +-4 at 128^3)."""
+    h = pscgen.poisson_hierarchy(128)
+    b = pscgen.rhs_poisson((128, 128, 128), 0, h.levels[0].n)
+    x, it, st, hist = oracle.fcg(h, b, tol=1e-6, maxit=100, coarse_pcg=True, coarse_maxit=40, coarse_tol=1e-10)
     assert st == 0
     assert abs(it - golden("vbm_iterations_1gpu_tol1e-6")) <= 4
