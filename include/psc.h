@@ -156,12 +156,26 @@ void psc_mat_destroy(psc_mat* m);
 
 /* -------------------------------------------------------------- hierarchy */
 
-/* Smoothing sweeps before / after the coarse correction and l1-Jacobi sweeps at
- * the coarsest level (defaults 4 / 4 / 30: Fig. 5 caption). */
+/* Coarsest-level solver B_ell of Eq. (2). */
+enum {
+  PSC_COARSE_SWEEPS = 0, /* coarse_sweeps l1-Jacobi sweeps from zero (Fig. 5 caption) */
+  PSC_COARSE_PCG = 1     /* PCG from zero with the l1-Jacobi preconditioner, at most coarse_maxit
+                            iterations, stopping when ||r||_2 <= coarse_tol ||b||_2 (the paper's
+                            VBM configuration; reading R23).  The preconditioner B then
+                            varies between applications: use PSC_KRYLOV_FCG. */
+};
+
+/* Smoothing sweeps before / after the coarse correction and the coarsest-level
+ * solver (defaults 4 / 4 / 30 sweeps: Fig. 5 caption).  Zero-
+ * initialise the struct: coarse_solver 0 = sweeps; coarse_maxit 0 -> 40 and
+ * coarse_tol 0 -> 1e-10 (defaults of PSC_COARSE_PCG, reading R23). */
 typedef struct {
   int pre_sweeps;
   int post_sweeps;
   int coarse_sweeps;
+  int coarse_solver;  /* PSC_COARSE_SWEEPS or PSC_COARSE_PCG */
+  int coarse_maxit;
+  double coarse_tol;
 } psc_cycle_opts;
 
 /* [collective] AMG hierarchy handle over given level matrices (D10/D11 in
@@ -183,7 +197,7 @@ int psc_hier_vcycle(psc_hier* h, const double* r_dev, double* z_dev);
 int psc_hier_dinv(psc_hier* h, int level, double* dinv_dev);
 
 /* [collective] Test hook: x_dev = nsweeps l1-Jacobi sweeps x <- x + M^{-1}(b - A_l x)
- * from x = 0 at `level` (the coarsest-level solver when level = nlevels-1). */
+ * from x = 0 at `level` (sweeps at every level, whatever the coarse_solver option). */
 int psc_hier_smooth(psc_hier* h, int level, const double* b_dev, double* x_dev, int nsweeps);
 
 /* Solve statistics. */
@@ -217,6 +231,25 @@ int psc_pcg_solve(psc_hier* h, const double* b_dev, double* x_dev, double tol, i
  * and x0 and the device->host copy of x are inside the call (end-to-end path). */
 int psc_pcg_solve_host(psc_hier* h, const double* b_host, double* x_host, double tol, int maxit,
                        double* res_hist_host, psc_stats* st);
+
+/* Krylov method of psc_krylov_solve ("a synchronization-reduced version of
+ * the Flexible Conjugate Gradient (FCG)"; Fig. 6). */
+enum {
+  PSC_KRYLOV_PCG = 0, /* as psc_pcg_solve */
+  PSC_KRYLOV_FCG = 1  /* Notay's FCG(1): z = B r; p = z - ((z, A p_old)/(p_old, A p_old)) p_old;
+                         alpha = (p, r)/(p, A p).  Equal to PCG in exact arithmetic for a fixed
+                         SPD B; stays convergent when B varies (PSC_COARSE_PCG).  Same stopping
+                         rule, history, statistics and status codes as PCG. */
+};
+
+/* [collective] psc_pcg_solve / psc_pcg_solve_host with the Krylov method chosen by
+ * `method` (PSC_KRYLOV_PCG or PSC_KRYLOV_FCG; anything else is PSC_ERR_ARG).
+ * b, x: device (psc_krylov_solve) or host (psc_krylov_solve_host) buffers of
+ * n_owned(0) doubles, x holding the initial guess on entry. */
+int psc_krylov_solve(psc_hier* h, int method, const double* b_dev, double* x_dev, double tol, int maxit,
+                     double* res_hist_host, psc_stats* st);
+int psc_krylov_solve_host(psc_hier* h, int method, const double* b_host, double* x_host, double tol, int maxit,
+                          double* res_hist_host, psc_stats* st);
 
 /* [collective] Timing hook: *us_per_exchange = device time of one halo exchange of a
  * level-`level` vector, averaged over `reps` back-to-back exchanges (eager launches). */

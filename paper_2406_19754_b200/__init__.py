@@ -32,8 +32,15 @@ PSC_ERR_ARG, PSC_ERR_STATE, PSC_ERR_CUDA, PSC_ERR_NCCL, PSC_ERR_NOMEM, PSC_ERR_B
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
 
+PSC_COARSE_SWEEPS, PSC_COARSE_PCG = 0, 1
+PSC_KRYLOV_PCG, PSC_KRYLOV_FCG = 0, 1
+_COARSE = {"sweeps": PSC_COARSE_SWEEPS, "pcg": PSC_COARSE_PCG}
+_KRYLOV = {"pcg": PSC_KRYLOV_PCG, "fcg": PSC_KRYLOV_FCG}
+
+
 class CycleOpts(ctypes.Structure):
-    _fields_ = [("pre_sweeps", _i32), ("post_sweeps", _i32), ("coarse_sweeps", _i32)]
+    _fields_ = [("pre_sweeps", _i32), ("post_sweeps", _i32), ("coarse_sweeps", _i32), ("coarse_solver", _i32),
+                ("coarse_maxit", _i32), ("coarse_tol", _f64)]
 
 
 class Stats(ctypes.Structure):
@@ -80,6 +87,8 @@ _sig("psc_hier_dinv", _i32, [_vp, _i32, _vp])
 _sig("psc_hier_smooth", _i32, [_vp, _i32, _vp, _vp, _i32])
 _sig("psc_pcg_solve", _i32, [_vp, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
 _sig("psc_pcg_solve_host", _i32, [_vp, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
+_sig("psc_krylov_solve", _i32, [_vp, _i32, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
+_sig("psc_krylov_solve_host", _i32, [_vp, _i32, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
 _sig("psc_hier_exchange_bench", _i32, [_vp, _i32, _i32, _P(_f64)])
 _sig("psc_hier_destroy", None, [_vp])
 
@@ -256,14 +265,20 @@ class Matrix:
 
 
 class Hierarchy:
-    """psc_hier_create over given level matrices A[l], P[l], R[l]; V-cycle + PCG."""
+    """psc_hier_create over given level matrices A[l], P[l], R[l]; V-cycle + PCG / FCG.
 
-    def __init__(self, ctx: Context, A, P, R, pre=4, post=4, coarse=30):
+    coarse_solver: "sweeps" (`coarse` l1-Jacobi sweeps) or "pcg" (PCG with
+    l1-Jacobi, at most coarse_maxit iterations to coarse_tol)."""
+
+    def __init__(self, ctx: Context, A, P, R, pre=4, post=4, coarse=30, coarse_solver="sweeps", coarse_maxit=40,
+                 coarse_tol=1e-10):
         L = len(A)
         Aa = (_vp * L)(*[m.handle for m in A])
         Pa = (_vp * max(L - 1, 1))(*[m.handle for m in P])
         Ra = (_vp * max(L - 1, 1))(*[m.handle for m in R])
-        opts = CycleOpts(pre, post, coarse)
+        if coarse_solver not in _COARSE:
+            raise ValueError(f"coarse_solver must be one of {sorted(_COARSE)}")
+        opts = CycleOpts(pre, post, coarse, _COARSE[coarse_solver], int(coarse_maxit), float(coarse_tol))
         h = _vp()
         _check(_lib.psc_hier_create(ctx.handle, L, Aa, Pa, Ra, ctypes.byref(opts), ctypes.byref(h)), ctx)
         self.ctx, self.handle, self.nlevels = ctx, h.value, L
@@ -294,17 +309,21 @@ class Hierarchy:
                self.ctx)
         return x
 
-    def solve(self, b, x, tol=1e-8, maxit=200):
-        """PCG on device tensors.  Returns (status, stats dict, residual history ndarray)."""
+    def solve(self, b, x, tol=1e-8, maxit=200, method="pcg"):
+        """PCG or FCG (method) on device tensors.  Returns (status, stats dict, residual history)."""
+        if method not in _KRYLOV:
+            raise ValueError(f"method must be one of {sorted(_KRYLOV)}")
         hist = np.full(maxit + 1, np.nan)
         st = Stats()
-        rc = _lib.psc_pcg_solve(self.handle, _dev_ptr(b, self.n0, "b"), _dev_ptr(x, self.n0, "x"), float(tol),
-                                int(maxit), hist.ctypes.data, ctypes.byref(st))
+        rc = _lib.psc_krylov_solve(self.handle, _KRYLOV[method], _dev_ptr(b, self.n0, "b"), _dev_ptr(x, self.n0, "x"),
+                                   float(tol), int(maxit), hist.ctypes.data, ctypes.byref(st))
         _check(rc, self.ctx, ok=(PSC_OK, PSC_NOT_CONVERGED))
         return rc, st.as_dict(), hist[: st.iters + 1]
 
-    def solve_host(self, b, x, tol=1e-8, maxit=200):
-        """PCG on host numpy arrays (end-to-end path: copies inside the call). x updated in place."""
+    def solve_host(self, b, x, tol=1e-8, maxit=200, method="pcg"):
+        """PCG / FCG on host numpy arrays (end-to-end path: copies inside the call). x updated in place."""
+        if method not in _KRYLOV:
+            raise ValueError(f"method must be one of {sorted(_KRYLOV)}")
         if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous):
             raise TypeError("x must be a C-contiguous float64 numpy array")
         b = _host(b, np.float64, "b")
@@ -312,8 +331,8 @@ class Hierarchy:
             raise ValueError("b/x size mismatch")
         hist = np.full(maxit + 1, np.nan)
         st = Stats()
-        rc = _lib.psc_pcg_solve_host(self.handle, b.ctypes.data, x.ctypes.data, float(tol), int(maxit),
-                                     hist.ctypes.data, ctypes.byref(st))
+        rc = _lib.psc_krylov_solve_host(self.handle, _KRYLOV[method], b.ctypes.data, x.ctypes.data, float(tol),
+                                        int(maxit), hist.ctypes.data, ctypes.byref(st))
         _check(rc, self.ctx, ok=(PSC_OK, PSC_NOT_CONVERGED))
         return rc, st.as_dict(), hist[: st.iters + 1]
 
@@ -329,7 +348,7 @@ class Hierarchy:
             self.handle = None
 
 
-def build_hierarchy(ctx: Context, levels, pre=4, post=4, coarse=30):
+def build_hierarchy(ctx: Context, levels, pre=4, post=4, coarse=30, **coarse_kw):
     """Create descriptors + matrices for this rank and assemble them, in the
     PSBLAS order.  `levels[l]` is a dict with
       n_global, row_start (nranks+1), A=(row_ptr, col_global, val) for this rank's rows,
@@ -344,5 +363,5 @@ def build_hierarchy(ctx: Context, levels, pre=4, post=4, coarse=30):
         d.assemble()
     for m in A + P + R:
         m.assemble()
-    h = Hierarchy(ctx, A, P, R, pre, post, coarse)
+    h = Hierarchy(ctx, A, P, R, pre, post, coarse, **coarse_kw)
     return h, descs, A, P, R

@@ -19,7 +19,17 @@ namespace {
 // vectors of the solve path: padded so TMA bulk copies of the last rows may overread
 double* dvec(int64_t n) { return dalloc<double>((size_t)n + 64); }
 
-enum Slot { S_PQ = 0, S_RR = 1, S_RZ = 2, S_BB = 3, NSLOT = 4 };
+// Gathered per-rank partial scalars (slot-major, nranks entries each).  Main
+// Krylov loop: (p, Ap), (r, r), (r, z) [FCG: (z, A p_old)], (b, b), FCG (p, r).
+// Coarsest PCG (general form): (p, Ap), (r, r), (r, z) double-buffered by
+// iteration parity, (b, b).  Every slot is read before a peer can write its
+// next value: between a read and the peer's next push lies an all-gather that
+// needs this rank's later contribution.
+enum Slot {
+  S_PQ = 0, S_RR = 1, S_RZ = 2, S_BB = 3, S_PR = 4,
+  S_CPQ = 5, S_CRR = 6, S_CZ0 = 7, S_CZ1 = 8, S_CBB = 9,
+  NSLOT = 10
+};
 
 struct LevelWS {
   psc_mat *A = nullptr, *P = nullptr, *R = nullptr;
@@ -32,6 +42,8 @@ struct LevelWS {
   // coarsest-level solver data (last level of a level array)
   double* dense = nullptr;    // n x n row-major copy of A when n <= coarse_dense_max_rows()
   bool one_cta = false;       // sparse one-CTA solver applies
+  double* cz = nullptr;       // general coarsest PCG: z and q = A p (n)
+  double* cq = nullptr;
 };
 
 // Replicated suffix (nranks > 1): levels first..L-1 are held whole on every
@@ -58,7 +70,7 @@ struct Replica {
 struct psc_hier_s {
   psc_ctx* ctx = nullptr;
   int L = 0;
-  psc_cycle_opts opt{4, 4, 30};
+  psc_cycle_opts opt{4, 4, 30, PSC_COARSE_SWEEPS, 40, 1e-10};
   std::vector<LevelWS> lv;
   Replica rep;
   bool z0_fused = false;  // CG update writes the first level-0 sweep of the next V-cycle
@@ -72,9 +84,13 @@ struct psc_hier_s {
   double* d_bhost = nullptr;  // device staging for psc_pcg_solve_host
   double* d_xhost = nullptr;
   RedSite red1, red2;
-  // graph of one PCG iteration
-  cudaGraphExec_t iter_exec = nullptr;
-  int64_t iter_launches = 0, iter_collectives = 0;
+  int* d_done = nullptr;        // stop flag of the general coarsest PCG
+  // weight of the (., z) reduction in the last level-0 post-sweep while an FCG
+  // iteration is recorded (q = A p_old); nullptr: r (PCG)
+  const double* rz_weight = nullptr;
+  // graph of one Krylov iteration, per method (PSC_KRYLOV_PCG, PSC_KRYLOV_FCG)
+  cudaGraphExec_t iter_exec[2] = {nullptr, nullptr};
+  int64_t iter_launches[2] = {0, 0}, iter_collectives[2] = {0, 0};
   double* z_ptr = nullptr;
   // dominant-kernel timing (level-0 l1-Jacobi sweep) inside the graph
   std::vector<cudaEvent_t> ev_dom;  // pairs (start, end)
@@ -145,9 +161,9 @@ void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------ coarsest level
-// B_ell = `nsweeps` l1-Jacobi sweeps from zero on the last
-// level of a level array.  Returns its iterate.
-double* coarse_solve(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream_t s) {
+// `nsweeps` l1-Jacobi sweeps from zero on the last level of a level
+// array.  Returns its iterate.
+double* coarse_sweeps(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream_t s) {
   psc_ctx* ctx = h->ctx;
   if (W.dense) {
     launch_coarse_dense(ctx, W.dense, W.n, W.dinv, b, W.x[0], nsweeps, s);
@@ -176,6 +192,63 @@ double* coarse_solve(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cuda
     cur ^= 1;
   }
   return W.x[cur];
+}
+
+// PCG from zero with the l1-Jacobi preconditioner, at most coarse_maxit
+// iterations, stopping at ||r|| <= coarse_tol ||b|| (reading R23).
+// Dense one-CTA kernel when the level has a dense copy; otherwise one SpMV +
+// two vector kernels per iteration, all recorded (the device flag h->d_done
+// makes the steps after convergence no-ops), with all-gathers of the partial
+// scalars when the level is distributed.  x in W.x[0], p in W.x[1] (halo-
+// bearing: exchanged before each SpMV), r in W.r.
+double* coarse_pcg(psc_hier* h, LevelWS& W, const double* b, cudaStream_t s) {
+  psc_ctx* ctx = h->ctx;
+  const int maxit = h->opt.coarse_maxit;
+  const double tol = h->opt.coarse_tol;
+  if (W.dense) {
+    launch_coarse_dense_pcg(ctx, W.dense, W.n, W.dinv, b, W.x[0], maxit, tol, s);
+    return W.x[0];
+  }
+  const int R = ctx->nranks;
+  const bool dist = W.d && R > 1;
+  const int nr = dist ? R : 1;
+  auto g = [&](Slot sl) { return dist ? scal(h, sl) : scal_mine(h, sl); };
+  double *x = W.x[0], *p = W.x[1], *r = W.r, *z = W.cz, *q = W.cq;
+  launch_cpcg_init(ctx, W.n, b, W.dinv, x, r, z, p, h->d_done, &h->red2, scal_mine(h, S_CZ0), (S_CBB - S_CZ0) * R,
+                   s);
+  if (dist) {
+    allgather_slot(h, S_CZ0, s);
+    allgather_slot(h, S_CBB, s);
+  }
+  for (int k = 1; k <= maxit; ++k) {
+    const Slot zo = (k & 1) ? S_CZ0 : S_CZ1;  // (r, z) of iteration k-1
+    const Slot zn = (k & 1) ? S_CZ1 : S_CZ0;  // (r, z) of iteration k
+    {
+      RowArgs a;
+      a.vec_padded = true;
+      a.x = p;
+      a.y = q;
+      a.red = &h->red1;
+      a.red_out = scal_mine(h, S_CPQ);
+      prep(h, W.d, a, s);
+      launch_rows(ctx, W.A->S, RowOp::SpmvDot, a, s);
+    }
+    if (dist) allgather_slot(h, S_CPQ, s);
+    launch_cpcg_update(ctx, W.n, x, p, r, q, z, W.dinv, g(S_CPQ), g(zo), nr, h->d_done, &h->red2,
+                       scal_mine(h, S_CRR), (zn - S_CRR) * R, s);
+    if (dist) {
+      allgather_slot(h, S_CRR, s);
+      allgather_slot(h, zn, s);
+    }
+    if (k < maxit) launch_cpcg_dir(ctx, W.n, z, p, g(S_CRR), g(S_CBB), g(zn), g(zo), nr, tol, h->d_done, s);
+  }
+  return x;
+}
+
+// B_ell: the configured coarsest-level solver
+double* coarse_solve(psc_hier* h, LevelWS& W, const double* b, cudaStream_t s) {
+  if (h->opt.coarse_solver == PSC_COARSE_PCG) return coarse_pcg(h, W, b, s);
+  return coarse_sweeps(h, W, b, h->opt.coarse_sweeps, s);
 }
 
 // nsweeps l1-Jacobi sweeps from zero on W (pre-smoothing: the rightmost factor
@@ -242,7 +315,7 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   psc_ctx* ctx = h->ctx;
   const int Lend = (int)LV.size();
   if (dist && h->rep.on && l == h->rep.first) return replicated_cycle(h, b, s);
-  if (l == Lend - 1) return coarse_solve(h, LV[l], b, h->opt.coarse_sweeps, s);
+  if (l == Lend - 1) return coarse_solve(h, LV[l], b, s);
   LevelWS& W = LV[l];
   LevelWS& C = LV[l + 1];
   const bool time_here = timing && dist && l == 0;
@@ -296,6 +369,7 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     if (last0) {
       a.red = &h->red1;
       a.red_out = scal_mine(h, S_RZ);
+      a.w = h->rz_weight;
     }
     prep(h, W.d, a, s);
     const bool t = time_here && h->dom_used + 2 <= (int)h->ev_dom.size();
@@ -307,7 +381,8 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     }
     cur ^= 1;
   }
-  if (level0 && post == 0) launch_dot(ctx, W.n, b, W.x[cur], &h->red1, scal_mine(h, S_RZ), s);
+  if (level0 && post == 0)
+    launch_dot(ctx, W.n, h->rz_weight ? h->rz_weight : b, W.x[cur], &h->red1, scal_mine(h, S_RZ), s);
   return W.x[cur];
 }
 
@@ -315,20 +390,33 @@ double* vcycle_level(psc_hier* h, int l, const double* b, cudaStream_t s, bool t
   return vcycle_rec(h, h->lv, l, b, s, timing, first_done, true);
 }
 
-// One PCG iteration k >= 1 (P:113-117 with B = V-cycle; reading R1):
+// One Krylov iteration k >= 1, preconditioned by one V-cycle.
+// PCG (P:113-117 with B = V-cycle; reading R1):
 //   z = B r ; rz = (r, z) ; beta = rz / rz_old ; p = z + beta p ; rz_old = rz
 //   q = A p ; pq = (p, q) ; alpha = rz_old / pq ; x += alpha p ; r -= alpha q ; rr = (r, r)
-// (at k = 1, p = 0 and rz_old = 1 so p = z exactly)
-void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
+//   (at k = 1, p = 0 and rz_old = 1 so p = z exactly)
+// FCG(1) (Notay): the same four reductions, fused the same way:
+//   z = B r ; zq = (z, q_old) [last post-sweep] ; beta = zq / pq_old ; p = z - beta p ;
+//   pr = (p, r) [same kernel] ; q = A p ; pq = (p, q) ; alpha = pr / pq ; x, r, rr as PCG
+//   (at k = 1, q_old = 0 and pq_old = 1 so p = z exactly)
+void record_iteration(psc_hier* h, cudaStream_t s, bool timing, int method) {
   psc_ctx* ctx = h->ctx;
   LevelWS& W = h->lv[0];
   const int R = ctx->nranks;
+  const bool fcg = (method == PSC_KRYLOV_FCG);
   h->dom_used = 0;
   // the CG update of the previous iteration (or the eager start) wrote x_0 = M^{-1} r
+  h->rz_weight = fcg ? h->q : nullptr;
   double* z = vcycle_level(h, 0, h->r_cg, s, timing, h->z0_fused);
+  h->rz_weight = nullptr;
   h->z_ptr = z;
   allgather_slot(h, S_RZ, s);
-  launch_xpby(ctx, W.n, z, h->p, scal(h, S_RZ), rz_old(h), R, &h->red2, s);
+  if (fcg) {
+    launch_fcg_dir(ctx, W.n, z, h->p, h->r_cg, scal(h, S_RZ), scal(h, S_PQ), R, &h->red1, scal_mine(h, S_PR), s);
+    allgather_slot(h, S_PR, s);
+  } else {
+    launch_xpby(ctx, W.n, z, h->p, scal(h, S_RZ), rz_old(h), R, &h->red2, s);
+  }
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -340,30 +428,32 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing) {
     launch_rows(ctx, W.A->S, RowOp::SpmvDot, a, s);
   }
   allgather_slot(h, S_PQ, s);
-  launch_cg_update(ctx, W.n, h->x_int, h->p, h->r_cg, h->q, scal(h, S_PQ), rz_old(h), R, &h->red1,
-                   scal_mine(h, S_RR), s, h->z0_fused ? W.dinv : nullptr, h->z0_fused ? W.x[0] : nullptr);
+  launch_cg_update(ctx, W.n, h->x_int, h->p, h->r_cg, h->q, scal(h, S_PQ), fcg ? scal(h, S_PR) : rz_old(h),
+                   fcg ? R : 1, R, &h->red1, scal_mine(h, S_RR), s, h->z0_fused ? W.dinv : nullptr,
+                   h->z0_fused ? W.x[0] : nullptr);
   allgather_slot(h, S_RR, s);
   PSC_CUDA(cudaMemcpyAsync(h->h_scal, h->d_scal, sizeof(double) * NSLOT * R, cudaMemcpyDeviceToHost, s));
 }
 
-void capture_iteration(psc_hier* h) {
+void capture_iteration(psc_hier* h, int method) {
   psc_ctx* ctx = h->ctx;
   cudaStream_t s = ctx->stream;
   const int64_t l0 = ctx->launches, c0 = ctx->collectives;
   cudaGraph_t g = nullptr;
   PSC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   try {
-    record_iteration(h, s, true);
+    record_iteration(h, s, true, method);
   } catch (...) {
+    h->rz_weight = nullptr;
     cudaStreamEndCapture(s, &g);
     if (g) cudaGraphDestroy(g);
     throw;
   }
   PSC_CUDA(cudaStreamEndCapture(s, &g));
-  PSC_CUDA(cudaGraphInstantiate(&h->iter_exec, g, 0));
+  PSC_CUDA(cudaGraphInstantiate(&h->iter_exec[method], g, 0));
   PSC_CUDA(cudaGraphDestroy(g));
-  h->iter_launches = ctx->launches - l0;
-  h->iter_collectives = ctx->collectives - c0;
+  h->iter_launches[method] = ctx->launches - l0;
+  h->iter_collectives[method] = ctx->collectives - c0;
   ctx->launches = l0;
   ctx->collectives = c0;
 }
@@ -528,6 +618,8 @@ void free_hier(psc_hier* h) {
   for (auto& W : h->lv) {
     dfree(W.dinv);
     if (&W != &h->lv[0]) dfree(W.b);
+    dfree(W.cz);
+    dfree(W.cq);
   }
   Replica& rp = h->rep;
   for (auto& W : rp.lv) {
@@ -537,6 +629,8 @@ void free_hier(psc_hier* h) {
     dfree(W.r);
     dfree(W.b);
     dfree(W.dense);
+    dfree(W.cz);
+    dfree(W.cq);
   }
   for (psc_mat* m : rp.mats) {
     sell_free(m->S);
@@ -554,15 +648,17 @@ void free_hier(psc_hier* h) {
   if (h->h_scal) cudaFreeHost(h->h_scal);
   red_free(h->red1);
   red_free(h->red2);
-  if (h->iter_exec) cudaGraphExecDestroy(h->iter_exec);
+  dfree(h->d_done);
+  for (auto e : h->iter_exec)
+    if (e) cudaGraphExecDestroy(e);
   for (auto e : h->ev_dom) cudaEventDestroy(e);
   if (h->ev_t0) cudaEventDestroy(h->ev_t0);
   if (h->ev_t1) cudaEventDestroy(h->ev_t1);
   delete h;
 }
 
-int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, double* hist, psc_stats* st,
-               double extra_h2d) {
+int solve_impl(psc_hier* h, int method, const double* b, double* x, double tol, int maxit, double* hist,
+               psc_stats* st, double extra_h2d) {
   psc_ctx* ctx = h->ctx;
   cudaStream_t s = ctx->stream;
   const int R = ctx->nranks;
@@ -607,15 +703,23 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
       status = PSC_OK;
     } else {
       PSC_CUDA(cudaMemsetAsync(h->p, 0, sizeof(double) * (W.n + W.nh), s));
-      const double one = 1.0;
-      PSC_CUDA(cudaMemcpyAsync(rz_old(h), &one, sizeof(double), cudaMemcpyHostToDevice, s));
+      if (method == PSC_KRYLOV_FCG) {
+        // q_old = 0 and pq_old = 1 (rank 0 holds the 1): p_1 = z_1 - 0 p_0 exactly
+        PSC_CUDA(cudaMemsetAsync(h->q, 0, sizeof(double) * W.n, s));
+        std::vector<double> pq0(R, 0.0);
+        pq0[0] = 1.0;
+        PSC_CUDA(cudaMemcpyAsync(scal(h, S_PQ), pq0.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s));
+      } else {
+        const double one = 1.0;
+        PSC_CUDA(cudaMemcpyAsync(rz_old(h), &one, sizeof(double), cudaMemcpyHostToDevice, s));
+      }
       if (h->z0_fused) launch_scale(ctx, W.n, W.dinv, h->r_cg, W.x[0], s);  // first V-cycle's first sweep
-      if (!h->iter_exec) capture_iteration(h);
+      if (!h->iter_exec[method]) capture_iteration(h, method);
       for (int k = 1; k <= maxit; ++k) {
-        PSC_CUDA(cudaGraphLaunch(h->iter_exec, s));
+        PSC_CUDA(cudaGraphLaunch(h->iter_exec[method], s));
         PSC_CUDA(cudaStreamSynchronize(s));
-        ctx->launches += h->iter_launches;
-        ctx->collectives += h->iter_collectives;
+        ctx->launches += h->iter_launches[method];
+        ctx->collectives += h->iter_collectives[method];
         for (int e = 0; e + 1 < h->dom_used; e += 2) {
           float ms = 0.f;
           PSC_CUDA(cudaEventElapsedTime(&ms, h->ev_dom[e], h->ev_dom[e + 1]));
@@ -657,9 +761,11 @@ int solve_impl(psc_hier* h, const double* b, double* x, double tol, int maxit, d
   S.dom_kernel_bytes = 8.0 * (double)W.A->nnz + 4.0 * (double)W.A->S.nnz_ell + 32.0 * (double)W.n;
   S.h2d_bytes = (int64_t)extra_h2d;
   S.halo_path = R == 1 ? 0 : (h->p2p.on ? 1 : 2);
-  S.iter_graph_nodes = (int)h->iter_launches;
+  S.iter_graph_nodes = (int)h->iter_launches[method];
   if (st) *st = S;
-  if (status == PSC_ERR_BREAKDOWN) throw Error(PSC_ERR_BREAKDOWN, "PCG breakdown: p^T A p <= 0 or not finite");
+  if (status == PSC_ERR_BREAKDOWN)
+    throw Error(PSC_ERR_BREAKDOWN, method == PSC_KRYLOV_FCG ? "FCG breakdown: p^T A p <= 0 or not finite"
+                                                            : "PCG breakdown: p^T A p <= 0 or not finite");
   return status;
 }
 
@@ -681,6 +787,12 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     if (opts) h->opt = *opts;
     PSC_REQUIRE(h->opt.pre_sweeps >= 0 && h->opt.post_sweeps >= 0 && h->opt.coarse_sweeps >= 0, PSC_ERR_ARG,
                 "negative sweep count");
+    PSC_REQUIRE(h->opt.coarse_solver == PSC_COARSE_SWEEPS || h->opt.coarse_solver == PSC_COARSE_PCG, PSC_ERR_ARG,
+                "unknown coarse_solver");
+    PSC_REQUIRE(h->opt.coarse_maxit >= 0 && h->opt.coarse_tol >= 0.0 && std::isfinite(h->opt.coarse_tol), PSC_ERR_ARG,
+                "coarse_maxit / coarse_tol must be non-negative");
+    if (h->opt.coarse_maxit == 0) h->opt.coarse_maxit = 40;
+    if (h->opt.coarse_tol == 0.0) h->opt.coarse_tol = 1e-10;  // reading R23
     h->lv.resize(nlevels);
     for (int l = 0; l < nlevels; ++l) {
       LevelWS& W = h->lv[l];
@@ -747,6 +859,8 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     h->z0_fused = getenv("PSC_Z0_FUSED") && fuse_first_sweep() && nlevels > 1 && h->opt.pre_sweeps > 0;
     h->red1 = red_alloc(ctx->num_sms, 1);
     h->red2 = red_alloc(ctx->num_sms, 2);
+    h->d_done = dalloc<int>(1);
+    PSC_CUDA(cudaMemset(h->d_done, 0, sizeof(int)));
     // live timing of the dominant kernel: one event pair around one level-0
     // sweep per iteration (each event-record node costs ~0.1% of an iteration);
     // PSC_DOM_TIMING=k times k of the 7 sweeps, 0 disables
@@ -778,6 +892,13 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       p2p_setup(ctx, h->p2p, hb, gs, ld, (char*)flagbuf - h->arena);
     } else {
       level_coarse_solver(h, Wc);
+    }
+    if (h->opt.coarse_solver == PSC_COARSE_PCG) {  // buffers of the general coarsest PCG
+      LevelWS& C = h->rep.on ? h->rep.lv.back() : Wc;
+      if (!C.dense) {
+        C.cz = dvec(C.n);
+        C.cq = dvec(C.n);
+      }
     }
     PSC_CUDA(cudaStreamSynchronize(s));
     *out = h;
@@ -845,7 +966,7 @@ int psc_hier_smooth(psc_hier* h, int level, const double* b, double* x, int nswe
     double* bl = W.b;
     if (W.n) PSC_CUDA(cudaMemcpyAsync(bl, b, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
     double* res;
-    if (level == h->L - 1) res = coarse_solve(h, W, bl, nsweeps, s);
+    if (level == h->L - 1) res = coarse_sweeps(h, W, bl, nsweeps, s);
     else res = W.x[pre_smooth(h, W, bl, nsweeps, s, false)];
     if (W.n) PSC_CUDA(cudaMemcpyAsync(x, res, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s));
     PSC_CUDA(cudaStreamSynchronize(s));
@@ -855,23 +976,35 @@ int psc_hier_smooth(psc_hier* h, int level, const double* b, double* x, int nswe
   }
 }
 
-int psc_pcg_solve(psc_hier* h, const double* b, double* x, double tol, int maxit, double* hist, psc_stats* st) {
+int psc_krylov_solve(psc_hier* h, int method, const double* b, double* x, double tol, int maxit, double* hist,
+                     psc_stats* st) {
   psc_ctx* ctx = h ? h->ctx : nullptr;
   try {
     PSC_REQUIRE(h && maxit >= 0 && tol >= 0.0, PSC_ERR_ARG, "bad argument");
+    PSC_REQUIRE(method == PSC_KRYLOV_PCG || method == PSC_KRYLOV_FCG, PSC_ERR_ARG, "unknown Krylov method");
     PSC_REQUIRE((b && x) || h->lv[0].n == 0, PSC_ERR_ARG, "null b/x");
     enter(ctx);
-    return solve_impl(h, b, x, tol, maxit, hist, st, 0.0);
+    return solve_impl(h, method, b, x, tol, maxit, hist, st, 0.0);
   } catch (const Error& e) {
     return hfail(ctx, e);
   }
 }
 
+int psc_pcg_solve(psc_hier* h, const double* b, double* x, double tol, int maxit, double* hist, psc_stats* st) {
+  return psc_krylov_solve(h, PSC_KRYLOV_PCG, b, x, tol, maxit, hist, st);
+}
+
 int psc_pcg_solve_host(psc_hier* h, const double* b_host, double* x_host, double tol, int maxit, double* hist,
                        psc_stats* st) {
+  return psc_krylov_solve_host(h, PSC_KRYLOV_PCG, b_host, x_host, tol, maxit, hist, st);
+}
+
+int psc_krylov_solve_host(psc_hier* h, int method, const double* b_host, double* x_host, double tol, int maxit,
+                          double* hist, psc_stats* st) {
   psc_ctx* ctx = h ? h->ctx : nullptr;
   try {
     PSC_REQUIRE(h && maxit >= 0 && tol >= 0.0, PSC_ERR_ARG, "bad argument");
+    PSC_REQUIRE(method == PSC_KRYLOV_PCG || method == PSC_KRYLOV_FCG, PSC_ERR_ARG, "unknown Krylov method");
     const int64_t n = h->lv[0].n;
     PSC_REQUIRE((b_host && x_host) || n == 0, PSC_ERR_ARG, "null b/x");
     enter(ctx);
@@ -885,7 +1018,7 @@ int psc_pcg_solve_host(psc_hier* h, const double* b_host, double* x_host, double
       PSC_CUDA(cudaMemcpyAsync(h->d_xhost, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     }
     psc_stats S{};
-    int rc = solve_impl(h, h->d_bhost, h->d_xhost, tol, maxit, hist, &S, 16.0 * (double)n);
+    int rc = solve_impl(h, method, h->d_bhost, h->d_xhost, tol, maxit, hist, &S, 16.0 * (double)n);
     if (n) PSC_CUDA(cudaMemcpyAsync(x_host, h->d_xhost, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     PSC_CUDA(cudaStreamSynchronize(s));
     S.d2h_bytes = 8 * n;

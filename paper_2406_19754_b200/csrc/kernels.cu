@@ -263,6 +263,7 @@ struct RowKArgs {
   double* y;
   double* y2;            // Spmv: if set, y2 = dinv2 .* y (first sweep from zero of the next level)
   const double* dinv2;
+  const double* w;       // SweepDot: weight of the reduction (nullptr: b)
   double* partials;
   unsigned int* ticket;
   double* red_out;
@@ -386,7 +387,7 @@ __device__ __forceinline__ void epi_store(const RowKArgs& a, int64_t i, double s
   } else if constexpr (OP == RowOp::Sweep || OP == RowOp::SweepDot) {
     const double xn = e.x + e.d * (e.b - sum);
     a.y[i] = xn;
-    if constexpr (OP == RowOp::SweepDot) acc[0] += e.b * xn;
+    if constexpr (OP == RowOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : e.b) * xn;
   } else if constexpr (OP == RowOp::Resid) {
     a.y[i] = e.b - sum;
   } else if constexpr (OP == RowOp::ResidDot2) {
@@ -1149,6 +1150,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.y = r.y;
   a.y2 = r.y2;
   a.dinv2 = r.dinv2;
+  a.w = r.w;
   a.partials = r.red ? r.red->partials : nullptr;
   a.ticket = r.red ? r.red->ticket : nullptr;
   a.red_out = r.red_out;
@@ -1282,11 +1284,11 @@ void launch_l1_dinv(psc_ctx* ctx, const Sell& A, double* dinv, cudaStream_t s) {
 __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __restrict__ x,
                                                            const double* __restrict__ p, double* __restrict__ r,
                                                            const double* __restrict__ q, const double* g_pq,
-                                                           const double* rz_old, int nranks, double* partials,
-                                                           unsigned int* ticket, double* out,
+                                                           const double* g_num, int num_ranks, int nranks,
+                                                           double* partials, unsigned int* ticket, double* out,
                                                            const double* __restrict__ dinv, double* __restrict__ z0) {
   pdl_enter();
-  const double alpha = __ldcg(rz_old) / gsum(g_pq, nranks);
+  const double alpha = gsum(g_num, num_ranks) / gsum(g_pq, nranks);
   double acc[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     x[i] = x[i] + alpha * p[i];
@@ -1300,11 +1302,137 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
 }
 
 void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
-                      const double* g_pq, const double* rz_old, int nranks, const RedSite* red, double* red_out,
-                      cudaStream_t s, const double* dinv, double* z0) {
+                      const double* g_pq, const double* g_num, int num_ranks, int nranks, const RedSite* red,
+                      double* red_out, cudaStream_t s, const double* dinv, double* z0) {
   const int g = std::min(vec_grid(ctx, n), red->grid);
-  launch_k(cg_update_kernel, g, kBlock, 0, s, n, x, p, r, q, g_pq, rz_old, nranks, red->partials, red->ticket,
-           red_out, dinv, z0);
+  launch_k(cg_update_kernel, g, kBlock, 0, s, n, x, p, r, q, g_pq, g_num, num_ranks, nranks, red->partials,
+           red->ticket, red_out, dinv, z0);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+// FCG(1) (Notay; the paper's Krylov method): the new direction is
+// A-orthogonalised against the previous one only, p = z - ((z, q_old) / (p_old,
+// q_old)) p_old with q_old = A p_old, and alpha needs (p, r), reduced here.
+__global__ void __launch_bounds__(kBlock) fcg_dir_kernel(int64_t n, const double* __restrict__ z,
+                                                         double* __restrict__ p, const double* __restrict__ r,
+                                                         const double* g_zq, const double* g_pq, int nranks,
+                                                         double* partials, unsigned int* ticket, double* out) {
+  pdl_enter();
+  const double beta = gsum(g_zq, nranks) / gsum(g_pq, nranks);
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double pi = z[i] - beta * p[i];
+    p[i] = pi;
+    acc[0] += pi * r[i];
+  }
+  pdl_exit();
+  grid_reduce<1>(acc, partials, ticket, out, 1);
+}
+
+void launch_fcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* r, const double* g_zq,
+                    const double* g_pq, int nranks, const RedSite* red, double* red_out, cudaStream_t s) {
+  const int g = std::min(vec_grid(ctx, n), red->grid);
+  launch_k(fcg_dir_kernel, g, kBlock, 0, s, n, z, p, r, g_zq, g_pq, nranks, red->partials, red->ticket, red_out);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+// ------------------------------------------- coarsest PCG, launch-per-step form
+// ("at most 40 iterations of the Preconditioned CG coupled to l1-Jacobi
+// preconditioner").  The host records all maxit iterations into the iteration
+// graph; `done` turns the remaining steps into no-ops once the coarse residual
+// test (or a breakdown) fires.  Every CTA takes the same decision from the same
+// gathered scalars, so either all CTAs enter a reduction or none does.
+__device__ __forceinline__ int ld_flag(const int* f) { return *(const volatile int*)f; }
+
+__global__ void __launch_bounds__(kBlock) cpcg_init_kernel(int64_t n, const double* __restrict__ b,
+                                                           const double* __restrict__ dinv, double* __restrict__ x,
+                                                           double* __restrict__ r, double* __restrict__ z,
+                                                           double* __restrict__ p, int* done, double* partials,
+                                                           unsigned int* ticket, double* out, int stride) {
+  pdl_enter();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *done = 0;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double bi = b[i];
+    const double zi = dinv[i] * bi;
+    x[i] = 0.0;
+    r[i] = bi;
+    z[i] = zi;
+    p[i] = zi;
+    acc[0] += bi * zi;
+    acc[1] += bi * bi;
+  }
+  pdl_exit();
+  grid_reduce<2>(acc, partials, ticket, out, stride);
+}
+
+__global__ void __launch_bounds__(kBlock) cpcg_update_kernel(int64_t n, double* __restrict__ x,
+                                                             const double* __restrict__ p, double* __restrict__ r,
+                                                             const double* __restrict__ q, double* __restrict__ z,
+                                                             const double* __restrict__ dinv, const double* g_pq,
+                                                             const double* g_rz, int nr, int* done, double* partials,
+                                                             unsigned int* ticket, double* out, int stride) {
+  pdl_enter();
+  if (ld_flag(done)) return;
+  const double pq = gsum(g_pq, nr);
+  if (!(pq > 0.0)) {  // breakdown (or b = 0): keep x
+    if (blockIdx.x == 0 && threadIdx.x == 0) *done = 1;
+    return;
+  }
+  const double alpha = gsum(g_rz, nr) / pq;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = x[i] + alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    const double zi = dinv[i] * ri;
+    r[i] = ri;
+    z[i] = zi;
+    acc[0] += ri * ri;
+    acc[1] += ri * zi;
+  }
+  pdl_exit();
+  grid_reduce<2>(acc, partials, ticket, out, stride);
+}
+
+__global__ void __launch_bounds__(kBlock) cpcg_dir_kernel(int64_t n, const double* __restrict__ z,
+                                                          double* __restrict__ p, const double* g_rr,
+                                                          const double* g_bb, const double* g_rzn, const double* g_rz,
+                                                          int nr, double tol, int* done) {
+  pdl_enter();
+  if (ld_flag(done)) return;
+  if (sqrt(gsum(g_rr, nr)) <= tol * sqrt(gsum(g_bb, nr))) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *done = 1;
+    return;
+  }
+  const double beta = gsum(g_rzn, nr) / gsum(g_rz, nr);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+  pdl_exit();
+}
+
+void launch_cpcg_init(psc_ctx* ctx, int64_t n, const double* b, const double* dinv, double* x, double* r, double* z,
+                      double* p, int* done, const RedSite* red, double* out, int stride, cudaStream_t s) {
+  const int g = std::min(vec_grid(ctx, n), red->grid);
+  launch_k(cpcg_init_kernel, g, kBlock, 0, s, n, b, dinv, x, r, z, p, done, red->partials, red->ticket, out, stride);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+void launch_cpcg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q, double* z,
+                        const double* dinv, const double* g_pq, const double* g_rz, int nr, int* done,
+                        const RedSite* red, double* out, int stride, cudaStream_t s) {
+  const int g = std::min(vec_grid(ctx, n), red->grid);
+  launch_k(cpcg_update_kernel, g, kBlock, 0, s, n, x, p, r, q, z, dinv, g_pq, g_rz, nr, done, red->partials,
+           red->ticket, out, stride);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+void launch_cpcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rr, const double* g_bb,
+                     const double* g_rzn, const double* g_rz, int nr, double tol, int* done, cudaStream_t s) {
+  launch_k(cpcg_dir_kernel, vec_grid(ctx, n), kBlock, 0, s, n, z, p, g_rr, g_bb, g_rzn, g_rz, nr, tol, done);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -1614,6 +1742,131 @@ void launch_coarse_dense(psc_ctx* ctx, const double* Ad, int64_t n, const double
                          int nsweeps, cudaStream_t s) {
   PSC_REQUIRE(n <= coarse_dense_max_rows(), PSC_ERR_STATE, "coarsest level too large for the dense solver");
   launch_k(coarse_dense, 1, kDenseWarps * 32, 0, s, Ad, (int)n, dinv, b, x, nsweeps, 0);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+// Dense one-CTA coarsest PCG with the l1-Jacobi preconditioner, same
+// register blocking of A as coarse_dense for q = A p (all 24 warps, p from
+// shared memory); the vector recurrences and the fixed-order reductions
+// (per-lane partials over c = 0..4, then an xor butterfly) run in warp 0 with
+// x, r, p, dinv in shared memory; two CTA barriers per iteration.  The stop
+// decision (||r|| <= tol ||b||, or p^T A p <= 0) is taken by warp 0 and read by
+// all warps after a barrier.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kDenseWarps * 32, 1) coarse_dense_pcg(const double* __restrict__ Ad, int n,
+                                                                      const double* __restrict__ dinv,
+                                                                      const double* __restrict__ b,
+                                                                      double* __restrict__ xout, int maxit,
+                                                                      double tol) {
+  pdl_enter();
+  constexpr int V = 32 * kCC;
+  __shared__ double ps[V], qs[V], xs[V], rs[V], ds[V];
+  __shared__ int stop_s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double a[kCR][kCC];
+#pragma unroll
+  for (int m = 0; m < kCR; ++m) {
+    const int i = w + kDenseWarps * m;
+#pragma unroll
+    for (int c = 0; c < kCC; ++c) {
+      const int j = lane + 32 * c;
+      a[m][c] = (i < n && j < n) ? __ldg(Ad + (size_t)i * n + j) : 0.0;
+    }
+  }
+  double rz = 0.0, nb = 0.0;  // warp 0
+  if (w == 0) {
+    double rz_l = 0.0, bb_l = 0.0;
+#pragma unroll
+    for (int c = 0; c < kCC; ++c) {
+      const int j = lane + 32 * c;
+      const double bj = j < n ? b[j] : 0.0;
+      const double dj = j < n ? dinv[j] : 0.0;
+      const double zj = dj * bj;
+      xs[j] = 0.0;
+      rs[j] = bj;
+      ds[j] = dj;
+      ps[j] = zj;
+      qs[j] = 0.0;
+      rz_l += bj * zj;
+      bb_l += bj * bj;
+    }
+    rz = warp_sum(rz_l);
+    nb = sqrt(warp_sum(bb_l));
+    if (lane == 0) stop_s = !(nb > 0.0);
+  }
+  __syncthreads();
+  for (int k = 1; k <= maxit; ++k) {
+    if (stop_s) break;
+    // q = A p
+    double pj[kCC];
+#pragma unroll
+    for (int c = 0; c < kCC; ++c) pj[c] = ps[lane + 32 * c];
+#pragma unroll
+    for (int m = 0; m < kCR; ++m) {
+      double sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < kCC; ++c) sum = fma(a[m][c], pj[c], sum);
+      sum = warp_sum(sum);
+      const int i = w + kDenseWarps * m;
+      if (lane == m && i < n) qs[i] = sum;
+    }
+    __syncthreads();
+    if (w == 0) {
+      double pq_l = 0.0;
+#pragma unroll
+      for (int c = 0; c < kCC; ++c) pq_l += ps[lane + 32 * c] * qs[lane + 32 * c];
+      const double pq = warp_sum(pq_l);
+      int stop = 0;
+      if (!(pq > 0.0)) {
+        stop = 1;  // breakdown: keep x
+      } else {
+        const double alpha = rz / pq;
+        double rr_l = 0.0;
+#pragma unroll
+        for (int c = 0; c < kCC; ++c) {
+          const int j = lane + 32 * c;
+          xs[j] = xs[j] + alpha * ps[j];
+          const double rj = rs[j] - alpha * qs[j];
+          rs[j] = rj;
+          rr_l += rj * rj;
+        }
+        if (sqrt(warp_sum(rr_l)) <= tol * nb) {
+          stop = 1;
+        } else {
+          double rz_l = 0.0;
+#pragma unroll
+          for (int c = 0; c < kCC; ++c) {
+            const int j = lane + 32 * c;
+            rz_l += rs[j] * (ds[j] * rs[j]);
+          }
+          const double rzn = warp_sum(rz_l);
+          const double beta = rzn / rz;
+          rz = rzn;
+#pragma unroll
+          for (int c = 0; c < kCC; ++c) {
+            const int j = lane + 32 * c;
+            ps[j] = ds[j] * rs[j] + beta * ps[j];
+          }
+        }
+      }
+      if (lane == 0) stop_s = stop;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xs[i];
+  pdl_exit();
+}
+
+void launch_coarse_dense_pcg(psc_ctx* ctx, const double* Ad, int64_t n, const double* dinv, const double* b,
+                             double* x, int maxit, double tol, cudaStream_t s) {
+  PSC_REQUIRE(n <= coarse_dense_max_rows(), PSC_ERR_STATE, "coarsest level too large for the dense solver");
+  launch_k(coarse_dense_pcg, 1, kDenseWarps * 32, 0, s, Ad, (int)n, dinv, b, x, maxit, tol);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }

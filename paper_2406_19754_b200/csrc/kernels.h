@@ -12,7 +12,8 @@ enum class RowOp {
   Spmv,       // y = alpha s + beta y           (beta == 0: y not read)
   SpmvDot,    // y = s;  red0 += x_i * s        (q = A p and (p, q))
   Sweep,      // y = x_i + dinv_i (b_i - s)     (l1-Jacobi sweep, Jacobi: reads old x)
-  SweepDot,   // Sweep, red0 += b_i * y_i       (last level-0 post-sweep: (r, z))
+  SweepDot,   // Sweep, red0 += w_i * y_i, w = b unless RowArgs::w is set
+              // (last level-0 post-sweep: (r, z) for PCG, (z, A p_old) for FCG)
   Resid,      // y = b_i - s
   ResidDot2,  // y = b_i - s; red0 += y_i^2; red1 += b_i^2
   PAdd,       // y += s                         (prolongation x_l += P x_{l+1})
@@ -51,6 +52,7 @@ struct RowArgs {
   double* y = nullptr;
   double* y2 = nullptr;        // Spmv only: y2 = dinv2 .* y
   const double* dinv2 = nullptr;
+  const double* w = nullptr;   // SweepDot only: weight of the reduction (nullptr: b)
   const RedSite* red = nullptr;
   double* red_out = nullptr;   // red0 -> red_out[0], red1 -> red_out[red_stride]
   int red_stride = 1;
@@ -72,11 +74,15 @@ void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, 
 // m_i = a_ii + sum_{j != i} |a_ij| over the stored row;  dinv_i = 1 / m_i
 void launch_l1_dinv(psc_ctx* ctx, const Sell& A, double* dinv, cudaStream_t s);
 // gathered scalars: value of slot = sum over ranks of g[slot*nranks + r], in rank order
-// CG: alpha = rz_old / pq ; x += alpha p ; r -= alpha q ; red(r.r)
+// CG: alpha = num / pq ; x += alpha p ; r -= alpha q ; red(r.r)
+// num = sum of g_num[0..num_ranks-1] (PCG: rz_old, 1 entry; FCG: gathered (p, r))
 // (optionally z0 = dinv .* r: the first level-0 sweep of the next V-cycle)
 void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
-                      const double* g_pq, const double* rz_old, int nranks, const RedSite* red, double* red_out,
-                      cudaStream_t s, const double* dinv = nullptr, double* z0 = nullptr);
+                      const double* g_pq, const double* g_num, int num_ranks, int nranks, const RedSite* red,
+                      double* red_out, cudaStream_t s, const double* dinv = nullptr, double* z0 = nullptr);
+// FCG(1) direction: beta = (z, q_old) / (p_old, q_old) (both gathered); p = z - beta p; red(p.r)
+void launch_fcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* r, const double* g_zq,
+                    const double* g_pq, int nranks, const RedSite* red, double* red_out, cudaStream_t s);
 // beta = rz / rz_old ; p = z + beta p ; then rz_old := rz (by the last CTA)
 void launch_xpby(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rz, double* rz_old,
                  int nranks, const RedSite* red, cudaStream_t s);
@@ -99,6 +105,24 @@ int64_t coarse_dense_max_rows();
 void dense_from_sell(psc_ctx* ctx, const Sell& A, double* dense, cudaStream_t s);
 void launch_coarse_dense(psc_ctx* ctx, const double* dense, int64_t n, const double* dinv, const double* b, double* x,
                          int nsweeps, cudaStream_t s);
+
+// Coarsest-level PCG with the l1-Jacobi preconditioner, dense one-CTA form:
+// x = PCG(A, b) from zero, at most maxit iterations, stop when ||r|| <= tol ||b||.
+void launch_coarse_dense_pcg(psc_ctx* ctx, const double* dense, int64_t n, const double* dinv, const double* b,
+                             double* x, int maxit, double tol, cudaStream_t s);
+// ... and its general (launch-per-step) form; scalars are gathered partials
+// (nr entries each, summed in rank order), `done` a device stop flag:
+//   init:   x = 0, r = b, z = dinv r, p = z; red (r, z) -> out[0], (b, b) -> out[stride]; done = 0
+//   update: if !done: pq = (p, q); pq <= 0: done; else alpha = rz / pq, x += alpha p,
+//           r -= alpha q, z = dinv r; red (r, r) -> out[0], (r, z) -> out[stride]
+//   dir:    if !done: ||r|| <= tol ||b||: done; else p = z + (rz_new / rz) p
+void launch_cpcg_init(psc_ctx* ctx, int64_t n, const double* b, const double* dinv, double* x, double* r, double* z,
+                      double* p, int* done, const RedSite* red, double* out, int stride, cudaStream_t s);
+void launch_cpcg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q, double* z,
+                        const double* dinv, const double* g_pq, const double* g_rz, int nr, int* done,
+                        const RedSite* red, double* out, int stride, cudaStream_t s);
+void launch_cpcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rr, const double* g_bb,
+                     const double* g_rzn, const double* g_rz, int nr, double tol, int* done, cudaStream_t s);
 
 // CSR (global int64 columns) -> sliced ELL with local int32 columns.
 // lanes: 0 = choose from the mean row length (choose_lanes), else 1 / 4 / 8 / 16 / 32.

@@ -68,6 +68,17 @@ def main():
     rc, st, hist = H.solve(torch.from_numpy(b[r0:r1].copy()).cuda(), x, tol=1e-8, maxit=200)
     parts = [None] * world
     dist.all_gather_object(parts, (z.cpu().numpy(), x.cpu().numpy(), rc, st["iters"], hist))
+    # the paper's VBM solve (NEXT-2): coarsest PCG(<= 40) with l1-Jacobi + FCG, on
+    # the same matrices (a general-form coarse PCG with all-gathers when the
+    # coarsest level is distributed, PSC_REPL_ROWS=0)
+    H2 = psc.Hierarchy(ctx, A, P, R, coarse_solver="pcg")
+    z2 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+    H2.vcycle(torch.from_numpy(b[r0:r1].copy()).cuda(), z2)
+    x2 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+    rc2, st2, hist2 = H2.solve(torch.from_numpy(b[r0:r1].copy()).cuda(), x2, tol=1e-8, maxit=200, method="fcg")
+    parts2 = [None] * world
+    dist.all_gather_object(parts2, (z2.cpu().numpy(), x2.cpu().numpy(), rc2, st2["iters"], hist2))
+    H2.close()
     ok = True
     if rank == 0:
         import oracle
@@ -97,6 +108,19 @@ def main():
         out["hist_identical_across_ranks"] = same_hist
         ok &= (len(its) == 1 and abs(parts[0][3] - ito) <= 1 and all(p[2] == 0 for p in parts)
                and out["hist_rel"] <= 1e-9 and out["x_rel"] <= 1e-7 and same_hist)
+        zg2 = np.concatenate([p[0] for p in parts2])
+        zo2 = oracle.vcycle(h, b, coarse_pcg=True)
+        out["vbm_vcycle_rel"] = float(np.linalg.norm(zg2 - zo2) / np.linalg.norm(zo2))
+        xg2 = np.concatenate([p[1] for p in parts2])
+        xo2, ito2, sto2, histo2 = oracle.fcg(h, b, tol=1e-8, maxit=200, coarse_pcg=True)
+        its2 = {p[3] for p in parts2}
+        k2 = min(20, ito2, parts2[0][3]) + 1
+        out.update(vbm_iters_gpu=sorted(its2), vbm_iters_oracle=ito2,
+                   vbm_hist_rel=float(np.max(np.abs(parts2[0][4][:k2] - histo2[:k2]) / histo2[:k2])),
+                   vbm_x_rel=float(np.linalg.norm(xg2 - xo2) / np.linalg.norm(xo2)))
+        ok &= (out["vbm_vcycle_rel"] <= 1e-9 and len(its2) == 1 and abs(parts2[0][3] - ito2) <= 1
+               and all(p[2] == 0 for p in parts2) and out["vbm_hist_rel"] <= 1e-9 and out["vbm_x_rel"] <= 1e-7
+               and all(np.array_equal(parts2[0][4], p[4]) for p in parts2))
         out["ok"] = bool(ok)
         print(json.dumps(out), flush=True)
     flag = [ok]
