@@ -13,6 +13,11 @@ Metric: Mdof*iters/s = N_global * iterations / solve seconds / 1e6 (whole job).
 
 --impl reference runs the CPU oracle (oracle/, single thread) on rank 0 only,
 each step one PCG iteration on a 256^3 single-box sample of the same workload.
+
+--vbm (= --krylov fcg --coarse-solver pcg) times the paper's VBM solve
+configuration instead: FCG(1) outer
+iterations and a coarsest-level PCG with l1-Jacobi (at most 40 iterations to
+1e-10 relative).
 """
 from __future__ import annotations
 
@@ -154,30 +159,53 @@ def run_reference(args, rank, world, out=sys.stdout):
     import oracle
     import pscgen
     g = args.grid
-    h = pscgen.poisson_hierarchy(g, g, g, (1, 1, 1))
+    h = pscgen.poisson_hierarchy(g, g, g, (1, 1, 1), problem=args.problem)
     n = h.levels[0].n
     b = pscgen.rhs_poisson((g, g, g), 0, n)
     times = []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        x, it, st, hist = oracle.pcg(h, b * (k + 1), tol=0.0, maxit=1)
+        x, it, st, hist = _oracle_solve(args)(h, b * (k + 1), tol=0.0, maxit=1, **_oracle_kw(args))
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             times.append(dt)
     t = sum(times)
     value = n * args.steps / t / 1e6
     line = {
-        "impl": "reference", "metric": "AMG-PCG Mdof*iters/s", "value": value, "unit": "Mdof*iters/s",
+        "impl": "reference", "metric": _metric(args), "value": value, "unit": "Mdof*iters/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"3D Poisson 7-point {g}^3 single-box sample of the {g}^3-per-GPU weak-scaling "
-                               "workload (BASELINE.json configs[2]); step = 1 PCG iteration of the CPU oracle",
-                   "levels": h.nlevels, "n_dof": n},
+        "config": {"workload": f"3D {args.problem} 7-point {g}^3 single-box sample of the {g}^3-per-GPU weak-scaling "
+                               f"workload (BASELINE.json configs[{4 if args.problem == 'jump' else 2}]); step = 1 "
+                               f"{args.krylov.upper()} iteration of the CPU oracle",
+                   "levels": h.nlevels, "n_dof": n, "solver": _solver_desc(args)},
         "cpu_baseline": {"value": value, "unit": "Mdof*iters/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} steps x 1 PCG iteration (incl. its V-cycles) on {g}^3"},
+                         "sample": f"{args.steps} steps x 1 {args.krylov.upper()} iteration (incl. its V-cycles) "
+                                   f"on {g}^3"},
         "e2e": {"value": value, "unit": "Mdof*iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), file=out, flush=True)
+
+
+def _metric(args):
+    """The metric string, identical on both arms (--impl psc / reference)."""
+    scope = f"{args.global_grid}^3 global" if args.global_grid > 0 else f"{args.grid}^3 dof per GPU"
+    return f"AMG-{args.krylov.upper()} Mdof*iters/s (3D {args.problem}, {scope}, tol {args.tol:g})"
+
+
+def _oracle_solve(args):
+    import oracle
+    return oracle.fcg if args.krylov == "fcg" else oracle.pcg
+
+
+def _oracle_kw(args):
+    return dict(coarse_pcg=True, coarse_maxit=40, coarse_tol=1e-10) if args.coarse_solver == "pcg" else {}
+
+
+def _solver_desc(args):
+    coarse = ("coarsest PCG(<=40, 1e-10) with l1-Jacobi" if args.coarse_solver == "pcg"
+              else "30 coarsest l1-Jacobi sweeps")
+    return f"{args.krylov.upper()}, V(4,4) l1-Jacobi, {coarse}"
 
 
 # ------------------------------------------------------------------- main
@@ -207,7 +235,12 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=2, help="oracle PCG iterations in the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--krylov", default="pcg", choices=["pcg", "fcg"])
+    ap.add_argument("--coarse-solver", default="sweeps", choices=["sweeps", "pcg"])
+    ap.add_argument("--vbm", action="store_true", help="the paper's VBM solve: --krylov fcg --coarse-solver pcg")
     args = ap.parse_args()
+    if args.vbm:
+        args.krylov, args.coarse_solver = "fcg", "pcg"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -264,7 +297,7 @@ def main():
         uid = obj[0]
     ctx = psc.Context(rank=rank, nranks=N, device=local, unique_id=uid)
     t1 = time.perf_counter()
-    H, descs, A, P, R = psc.build_hierarchy(ctx, levels)
+    H, descs, A, P, R = psc.build_hierarchy(ctx, levels, coarse_solver=args.coarse_solver)
     t_build = time.perf_counter() - t1
     info = H.info()
     n_loc = info["n_owned"][0]
@@ -289,7 +322,7 @@ def main():
         return float(t.item())
 
     for k in range(args.warmup):
-        H.solve(bs[k], xs[k], tol=args.tol, maxit=args.maxit)
+        H.solve(bs[k], xs[k], tol=args.tol, maxit=args.maxit, method=args.krylov)
 
     barrier()
     clocks = ClockSampler() if local == 0 else None
@@ -297,7 +330,7 @@ def main():
     stats = []
     e0.record(lib_stream)
     for k in range(args.warmup, nsteps):
-        rc, st, hist = H.solve(bs[k], xs[k], tol=args.tol, maxit=args.maxit)
+        rc, st, hist = H.solve(bs[k], xs[k], tol=args.tol, maxit=args.maxit, method=args.krylov)
         stats.append(st)
     e1.record(lib_stream)
     barrier()
@@ -326,13 +359,13 @@ def main():
     if not args.no_e2e:
         bh = [torch.from_numpy(b_base * (k + 1)).pin_memory().numpy() for k in range(args.steps)]
         xh = [torch.zeros(n_loc, dtype=torch.float64).pin_memory().numpy() for _ in range(args.steps)]
-        H.solve_host(bh[0], xh[0].copy(), tol=args.tol, maxit=args.maxit)  # warm
+        H.solve_host(bh[0], xh[0].copy(), tol=args.tol, maxit=args.maxit, method=args.krylov)  # warm
         barrier()
         e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         it_h, h2d, d2h = 0, 0, 0
         e2.record(lib_stream)
         for k in range(args.steps):
-            rc, st, hist = H.solve_host(bh[k], xh[k], tol=args.tol, maxit=args.maxit)
+            rc, st, hist = H.solve_host(bh[k], xh[k], tol=args.tol, maxit=args.maxit, method=args.krylov)
             it_h += st["iters"]
             h2d += st["h2d_bytes"]
             d2h += st["d2h_bytes"]
@@ -341,17 +374,17 @@ def main():
         te = maxover(e2.elapsed_time(e3) * 1e-3)
         e2e = {"value": n_global * it_h / te / 1e6, "unit": "Mdof*iters/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-               "api": "psc_pcg_solve_host"}
+               "api": "psc_krylov_solve_host"}
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         import oracle
         bcpu = pscgen.rhs_poisson(grid, 0, n_global)
         t0 = time.perf_counter()
-        oracle.pcg(h, bcpu, tol=0.0, maxit=args.cpu_iters)
+        _oracle_solve(args)(h, bcpu, tol=0.0, maxit=args.cpu_iters, **_oracle_kw(args))
         tc = time.perf_counter() - t0
         cpu = {"value": n_global * args.cpu_iters / tc / 1e6, "unit": "Mdof*iters/s", "cores": 1, "kind": "oracle",
-               "sample": f"{args.cpu_iters} PCG iterations (tol 0) of the same {grid[0]}x{grid[1]}x{grid[2]} "
+               "sample": f"{args.cpu_iters} {args.krylov.upper()} iterations (tol 0) of the same {grid[0]}x{grid[1]}x{grid[2]} "
                          f"workload, single thread, {tc:.1f} s"}
 
     if rank == 0:
@@ -364,8 +397,7 @@ def main():
         else:
             workload = f"3D {args.problem} 7-point {g}^3 dof per GPU, weak scaling (BASELINE.json configs[2])"
         line = {
-            "metric": f"AMG-PCG Mdof*iters/s (3D {args.problem}, "
-                      + (f"{grid[0]}^3 global" if strong else f"{g}^3 dof per GPU") + ", tol 1e-8)",
+            "metric": _metric(args),
             "value": value, "unit": "Mdof*iters/s", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -373,7 +405,7 @@ def main():
                 "workload": workload,
                 "global_grid": list(grid), "procs": [px, py, pz], "n_global": n_global, "levels": info["nlevels"],
                 "rows_rank0": info["n_owned"], "nnz_A_rank0": info["nnz_A"], "operator_complexity": oc,
-                "cycle": "V(4,4) l1-Jacobi, 30 coarsest sweeps", "tol": args.tol, "iters": iters,
+                "cycle": _solver_desc(args), "tol": args.tol, "iters": iters,
                 "solve_s_median": statistics.median(solve_s), "solve_s_per_step": solve_s,
                 "rhs": "b_k = (k+1) h^2 1, x0 = 0", "parallelism": f"dp{N} row-block",
                 "l2": "inputs larger than L2 (A_0 alone ~1.4 GB/GPU vs 126 MB L2)",
