@@ -210,10 +210,12 @@ typedef struct {
   int64_t collectives;          /* NCCL calls issued during the solve */
   double dom_kernel_seconds;    /* summed device time of the level-0 l1-Jacobi sweep launches */
   int64_t dom_kernel_launches;  /* number of those launches */
-  double dom_kernel_bytes;      /* algorithmic bytes per launch: 12 nnz(A_0) + 32 n_0 */
+  double dom_kernel_bytes;      /* algorithmic bytes per launch: 8 nnz(A_0) + 4 nnz_ell(A_0) + 32 n_0 */
   int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by psc_pcg_solve_host */
   int halo_path;                /* 0 single rank, 1 NVLink peer stores (CUDA IPC), 2 NCCL */
   int iter_graph_nodes;         /* kernel launches per PCG iteration (captured graph) */
+  int dom_kernel_sweeps;        /* l1-Jacobi sweeps done by one timed launch: 1, or post_sweeps when the
+                                   level-0 post-smoothing runs as one fused wavefront pass */
 } psc_stats;
 
 /* [collective] PCG (reading R1 of DESIGN.md) preconditioned by one

@@ -44,6 +44,10 @@ struct LevelWS {
   bool one_cta = false;       // sparse one-CTA solver applies
   double* cz = nullptr;       // general coarsest PCG: z and q = A p (n)
   double* cq = nullptr;
+  // wavefront passes (sell_wave): dependency reach in 256-row chunks, chunk
+  // counters + watermarks; wave_h < 0: the level runs stage by stage
+  int64_t wave_h = -1;
+  unsigned int* wave_flags = nullptr;
 };
 
 // Replicated suffix (nranks > 1): levels first..L-1 are held whole on every
@@ -287,6 +291,79 @@ int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream
 
 bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
 
+// ------------------------------------------------------- wavefront passes
+// (sell_wave, kernels.cu) on levels whose A qualifies: single rank (no halo),
+// slices at most 8 wide.  Opt-in (PSC_WAVE=1) until measured.
+int64_t wave_slack(psc_hier* h, int nst) {
+  const char* e = getenv("PSC_WAVE_SLACK");
+  return e ? std::max(0, atoi(e)) : std::max<int64_t>(8, 2 * (int64_t)h->ctx->num_sms / std::max(nst, 1));
+}
+
+void wave_setup(psc_hier* h, LevelWS& W) {
+  if (!getenv("PSC_WAVE") || h->ctx->nranks != 1 || W.nh != 0 || !wave_supported(W.A->S)) return;
+  const int64_t bw = sell_bandwidth(h->ctx, W.A->S, h->ctx->stream);
+  W.wave_h = (bw + kWaveChunkRows - 1) / kWaveChunkRows;
+  W.wave_flags = dalloc<unsigned int>((size_t)kWaveMaxStages * (wave_chunks(W.A->S) + 1));
+}
+
+void wave_launch(psc_hier* h, LevelWS& W, WaveArgs& a, cudaStream_t s) {
+  a.h = W.wave_h;
+  a.G = W.wave_h + 1 + wave_slack(h, a.nst);
+  a.flags = W.wave_flags;
+  launch_wave(h->ctx, W.A->S, a, s);
+}
+
+// pre-smoothing and the residual of the coarse-grid correction in one pass:
+// [x0 = M^-1 b,] pre-1 sweeps, r = b - A x.  Returns the buffer index of x.
+int wave_pre(psc_hier* h, LevelWS& W, const double* b, int pre, bool first_done, cudaStream_t s) {
+  WaveArgs a;
+  a.b = b;
+  a.dinv = W.dinv;
+  int cur = 0;
+  if (!first_done) {
+    a.op[a.nst] = (int)WaveOp::Scale;
+    a.xin[a.nst] = nullptr;
+    a.xout[a.nst++] = W.x[0];
+  }
+  for (int k = 1; k < pre; ++k) {
+    a.op[a.nst] = (int)WaveOp::Sweep;
+    a.xin[a.nst] = W.x[cur];
+    a.xout[a.nst++] = W.x[cur ^ 1];
+    cur ^= 1;
+  }
+  a.op[a.nst] = (int)WaveOp::Resid;
+  a.xin[a.nst] = W.x[cur];
+  a.xout[a.nst++] = W.r;
+  wave_launch(h, W, a, s);
+  return cur;
+}
+
+// post-smoothing: `post` sweeps from x[cur]; the last one reduces (w, x) into
+// red_out when red_out is set.  Returns the buffer index of x.
+int wave_post(psc_hier* h, LevelWS& W, const double* b, int post, int cur, double* red_out, cudaStream_t s) {
+  WaveArgs a;
+  a.b = b;
+  a.dinv = W.dinv;
+  for (int k = 0; k < post; ++k) {
+    a.op[a.nst] = (int)((red_out && k == post - 1) ? WaveOp::SweepDot : WaveOp::Sweep);
+    a.xin[a.nst] = W.x[cur];
+    a.xout[a.nst++] = W.x[cur ^ 1];
+    cur ^= 1;
+  }
+  if (red_out) {
+    a.reduce = 1;
+    a.w = h->rz_weight;
+    a.partials = h->red1.partials;
+    a.ticket = h->red1.ticket;
+    a.red_grid = h->red1.grid;
+    a.red_out = red_out;
+  }
+  wave_launch(h, W, a, s);
+  return cur;
+}
+
+bool wave_fits(const LevelWS& W, int nst) { return W.wave_h >= 0 && nst >= 1 && nst <= kWaveMaxStages; }
+
 double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b, cudaStream_t s, bool timing,
                    bool first_done, bool dist);
 
@@ -320,10 +397,14 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   LevelWS& C = LV[l + 1];
   const bool time_here = timing && dist && l == 0;
   const bool next_replicated = dist && h->rep.on && l + 1 == h->rep.first;
-  // (I - M^-1 A)^pre
-  int cur = pre_smooth(h, W, b, h->opt.pre_sweeps, s, time_here, first_done);
-  // coarse-grid correction (I - P B_{l+1} P^T A): r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
-  {
+  // (I - M^-1 A)^pre, then the coarse-grid correction (I - P B_{l+1} P^T A):
+  // r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
+  const int pre = h->opt.pre_sweeps;
+  int cur;
+  if (pre > 0 && wave_fits(W, pre + (first_done ? 0 : 1))) {
+    cur = wave_pre(h, W, b, pre, first_done, s);  // sweeps + residual in one pass
+  } else {
+    cur = pre_smooth(h, W, b, pre, s, time_here, first_done);
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
@@ -358,6 +439,16 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
   const int post = h->opt.post_sweeps;
   const bool level0 = dist && l == 0;
+  if (post > 0 && wave_fits(W, post)) {
+    const bool t = time_here && h->dom_used + 2 <= (int)h->ev_dom.size();
+    if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
+    cur = wave_post(h, W, b, post, cur, level0 ? scal_mine(h, S_RZ) : nullptr, s);
+    if (t) {
+      PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
+      h->dom_used += 2;
+    }
+    return W.x[cur];
+  }
   for (int k = 0; k < post; ++k) {
     const bool last0 = (level0 && k == post - 1);
     RowArgs a;
@@ -620,6 +711,7 @@ void free_hier(psc_hier* h) {
     if (&W != &h->lv[0]) dfree(W.b);
     dfree(W.cz);
     dfree(W.cq);
+    dfree(W.wave_flags);
   }
   Replica& rp = h->rep;
   for (auto& W : rp.lv) {
@@ -759,6 +851,9 @@ int solve_impl(psc_hier* h, int method, const double* b, double* x, double tol, 
   // bytes the level-0 sweep must move in its layout: 8 B per stored value, 4 B per
   // explicit column index (ELL slices), x in, b, dinv, x out
   S.dom_kernel_bytes = 8.0 * (double)W.A->nnz + 4.0 * (double)W.A->S.nnz_ell + 32.0 * (double)W.n;
+  // the timed launch: one sweep, or the fused post-smoothing pass (A, b, 1/M and x
+  // read once, x written once: the same algorithmic bytes for `post` sweeps)
+  S.dom_kernel_sweeps = (h->L > 1 && wave_fits(W, h->opt.post_sweeps)) ? h->opt.post_sweeps : 1;
   S.h2d_bytes = (int64_t)extra_h2d;
   S.halo_path = R == 1 ? 0 : (h->p2p.on ? 1 : 2);
   S.iter_graph_nodes = (int)h->iter_launches[method];
@@ -892,6 +987,7 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       p2p_setup(ctx, h->p2p, hb, gs, ld, (char*)flagbuf - h->arena);
     } else {
       level_coarse_solver(h, Wc);
+      for (int l = 0; l + 1 < nlevels; ++l) wave_setup(h, h->lv[l]);
     }
     if (h->opt.coarse_solver == PSC_COARSE_PCG) {  // buffers of the general coarsest PCG
       LevelWS& C = h->rep.on ? h->rep.lv.back() : Wc;

@@ -942,6 +942,242 @@ static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_s
   launch_k(sell_tma<OP>, grid, kTmaThreads, kTmaSmem, s, a, nchunks, n_slices);
 }
 
+// ------------------------------------------ wavefront multi-stage pass (sell_wave)
+// Several consecutive row-wise stages of one V-cycle level over the same square
+// matrix A without halo columns — [x = M^-1 b,] k l1-Jacobi sweeps[, r = b - A x]
+// — in ONE persistent launch, so that A, b and 1/M stream from HBM once per pass
+// and are re-read from L2 by the later stages.  Every stage does exactly the row
+// arithmetic of the separate kernels (same FMA order), so the results are
+// bit-identical to launching the stages one by one.
+//
+// Work item = (stage s, chunk k of 8 slices = 256 rows).  A row of chunk k reads
+// x only in chunks k-h .. k+h (h from the matrix bandwidth), so stage s may
+// process chunk k once stage s-1 has completed every chunk <= k+h.  With two
+// ping-pong x buffers that one rule also orders the write of x^(s) over x^(s-2)
+// after the last stage-(s-1) read of it.  Items are dealt round-robin in the
+// order of the key k + G s (G = h + 1 + slack, so an item's dependencies were
+// dealt ~slack*stages items earlier); every CTA handles its items in that order
+// and all CTAs are co-resident, so the earliest unfinished item can always run.
+// Completion: every consumer warp fences its stores and bumps the chunk's
+// counter; the 8th bump publishes by advancing the stage's watermark (the
+// longest completed prefix of chunks) with release semantics; a waiting warp
+// acquire-polls the watermark.  Vectors written inside the pass are read through
+// L2 (ld.global.cg): L1 is not coherent across SMs.
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wave_wait(const unsigned int* wm, unsigned int need) {
+  if (ld_acquire_u32(wm) >= need) return;
+  const long long t0 = clock64();
+  while (ld_acquire_u32(wm) < need) {
+    __nanosleep(64);
+    if (clock64() - t0 > (1ll << 34)) __trap();  // ~9 s: a broken schedule fails loudly instead of hanging
+  }
+}
+
+__device__ __forceinline__ void wave_publish(unsigned int* flags, unsigned int* wm, unsigned int nchunks) {
+  unsigned int w = ld_acquire_u32(wm);
+  while (w < nchunks && ld_acquire_u32(flags + w) == (unsigned int)kTmaSlices) {
+    __threadfence();
+    const unsigned int old = atomicCAS(wm, w, w + 1);
+    w = (old == w) ? w + 1 : old;
+  }
+}
+
+__device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, int64_t& k) {
+  const int64_t K = m / a.nst;
+  s = (int)(m - K * a.nst);
+  k = K - a.G * s;
+}
+
+__global__ void __launch_bounds__(kTmaThreads) sell_wave(WaveArgs a) {
+  pdl_enter();
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaStageBytes);
+  uint64_t* empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTmaStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kTmaSlices);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
+  double acc[1] = {0.0};
+  if (warp == kTmaSlices) {
+    // ---------------- producer (one lane): matrix slices, b, 1/M of each item
+    if (lane == 0) {
+      uint64_t pol_stream, pol_keep;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+      int64_t it = 0;
+      for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
+        int s;
+        int64_t k;
+        wave_item(a, m, s, k);
+        if (k < 0 || k >= a.nchunks) continue;
+        const int op = a.op[s];
+        // re-read by a later stage: keep in L2; last reader: stream out
+        const uint64_t pol = (s + 1 < a.nst) ? pol_keep : pol_stream;
+        const int st = (int)(it % kTmaStages);
+        if (it >= kTmaStages) mbar_wait(&empty[st], (uint32_t)((it / kTmaStages - 1) & 1));
+        unsigned char* base = smem + st * kTmaStageBytes;
+        const int64_t s0 = k * kTmaSlices, s1 = min(s0 + kTmaSlices, a.n_slices);
+        const int64_t r0 = s0 * 32, r1 = min(s1 * 32, a.n_rows);
+        uint32_t hb = 0, vbytes = 0, cbytes = 0;
+        int64_t vb0 = 0, cb0 = 0;
+        if (op != (int)WaveOp::Scale) {
+          vb0 = a.ptr[s0];
+          cb0 = a.cptr[s0];
+          hb = (uint32_t)(s1 - s0) * kHdr * 4;
+          vbytes = (uint32_t)(a.ptr[s1] - vb0) * 8;
+          cbytes = (uint32_t)(a.cptr[s1] - cb0) * 4;
+        }
+        const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
+        const bool needd = (op != (int)WaveOp::Resid);
+        mbar_expect_tx(&full[st], hb + vbytes + cbytes + rbytes * (needd ? 2u : 1u));
+        if (hb) bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol);
+        if (vbytes) bulk_g2s(base + kTmaHdrBytes, a.val + vb0, vbytes, &full[st], pol);
+        if (cbytes) bulk_g2s(base + kTmaHdrBytes + kTmaValBytes, a.col + cb0, cbytes, &full[st], pol);
+        unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
+        if (rbytes) {
+          bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol);
+          if (needd) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol);
+        }
+        ++it;
+      }
+    }
+  } else {
+    // ---------------- consumers: warp `warp` takes slice 8k + warp of each item
+    const uint32_t nc = (uint32_t)a.ncols;
+    int64_t it = 0;
+    for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
+      int s;
+      int64_t k;
+      wave_item(a, m, s, k);
+      if (k < 0 || k >= a.nchunks) continue;
+      const int op = a.op[s];
+      const int st = (int)(it % kTmaStages);
+      mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
+      if (s > 0) {  // stage s-1 done on chunks <= k + h
+        if (lane == 0) wave_wait(a.wm + (s - 1), (unsigned int)min(k + a.h + 1, a.nchunks));
+        __syncwarp();
+      }
+      const double* xin = a.xin[s];
+      double* xout = a.xout[s];
+      const bool fresh = (s > 0);  // x produced inside this pass: read through L2
+      const unsigned char* base = smem + st * kTmaStageBytes;
+      const double* vec = reinterpret_cast<const double*>(base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes);
+      const int64_t sl = k * kTmaSlices + warp;
+      if (sl < a.n_slices) {
+        const uint32_t i = (uint32_t)(sl * 32 + lane);
+        const int rl = warp * 32 + lane;
+        double sum = 0.0;
+        if (op != (int)WaveOp::Scale) {
+          const int32_t* hs = reinterpret_cast<const int32_t*>(base);
+          const double* vs = reinterpret_cast<const double*>(base + kTmaHdrBytes);
+          const int32_t* cs = reinterpret_cast<const int32_t*>(base + kTmaHdrBytes + kTmaValBytes);
+          const int32_t h = lane < kHdr ? hs[warp * kHdr + lane] : 0;
+          const int32_t h0 = hs[0], h1 = hs[1], h2 = hs[2], h3 = hs[3];
+          const int64_t vbase = ((int64_t)(uint32_t)h1 << 32) | (uint32_t)h0;
+          const int64_t cbase = ((int64_t)(uint32_t)h3 << 32) | (uint32_t)h2;
+          const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
+                             (uint32_t)__shfl_sync(0xffffffffu, h, 0);
+          const int w = __shfl_sync(0xffffffffu, h, 4);
+          const bool dia = __shfl_sync(0xffffffffu, h, 5) != 0;
+          const double* v = vs + (vb - vbase) + lane;
+          double xv[kTmaMaxW];
+          if (dia) {
+#pragma unroll
+            for (int j = 0; j < kTmaMaxW; ++j) {
+              const uint32_t cj = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
+              const double* px = xin + (cj < nc ? cj : 0u);
+              xv[j] = (j < w) ? (fresh ? __ldcg(px) : __ldg(px)) : 0.0;
+            }
+          } else {
+            const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
+                               (uint32_t)__shfl_sync(0xffffffffu, h, 2);
+            const int32_t* cc = cs + (cb - cbase) + lane;
+#pragma unroll
+            for (int j = 0; j < kTmaMaxW; ++j) {
+              const double* px = xin + (j < w ? cc[32 * j] : 0);
+              xv[j] = (j < w) ? (fresh ? __ldcg(px) : __ldg(px)) : 0.0;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < kTmaMaxW; ++j)
+            if (j < w) sum = fma(v[32 * j], xv[j], sum);
+        }
+        if ((int64_t)i < a.n_rows) {
+          const double bi = vec[rl];
+          if (op == (int)WaveOp::Scale) {
+            xout[i] = vec[kTmaRows + rl] * bi;
+          } else if (op == (int)WaveOp::Resid) {
+            xout[i] = bi - sum;
+          } else {
+            const double xi = fresh ? __ldcg(xin + i) : __ldg(xin + i);
+            const double xn = xi + vec[kTmaRows + rl] * (bi - sum);
+            xout[i] = xn;
+            if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      // publish: this warp's stores, then the chunk counter; the 8th warp advances the watermark
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        unsigned int* fl = a.flags + (int64_t)s * a.nchunks;
+        const unsigned int old = atomicAdd(fl + k, 1u);
+        if (old == (unsigned int)kTmaSlices - 1) wave_publish(fl, a.wm + s, (unsigned int)a.nchunks);
+      }
+      ++it;
+    }
+  }
+  pdl_exit();
+  if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
+}
+
+bool wave_supported(const Sell& A) {
+  return A.lanes == 1 && A.max_width <= kTmaMaxW && A.hdr && A.n_units > 0 && A.n_cols_local == A.n_rows;
+}
+
+int64_t wave_chunks(const Sell& A) { return (A.n_units + kTmaSlices - 1) / kTmaSlices; }
+
+void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& in, cudaStream_t s) {
+  static int occ = -1;
+  if (occ < 0) {
+    PSC_CUDA(cudaFuncSetAttribute(sell_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+    PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sell_wave, kTmaThreads, kTmaSmem));
+  }
+  PSC_REQUIRE(occ >= 1, PSC_ERR_STATE, "sell_wave cannot be resident");
+  WaveArgs a = in;
+  a.ptr = A.ptr;
+  a.cptr = A.cptr;
+  a.hdr = A.hdr;
+  a.col = A.col;
+  a.val = A.val;
+  a.ncols = A.n_cols_local;
+  a.n_rows = A.n_rows;
+  a.n_slices = A.n_units;
+  a.nchunks = wave_chunks(A);
+  a.wm = a.flags + (size_t)a.nst * a.nchunks;
+  const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
+  // every CTA must be resident at once (items wait on other CTAs' items)
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)occ * ctx->num_sms));
+  PSC_REQUIRE(!a.reduce || grid <= a.red_grid, PSC_ERR_STATE, "reduction site too small");
+  PSC_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(unsigned int) * ((size_t)a.nst * a.nchunks + kWaveMaxStages), s));
+  launch_k(sell_wave, grid, kTmaThreads, kTmaSmem, s, a);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
 // ---------------------------------------------- TMA-staged row-group kernel
 // Same producer / consumer ring as sell_tma for the row-group layout: a chunk
 // is 8 units (8 x 32/G consecutive rows, contiguous in memory); the producer
@@ -1869,6 +2105,44 @@ void launch_coarse_dense_pcg(psc_ctx* ctx, const double* Ad, int64_t n, const do
   launch_k(coarse_dense_pcg, 1, kDenseWarps * 32, 0, s, Ad, (int)n, dinv, b, x, maxit, tol);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
+}
+
+// Row bandwidth of a square matrix in the sliced-ELL layout: max |j - i| over
+// the stored entries (DIA slices: their offsets; ELL padding repeats a real
+// column of the row, an empty row pads with column 0 — conservative).
+__global__ void sell_bw_kernel(const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
+                               const int32_t* __restrict__ col, int64_t n_rows, int64_t n_slices,
+                               unsigned long long* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_slices * 32) return;
+  const int64_t sl = i >> 5;
+  const int w = (int)((ptr[sl + 1] - ptr[sl]) >> 5);
+  const int64_t cb = cptr[sl];
+  const bool dia = (cptr[sl + 1] - cb) < 32 * (int64_t)w;
+  unsigned long long m = 0;
+  if (dia) {
+    if ((i & 31) == 0)
+      for (int k = 0; k < w; ++k) m = max(m, (unsigned long long)llabs((long long)col[cb + k]));
+  } else if (i < n_rows) {
+    for (int k = 0; k < w; ++k) m = max(m, (unsigned long long)llabs((long long)col[cb + 32 * (int64_t)k + (i & 31)] - i));
+  }
+  if (m) atomicMax(out, m);
+}
+
+int64_t sell_bandwidth(psc_ctx* ctx, const Sell& A, cudaStream_t s) {
+  PSC_REQUIRE(A.lanes == 1, PSC_ERR_STATE, "bandwidth: sliced ELL only");
+  if (A.n_units == 0) return 0;
+  unsigned long long* d = dalloc<unsigned long long>(1);
+  PSC_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
+  const int64_t nt = A.n_units * 32;
+  sell_bw_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(A.ptr, A.cptr, A.col, A.n_rows, A.n_units, d);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+  unsigned long long hbw = 0;
+  PSC_CUDA(cudaMemcpyAsync(&hbw, d, sizeof(hbw), cudaMemcpyDeviceToHost, s));
+  PSC_CUDA(cudaStreamSynchronize(s));
+  dfree(d);
+  return (int64_t)hbw;
 }
 
 // --------------------------------------------------------- CSR -> sliced ELL

@@ -124,6 +124,50 @@ void launch_cpcg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, dou
 void launch_cpcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rr, const double* g_bb,
                      const double* g_rzn, const double* g_rz, int nr, double tol, int* done, cudaStream_t s);
 
+// Wavefront multi-stage pass (sell_wave, kernels.cu): up to kWaveMaxStages
+// row-wise stages of one level over a square, halo-free, TMA-able matrix in one
+// persistent launch (A streamed from HBM once, re-read from L2 by later stages).
+enum class WaveOp : int {
+  Scale = 0,     // xout = dinv .* b          (first sweep from x = 0; no matrix)
+  Sweep = 1,     // xout = xin + dinv (b - A xin)
+  SweepDot = 2,  // Sweep; red += w_i xout_i (w = b if null)
+  Resid = 3,     // xout = b - A xin
+};
+constexpr int kWaveMaxStages = 6;
+struct WaveArgs {
+  // matrix (filled by launch_wave)
+  const int64_t* ptr = nullptr;
+  const int64_t* cptr = nullptr;
+  const int32_t* hdr = nullptr;
+  const int32_t* col = nullptr;
+  const double* val = nullptr;
+  int64_t ncols = 0, n_rows = 0, n_slices = 0, nchunks = 0;
+  // stages
+  const double* b = nullptr;
+  const double* dinv = nullptr;
+  const double* w = nullptr;  // SweepDot weight
+  int nst = 0;
+  int op[kWaveMaxStages] = {};
+  const double* xin[kWaveMaxStages] = {};
+  double* xout[kWaveMaxStages] = {};
+  // schedule: dependency reach h (chunks), key skew G
+  int64_t h = 0, G = 1;
+  unsigned int* flags = nullptr;  // kWaveMaxStages * nchunks chunk counters, then kWaveMaxStages watermarks
+  unsigned int* wm = nullptr;
+  // SweepDot reduction
+  int reduce = 0;
+  double* partials = nullptr;
+  unsigned int* ticket = nullptr;
+  double* red_out = nullptr;
+  int red_grid = 0;
+};
+bool wave_supported(const Sell& A);
+int64_t wave_chunks(const Sell& A);   // 256-row chunks
+constexpr int64_t kWaveChunkRows = 256;
+int64_t sell_bandwidth(psc_ctx* ctx, const Sell& A, cudaStream_t s);  // max |j - i| (sliced ELL)
+// flags must hold kWaveMaxStages * (wave_chunks(A) + 1) counters; a.wm = a.flags + nst * nchunks is set here
+void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& a, cudaStream_t s);
+
 // CSR (global int64 columns) -> sliced ELL with local int32 columns.
 // lanes: 0 = choose from the mean row length (choose_lanes), else 1 / 4 / 8 / 16 / 32.
 int choose_lanes(int64_t n_rows, int64_t nnz);

@@ -101,6 +101,25 @@ class Level:
     R: CSR | None = None   # n_{l+1} x n_l  (= P^T, stored explicitly)
 
 
+class _Handle:
+    """Owns the C hierarchy; every numpy view of its CSR arrays keeps it alive."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h is not None and _lib is not None:
+            _lib.pscgen_free(self.h)
+            self.h = None
+
+
+def _view(ptr, n, ctype, dtype, owner):
+    """numpy view of n elements at a C pointer, holding a reference to `owner`."""
+    buf = (ctype * n).from_address(ctypes.addressof(ptr.contents))
+    buf._owner = owner
+    return np.frombuffer(buf, dtype=dtype)
+
+
 @dataclass
 class Hierarchy:
     levels: list
@@ -130,14 +149,11 @@ class Hierarchy:
             return L.R.rows(int(rs[r]), int(rs[r + 1]))
         raise ValueError(kind)
 
-    def __del__(self):
-        if self._handle is not None and _lib is not None:
-            _lib.pscgen_free(self._handle)
-            self._handle = None
 
 
 def _wrap(handle, meta) -> Hierarchy:
     L = lib()
+    owner = _Handle(handle)
     nl = L.pscgen_nlevels(handle)
     nr = L.pscgen_nranks(handle)
     levels = []
@@ -155,15 +171,15 @@ def _wrap(handle, meta) -> Hierarchy:
                             ctypes.byref(cp), ctypes.byref(vp)) != 0:
                 mats.append(None)
                 continue
-            ptr = np.ctypeslib.as_array(pp, shape=(nrows.value + 1,))
+            ptr = _view(pp, nrows.value + 1, ctypes.c_int64, np.int64, owner)
             nnz = int(ptr[-1])
-            col = np.ctypeslib.as_array(cp, shape=(nnz,)) if nnz else np.zeros(0, np.int64)
-            val = np.ctypeslib.as_array(vp, shape=(nnz,)) if nnz else np.zeros(0, np.float64)
+            col = _view(cp, nnz, ctypes.c_int64, np.int64, owner) if nnz else np.zeros(0, np.int64)
+            val = _view(vp, nnz, ctypes.c_double, np.float64, owner) if nnz else np.zeros(0, np.float64)
             mats.append(CSR((nrows.value, ncols.value), ptr, col, val))
         levels.append(Level(n, rs, mats[0], mats[1], mats[2]))
     meta = dict(meta)
     meta["omega"] = [L.pscgen_omega(handle, l) for l in range(nl - 1)]
-    return Hierarchy(levels, nr, meta, handle)
+    return Hierarchy(levels, nr, meta, owner)
 
 
 def poisson_hierarchy(nx: int, ny: int | None = None, nz: int | None = None, procs=(1, 1, 1), *,
