@@ -303,12 +303,12 @@ void wave_setup(psc_hier* h, LevelWS& W) {
   if (!getenv("PSC_WAVE") || h->ctx->nranks != 1 || W.nh != 0 || !wave_supported(W.A->S)) return;
   const int64_t bw = sell_bandwidth(h->ctx, W.A->S, h->ctx->stream);
   W.wave_h = (bw + kWaveChunkRows - 1) / kWaveChunkRows;
-  W.wave_flags = dalloc<unsigned int>((size_t)kWaveMaxStages * (wave_chunks(W.A->S) + 1));
+  W.wave_flags = dalloc<unsigned int>((size_t)kWaveMaxStages * ((wave_chunks(W.A->S) + kWaveBlk - 1) / kWaveBlk));
 }
 
 void wave_launch(psc_hier* h, LevelWS& W, WaveArgs& a, cudaStream_t s) {
   a.h = W.wave_h;
-  a.G = W.wave_h + 1 + wave_slack(h, a.nst);
+  a.G = W.wave_h + kWaveBlk + wave_slack(h, a.nst);
   a.flags = W.wave_flags;
   launch_wave(h->ctx, W.A->S, a, s);
 }

@@ -128,7 +128,16 @@ __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int
 __device__ __forceinline__ double ldm(const double* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
 __device__ __forceinline__ int32_t ldm(const int32_t* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
 
-template <int W>
+// x gathers: read-only texture path, or (CG) through L2 only — for vectors
+// written by other CTAs of the same launch (the wavefront pass), which the
+// non-coherent L1 may hold stale
+template <bool CG>
+__device__ __forceinline__ double ldx(const double* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return __ldg(p);
+}
+
+template <int W, bool CG = false>
 __device__ __forceinline__ double dia_sum(int32_t h, uint32_t i, const double* __restrict__ v,
                                           const double* __restrict__ x, uint32_t nc, bool keep) {
   double vi[W];
@@ -138,7 +147,7 @@ __device__ __forceinline__ double dia_sum(int32_t h, uint32_t i, const double* _
 #pragma unroll
   for (int j = 0; j < W; ++j) {
     const uint32_t c = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
-    xv[j] = __ldg(x + (c < nc ? c : 0u));
+    xv[j] = ldx<CG>(x + (c < nc ? c : 0u));
   }
   double sum = 0.0;
 #pragma unroll
@@ -150,6 +159,7 @@ __device__ __forceinline__ double dia_sum(int32_t h, uint32_t i, const double* _
 // lane holds: s = sum_k val[k] * x[col[k]], k in stored order (padding adds
 // fma(0, x, s) = s).  DIA slices: dia_sum<W>.  ELL slices: explicit columns,
 // batches of 8 (value, column) loads issued before the dependent gathers.
+template <bool CG = false>
 __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, const int32_t* __restrict__ col,
                                                const double* __restrict__ val, const double* __restrict__ x,
                                                int64_t ncols, bool keep) {
@@ -163,14 +173,14 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
     const uint32_t i = (uint32_t)(s * 32 + lane);
     const uint32_t nc = (uint32_t)ncols;
     switch (w) {
-      case 1: return dia_sum<1>(h, i, v, x, nc, keep);
-      case 2: return dia_sum<2>(h, i, v, x, nc, keep);
-      case 3: return dia_sum<3>(h, i, v, x, nc, keep);
-      case 4: return dia_sum<4>(h, i, v, x, nc, keep);
-      case 5: return dia_sum<5>(h, i, v, x, nc, keep);
-      case 6: return dia_sum<6>(h, i, v, x, nc, keep);
-      case 7: return dia_sum<7>(h, i, v, x, nc, keep);
-      case 8: return dia_sum<8>(h, i, v, x, nc, keep);
+      case 1: return dia_sum<1, CG>(h, i, v, x, nc, keep);
+      case 2: return dia_sum<2, CG>(h, i, v, x, nc, keep);
+      case 3: return dia_sum<3, CG>(h, i, v, x, nc, keep);
+      case 4: return dia_sum<4, CG>(h, i, v, x, nc, keep);
+      case 5: return dia_sum<5, CG>(h, i, v, x, nc, keep);
+      case 6: return dia_sum<6, CG>(h, i, v, x, nc, keep);
+      case 7: return dia_sum<7, CG>(h, i, v, x, nc, keep);
+      case 8: return dia_sum<8, CG>(h, i, v, x, nc, keep);
       default: return 0.0;
     }
   }
@@ -188,7 +198,7 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
       vi[j] = ldm(v + 32 * j, keep);
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) sum = fma(vi[j], __ldg(x + ci[j]), sum);
+    for (int j = 0; j < 8; ++j) sum = fma(vi[j], ldx<CG>(x + ci[j]), sum);
     c += 256;
     v += 256;
   }
@@ -204,7 +214,7 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
       }
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (j < rem) sum = fma(vi[j], __ldg(x + ci[j]), sum);
+      if (j < rem) sum = fma(vi[j], ldx<CG>(x + ci[j]), sum);
   }
   return sum;
 }
@@ -952,39 +962,39 @@ static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_s
 //
 // Work item = (stage s, chunk k of 8 slices = 256 rows).  A row of chunk k reads
 // x only in chunks k-h .. k+h (h from the matrix bandwidth), so stage s may
-// process chunk k once stage s-1 has completed every chunk <= k+h.  With two
-// ping-pong x buffers that one rule also orders the write of x^(s) over x^(s-2)
-// after the last stage-(s-1) read of it.  Items are dealt round-robin in the
-// order of the key k + G s (G = h + 1 + slack, so an item's dependencies were
-// dealt ~slack*stages items earlier); every CTA handles its items in that order
-// and all CTAs are co-resident, so the earliest unfinished item can always run.
-// Completion: every consumer warp fences its stores and bumps the chunk's
-// counter; the 8th bump publishes by advancing the stage's watermark (the
-// longest completed prefix of chunks) with release semantics; a waiting warp
-// acquire-polls the watermark.  Vectors written inside the pass are read through
-// L2 (ld.global.cg): L1 is not coherent across SMs.
+// process chunk k once stage s-1 has completed chunks k-h .. k+h.  With two
+// ping-pong x buffers the same window also orders the write of x^(s) over
+// x^(s-2) after the last stage-(s-1) reads of it (exactly those items read
+// chunk k).  Completion is counted per block of kWaveBlk chunks (every consumer
+// warp fences its stores, then bumps its block's counter); a waiting warp
+// acquire-polls the blocks covering its window, one block per lane — no serial
+// chain (a prefix watermark advanced chunk by chunk costs an atomic round trip
+// per chunk: 95 ms per pass at 256^3).  Items are dealt round-robin in the order
+// of the key k + G s with G >= h + kWaveBlk + slack, so every dependency of an
+// item (whole blocks, i.e. chunks up to k + h + kWaveBlk - 1 of stage s-1) was
+// dealt earlier; every CTA handles its items in that order and all CTAs are
+// co-resident, so the earliest unfinished item can always run.  Vectors written
+// inside the pass are read through L2 (ld.global.cg): L1 is not coherent across SMs.
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-__device__ __forceinline__ void wave_wait(const unsigned int* wm, unsigned int need) {
-  if (ld_acquire_u32(wm) >= need) return;
-  const long long t0 = clock64();
-  while (ld_acquire_u32(wm) < need) {
-    __nanosleep(64);
-    if (clock64() - t0 > (1ll << 34)) __trap();  // ~9 s: a broken schedule fails loudly instead of hanging
+// whole warp: wait until stage-(s-1) blocks covering chunks [k-h, k+h] are complete
+__device__ __forceinline__ void wave_wait(const unsigned int* cnt, int64_t k, int64_t h, int64_t nchunks,
+                                          int lane) {
+  const int64_t b0 = max(k - h, (int64_t)0) / kWaveBlk, b1 = min(k + h, nchunks - 1) / kWaveBlk;
+  for (int64_t b = b0 + lane; b <= b1; b += 32) {
+    const unsigned int need = (unsigned int)(kTmaSlices * min((int64_t)kWaveBlk, nchunks - b * kWaveBlk));
+    if (ld_acquire_u32(cnt + b) >= need) continue;
+    const long long t0 = clock64();
+    while (ld_acquire_u32(cnt + b) < need) {
+      __nanosleep(32);
+      if (clock64() - t0 > (1ll << 34)) __trap();  // ~9 s: a broken schedule fails loudly instead of hanging
+    }
   }
-}
-
-__device__ __forceinline__ void wave_publish(unsigned int* flags, unsigned int* wm, unsigned int nchunks) {
-  unsigned int w = ld_acquire_u32(wm);
-  while (w < nchunks && ld_acquire_u32(flags + w) == (unsigned int)kTmaSlices) {
-    __threadfence();
-    const unsigned int old = atomicCAS(wm, w, w + 1);
-    w = (old == w) ? w + 1 : old;
-  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, int64_t& k) {
@@ -1064,10 +1074,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_wave(WaveArgs a) {
       const int op = a.op[s];
       const int st = (int)(it % kTmaStages);
       mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
-      if (s > 0) {  // stage s-1 done on chunks <= k + h
-        if (lane == 0) wave_wait(a.wm + (s - 1), (unsigned int)min(k + a.h + 1, a.nchunks));
-        __syncwarp();
-      }
+      if (s > 0) wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, k, a.h, a.nchunks, lane);
       const double* xin = a.xin[s];
       double* xout = a.xout[s];
       const bool fresh = (s > 0);  // x produced inside this pass: read through L2
@@ -1129,14 +1136,10 @@ __global__ void __launch_bounds__(kTmaThreads) sell_wave(WaveArgs a) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
-      // publish: this warp's stores, then the chunk counter; the 8th warp advances the watermark
+      // publish: this warp's stores, then its block's counter
       __threadfence();
       __syncwarp();
-      if (lane == 0) {
-        unsigned int* fl = a.flags + (int64_t)s * a.nchunks;
-        const unsigned int old = atomicAdd(fl + k, 1u);
-        if (old == (unsigned int)kTmaSlices - 1) wave_publish(fl, a.wm + s, (unsigned int)a.nchunks);
-      }
+      if (lane == 0) atomicAdd(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, 1u);
       ++it;
     }
   }
@@ -1144,19 +1147,76 @@ __global__ void __launch_bounds__(kTmaThreads) sell_wave(WaveArgs a) {
   if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
 }
 
-bool wave_supported(const Sell& A) {
-  return A.lanes == 1 && A.max_width <= kTmaMaxW && A.hdr && A.n_units > 0 && A.n_cols_local == A.n_rows;
+// Direct-load form of the wavefront pass for slices of any width (e.g. A_1 of
+// the aggregation hierarchy, 20-50 entries per row): no TMA ring, 8 warps per
+// CTA, warp w takes slice 8k + w of each item and streams it with the batched
+// loads of sell_row_sum; same schedule, dependencies and publication.
+constexpr int kWaveDirectThreads = kTmaSlices * 32;
+
+__global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveArgs a) {
+  pdl_enter();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
+  double acc[1] = {0.0};
+  for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
+    int s;
+    int64_t k;
+    wave_item(a, m, s, k);
+    if (k < 0 || k >= a.nchunks) continue;
+    const int op = a.op[s];
+    const bool keep = (s + 1 < a.nst);  // a later stage re-reads the slice: normal caching, else stream
+    const int64_t sl = k * kTmaSlices + warp;
+    int32_t h = 0;
+    if (op != (int)WaveOp::Scale && sl < a.n_slices) h = load_hdr(a.hdr, sl, lane);
+    if (s > 0) wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, k, a.h, a.nchunks, lane);
+    const double* xin = a.xin[s];
+    double* xout = a.xout[s];
+    if (sl < a.n_slices) {
+      const int64_t i = sl * 32 + lane;
+      double sum = 0.0;
+      if (op != (int)WaveOp::Scale)
+        sum = (s > 0) ? sell_row_sum<true>(h, sl, lane, a.col, a.val, xin, a.ncols, keep)
+                      : sell_row_sum<false>(h, sl, lane, a.col, a.val, xin, a.ncols, keep);
+      if (i < a.n_rows) {
+        const double bi = ldm(a.b + i, keep);
+        if (op == (int)WaveOp::Scale) {
+          xout[i] = ldm(a.dinv + i, keep) * bi;
+        } else if (op == (int)WaveOp::Resid) {
+          xout[i] = bi - sum;
+        } else {
+          const double xi = (s > 0) ? __ldcg(xin + i) : __ldg(xin + i);
+          const double xn = xi + ldm(a.dinv + i, keep) * (bi - sum);
+          xout[i] = xn;
+          if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
+        }
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, 1u);
+  }
+  pdl_exit();
+  if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
 }
+
+bool wave_supported(const Sell& A) {
+  return A.lanes == 1 && A.hdr && A.n_units > 0 && A.n_cols_local == A.n_rows;
+}
+
+static bool wave_tma(const Sell& A) { return A.max_width <= kTmaMaxW && !env_int("PSC_WAVE_DIRECT", 0); }
 
 int64_t wave_chunks(const Sell& A) { return (A.n_units + kTmaSlices - 1) / kTmaSlices; }
 
 void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& in, cudaStream_t s) {
-  static int occ = -1;
+  static int occ = -1, occ_d = -1;
   if (occ < 0) {
     PSC_CUDA(cudaFuncSetAttribute(sell_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
     PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sell_wave, kTmaThreads, kTmaSmem));
+    PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, sell_wave_direct, kWaveDirectThreads, 0));
   }
-  PSC_REQUIRE(occ >= 1, PSC_ERR_STATE, "sell_wave cannot be resident");
+  const bool tma = wave_tma(A);
+  const int o = tma ? occ : occ_d;
+  PSC_REQUIRE(o >= 1, PSC_ERR_STATE, "sell_wave cannot be resident");
   WaveArgs a = in;
   a.ptr = A.ptr;
   a.cptr = A.cptr;
@@ -1167,13 +1227,15 @@ void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& in, cudaStream_t s
   a.n_rows = A.n_rows;
   a.n_slices = A.n_units;
   a.nchunks = wave_chunks(A);
-  a.wm = a.flags + (size_t)a.nst * a.nchunks;
+  a.nblk = (a.nchunks + kWaveBlk - 1) / kWaveBlk;
+  PSC_REQUIRE(a.G >= a.h + kWaveBlk, PSC_ERR_STATE, "wave schedule: key skew below the dependency reach");
   const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
   // every CTA must be resident at once (items wait on other CTAs' items)
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)occ * ctx->num_sms));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)o * ctx->num_sms));
   PSC_REQUIRE(!a.reduce || grid <= a.red_grid, PSC_ERR_STATE, "reduction site too small");
-  PSC_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(unsigned int) * ((size_t)a.nst * a.nchunks + kWaveMaxStages), s));
-  launch_k(sell_wave, grid, kTmaThreads, kTmaSmem, s, a);
+  PSC_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(unsigned int) * (size_t)a.nst * a.nblk, s));
+  if (tma) launch_k(sell_wave, grid, kTmaThreads, kTmaSmem, s, a);
+  else launch_k(sell_wave_direct, grid, kWaveDirectThreads, 0, s, a);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }

@@ -134,6 +134,7 @@ enum class WaveOp : int {
   Resid = 3,     // xout = b - A xin
 };
 constexpr int kWaveMaxStages = 6;
+constexpr int kWaveBlk = 16;  // chunks per completion counter
 struct WaveArgs {
   // matrix (filled by launch_wave)
   const int64_t* ptr = nullptr;
@@ -152,8 +153,8 @@ struct WaveArgs {
   double* xout[kWaveMaxStages] = {};
   // schedule: dependency reach h (chunks), key skew G
   int64_t h = 0, G = 1;
-  unsigned int* flags = nullptr;  // kWaveMaxStages * nchunks chunk counters, then kWaveMaxStages watermarks
-  unsigned int* wm = nullptr;
+  unsigned int* flags = nullptr;  // per stage: nblk block counters (8 warp arrivals per chunk)
+  int64_t nblk = 0;
   // SweepDot reduction
   int reduce = 0;
   double* partials = nullptr;
@@ -165,7 +166,7 @@ bool wave_supported(const Sell& A);
 int64_t wave_chunks(const Sell& A);   // 256-row chunks
 constexpr int64_t kWaveChunkRows = 256;
 int64_t sell_bandwidth(psc_ctx* ctx, const Sell& A, cudaStream_t s);  // max |j - i| (sliced ELL)
-// flags must hold kWaveMaxStages * (wave_chunks(A) + 1) counters; a.wm = a.flags + nst * nchunks is set here
+// flags must hold kWaveMaxStages * ceil(wave_chunks(A) / kWaveBlk) counters; requires G >= h + kWaveBlk
 void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& a, cudaStream_t s);
 
 // CSR (global int64 columns) -> sliced ELL with local int32 columns.
