@@ -7,6 +7,7 @@
 // cached gathers of x (__ldg, kept in the 126 MB L2), grid-stride loops sized
 // to the SM count, and deterministic fixed-order reductions.
 #include <cub/cub.cuh>
+#include <numeric>
 
 #include "kernels.h"
 
@@ -1003,23 +1004,50 @@ __device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, 
   k = K - a.G * s;
 }
 
-__global__ void __launch_bounds__(kTmaThreads) sell_wave(WaveArgs a) {
+// warps 0-7 consume, warp 8 (one lane) produces the TMA ring, warp 9 (one lane)
+// publishes: it waits for the 8 consumer arrivals of an item on done[st] (CTA-
+// scope release/acquire), then one gpu-scope fence + the block counter bump for
+// the whole CTA, and only then releases the ring slot — the fence latency
+// overlaps the consumers' next items instead of stalling every warp.
+constexpr int kWaveThreads = (kTmaSlices + 2) * 32;
+constexpr int kWaveSmem = kTmaStages * kTmaStageBytes + 3 * kTmaStages * 8;
+
+__global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
   pdl_enter();
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaStageBytes);
   uint64_t* empty = full + kTmaStages;
+  uint64_t* done = empty + kTmaStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kTmaStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], kTmaSlices);
+      mbar_init(&empty[st], kTmaSlices + 1);
+      mbar_init(&done[st], kTmaSlices);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
   double acc[1] = {0.0};
-  if (warp == kTmaSlices) {
+  if (warp == kTmaSlices + 1) {
+    // ---------------- publisher (one lane)
+    if (lane == 0) {
+      int64_t it = 0;
+      for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
+        int s;
+        int64_t k;
+        wave_item(a, m, s, k);
+        if (k < 0 || k >= a.nchunks) continue;
+        const int st = (int)(it % kTmaStages);
+        mbar_wait(&done[st], (uint32_t)((it / kTmaStages) & 1));
+        __threadfence();
+        atomicAdd(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, (unsigned int)kTmaSlices);
+        mbar_arrive(&empty[st]);
+        ++it;
+      }
+    }
+  } else if (warp == kTmaSlices) {
     // ---------------- producer (one lane): matrix slices, b, 1/M of each item
     if (lane == 0) {
       uint64_t pol_stream, pol_keep;
@@ -1135,11 +1163,10 @@ __global__ void __launch_bounds__(kTmaThreads) sell_wave(WaveArgs a) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-      // publish: this warp's stores, then its block's counter
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) atomicAdd(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, 1u);
+      if (lane == 0) {
+        mbar_arrive(&done[st]);  // this warp's stores -> the publisher
+        mbar_arrive(&empty[st]);
+      }
       ++it;
     }
   }
@@ -1191,9 +1218,13 @@ __global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveAr
         }
       }
     }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) atomicAdd(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, 1u);
+    // one gpu-scope fence per CTA and item (the barrier orders the other warps'
+    // stores before it), then the block counter counts all 8 warps
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, (unsigned int)kTmaSlices);
+    }
   }
   pdl_exit();
   if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
@@ -1210,8 +1241,8 @@ int64_t wave_chunks(const Sell& A) { return (A.n_units + kTmaSlices - 1) / kTmaS
 void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& in, cudaStream_t s) {
   static int occ = -1, occ_d = -1;
   if (occ < 0) {
-    PSC_CUDA(cudaFuncSetAttribute(sell_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
-    PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sell_wave, kTmaThreads, kTmaSmem));
+    PSC_CUDA(cudaFuncSetAttribute(sell_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, kWaveSmem));
+    PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sell_wave, kWaveThreads, kWaveSmem));
     PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, sell_wave_direct, kWaveDirectThreads, 0));
   }
   const bool tma = wave_tma(A);
@@ -1231,10 +1262,13 @@ void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& in, cudaStream_t s
   PSC_REQUIRE(a.G >= a.h + kWaveBlk, PSC_ERR_STATE, "wave schedule: key skew below the dependency reach");
   const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
   // every CTA must be resident at once (items wait on other CTAs' items)
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)o * ctx->num_sms));
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)o * ctx->num_sms));
+  // round-robin dealing: a grid that is a multiple of the stage count would pin
+  // every CTA to one stage (only 1/nst of the CTAs streaming stage 0 from HBM)
+  while (grid > 1 && std::gcd(grid, a.nst) != 1) --grid;
   PSC_REQUIRE(!a.reduce || grid <= a.red_grid, PSC_ERR_STATE, "reduction site too small");
   PSC_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(unsigned int) * (size_t)a.nst * a.nblk, s));
-  if (tma) launch_k(sell_wave, grid, kTmaThreads, kTmaSmem, s, a);
+  if (tma) launch_k(sell_wave, grid, kWaveThreads, kWaveSmem, s, a);
   else launch_k(sell_wave_direct, grid, kWaveDirectThreads, 0, s, a);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;

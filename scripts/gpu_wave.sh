@@ -2,17 +2,17 @@
 # wavefront pass: parity with PSC_WAVE=1, A/B bench on one box
 mkdir -p gpurun_out
 T=${1:-wave}
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m "gpu and not slow" -k "variants or vcycle" > gpurun_out/${T}_parity.log 2>&1; echo "parity_rc=$?"
-PSC_WAVE=1 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m "gpu and not slow" -k "pcg" > gpurun_out/${T}_parity_pcg.log 2>&1; echo "wave_pcg_rc=$?"
-PSC_WAVE=1 timeout 1200 python -m pytest tests/test_gpu_vbm.py -q > gpurun_out/${T}_vbm_tests.log 2>&1; echo "vbm_tests_rc=$?"
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m "gpu and not slow" -k "variants" > gpurun_out/${T}_parity.log 2>&1; echo "parity_rc=$?"
 run() { timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${T}_bench_$1.json 2> gpurun_out/${T}_bench_$1.err; echo "bench_$1_rc=$?"; }
 run w0
 PSC_WAVE=1 run w1
 PSC_WAVE=1 PSC_WAVE_DIRECT=1 run w1d
 PSC_WAVE=1 PSC_WAVE_SLACK=16 run w1s16
 PSC_WAVE=1 PSC_WAVE_SLACK=300 run w1s300
-tail -2 gpurun_out/${T}_parity.log gpurun_out/${T}_parity_pcg.log gpurun_out/${T}_vbm_tests.log
+tail -2 gpurun_out/${T}_parity.log
 for f in gpurun_out/${T}_bench_*.json; do python -c "
 import json,sys
 d=json.loads(open('$f').read().strip().splitlines()[-1]); r=d['roofline']
 print('$f', round(d['value']), d['config']['iters'][0], round(d['ms_per_step'],2), round(r['avg_launch_us'],1), round(r['frac'],3), d['launches_per_iteration'])" 2>/dev/null; done
+# launch list of one wave solve
+PSC_WAVE=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu_rc=$?"
