@@ -1005,26 +1005,31 @@ __device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, 
 }
 
 // warps 0-7 consume, warp 8 (one lane) produces the TMA ring, warp 9 (one lane)
-// publishes: it waits for the 8 consumer arrivals of an item on done[st] (CTA-
-// scope release/acquire), then one gpu-scope fence + the block counter bump for
-// the whole CTA, and only then releases the ring slot — the fence latency
-// overlaps the consumers' next items instead of stalling every warp.
+// publishes: it waits until the 8 consumer warps have counted item `it` in the
+// shared counter done[it % kWaveLag] (monotone: +8 per use, so no phase
+// aliasing; CTA-scope release by the consumers, acquire by the publisher), then
+// issues ONE gpu-scope fence and the block-counter bump for the whole CTA.  The
+// ring slots do not wait for it (consumers run at most kWaveLag items ahead of
+// the publisher), so the fence latency is off the ring's critical path.
 constexpr int kWaveThreads = (kTmaSlices + 2) * 32;
-constexpr int kWaveSmem = kTmaStages * kTmaStageBytes + 3 * kTmaStages * 8;
+constexpr int kWaveLag = 16;
+constexpr int kWaveSmem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8 + (kWaveLag + 2) * 4;
 
 __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
   pdl_enter();
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaStageBytes);
   uint64_t* empty = full + kTmaStages;
-  uint64_t* done = empty + kTmaStages;
+  unsigned int* done = reinterpret_cast<unsigned int*>(empty + kTmaStages);  // [kWaveLag]
+  volatile unsigned int* published = done + kWaveLag;                         // items published so far
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kTmaStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], kTmaSlices + 1);
-      mbar_init(&done[st], kTmaSlices);
+      mbar_init(&empty[st], kTmaSlices);
     }
+    for (int j = 0; j < kWaveLag; ++j) done[j] = 0;
+    *published = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1039,11 +1044,13 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
         int64_t k;
         wave_item(a, m, s, k);
         if (k < 0 || k >= a.nchunks) continue;
-        const int st = (int)(it % kTmaStages);
-        mbar_wait(&done[st], (uint32_t)((it / kTmaStages) & 1));
-        __threadfence();
+        const unsigned int need = (unsigned int)kTmaSlices * (unsigned int)(it / kWaveLag + 1);
+        volatile unsigned int* dc = done + (it % kWaveLag);
+        while (*dc < need) {
+        }
+        __threadfence();  // the consumers' stores (CTA-ordered before their counts) -> gpu scope
         atomicAdd(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, (unsigned int)kTmaSlices);
-        mbar_arrive(&empty[st]);
+        *published = (unsigned int)(it + 1);
         ++it;
       }
     }
@@ -1053,12 +1060,30 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
       uint64_t pol_stream, pol_keep;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+      // the next valid item and its slice offsets are loaded one item ahead
+      auto next_valid = [&](int64_t m0, int& s_, int64_t& k_) {
+        for (int64_t mm = m0; mm < total; mm += gridDim.x) {
+          wave_item(a, mm, s_, k_);
+          if (k_ >= 0 && k_ < a.nchunks) return mm;
+        }
+        return total;
+      };
+      auto offsets = [&](int64_t k_, int64_t (&o)[4]) {
+        const int64_t s0 = k_ * kTmaSlices, s1 = min(s0 + kTmaSlices, a.n_slices);
+        o[0] = a.ptr[s0]; o[1] = a.ptr[s1]; o[2] = a.cptr[s0]; o[3] = a.cptr[s1];
+      };
+      int s;
+      int64_t k;
+      int64_t m = next_valid(blockIdx.x, s, k);
+      int64_t off[4] = {0, 0, 0, 0};
+      if (m < total) offsets(k, off);
       int64_t it = 0;
-      for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
-        int s;
-        int64_t k;
-        wave_item(a, m, s, k);
-        if (k < 0 || k >= a.nchunks) continue;
+      while (m < total) {
+        int sn = 0;
+        int64_t kn = 0;
+        const int64_t mn = next_valid(m + gridDim.x, sn, kn);
+        int64_t offn[4] = {0, 0, 0, 0};
+        if (mn < total) offsets(kn, offn);
         const int op = a.op[s];
         // re-read by a later stage: keep in L2; last reader: stream out
         const uint64_t pol = (s + 1 < a.nst) ? pol_keep : pol_stream;
@@ -1070,11 +1095,11 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
         uint32_t hb = 0, vbytes = 0, cbytes = 0;
         int64_t vb0 = 0, cb0 = 0;
         if (op != (int)WaveOp::Scale) {
-          vb0 = a.ptr[s0];
-          cb0 = a.cptr[s0];
+          vb0 = off[0];
+          cb0 = off[2];
           hb = (uint32_t)(s1 - s0) * kHdr * 4;
-          vbytes = (uint32_t)(a.ptr[s1] - vb0) * 8;
-          cbytes = (uint32_t)(a.cptr[s1] - cb0) * 4;
+          vbytes = (uint32_t)(off[1] - vb0) * 8;
+          cbytes = (uint32_t)(off[3] - cb0) * 4;
         }
         const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
         const bool needd = (op != (int)WaveOp::Resid);
@@ -1088,6 +1113,10 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
           if (needd) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol);
         }
         ++it;
+        m = mn;
+        s = sn;
+        k = kn;
+        for (int j = 0; j < 4; ++j) off[j] = offn[j];
       }
     }
   } else {
@@ -1101,8 +1130,13 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
       if (k < 0 || k >= a.nchunks) continue;
       const int op = a.op[s];
       const int st = (int)(it % kTmaStages);
-      mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
+      // at most kWaveLag items ahead of the publisher (its done counters are reused)
+      if (it >= kWaveLag)
+        while (*published + kWaveLag <= (unsigned int)it) {
+        }
+      // dependencies first: the item's bulk copies are in flight meanwhile
       if (s > 0) wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, k, a.h, a.nchunks, lane);
+      mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
       const double* xin = a.xin[s];
       double* xout = a.xout[s];
       const bool fresh = (s > 0);  // x produced inside this pass: read through L2
@@ -1164,8 +1198,9 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
       }
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&done[st]);  // this warp's stores -> the publisher
         mbar_arrive(&empty[st]);
+        __threadfence_block();  // this warp's stores before its count (CTA-scope release)
+        atomicAdd(done + (it % kWaveLag), 1u);
       }
       ++it;
     }
