@@ -296,13 +296,13 @@ bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
 // slices at most 8 wide.  Opt-in (PSC_WAVE=1) until measured.
 // key slack: dependencies should lie outside the items in flight (~3 per CTA,
 // 2 CTAs per SM), while the rows between a chunk's first and last stage must
-// stay in L2 (window (nst-1) * G chunks, budget ~64 MB of the 126 MB)
+// stay in L2 (window (nst-1) * G chunks, budget ~96 MB of the 126 MB)
 int64_t wave_slack(psc_hier* h, const LevelWS& W, int nst) {
   const char* e = getenv("PSC_WAVE_SLACK");
   if (e) return std::max(0, atoi(e));
   const int64_t inflight = 3 * 2 * (int64_t)h->ctx->num_sms / std::max(nst, 1);
   const double row_bytes = 12.0 * (double)W.A->S.padded / std::max<int64_t>(W.n, 1) + 32.0;
-  const int64_t gmax = (int64_t)(64.0 * (1 << 20) / (std::max(nst - 1, 1) * kWaveChunkRows * row_bytes));
+  const int64_t gmax = (int64_t)(96.0 * (1 << 20) / (std::max(nst - 1, 1) * kWaveChunkRows * row_bytes));
   return std::max<int64_t>(8, std::min(inflight, gmax - W.wave_h - kWaveBlk));
 }
 

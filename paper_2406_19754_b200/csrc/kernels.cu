@@ -982,19 +982,36 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   return v;
 }
 
-// whole warp: wait until stage-(s-1) blocks covering chunks [k-h, k+h] are complete
-__device__ __forceinline__ void wave_wait(const unsigned int* cnt, int64_t k, int64_t h, int64_t nchunks,
-                                          int lane) {
-  const int64_t b0 = max(k - h, (int64_t)0) / kWaveBlk, b1 = min(k + h, nchunks - 1) / kWaveBlk;
-  for (int64_t b = b0 + lane; b <= b1; b += 32) {
-    const unsigned int need = (unsigned int)(kTmaSlices * min((int64_t)kWaveBlk, nchunks - b * kWaveBlk));
-    if (ld_acquire_u32(cnt + b) >= need) continue;
-    const long long t0 = clock64();
-    while (ld_acquire_u32(cnt + b) < need) {
-      __nanosleep(32);
+// Whole warp: wait until stage s-1 has completed every block up to the one
+// holding chunk k+h.  *front = this warp's verified prefix of complete blocks of
+// that stage (shared memory, per warp and stage; counters only grow within a
+// pass): most items find it already far enough and need no memory round trip;
+// otherwise one bulk check of the next 64 blocks (2 per lane, ld.acquire, ballot)
+// advances it.  The acquire that verified a block orders this warp's later reads.
+__device__ __forceinline__ bool wave_block_done(const unsigned int* cnt, int64_t b, int64_t nblk, int64_t nchunks) {
+  if (b >= nblk) return true;
+  const unsigned int need = (unsigned int)(kTmaSlices * min((int64_t)kWaveBlk, nchunks - b * kWaveBlk));
+  return ld_acquire_u32(cnt + b) >= need;
+}
+
+__device__ __forceinline__ void wave_wait(const unsigned int* cnt, unsigned int* front, int64_t k, int64_t h,
+                                          int64_t nchunks, int64_t nblk, int lane) {
+  const int64_t b1 = min(k + h, nchunks - 1) / kWaveBlk;
+  int64_t f = *(volatile unsigned int*)front;
+  if (f > b1) return;
+  const long long t0 = clock64();
+  while (f <= b1) {
+    const unsigned int m0 = __ballot_sync(0xffffffffu, wave_block_done(cnt, f + lane, nblk, nchunks));
+    const unsigned int m1 = __ballot_sync(0xffffffffu, wave_block_done(cnt, f + 32 + lane, nblk, nchunks));
+    const int p = (m0 != 0xffffffffu) ? __ffs(~m0) - 1 : (m1 != 0xffffffffu ? 32 + __ffs(~m1) - 1 : 64);
+    f += p;
+    if (f <= b1 && p == 0) {
+      __nanosleep(64);
       if (clock64() - t0 > (1ll << 34)) __trap();  // ~9 s: a broken schedule fails loudly instead of hanging
     }
   }
+  __syncwarp();
+  if (lane == 0) *(volatile unsigned int*)front = (unsigned int)f;
   __syncwarp();
 }
 
@@ -1013,7 +1030,8 @@ __device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, 
 // the publisher), so the fence latency is off the ring's critical path.
 constexpr int kWaveThreads = (kTmaSlices + 2) * 32;
 constexpr int kWaveLag = 16;
-constexpr int kWaveSmem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8 + (kWaveLag + 2) * 4;
+constexpr int kWaveSmem =
+    kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8 + (kWaveLag + 2) * 4 + kTmaSlices * kWaveMaxStages * 4;
 
 __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
   pdl_enter();
@@ -1022,6 +1040,7 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
   uint64_t* empty = full + kTmaStages;
   unsigned int* done = reinterpret_cast<unsigned int*>(empty + kTmaStages);  // [kWaveLag]
   volatile unsigned int* published = done + kWaveLag;                         // items published so far
+  unsigned int* fronts = done + kWaveLag + 2;                                  // [8 warps][stages]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kTmaStages; ++st) {
@@ -1029,6 +1048,7 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
       mbar_init(&empty[st], kTmaSlices);
     }
     for (int j = 0; j < kWaveLag; ++j) done[j] = 0;
+    for (int j = 0; j < kTmaSlices * kWaveMaxStages; ++j) fronts[j] = 0;
     *published = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1135,7 +1155,9 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
         while (*published + kWaveLag <= (unsigned int)it) {
         }
       // dependencies first: the item's bulk copies are in flight meanwhile
-      if (s > 0) wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, k, a.h, a.nchunks, lane);
+      if (s > 0)
+        wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, fronts + warp * kWaveMaxStages + (s - 1), k, a.h, a.nchunks,
+                  a.nblk, lane);
       mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
       const double* xin = a.xin[s];
       double* xout = a.xout[s];
@@ -1218,6 +1240,9 @@ constexpr int kWaveDirectThreads = kTmaSlices * 32;
 __global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveArgs a) {
   pdl_enter();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ unsigned int fronts[kTmaSlices * kWaveMaxStages];
+  if (threadIdx.x < kTmaSlices * kWaveMaxStages) fronts[threadIdx.x] = 0;
+  __syncthreads();
   const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
   double acc[1] = {0.0};
   for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
@@ -1230,7 +1255,9 @@ __global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveAr
     const int64_t sl = k * kTmaSlices + warp;
     int32_t h = 0;
     if (op != (int)WaveOp::Scale && sl < a.n_slices) h = load_hdr(a.hdr, sl, lane);
-    if (s > 0) wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, k, a.h, a.nchunks, lane);
+    if (s > 0)
+      wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, fronts + warp * kWaveMaxStages + (s - 1), k, a.h, a.nchunks,
+                a.nblk, lane);
     const double* xin = a.xin[s];
     double* xout = a.xout[s];
     if (sl < a.n_slices) {
