@@ -1,0 +1,7 @@
+#!/bin/bash
+# one ncu --set full capture of the level-0 sell_wave launches (program first run without ncu)
+mkdir -p gpurun_out
+T=${1:-ncuwave}
+PSC_WAVE=1 timeout 600 python bench.py --steps 1 --warmup 0 --grid 128 --no-cpu-baseline --no-e2e > gpurun_out/${T}_plain.json 2>&1; echo "plain_rc=$?"
+PSC_WAVE=1 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sell_wave -s 2 -c 2 -o gpurun_out/${T} python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/${T}_ncu.log 2>&1; echo "ncu_rc=$?"
+tail -3 gpurun_out/${T}_ncu.log
