@@ -1168,6 +1168,10 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
       if (sl < a.n_slices) {
         const uint32_t i = (uint32_t)(sl * 32 + lane);
         const int rl = warp * 32 + lane;
+        // the row's own x: issued before the gathers (not one more round trip after them)
+        const bool sweep = (op == (int)WaveOp::Sweep || op == (int)WaveOp::SweepDot);
+        const uint32_t ic = (int64_t)i < a.n_rows ? i : 0u;
+        const double xi = sweep ? (fresh ? __ldcg(xin + ic) : __ldg(xin + ic)) : 0.0;
         double sum = 0.0;
         if (op != (int)WaveOp::Scale) {
           const int32_t* hs = reinterpret_cast<const int32_t*>(base);
@@ -1211,7 +1215,6 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
           } else if (op == (int)WaveOp::Resid) {
             xout[i] = bi - sum;
           } else {
-            const double xi = fresh ? __ldcg(xin + i) : __ldg(xin + i);
             const double xn = xi + vec[kTmaRows + rl] * (bi - sum);
             xout[i] = xn;
             if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
@@ -1262,19 +1265,23 @@ __global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveAr
     double* xout = a.xout[s];
     if (sl < a.n_slices) {
       const int64_t i = sl * 32 + lane;
+      // epilogue operands issued before the row sum (they travel with the matrix loads)
+      const int64_t ic = i < a.n_rows ? i : 0;
+      const bool sweep = (op == (int)WaveOp::Sweep || op == (int)WaveOp::SweepDot);
+      const double bi = ldm(a.b + ic, keep);
+      const double di = (op != (int)WaveOp::Resid) ? ldm(a.dinv + ic, keep) : 0.0;
+      const double xi = sweep ? ((s > 0) ? __ldcg(xin + ic) : __ldg(xin + ic)) : 0.0;
       double sum = 0.0;
       if (op != (int)WaveOp::Scale)
         sum = (s > 0) ? sell_row_sum<true>(h, sl, lane, a.col, a.val, xin, a.ncols, keep)
                       : sell_row_sum<false>(h, sl, lane, a.col, a.val, xin, a.ncols, keep);
       if (i < a.n_rows) {
-        const double bi = ldm(a.b + i, keep);
         if (op == (int)WaveOp::Scale) {
-          xout[i] = ldm(a.dinv + i, keep) * bi;
+          xout[i] = di * bi;
         } else if (op == (int)WaveOp::Resid) {
           xout[i] = bi - sum;
         } else {
-          const double xi = (s > 0) ? __ldcg(xin + i) : __ldg(xin + i);
-          const double xn = xi + ldm(a.dinv + i, keep) * (bi - sum);
+          const double xn = xi + di * (bi - sum);
           xout[i] = xn;
           if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
         }
