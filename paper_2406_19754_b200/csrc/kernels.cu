@@ -115,6 +115,13 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NR], double* partials,
 
 constexpr int kHdr = 16;     // int32 words per slice header
 constexpr int kMaxDia = 8;   // most diagonals a DIA slice may have (header words 6..13)
+// DICT slice: ELL values, columns as 1-byte indices into a per-slice table of at
+// most kMaxDict distinct offsets j - i (header word 5 = 2, word 6 = table size).
+// Column region: table (rounded up to 4 words), then the indices packed 4 per
+// word, word (q / 4) * 32 + lane holding entries q..q+3 of the slice's row `lane`.
+constexpr int kMaxDict = 64;
+enum SliceKind : int { kEll = 0, kDia = 1, kDict = 2 };
+__device__ __forceinline__ int64_t dict_t4(int d) { return (d + 3) & ~3; }
 
 __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int64_t s, int lane) {
   return lane < kHdr ? __ldg(hdr + s * kHdr + lane) : 0;
@@ -167,7 +174,7 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
   const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
                      (uint32_t)__shfl_sync(0xffffffffu, h, 0);
   const int w = __shfl_sync(0xffffffffu, h, 4);
-  const bool dia = __shfl_sync(0xffffffffu, h, 5) != 0;
+  const bool dia = __shfl_sync(0xffffffffu, h, 5) == 1;
   const double* v = val + vb + lane;
   if (dia) {
     // local indices < 2^31: unsigned 32-bit wrap-around maps out-of-range columns above ncols
@@ -187,6 +194,36 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
   }
   const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
                      (uint32_t)__shfl_sync(0xffffffffu, h, 2);
+  if (__shfl_sync(0xffffffffu, h, 5) == kDict) {
+    // table entries t and 32 + t held by lane t; an index byte selects one by two shuffles
+    const int d = __shfl_sync(0xffffffffu, h, 6);
+    const int32_t t0 = lane < d ? ldm(col + cb + lane, keep) : 0;
+    const int32_t t1 = lane + 32 < d ? ldm(col + cb + 32 + lane, keep) : 0;
+    const uint32_t* iw = reinterpret_cast<const uint32_t*>(col + cb + dict_t4(d)) + lane;
+    const int32_t i = (int32_t)(s * 32 + lane);
+    double sum = 0.0;
+    for (int k = 0; k < w; k += 8) {
+      uint32_t wd[2];
+      double vi[8];
+      wd[0] = (uint32_t)ldm(reinterpret_cast<const int32_t*>(iw + 32 * (k >> 2)), keep);
+      wd[1] = (k + 4 < w) ? (uint32_t)ldm(reinterpret_cast<const int32_t*>(iw + 32 * ((k >> 2) + 1)), keep) : 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) vi[j] = (k + j < w) ? ldm(v + 32 * j, keep) : 0.0;
+      double xv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t bsel = (wd[j >> 2] >> (8 * (j & 3))) & 0xffu;
+        const int32_t o0 = __shfl_sync(0xffffffffu, t0, (int)(bsel & 31u));
+        const int32_t o1 = __shfl_sync(0xffffffffu, t1, (int)(bsel & 31u));
+        xv[j] = (k + j < w) ? ldx<CG>(x + (i + ((bsel & 32u) ? o1 : o0))) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (k + j < w) sum = fma(vi[j], xv[j], sum);
+      v += 256;
+    }
+    return sum;
+  }
   const int32_t* c = col + cb + lane;
   double sum = 0.0;
   int k = 0;
@@ -222,12 +259,20 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
 
 // Column of entry k of local row i (lane = i & 31) in slice s; -1 if a DIA
 // offset points outside [0, ncols) (absent entry).
-__device__ __forceinline__ int64_t sell_col(const int64_t* __restrict__ cptr, const int32_t* __restrict__ col,
-                                            int64_t s, int w, int64_t i, int k, int64_t ncols) {
+__device__ __forceinline__ int64_t sell_col(const int32_t* __restrict__ hdr, const int64_t* __restrict__ cptr,
+                                            const int32_t* __restrict__ col, int64_t s, int w, int64_t i, int k,
+                                            int64_t ncols) {
   const int64_t cb = cptr[s];
-  if ((cptr[s + 1] - cb) < 32 * (int64_t)w) {
+  const int kind = hdr[s * kHdr + 5];
+  if (kind == kDia) {
     const int64_t c = i + col[cb + k];
     return ((uint64_t)c < (uint64_t)ncols) ? c : -1;
+  }
+  if (kind == kDict) {
+    const int d = hdr[s * kHdr + 6];
+    const uint8_t* ib = reinterpret_cast<const uint8_t*>(col + cb + dict_t4(d));
+    const int b = ib[4 * (32 * (int64_t)(k >> 2) + (i & 31)) + (k & 3)];
+    return i + col[cb + b];
   }
   return col[cb + 32 * (int64_t)k + (i & 31)];
 }
@@ -726,7 +771,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
                            (uint32_t)__shfl_sync(0xffffffffu, h, 0);
         const int w = __shfl_sync(0xffffffffu, h, 4);
-        const bool dia = __shfl_sync(0xffffffffu, h, 5) != 0;
+        const bool dia = __shfl_sync(0xffffffffu, h, 5) == 1;
         const double* v = vs + (vb - vbase) + lane;
         const uint32_t i = (uint32_t)(s * 32 + lane);
         double xv[kTmaMaxW];
@@ -890,7 +935,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tmak(RowKArgs a, int64_t nch
           const int32_t* hs = reinterpret_cast<const int32_t*>(base);
           h = (mine && lane < kHdr) ? hs[warp * kHdr + lane] : 0;
           w = __shfl_sync(0xffffffffu, h, 4);
-          dia = __shfl_sync(0xffffffffu, h, 5) != 0;
+          dia = __shfl_sync(0xffffffffu, h, 5) == 1;
           int wm = lane < nsl ? hs[lane * kHdr + 4] : 0;
           for (int o = 16; o > 0; o >>= 1) wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
           nkb = max(1, (wm + kTmaMaxW - 1) / kTmaMaxW);
@@ -1034,6 +1079,55 @@ __device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, 
   k = K - a.G * s;
 }
 
+constexpr int kWaveLag = 16;  // consumers run at most this many items ahead of the publisher
+constexpr int kWaveRun = 8;   // items published per gpu-scope fence, at most
+
+// One lane per CTA publishes its items in order: it waits until the 8 consumer
+// warps have counted item `it` in done[it % kWaveLag] (monotone, +8 per use: no
+// phase aliasing; CTA-scope release by the consumers), extends the run with the
+// following items that are already complete (up to kWaveRun), then ONE gpu-scope
+// fence and a relaxed counter bump per item.  A fence per item (a MEMBAR.GPU, ~2 us
+// under load, in series on one lane) capped a CTA at one item per ~2.2 us.
+__device__ __forceinline__ void wave_publisher(const WaveArgs& a, int64_t total, const unsigned int* done,
+                                               volatile unsigned int* published) {
+  int64_t m = blockIdx.x, it = 0;
+  auto next_item = [&](int64_t& mm, int& s_, int64_t& k_) {
+    for (; mm < total; mm += gridDim.x) {
+      wave_item(a, mm, s_, k_);
+      if (k_ >= 0 && k_ < a.nchunks) return true;
+    }
+    return false;
+  };
+  int s;
+  int64_t k;
+  bool have = next_item(m, s, k);
+  while (have) {
+    // wait for the first item of the run
+    const unsigned int need0 = (unsigned int)kTmaSlices * (unsigned int)(it / kWaveLag + 1);
+    while (*(volatile const unsigned int*)(done + (it % kWaveLag)) < need0) {
+    }
+    const int64_t m0 = m;
+    int np = 0;
+    do {
+      ++np;
+      ++it;
+      m += gridDim.x;
+      have = next_item(m, s, k);
+    } while (have && np < kWaveRun &&
+             *(volatile const unsigned int*)(done + (it % kWaveLag)) >=
+                 (unsigned int)kTmaSlices * (unsigned int)(it / kWaveLag + 1));
+    __threadfence();  // the consumers' stores of the whole run -> gpu scope
+    int64_t mm = m0;
+    for (int j = 0; j < np; ++j, mm += gridDim.x) {  // the run's items again (no local array)
+      int sj;
+      int64_t kj;
+      next_item(mm, sj, kj);
+      atomicAdd(a.flags + (int64_t)sj * a.nblk + kj / kWaveBlk, (unsigned int)kTmaSlices);
+    }
+    *published = (unsigned int)it;
+  }
+}
+
 // warps 0-7 consume, warp 8 (one lane) produces the TMA ring, warp 9 (one lane)
 // publishes: it waits until the 8 consumer warps have counted item `it` in the
 // shared counter done[it % kWaveLag] (monotone: +8 per use, so no phase
@@ -1042,7 +1136,6 @@ __device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, 
 // ring slots do not wait for it (consumers run at most kWaveLag items ahead of
 // the publisher), so the fence latency is off the ring's critical path.
 constexpr int kWaveThreads = (kTmaSlices + 2) * 32;
-constexpr int kWaveLag = 16;
 constexpr int kWaveSmem =
     kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8 + (kWaveLag + 2) * 4 + kTmaSlices * kWaveMaxStages * 4;
 
@@ -1070,23 +1163,7 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
   double acc[1] = {0.0};
   if (warp == kTmaSlices + 1) {
     // ---------------- publisher (one lane)
-    if (lane == 0) {
-      int64_t it = 0;
-      for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
-        int s;
-        int64_t k;
-        wave_item(a, m, s, k);
-        if (k < 0 || k >= a.nchunks) continue;
-        const unsigned int need = (unsigned int)kTmaSlices * (unsigned int)(it / kWaveLag + 1);
-        volatile unsigned int* dc = done + (it % kWaveLag);
-        while (*dc < need) {
-        }
-        // the consumers' stores (CTA-ordered before their counts) -> gpu scope, with the count
-        red_release_add(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, (unsigned int)kTmaSlices);
-        *published = (unsigned int)(it + 1);
-        ++it;
-      }
-    }
+    if (lane == 0) wave_publisher(a, total, done, published);
   } else if (warp == kTmaSlices) {
     // ---------------- producer (one lane): matrix slices, b, 1/M of each item
     if (lane == 0) {
@@ -1197,7 +1274,7 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
           const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
                              (uint32_t)__shfl_sync(0xffffffffu, h, 0);
           const int w = __shfl_sync(0xffffffffu, h, 4);
-          const bool dia = __shfl_sync(0xffffffffu, h, 5) != 0;
+          const bool dia = __shfl_sync(0xffffffffu, h, 5) == 1;
           const double* v = vs + (vb - vbase) + lane;
           double xv[kTmaMaxW];
           if (dia) {
@@ -1251,21 +1328,33 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
 // the aggregation hierarchy, 20-50 entries per row): no TMA ring, 8 warps per
 // CTA, warp w takes slice 8k + w of each item and streams it with the batched
 // loads of sell_row_sum; same schedule, dependencies and publication.
-constexpr int kWaveDirectThreads = kTmaSlices * 32;
+constexpr int kWaveDirectThreads = (kTmaSlices + 1) * 32;  // + the publisher warp
 
 __global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveArgs a) {
   pdl_enter();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ unsigned int fronts[kTmaSlices * kWaveMaxStages];
+  __shared__ unsigned int done[kWaveLag];
+  __shared__ unsigned int published_s;
+  volatile unsigned int* published = &published_s;
   if (threadIdx.x < kTmaSlices * kWaveMaxStages) fronts[threadIdx.x] = 0;
+  if (threadIdx.x < kWaveLag) done[threadIdx.x] = 0;
+  if (threadIdx.x == 0) published_s = 0;
   __syncthreads();
   const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
   double acc[1] = {0.0};
+  if (warp == kTmaSlices) {
+    if (lane == 0) wave_publisher(a, total, done, published);
+  } else {
+  int64_t it = 0;
   for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
     int s;
     int64_t k;
     wave_item(a, m, s, k);
     if (k < 0 || k >= a.nchunks) continue;
+    if (it >= kWaveLag)
+      while (*published + kWaveLag <= (unsigned int)it) {
+      }
     const int op = a.op[s];
     const bool keep = (s + 1 < a.nst);  // a later stage re-reads the slice: normal caching, else stream
     const int64_t sl = k * kTmaSlices + warp;
@@ -1300,10 +1389,13 @@ __global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveAr
         }
       }
     }
-    // one gpu-scope fence per CTA and item (the barrier orders the other warps'
-    // stores before it), then the block counter counts all 8 warps
-    __syncthreads();
-    if (threadIdx.x == 0) red_release_add(a.flags + (int64_t)s * a.nblk + k / kWaveBlk, (unsigned int)kTmaSlices);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();  // this warp's stores before its count (CTA-scope release)
+      atomicAdd(done + (it % kWaveLag), 1u);
+    }
+    ++it;
+  }
   }
   pdl_exit();
   if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
@@ -1520,7 +1612,7 @@ static bool tmak_ok(const Sell& A, const RowArgs& r, SliceSet set) {
   // slices of 256^3 (A_1: 99 vs 93 us, R_0: 190 vs 178 us): opt-in (PSC_TMAK=1)
   const int off = env_int("PSC_NO_TMA", 0) || !env_int("PSC_TMAK", 0);
   return !off && A.lanes == 1 && A.max_width > kTmaMaxW && set == SliceSet::All && r.vec_padded && A.hdr &&
-         A.n_units > 0;
+         A.n_units > 0 && A.n_dict == 0;  // reads explicit int32 columns
 }
 
 static bool rg_tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
@@ -1647,7 +1739,8 @@ void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, 
 // first stored entry whose local column equals the local row (padding repeats
 // the last column with value 0 and is skipped by the `found` flag);
 // off-diagonal |a_ij| summed in stored order; m = a_ii + sum; dinv = 1/m.
-__global__ void __launch_bounds__(kBlock) l1_dinv_kernel(const int64_t* __restrict__ ptr,
+__global__ void __launch_bounds__(kBlock) l1_dinv_kernel(const int32_t* __restrict__ hdr,
+                                                         const int64_t* __restrict__ ptr,
                                                          const int64_t* __restrict__ cptr,
                                                          const int32_t* __restrict__ col,
                                                          const double* __restrict__ val, int64_t n, int64_t ncols,
@@ -1660,7 +1753,7 @@ __global__ void __launch_bounds__(kBlock) l1_dinv_kernel(const int64_t* __restri
       const int64_t vb = ptr[s] + (i & 31);
       const int w = (int)((ptr[s + 1] - ptr[s]) >> 5);
       for (int k = 0; k < w; ++k) {
-        const int64_t c = sell_col(cptr, col, s, w, i, k, ncols);
+        const int64_t c = sell_col(hdr, cptr, col, s, w, i, k, ncols);
         const double v = val[vb + 32 * (int64_t)k];
         if (c == i && !found) {
           aii = v;
@@ -1686,7 +1779,7 @@ __global__ void __launch_bounds__(kBlock) l1_dinv_kernel(const int64_t* __restri
 
 void launch_l1_dinv(psc_ctx* ctx, const Sell& A, double* dinv, cudaStream_t s) {
   if (A.n_rows == 0) return;
-  l1_dinv_kernel<<<vec_grid(ctx, A.n_rows), kBlock, 0, s>>>(A.ptr, A.cptr, A.col, A.val, A.n_rows, A.n_cols_local,
+  l1_dinv_kernel<<<vec_grid(ctx, A.n_rows), kBlock, 0, s>>>(A.hdr, A.ptr, A.cptr, A.col, A.val, A.n_rows, A.n_cols_local,
                                                             A.lanes, dinv);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
@@ -1937,6 +2030,7 @@ constexpr int kMaxSmem = 227 * 1024;
 int64_t coarse_smem_rows() { return (64 * 1024) / (4 * sizeof(double)); }
 
 struct CoarseArgs {
+  const int32_t* hdr;   // sliced ELL only
   const int64_t* ptr;
   const int64_t* cptr;  // sliced ELL only
   const int32_t* col;
@@ -1997,7 +2091,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve(CoarseArgs a) {
           const int64_t base = ptr[s] + (i & 31);
           const int w = (int)((ptr[s + 1] - ptr[s]) >> 5);
           for (int k = sub; k < w; k += gk) {
-            const int64_t c = sell_col(cptr, col, s, w, i, k, n);
+            const int64_t c = sell_col(a.hdr, cptr, col, s, w, i, k, n);
             if (c >= 0) sum = fma(val[base + 32 * k], xa[c], sum);
           }
         } else {
@@ -2049,7 +2143,7 @@ void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const 
   const int64_t nptr = sell ? A.n_units + 1 : n + 1;
   int gk = 1;
   while (gk < 32 && (int64_t)(gk * 2) * std::max<int64_t>(n, 1) <= kCoarseThreads) gk *= 2;
-  CoarseArgs a{A.ptr, A.cptr, A.col, A.val, n, nptr, A.padded, A.col_slots, gk, dinv, b, x, nsweeps};
+  CoarseArgs a{A.hdr, A.ptr, A.cptr, A.col, A.val, n, nptr, A.padded, A.col_slots, gk, dinv, b, x, nsweeps};
   const size_t vec = (size_t)std::max<int64_t>(n, 1) * 4 * sizeof(double);
   const size_t mat = (size_t)A.padded * sizeof(double) + (size_t)A.col_slots * sizeof(int32_t) +
                      (size_t)nptr * sizeof(int64_t) * (sell ? 2 : 1);
@@ -2067,7 +2161,8 @@ void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const 
 // all 1024 threads (gk lanes per row, fixed shuffle tree).
 int64_t coarse_dense_max_rows() { return 144; }
 
-__global__ void dense_from_sell_kernel(const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
+__global__ void dense_from_sell_kernel(const int32_t* __restrict__ hdr, const int64_t* __restrict__ ptr,
+                                       const int64_t* __restrict__ cptr,
                                        const int32_t* __restrict__ col, const double* __restrict__ val, int64_t n,
                                        int lanes, double* __restrict__ dense) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2078,7 +2173,7 @@ __global__ void dense_from_sell_kernel(const int64_t* __restrict__ ptr, const in
     const int64_t vb = ptr[s] + (i & 31);
     const int w = (int)((ptr[s + 1] - ptr[s]) >> 5);
     for (int k = 0; k < w; ++k) {
-      const int64_t c = sell_col(cptr, col, s, w, i, k, n);
+      const int64_t c = sell_col(hdr, cptr, col, s, w, i, k, n);
       if (c >= 0) row[c] += val[vb + 32 * (int64_t)k];  // padding adds 0.0
     }
   } else {
@@ -2090,7 +2185,8 @@ void dense_from_sell(psc_ctx* ctx, const Sell& A, double* dense, cudaStream_t s)
   const int64_t n = A.n_rows;
   PSC_CUDA(cudaMemsetAsync(dense, 0, sizeof(double) * n * n, s));
   if (n == 0) return;
-  dense_from_sell_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A.ptr, A.cptr, A.col, A.val, n, A.lanes, dense);
+  dense_from_sell_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A.hdr, A.ptr, A.cptr, A.col, A.val, n, A.lanes,
+                                                                      dense);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -2285,19 +2381,20 @@ void launch_coarse_dense_pcg(psc_ctx* ctx, const double* Ad, int64_t n, const do
 // Row bandwidth of a square matrix in the sliced-ELL layout: max |j - i| over
 // the stored entries (DIA slices: their offsets; ELL padding repeats a real
 // column of the row, an empty row pads with column 0 — conservative).
-__global__ void sell_bw_kernel(const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
-                               const int32_t* __restrict__ col, int64_t n_rows, int64_t n_slices,
-                               unsigned long long* out) {
+__global__ void sell_bw_kernel(const int32_t* __restrict__ hdr, const int64_t* __restrict__ ptr,
+                               const int64_t* __restrict__ cptr, const int32_t* __restrict__ col, int64_t n_rows,
+                               int64_t n_slices, unsigned long long* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_slices * 32) return;
   const int64_t sl = i >> 5;
   const int w = (int)((ptr[sl + 1] - ptr[sl]) >> 5);
   const int64_t cb = cptr[sl];
-  const bool dia = (cptr[sl + 1] - cb) < 32 * (int64_t)w;
+  const int kind = hdr[sl * kHdr + 5];
   unsigned long long m = 0;
-  if (dia) {
+  if (kind != kEll) {  // DIA offsets / DICT table
+    const int nt = kind == kDia ? w : hdr[sl * kHdr + 6];
     if ((i & 31) == 0)
-      for (int k = 0; k < w; ++k) m = max(m, (unsigned long long)llabs((long long)col[cb + k]));
+      for (int k = 0; k < nt; ++k) m = max(m, (unsigned long long)llabs((long long)col[cb + k]));
   } else if (i < n_rows) {
     for (int k = 0; k < w; ++k) m = max(m, (unsigned long long)llabs((long long)col[cb + 32 * (int64_t)k + (i & 31)] - i));
   }
@@ -2310,7 +2407,7 @@ int64_t sell_bandwidth(psc_ctx* ctx, const Sell& A, cudaStream_t s) {
   unsigned long long* d = dalloc<unsigned long long>(1);
   PSC_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
   const int64_t nt = A.n_units * 32;
-  sell_bw_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(A.ptr, A.cptr, A.col, A.n_rows, A.n_units, d);
+  sell_bw_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(A.hdr, A.ptr, A.cptr, A.col, A.n_rows, A.n_units, d);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
   unsigned long long hbw = 0;
@@ -2343,9 +2440,9 @@ __device__ __forceinline__ int32_t map_col(int64_t g, int64_t own_begin, int64_t
 // (8 B x 32 d value slots beat 12 B x 32 w value+column slots).
 __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_t* __restrict__ rowptr,
                                   const int64_t* __restrict__ colg, int64_t own_begin, int64_t n_own, int allow_dia,
-                                  int64_t* __restrict__ vslots, int64_t* __restrict__ cslots,
+                                  int allow_dict, int64_t* __restrict__ vslots, int64_t* __restrict__ cslots,
                                   int64_t* __restrict__ snnz, int32_t* __restrict__ bflag, int32_t* __restrict__ dia_d,
-                                  int32_t* __restrict__ dia_off) {
+                                  int32_t* __restrict__ dia_off, int32_t* __restrict__ dict_d) {
   const int lane = threadIdx.x & 31;
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= n_slices) return;
@@ -2386,12 +2483,34 @@ __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_
     }
     if (!ok || 2 * d > 3 * w) d = 0;
   }
+  // DICT: wide slice of owned columns with at most kMaxDict distinct offsets j - i
+  // (sorted, by the same merge of the rows' sorted offsets)
+  int dd = 0;
+  if (d == 0 && allow_dict && !off && w > kTmaMaxW) {
+    int q = 0, t = 0;
+    bool ok = true;
+    for (;;) {
+      const long long my = (q < len) ? (long long)(colg[b + q] - own_begin - i) : LLONG_MAX;
+      long long mn = my;
+      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      if (mn == LLONG_MAX) break;
+      if (t == kMaxDict) {
+        ok = false;
+        break;
+      }
+      ++t;
+      if (my == mn) ++q;
+    }
+    if (ok) dd = t;
+  }
   if (lane == 0) {
     vslots[s] = 32 * (int64_t)(d ? d : w);
-    cslots[s] = d ? (int64_t)((d + 3) & ~3) : 32 * (int64_t)w;  // DIA: offsets, padded to 16 B
+    // DIA: offsets, padded to 16 B; DICT: table + byte indices; ELL: int32 columns
+    cslots[s] = d ? (int64_t)((d + 3) & ~3) : (dd ? (int64_t)((dd + 3) & ~3) + 32 * (int64_t)((w + 3) / 4) : 32 * (int64_t)w);
     snnz[s] = tot;
     bflag[s] = off;
     dia_d[s] = d;
+    dict_d[s] = dd;
   }
 }
 
@@ -2401,8 +2520,9 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
                                  const int64_t* __restrict__ colg, const double* __restrict__ valcsr,
                                  const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
                                  const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
-                                 int64_t own_begin, int64_t n_own, const int64_t* __restrict__ halo, int64_t nh,
-                                 int32_t* __restrict__ col, double* __restrict__ val, int* err) {
+                                 const int32_t* __restrict__ dict_d, int64_t own_begin, int64_t n_own,
+                                 const int64_t* __restrict__ halo, int64_t nh, int32_t* __restrict__ col,
+                                 double* __restrict__ val, int* err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_slices * 32) return;
   const int64_t s = i >> 5;
@@ -2430,6 +2550,46 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
     if (lane == 0)
       for (int j = d; j < ((d + 3) & ~3); ++j) col[cb + j] = 0;
     if (q != e) *err = 2;
+    return;
+  }
+  const int dd = dict_d[s];
+  if (dd > 0) {  // DICT slice (warp = slice): table of sorted distinct offsets, byte indices
+    int32_t* tbl = col + cb;
+    uint32_t* iw = reinterpret_cast<uint32_t*>(col + cb + ((dd + 3) & ~3));
+    const int len = (int)(e - b);
+    int q = 0, t = 0, lastb = 0;
+    uint32_t word = 0;
+    for (;;) {
+      const long long my = (q < len) ? (long long)(colg[b + q] - own_begin - i) : LLONG_MAX;
+      long long mn = my;
+      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      if (mn == LLONG_MAX) break;
+      if (lane == 0 && t < dd) tbl[t] = (int32_t)mn;
+      if (my == mn) {
+        word |= (uint32_t)t << (8 * (q & 3));
+        val[vb + 32 * (int64_t)q + lane] = valcsr[b + q];
+        lastb = t;
+        if ((q & 3) == 3) {
+          iw[32 * (int64_t)(q >> 2) + lane] = word;
+          word = 0;
+        }
+        ++q;
+      }
+      ++t;
+    }
+    for (; q < 4 * ((w + 3) / 4); ++q) {  // padding: repeat the last column with value 0
+      if (q < w) {
+        word |= (uint32_t)lastb << (8 * (q & 3));
+        val[vb + 32 * (int64_t)q + lane] = 0.0;
+      }
+      if ((q & 3) == 3) {
+        iw[32 * (int64_t)(q >> 2) + lane] = word;
+        word = 0;
+      }
+    }
+    if (lane == 0)
+      for (int j = dd; j < ((dd + 3) & ~3); ++j) tbl[j] = 0;
+    if (t != dd) *err = 2;
     return;
   }
   int32_t last = 0;
@@ -2501,7 +2661,7 @@ int choose_lanes(int64_t n_rows, int64_t nnz) {
 
 __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
                                 const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
-                                int32_t* __restrict__ hdr, int* all_dia_diag) {
+                                const int32_t* __restrict__ dict_d, int32_t* __restrict__ hdr, int* all_dia_diag) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_slices) return;
   int32_t* h = hdr + s * kHdr;
@@ -2511,13 +2671,14 @@ __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ pt
   h[2] = (int32_t)(uint32_t)(cb & 0xffffffffu);
   h[3] = (int32_t)(uint32_t)((uint64_t)cb >> 32);
   h[4] = (int32_t)((ptr[s + 1] - vb) >> 5);
-  const int d = dia_d[s];
-  h[5] = d > 0 ? 1 : 0;
+  const int d = dia_d[s], dd = dict_d[s];
+  h[5] = d > 0 ? kDia : (dd > 0 ? kDict : kEll);
   int j0 = -1;
   for (int j = 0; j < kMaxDia; ++j) {
     h[6 + j] = j < d ? dia_off[s * kMaxDia + j] : 0;
     if (j < d && dia_off[s * kMaxDia + j] == 0) j0 = j;
   }
+  if (dd > 0) h[6] = dd;
   h[14] = j0;  // DIA: slot of the diagonal (offset 0), -1 if none
   h[15] = 0;
   if (j0 < 0) atomicAnd(all_dia_diag, 0);
@@ -2541,6 +2702,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
   std::vector<int32_t> flag;      // per unit (sell) or per row (row groups)
   std::vector<int64_t> hp;        // ptr on the host
   std::vector<int32_t> hdia;      // DIA widths per slice
+  std::vector<int32_t> hdict;     // DICT table sizes per slice
   std::vector<int64_t> hsnnz;     // nnz per slice
   size_t tmp_bytes = 0;
   if (sell) {
@@ -2550,12 +2712,14 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     int32_t* d_flag = dalloc<int32_t>(nu);
     int32_t* d_diad = dalloc<int32_t>(nu);
     int32_t* d_diaoff = dalloc<int32_t>((size_t)nu * kMaxDia);
+    int32_t* d_dictd = dalloc<int32_t>(nu);
+    const bool allow_dict = !env_int("PSC_NO_DICT", 0);
     PSC_CUDA(cudaMemsetAsync(d_vs, 0, sizeof(int64_t) * (nu + 1), s));
     PSC_CUDA(cudaMemsetAsync(d_cs, 0, sizeof(int64_t) * (nu + 1), s));
     if (nu > 0) {
       sell_width_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
-          n_rows, nu, d_rowptr, d_colg, own_begin, n_own, allow_dia ? 1 : 0, d_vs, d_cs, d_snnz, d_flag, d_diad,
-          d_diaoff);
+          n_rows, nu, d_rowptr, d_colg, own_begin, n_own, allow_dia ? 1 : 0, allow_dict ? 1 : 0, d_vs, d_cs, d_snnz,
+          d_flag, d_diad, d_diaoff, d_dictd);
       PSC_CUDA(cudaGetLastError());
     }
     S.ptr = dalloc<int64_t>(nu + 1);
@@ -2575,13 +2739,14 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     S.hdr = dalloc<int32_t>((size_t)nu * kHdr);
     if (nu > 0) {
       sell_fill_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
-          n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, own_begin, n_own, d_halo, n_halo,
-          S.col, S.val, d_err);
+          n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, d_dictd, own_begin, n_own, d_halo,
+          n_halo, S.col, S.val, d_err);
       PSC_CUDA(cudaGetLastError());
       int* d_all = dalloc<int>(1);
       const int one = 1;
       PSC_CUDA(cudaMemcpyAsync(d_all, &one, sizeof(int), cudaMemcpyHostToDevice, s));
-      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, S.hdr, d_all);
+      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, d_dictd, S.hdr,
+                                                                   d_all);
       PSC_CUDA(cudaGetLastError());
       int h_all = 0;
       PSC_CUDA(cudaMemcpyAsync(&h_all, d_all, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -2593,7 +2758,9 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     hp.resize(nu + 1);
     hdia.resize(nu);
     hsnnz.resize(nu);
+    hdict.resize(nu);
     if (nu) {
+      PSC_CUDA(cudaMemcpyAsync(hdict.data(), d_dictd, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
       PSC_CUDA(cudaMemcpyAsync(flag.data(), d_flag, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
       PSC_CUDA(cudaMemcpyAsync(hdia.data(), d_diad, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
       PSC_CUDA(cudaMemcpyAsync(hsnnz.data(), d_snnz, sizeof(int64_t) * nu, cudaMemcpyDeviceToHost, s));
@@ -2604,6 +2771,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     dfree(d_flag);
     dfree(d_diad);
     dfree(d_diaoff);
+    dfree(d_dictd);
   } else {
     int64_t* d_len = dalloc<int64_t>(nptr);
     int32_t* d_flag = dalloc<int32_t>(n_rows);
@@ -2642,7 +2810,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
   PSC_CUDA(cudaStreamSynchronize(s));
   dfree(d_err);
   PSC_REQUIRE(h_err == 0, PSC_ERR_STATE,
-              h_err == 2 ? "DIA slice fill mismatch" : "column not in the owned block nor in the assembled halo");
+              h_err == 2 ? "DIA/DICT slice fill mismatch" : "column not in the owned block nor in the assembled halo");
   std::vector<int32_t> in, bd;
   S.nnz_ell = sell ? 0 : nnz;
   for (int64_t u = 0; u < nu; ++u) {
@@ -2651,6 +2819,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
       f = flag[u];
       S.max_width = std::max<int>(S.max_width, (int)((hp[u + 1] - hp[u]) / 32));
       if (hdia[u]) S.n_dia++;
+      else if (hdict[u]) S.n_dict++;
       else S.nnz_ell += hsnnz[u];
     } else {
       for (int64_t i = u * RU; i < std::min<int64_t>(n_rows, (u + 1) * RU); ++i) {
