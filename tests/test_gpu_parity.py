@@ -255,8 +255,8 @@ VARIANTS = [
     {"PSC_LANES": "8"},
     {"PSC_LANES": "32", "PSC_NO_TMA": "1"},
     {"PSC_RG_MIN": "4", "PSC_RG_DIV": "1"},
-    {"PSC_NO_DICT": "1"},
-    {"PSC_NO_DICT": "1", "PSC_NO_TMA": "1"},
+    {"PSC_DICT": "1"},
+    {"PSC_DICT": "1", "PSC_NO_TMA": "1", "PSC_NO_DENSE_COARSE": "1"},
     {"PSC_WAVE": "1"},
     {"PSC_WAVE": "1", "PSC_WAVE_DIRECT": "1"},
     {"PSC_WAVE": "1", "PSC_WAVE_SLACK": "0", "PSC_NO_FUSED_SCALE": "1"},
