@@ -227,6 +227,46 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
   const int32_t* c = col + cb + lane;
   double sum = 0.0;
   int k = 0;
+#ifdef PSC_ELL_PIPE
+  // software-pipelined batches: the next batch's (value, column) loads are in
+  // flight while the current batch's gathers are
+  if (w >= 16) {
+    int ci[8], cn[8];
+    double vi[8], vn[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      ci[j] = ldm(c + 32 * j, keep);
+      vi[j] = ldm(v + 32 * j, keep);
+    }
+    for (; k + 16 <= w; k += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cn[j] = ldm(c + 256 + 32 * j, keep);
+        vn[j] = ldm(v + 256 + 32 * j, keep);
+      }
+      double xv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) xv[j] = ldx<CG>(x + ci[j]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum = fma(vi[j], xv[j], sum);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ci[j] = cn[j];
+        vi[j] = vn[j];
+      }
+      c += 256;
+      v += 256;
+    }
+    double xv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xv[j] = ldx<CG>(x + ci[j]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sum = fma(vi[j], xv[j], sum);
+    c += 256;
+    v += 256;
+    k += 8;
+  }
+#endif
   for (; k + 8 <= w; k += 8) {
     int ci[8];
     double vi[8];
