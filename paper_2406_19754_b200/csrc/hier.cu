@@ -297,13 +297,14 @@ bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
 // key slack: dependencies should lie outside the items in flight (~3 per CTA,
 // 2 CTAs per SM), while the rows between a chunk's first and last stage must
 // stay in L2 (window (nst-1) * G chunks, budget ~96 MB of the 126 MB)
+// (all in items of 8 chunks = 2048 rows)
 int64_t wave_slack(psc_hier* h, const LevelWS& W, int nst) {
   const char* e = getenv("PSC_WAVE_SLACK");
   if (e) return std::max(0, atoi(e));
-  const int64_t inflight = 3 * 2 * (int64_t)h->ctx->num_sms / std::max(nst, 1);
+  const int64_t inflight = 2 * 2 * (int64_t)h->ctx->num_sms / std::max(nst, 1);
   const double row_bytes = 12.0 * (double)W.A->S.padded / std::max<int64_t>(W.n, 1) + 32.0;
-  const int64_t gmax = (int64_t)(96.0 * (1 << 20) / (std::max(nst - 1, 1) * kWaveChunkRows * row_bytes));
-  return std::max<int64_t>(8, std::min(inflight, gmax - W.wave_h - kWaveBlk));
+  const int64_t gmax = (int64_t)(96.0 * (1 << 20) / (std::max(nst - 1, 1) * 8 * kWaveChunkRows * row_bytes));
+  return std::max<int64_t>(2, std::min(inflight, gmax - (W.wave_h + kWaveBlk + 8) / 8 - 1));
 }
 
 void wave_setup(psc_hier* h, LevelWS& W) {
@@ -315,7 +316,7 @@ void wave_setup(psc_hier* h, LevelWS& W) {
 
 void wave_launch(psc_hier* h, LevelWS& W, WaveArgs& a, cudaStream_t s) {
   a.h = W.wave_h;
-  a.G = W.wave_h + kWaveBlk + wave_slack(h, W, a.nst);
+  a.G = (W.wave_h + kWaveBlk + 8 + 7) / 8 + wave_slack(h, W, a.nst);  // items of 8 chunks
   a.flags = W.wave_flags;
   launch_wave(h->ctx, W.A->S, a, s);
 }

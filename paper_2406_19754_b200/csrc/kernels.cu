@@ -227,46 +227,6 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
   const int32_t* c = col + cb + lane;
   double sum = 0.0;
   int k = 0;
-#ifdef PSC_ELL_PIPE
-  // software-pipelined batches: the next batch's (value, column) loads are in
-  // flight while the current batch's gathers are
-  if (w >= 16) {
-    int ci[8], cn[8];
-    double vi[8], vn[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      ci[j] = ldm(c + 32 * j, keep);
-      vi[j] = ldm(v + 32 * j, keep);
-    }
-    for (; k + 16 <= w; k += 8) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        cn[j] = ldm(c + 256 + 32 * j, keep);
-        vn[j] = ldm(v + 256 + 32 * j, keep);
-      }
-      double xv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) xv[j] = ldx<CG>(x + ci[j]);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) sum = fma(vi[j], xv[j], sum);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        ci[j] = cn[j];
-        vi[j] = vn[j];
-      }
-      c += 256;
-      v += 256;
-    }
-    double xv[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) xv[j] = ldx<CG>(x + ci[j]);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) sum = fma(vi[j], xv[j], sum);
-    c += 256;
-    v += 256;
-    k += 8;
-  }
-#endif
   for (; k + 8 <= w; k += 8) {
     int ci[8];
     double vi[8];
@@ -1080,21 +1040,19 @@ __device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v)
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Whole warp: wait until stage s-1 has completed every block up to the one
-// holding chunk k+h.  *front = this warp's verified prefix of complete blocks of
-// that stage (shared memory, per warp and stage; counters only grow within a
-// pass): most items find it already far enough and need no memory round trip;
-// otherwise one bulk check of the next 64 blocks (2 per lane, ld.acquire, ballot)
-// advances it.  The acquire that verified a block orders this warp's later reads.
+// Whole warp: wait until stage s-1 has completed every block up to `b1`.
+// *front = this warp's verified prefix of complete blocks of that stage (shared
+// memory, per warp and stage; counters only grow within a pass): most items find
+// it already far enough; otherwise one bulk check of the next 64 blocks (2 per
+// lane, ballot) advances it.
 __device__ __forceinline__ bool wave_block_done(const unsigned int* cnt, int64_t b, int64_t nblk, int64_t nchunks) {
   if (b >= nblk) return true;
   const unsigned int need = (unsigned int)(kTmaSlices * min((int64_t)kWaveBlk, nchunks - b * kWaveBlk));
   return ld_acquire_u32(cnt + b) >= need;
 }
 
-__device__ __forceinline__ void wave_wait(const unsigned int* cnt, unsigned int* front, int64_t k, int64_t h,
-                                          int64_t nchunks, int64_t nblk, int lane) {
-  const int64_t b1 = min(k + h, nchunks - 1) / kWaveBlk;
+__device__ __forceinline__ void wave_wait(const unsigned int* cnt, unsigned int* front, int64_t b1, int64_t nchunks,
+                                          int64_t nblk, int lane) {
   int64_t f = *(volatile unsigned int*)front;
   if (f > b1) return;
   const long long t0 = clock64();
@@ -1113,68 +1071,53 @@ __device__ __forceinline__ void wave_wait(const unsigned int* cnt, unsigned int*
   __syncwarp();
 }
 
-__device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, int64_t& k) {
+// Items are super-chunks of kWaveItem chunks (2048 rows): the dependency check
+// and the publication (a gpu-scope fence, ~2 us under load) are paid once per
+// ~8 us of streaming instead of per chunk (with 256-row items the pass was
+// dependency-bound: ~4 failed polls per item, 2.2-2.4 ms per 4-stage pass).
+constexpr int kWaveItem = 8;
+static_assert(kWaveBlk % kWaveItem == 0, "items must not straddle completion blocks");
+
+__device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, int64_t& q) {
   const int64_t K = m / a.nst;
   s = (int)(m - K * a.nst);
-  k = K - a.G * s;
+  q = K - a.G * s;  // item index: chunks [kWaveItem q, kWaveItem (q + 1))
 }
 
-constexpr int kWaveLag = 16;  // consumers run at most this many items ahead of the publisher
-constexpr int kWaveRun = 8;   // items published per gpu-scope fence, at most
+__device__ __forceinline__ int64_t wave_nitems(const WaveArgs& a) { return (a.nchunks + kWaveItem - 1) / kWaveItem; }
+
+// the last completion block stage s-1 must have finished before item q of stage s
+__device__ __forceinline__ int64_t wave_dep_block(const WaveArgs& a, int64_t q) {
+  return min(kWaveItem * q + kWaveItem - 1 + a.h, a.nchunks - 1) / kWaveBlk;
+}
+
+constexpr int kWaveLag = 8;  // consumers run at most this many items ahead of the publisher
 
 // One lane per CTA publishes its items in order: it waits until the 8 consumer
 // warps have counted item `it` in done[it % kWaveLag] (monotone, +8 per use: no
-// phase aliasing; CTA-scope release by the consumers), extends the run with the
-// following items that are already complete (up to kWaveRun), then ONE gpu-scope
-// fence and a relaxed counter bump per item.  A fence per item (a MEMBAR.GPU, ~2 us
-// under load, in series on one lane) capped a CTA at one item per ~2.2 us.
+// phase aliasing; CTA-scope release by the consumers), then ONE gpu-scope fence
+// and the block-counter bump (8 warps x the item's chunks).
 __device__ __forceinline__ void wave_publisher(const WaveArgs& a, int64_t total, const unsigned int* done,
                                                volatile unsigned int* published) {
-  int64_t m = blockIdx.x, it = 0;
-  auto next_item = [&](int64_t& mm, int& s_, int64_t& k_) {
-    for (; mm < total; mm += gridDim.x) {
-      wave_item(a, mm, s_, k_);
-      if (k_ >= 0 && k_ < a.nchunks) return true;
+  const int64_t nit = wave_nitems(a);
+  int64_t it = 0;
+  for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
+    int s;
+    int64_t q;
+    wave_item(a, m, s, q);
+    if (q < 0 || q >= nit) continue;
+    const unsigned int need = (unsigned int)kTmaSlices * (unsigned int)(it / kWaveLag + 1);
+    while (*(volatile const unsigned int*)(done + (it % kWaveLag)) < need) {
     }
-    return false;
-  };
-  int s;
-  int64_t k;
-  bool have = next_item(m, s, k);
-  while (have) {
-    // wait for the first item of the run
-    const unsigned int need0 = (unsigned int)kTmaSlices * (unsigned int)(it / kWaveLag + 1);
-    while (*(volatile const unsigned int*)(done + (it % kWaveLag)) < need0) {
-    }
-    const int64_t m0 = m;
-    int np = 0;
-    do {
-      ++np;
-      ++it;
-      m += gridDim.x;
-      have = next_item(m, s, k);
-    } while (have && np < kWaveRun &&
-             *(volatile const unsigned int*)(done + (it % kWaveLag)) >=
-                 (unsigned int)kTmaSlices * (unsigned int)(it / kWaveLag + 1));
-    __threadfence();  // the consumers' stores of the whole run -> gpu scope
-    int64_t mm = m0;
-    for (int j = 0; j < np; ++j, mm += gridDim.x) {  // the run's items again (no local array)
-      int sj;
-      int64_t kj;
-      next_item(mm, sj, kj);
-      atomicAdd(a.flags + (int64_t)sj * a.nblk + kj / kWaveBlk, (unsigned int)kTmaSlices);
-    }
-    *published = (unsigned int)it;
+    const int64_t c0 = kWaveItem * q, nc = min((int64_t)kWaveItem, a.nchunks - c0);
+    __threadfence();  // the consumers' stores of the item -> gpu scope
+    atomicAdd(a.flags + (int64_t)s * a.nblk + c0 / kWaveBlk, (unsigned int)(kTmaSlices * nc));
+    *published = (unsigned int)(++it);
   }
 }
 
-// warps 0-7 consume, warp 8 (one lane) produces the TMA ring, warp 9 (one lane)
-// publishes: it waits until the 8 consumer warps have counted item `it` in the
-// shared counter done[it % kWaveLag] (monotone: +8 per use, so no phase
-// aliasing; CTA-scope release by the consumers, acquire by the publisher), then
-// issues ONE gpu-scope fence and the block-counter bump for the whole CTA.  The
-// ring slots do not wait for it (consumers run at most kWaveLag items ahead of
-// the publisher), so the fence latency is off the ring's critical path.
+// warps 0-7 consume, warp 8 (one lane) produces the TMA ring (chunk by chunk),
+// warp 9 (one lane) publishes items.
 constexpr int kWaveThreads = (kTmaSlices + 2) * 32;
 constexpr int kWaveSmem =
     kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8 + (kWaveLag + 2) * 4 + kTmaSlices * kWaveMaxStages * 4;
@@ -1199,176 +1142,164 @@ __global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
+  const int64_t nit = wave_nitems(a);
+  const int64_t total = (int64_t)a.nst * (nit + a.G * (a.nst - 1));
   double acc[1] = {0.0};
   if (warp == kTmaSlices + 1) {
-    // ---------------- publisher (one lane)
     if (lane == 0) wave_publisher(a, total, done, published);
   } else if (warp == kTmaSlices) {
-    // ---------------- producer (one lane): matrix slices, b, 1/M of each item
+    // ---------------- producer (one lane): matrix slices, b, 1/M of every chunk
     if (lane == 0) {
       uint64_t pol_stream, pol_keep;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
-      // the next valid item and its slice offsets are loaded one item ahead
-      auto next_valid = [&](int64_t m0, int& s_, int64_t& k_) {
-        for (int64_t mm = m0; mm < total; mm += gridDim.x) {
-          wave_item(a, mm, s_, k_);
-          if (k_ >= 0 && k_ < a.nchunks) return mm;
-        }
-        return total;
-      };
-      auto offsets = [&](int64_t k_, int64_t (&o)[4]) {
-        const int64_t s0 = k_ * kTmaSlices, s1 = min(s0 + kTmaSlices, a.n_slices);
-        o[0] = a.ptr[s0]; o[1] = a.ptr[s1]; o[2] = a.cptr[s0]; o[3] = a.cptr[s1];
-      };
-      int s;
-      int64_t k;
-      int64_t m = next_valid(blockIdx.x, s, k);
-      int64_t off[4] = {0, 0, 0, 0};
-      if (m < total) offsets(k, off);
-      int64_t it = 0;
-      while (m < total) {
-        int sn = 0;
-        int64_t kn = 0;
-        const int64_t mn = next_valid(m + gridDim.x, sn, kn);
-        int64_t offn[4] = {0, 0, 0, 0};
-        if (mn < total) offsets(kn, offn);
+      int64_t it = 0;  // chunks produced
+      for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
+        int s;
+        int64_t q;
+        wave_item(a, m, s, q);
+        if (q < 0 || q >= nit) continue;
         const int op = a.op[s];
-        // re-read by a later stage: keep in L2; last reader: stream out
-        const uint64_t pol = (s + 1 < a.nst) ? pol_keep : pol_stream;
-        const int st = (int)(it % kTmaStages);
-        if (it >= kTmaStages) mbar_wait(&empty[st], (uint32_t)((it / kTmaStages - 1) & 1));
-        unsigned char* base = smem + st * kTmaStageBytes;
-        const int64_t s0 = k * kTmaSlices, s1 = min(s0 + kTmaSlices, a.n_slices);
-        const int64_t r0 = s0 * 32, r1 = min(s1 * 32, a.n_rows);
-        uint32_t hb = 0, vbytes = 0, cbytes = 0;
-        int64_t vb0 = 0, cb0 = 0;
+        const uint64_t pol = (s + 1 < a.nst) ? pol_keep : pol_stream;  // re-read by a later stage: keep
+        const int64_t c1 = min(kWaveItem * q + kWaveItem, a.nchunks);
+        int64_t nxt[4] = {0, 0, 0, 0};
         if (op != (int)WaveOp::Scale) {
-          vb0 = off[0];
-          cb0 = off[2];
-          hb = (uint32_t)(s1 - s0) * kHdr * 4;
-          vbytes = (uint32_t)(off[1] - vb0) * 8;
-          cbytes = (uint32_t)(off[3] - cb0) * 4;
+          const int64_t s0 = kWaveItem * q * kTmaSlices;
+          nxt[0] = a.ptr[s0];
+          nxt[2] = a.cptr[s0];
         }
-        const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
-        const bool needd = (op != (int)WaveOp::Resid);
-        mbar_expect_tx(&full[st], hb + vbytes + cbytes + rbytes * (needd ? 2u : 1u));
-        if (hb) bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol);
-        if (vbytes) bulk_g2s(base + kTmaHdrBytes, a.val + vb0, vbytes, &full[st], pol);
-        if (cbytes) bulk_g2s(base + kTmaHdrBytes + kTmaValBytes, a.col + cb0, cbytes, &full[st], pol);
-        unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
-        if (rbytes) {
-          bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol);
-          if (needd) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol);
+        for (int64_t k = kWaveItem * q; k < c1; ++k, ++it) {
+          const int64_t s0 = k * kTmaSlices, s1 = min(s0 + kTmaSlices, a.n_slices);
+          int64_t vb0 = nxt[0], cb0 = nxt[2];
+          if (op != (int)WaveOp::Scale) {  // this chunk's end = the next chunk's start
+            nxt[0] = a.ptr[s1];
+            nxt[2] = a.cptr[s1];
+          }
+          const int st = (int)(it % kTmaStages);
+          if (it >= kTmaStages) mbar_wait(&empty[st], (uint32_t)((it / kTmaStages - 1) & 1));
+          unsigned char* base = smem + st * kTmaStageBytes;
+          const int64_t r0 = s0 * 32, r1 = min(s1 * 32, a.n_rows);
+          uint32_t hb = 0, vbytes = 0, cbytes = 0;
+          if (op != (int)WaveOp::Scale) {
+            hb = (uint32_t)(s1 - s0) * kHdr * 4;
+            vbytes = (uint32_t)(nxt[0] - vb0) * 8;
+            cbytes = (uint32_t)(nxt[2] - cb0) * 4;
+          }
+          const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
+          const bool needd = (op != (int)WaveOp::Resid);
+          mbar_expect_tx(&full[st], hb + vbytes + cbytes + rbytes * (needd ? 2u : 1u));
+          if (hb) bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol);
+          if (vbytes) bulk_g2s(base + kTmaHdrBytes, a.val + vb0, vbytes, &full[st], pol);
+          if (cbytes) bulk_g2s(base + kTmaHdrBytes + kTmaValBytes, a.col + cb0, cbytes, &full[st], pol);
+          unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
+          if (rbytes) {
+            bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol);
+            if (needd) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol);
+          }
         }
-        ++it;
-        m = mn;
-        s = sn;
-        k = kn;
-        for (int j = 0; j < 4; ++j) off[j] = offn[j];
       }
     }
   } else {
-    // ---------------- consumers: warp `warp` takes slice 8k + warp of each item
+    // ---------------- consumers: warp `warp` takes slice 8k + warp of every chunk k
     const uint32_t nc = (uint32_t)a.ncols;
-    int64_t it = 0;
+    int64_t it = 0, ii = 0;  // chunks consumed, items consumed
     for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
       int s;
-      int64_t k;
-      wave_item(a, m, s, k);
-      if (k < 0 || k >= a.nchunks) continue;
+      int64_t q;
+      wave_item(a, m, s, q);
+      if (q < 0 || q >= nit) continue;
       const int op = a.op[s];
-      const int st = (int)(it % kTmaStages);
       // at most kWaveLag items ahead of the publisher (its done counters are reused)
-      if (it >= kWaveLag)
-        while (*published + kWaveLag <= (unsigned int)it) {
+      if (ii >= kWaveLag)
+        while (*published + kWaveLag <= (unsigned int)ii) {
         }
-      // dependencies first: the item's bulk copies are in flight meanwhile
       if (s > 0)
-        wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, fronts + warp * kWaveMaxStages + (s - 1), k, a.h, a.nchunks,
-                  a.nblk, lane);
-      mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
+        wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, fronts + warp * kWaveMaxStages + (s - 1), wave_dep_block(a, q),
+                  a.nchunks, a.nblk, lane);
       const double* xin = a.xin[s];
       double* xout = a.xout[s];
       const bool fresh = (s > 0);  // x produced inside this pass: read through L2
-      const unsigned char* base = smem + st * kTmaStageBytes;
-      const double* vec = reinterpret_cast<const double*>(base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes);
-      const int64_t sl = k * kTmaSlices + warp;
-      if (sl < a.n_slices) {
+      const bool sweep = (op == (int)WaveOp::Sweep || op == (int)WaveOp::SweepDot);
+      const int64_t c1 = min(kWaveItem * q + kWaveItem, a.nchunks);
+      for (int64_t k = kWaveItem * q; k < c1; ++k, ++it) {
+        const int st = (int)(it % kTmaStages);
+        const int64_t sl = k * kTmaSlices + warp;
         const uint32_t i = (uint32_t)(sl * 32 + lane);
-        const int rl = warp * 32 + lane;
-        // the row's own x: issued before the gathers (not one more round trip after them)
-        const bool sweep = (op == (int)WaveOp::Sweep || op == (int)WaveOp::SweepDot);
         const uint32_t ic = (int64_t)i < a.n_rows ? i : 0u;
-        const double xi = sweep ? (fresh ? __ldcg(xin + ic) : __ldg(xin + ic)) : 0.0;
-        double sum = 0.0;
-        if (op != (int)WaveOp::Scale) {
-          const int32_t* hs = reinterpret_cast<const int32_t*>(base);
-          const double* vs = reinterpret_cast<const double*>(base + kTmaHdrBytes);
-          const int32_t* cs = reinterpret_cast<const int32_t*>(base + kTmaHdrBytes + kTmaValBytes);
-          const int32_t h = lane < kHdr ? hs[warp * kHdr + lane] : 0;
-          const int32_t h0 = hs[0], h1 = hs[1], h2 = hs[2], h3 = hs[3];
-          const int64_t vbase = ((int64_t)(uint32_t)h1 << 32) | (uint32_t)h0;
-          const int64_t cbase = ((int64_t)(uint32_t)h3 << 32) | (uint32_t)h2;
-          const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
-                             (uint32_t)__shfl_sync(0xffffffffu, h, 0);
-          const int w = __shfl_sync(0xffffffffu, h, 4);
-          const bool dia = __shfl_sync(0xffffffffu, h, 5) == 1;
-          const double* v = vs + (vb - vbase) + lane;
-          double xv[kTmaMaxW];
-          if (dia) {
+        // the row's own x, issued before the gathers
+        const double xi = (sweep && sl < a.n_slices) ? (fresh ? __ldcg(xin + ic) : __ldg(xin + ic)) : 0.0;
+        mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
+        const unsigned char* base = smem + st * kTmaStageBytes;
+        const double* vec = reinterpret_cast<const double*>(base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes);
+        if (sl < a.n_slices) {
+          const int rl = warp * 32 + lane;
+          double sum = 0.0;
+          if (op != (int)WaveOp::Scale) {
+            const int32_t* hs = reinterpret_cast<const int32_t*>(base);
+            const double* vs = reinterpret_cast<const double*>(base + kTmaHdrBytes);
+            const int32_t* cs = reinterpret_cast<const int32_t*>(base + kTmaHdrBytes + kTmaValBytes);
+            const int32_t h = lane < kHdr ? hs[warp * kHdr + lane] : 0;
+            const int32_t h0 = hs[0], h1 = hs[1], h2 = hs[2], h3 = hs[3];
+            const int64_t vbase = ((int64_t)(uint32_t)h1 << 32) | (uint32_t)h0;
+            const int64_t cbase = ((int64_t)(uint32_t)h3 << 32) | (uint32_t)h2;
+            const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
+                               (uint32_t)__shfl_sync(0xffffffffu, h, 0);
+            const int w = __shfl_sync(0xffffffffu, h, 4);
+            const bool dia = __shfl_sync(0xffffffffu, h, 5) == 1;
+            const double* v = vs + (vb - vbase) + lane;
+            double xv[kTmaMaxW];
+            if (dia) {
 #pragma unroll
-            for (int j = 0; j < kTmaMaxW; ++j) {
-              const uint32_t cj = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
-              const double* px = xin + (cj < nc ? cj : 0u);
-              xv[j] = (j < w) ? (fresh ? __ldcg(px) : __ldg(px)) : 0.0;
+              for (int j = 0; j < kTmaMaxW; ++j) {
+                const uint32_t cj = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
+                const double* px = xin + (cj < nc ? cj : 0u);
+                xv[j] = (j < w) ? (fresh ? __ldcg(px) : __ldg(px)) : 0.0;
+              }
+            } else {
+              const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
+                                 (uint32_t)__shfl_sync(0xffffffffu, h, 2);
+              const int32_t* cc = cs + (cb - cbase) + lane;
+#pragma unroll
+              for (int j = 0; j < kTmaMaxW; ++j) {
+                const double* px = xin + (j < w ? cc[32 * j] : 0);
+                xv[j] = (j < w) ? (fresh ? __ldcg(px) : __ldg(px)) : 0.0;
+              }
             }
-          } else {
-            const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
-                               (uint32_t)__shfl_sync(0xffffffffu, h, 2);
-            const int32_t* cc = cs + (cb - cbase) + lane;
 #pragma unroll
-            for (int j = 0; j < kTmaMaxW; ++j) {
-              const double* px = xin + (j < w ? cc[32 * j] : 0);
-              xv[j] = (j < w) ? (fresh ? __ldcg(px) : __ldg(px)) : 0.0;
+            for (int j = 0; j < kTmaMaxW; ++j)
+              if (j < w) sum = fma(v[32 * j], xv[j], sum);
+          }
+          if ((int64_t)i < a.n_rows) {
+            const double bi = vec[rl];
+            if (op == (int)WaveOp::Scale) {
+              xout[i] = vec[kTmaRows + rl] * bi;
+            } else if (op == (int)WaveOp::Resid) {
+              xout[i] = bi - sum;
+            } else {
+              const double xn = xi + vec[kTmaRows + rl] * (bi - sum);
+              xout[i] = xn;
+              if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
             }
           }
-#pragma unroll
-          for (int j = 0; j < kTmaMaxW; ++j)
-            if (j < w) sum = fma(v[32 * j], xv[j], sum);
         }
-        if ((int64_t)i < a.n_rows) {
-          const double bi = vec[rl];
-          if (op == (int)WaveOp::Scale) {
-            xout[i] = vec[kTmaRows + rl] * bi;
-          } else if (op == (int)WaveOp::Resid) {
-            xout[i] = bi - sum;
-          } else {
-            const double xn = xi + vec[kTmaRows + rl] * (bi - sum);
-            xout[i] = xn;
-            if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
-          }
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
       }
-      __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&empty[st]);
-        __threadfence_block();  // this warp's stores before its count (CTA-scope release)
-        atomicAdd(done + (it % kWaveLag), 1u);
+        __threadfence_block();  // this warp's stores of the item before its count (CTA-scope release)
+        atomicAdd(done + (ii % kWaveLag), 1u);
       }
-      ++it;
+      ++ii;
     }
   }
   pdl_exit();
   if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
 }
 
-// Direct-load form of the wavefront pass for slices of any width (e.g. A_1 of
-// the aggregation hierarchy, 20-50 entries per row): no TMA ring, 8 warps per
-// CTA, warp w takes slice 8k + w of each item and streams it with the batched
-// loads of sell_row_sum; same schedule, dependencies and publication.
-constexpr int kWaveDirectThreads = (kTmaSlices + 1) * 32;  // + the publisher warp
+// Direct-load form of the wavefront pass for slices of any width (A_1, A_2):
+// no TMA ring, 8 consumer warps (warp w takes slice 8k + w of every chunk of an
+// item, streamed with the batched loads of sell_row_sum) + a publisher warp.
+constexpr int kWaveDirectThreads = (kTmaSlices + 1) * 32;
 
 __global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveArgs a) {
   pdl_enter();
@@ -1381,61 +1312,62 @@ __global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveAr
   if (threadIdx.x < kWaveLag) done[threadIdx.x] = 0;
   if (threadIdx.x == 0) published_s = 0;
   __syncthreads();
-  const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
+  const int64_t nit = wave_nitems(a);
+  const int64_t total = (int64_t)a.nst * (nit + a.G * (a.nst - 1));
   double acc[1] = {0.0};
   if (warp == kTmaSlices) {
     if (lane == 0) wave_publisher(a, total, done, published);
   } else {
-  int64_t it = 0;
-  for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
-    int s;
-    int64_t k;
-    wave_item(a, m, s, k);
-    if (k < 0 || k >= a.nchunks) continue;
-    if (it >= kWaveLag)
-      while (*published + kWaveLag <= (unsigned int)it) {
-      }
-    const int op = a.op[s];
-    const bool keep = (s + 1 < a.nst);  // a later stage re-reads the slice: normal caching, else stream
-    const int64_t sl = k * kTmaSlices + warp;
-    int32_t h = 0;
-    if (op != (int)WaveOp::Scale && sl < a.n_slices) h = load_hdr(a.hdr, sl, lane);
-    if (s > 0)
-      wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, fronts + warp * kWaveMaxStages + (s - 1), k, a.h, a.nchunks,
-                a.nblk, lane);
-    const double* xin = a.xin[s];
-    double* xout = a.xout[s];
-    if (sl < a.n_slices) {
-      const int64_t i = sl * 32 + lane;
-      // epilogue operands issued before the row sum (they travel with the matrix loads)
-      const int64_t ic = i < a.n_rows ? i : 0;
+    int64_t ii = 0;
+    for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
+      int s;
+      int64_t q;
+      wave_item(a, m, s, q);
+      if (q < 0 || q >= nit) continue;
+      if (ii >= kWaveLag)
+        while (*published + kWaveLag <= (unsigned int)ii) {
+        }
+      const int op = a.op[s];
+      const bool keep = (s + 1 < a.nst);  // a later stage re-reads the slice: normal caching, else stream
+      if (s > 0)
+        wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, fronts + warp * kWaveMaxStages + (s - 1), wave_dep_block(a, q),
+                  a.nchunks, a.nblk, lane);
+      const double* xin = a.xin[s];
+      double* xout = a.xout[s];
       const bool sweep = (op == (int)WaveOp::Sweep || op == (int)WaveOp::SweepDot);
-      const double bi = ldm(a.b + ic, keep);
-      const double di = (op != (int)WaveOp::Resid) ? ldm(a.dinv + ic, keep) : 0.0;
-      const double xi = sweep ? ((s > 0) ? __ldcg(xin + ic) : __ldg(xin + ic)) : 0.0;
-      double sum = 0.0;
-      if (op != (int)WaveOp::Scale)
-        sum = (s > 0) ? sell_row_sum<true>(h, sl, lane, a.col, a.val, xin, a.ncols, keep)
-                      : sell_row_sum<false>(h, sl, lane, a.col, a.val, xin, a.ncols, keep);
-      if (i < a.n_rows) {
-        if (op == (int)WaveOp::Scale) {
-          xout[i] = di * bi;
-        } else if (op == (int)WaveOp::Resid) {
-          xout[i] = bi - sum;
-        } else {
-          const double xn = xi + di * (bi - sum);
-          xout[i] = xn;
-          if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
+      const int64_t c1 = min(kWaveItem * q + kWaveItem, a.nchunks);
+      for (int64_t k = kWaveItem * q; k < c1; ++k) {
+        const int64_t sl = k * kTmaSlices + warp;
+        if (sl >= a.n_slices) continue;
+        const int32_t h = (op != (int)WaveOp::Scale) ? load_hdr(a.hdr, sl, lane) : 0;
+        const int64_t i = sl * 32 + lane;
+        const int64_t ic = i < a.n_rows ? i : 0;
+        const double bi = ldm(a.b + ic, keep);
+        const double di = (op != (int)WaveOp::Resid) ? ldm(a.dinv + ic, keep) : 0.0;
+        const double xi = sweep ? ((s > 0) ? __ldcg(xin + ic) : __ldg(xin + ic)) : 0.0;
+        double sum = 0.0;
+        if (op != (int)WaveOp::Scale)
+          sum = (s > 0) ? sell_row_sum<true>(h, sl, lane, a.col, a.val, xin, a.ncols, keep)
+                        : sell_row_sum<false>(h, sl, lane, a.col, a.val, xin, a.ncols, keep);
+        if (i < a.n_rows) {
+          if (op == (int)WaveOp::Scale) {
+            xout[i] = di * bi;
+          } else if (op == (int)WaveOp::Resid) {
+            xout[i] = bi - sum;
+          } else {
+            const double xn = xi + di * (bi - sum);
+            xout[i] = xn;
+            if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
+          }
         }
       }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();  // this warp's stores before its count (CTA-scope release)
+        atomicAdd(done + (ii % kWaveLag), 1u);
+      }
+      ++ii;
     }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();  // this warp's stores before its count (CTA-scope release)
-      atomicAdd(done + (it % kWaveLag), 1u);
-    }
-    ++it;
-  }
   }
   pdl_exit();
   if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
@@ -1470,8 +1402,11 @@ void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& in, cudaStream_t s
   a.n_slices = A.n_units;
   a.nchunks = wave_chunks(A);
   a.nblk = (a.nchunks + kWaveBlk - 1) / kWaveBlk;
-  PSC_REQUIRE(a.G >= a.h + kWaveBlk, PSC_ERR_STATE, "wave schedule: key skew below the dependency reach");
-  const int64_t total = (int64_t)a.nst * (a.nchunks + a.G * (a.nst - 1));
+  // G (in items) must put every dependency of an item (whole blocks up to chunk
+  // 8q + 7 + h + kWaveBlk - 1 of the previous stage) at a smaller key
+  PSC_REQUIRE(a.G * kWaveItem >= a.h + kWaveBlk + kWaveItem, PSC_ERR_STATE,
+              "wave schedule: key skew below the dependency reach");
+  const int64_t total = (int64_t)a.nst * ((a.nchunks + kWaveItem - 1) / kWaveItem + a.G * (a.nst - 1));
   // every CTA must be resident at once (items wait on other CTAs' items)
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)o * ctx->num_sms));
   // round-robin dealing: a grid that is a multiple of the stage count would pin

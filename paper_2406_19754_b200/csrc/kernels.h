@@ -151,7 +151,7 @@ struct WaveArgs {
   int op[kWaveMaxStages] = {};
   const double* xin[kWaveMaxStages] = {};
   double* xout[kWaveMaxStages] = {};
-  // schedule: dependency reach h (chunks), key skew G
+  // schedule: dependency reach h (chunks), key skew G (in items of kWaveItem = 8 chunks)
   int64_t h = 0, G = 1;
   unsigned int* flags = nullptr;  // per stage: nblk block counters (8 warp arrivals per chunk)
   int64_t nblk = 0;
