@@ -1696,15 +1696,27 @@ static int vec_grid(psc_ctx* ctx, int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * 8));
 }
 
+// Vector kernels: two elements per thread and iteration with 16-byte accesses
+// (library buffers are 256-byte aligned), the odd tail element by thread 0.
+__device__ __forceinline__ double2 ld2(const double* p, int64_t j) { return reinterpret_cast<const double2*>(p)[j]; }
+__device__ __forceinline__ void st2(double* p, int64_t j, double2 v) { reinterpret_cast<double2*>(p)[j] = v; }
+
 __global__ void __launch_bounds__(kBlock) scale_kernel(int64_t n, const double* __restrict__ dinv,
                                                        const double* __restrict__ b, double* __restrict__ x) {
   pdl_enter();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    x[i] = dinv[i] * b[i];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = tid; j < (n >> 1); j += stride) {
+    const double2 d = ld2(dinv, j), bb = ld2(b, j);
+    st2(x, j, make_double2(d.x * bb.x, d.y * bb.y));
+  }
+  if ((n & 1) && tid == 0) x[n - 1] = dinv[n - 1] * b[n - 1];
   pdl_exit();
 }
 
+static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
 void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, double* x, cudaStream_t s) {
+  PSC_REQUIRE(al16(dinv) && al16(b) && al16(x), PSC_ERR_STATE, "vector kernels need 16-byte aligned buffers");
   launch_k(scale_kernel, vec_grid(ctx, n), kBlock, 0, s, n, dinv, b, x);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
@@ -1769,11 +1781,29 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
   pdl_enter();
   const double alpha = gsum(g_num, num_ranks) / gsum(g_pq, nranks);
   double acc[1] = {0.0};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = tid; j < (n >> 1); j += stride) {
+    double2 xv = ld2(x, j), rv = ld2(r, j);
+    const double2 pv = ld2(p, j), qv = ld2(q, j);
+    xv.x = xv.x + alpha * pv.x;
+    xv.y = xv.y + alpha * pv.y;
+    rv.x = rv.x - alpha * qv.x;
+    rv.y = rv.y - alpha * qv.y;
+    st2(x, j, xv);
+    st2(r, j, rv);
+    if (z0) {  // first level-0 sweep of the next V-cycle, from zero
+      const double2 d = ld2(dinv, j);
+      st2(z0, j, make_double2(d.x * rv.x, d.y * rv.y));
+    }
+    acc[0] += rv.x * rv.x;
+    acc[0] += rv.y * rv.y;
+  }
+  if ((n & 1) && tid == 0) {
+    const int64_t i = n - 1;
     x[i] = x[i] + alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
-    if (z0) z0[i] = dinv[i] * ri;  // first level-0 sweep of the next V-cycle, from zero
+    if (z0) z0[i] = dinv[i] * ri;
     acc[0] += ri * ri;
   }
   pdl_exit();
@@ -1783,6 +1813,8 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
 void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
                       const double* g_pq, const double* g_num, int num_ranks, int nranks, const RedSite* red,
                       double* red_out, cudaStream_t s, const double* dinv, double* z0) {
+  PSC_REQUIRE(al16(x) && al16(p) && al16(r) && al16(q) && al16(dinv) && al16(z0), PSC_ERR_STATE,
+              "vector kernels need 16-byte aligned buffers");
   const int g = std::min(vec_grid(ctx, n), red->grid);
   launch_k(cg_update_kernel, g, kBlock, 0, s, n, x, p, r, q, g_pq, g_num, num_ranks, nranks, red->partials,
            red->ticket, red_out, dinv, z0);
@@ -1800,10 +1832,20 @@ __global__ void __launch_bounds__(kBlock) fcg_dir_kernel(int64_t n, const double
   pdl_enter();
   const double beta = gsum(g_zq, nranks) / gsum(g_pq, nranks);
   double acc[1] = {0.0};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double pi = z[i] - beta * p[i];
-    p[i] = pi;
-    acc[0] += pi * r[i];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = tid; j < (n >> 1); j += stride) {
+    const double2 zv = ld2(z, j), rv = ld2(r, j);
+    double2 pv = ld2(p, j);
+    pv.x = zv.x - beta * pv.x;
+    pv.y = zv.y - beta * pv.y;
+    st2(p, j, pv);
+    acc[0] += pv.x * rv.x;
+    acc[0] += pv.y * rv.y;
+  }
+  if ((n & 1) && tid == 0) {
+    const double pi = z[n - 1] - beta * p[n - 1];
+    p[n - 1] = pi;
+    acc[0] += pi * r[n - 1];
   }
   pdl_exit();
   grid_reduce<1>(acc, partials, ticket, out, 1);
@@ -1811,6 +1853,7 @@ __global__ void __launch_bounds__(kBlock) fcg_dir_kernel(int64_t n, const double
 
 void launch_fcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* r, const double* g_zq,
                     const double* g_pq, int nranks, const RedSite* red, double* red_out, cudaStream_t s) {
+  PSC_REQUIRE(al16(z) && al16(p) && al16(r), PSC_ERR_STATE, "vector kernels need 16-byte aligned buffers");
   const int g = std::min(vec_grid(ctx, n), red->grid);
   launch_k(fcg_dir_kernel, g, kBlock, 0, s, n, z, p, r, g_zq, g_pq, nranks, red->partials, red->ticket, red_out);
   PSC_CUDA(cudaGetLastError());
@@ -1922,8 +1965,12 @@ __global__ void __launch_bounds__(kBlock) xpby_kernel(int64_t n, const double* _
   pdl_enter();
   const double rz = gsum(g_rz, nranks);
   const double beta = rz / __ldcg(rz_old);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = z[i] + beta * p[i];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = tid; j < (n >> 1); j += stride) {
+    const double2 zv = ld2(z, j), pv = ld2(p, j);
+    st2(p, j, make_double2(zv.x + beta * pv.x, zv.y + beta * pv.y));
+  }
+  if ((n & 1) && tid == 0) p[n - 1] = z[n - 1] + beta * p[n - 1];
   pdl_exit();
   // rz_old := rz once every CTA has read the old value
   __syncthreads();
@@ -1939,6 +1986,7 @@ __global__ void __launch_bounds__(kBlock) xpby_kernel(int64_t n, const double* _
 
 void launch_xpby(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rz, double* rz_old, int nranks,
                  const RedSite* red, cudaStream_t s) {
+  PSC_REQUIRE(al16(z) && al16(p), PSC_ERR_STATE, "vector kernels need 16-byte aligned buffers");
   launch_k(xpby_kernel, vec_grid(ctx, n), kBlock, 0, s, n, z, p, g_rz, rz_old, nranks, red->ticket);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
