@@ -131,3 +131,17 @@ def test_csr_hierarchy_general_matrix():
     assert h.nlevels >= 2
     for l in range(h.nlevels - 1):
         assert abs(h.levels[l].R.to_scipy() - h.levels[l].P.to_scipy().T).max() == 0
+
+
+def test_csr_arrays_outlive_the_hierarchy_object():
+    """The CSR arrays are views of C memory: they must keep the C hierarchy alive
+    (a temporary hierarchy's matrix once read freed memory)."""
+    import gc
+    A = pscgen.poisson_hierarchy(6, max_levels=2).levels[0].A
+    S = pscgen.poisson_hierarchy(5, max_levels=1).levels[0].A.to_scipy()
+    gc.collect()
+    junk = [np.ones(1 << 16) for _ in range(64)]  # reuse freed memory if it were freed
+    assert A.ptr[0] == 0 and A.nnz == 6 ** 3 * 7 - 6 * 6 * 6
+    assert S.indptr[0] == 0 and S.shape == (125, 125) and S.nnz == 725
+    np.testing.assert_array_equal(S.diagonal(), np.full(125, 6.0))
+    del junk
