@@ -100,6 +100,7 @@ struct psc_hier_s {
   std::vector<cudaEvent_t> ev_dom;  // pairs (start, end)
   int dom_used = 0;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // exchange / interior overlap (run_rows)
   // buffers peers write into (halo-bearing vectors, gathered scalars, coarse
   // gather buffer, P2P flags) live in one arena: one CUDA IPC handle maps them
   char* arena = nullptr;
@@ -164,6 +165,33 @@ void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
   exchange(h, d, const_cast<double*>(a.x), s);
 }
 
+// A row kernel whose input x needs a halo exchange first.  Distributed levels
+// (non-reducing kernels): the exchange runs on the communication stream while the
+// interior chunks (no halo column) run on the main stream; the boundary chunks
+// follow once the exchange has landed — the exchange (~10 us) hides behind the
+// interior work instead of preceding it.  Otherwise: prep() + one launch.
+// PSC_NO_OVERLAP=1 keeps exchange-then-kernel.
+void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cudaStream_t s) {
+  psc_ctx* ctx = h->ctx;
+  static const bool no_overlap = getenv("PSC_NO_OVERLAP") != nullptr || getenv("PSC_DEBUG_SKIP_HALO") != nullptr ||
+                                 getenv("PSC_DEBUG_SKIP_HALO_FROM") != nullptr ||
+                                 getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr || getenv("PSC_FUSED_EXCHANGE") != nullptr;
+  const bool reduces = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
+  if (!no_overlap && ctx->nranks > 1 && d && !reduces && S.n_bchunks > 0 && S.n_ichunks > 0 && S.n_boundary > 0 &&
+      S.n_interior > 0) {
+    PSC_CUDA(cudaEventRecord(h->ev_fork, s));
+    PSC_CUDA(cudaStreamWaitEvent(ctx->comm_stream, h->ev_fork, 0));
+    exchange(h, d, const_cast<double*>(a.x), ctx->comm_stream);
+    PSC_CUDA(cudaEventRecord(h->ev_join, ctx->comm_stream));
+    launch_rows(ctx, S, op, a, s, SliceSet::Interior);
+    PSC_CUDA(cudaStreamWaitEvent(s, h->ev_join, 0));
+    launch_rows(ctx, S, op, a, s, SliceSet::Boundary);
+    return;
+  }
+  prep(h, d, a, s);
+  launch_rows(ctx, S, op, a, s);
+}
+
 // ------------------------------------------------------------ coarsest level
 // `nsweeps` l1-Jacobi sweeps from zero on the last level of a level
 // array.  Returns its iterate.
@@ -191,8 +219,7 @@ double* coarse_sweeps(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cud
     a.b = b;
     a.dinv = W.dinv;
     a.y = W.x[cur ^ 1];
-    prep(h, W.d, a, s);
-    launch_rows(ctx, W.A->S, RowOp::Sweep, a, s);
+    run_rows(h, W.d, W.A->S, RowOp::Sweep, a, s);
     cur ^= 1;
   }
   return W.x[cur];
@@ -276,10 +303,9 @@ int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream
     a.b = b;
     a.dinv = W.dinv;
     a.y = W.x[cur ^ 1];
-    prep(h, W.d, a, s);
     const bool t = timing && h->dom_used + 2 <= (int)h->ev_dom.size();
     if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
-    launch_rows(ctx, W.A->S, RowOp::Sweep, a, s);
+    run_rows(h, W.d, W.A->S, RowOp::Sweep, a, s);
     if (t) {
       PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
       h->dom_used += 2;
@@ -418,8 +444,7 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     a.x = W.x[cur];
     a.b = b;
     a.y = W.r;
-    prep(h, W.d, a, s);
-    launch_rows(ctx, W.A->S, RowOp::Resid, a, s);
+    run_rows(h, W.d, W.A->S, RowOp::Resid, a, s);
   }
   // fused: the next level's first sweep from zero, x_{l+1} = M^{-1} b_{l+1}
   const bool fuse = fuse_first_sweep() && l + 1 < Lend - 1 && h->opt.pre_sweeps > 0 && !next_replicated;
@@ -432,8 +457,7 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
       a.y2 = C.x[0];
       a.dinv2 = C.dinv;
     }
-    prep(h, W.d, a, s);
-    launch_rows(ctx, W.R->S, RowOp::Spmv, a, s);
+    run_rows(h, W.d, W.R->S, RowOp::Spmv, a, s);
   }
   double* xc = vcycle_rec(h, LV, l + 1, C.b, s, timing, fuse, dist);
   {
@@ -441,8 +465,8 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = xc;
     a.y = W.x[cur];
-    if (!next_replicated) prep(h, C.d, a, s);  // the replicated cycle filled xc's halo
-    launch_rows(ctx, W.P->S, RowOp::PAdd, a, s);
+    if (next_replicated) launch_rows(ctx, W.P->S, RowOp::PAdd, a, s);  // the replicated cycle filled xc's halo
+    else run_rows(h, C.d, W.P->S, RowOp::PAdd, a, s);
   }
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
   const int post = h->opt.post_sweeps;
@@ -470,10 +494,9 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
       a.red_out = scal_mine(h, S_RZ);
       a.w = h->rz_weight;
     }
-    prep(h, W.d, a, s);
     const bool t = time_here && h->dom_used + 2 <= (int)h->ev_dom.size();
     if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
-    launch_rows(ctx, W.A->S, last0 ? RowOp::SweepDot : RowOp::Sweep, a, s);
+    run_rows(h, W.d, W.A->S, last0 ? RowOp::SweepDot : RowOp::Sweep, a, s);
     if (t) {
       PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
       h->dom_used += 2;
@@ -754,6 +777,8 @@ void free_hier(psc_hier* h) {
   for (auto e : h->ev_dom) cudaEventDestroy(e);
   if (h->ev_t0) cudaEventDestroy(h->ev_t0);
   if (h->ev_t1) cudaEventDestroy(h->ev_t1);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
 }
 
@@ -974,6 +999,8 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     for (auto& e : h->ev_dom) PSC_CUDA(cudaEventCreate(&e));
     PSC_CUDA(cudaEventCreate(&h->ev_t0));
     PSC_CUDA(cudaEventCreate(&h->ev_t1));
+    PSC_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    PSC_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     // coarsest solver: one CTA when the level is small enough; replicated on
     // every rank when distributed
     LevelWS& Wc = h->lv[nlevels - 1];

@@ -311,6 +311,7 @@ struct RowKArgs {
   const double* val;
   const int32_t* list;  // nullptr: units 0..nlist-1
   int64_t nlist;
+  const int32_t* clist;  // TMA kernels: chunks to process (nullptr: 0..nchunks-1)
   int64_t n_rows;
   double alpha, beta;
   const double* x;
@@ -326,6 +327,11 @@ struct RowKArgs {
   int red_stride;
   FusedExchange ex;
 };
+
+// position ci of a TMA kernel's chunk sequence -> chunk index
+__device__ __forceinline__ int64_t chunk_at(const RowKArgs& a, int64_t ci) {
+  return a.clist ? (int64_t)__ldg(a.clist + ci) : ci;
+}
 
 template <RowOp OP>
 struct NRed {
@@ -709,17 +715,20 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
       const uint64_t pol_mat = a.keep_matrix ? pol_keep : pol_stream;
-      int64_t c = blockIdx.x;
+      int64_t ci = blockIdx.x;
       int64_t vb0 = 0, vb1 = 0, cb0 = 0, cb1 = 0;
-      if (c < nchunks) {
+      if (ci < nchunks) {
+        const int64_t c = chunk_at(a, ci);
         const int64_t s0 = c * kTmaSlices, s1 = min(s0 + kTmaSlices, n_slices);
         vb0 = a.ptr[s0]; vb1 = a.ptr[s1]; cb0 = a.cptr[s0]; cb1 = a.cptr[s1];
       }
-      for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
+      for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
+        const int64_t c = chunk_at(a, ci);
         // prefetch the next chunk's offsets before blocking on the ring
-        const int64_t cn = c + gridDim.x;
+        const int64_t cin = ci + gridDim.x;
         int64_t nvb0 = 0, nvb1 = 0, ncb0 = 0, ncb1 = 0;
-        if (cn < nchunks) {
+        if (cin < nchunks) {
+          const int64_t cn = chunk_at(a, cin);
           const int64_t s0 = cn * kTmaSlices, s1 = min(s0 + kTmaSlices, n_slices);
           nvb0 = a.ptr[s0]; nvb1 = a.ptr[s1]; ncb0 = a.cptr[s0]; ncb1 = a.cptr[s1];
         }
@@ -752,8 +761,9 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
   } else {
     // ---------------- consumers: warp `warp` takes slice s0 + warp of each chunk
     const uint32_t nc = (uint32_t)a.ncols;
-    int64_t c = blockIdx.x;
-    for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
+    int64_t ci = blockIdx.x;
+    for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
+      const int64_t c = chunk_at(a, ci);
       const int st = (int)(it % kTmaStages);
       mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
       const unsigned char* base = smem + st * kTmaStageBytes;
@@ -1466,16 +1476,19 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
       const uint64_t pol_mat = a.keep_matrix ? pol_keep : pol_stream;
-      int64_t c = blockIdx.x;
+      int64_t ci = blockIdx.x;
       int64_t e0 = 0, e1 = 0;
-      if (c < nchunks) {
+      if (ci < nchunks) {
+        const int64_t c = chunk_at(a, ci);
         e0 = a.ptr[c * CR];
         e1 = a.ptr[min((c + 1) * CR, a.n_rows)];
       }
-      for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
-        const int64_t cn = c + gridDim.x;
+      for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
+        const int64_t c = chunk_at(a, ci);
+        const int64_t cin = ci + gridDim.x;
         int64_t ne0 = 0, ne1 = 0;
-        if (cn < nchunks) {
+        if (cin < nchunks) {
+          const int64_t cn = chunk_at(a, cin);
           ne0 = a.ptr[cn * CR];
           ne1 = a.ptr[min((cn + 1) * CR, a.n_rows)];
         }
@@ -1505,8 +1518,9 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
     }
   } else {
     const int sub = lane & (G - 1), grp = lane / G;
-    int64_t c = blockIdx.x;
-    for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
+    int64_t ci = blockIdx.x;
+    for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
+      const int64_t c = chunk_at(a, ci);
       const int st = (int)(it % kRgStages);
       mbar_wait(&full[st], (uint32_t)((it / kRgStages) & 1));
       const unsigned char* base = smem + st * kRgStageBytes;
@@ -1590,16 +1604,21 @@ static bool tmak_ok(const Sell& A, const RowArgs& r, SliceSet set) {
          A.n_units > 0 && A.n_dict == 0;  // reads explicit int32 columns
 }
 
+// interior / boundary subsets run through the TMA kernels as chunk lists
+static bool chunk_set_ok(const Sell& A, SliceSet set) {
+  return set == SliceSet::All || (A.ichunks && A.bchunks && (A.n_ichunks + A.n_bchunks) > 0);
+}
+
 static bool rg_tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
   const int off = env_int("PSC_NO_TMA", 0) || env_int("PSC_NO_RG_TMA", 0);
-  return !off && A.lanes > 1 && A.max_chunk <= kRgCap && set == SliceSet::All && r.vec_padded && A.n_units > 0;
+  return !off && A.lanes > 1 && A.max_chunk <= kRgCap && chunk_set_ok(A, set) && r.vec_padded && A.n_units > 0;
 }
 
 // TMA path: sliced ELL, every slice at most kTmaMaxW wide, all slices, vectors
 // padded (the bulk copies of the last chunk's rows round up to 16 bytes).
 static bool tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
   const int off = env_int("PSC_NO_TMA", 0);
-  return !off && A.lanes == 1 && A.max_width <= kTmaMaxW && set == SliceSet::All && r.vec_padded && A.hdr &&
+  return !off && A.lanes == 1 && A.max_width <= kTmaMaxW && chunk_set_ok(A, set) && r.vec_padded && A.hdr &&
          A.n_units > 0;
 }
 
@@ -1619,6 +1638,10 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.val = A.val;
   a.list = set == SliceSet::All ? nullptr : (set == SliceSet::Interior ? A.interior : A.boundary);
   a.nlist = set_count(A, set);
+  a.clist = set == SliceSet::All ? nullptr : (set == SliceSet::Interior ? A.ichunks : A.bchunks);
+  const int64_t nchunks_set = set == SliceSet::All ? (A.n_units + kTmaSlices - 1) / kTmaSlices
+                                                   : (set == SliceSet::Interior ? A.n_ichunks : A.n_bchunks);
+  if (set != SliceSet::All && (nchunks_set == 0 || a.nlist == 0)) return;  // empty subset (no reductions here)
   a.n_rows = A.n_rows;
   a.alpha = r.alpha;
   a.beta = r.beta;
@@ -1636,7 +1659,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.ex = r.ex;
   const bool needs_red = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
   if (tma_ok(A, r, set)) {
-    const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
+    const int64_t nchunks = nchunks_set;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
     PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
     switch (op) {
@@ -1670,7 +1693,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
     return;
   }
   if (rg_tma_ok(A, r, set)) {
-    const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
+    const int64_t nchunks = nchunks_set;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
     PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
     switch (A.lanes) {
@@ -2855,6 +2878,20 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
   }
   S.n_interior = (int64_t)in.size();
   S.n_boundary = (int64_t)bd.size();
+  {
+    std::vector<char> cb((nu + 7) / 8, 0);
+    for (int32_t u : bd) cb[u / 8] = 1;
+    std::vector<int32_t> ic, bc;
+    for (int64_t c = 0; c < (int64_t)cb.size(); ++c) (cb[c] ? bc : ic).push_back((int32_t)c);
+    S.n_ichunks = (int64_t)ic.size();
+    S.n_bchunks = (int64_t)bc.size();
+    S.ichunks = dalloc<int32_t>(ic.size());
+    S.bchunks = dalloc<int32_t>(bc.size());
+    if (!ic.empty())
+      PSC_CUDA(cudaMemcpyAsync(S.ichunks, ic.data(), sizeof(int32_t) * ic.size(), cudaMemcpyHostToDevice, s));
+    if (!bc.empty())
+      PSC_CUDA(cudaMemcpyAsync(S.bchunks, bc.data(), sizeof(int32_t) * bc.size(), cudaMemcpyHostToDevice, s));
+  }
   S.interior = dalloc<int32_t>(in.size());
   S.boundary = dalloc<int32_t>(bd.size());
   if (!in.empty())
@@ -2872,6 +2909,8 @@ void sell_free(Sell& S) {
   dfree(S.val);
   dfree(S.interior);
   dfree(S.boundary);
+  dfree(S.ichunks);
+  dfree(S.bchunks);
   S = Sell();
 }
 
