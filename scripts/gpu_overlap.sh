@@ -2,6 +2,8 @@
 # exchange/interior overlap on N GPUs: dist parity + A/B
 N=${1:-2}
 mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_vbm.py -q -x -m "gpu and not slow" > gpurun_out/ovl${N}_parity.log 2>&1; echo parity_rc=$?
+tail -1 gpurun_out/ovl${N}_parity.log
 timeout 1500 python -m pytest tests/test_gpu_dist.py -q -x > gpurun_out/ovl${N}_tests.log 2>&1; echo dist_tests_rc=$?
 tail -2 gpurun_out/ovl${N}_tests.log
 for v in ovl noovl ovl2 noovl2; do
