@@ -170,10 +170,12 @@ void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
 // interior chunks (no halo column) run on the main stream; the boundary chunks
 // follow once the exchange has landed — the exchange (~10 us) hides behind the
 // interior work instead of preceding it.  Otherwise: prep() + one launch.
-// PSC_NO_OVERLAP=1 keeps exchange-then-kernel.
+// Opt-in (PSC_OVERLAP=1): measured slower on 2 B200 (6122 vs 6555 Mdof*iters/s at
+// 256^3/GPU): the split adds a launch and a join per kernel (92 -> 120 launches per
+// iteration), which costs more than the ~10 us exchange it hides.
 void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cudaStream_t s) {
   psc_ctx* ctx = h->ctx;
-  static const bool no_overlap = getenv("PSC_NO_OVERLAP") != nullptr || getenv("PSC_DEBUG_SKIP_HALO") != nullptr ||
+  static const bool no_overlap = getenv("PSC_OVERLAP") == nullptr || getenv("PSC_DEBUG_SKIP_HALO") != nullptr ||
                                  getenv("PSC_DEBUG_SKIP_HALO_FROM") != nullptr ||
                                  getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr || getenv("PSC_FUSED_EXCHANGE") != nullptr;
   const bool reduces = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
