@@ -162,6 +162,13 @@ void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
   static const bool twice = getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr;
   if (twice) exchange(h, d, const_cast<double*>(a.x), s);
   if (!nofuse && p2p_fused(ctx, h->p2p, d, a.x, a.ex)) return;
+  // deferred fused exchange (PSC_DEFER_EXCHANGE=1): push in the prologue, wait
+  // before the first boundary chunk of the (interior-first) TMA kernel
+  static const bool defer = getenv("PSC_DEFER_EXCHANGE") != nullptr;
+  if (defer && p2p_fused(ctx, h->p2p, d, a.x, a.ex)) {
+    a.ex.deferred = 1;
+    return;
+  }
   exchange(h, d, const_cast<double*>(a.x), s);
 }
 

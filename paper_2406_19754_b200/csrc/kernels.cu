@@ -312,6 +312,7 @@ struct RowKArgs {
   const int32_t* list;  // nullptr: units 0..nlist-1
   int64_t nlist;
   const int32_t* clist;  // TMA kernels: chunks to process (nullptr: 0..nchunks-1)
+  int64_t n_first;       // deferred fused exchange: list positions < n_first need no halo
   int64_t n_rows;
   double alpha, beta;
   const double* x;
@@ -352,10 +353,29 @@ static __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 
 // Prologue of a row kernel whose input x is halo-exchanged (see FusedExchange).
 // Must be reached by every thread of every CTA before x's halo is read.
-__device__ __forceinline__ void fused_exchange(const FusedExchange& e, const double* __restrict__ x) {
+// Deferred form (e.deferred, TMA kernels with an interior-first chunk order):
+// the prologue only pushes and signals; each consumer warp waits for the
+// neighbours' counters right before its first boundary chunk
+// (fused_exchange_wait), so the exchange overlaps the interior chunks in ONE
+// launch.  tgt[] keeps this exchange's generations for the wait.
+__device__ __forceinline__ void fused_exchange_wait(const FusedExchange& e, const uint64_t* tgt, int lane) {
+  if (lane == 0)
+    for (int q = 0; q < e.R; ++q)
+      if (e.nbr[q])
+        while (ld_acquire_sys(e.myflag + q) < tgt[q]) {
+        }
+  __syncwarp();
+  // interior rows may have pulled the lines holding the first halo slots into the
+  // (non-coherent) L1 before the neighbours wrote them: drop them (CCTL.IVALL)
+  __threadfence();
+}
+
+__device__ __forceinline__ void fused_exchange(const FusedExchange& e, const double* __restrict__ x,
+                                               uint64_t* tgt_out = nullptr) {
   __shared__ uint64_t tgt[kMaxExRanks];
   __shared__ bool last;
   if (threadIdx.x < e.R) tgt[threadIdx.x] = e.gen[e.R + threadIdx.x] + 1;  // this exchange's generation
+  if (tgt_out && threadIdx.x < e.R) tgt_out[threadIdx.x] = tgt[threadIdx.x];
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e.nsend; k += nthr) {
     int p = 0;
@@ -368,6 +388,18 @@ __device__ __forceinline__ void fused_exchange(const FusedExchange& e, const dou
     last = (atomicAdd(e.ticket, 1u) == gridDim.x - 1);
   }
   __syncthreads();
+  if (e.deferred) {  // signal only; the consumer warps wait before their boundary chunks
+    if (threadIdx.x == 0 && last) {
+      __threadfence_system();
+      for (int q = 0; q < e.R; ++q)
+        if (e.nbr[q]) st_release_sys(e.pflag[q], ++e.gen[q]);
+      for (int q = 0; q < e.R; ++q)
+        if (e.nbr[q]) e.gen[e.R + q] = tgt[q];
+      *e.ticket = 0u;
+    }
+    __syncthreads();
+    return;
+  }
   if (threadIdx.x == 0) {
     if (e.mode == 1) {
       // the signalling CTA alone polls the peers, then releases the others on the GPU
@@ -704,8 +736,9 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  __shared__ uint64_t ex_tgt[kMaxExRanks];
 #ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x);
+  if (a.ex.on) fused_exchange(a.ex, a.x, ex_tgt);
 #endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
@@ -762,9 +795,16 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
     // ---------------- consumers: warp `warp` takes slice s0 + warp of each chunk
     const uint32_t nc = (uint32_t)a.ncols;
     int64_t ci = blockIdx.x;
+    bool halo_ready = !(a.ex.on && a.ex.deferred);
     for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
       const int64_t c = chunk_at(a, ci);
       const int st = (int)(it % kTmaStages);
+#ifndef PSC_NO_FUSED_EX_CODE
+      if (!halo_ready && ci >= a.n_first) {  // first boundary chunk: the halo must have landed
+        fused_exchange_wait(a.ex, ex_tgt, lane);
+        halo_ready = true;
+      }
+#endif
       mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
       const unsigned char* base = smem + st * kTmaStageBytes;
       const int32_t* hs = reinterpret_cast<const int32_t*>(base);
@@ -1466,8 +1506,9 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  __shared__ uint64_t ex_tgt[kMaxExRanks];
 #ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x);
+  if (a.ex.on) fused_exchange(a.ex, a.x, ex_tgt);
 #endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
@@ -1519,9 +1560,16 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
   } else {
     const int sub = lane & (G - 1), grp = lane / G;
     int64_t ci = blockIdx.x;
+    bool halo_ready = !(a.ex.on && a.ex.deferred);
     for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
       const int64_t c = chunk_at(a, ci);
       const int st = (int)(it % kRgStages);
+#ifndef PSC_NO_FUSED_EX_CODE
+      if (!halo_ready && ci >= a.n_first) {  // first boundary chunk: the halo must have landed
+        fused_exchange_wait(a.ex, ex_tgt, lane);
+        halo_ready = true;
+      }
+#endif
       mbar_wait(&full[st], (uint32_t)((it / kRgStages) & 1));
       const unsigned char* base = smem + st * kRgStageBytes;
       const double* vs = reinterpret_cast<const double*>(base);
@@ -1639,6 +1687,13 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.list = set == SliceSet::All ? nullptr : (set == SliceSet::Interior ? A.interior : A.boundary);
   a.nlist = set_count(A, set);
   a.clist = set == SliceSet::All ? nullptr : (set == SliceSet::Interior ? A.ichunks : A.bchunks);
+  a.n_first = 0;
+  const bool tma_path = tma_ok(A, r, set) || (!tmak_ok(A, r, set) && rg_tma_ok(A, r, set));
+  const bool defer = r.ex.on && r.ex.deferred && tma_path && set == SliceSet::All && A.ochunks;
+  if (defer) {
+    a.clist = A.ochunks;  // interior chunks first: they run while the halo is in flight
+    a.n_first = A.n_ichunks;
+  }
   const int64_t nchunks_set = set == SliceSet::All ? (A.n_units + kTmaSlices - 1) / kTmaSlices
                                                    : (set == SliceSet::Interior ? A.n_ichunks : A.n_bchunks);
   if (set != SliceSet::All && (nchunks_set == 0 || a.nlist == 0)) return;  // empty subset (no reductions here)
@@ -1657,6 +1712,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.red_out = r.red_out;
   a.red_stride = r.red_stride;
   a.ex = r.ex;
+  if (!defer) a.ex.deferred = 0;  // plain kernels (and subsets) wait in the prologue
   const bool needs_red = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
   if (tma_ok(A, r, set)) {
     const int64_t nchunks = nchunks_set;
@@ -2887,6 +2943,11 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     S.n_bchunks = (int64_t)bc.size();
     S.ichunks = dalloc<int32_t>(ic.size());
     S.bchunks = dalloc<int32_t>(bc.size());
+    std::vector<int32_t> oc(ic);
+    oc.insert(oc.end(), bc.begin(), bc.end());
+    S.ochunks = dalloc<int32_t>(oc.size());
+    if (!oc.empty())
+      PSC_CUDA(cudaMemcpyAsync(S.ochunks, oc.data(), sizeof(int32_t) * oc.size(), cudaMemcpyHostToDevice, s));
     if (!ic.empty())
       PSC_CUDA(cudaMemcpyAsync(S.ichunks, ic.data(), sizeof(int32_t) * ic.size(), cudaMemcpyHostToDevice, s));
     if (!bc.empty())
@@ -2911,6 +2972,7 @@ void sell_free(Sell& S) {
   dfree(S.boundary);
   dfree(S.ichunks);
   dfree(S.bchunks);
+  dfree(S.ochunks);
   S = Sell();
 }
 
