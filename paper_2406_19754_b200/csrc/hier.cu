@@ -78,6 +78,11 @@ struct psc_hier_s {
   std::vector<LevelWS> lv;
   Replica rep;
   bool z0_fused = false;  // CG update writes the first level-0 sweep of the next V-cycle
+  // dense suffix: the V-cycle operator of levels dsuf_l.. of the level array
+  // *dsuf_lv, precomputed as a dense row-major matrix (linear coarse solver only)
+  const std::vector<LevelWS>* dsuf_lv = nullptr;
+  int dsuf_l = -1;
+  double* dsuf = nullptr;
   // CG state (level 0)
   double* x_int = nullptr;  // n0 + nh0
   double* r_cg = nullptr;   // n0
@@ -435,6 +440,10 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   psc_ctx* ctx = h->ctx;
   const int Lend = (int)LV.size();
   if (dist && h->rep.on && l == h->rep.first) return replicated_cycle(h, b, s);
+  if (h->dsuf && &LV == h->dsuf_lv && l == h->dsuf_l) {  // the whole sub-cycle as one dense product
+    launch_dense_gemv(ctx, h->dsuf, LV[l].n, b, LV[l].x[0], s);
+    return LV[l].x[0];
+  }
   if (l == Lend - 1) return coarse_solve(h, LV[l], b, s);
   LevelWS& W = LV[l];
   LevelWS& C = LV[l + 1];
@@ -456,7 +465,8 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     run_rows(h, W.d, W.A->S, RowOp::Resid, a, s);
   }
   // fused: the next level's first sweep from zero, x_{l+1} = M^{-1} b_{l+1}
-  const bool fuse = fuse_first_sweep() && l + 1 < Lend - 1 && h->opt.pre_sweeps > 0 && !next_replicated;
+  const bool next_dense = h->dsuf && &LV == h->dsuf_lv && l + 1 == h->dsuf_l;
+  const bool fuse = fuse_first_sweep() && l + 1 < Lend - 1 && h->opt.pre_sweeps > 0 && !next_replicated && !next_dense;
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -691,6 +701,51 @@ void level_coarse_solver(psc_hier* h, LevelWS& W) {
   }
 }
 
+// Dense suffix operator.  With the l1-Jacobi coarsest solver the V-cycle B_k of
+// levels k.. (Eq. (2) applied recursively) is a fixed linear map;
+// for the first level with at most PSC_DENSE_SUFFIX_ROWS rows (default 3072,
+// 0 disables) it is precomputed column by column — the sub-cycle applied to the
+// unit vectors — and each V-cycle then applies it as one dense product instead
+// of the ~15 latency-bound launches of the deepest levels.  Same operator,
+// different rounding order.  Not with PSC_COARSE_PCG (a nonlinear coarse solve).
+void build_dense_suffix(psc_hier* h) {
+  psc_ctx* ctx = h->ctx;
+  if (h->opt.coarse_solver != PSC_COARSE_SWEEPS) return;
+  const char* e = getenv("PSC_DENSE_SUFFIX_ROWS");
+  const int64_t lim = std::min<int64_t>(e ? atoll(e) : 3072, dense_gemv_max_rows());
+  if (lim <= 0) return;
+  std::vector<LevelWS>* LV = nullptr;
+  int k = -1;
+  if (ctx->nranks == 1) {
+    LV = &h->lv;
+    for (int l = 1; l < h->L && k < 0; ++l)
+      if (h->lv[l].n <= lim) k = l;
+  } else if (h->rep.on) {
+    LV = &h->rep.lv;
+    for (int l = 0; l < (int)h->rep.lv.size() && k < 0; ++l)
+      if (h->rep.lv[l].n <= lim) k = l;
+  }
+  if (k < 0) return;
+  const bool dist = (LV == &h->lv);
+  LevelWS& W = (*LV)[k];
+  const int64_t n = W.n;
+  cudaStream_t s = ctx->stream;
+  double* DT = dvec(n * n);
+  const double one = 1.0;
+  for (int64_t j = 0; j < n; ++j) {
+    PSC_CUDA(cudaMemsetAsync(W.b, 0, sizeof(double) * n, s));
+    PSC_CUDA(cudaMemcpyAsync(W.b + j, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+    const double* xj = vcycle_rec(h, *LV, k, W.b, s, false, false, dist);
+    PSC_CUDA(cudaMemcpyAsync(DT + j * n, xj, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
+  h->dsuf = dvec(n * n);
+  launch_transpose(ctx, DT, n, h->dsuf, s);
+  PSC_CUDA(cudaStreamSynchronize(s));
+  dfree(DT);
+  h->dsuf_lv = LV;
+  h->dsuf_l = k;
+}
+
 void build_replica(psc_hier* h, int first) {
   psc_ctx* ctx = h->ctx;
   const int R = ctx->nranks;
@@ -774,6 +829,7 @@ void free_hier(psc_hier* h) {
   for (auto& W : h->lv) dfree(W.dense);
   dfree(h->r_cg);
   dfree(h->q);
+  dfree(h->dsuf);
   dfree(h->arena);  // x[0], x[1], r of every level, x_int, p, d_scal, coarse gather buffer, flags
   dfree(h->d_bhost);
   dfree(h->d_xhost);
@@ -1033,6 +1089,7 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       level_coarse_solver(h, Wc);
       for (int l = 0; l + 1 < nlevels; ++l) wave_setup(h, h->lv[l]);
     }
+    build_dense_suffix(h);
     if (h->opt.coarse_solver == PSC_COARSE_PCG) {  // buffers of the general coarsest PCG
       LevelWS& C = h->rep.on ? h->rep.lv.back() : Wc;
       if (!C.dense) {

@@ -2513,6 +2513,59 @@ int64_t sell_bandwidth(psc_ctx* ctx, const Sell& A, cudaStream_t s) {
   return (int64_t)hbw;
 }
 
+// -------------------------------------------------- dense suffix operator
+// y = D b for a dense row-major n x n operator (the V-cycle of the deepest
+// levels precomputed as a matrix, hier.cu): one warp per row, b staged in
+// shared memory, four accumulators over column blocks (fixed order), xor tree.
+__global__ void __launch_bounds__(256) dense_gemv_kernel(const double* __restrict__ D, int64_t n,
+                                                         const double* __restrict__ b, double* __restrict__ y) {
+  pdl_enter();
+  extern __shared__ double bs[];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) bs[i] = b[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (row < n) {
+    const double* Dr = D + row * n;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t j = lane;
+    for (; j + 96 < n; j += 128) {
+      s0 = fma(__ldg(Dr + j), bs[j], s0);
+      s1 = fma(__ldg(Dr + j + 32), bs[j + 32], s1);
+      s2 = fma(__ldg(Dr + j + 64), bs[j + 64], s2);
+      s3 = fma(__ldg(Dr + j + 96), bs[j + 96], s3);
+    }
+    for (; j < n; j += 32) s0 = fma(__ldg(Dr + j), bs[j], s0);
+    double sum = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) y[row] = sum;
+  }
+  pdl_exit();
+}
+
+int64_t dense_gemv_max_rows() { return 6144; }  // b in 48 KB of shared memory
+
+void launch_dense_gemv(psc_ctx* ctx, const double* D, int64_t n, const double* b, double* y, cudaStream_t s) {
+  PSC_REQUIRE(n >= 1 && n <= dense_gemv_max_rows(), PSC_ERR_STATE, "dense operator too large");
+  launch_k(dense_gemv_kernel, (unsigned)((n + 7) / 8), 256, (size_t)n * sizeof(double), s, D, n, b, y);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ in, int64_t n, double* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n * n) return;
+  const int64_t i = k / n, j = k - i * n;
+  out[i * n + j] = in[j * n + i];
+}
+
+void launch_transpose(psc_ctx* ctx, const double* in, int64_t n, double* out, cudaStream_t s) {
+  transpose_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(in, n, out);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
 // --------------------------------------------------------- CSR -> sliced ELL
 __device__ __forceinline__ int32_t map_col(int64_t g, int64_t own_begin, int64_t n_own,
                                            const int64_t* __restrict__ halo, int64_t nh, int* err) {

@@ -172,6 +172,11 @@ int64_t sell_bandwidth(psc_ctx* ctx, const Sell& A, cudaStream_t s);  // max |j 
 // flags must hold kWaveMaxStages * ceil(wave_chunks(A) / kWaveBlk) counters; requires G >= h + kWaveBlk
 void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& a, cudaStream_t s);
 
+// y = D b, D dense row-major n x n (n <= dense_gemv_max_rows()); out = in^T (n x n)
+int64_t dense_gemv_max_rows();
+void launch_dense_gemv(psc_ctx* ctx, const double* D, int64_t n, const double* b, double* y, cudaStream_t s);
+void launch_transpose(psc_ctx* ctx, const double* in, int64_t n, double* out, cudaStream_t s);
+
 // CSR (global int64 columns) -> sliced ELL with local int32 columns.
 // lanes: 0 = choose from the mean row length (choose_lanes), else 1 / 4 / 8 / 16 / 32.
 int choose_lanes(int64_t n_rows, int64_t nnz);
