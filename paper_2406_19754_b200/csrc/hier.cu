@@ -703,7 +703,7 @@ void level_coarse_solver(psc_hier* h, LevelWS& W) {
 
 // Dense suffix operator.  With the l1-Jacobi coarsest solver the V-cycle B_k of
 // levels k.. (Eq. (2) applied recursively) is a fixed linear map;
-// for the first level with at most PSC_DENSE_SUFFIX_ROWS rows (default 3072,
+// for the first level with at most PSC_DENSE_SUFFIX_ROWS rows (default 6144,
 // 0 disables) it is precomputed column by column — the sub-cycle applied to the
 // unit vectors — and each V-cycle then applies it as one dense product instead
 // of the ~15 latency-bound launches of the deepest levels.  Same operator,
@@ -712,7 +712,7 @@ void build_dense_suffix(psc_hier* h) {
   psc_ctx* ctx = h->ctx;
   if (h->opt.coarse_solver != PSC_COARSE_SWEEPS) return;
   const char* e = getenv("PSC_DENSE_SUFFIX_ROWS");
-  const int64_t lim = std::min<int64_t>(e ? atoll(e) : 3072, dense_gemv_max_rows());
+  const int64_t lim = std::min<int64_t>(e ? atoll(e) : 6144, dense_gemv_max_rows());
   if (lim <= 0) return;
   std::vector<LevelWS>* LV = nullptr;
   int k = -1;
