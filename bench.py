@@ -328,11 +328,18 @@ def main():
     clocks = ClockSampler() if local == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stats = []
+    # PSC_PROFILE_SOLVE=1: bracket the timed solves for `ncu --profile-from-start off`
+    # (launch lists of the solve without the set-up launches)
+    prof = os.environ.get("PSC_PROFILE_SOLVE") == "1"
+    if prof:
+        torch.cuda.profiler.start()
     e0.record(lib_stream)
     for k in range(args.warmup, nsteps):
         rc, st, hist = H.solve(bs[k], xs[k], tol=args.tol, maxit=args.maxit, method=args.krylov)
         stats.append(st)
     e1.record(lib_stream)
+    if prof:
+        torch.cuda.profiler.stop()
     barrier()
     clk = clocks.stop(list(range(N))) if clocks else None
     t = maxover(e0.elapsed_time(e1) * 1e-3)
