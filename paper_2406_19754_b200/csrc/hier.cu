@@ -167,13 +167,6 @@ void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
   static const bool twice = getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr;
   if (twice) exchange(h, d, const_cast<double*>(a.x), s);
   if (!nofuse && p2p_fused(ctx, h->p2p, d, a.x, a.ex)) return;
-  // deferred fused exchange (PSC_DEFER_EXCHANGE=1): push in the prologue, wait
-  // before the first boundary chunk of the (interior-first) TMA kernel
-  static const bool defer = getenv("PSC_DEFER_EXCHANGE") != nullptr;
-  if (defer && p2p_fused(ctx, h->p2p, d, a.x, a.ex)) {
-    a.ex.deferred = 1;
-    return;
-  }
   exchange(h, d, const_cast<double*>(a.x), s);
 }
 
@@ -191,8 +184,7 @@ void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cud
                                  getenv("PSC_DEBUG_SKIP_HALO_FROM") != nullptr ||
                                  getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr || getenv("PSC_FUSED_EXCHANGE") != nullptr;
   const bool reduces = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
-  if (!no_overlap && ctx->nranks > 1 && d && !reduces && S.n_bchunks > 0 && S.n_ichunks > 0 && S.n_boundary > 0 &&
-      S.n_interior > 0) {
+  if (!no_overlap && ctx->nranks > 1 && d && !reduces && S.n_boundary > 0 && S.n_interior > 0) {
     PSC_CUDA(cudaEventRecord(h->ev_fork, s));
     PSC_CUDA(cudaStreamWaitEvent(ctx->comm_stream, h->ev_fork, 0));
     exchange(h, d, const_cast<double*>(a.x), ctx->comm_stream);

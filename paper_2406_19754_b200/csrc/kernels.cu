@@ -311,8 +311,6 @@ struct RowKArgs {
   const double* val;
   const int32_t* list;  // nullptr: units 0..nlist-1
   int64_t nlist;
-  const int32_t* clist;  // TMA kernels: chunks to process (nullptr: 0..nchunks-1)
-  int64_t n_first;       // deferred fused exchange: list positions < n_first need no halo
   int64_t n_rows;
   double alpha, beta;
   const double* x;
@@ -328,11 +326,6 @@ struct RowKArgs {
   int red_stride;
   FusedExchange ex;
 };
-
-// position ci of a TMA kernel's chunk sequence -> chunk index
-__device__ __forceinline__ int64_t chunk_at(const RowKArgs& a, int64_t ci) {
-  return a.clist ? (int64_t)__ldg(a.clist + ci) : ci;
-}
 
 template <RowOp OP>
 struct NRed {
@@ -353,29 +346,10 @@ static __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 
 // Prologue of a row kernel whose input x is halo-exchanged (see FusedExchange).
 // Must be reached by every thread of every CTA before x's halo is read.
-// Deferred form (e.deferred, TMA kernels with an interior-first chunk order):
-// the prologue only pushes and signals; each consumer warp waits for the
-// neighbours' counters right before its first boundary chunk
-// (fused_exchange_wait), so the exchange overlaps the interior chunks in ONE
-// launch.  tgt[] keeps this exchange's generations for the wait.
-__device__ __forceinline__ void fused_exchange_wait(const FusedExchange& e, const uint64_t* tgt, int lane) {
-  if (lane == 0)
-    for (int q = 0; q < e.R; ++q)
-      if (e.nbr[q])
-        while (ld_acquire_sys(e.myflag + q) < tgt[q]) {
-        }
-  __syncwarp();
-  // interior rows may have pulled the lines holding the first halo slots into the
-  // (non-coherent) L1 before the neighbours wrote them: drop them (CCTL.IVALL)
-  __threadfence();
-}
-
-__device__ __forceinline__ void fused_exchange(const FusedExchange& e, const double* __restrict__ x,
-                                               uint64_t* tgt_out = nullptr) {
+__device__ __forceinline__ void fused_exchange(const FusedExchange& e, const double* __restrict__ x) {
   __shared__ uint64_t tgt[kMaxExRanks];
   __shared__ bool last;
   if (threadIdx.x < e.R) tgt[threadIdx.x] = e.gen[e.R + threadIdx.x] + 1;  // this exchange's generation
-  if (tgt_out && threadIdx.x < e.R) tgt_out[threadIdx.x] = tgt[threadIdx.x];
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e.nsend; k += nthr) {
     int p = 0;
@@ -388,18 +362,6 @@ __device__ __forceinline__ void fused_exchange(const FusedExchange& e, const dou
     last = (atomicAdd(e.ticket, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (e.deferred) {  // signal only; the consumer warps wait before their boundary chunks
-    if (threadIdx.x == 0 && last) {
-      __threadfence_system();
-      for (int q = 0; q < e.R; ++q)
-        if (e.nbr[q]) st_release_sys(e.pflag[q], ++e.gen[q]);
-      for (int q = 0; q < e.R; ++q)
-        if (e.nbr[q]) e.gen[e.R + q] = tgt[q];
-      *e.ticket = 0u;
-    }
-    __syncthreads();
-    return;
-  }
   if (threadIdx.x == 0) {
     if (e.mode == 1) {
       // the signalling CTA alone polls the peers, then releases the others on the GPU
@@ -736,9 +698,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  __shared__ uint64_t ex_tgt[kMaxExRanks];
 #ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x, ex_tgt);
+  if (a.ex.on) fused_exchange(a.ex, a.x);
 #endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
@@ -748,20 +709,17 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
       const uint64_t pol_mat = a.keep_matrix ? pol_keep : pol_stream;
-      int64_t ci = blockIdx.x;
+      int64_t c = blockIdx.x;
       int64_t vb0 = 0, vb1 = 0, cb0 = 0, cb1 = 0;
-      if (ci < nchunks) {
-        const int64_t c = chunk_at(a, ci);
+      if (c < nchunks) {
         const int64_t s0 = c * kTmaSlices, s1 = min(s0 + kTmaSlices, n_slices);
         vb0 = a.ptr[s0]; vb1 = a.ptr[s1]; cb0 = a.cptr[s0]; cb1 = a.cptr[s1];
       }
-      for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
-        const int64_t c = chunk_at(a, ci);
+      for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
         // prefetch the next chunk's offsets before blocking on the ring
-        const int64_t cin = ci + gridDim.x;
+        const int64_t cn = c + gridDim.x;
         int64_t nvb0 = 0, nvb1 = 0, ncb0 = 0, ncb1 = 0;
-        if (cin < nchunks) {
-          const int64_t cn = chunk_at(a, cin);
+        if (cn < nchunks) {
           const int64_t s0 = cn * kTmaSlices, s1 = min(s0 + kTmaSlices, n_slices);
           nvb0 = a.ptr[s0]; nvb1 = a.ptr[s1]; ncb0 = a.cptr[s0]; ncb1 = a.cptr[s1];
         }
@@ -794,17 +752,9 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
   } else {
     // ---------------- consumers: warp `warp` takes slice s0 + warp of each chunk
     const uint32_t nc = (uint32_t)a.ncols;
-    int64_t ci = blockIdx.x;
-    bool halo_ready = !(a.ex.on && a.ex.deferred);
-    for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
-      const int64_t c = chunk_at(a, ci);
+    int64_t c = blockIdx.x;
+    for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
       const int st = (int)(it % kTmaStages);
-#ifndef PSC_NO_FUSED_EX_CODE
-      if (!halo_ready && ci >= a.n_first) {  // first boundary chunk: the halo must have landed
-        fused_exchange_wait(a.ex, ex_tgt, lane);
-        halo_ready = true;
-      }
-#endif
       mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
       const unsigned char* base = smem + st * kTmaStageBytes;
       const int32_t* hs = reinterpret_cast<const int32_t*>(base);
@@ -1506,9 +1456,8 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  __shared__ uint64_t ex_tgt[kMaxExRanks];
 #ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x, ex_tgt);
+  if (a.ex.on) fused_exchange(a.ex, a.x);
 #endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
@@ -1517,19 +1466,16 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
       const uint64_t pol_mat = a.keep_matrix ? pol_keep : pol_stream;
-      int64_t ci = blockIdx.x;
+      int64_t c = blockIdx.x;
       int64_t e0 = 0, e1 = 0;
-      if (ci < nchunks) {
-        const int64_t c = chunk_at(a, ci);
+      if (c < nchunks) {
         e0 = a.ptr[c * CR];
         e1 = a.ptr[min((c + 1) * CR, a.n_rows)];
       }
-      for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
-        const int64_t c = chunk_at(a, ci);
-        const int64_t cin = ci + gridDim.x;
+      for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
+        const int64_t cn = c + gridDim.x;
         int64_t ne0 = 0, ne1 = 0;
-        if (cin < nchunks) {
-          const int64_t cn = chunk_at(a, cin);
+        if (cn < nchunks) {
           ne0 = a.ptr[cn * CR];
           ne1 = a.ptr[min((cn + 1) * CR, a.n_rows)];
         }
@@ -1559,17 +1505,9 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
     }
   } else {
     const int sub = lane & (G - 1), grp = lane / G;
-    int64_t ci = blockIdx.x;
-    bool halo_ready = !(a.ex.on && a.ex.deferred);
-    for (int64_t it = 0; ci < nchunks; ++it, ci += gridDim.x) {
-      const int64_t c = chunk_at(a, ci);
+    int64_t c = blockIdx.x;
+    for (int64_t it = 0; c < nchunks; ++it, c += gridDim.x) {
       const int st = (int)(it % kRgStages);
-#ifndef PSC_NO_FUSED_EX_CODE
-      if (!halo_ready && ci >= a.n_first) {  // first boundary chunk: the halo must have landed
-        fused_exchange_wait(a.ex, ex_tgt, lane);
-        halo_ready = true;
-      }
-#endif
       mbar_wait(&full[st], (uint32_t)((it / kRgStages) & 1));
       const unsigned char* base = smem + st * kRgStageBytes;
       const double* vs = reinterpret_cast<const double*>(base);
@@ -1652,21 +1590,16 @@ static bool tmak_ok(const Sell& A, const RowArgs& r, SliceSet set) {
          A.n_units > 0 && A.n_dict == 0;  // reads explicit int32 columns
 }
 
-// interior / boundary subsets run through the TMA kernels as chunk lists
-static bool chunk_set_ok(const Sell& A, SliceSet set) {
-  return set == SliceSet::All || (A.ichunks && A.bchunks && (A.n_ichunks + A.n_bchunks) > 0);
-}
-
 static bool rg_tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
   const int off = env_int("PSC_NO_TMA", 0) || env_int("PSC_NO_RG_TMA", 0);
-  return !off && A.lanes > 1 && A.max_chunk <= kRgCap && chunk_set_ok(A, set) && r.vec_padded && A.n_units > 0;
+  return !off && A.lanes > 1 && A.max_chunk <= kRgCap && set == SliceSet::All && r.vec_padded && A.n_units > 0;
 }
 
 // TMA path: sliced ELL, every slice at most kTmaMaxW wide, all slices, vectors
 // padded (the bulk copies of the last chunk's rows round up to 16 bytes).
 static bool tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
   const int off = env_int("PSC_NO_TMA", 0);
-  return !off && A.lanes == 1 && A.max_width <= kTmaMaxW && chunk_set_ok(A, set) && r.vec_padded && A.hdr &&
+  return !off && A.lanes == 1 && A.max_width <= kTmaMaxW && set == SliceSet::All && r.vec_padded && A.hdr &&
          A.n_units > 0;
 }
 
@@ -1686,17 +1619,6 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.val = A.val;
   a.list = set == SliceSet::All ? nullptr : (set == SliceSet::Interior ? A.interior : A.boundary);
   a.nlist = set_count(A, set);
-  a.clist = set == SliceSet::All ? nullptr : (set == SliceSet::Interior ? A.ichunks : A.bchunks);
-  a.n_first = 0;
-  const bool tma_path = tma_ok(A, r, set) || (!tmak_ok(A, r, set) && rg_tma_ok(A, r, set));
-  const bool defer = r.ex.on && r.ex.deferred && tma_path && set == SliceSet::All && A.ochunks;
-  if (defer) {
-    a.clist = A.ochunks;  // interior chunks first: they run while the halo is in flight
-    a.n_first = A.n_ichunks;
-  }
-  const int64_t nchunks_set = set == SliceSet::All ? (A.n_units + kTmaSlices - 1) / kTmaSlices
-                                                   : (set == SliceSet::Interior ? A.n_ichunks : A.n_bchunks);
-  if (set != SliceSet::All && (nchunks_set == 0 || a.nlist == 0)) return;  // empty subset (no reductions here)
   a.n_rows = A.n_rows;
   a.alpha = r.alpha;
   a.beta = r.beta;
@@ -1712,10 +1634,9 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.red_out = r.red_out;
   a.red_stride = r.red_stride;
   a.ex = r.ex;
-  if (!defer) a.ex.deferred = 0;  // plain kernels (and subsets) wait in the prologue
   const bool needs_red = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
   if (tma_ok(A, r, set)) {
-    const int64_t nchunks = nchunks_set;
+    const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
     PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
     switch (op) {
@@ -1749,7 +1670,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
     return;
   }
   if (rg_tma_ok(A, r, set)) {
-    const int64_t nchunks = nchunks_set;
+    const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
     PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
     switch (A.lanes) {
@@ -2987,25 +2908,6 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
   }
   S.n_interior = (int64_t)in.size();
   S.n_boundary = (int64_t)bd.size();
-  {
-    std::vector<char> cb((nu + 7) / 8, 0);
-    for (int32_t u : bd) cb[u / 8] = 1;
-    std::vector<int32_t> ic, bc;
-    for (int64_t c = 0; c < (int64_t)cb.size(); ++c) (cb[c] ? bc : ic).push_back((int32_t)c);
-    S.n_ichunks = (int64_t)ic.size();
-    S.n_bchunks = (int64_t)bc.size();
-    S.ichunks = dalloc<int32_t>(ic.size());
-    S.bchunks = dalloc<int32_t>(bc.size());
-    std::vector<int32_t> oc(ic);
-    oc.insert(oc.end(), bc.begin(), bc.end());
-    S.ochunks = dalloc<int32_t>(oc.size());
-    if (!oc.empty())
-      PSC_CUDA(cudaMemcpyAsync(S.ochunks, oc.data(), sizeof(int32_t) * oc.size(), cudaMemcpyHostToDevice, s));
-    if (!ic.empty())
-      PSC_CUDA(cudaMemcpyAsync(S.ichunks, ic.data(), sizeof(int32_t) * ic.size(), cudaMemcpyHostToDevice, s));
-    if (!bc.empty())
-      PSC_CUDA(cudaMemcpyAsync(S.bchunks, bc.data(), sizeof(int32_t) * bc.size(), cudaMemcpyHostToDevice, s));
-  }
   S.interior = dalloc<int32_t>(in.size());
   S.boundary = dalloc<int32_t>(bd.size());
   if (!in.empty())
@@ -3023,9 +2925,6 @@ void sell_free(Sell& S) {
   dfree(S.val);
   dfree(S.interior);
   dfree(S.boundary);
-  dfree(S.ichunks);
-  dfree(S.bchunks);
-  dfree(S.ochunks);
   S = Sell();
 }
 

@@ -42,9 +42,6 @@ struct FusedExchange {
   // publishes the exchange's generation in `go` (GPU scope) for the other CTAs
   int mode = 1;
   uint64_t* go = nullptr;
-  // 1: push + signal in the prologue, wait right before the first boundary chunk
-  // (TMA kernels, interior-first chunk order); launch_rows falls back to 0 elsewhere
-  int deferred = 0;
 };
 
 struct RowArgs {

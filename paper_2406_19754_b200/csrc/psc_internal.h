@@ -96,12 +96,6 @@ struct Sell {
   int32_t* interior = nullptr;
   int32_t* boundary = nullptr;
   int64_t n_interior = 0, n_boundary = 0;
-  // the same split in chunks of 8 units (the TMA kernels' work unit): a chunk is
-  // boundary if any of its units is
-  int32_t* ichunks = nullptr;
-  int32_t* bchunks = nullptr;
-  int64_t n_ichunks = 0, n_bchunks = 0;
-  int32_t* ochunks = nullptr;  // interior chunks, then boundary chunks (deferred fused exchange)
   int max_width = 0;  // longest (padded) row
   int64_t max_chunk = 0;  // row groups: most entries in one chunk of 8 units (TMA ring capacity check)
   int rows_per_unit() const { return lanes == 1 ? 32 : 32 / lanes; }

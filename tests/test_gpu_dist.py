@@ -44,8 +44,7 @@ def test_four_gpu_parity():
 
 
 @pytest.mark.parametrize("env", [{"PSC_REPL_ROWS": "0"}, {"PSC_REPL_ROWS": "100000000"}, {"PSC_FUSED_EXCHANGE": "1"},
-                                 {"PSC_NO_P2P": "1"}, {"PSC_OVERLAP": "1"}, {"PSC_OVERLAP": "1", "PSC_NO_P2P": "1"},
-                                 {"PSC_DEFER_EXCHANGE": "1"}],
+                                 {"PSC_NO_P2P": "1"}, {"PSC_OVERLAP": "1"}, {"PSC_OVERLAP": "1", "PSC_NO_P2P": "1"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_two_gpu_exchange_and_replication_variants(env):
     """Replicated suffix from the coarsest level only / from level 1; fused and
