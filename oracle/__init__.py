@@ -43,7 +43,7 @@ class _Hier(ctypes.Structure):
     _fields_ = [("nlevels", ctypes.c_int), ("A", ctypes.POINTER(_CSR)), ("P", ctypes.POINTER(_CSR)),
                 ("R", ctypes.POINTER(_CSR)), ("pre", ctypes.c_int), ("post", ctypes.c_int),
                 ("coarse", ctypes.c_int), ("coarse_pcg", ctypes.c_int), ("coarse_maxit", ctypes.c_int),
-                ("coarse_tol", ctypes.c_double)]
+                ("coarse_tol", ctypes.c_double), ("variable_v", ctypes.c_int)]
 
 
 def lib():
@@ -88,7 +88,8 @@ class _CsrHolder:
 
 
 class _HierHolder:
-    def __init__(self, hier, pre=4, post=4, coarse=30, coarse_pcg=False, coarse_maxit=40, coarse_tol=1e-10):
+    def __init__(self, hier, pre=4, post=4, coarse=30, coarse_pcg=False, coarse_maxit=40, coarse_tol=1e-10,
+                 variable_v=False):
         L = hier.nlevels
         self.A = [_CsrHolder(hier.levels[l].A) for l in range(L)]
         self.P = [_CsrHolder(hier.levels[l].P) for l in range(L - 1)]
@@ -97,7 +98,7 @@ class _HierHolder:
         self.Pa = (_CSR * max(L - 1, 1))(*[h.c for h in self.P])
         self.Ra = (_CSR * max(L - 1, 1))(*[h.c for h in self.R])
         self.c = _Hier(L, self.Aa, self.Pa, self.Ra, pre, post, coarse, 1 if coarse_pcg else 0, coarse_maxit,
-                       coarse_tol)
+                       coarse_tol, 1 if variable_v else 0)
 
 
 def spmv(A, x) -> np.ndarray:
@@ -137,7 +138,8 @@ def l1_sweeps_from_zero(A, b, nsweeps: int) -> np.ndarray:
 
 
 def vcycle(hier, r, pre=4, post=4, coarse=30, **coarse_kw) -> np.ndarray:
-    """z = B_0 r, Eq. (2).  coarse_kw: coarse_pcg, coarse_maxit, coarse_tol."""
+    """z = B_0 r, Eq. (2).  coarse_kw: coarse_pcg, coarse_maxit, coarse_tol,
+    variable_v (pre/post sweeps doubled per level, P:330 footnote)."""
     hh = _HierHolder(hier, pre, post, coarse, **coarse_kw)
     r = _arr(r, np.float64)
     z = np.empty_like(r)

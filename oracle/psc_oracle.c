@@ -35,6 +35,7 @@ typedef struct {
   int coarse_pcg;   /* 1: coarsest solver = PCG with l1-Jacobi preconditioner (VBM) */
   int coarse_maxit; /* its iteration cap ("at most 40 iterations") */
   double coarse_tol;/* its relative-residual tolerance (reading R23) */
+  int variable_v;   /* 1: variable V-cycle, pre/post sweeps doubled per level (P:330 footnote, R25) */
 } or_hier;
 
 /* y = A x.  Row sums in stored column order. */
@@ -146,7 +147,12 @@ static void vcycle_level(const or_hier* h, double* const* m, int l, const double
     free(w);
     return;
   }
-  or_l1_sweeps_from_zero(A, m[l], b, h->pre, x, w);
+  /* variable V-cycle (VMATCH, P:330 footnote): "2 smoother iteration at the
+   * first level, and doubled at each following level" -> pre/post sweeps at
+   * level l = pre/post * 2^l (reading R25: both pre and post double) */
+  const int pre = h->variable_v ? h->pre << l : h->pre;
+  const int post = h->variable_v ? h->post << l : h->post;
+  or_l1_sweeps_from_zero(A, m[l], b, pre, x, w);
   /* coarse-grid correction */
   const or_csr* R = &h->R[l];
   const or_csr* P = &h->P[l];
@@ -163,7 +169,7 @@ static void vcycle_level(const or_hier* h, double* const* m, int l, const double
   free(r);
   free(bc);
   free(xc);
-  for (int s = 0; s < h->post; ++s) {
+  for (int s = 0; s < post; ++s) {
     or_l1_sweep(A, m[l], b, x, w);
     memcpy(x, w, sizeof(double) * (size_t)n);
   }

@@ -10,7 +10,9 @@ sign or index, transposed operand) fails at least one test here:
   or_l1_sweep(s)     -> fixed point, closed form (I - G^k) A^-1 b, A-norm decrease,
                         rho(I - M^-1 A) < 1 ("A_l-convergent")
   or_vcycle          -> dense Eq. (2) composition on 2- and 3-level
-                        hierarchies, symmetry, SPD, ||I - BA||_A < 1, linearity
+                        hierarchies, symmetry, SPD, ||I - BA||_A < 1, linearity;
+                        variable V-cycle (P:330 footnote) vs dense Eq. (2) with
+                        G_l^(pre 2^l), 2-level special case, symmetry/SPD
   or_pcg             -> Cholesky / DST exact solve, scipy's CG with the same B,
                         A = I, diag(1..10), b = 0, A-norm error monotone,
                         true vs recurrence residual, paper Fig. 2 loose pin
@@ -134,9 +136,10 @@ def test_l1_jacobi_is_A_convergent(seed):
 
 
 # ---------------------------------------------------------------- or_vcycle
-def _dense_B(hier, pre, post, coarse):
+def _dense_B(hier, pre, post, coarse, variable_v=False):
     """B_0 from the error-propagation form of Eq. (2), built with dense
-    matrices, recursively; B_ell = (I - G^coarse) A^-1 at the coarsest level."""
+    matrices, recursively; B_ell = (I - G^coarse) A^-1 at the coarsest level.
+    variable_v: level l smooths pre*2^l / post*2^l times (P:330 footnote, R25)."""
     L = hier.nlevels
 
     def Bl(l):
@@ -147,16 +150,17 @@ def _dense_B(hier, pre, post, coarse):
             return (np.eye(n) - np.linalg.matrix_power(G, coarse)) @ np.linalg.inv(A)
         P = hier.levels[l].P.to_scipy().toarray()
         R = hier.levels[l].R.to_scipy().toarray()
-        E = (np.linalg.matrix_power(G, post) @ (np.eye(n) - P @ Bl(l + 1) @ R @ A)
-             @ np.linalg.matrix_power(G, pre))
+        k = 2 ** l if variable_v else 1
+        E = (np.linalg.matrix_power(G, post * k) @ (np.eye(n) - P @ Bl(l + 1) @ R @ A)
+             @ np.linalg.matrix_power(G, pre * k))
         return (np.eye(n) - E) @ np.linalg.inv(A)
 
     return Bl(0)
 
 
-def _oracle_B(hier, pre, post, coarse):
+def _oracle_B(hier, pre, post, coarse, **kw):
     n = hier.levels[0].n
-    return np.column_stack([oracle.vcycle(hier, e, pre, post, coarse) for e in np.eye(n)])
+    return np.column_stack([oracle.vcycle(hier, e, pre, post, coarse, **kw) for e in np.eye(n)])
 
 
 @pytest.mark.parametrize("grid,procs,maxl,opts", [
@@ -194,6 +198,44 @@ def test_vcycle_unequal_sweeps_not_symmetric():
     h = pscgen.poisson_hierarchy(6, max_levels=2)
     B = _oracle_B(h, 1, 3, 30)
     assert np.linalg.norm(B - B.T) / np.linalg.norm(B) > 1e-6
+
+
+@pytest.mark.parametrize("grid,procs,maxl,opts", [
+    (6, (1, 1, 1), 3, (2, 2, 30)),
+    (8, (2, 1, 1), 4, (1, 2, 7)),
+])
+def test_variable_vcycle_equals_dense_eq2(grid, procs, maxl, opts):
+    """Variable V-cycle (P:330 footnote, R25): sweeps pre*2^l / post*2^l at level l,
+    against the dense Eq. (2) composition with those powers of G_l."""
+    h = pscgen.poisson_hierarchy(grid, grid, grid, procs, max_levels=maxl, coarse_target=1)
+    assert h.nlevels == maxl
+    Bo = _oracle_B(h, *opts, variable_v=True)
+    Bd = _dense_B(h, *opts, variable_v=True)
+    np.testing.assert_allclose(Bo, Bd, rtol=0, atol=1e-11 * np.abs(Bd).max())
+    # and it is a different operator from the plain V-cycle (level 1 smooths twice as often)
+    assert np.abs(Bo - _oracle_B(h, *opts)).max() > 1e-6 * np.abs(Bd).max()
+
+
+def test_variable_vcycle_two_levels_is_plain_vcycle():
+    """Special case: with two levels only level 0 smooths, and 2^0 = 1, so the variable
+    V-cycle is the plain V-cycle bit for bit."""
+    h = pscgen.poisson_hierarchy(6, max_levels=2)
+    r = np.random.default_rng(3).standard_normal(h.levels[0].n)
+    assert np.array_equal(oracle.vcycle(h, r, 2, 2, 30, variable_v=True), oracle.vcycle(h, r, 2, 2, 30))
+
+
+def test_variable_vcycle_symmetric_spd():
+    """Equal pre/post counts stay equal at every level under doubling, so B stays
+    symmetric and SPD (PCG-admissible) and ||I - BA||_A < 1."""
+    h = pscgen.poisson_hierarchy(8, problem="jump", cube=2, coarse_target=10)
+    assert h.nlevels >= 3
+    B = _oracle_B(h, 2, 2, 30, variable_v=True)
+    assert np.linalg.norm(B - B.T) / np.linalg.norm(B) < 1e-13
+    assert np.linalg.eigvalsh(0.5 * (B + B.T)).min() > 0
+    A = h.levels[0].A.to_scipy().toarray()
+    Lc = np.linalg.cholesky(A)
+    E = Lc.T @ (np.eye(A.shape[0]) - B @ A) @ np.linalg.inv(Lc.T)
+    assert np.linalg.norm(E, 2) < 1.0
 
 
 def test_vcycle_linear():
