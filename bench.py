@@ -198,14 +198,21 @@ def _oracle_solve(args):
     return oracle.fcg if args.krylov == "fcg" else oracle.pcg
 
 
+def _cycle_kw(args):
+    """Variable V-cycle (--variable-v, P:330 footnote): 2 sweeps at level 0, doubled per level."""
+    return dict(pre=2, post=2, variable_v=True) if args.variable_v else {}
+
+
 def _oracle_kw(args):
-    return dict(coarse_pcg=True, coarse_maxit=40, coarse_tol=1e-10) if args.coarse_solver == "pcg" else {}
+    kw = dict(coarse_pcg=True, coarse_maxit=40, coarse_tol=1e-10) if args.coarse_solver == "pcg" else {}
+    return {**kw, **_cycle_kw(args)}
 
 
 def _solver_desc(args):
     coarse = ("coarsest PCG(<=40, 1e-10) with l1-Jacobi" if args.coarse_solver == "pcg"
               else "30 coarsest l1-Jacobi sweeps")
-    return f"{args.krylov.upper()}, V(4,4) l1-Jacobi, {coarse}"
+    cyc = "variable V(2*2^l,2*2^l)" if args.variable_v else "V(4,4)"
+    return f"{args.krylov.upper()}, {cyc} l1-Jacobi, {coarse}"
 
 
 # ------------------------------------------------------------------- main
@@ -238,6 +245,8 @@ def main():
     ap.add_argument("--krylov", default="pcg", choices=["pcg", "fcg"])
     ap.add_argument("--coarse-solver", default="sweeps", choices=["sweeps", "pcg"])
     ap.add_argument("--vbm", action="store_true", help="the paper's VBM solve: --krylov fcg --coarse-solver pcg")
+    ap.add_argument("--variable-v", action="store_true",
+                    help="variable V-cycle (P:330 footnote): 2 sweeps at level 0, doubled per level")
     args = ap.parse_args()
     if args.vbm:
         args.krylov, args.coarse_solver = "fcg", "pcg"
@@ -297,7 +306,7 @@ def main():
         uid = obj[0]
     ctx = psc.Context(rank=rank, nranks=N, device=local, unique_id=uid)
     t1 = time.perf_counter()
-    H, descs, A, P, R = psc.build_hierarchy(ctx, levels, coarse_solver=args.coarse_solver)
+    H, descs, A, P, R = psc.build_hierarchy(ctx, levels, coarse_solver=args.coarse_solver, **_cycle_kw(args))
     t_build = time.perf_counter() - t1
     info = H.info()
     n_loc = info["n_owned"][0]

@@ -168,7 +168,11 @@ enum {
 /* Smoothing sweeps before / after the coarse correction and the coarsest-level
  * solver (defaults 4 / 4 / 30 sweeps: Fig. 5 caption).  Zero-
  * initialise the struct: coarse_solver 0 = sweeps; coarse_maxit 0 -> 40 and
- * coarse_tol 0 -> 1e-10 (defaults of PSC_COARSE_PCG, reading R23). */
+ * coarse_tol 0 -> 1e-10 (defaults of PSC_COARSE_PCG, reading R23).
+ * variable_v 1 = variable V-cycle (VMATCH, P:330 footnote: "2 smoother iteration
+ * at the first level, and doubled at each following level"): level l < L-1 runs
+ * pre_sweeps*2^l / post_sweeps*2^l sweeps (reading R25); the coarsest solver is
+ * unchanged.  PSC_ERR_ARG when a level would need more than 2^20 sweeps. */
 typedef struct {
   int pre_sweeps;
   int post_sweeps;
@@ -176,6 +180,7 @@ typedef struct {
   int coarse_solver;  /* PSC_COARSE_SWEEPS or PSC_COARSE_PCG */
   int coarse_maxit;
   double coarse_tol;
+  int variable_v;     /* 0 = V-cycle, 1 = variable V-cycle (P:330 footnote) */
 } psc_cycle_opts;
 
 /* [collective] AMG hierarchy handle over given level matrices (D10/D11 in

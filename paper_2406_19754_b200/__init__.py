@@ -40,7 +40,7 @@ _KRYLOV = {"pcg": PSC_KRYLOV_PCG, "fcg": PSC_KRYLOV_FCG}
 
 class CycleOpts(ctypes.Structure):
     _fields_ = [("pre_sweeps", _i32), ("post_sweeps", _i32), ("coarse_sweeps", _i32), ("coarse_solver", _i32),
-                ("coarse_maxit", _i32), ("coarse_tol", _f64)]
+                ("coarse_maxit", _i32), ("coarse_tol", _f64), ("variable_v", _i32)]
 
 
 class Stats(ctypes.Structure):
@@ -269,17 +269,19 @@ class Hierarchy:
     """psc_hier_create over given level matrices A[l], P[l], R[l]; V-cycle + PCG / FCG.
 
     coarse_solver: "sweeps" (`coarse` l1-Jacobi sweeps) or "pcg" (PCG with
-    l1-Jacobi, at most coarse_maxit iterations to coarse_tol)."""
+    l1-Jacobi, at most coarse_maxit iterations to coarse_tol).
+    variable_v: variable V-cycle, pre/post sweeps doubled per level (P:330 footnote)."""
 
     def __init__(self, ctx: Context, A, P, R, pre=4, post=4, coarse=30, coarse_solver="sweeps", coarse_maxit=40,
-                 coarse_tol=1e-10):
+                 coarse_tol=1e-10, variable_v=False):
         L = len(A)
         Aa = (_vp * L)(*[m.handle for m in A])
         Pa = (_vp * max(L - 1, 1))(*[m.handle for m in P])
         Ra = (_vp * max(L - 1, 1))(*[m.handle for m in R])
         if coarse_solver not in _COARSE:
             raise ValueError(f"coarse_solver must be one of {sorted(_COARSE)}")
-        opts = CycleOpts(pre, post, coarse, _COARSE[coarse_solver], int(coarse_maxit), float(coarse_tol))
+        opts = CycleOpts(pre, post, coarse, _COARSE[coarse_solver], int(coarse_maxit), float(coarse_tol),
+                         1 if variable_v else 0)
         h = _vp()
         _check(_lib.psc_hier_create(ctx.handle, L, Aa, Pa, Ra, ctypes.byref(opts), ctypes.byref(h)), ctx)
         self.ctx, self.handle, self.nlevels = ctx, h.value, L

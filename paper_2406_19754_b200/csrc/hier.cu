@@ -74,7 +74,7 @@ struct Replica {
 struct psc_hier_s {
   psc_ctx* ctx = nullptr;
   int L = 0;
-  psc_cycle_opts opt{4, 4, 30, PSC_COARSE_SWEEPS, 40, 1e-10};
+  psc_cycle_opts opt{4, 4, 30, PSC_COARSE_SWEEPS, 40, 1e-10, 0};
   std::vector<LevelWS> lv;
   Replica rep;
   bool z0_fused = false;  // CG update writes the first level-0 sweep of the next V-cycle
@@ -404,6 +404,10 @@ int wave_post(psc_hier* h, LevelWS& W, const double* b, int post, int cur, doubl
 
 bool wave_fits(const LevelWS& W, int nst) { return W.wave_h >= 0 && nst >= 1 && nst <= kWaveMaxStages; }
 
+// Smoothing sweeps at hierarchy level `glev`: the base count, doubled per level
+// for the variable V-cycle (P:330 footnote, reading R25).
+int level_sweeps(const psc_hier* h, int base, int glev) { return h->opt.variable_v ? base << glev : base; }
+
 double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b, cudaStream_t s, bool timing,
                    bool first_done, bool dist);
 
@@ -443,7 +447,9 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   const bool next_replicated = dist && h->rep.on && l + 1 == h->rep.first;
   // (I - M^-1 A)^pre, then the coarse-grid correction (I - P B_{l+1} P^T A):
   // r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
-  const int pre = h->opt.pre_sweeps;
+  // hierarchy level of LV[l] (the replicated suffix starts at level rep.first)
+  const int glev = l + (&LV == &h->rep.lv ? h->rep.first : 0);
+  const int pre = level_sweeps(h, h->opt.pre_sweeps, glev);
   int cur;
   if (pre > 0 && wave_fits(W, pre + (first_done ? 0 : 1))) {
     cur = wave_pre(h, W, b, pre, first_done, s);  // sweeps + residual in one pass
@@ -480,7 +486,7 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     else run_rows(h, C.d, W.P->S, RowOp::PAdd, a, s);
   }
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
-  const int post = h->opt.post_sweeps;
+  const int post = level_sweeps(h, h->opt.post_sweeps, glev);
   const bool level0 = dist && l == 0;
   if (post > 0 && wave_fits(W, post)) {
     const bool t = time_here && h->dom_used + 2 <= (int)h->ev_dom.size();
@@ -976,6 +982,10 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
                 "unknown coarse_solver");
     PSC_REQUIRE(h->opt.coarse_maxit >= 0 && h->opt.coarse_tol >= 0.0 && std::isfinite(h->opt.coarse_tol), PSC_ERR_ARG,
                 "coarse_maxit / coarse_tol must be non-negative");
+    PSC_REQUIRE(h->opt.variable_v == 0 || h->opt.variable_v == 1, PSC_ERR_ARG, "variable_v must be 0 or 1");
+    PSC_REQUIRE(!h->opt.variable_v || nlevels < 2 ||
+                    (nlevels - 2 <= 20 && ((int64_t)std::max(h->opt.pre_sweeps, h->opt.post_sweeps) << (nlevels - 2)) <= (1 << 20)),
+                PSC_ERR_ARG, "variable V-cycle: more than 2^20 sweeps at a level");
     if (h->opt.coarse_maxit == 0) h->opt.coarse_maxit = 40;
     if (h->opt.coarse_tol == 0.0) h->opt.coarse_tol = 1e-10;  // reading R23
     h->lv.resize(nlevels);

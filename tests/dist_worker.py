@@ -79,6 +79,14 @@ def main():
     parts2 = [None] * world
     dist.all_gather_object(parts2, (z2.cpu().numpy(), x2.cpu().numpy(), rc2, st2["iters"], hist2))
     H2.close()
+    # the variable V-cycle (P:330 footnote): 2 sweeps at level 0, doubled per level,
+    # through the distributed levels and the replicated suffix alike
+    H3 = psc.Hierarchy(ctx, A, P, R, pre=2, post=2, variable_v=True)
+    z3 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+    H3.vcycle(torch.from_numpy(b[r0:r1].copy()).cuda(), z3)
+    parts3 = [None] * world
+    dist.all_gather_object(parts3, z3.cpu().numpy())
+    H3.close()
     ok = True
     if rank == 0:
         import oracle
@@ -121,6 +129,10 @@ def main():
         ok &= (out["vbm_vcycle_rel"] <= 1e-9 and len(its2) == 1 and abs(parts2[0][3] - ito2) <= 1
                and all(p[2] == 0 for p in parts2) and out["vbm_hist_rel"] <= 1e-9 and out["vbm_x_rel"] <= 1e-7
                and all(np.array_equal(parts2[0][4], p[4]) for p in parts2))
+        zg3 = np.concatenate(parts3)
+        zo3 = oracle.vcycle(h, b, 2, 2, 30, variable_v=True)
+        out["varv_vcycle_rel"] = float(np.linalg.norm(zg3 - zo3) / np.linalg.norm(zo3))
+        ok &= out["varv_vcycle_rel"] <= 1e-12
         out["ok"] = bool(ok)
         print(json.dumps(out), flush=True)
     flag = [ok]
