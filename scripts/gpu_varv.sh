@@ -4,3 +4,5 @@ timeout 900 python -m pytest tests/test_gpu_variable_v.py -q -x > gpurun_out/var
 tail -2 gpurun_out/varv_tests.log
 timeout 900 python bench.py --variable-v --no-cpu-baseline > gpurun_out/varv_bench.json 2> gpurun_out/varv_bench.err; echo varv_bench_rc=$?
 tail -c 600 gpurun_out/varv_bench.json
+timeout 900 python bench.py --variable-v --vbm --no-cpu-baseline > gpurun_out/varv_vbm_bench.json 2> gpurun_out/varv_vbm_bench.err; echo varv_vbm_bench_rc=$?
+tail -c 300 gpurun_out/varv_vbm_bench.json

@@ -86,3 +86,25 @@ def test_variable_vcycle_rejects_overflowing_sweep_counts(psc):
     with pytest.raises(psc.PscError):
         psc.build_hierarchy(ctx, pscgen.rank_levels(h, 0), pre=1 << 20, post=1, variable_v=True)
     ctx.close()
+
+
+@pytest.mark.parametrize("grid,kw", [(16, {}), ((40, 24, 16), {}), (24, dict(problem="jump", cube=4, coarse_target=300))])
+def test_variable_vcycle_vbm_choices_fcg_parity(psc, grid, kw):
+    """VMATCH's "further algorithmic choices as in VBM" (P:330): FCG(1) outer
+    iterations and the coarsest PCG(<= 40) with l1-Jacobi, with the variable cycle."""
+    g = grid if isinstance(grid, tuple) else (grid,) * 3
+    h = pscgen.poisson_hierarchy(*g, **kw)
+    n = h.levels[0].n
+    b = pscgen.rhs_random(6, 0, n)
+    ctx = psc.Context()
+    H, *_ = psc.build_hierarchy(ctx, pscgen.rank_levels(h, 0), pre=2, post=2, variable_v=True,
+                                coarse_solver="pcg")
+    xo, ito, sto, histo = oracle.fcg(h, b, tol=1e-8, maxit=200, pre=2, post=2, variable_v=True, coarse_pcg=True)
+    x = dev(np.zeros(n))
+    rc, st, hist = H.solve(dev(b), x, tol=1e-8, maxit=200, method="fcg")
+    assert sto == 0 and rc == 0
+    assert abs(st["iters"] - ito) <= 1, (st["iters"], ito)
+    k = min(20, ito, st["iters"]) + 1
+    np.testing.assert_allclose(hist[:k], histo[:k], rtol=1e-9, atol=0)
+    assert np.linalg.norm(host(x) - xo) / np.linalg.norm(xo) <= 1e-7
+    ctx.close()
