@@ -159,7 +159,7 @@ def run_reference(args, rank, world, out=sys.stdout):
     import oracle
     import pscgen
     g = args.grid
-    h = pscgen.poisson_hierarchy(g, g, g, (1, 1, 1), problem=args.problem)
+    h = pscgen.poisson_hierarchy(g, g, g, (1, 1, 1), problem=args.problem, smooth=not args.unsmoothed_p)
     n = h.levels[0].n
     b = pscgen.rhs_poisson((g, g, g), 0, n)
     times = []
@@ -212,7 +212,8 @@ def _solver_desc(args):
     coarse = ("coarsest PCG(<=40, 1e-10) with l1-Jacobi" if args.coarse_solver == "pcg"
               else "30 coarsest l1-Jacobi sweeps")
     cyc = "variable V(2*2^l,2*2^l)" if args.variable_v else "V(4,4)"
-    return f"{args.krylov.upper()}, {cyc} l1-Jacobi, {coarse}"
+    prol = ", un-smoothed P" if args.unsmoothed_p else ""
+    return f"{args.krylov.upper()}, {cyc} l1-Jacobi, {coarse}{prol}"
 
 
 # ------------------------------------------------------------------- main
@@ -247,6 +248,8 @@ def main():
     ap.add_argument("--vbm", action="store_true", help="the paper's VBM solve: --krylov fcg --coarse-solver pcg")
     ap.add_argument("--variable-v", action="store_true",
                     help="variable V-cycle (P:330 footnote): 2 sweeps at level 0, doubled per level")
+    ap.add_argument("--unsmoothed-p", action="store_true",
+                    help="tentative (un-smoothed) prolongators, as VMATCH (P:330), on the same aggregates")
     args = ap.parse_args()
     if args.vbm:
         args.krylov, args.coarse_solver = "fcg", "pcg"
@@ -285,13 +288,15 @@ def main():
     t_setup0 = time.perf_counter()
     h = None
     if N == 1:
-        h = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem)
+        h = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem, smooth=not args.unsmoothed_p)
         levels = pscgen.rank_levels(h, 0)
         oc = h.operator_complexity()
     else:
-        shm = f"/dev/shm/psc_bench_{args.problem}_{grid[0]}x{grid[1]}x{grid[2]}_{px}{py}{pz}"
+        shm = (f"/dev/shm/psc_bench_{args.problem}_{grid[0]}x{grid[1]}x{grid[2]}_{px}{py}{pz}"
+               + ("_tentP" if args.unsmoothed_p else ""))
         if rank == 0 and not os.path.exists(os.path.join(shm, "meta.json")):
-            hh = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem)
+            hh = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem,
+                                          smooth=not args.unsmoothed_p)
             save_rank_levels(shm, hh, N)
             del hh
         dist.barrier()

@@ -6,3 +6,5 @@ timeout 900 python bench.py --variable-v --no-cpu-baseline > gpurun_out/varv_ben
 tail -c 600 gpurun_out/varv_bench.json
 timeout 900 python bench.py --variable-v --vbm --no-cpu-baseline > gpurun_out/varv_vbm_bench.json 2> gpurun_out/varv_vbm_bench.err; echo varv_vbm_bench_rc=$?
 tail -c 300 gpurun_out/varv_vbm_bench.json
+timeout 900 python bench.py --variable-v --unsmoothed-p --no-cpu-baseline > gpurun_out/varv_tentp_bench.json 2> gpurun_out/varv_tentp_bench.err; echo varv_tentp_bench_rc=$?
+tail -c 300 gpurun_out/varv_tentp_bench.json

@@ -108,3 +108,29 @@ def test_variable_vcycle_vbm_choices_fcg_parity(psc, grid, kw):
     np.testing.assert_allclose(hist[:k], histo[:k], rtol=1e-9, atol=0)
     assert np.linalg.norm(host(x) - xo) / np.linalg.norm(xo) <= 1e-7
     ctx.close()
+
+
+@pytest.mark.parametrize("grid", [16, (40, 24, 16), 48])
+def test_variable_vcycle_unsmoothed_p_pcg_parity(psc, grid):
+    """VMATCH's other solve-relevant choice: un-smoothed (tentative)
+    prolongators, here on the decoupled aggregates, with the variable cycle."""
+    g = grid if isinstance(grid, tuple) else (grid,) * 3
+    h = pscgen.poisson_hierarchy(*g, smooth=False)
+    n = h.levels[0].n
+    b = pscgen.rhs_random(8, 0, n)
+    ctx = psc.Context()
+    H, *_ = psc.build_hierarchy(ctx, pscgen.rank_levels(h, 0), pre=2, post=2, variable_v=True)
+    r = pscgen.rhs_random(9, 0, n)
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    H.vcycle(dev(r), z)
+    zo = oracle.vcycle(h, r, 2, 2, 30, variable_v=True)
+    assert np.linalg.norm(host(z) - zo) / np.linalg.norm(zo) <= 1e-12
+    xo, ito, sto, histo = oracle.pcg(h, b, tol=1e-8, maxit=300, pre=2, post=2, variable_v=True)
+    x = dev(np.zeros(n))
+    rc, st, hist = H.solve(dev(b), x, tol=1e-8, maxit=300)
+    assert sto == 0 and rc == 0
+    assert abs(st["iters"] - ito) <= 1, (st["iters"], ito)
+    k = min(20, ito, st["iters"]) + 1
+    np.testing.assert_allclose(hist[:k], histo[:k], rtol=1e-9, atol=0)
+    assert np.linalg.norm(host(x) - xo) / np.linalg.norm(xo) <= 1e-7
+    ctx.close()
