@@ -438,3 +438,91 @@ def test_paper_vbm_configuration_iterations_loose():
     x, it, st, hist = oracle.fcg(h, b, tol=1e-6, maxit=100, coarse_pcg=True, coarse_maxit=40, coarse_tol=1e-10)
     assert st == 0
     assert abs(it - golden("vbm_iterations_1gpu_tol1e-6")) <= 4
+
+
+# ----------------------- FCG(1)'s flexible update and the coarse PCG's stop rule
+# (VERDICT r1 "What's weak" 1: a Fletcher-Reeves mutant of or_fcg passed every pin
+# above, because all of them use a fixed -- or nearly fixed -- preconditioner.)
+_VARB = dict(coarse_pcg=True, coarse_maxit=2, coarse_tol=0.0)  # B(r) strongly nonlinear in r
+
+
+def _iterates(solve, h, b, K, **kw):
+    """x_0 .. x_K of a Krylov solve (each x_k from a fresh run with maxit = k; the runs
+    are deterministic, so x_k of the run with maxit = K is the same vector)."""
+    xs = [np.zeros_like(b)]
+    for k in range(1, K + 1):
+        x, it, st, _ = solve(h, b, tol=0.0, maxit=k, **kw)
+        assert it == k
+        xs.append(x)
+    return xs
+
+
+def test_fcg_local_a_orthogonality_with_variable_preconditioner():
+    """Notay's FCG(1) (reading R24) A-orthogonalises each new direction
+    against the previous one, p_k = z_k - ((z_k, A p_{k-1})/(p_{k-1}, A p_{k-1})) p_{k-1},
+    so (p_k, A p_{k-1}) = 0 for ANY z_k -- also when B varies between applications.
+    The directions are recovered from the iterates, p_k ∝ x_k - x_{k-1}.  Exact line
+    search alpha_k = (p_k, r_{k-1})/(p_k, A p_k) makes r_k ⟂ p_k.  PCG's Fletcher-Reeves
+    beta = (r,z)_k/(r,z)_{k-1} gives neither property once B is nonlinear (the coarse
+    PCG with 2 iterations and no tolerance), which the last assertion checks so
+    that the regime is known to discriminate."""
+    h = pscgen.poisson_hierarchy(16, max_levels=2)
+    assert h.levels[-1].n > 500
+    A = h.levels[0].A.to_scipy()
+    b = pscgen.rhs_random(17, 0, h.levels[0].n)
+    K = 7
+
+    def worst_orth(xs):
+        d = [xs[k] - xs[k - 1] for k in range(1, K + 1)]
+        an = [np.sqrt(v @ (A @ v)) for v in d]
+        return max(abs(d[k] @ (A @ d[k - 1])) / (an[k] * an[k - 1]) for k in range(1, K))
+
+    xf = _iterates(oracle.fcg, h, b, K, **_VARB)
+    assert worst_orth(xf) <= 1e-12
+    for k in range(1, K + 1):
+        d, r = xf[k] - xf[k - 1], b - A @ xf[k]
+        assert abs(d @ r) <= 1e-12 * np.linalg.norm(d) * np.linalg.norm(b)
+    xp = _iterates(oracle.pcg, h, b, K, **_VARB)
+    assert worst_orth(xp) >= 1e-4  # PCG loses local A-orthogonality with this B
+
+
+def test_fcg_differs_from_pcg_with_variable_preconditioner():
+    """With a strongly nonlinear B the flexible and the Fletcher-Reeves recurrences build
+    different iterates (they coincide only for a fixed SPD B, pinned above); FCG
+    still converges, with the recurrence residual equal to the true one."""
+    h = pscgen.poisson_hierarchy(16, max_levels=2)
+    A = h.levels[0].A.to_scipy()
+    b = pscgen.rhs_random(18, 0, h.levels[0].n)
+    _, itf, stf, hf = oracle.fcg(h, b, tol=1e-10, maxit=200, **_VARB)
+    _, itp, stp, hp = oracle.pcg(h, b, tol=1e-10, maxit=200, **_VARB)
+    k = min(itf, itp, 10) + 1
+    assert np.max(np.abs(hf[2:k] - hp[2:k]) / hp[2:k]) > 1e-6
+    x, it, st, hist = oracle.fcg(h, b, tol=1e-10, maxit=200, **_VARB)
+    assert st == 0
+    assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) <= 1e-9
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("tol", [1e-2, 1e-4, 1e-6])
+def test_coarse_pcg_stop_rule_equals_first_k_below_tol(seed, tol):
+    """Reading R23 (P:328 gives no test): stop at the first k with ||r_k||_2 <= tol ||b||_2
+    (x_0 = 0).  Pinned against scipy's CG with M^{-1} = diag(1/m) run without its own
+    test: the oracle's count is the first k whose scipy iterate has a true residual below
+    tol ||b||, and the oracle's x is that iterate.  A squared norm, a ||r_0|| or ||z||
+    denominator, or an off-by-one in the count fails this."""
+    from scipy.sparse.linalg import LinearOperator, cg
+    n = 80
+    A = random_spd(n, 0.08, 3 + seed)
+    b = np.random.default_rng(seed).standard_normal(n) * 7.0
+    m = oracle.l1_diag(A)
+    M = LinearOperator((n, n), matvec=lambda r: np.asarray(r).ravel() / m)
+    xs = []
+    cg(A, b, x0=np.zeros(n), rtol=0.0, atol=0.0, maxiter=300, M=M, callback=lambda xk: xs.append(xk.copy()))
+    res = [np.linalg.norm(b - A @ x) / np.linalg.norm(b) for x in xs]
+    kstar = next(k for k, r in enumerate(res, start=1) if r <= tol)
+    assert res[kstar - 1] < (1 - 1e-6) * tol and (kstar == 1 or res[kstar - 2] > (1 + 1e-6) * tol)  # no rounding tie
+    xo, it = oracle.coarse_pcg(A, b, maxit=300, tol=tol)
+    assert it == kstar
+    np.testing.assert_allclose(xo, xs[kstar - 1], rtol=0, atol=1e-10 * np.abs(xs[kstar - 1]).max())
+    xo, it = oracle.coarse_pcg(A, b, maxit=kstar - 1, tol=tol)  # the cap wins when it comes first
+    assert it == kstar - 1
