@@ -11,8 +11,9 @@ decoupled-VMB smoothed-aggregation hierarchy, V-cycle 4/4 l1-Jacobi sweeps,
 solve (every row of SURVEY.md §8(a)), right-hand side b_k = (k+1) h^2 1.
 Metric: Mdof*iters/s = N_global * iterations / solve seconds / 1e6 (whole job).
 
---impl reference runs the CPU oracle (oracle/, single thread) on rank 0 only,
-each step one PCG iteration on a 256^3 single-box sample of the same workload.
+--impl reference runs the CPU oracle (oracle/, OpenMP build on all host cores) on
+rank 0 only; each step = the per-iteration cost (T(3 it) - T(1 it)) / 2 on a
+256^3 single-box sample of the same workload.
 
 --vbm (= --krylov fcg --coarse-solver pcg) times the paper's VBM solve
 configuration instead: FCG(1) outer
@@ -152,24 +153,44 @@ def load_rank_levels(d, r):
 
 
 # -------------------------------------------------------------- reference
+def oracle_threads():
+    """Host cores for the oracle's OpenMP build (all of them; OMP_NUM_THREADS overrides)."""
+    env = os.environ.get("OMP_NUM_THREADS")
+    return int(env) if env else (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+
+
+def oracle_seconds_per_iteration(args, h, b, k1=1, k2=3):
+    """Seconds per Krylov iteration of the oracle, as a difference T(k2) - T(k1) over
+    k2 - k1 iterations: the set-up inside one call (l1 diagonals, initial residual,
+    the first V-cycle) cancels, so what is credited is exactly k2 - k1 iterations
+    (each = one V-cycle, one SpMV, the dots and the vector updates)."""
+    solve = _oracle_solve(args)
+    t = []
+    for k in (k1, k2):
+        t0 = time.perf_counter()
+        solve(h, b, tol=0.0, maxit=k, **_oracle_kw(args))
+        t.append(time.perf_counter() - t0)
+    return max(t[1] - t[0], 1e-9) / (k2 - k1), t[0] + t[1]
+
+
 def run_reference(args, rank, world, out=sys.stdout):
-    """CPU oracle arm: rank 0 only; each step = 1 PCG iteration on a 256^3 sample."""
+    """CPU oracle arm: rank 0 only.  Each step = 2 iterations of the oracle (T(3) - T(1))
+    on a single-box sample of the same workload, OpenMP build on all host cores."""
     if rank != 0:
         return
     import oracle
     import pscgen
+    cores = oracle.set_threads(oracle_threads())
     g = args.grid
     h = pscgen.poisson_hierarchy(g, g, g, (1, 1, 1), problem=args.problem, smooth=not args.unsmoothed_p)
     n = h.levels[0].n
     b = pscgen.rhs_poisson((g, g, g), 0, n)
-    times = []
+    per_it = []
     for k in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        x, it, st, hist = _oracle_solve(args)(h, b * (k + 1), tol=0.0, maxit=1, **_oracle_kw(args))
-        dt = time.perf_counter() - t0
+        s_it, _ = oracle_seconds_per_iteration(args, h, b * (k + 1))
         if k >= args.warmup:
-            times.append(dt)
-    t = sum(times)
+            per_it.append(s_it)
+    t = sum(per_it)  # seconds for `steps` iterations
     value = n * args.steps / t / 1e6
     line = {
         "impl": "reference", "metric": _metric(args), "value": value, "unit": "Mdof*iters/s",
@@ -177,20 +198,29 @@ def run_reference(args, rank, world, out=sys.stdout):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"3D {args.problem} 7-point {g}^3 single-box sample of the {g}^3-per-GPU weak-scaling "
                                f"workload (BASELINE.json configs[{4 if args.problem == 'jump' else 2}]); step = 1 "
-                               f"{args.krylov.upper()} iteration of the CPU oracle",
+                               f"{args.krylov.upper()} iteration of the CPU oracle, timed as (T(3 it) - T(1 it)) / 2",
                    "levels": h.nlevels, "n_dof": n, "solver": _solver_desc(args)},
-        "cpu_baseline": {"value": value, "unit": "Mdof*iters/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} steps x 1 {args.krylov.upper()} iteration (incl. its V-cycles) "
-                                   f"on {g}^3"},
+        "cpu_baseline": {"value": value, "unit": "Mdof*iters/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} steps x (T(3) - T(1))/2 {args.krylov.upper()} iterations "
+                                   f"(incl. their V-cycles) on {g}^3, OpenMP build of the oracle, {cores} threads"},
         "e2e": {"value": value, "unit": "Mdof*iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), file=out, flush=True)
 
 
 def _metric(args):
-    """The metric string, identical on both arms (--impl psc / reference)."""
+    """The metric string, identical on both arms (--impl psc / reference); non-default
+    cycles / prolongators are named, so lines with different per-iteration work never
+    share a metric name."""
     scope = f"{args.global_grid}^3 global" if args.global_grid > 0 else f"{args.grid}^3 dof per GPU"
-    return f"AMG-{args.krylov.upper()} Mdof*iters/s (3D {args.problem}, {scope}, tol {args.tol:g})"
+    var = ""
+    if args.variable_v:
+        var += ", variable V(2*2^l,2*2^l)"
+    if args.unsmoothed_p:
+        var += ", un-smoothed P"
+    if args.coarse_solver == "pcg":
+        var += ", coarsest PCG"
+    return f"AMG-{args.krylov.upper()} Mdof*iters/s (3D {args.problem}, {scope}, tol {args.tol:g}{var})"
 
 
 def _oracle_solve(args):
@@ -240,7 +270,6 @@ def main():
     ap.add_argument("--problem", default="poisson", choices=["poisson", "jump"])
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--maxit", type=int, default=200)
-    ap.add_argument("--cpu-iters", type=int, default=2, help="oracle PCG iterations in the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--krylov", default="pcg", choices=["pcg", "fcg"])
@@ -366,20 +395,14 @@ def main():
     dom_b = stats[0]["dom_kernel_bytes"]
     peak, peak_src = load_peaks()
     achieved = dom_b * dom_n / dom_s / 1e9 if dom_s > 0 else None
-    sweeps = stats[0].get("dom_kernel_sweeps", 1)
-    if sweeps > 1:
-        # the level-0 post-smoothing pass: `sweeps` l1-Jacobi sweeps in one wavefront launch
-        # (A_0, b, 1/M, x_in read once, x_out written once); one per iteration, all timed
-        kname = f"sell_wave (level-0 post-smoothing: {sweeps} fused l1-Jacobi sweeps, TMA-staged wavefront)"
-        per_iter, tkey = 1, f"wave_post_l0_{g}"
-    else:
-        kname = "sell_tma<Sweep> (level-0 fused l1-Jacobi sweep, TMA-staged)"
-        per_iter, tkey = 7, f"sweep_l0_{g}"  # 3 pre + 4 post sweep launches (R4); one timed per iteration
+    kname = "sell_tma<Sweep> (level-0 fused l1-Jacobi sweep, TMA-staged)"
+    per_iter = stats[0]["dom_kernel_per_iter"]  # (pre-1) + post level-0 sweep launches per iteration
+    tkey = f"sweep_l0_{g}"
     roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": achieved / peak if achieved else None,
             "traffic": None if strong else load_traffic(tkey), "algorithmic_bytes_per_launch": dom_b,
-            "sweeps_per_launch": sweeps,
+            "launches_per_iteration": per_iter,
             "launches_timed": dom_n, "avg_launch_us": 1e6 * dom_s / dom_n if dom_n else None,
             "share_of_step": (dom_s / dom_n * per_iter * sum(iters) / sum(s["solve_seconds"] for s in stats)
                               if dom_n else None)}
@@ -409,13 +432,13 @@ def main():
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         import oracle
+        cores = oracle.set_threads(oracle_threads())
         bcpu = pscgen.rhs_poisson(grid, 0, n_global)
-        t0 = time.perf_counter()
-        _oracle_solve(args)(h, bcpu, tol=0.0, maxit=args.cpu_iters, **_oracle_kw(args))
-        tc = time.perf_counter() - t0
-        cpu = {"value": n_global * args.cpu_iters / tc / 1e6, "unit": "Mdof*iters/s", "cores": 1, "kind": "oracle",
-               "sample": f"{args.cpu_iters} {args.krylov.upper()} iterations (tol 0) of the same {grid[0]}x{grid[1]}x{grid[2]} "
-                         f"workload, single thread, {tc:.1f} s"}
+        s_it, tc = oracle_seconds_per_iteration(args, h, bcpu)
+        cpu = {"value": n_global / s_it / 1e6, "unit": "Mdof*iters/s", "cores": cores, "kind": "oracle",
+               "sample": f"(T(3) - T(1)) / 2 {args.krylov.upper()} iterations (tol 0) of the same "
+                         f"{grid[0]}x{grid[1]}x{grid[2]} workload, OpenMP build of the oracle on {cores} threads, "
+                         f"{tc:.1f} s total"}
 
     if rank == 0:
         solve_s = [s["solve_seconds"] for s in stats]
@@ -431,6 +454,7 @@ def main():
             "value": value, "unit": "Mdof*iters/s", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "time_to_solution_s": statistics.median(solve_s),
             "config": {
                 "workload": workload,
                 "global_grid": list(grid), "procs": [px, py, pz], "n_global": n_global, "levels": info["nlevels"],

@@ -219,8 +219,7 @@ typedef struct {
   int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by psc_pcg_solve_host */
   int halo_path;                /* 0 single rank, 1 NVLink peer stores (CUDA IPC), 2 NCCL */
   int iter_graph_nodes;         /* kernel launches per PCG iteration (captured graph) */
-  int dom_kernel_sweeps;        /* l1-Jacobi sweeps done by one timed launch: 1, or post_sweeps when the
-                                   level-0 post-smoothing runs as one fused wavefront pass */
+  int dom_kernel_per_iter;      /* level-0 sweep launches per Krylov iteration ((pre-1) + post) */
 } psc_stats;
 
 /* [collective] PCG (reading R1 of DESIGN.md) preconditioned by one

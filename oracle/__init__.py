@@ -24,14 +24,33 @@ _lib = None
 STATUS = {0: "converged", 1: "not converged", -6: "breakdown"}
 
 
+_SO_OMP = os.path.join(_HERE, "liboracle_omp.so")
+_threads = 1
+
+
 def build(force: bool = False) -> str:
+    """Serial build (liboracle.so, what the tests use) and the OpenMP build of the same
+    source (liboracle_omp.so, bitwise identical results; cpu_baseline on all cores)."""
     src = os.path.join(_HERE, "psc_oracle.c")
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
-        tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-fPIC",
-                               "-shared", "-o", tmp, src, "-lm"])
-        os.replace(tmp, _SO)
+    for so, extra in ((_SO, []), (_SO_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            tmp = so + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-fPIC",
+                                   "-shared", *extra, "-o", tmp, src, "-lm"])
+            os.replace(tmp, so)
     return _SO
+
+
+def set_threads(n: int) -> int:
+    """Use the OpenMP build with n threads (n <= 1: the serial build).  Returns the thread count.
+    Must be called before the first oracle call of the process."""
+    global _threads, _lib
+    if _lib is not None and (n > 1) != (_threads > 1):
+        raise RuntimeError("oracle.set_threads must be called before the first oracle call")
+    _threads = max(1, int(n))
+    if _threads > 1:
+        return lib().or_set_threads(_threads)
+    return 1
 
 
 class _CSR(ctypes.Structure):
@@ -50,7 +69,9 @@ def lib():
     global _lib
     if _lib is None:
         build()
-        L = ctypes.CDLL(_SO)
+        L = ctypes.CDLL(_SO_OMP if _threads > 1 else _SO)
+        L.or_set_threads.argtypes = [ctypes.c_int]
+        L.or_set_threads.restype = ctypes.c_int
         vp = ctypes.c_void_p
         L.or_spmv.argtypes = [vp, vp, vp]
         L.or_l1_diag.argtypes = [vp, vp]

@@ -12,11 +12,36 @@
  *
  * Matrices are global CSR (int64 row_ptr, int64 column, f64 value).  The
  * hierarchy {A_l, P_l, R_l} is GIVEN (BASELINE.json north_star).
+ *
+ * Threads (SURVEY.md §8(d) "Oracle timing"): the same source also builds with
+ * -fopenmp (liboracle_omp.so, the cpu_baseline timed on all host cores).  Only
+ * row-independent loops are parallel (each output element is computed by one
+ * thread with the serial arithmetic), and dot products sum fixed 4096-element
+ * chunks serially and then the chunk sums in chunk order (reading R13: any fixed
+ * order), so both builds are bitwise identical for any thread count.
  */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#define OR_PAR _Pragma("omp parallel for schedule(static)")
+#else
+#define OR_PAR
+#endif
+
+/* number of threads of the OpenMP build (1 in the serial build) */
+int or_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
+}
 
 typedef struct {
   int64_t nrows, ncols;
@@ -40,6 +65,7 @@ typedef struct {
 
 /* y = A x.  Row sums in stored column order. */
 void or_spmv(const or_csr* A, const double* x, double* y) {
+  OR_PAR
   for (int64_t i = 0; i < A->nrows; ++i) {
     double s = 0.0;
     for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) s += A->val[k] * x[A->col[k]];
@@ -51,6 +77,7 @@ void or_spmv(const or_csr* A, const double* x, double* y) {
  *   M_l = diag(A_l) + diag( { sum_{j=1, j!=i}^{N} |a_ij| }_i )
  * over the whole row (reading R7).  m[i] is the i-th diagonal entry of M_l. */
 void or_l1_diag(const or_csr* A, double* m) {
+  OR_PAR
   for (int64_t i = 0; i < A->nrows; ++i) {
     double aii = 0.0, off = 0.0;
     for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) {
@@ -64,6 +91,7 @@ void or_l1_diag(const or_csr* A, double* m) {
 /* One smoothing sweep x_new = x + M^{-1} (b - A x) (the factor (I - M^{-1}A)
  * of Eq. (2)), Jacobi: every row reads the old x (reading R8). */
 void or_l1_sweep(const or_csr* A, const double* m, const double* b, const double* x, double* xnew) {
+  OR_PAR
   for (int64_t i = 0; i < A->nrows; ++i) {
     double s = 0.0;
     for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) s += A->val[k] * x[A->col[k]];
@@ -85,9 +113,21 @@ void or_l1_sweeps_from_zero(const or_csr* A, const double* m, const double* b, i
 
 static double* dalloc(int64_t n) { return (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double)); }
 
+/* (a, b): serial sums over fixed chunks of 4096 entries, then the chunk sums in
+ * chunk order (fixed order, independent of the thread count). */
 static double dot(int64_t n, const double* a, const double* b) {
+  const int64_t C = 4096, nc = (n + C - 1) / C;
+  double* part = (double*)calloc((size_t)(nc > 0 ? nc : 1), sizeof(double));
+  OR_PAR
+  for (int64_t c = 0; c < nc; ++c) {
+    double s = 0.0;
+    const int64_t e = (c + 1) * C < n ? (c + 1) * C : n;
+    for (int64_t i = c * C; i < e; ++i) s += a[i] * b[i];
+    part[c] = s;
+  }
   double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  for (int64_t c = 0; c < nc; ++c) s += part[c];
+  free(part);
   return s;
 }
 
@@ -107,6 +147,7 @@ int or_coarse_pcg(const or_csr* A, const double* m, const double* b, double* x, 
   const double nb = sqrt(dot(n, b, b));
   int k = 0;
   if (nb > 0.0) {
+    OR_PAR
     for (int64_t i = 0; i < n; ++i) z[i] = r[i] / m[i];
     memcpy(p, z, sizeof(double) * (size_t)n);
     double rz = dot(n, r, z);
@@ -115,13 +156,17 @@ int or_coarse_pcg(const or_csr* A, const double* m, const double* b, double* x, 
       const double pq = dot(n, p, q);
       if (!(pq > 0.0)) { k -= 1; break; }
       const double alpha = rz / pq;
+      OR_PAR
       for (int64_t i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
+      OR_PAR
       for (int64_t i = 0; i < n; ++i) r[i] = r[i] - alpha * q[i];
       if (sqrt(dot(n, r, r)) <= tol * nb) break;
+      OR_PAR
       for (int64_t i = 0; i < n; ++i) z[i] = r[i] / m[i];
       const double rz_new = dot(n, r, z);
       const double beta = rz_new / rz;
       rz = rz_new;
+      OR_PAR
       for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
     }
     if (k > maxit) k = maxit;
@@ -161,10 +206,12 @@ static void vcycle_level(const or_hier* h, double* const* m, int l, const double
   double* bc = dalloc(nc);
   double* xc = dalloc(nc);
   or_spmv(A, x, r);
+  OR_PAR
   for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
   or_spmv(R, r, bc);
   vcycle_level(h, m, l + 1, bc, xc);
   or_spmv(P, xc, r);
+  OR_PAR
   for (int64_t i = 0; i < n; ++i) x[i] = x[i] + r[i];
   free(r);
   free(bc);
@@ -219,6 +266,7 @@ int or_pcg(const or_hier* h, const double* b, double* x, double tol, int maxit, 
   double* q = dalloc(n);
   int status = 1;
   or_spmv(A, x, r);
+  OR_PAR
   for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
   hist[0] = sqrt(dot(n, r, r)) / nb;
   if (hist[0] <= tol) { status = 0; goto done; }
@@ -230,7 +278,9 @@ int or_pcg(const or_hier* h, const double* b, double* x, double tol, int maxit, 
     const double pq = dot(n, p, q);
     if (!(pq > 0.0) || !isfinite(pq)) { status = -6; *iters = k; goto done; }
     const double alpha = rz / pq;
+    OR_PAR
     for (int64_t i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
+    OR_PAR
     for (int64_t i = 0; i < n; ++i) r[i] = r[i] - alpha * q[i];
     hist[k] = sqrt(dot(n, r, r)) / nb;
     *iters = k;
@@ -239,6 +289,7 @@ int or_pcg(const or_hier* h, const double* b, double* x, double tol, int maxit, 
     const double rz_new = dot(n, r, z);
     const double beta = rz_new / rz;
     rz = rz_new;
+    OR_PAR
     for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
   }
 done:
@@ -272,6 +323,7 @@ int or_fcg(const or_hier* h, const double* b, double* x, double tol, int maxit, 
   int status = 1;
   double delta = 0.0;
   or_spmv(A, x, r);
+  OR_PAR
   for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
   hist[0] = sqrt(dot(n, r, r)) / nb;
   if (hist[0] <= tol) { status = 0; goto done; }
@@ -281,13 +333,16 @@ int or_fcg(const or_hier* h, const double* b, double* x, double tol, int maxit, 
       memcpy(p, z, sizeof(double) * (size_t)n);
     } else {
       const double beta = dot(n, z, q) / delta; /* q = A p_{k-1} */
+      OR_PAR
       for (int64_t i = 0; i < n; ++i) p[i] = z[i] - beta * p[i];
     }
     or_spmv(A, p, q);
     delta = dot(n, p, q);
     if (!(delta > 0.0) || !isfinite(delta)) { status = -6; *iters = k; goto done; }
     const double alpha = dot(n, p, r) / delta;
+    OR_PAR
     for (int64_t i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
+    OR_PAR
     for (int64_t i = 0; i < n; ++i) r[i] = r[i] - alpha * q[i];
     hist[k] = sqrt(dot(n, r, r)) / nb;
     *iters = k;

@@ -48,7 +48,7 @@ class Stats(ctypes.Structure):
                 ("kernel_launches", _i64), ("collectives", _i64), ("dom_kernel_seconds", _f64),
                 ("dom_kernel_launches", _i64), ("dom_kernel_bytes", _f64), ("h2d_bytes", _i64),
                 ("d2h_bytes", _i64), ("halo_path", _i32), ("iter_graph_nodes", _i32),
-                ("dom_kernel_sweeps", _i32)]
+                ("dom_kernel_per_iter", _i32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -14,6 +14,14 @@ thread_local std::string g_err;  // last error without a context (psc_init failu
 int fail(psc_ctx* ctx, const Error& e) {
   if (ctx) ctx->err = e.what();
   g_err = e.what();
+  // A device fault (e.g. a peer-flag wait that timed out and trapped, p2p.cu) or an
+  // NCCL failure leaves the other ranks inside a collective: abort the communicator
+  // so their NCCL calls return an error instead of hanging.  Later collective calls
+  // on this context fail with PSC_ERR_STATE.
+  if (ctx && ctx->comm && ctx->nranks > 1 && (e.code == PSC_ERR_CUDA || e.code == PSC_ERR_NCCL)) {
+    ncclCommAbort(ctx->comm);
+    ctx->comm = nullptr;
+  }
   return e.code;
 }
 int fail(psc_ctx* ctx, const std::exception& e) {

@@ -44,10 +44,6 @@ struct LevelWS {
   bool one_cta = false;       // sparse one-CTA solver applies
   double* cz = nullptr;       // general coarsest PCG: z and q = A p (n)
   double* cq = nullptr;
-  // wavefront passes (sell_wave): dependency reach in 256-row chunks, chunk
-  // counters + watermarks; wave_h < 0: the level runs stage by stage
-  int64_t wave_h = -1;
-  unsigned int* wave_flags = nullptr;
 };
 
 // Replicated suffix (nranks > 1): levels first..L-1 are held whole on every
@@ -77,7 +73,6 @@ struct psc_hier_s {
   psc_cycle_opts opt{4, 4, 30, PSC_COARSE_SWEEPS, 40, 1e-10, 0};
   std::vector<LevelWS> lv;
   Replica rep;
-  bool z0_fused = false;  // CG update writes the first level-0 sweep of the next V-cycle
   // dense suffix: the V-cycle operator of levels dsuf_l.. of the level array
   // *dsuf_lv, precomputed as a dense row-major matrix (linear coarse solver only)
   const std::vector<LevelWS>* dsuf_lv = nullptr;
@@ -148,9 +143,7 @@ void exchange(psc_hier* h, psc_desc* d, double* x, cudaStream_t s) {
   halo_exchange(ctx, d, x, s);
 }
 
-// Halo exchange of a.x before the row kernel `a` is launched: folded into that
-// kernel's prologue when the NVLink path is on (no separate launch), else a
-// standalone exchange.  PSC_NO_FUSED_EXCHANGE=1 keeps the standalone kernel.
+// Halo exchange of a.x before the row kernel `a` is launched.
 void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
   psc_ctx* ctx = h->ctx;
   if (ctx->nranks == 1 || !d) return;
@@ -160,13 +153,9 @@ void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
   if (skip) return;
   for (int l = skip_from; l < h->L; ++l)
     if (h->lv[l].d == d) return;
-  // measured slower than the standalone exchange kernel on 2 B200 (5.51 vs 5.40
-  // ms per iteration at 256^3/GPU): opt-in with PSC_FUSED_EXCHANGE=1
-  static const bool nofuse = getenv("PSC_FUSED_EXCHANGE") == nullptr;
   // TIMING EXPERIMENTS ONLY: PSC_DEBUG_DOUBLE_HALO=1 adds a second, standalone exchange
   static const bool twice = getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr;
   if (twice) exchange(h, d, const_cast<double*>(a.x), s);
-  if (!nofuse && p2p_fused(ctx, h->p2p, d, a.x, a.ex)) return;
   exchange(h, d, const_cast<double*>(a.x), s);
 }
 
@@ -182,7 +171,7 @@ void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cud
   psc_ctx* ctx = h->ctx;
   static const bool no_overlap = getenv("PSC_OVERLAP") == nullptr || getenv("PSC_DEBUG_SKIP_HALO") != nullptr ||
                                  getenv("PSC_DEBUG_SKIP_HALO_FROM") != nullptr ||
-                                 getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr || getenv("PSC_FUSED_EXCHANGE") != nullptr;
+                                 getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr;
   const bool reduces = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
   if (!no_overlap && ctx->nranks > 1 && d && !reduces && S.n_boundary > 0 && S.n_interior > 0) {
     PSC_CUDA(cudaEventRecord(h->ev_fork, s));
@@ -323,87 +312,6 @@ int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream
 
 bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
 
-// ------------------------------------------------------- wavefront passes
-// (sell_wave, kernels.cu) on levels whose A qualifies: single rank (no halo),
-// slices at most 8 wide.  Opt-in (PSC_WAVE=1) until measured.
-// key slack: dependencies should lie outside the items in flight (~3 per CTA,
-// 2 CTAs per SM), while the rows between a chunk's first and last stage must
-// stay in L2 (window (nst-1) * G chunks, budget ~96 MB of the 126 MB)
-// (all in items of 8 chunks = 2048 rows)
-int64_t wave_slack(psc_hier* h, const LevelWS& W, int nst) {
-  const char* e = getenv("PSC_WAVE_SLACK");
-  if (e) return std::max(0, atoi(e));
-  const int64_t inflight = 2 * 2 * (int64_t)h->ctx->num_sms / std::max(nst, 1);
-  const double row_bytes = 12.0 * (double)W.A->S.padded / std::max<int64_t>(W.n, 1) + 32.0;
-  const int64_t gmax = (int64_t)(96.0 * (1 << 20) / (std::max(nst - 1, 1) * 8 * kWaveChunkRows * row_bytes));
-  return std::max<int64_t>(2, std::min(inflight, gmax - (W.wave_h + kWaveBlk + 8) / 8 - 1));
-}
-
-void wave_setup(psc_hier* h, LevelWS& W) {
-  if (!getenv("PSC_WAVE") || h->ctx->nranks != 1 || W.nh != 0 || !wave_supported(W.A->S)) return;
-  const int64_t bw = sell_bandwidth(h->ctx, W.A->S, h->ctx->stream);
-  W.wave_h = (bw + kWaveChunkRows - 1) / kWaveChunkRows;
-  W.wave_flags = dalloc<unsigned int>((size_t)kWaveMaxStages * ((wave_chunks(W.A->S) + kWaveBlk - 1) / kWaveBlk));
-}
-
-void wave_launch(psc_hier* h, LevelWS& W, WaveArgs& a, cudaStream_t s) {
-  a.h = W.wave_h;
-  a.G = (W.wave_h + kWaveBlk + 8 + 7) / 8 + wave_slack(h, W, a.nst);  // items of 8 chunks
-  a.flags = W.wave_flags;
-  launch_wave(h->ctx, W.A->S, a, s);
-}
-
-// pre-smoothing and the residual of the coarse-grid correction in one pass:
-// [x0 = M^-1 b,] pre-1 sweeps, r = b - A x.  Returns the buffer index of x.
-int wave_pre(psc_hier* h, LevelWS& W, const double* b, int pre, bool first_done, cudaStream_t s) {
-  WaveArgs a;
-  a.b = b;
-  a.dinv = W.dinv;
-  int cur = 0;
-  if (!first_done) {
-    a.op[a.nst] = (int)WaveOp::Scale;
-    a.xin[a.nst] = nullptr;
-    a.xout[a.nst++] = W.x[0];
-  }
-  for (int k = 1; k < pre; ++k) {
-    a.op[a.nst] = (int)WaveOp::Sweep;
-    a.xin[a.nst] = W.x[cur];
-    a.xout[a.nst++] = W.x[cur ^ 1];
-    cur ^= 1;
-  }
-  a.op[a.nst] = (int)WaveOp::Resid;
-  a.xin[a.nst] = W.x[cur];
-  a.xout[a.nst++] = W.r;
-  wave_launch(h, W, a, s);
-  return cur;
-}
-
-// post-smoothing: `post` sweeps from x[cur]; the last one reduces (w, x) into
-// red_out when red_out is set.  Returns the buffer index of x.
-int wave_post(psc_hier* h, LevelWS& W, const double* b, int post, int cur, double* red_out, cudaStream_t s) {
-  WaveArgs a;
-  a.b = b;
-  a.dinv = W.dinv;
-  for (int k = 0; k < post; ++k) {
-    a.op[a.nst] = (int)((red_out && k == post - 1) ? WaveOp::SweepDot : WaveOp::Sweep);
-    a.xin[a.nst] = W.x[cur];
-    a.xout[a.nst++] = W.x[cur ^ 1];
-    cur ^= 1;
-  }
-  if (red_out) {
-    a.reduce = 1;
-    a.w = h->rz_weight;
-    a.partials = h->red1.partials;
-    a.ticket = h->red1.ticket;
-    a.red_grid = h->red1.grid;
-    a.red_out = red_out;
-  }
-  wave_launch(h, W, a, s);
-  return cur;
-}
-
-bool wave_fits(const LevelWS& W, int nst) { return W.wave_h >= 0 && nst >= 1 && nst <= kWaveMaxStages; }
-
 // Smoothing sweeps at hierarchy level `glev`: the base count, doubled per level
 // for the variable V-cycle (P:330 footnote, reading R25).
 int level_sweeps(const psc_hier* h, int base, int glev) { return h->opt.variable_v ? base << glev : base; }
@@ -450,11 +358,8 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   // hierarchy level of LV[l] (the replicated suffix starts at level rep.first)
   const int glev = l + (&LV == &h->rep.lv ? h->rep.first : 0);
   const int pre = level_sweeps(h, h->opt.pre_sweeps, glev);
-  int cur;
-  if (pre > 0 && wave_fits(W, pre + (first_done ? 0 : 1))) {
-    cur = wave_pre(h, W, b, pre, first_done, s);  // sweeps + residual in one pass
-  } else {
-    cur = pre_smooth(h, W, b, pre, s, time_here, first_done);
+  int cur = pre_smooth(h, W, b, pre, s, time_here, first_done);
+  {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
@@ -488,16 +393,6 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
   const int post = level_sweeps(h, h->opt.post_sweeps, glev);
   const bool level0 = dist && l == 0;
-  if (post > 0 && wave_fits(W, post)) {
-    const bool t = time_here && h->dom_used + 2 <= (int)h->ev_dom.size();
-    if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
-    cur = wave_post(h, W, b, post, cur, level0 ? scal_mine(h, S_RZ) : nullptr, s);
-    if (t) {
-      PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
-      h->dom_used += 2;
-    }
-    return W.x[cur];
-  }
   for (int k = 0; k < post; ++k) {
     const bool last0 = (level0 && k == post - 1);
     RowArgs a;
@@ -546,7 +441,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing, int method) {
   h->dom_used = 0;
   // the CG update of the previous iteration (or the eager start) wrote x_0 = M^{-1} r
   h->rz_weight = fcg ? h->q : nullptr;
-  double* z = vcycle_level(h, 0, h->r_cg, s, timing, h->z0_fused);
+  double* z = vcycle_level(h, 0, h->r_cg, s, timing);
   h->rz_weight = nullptr;
   h->z_ptr = z;
   allgather_slot(h, S_RZ, s);
@@ -568,8 +463,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing, int method) {
   }
   allgather_slot(h, S_PQ, s);
   launch_cg_update(ctx, W.n, h->x_int, h->p, h->r_cg, h->q, scal(h, S_PQ), fcg ? scal(h, S_PR) : rz_old(h),
-                   fcg ? R : 1, R, &h->red1, scal_mine(h, S_RR), s, h->z0_fused ? W.dinv : nullptr,
-                   h->z0_fused ? W.x[0] : nullptr);
+                   fcg ? R : 1, R, &h->red1, scal_mine(h, S_RR), s);
   allgather_slot(h, S_RR, s);
   PSC_CUDA(cudaMemcpyAsync(h->h_scal, h->d_scal, sizeof(double) * NSLOT * R, cudaMemcpyDeviceToHost, s));
 }
@@ -686,9 +580,13 @@ int replica_first(psc_hier* h) {
         if (m && (int64_t)m->h_rowptr.size() != m->n_rows + 1) return false;
     return true;
   };
+  // Host copies are kept per rank by local size (api.cu), so the decision is agreed on
+  // by all ranks: the replicated suffix is built only if every rank has the copies
+  // (a rank-local choice would send ranks into different collectives).
+  auto all_have_host = [&](int l) { return allreduce_min(h->ctx, has_host(l) ? 1 : 0) == 1; };
   for (int l = 1; l < h->L; ++l)
-    if (h->lv[l].d->n_global <= lim) return has_host(l) ? l : -1;
-  return (h->lv[h->L - 1].d->n_global <= coarse_smem_rows() && has_host(h->L - 1)) ? h->L - 1 : -1;
+    if (h->lv[l].d->n_global <= lim) return all_have_host(l) ? l : -1;
+  return (h->lv[h->L - 1].d->n_global <= coarse_smem_rows() && all_have_host(h->L - 1)) ? h->L - 1 : -1;
 }
 
 void level_coarse_solver(psc_hier* h, LevelWS& W) {
@@ -804,7 +702,6 @@ void free_hier(psc_hier* h) {
     if (&W != &h->lv[0]) dfree(W.b);
     dfree(W.cz);
     dfree(W.cq);
-    dfree(W.wave_flags);
   }
   Replica& rp = h->rep;
   for (auto& W : rp.lv) {
@@ -901,7 +798,6 @@ int solve_impl(psc_hier* h, int method, const double* b, double* x, double tol, 
         const double one = 1.0;
         PSC_CUDA(cudaMemcpyAsync(rz_old(h), &one, sizeof(double), cudaMemcpyHostToDevice, s));
       }
-      if (h->z0_fused) launch_scale(ctx, W.n, W.dinv, h->r_cg, W.x[0], s);  // first V-cycle's first sweep
       if (!h->iter_exec[method]) capture_iteration(h, method);
       for (int k = 1; k <= maxit; ++k) {
         PSC_CUDA(cudaGraphLaunch(h->iter_exec[method], s));
@@ -947,9 +843,9 @@ int solve_impl(psc_hier* h, int method, const double* b, double* x, double tol, 
   // bytes the level-0 sweep must move in its layout: 8 B per stored value, 4 B per
   // explicit column index (ELL slices), x in, b, dinv, x out
   S.dom_kernel_bytes = 8.0 * (double)W.A->nnz + 4.0 * (double)W.A->S.nnz_ell + 32.0 * (double)W.n;
-  // the timed launch: one sweep, or the fused post-smoothing pass (A, b, 1/M and x
-  // read once, x written once: the same algorithmic bytes for `post` sweeps)
-  S.dom_kernel_sweeps = (h->L > 1 && wave_fits(W, h->opt.post_sweeps)) ? h->opt.post_sweeps : 1;
+  // level-0 sweep launches per iteration: pre-1 (the first pre-sweep from zero is
+  // x = M^-1 b, no matrix) + post; one level: the coarsest solver's sweeps
+  S.dom_kernel_per_iter = h->L > 1 ? std::max(h->opt.pre_sweeps - 1, 0) + h->opt.post_sweeps : 0;
   S.h2d_bytes = (int64_t)extra_h2d;
   S.halo_path = R == 1 ? 0 : (h->p2p.on ? 1 : 2);
   S.iter_graph_nodes = (int)h->iter_launches[method];
@@ -1049,9 +945,6 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       h->rep.maxcnt = maxcnt;
     }
     PSC_CUDA(cudaMallocHost(&h->h_scal, sizeof(double) * ((size_t)NSLOT * ctx->nranks + 1)));
-    // level 0: writing z0 = M^{-1} r from the CG update measured slower than the
-    // separate scale kernel (201 us vs 123 + 57 us at 256^3): opt-in PSC_Z0_FUSED=1
-    h->z0_fused = getenv("PSC_Z0_FUSED") && fuse_first_sweep() && nlevels > 1 && h->opt.pre_sweeps > 0;
     h->red1 = red_alloc(ctx->num_sms, 1);
     h->red2 = red_alloc(ctx->num_sms, 2);
     h->d_done = dalloc<int>(1);
@@ -1089,7 +982,6 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       p2p_setup(ctx, h->p2p, hb, gs, ld, (char*)flagbuf - h->arena);
     } else {
       level_coarse_solver(h, Wc);
-      for (int l = 0; l + 1 < nlevels; ++l) wave_setup(h, h->lv[l]);
     }
     build_dense_suffix(h);
     if (h->opt.coarse_solver == PSC_COARSE_PCG) {  // buffers of the general coarsest PCG

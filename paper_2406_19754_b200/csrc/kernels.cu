@@ -18,35 +18,14 @@ static int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
-// ---------------------------------------------- programmatic dependent launch
-// Every solve-path kernel starts with griddepcontrol.wait (all prior grids
-// complete and visible; a no-op without PDL) followed by
-// griddepcontrol.launch_dependents, and is launched with programmatic stream
-// serialization: inside the captured iteration graph the next kernel's CTAs
-// are staged while the current one drains, hiding launch latency between the
-// ~50 dependent kernels of a PCG iteration.  The trigger is issued when a CTA
-// has finished its work (an entry-time trigger let waiting dependent CTAs take
-// SM resources from the running grid: 3080 vs 3634 Mdof*it/s).  Measured
-// slower even with the end-of-work trigger (3523 vs 3645), so it is off unless
-// PSC_PDL=1.
-__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// a CTA is done with its share: the dependent grid may be scheduled once every CTA got here
-__device__ __forceinline__ void pdl_exit() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
 template <typename... KArgs, typename... Args>
 static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {
-  static const bool pdl = env_int("PSC_PDL", 0) != 0;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cfg.attrs = pdl ? attr : nullptr;
-  cfg.numAttrs = pdl ? 1 : 0;
   PSC_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
@@ -115,13 +94,7 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NR], double* partials,
 
 constexpr int kHdr = 16;     // int32 words per slice header
 constexpr int kMaxDia = 8;   // most diagonals a DIA slice may have (header words 6..13)
-// DICT slice: ELL values, columns as 1-byte indices into a per-slice table of at
-// most kMaxDict distinct offsets j - i (header word 5 = 2, word 6 = table size).
-// Column region: table (rounded up to 4 words), then the indices packed 4 per
-// word, word (q / 4) * 32 + lane holding entries q..q+3 of the slice's row `lane`.
-constexpr int kMaxDict = 64;
-enum SliceKind : int { kEll = 0, kDia = 1, kDict = 2 };
-__device__ __forceinline__ int64_t dict_t4(int d) { return (d + 3) & ~3; }
+enum SliceKind : int { kEll = 0, kDia = 1 };
 
 __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int64_t s, int lane) {
   return lane < kHdr ? __ldg(hdr + s * kHdr + lane) : 0;
@@ -136,9 +109,7 @@ __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int
 __device__ __forceinline__ double ldm(const double* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
 __device__ __forceinline__ int32_t ldm(const int32_t* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
 
-// x gathers: read-only texture path, or (CG) through L2 only — for vectors
-// written by other CTAs of the same launch (the wavefront pass), which the
-// non-coherent L1 may hold stale
+// x gathers: read-only texture path, or (CG) through L2 only
 template <bool CG>
 __device__ __forceinline__ double ldx(const double* p) {
   if constexpr (CG) return __ldcg(p);
@@ -194,36 +165,6 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
   }
   const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
                      (uint32_t)__shfl_sync(0xffffffffu, h, 2);
-  if (__shfl_sync(0xffffffffu, h, 5) == kDict) {
-    // table entries t and 32 + t held by lane t; an index byte selects one by two shuffles
-    const int d = __shfl_sync(0xffffffffu, h, 6);
-    const int32_t t0 = lane < d ? ldm(col + cb + lane, keep) : 0;
-    const int32_t t1 = lane + 32 < d ? ldm(col + cb + 32 + lane, keep) : 0;
-    const uint32_t* iw = reinterpret_cast<const uint32_t*>(col + cb + dict_t4(d)) + lane;
-    const int32_t i = (int32_t)(s * 32 + lane);
-    double sum = 0.0;
-    for (int k = 0; k < w; k += 8) {
-      uint32_t wd[2];
-      double vi[8];
-      wd[0] = (uint32_t)ldm(reinterpret_cast<const int32_t*>(iw + 32 * (k >> 2)), keep);
-      wd[1] = (k + 4 < w) ? (uint32_t)ldm(reinterpret_cast<const int32_t*>(iw + 32 * ((k >> 2) + 1)), keep) : 0u;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) vi[j] = (k + j < w) ? ldm(v + 32 * j, keep) : 0.0;
-      double xv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t bsel = (wd[j >> 2] >> (8 * (j & 3))) & 0xffu;
-        const int32_t o0 = __shfl_sync(0xffffffffu, t0, (int)(bsel & 31u));
-        const int32_t o1 = __shfl_sync(0xffffffffu, t1, (int)(bsel & 31u));
-        xv[j] = (k + j < w) ? ldx<CG>(x + (i + ((bsel & 32u) ? o1 : o0))) : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (k + j < w) sum = fma(vi[j], xv[j], sum);
-      v += 256;
-    }
-    return sum;
-  }
   const int32_t* c = col + cb + lane;
   double sum = 0.0;
   int k = 0;
@@ -268,12 +209,6 @@ __device__ __forceinline__ int64_t sell_col(const int32_t* __restrict__ hdr, con
     const int64_t c = i + col[cb + k];
     return ((uint64_t)c < (uint64_t)ncols) ? c : -1;
   }
-  if (kind == kDict) {
-    const int d = hdr[s * kHdr + 6];
-    const uint8_t* ib = reinterpret_cast<const uint8_t*>(col + cb + dict_t4(d));
-    const int b = ib[4 * (32 * (int64_t)(k >> 2) + (i & 31)) + (k & 3)];
-    return i + col[cb + b];
-  }
   return col[cb + 32 * (int64_t)k + (i & 31)];
 }
 
@@ -302,7 +237,6 @@ __device__ __forceinline__ double rg_row_sum(const int32_t* __restrict__ col, co
 
 struct RowKArgs {
   int keep_matrix;  // 1: matrix small enough to stay in L2 across the level's launches (evict_last)
-  int dinv_fly;     // sell_tma sweeps on all-DIA matrices: 1/M_ii from the row's values, no dinv stream
   const int64_t* ptr;
   const int64_t* cptr;
   const int32_t* hdr;
@@ -324,7 +258,6 @@ struct RowKArgs {
   unsigned int* ticket;
   double* red_out;
   int red_stride;
-  FusedExchange ex;
 };
 
 template <RowOp OP>
@@ -332,77 +265,6 @@ struct NRed {
   static constexpr int value =
       (OP == RowOp::SpmvDot || OP == RowOp::SweepDot) ? 1 : (OP == RowOp::ResidDot2 ? 2 : 0);
 };
-
-// ----------------------------------------------------- fused halo exchange
-constexpr int kMaxExRanks = 64;
-static __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-static __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Prologue of a row kernel whose input x is halo-exchanged (see FusedExchange).
-// Must be reached by every thread of every CTA before x's halo is read.
-__device__ __forceinline__ void fused_exchange(const FusedExchange& e, const double* __restrict__ x) {
-  __shared__ uint64_t tgt[kMaxExRanks];
-  __shared__ bool last;
-  if (threadIdx.x < e.R) tgt[threadIdx.x] = e.gen[e.R + threadIdx.x] + 1;  // this exchange's generation
-  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e.nsend; k += nthr) {
-    int p = 0;
-    while (k >= e.soff[p + 1]) ++p;
-    e.dst[p][k - e.soff[p]] = x[e.send_idx[k]];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    last = (atomicAdd(e.ticket, 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (e.mode == 1) {
-      // the signalling CTA alone polls the peers, then releases the others on the GPU
-      const uint64_t goal = __ldcg(e.go) + 1;  // read before this CTA's ticket (program order)
-      if (last) {
-        __threadfence_system();
-        for (int q = 0; q < e.R; ++q)
-          if (e.nbr[q]) st_release_sys(e.pflag[q], ++e.gen[q]);
-        for (int q = 0; q < e.R; ++q)
-          if (e.nbr[q]) e.gen[e.R + q] = tgt[q];
-        *e.ticket = 0u;
-        for (int q = 0; q < e.R; ++q)
-          if (e.nbr[q])
-            while (ld_acquire_sys(e.myflag + q) < tgt[q]) {
-            }
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(e.go), "l"(goal) : "memory");
-      } else {
-        uint64_t v;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(e.go) : "memory");
-          if (v >= goal) break;
-          __nanosleep(64);
-        }
-      }
-    } else {
-      if (last) {
-        __threadfence_system();
-        for (int q = 0; q < e.R; ++q)
-          if (e.nbr[q]) st_release_sys(e.pflag[q], ++e.gen[q]);
-        for (int q = 0; q < e.R; ++q)
-          if (e.nbr[q]) e.gen[e.R + q] = tgt[q];
-        *e.ticket = 0u;
-      }
-      for (int q = 0; q < e.R; ++q)
-        if (e.nbr[q])
-          while (ld_acquire_sys(e.myflag + q) < tgt[q]) {
-          }
-    }
-  }
-  __syncthreads();
-}
 
 // Fused epilogue of row i with row sum `sum`, split in two: the row's vector
 // operands are loaded by epi_load BEFORE the row sum (so they travel with the
@@ -466,10 +328,6 @@ __device__ __forceinline__ void epilogue(const RowKArgs& a, int64_t i, double su
 // less per slice)
 template <RowOp OP>
 __device__ __forceinline__ void sell_body(const RowKArgs& a) {
-  pdl_enter();
-#ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x);
-#endif
   constexpr int NR = NRed<OP>::value;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -500,17 +358,12 @@ __device__ __forceinline__ void sell_body(const RowKArgs& a) {
     s = sn;
     h = hn;
   }
-  pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
 // row groups: one warp per unit of 32/G rows, G lanes per row, fixed shuffle tree
 template <RowOp OP, int G>
 __device__ __forceinline__ void rg_body(const RowKArgs& a) {
-  pdl_enter();
-#ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x);
-#endif
   constexpr int NR = NRed<OP>::value;
   constexpr int RU = 32 / G;
   const int lane = threadIdx.x & 31;
@@ -532,7 +385,6 @@ __device__ __forceinline__ void rg_body(const RowKArgs& a) {
     for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, G);
     if (sub == 0 && i < a.n_rows) epilogue<OP>(a, i, sum, acc);
   }
-  pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
@@ -682,7 +534,6 @@ struct EpiVecs {  // which row vectors the epilogue reads: b, dinv, x(own), y
 
 template <RowOp OP>
 __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchunks, int64_t n_slices) {
-  pdl_enter();
   constexpr int NR = NRed<OP>::value;
   using EV = EpiVecs<OP>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -698,9 +549,6 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-#ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x);
-#endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     // ---------------- producer (one lane)
@@ -732,7 +580,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const uint32_t vbytes = (uint32_t)(vb1 - vb0) * 8;
         const uint32_t cbytes = (uint32_t)(cb1 - cb0) * 4;
         const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
-        const uint32_t nvec = (EV::B ? 1 : 0) + ((EV::D_SELL && !a.dinv_fly) ? 1 : 0) +
+        const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) +
                               ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0);
         mbar_expect_tx(&full[st], hb + vbytes + cbytes + nvec * rbytes);
         bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol_keep);
@@ -741,8 +589,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
         if (rbytes) {
           if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol_stream);
-          if constexpr (EV::D_SELL)
-            if (!a.dinv_fly) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
+          if constexpr (EV::D_SELL) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
           if constexpr (EV::X || EV::XPRE) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
           if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
         }
@@ -792,29 +639,11 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
 #pragma unroll
         for (int j = 0; j < kTmaMaxW; ++j)
           if (j < w) sum = fma(v[32 * j], xv[j], sum);
-        double dfly = 0.0;
-        if constexpr (EV::D) {
-          if (a.dinv_fly) {
-            // l1 diagonal M_ii = a_ii + sum_{j != i} |a_ij| from the slice in
-            // shared memory, same order as l1_dinv_kernel; __drcp_rn is the correctly
-            // rounded 1/M_ii, i.e. bit-identical to the stored dinv
-            const int j0 = __shfl_sync(0xffffffffu, h, 14);
-            double aii = 0.0, off = 0.0;
-#pragma unroll
-            for (int j = 0; j < kTmaMaxW; ++j)
-              if (j < w) {
-                const double vj = v[32 * j];
-                if (j == j0) aii = vj;
-                else off += fabs(vj);
-              }
-            dfly = __drcp_rn(aii + off);
-          }
-        }
         if ((int64_t)i < a.n_rows) {
           const int rl = warp * 32 + lane;
           EpiIn e{0.0, 0.0, 0.0};
           if constexpr (EV::B) e.b = vec[rl];
-          if constexpr (EV::D) e.d = a.dinv_fly ? dfly : vec[kTmaRows + rl];
+          if constexpr (EV::D) e.d = vec[kTmaRows + rl];
           if constexpr (EV::X) e.x = vec[2 * kTmaRows + rl];
           if (readY) e.x = vec[2 * kTmaRows + rl];
           epi_store<OP>(a, (int64_t)i, sum, e, acc);
@@ -824,168 +653,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
-  pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
-}
-
-// k-blocked variant for slices wider than kTmaMaxW (level-1 A_1, R_0, P_1, A_2
-// of 256^3): a chunk of 8 slices is streamed in blocks of 8 columns, one stage
-// per block (values / columns of block kb of each slice are contiguous in the
-// column-major slice); consumer warps carry their row sums across the blocks
-// and run the epilogue after the chunk's last block.  Headers and epilogue
-// vectors travel with block 0.  The producer warp's lanes handle one slice each.
-template <RowOp OP>
-__global__ void __launch_bounds__(kTmaThreads) sell_tmak(RowKArgs a, int64_t nchunks, int64_t n_slices) {
-  pdl_enter();
-  constexpr int NR = NRed<OP>::value;
-  using EV = EpiVecs<OP>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaStageBytes);
-  uint64_t* empty = full + kTmaStages;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool readY = EV::Y && !(OP == RowOp::Spmv && a.beta == 0.0);
-  const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) + ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0);
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < kTmaStages; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], kTmaSlices);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-#ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x);
-#endif
-  double acc[NR > 0 ? NR : 1] = {};
-  if (warp == kTmaSlices) {
-    // ---------------- producer warp: lane j issues the copies of slice j
-    uint64_t pol_stream, pol_keep;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
-    const uint64_t pol_mat = a.keep_matrix ? pol_keep : pol_stream;
-    int64_t it = 0;
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-      const int64_t s0 = c * kTmaSlices;
-      const int nsl = (int)min((int64_t)kTmaSlices, n_slices - s0);
-      int64_t vb = 0, cb = 0;
-      int w = 0, dia = 0;
-      if (lane < nsl) {
-        const int32_t* h = a.hdr + (s0 + lane) * kHdr;
-        vb = ((int64_t)(uint32_t)__ldg(h + 1) << 32) | (uint32_t)__ldg(h + 0);
-        cb = ((int64_t)(uint32_t)__ldg(h + 3) << 32) | (uint32_t)__ldg(h + 2);
-        w = __ldg(h + 4);
-        dia = __ldg(h + 5);
-      }
-      int wmax = w;
-      for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-      const int nkb = max(1, (wmax + kTmaMaxW - 1) / kTmaMaxW);
-      const int64_t r0 = s0 * 32, r1 = min((s0 + nsl) * 32, a.n_rows);
-      const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int st = (int)(it % kTmaStages);
-        if (lane == 0 && it >= kTmaStages) mbar_wait(&empty[st], (uint32_t)((it / kTmaStages - 1) & 1));
-        __syncwarp();
-        const int cnt = (lane < nsl) ? min(max(w - kb * kTmaMaxW, 0), kTmaMaxW) : 0;
-        const uint32_t vbytes = (uint32_t)cnt * 256u;
-        const uint32_t cbytes = dia ? 0u : (uint32_t)cnt * 128u;
-        uint32_t tot = vbytes + cbytes;
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if (kb == 0) tot += (uint32_t)nsl * kHdr * 4 + nvec * rbytes;
-        if (lane == 0) mbar_expect_tx(&full[st], tot);
-        __syncwarp();
-        unsigned char* base = smem + st * kTmaStageBytes;
-        if (kb == 0 && lane == 0) {
-          bulk_g2s(base, a.hdr + s0 * kHdr, (uint32_t)nsl * kHdr * 4, &full[st], pol_keep);
-          unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
-          if (rbytes) {
-            if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol_stream);
-            if constexpr (EV::D_SELL) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
-            if constexpr (EV::X || EV::XPRE) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
-            if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
-          }
-        }
-        if (vbytes)
-          bulk_g2s(base + kTmaHdrBytes + lane * (kTmaMaxW * 256), a.val + vb + (int64_t)kb * kTmaMaxW * 32, vbytes,
-                   &full[st], pol_mat);
-        if (cbytes)
-          bulk_g2s(base + kTmaHdrBytes + kTmaValBytes + lane * (kTmaMaxW * 128),
-                   a.col + cb + (int64_t)kb * kTmaMaxW * 32, cbytes, &full[st], pol_mat);
-      }
-    }
-  } else {
-    // ---------------- consumers: warp `warp` takes slice s0 + warp
-    const uint32_t nc = (uint32_t)a.ncols;
-    int64_t it = 0;
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-      const int64_t s0 = c * kTmaSlices;
-      const int nsl = (int)min((int64_t)kTmaSlices, n_slices - s0);
-      const bool mine = warp < nsl;
-      const uint32_t i = (uint32_t)((s0 + warp) * 32 + lane);
-      const bool live = mine && (int64_t)i < a.n_rows;
-      int32_t h = 0;
-      int w = 0, nkb = 1;
-      bool dia = false;
-      EpiIn e{0.0, 0.0, 0.0};
-      double sum = 0.0;
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int st = (int)(it % kTmaStages);
-        mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
-        const unsigned char* base = smem + st * kTmaStageBytes;
-        if (kb == 0) {
-          const int32_t* hs = reinterpret_cast<const int32_t*>(base);
-          h = (mine && lane < kHdr) ? hs[warp * kHdr + lane] : 0;
-          w = __shfl_sync(0xffffffffu, h, 4);
-          dia = __shfl_sync(0xffffffffu, h, 5) == 1;
-          int wm = lane < nsl ? hs[lane * kHdr + 4] : 0;
-          for (int o = 16; o > 0; o >>= 1) wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-          nkb = max(1, (wm + kTmaMaxW - 1) / kTmaMaxW);
-          if (live) {
-            const double* vec = reinterpret_cast<const double*>(base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes);
-            const int rl = warp * 32 + lane;
-            if constexpr (EV::B) e.b = vec[rl];
-            if constexpr (EV::D) e.d = vec[kTmaRows + rl];
-            if constexpr (EV::X) e.x = vec[2 * kTmaRows + rl];
-            if (readY) e.x = vec[2 * kTmaRows + rl];
-          }
-        }
-        const int cnt = mine ? min(max(w - kb * kTmaMaxW, 0), kTmaMaxW) : 0;
-        if (cnt > 0) {
-          const double* v = reinterpret_cast<const double*>(base + kTmaHdrBytes) + warp * (kTmaMaxW * 32) + lane;
-          const int32_t* cc =
-              reinterpret_cast<const int32_t*>(base + kTmaHdrBytes + kTmaValBytes) + warp * (kTmaMaxW * 32) + lane;
-          double xv[kTmaMaxW];
-          if (dia) {
-#pragma unroll
-            for (int j = 0; j < kTmaMaxW; ++j) {
-              const uint32_t cj = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
-              xv[j] = (j < cnt) ? __ldg(a.x + (cj < nc ? cj : 0u)) : 0.0;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < kTmaMaxW; ++j) xv[j] = (j < cnt) ? __ldg(a.x + cc[32 * j]) : 0.0;
-          }
-#pragma unroll
-          for (int j = 0; j < kTmaMaxW; ++j)
-            if (j < cnt) sum = fma(v[32 * j], xv[j], sum);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-      }
-      if (live) epi_store<OP>(a, (int64_t)i, sum, e, acc);
-    }
-  }
-  pdl_exit();
-  if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
-}
-
-template <RowOp OP>
-static void tmak_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    PSC_CUDA(cudaFuncSetAttribute(sell_tmak<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
-    attr = true;
-  }
-  launch_k(sell_tmak<OP>, grid, kTmaThreads, kTmaSmem, s, a, nchunks, n_slices);
 }
 
 template <RowOp OP>
@@ -996,428 +664,6 @@ static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_s
     attr = true;
   }
   launch_k(sell_tma<OP>, grid, kTmaThreads, kTmaSmem, s, a, nchunks, n_slices);
-}
-
-// ------------------------------------------ wavefront multi-stage pass (sell_wave)
-// Several consecutive row-wise stages of one V-cycle level over the same square
-// matrix A without halo columns — [x = M^-1 b,] k l1-Jacobi sweeps[, r = b - A x]
-// — in ONE persistent launch, so that A, b and 1/M stream from HBM once per pass
-// and are re-read from L2 by the later stages.  Every stage does exactly the row
-// arithmetic of the separate kernels (same FMA order), so the results are
-// bit-identical to launching the stages one by one.
-//
-// Work item = (stage s, chunk k of 8 slices = 256 rows).  A row of chunk k reads
-// x only in chunks k-h .. k+h (h from the matrix bandwidth), so stage s may
-// process chunk k once stage s-1 has completed chunks k-h .. k+h.  With two
-// ping-pong x buffers the same window also orders the write of x^(s) over
-// x^(s-2) after the last stage-(s-1) reads of it (exactly those items read
-// chunk k).  Completion is counted per block of kWaveBlk chunks (every consumer
-// warp fences its stores, then bumps its block's counter); a waiting warp
-// acquire-polls the blocks covering its window, one block per lane — no serial
-// chain (a prefix watermark advanced chunk by chunk costs an atomic round trip
-// per chunk: 95 ms per pass at 256^3).  Items are dealt round-robin in the order
-// of the key k + G s with G >= h + kWaveBlk + slack, so every dependency of an
-// item (whole blocks, i.e. chunks up to k + h + kWaveBlk - 1 of stage s-1) was
-// dealt earlier; every CTA handles its items in that order and all CTAs are
-// co-resident, so the earliest unfinished item can always run.  Vectors written
-// inside the pass are read through L2 (ld.global.cg): L1 is not coherent across SMs.
-// Completion counters are polled with relaxed gpu-scope loads: ld.acquire.gpu
-// compiles to an L1 invalidation (CCTL.IVALL) per load — measured as the top
-// stall of the pass (25% of samples), wiping every warp's L1 lines.  The data
-// guarded by a counter is only ever read through L2 (ld.global.cg) by loads
-// that are control-dependent on the observed count, and the writer fenced its
-// stores to gpu scope before bumping it — the flag protocol of decoupled
-// look-back scans.
-__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// release RMW, cumulative: it also publishes the stores other threads ordered
-// before it through a CTA barrier or a CTA-scope release
-__device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Whole warp: wait until stage s-1 has completed every block up to `b1`.
-// *front = this warp's verified prefix of complete blocks of that stage (shared
-// memory, per warp and stage; counters only grow within a pass): most items find
-// it already far enough; otherwise one bulk check of the next 64 blocks (2 per
-// lane, ballot) advances it.
-__device__ __forceinline__ bool wave_block_done(const unsigned int* cnt, int64_t b, int64_t nblk, int64_t nchunks) {
-  if (b >= nblk) return true;
-  const unsigned int need = (unsigned int)(kTmaSlices * min((int64_t)kWaveBlk, nchunks - b * kWaveBlk));
-  return ld_acquire_u32(cnt + b) >= need;
-}
-
-__device__ __forceinline__ void wave_wait(const unsigned int* cnt, unsigned int* front, int64_t b1, int64_t nchunks,
-                                          int64_t nblk, int lane) {
-  int64_t f = *(volatile unsigned int*)front;
-  if (f > b1) return;
-  const long long t0 = clock64();
-  while (f <= b1) {
-    const unsigned int m0 = __ballot_sync(0xffffffffu, wave_block_done(cnt, f + lane, nblk, nchunks));
-    const unsigned int m1 = __ballot_sync(0xffffffffu, wave_block_done(cnt, f + 32 + lane, nblk, nchunks));
-    const int p = (m0 != 0xffffffffu) ? __ffs(~m0) - 1 : (m1 != 0xffffffffu ? 32 + __ffs(~m1) - 1 : 64);
-    f += p;
-    if (f <= b1 && p == 0) {
-      __nanosleep(64);
-      if (clock64() - t0 > (1ll << 34)) __trap();  // ~9 s: a broken schedule fails loudly instead of hanging
-    }
-  }
-  __syncwarp();
-  if (lane == 0) *(volatile unsigned int*)front = (unsigned int)f;
-  __syncwarp();
-}
-
-// Items are super-chunks of kWaveItem chunks (2048 rows): the dependency check
-// and the publication (a gpu-scope fence, ~2 us under load) are paid once per
-// ~8 us of streaming instead of per chunk (with 256-row items the pass was
-// dependency-bound: ~4 failed polls per item, 2.2-2.4 ms per 4-stage pass).
-constexpr int kWaveItem = 8;
-static_assert(kWaveBlk % kWaveItem == 0, "items must not straddle completion blocks");
-
-__device__ __forceinline__ void wave_item(const WaveArgs& a, int64_t m, int& s, int64_t& q) {
-  const int64_t K = m / a.nst;
-  s = (int)(m - K * a.nst);
-  q = K - a.G * s;  // item index: chunks [kWaveItem q, kWaveItem (q + 1))
-}
-
-__device__ __forceinline__ int64_t wave_nitems(const WaveArgs& a) { return (a.nchunks + kWaveItem - 1) / kWaveItem; }
-
-// the last completion block stage s-1 must have finished before item q of stage s
-__device__ __forceinline__ int64_t wave_dep_block(const WaveArgs& a, int64_t q) {
-  return min(kWaveItem * q + kWaveItem - 1 + a.h, a.nchunks - 1) / kWaveBlk;
-}
-
-constexpr int kWaveLag = 8;  // consumers run at most this many items ahead of the publisher
-
-// One lane per CTA publishes its items in order: it waits until the 8 consumer
-// warps have counted item `it` in done[it % kWaveLag] (monotone, +8 per use: no
-// phase aliasing; CTA-scope release by the consumers), then ONE gpu-scope fence
-// and the block-counter bump (8 warps x the item's chunks).
-__device__ __forceinline__ void wave_publisher(const WaveArgs& a, int64_t total, const unsigned int* done,
-                                               volatile unsigned int* published) {
-  const int64_t nit = wave_nitems(a);
-  int64_t it = 0;
-  for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
-    int s;
-    int64_t q;
-    wave_item(a, m, s, q);
-    if (q < 0 || q >= nit) continue;
-    const unsigned int need = (unsigned int)kTmaSlices * (unsigned int)(it / kWaveLag + 1);
-    while (*(volatile const unsigned int*)(done + (it % kWaveLag)) < need) {
-    }
-    const int64_t c0 = kWaveItem * q, nc = min((int64_t)kWaveItem, a.nchunks - c0);
-    __threadfence();  // the consumers' stores of the item -> gpu scope
-    atomicAdd(a.flags + (int64_t)s * a.nblk + c0 / kWaveBlk, (unsigned int)(kTmaSlices * nc));
-    *published = (unsigned int)(++it);
-  }
-}
-
-// warps 0-7 consume, warp 8 (one lane) produces the TMA ring (chunk by chunk),
-// warp 9 (one lane) publishes items.
-constexpr int kWaveThreads = (kTmaSlices + 2) * 32;
-constexpr int kWaveSmem =
-    kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8 + (kWaveLag + 2) * 4 + kTmaSlices * kWaveMaxStages * 4;
-
-__global__ void __launch_bounds__(kWaveThreads) sell_wave(WaveArgs a) {
-  pdl_enter();
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaStageBytes);
-  uint64_t* empty = full + kTmaStages;
-  unsigned int* done = reinterpret_cast<unsigned int*>(empty + kTmaStages);  // [kWaveLag]
-  volatile unsigned int* published = done + kWaveLag;                         // items published so far
-  unsigned int* fronts = done + kWaveLag + 2;                                  // [8 warps][stages]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < kTmaStages; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], kTmaSlices);
-    }
-    for (int j = 0; j < kWaveLag; ++j) done[j] = 0;
-    for (int j = 0; j < kTmaSlices * kWaveMaxStages; ++j) fronts[j] = 0;
-    *published = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const int64_t nit = wave_nitems(a);
-  const int64_t total = (int64_t)a.nst * (nit + a.G * (a.nst - 1));
-  double acc[1] = {0.0};
-  if (warp == kTmaSlices + 1) {
-    if (lane == 0) wave_publisher(a, total, done, published);
-  } else if (warp == kTmaSlices) {
-    // ---------------- producer (one lane): matrix slices, b, 1/M of every chunk
-    if (lane == 0) {
-      uint64_t pol_stream, pol_keep;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
-      int64_t it = 0;  // chunks produced
-      for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
-        int s;
-        int64_t q;
-        wave_item(a, m, s, q);
-        if (q < 0 || q >= nit) continue;
-        const int op = a.op[s];
-        const uint64_t pol = (s + 1 < a.nst) ? pol_keep : pol_stream;  // re-read by a later stage: keep
-        const int64_t c1 = min(kWaveItem * q + kWaveItem, a.nchunks);
-        int64_t nxt[4] = {0, 0, 0, 0};
-        if (op != (int)WaveOp::Scale) {
-          const int64_t s0 = kWaveItem * q * kTmaSlices;
-          nxt[0] = a.ptr[s0];
-          nxt[2] = a.cptr[s0];
-        }
-        for (int64_t k = kWaveItem * q; k < c1; ++k, ++it) {
-          const int64_t s0 = k * kTmaSlices, s1 = min(s0 + kTmaSlices, a.n_slices);
-          int64_t vb0 = nxt[0], cb0 = nxt[2];
-          if (op != (int)WaveOp::Scale) {  // this chunk's end = the next chunk's start
-            nxt[0] = a.ptr[s1];
-            nxt[2] = a.cptr[s1];
-          }
-          const int st = (int)(it % kTmaStages);
-          if (it >= kTmaStages) mbar_wait(&empty[st], (uint32_t)((it / kTmaStages - 1) & 1));
-          unsigned char* base = smem + st * kTmaStageBytes;
-          const int64_t r0 = s0 * 32, r1 = min(s1 * 32, a.n_rows);
-          uint32_t hb = 0, vbytes = 0, cbytes = 0;
-          if (op != (int)WaveOp::Scale) {
-            hb = (uint32_t)(s1 - s0) * kHdr * 4;
-            vbytes = (uint32_t)(nxt[0] - vb0) * 8;
-            cbytes = (uint32_t)(nxt[2] - cb0) * 4;
-          }
-          const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
-          const bool needd = (op != (int)WaveOp::Resid);
-          mbar_expect_tx(&full[st], hb + vbytes + cbytes + rbytes * (needd ? 2u : 1u));
-          if (hb) bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol);
-          if (vbytes) bulk_g2s(base + kTmaHdrBytes, a.val + vb0, vbytes, &full[st], pol);
-          if (cbytes) bulk_g2s(base + kTmaHdrBytes + kTmaValBytes, a.col + cb0, cbytes, &full[st], pol);
-          unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
-          if (rbytes) {
-            bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol);
-            if (needd) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol);
-          }
-        }
-      }
-    }
-  } else {
-    // ---------------- consumers: warp `warp` takes slice 8k + warp of every chunk k
-    const uint32_t nc = (uint32_t)a.ncols;
-    int64_t it = 0, ii = 0;  // chunks consumed, items consumed
-    for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
-      int s;
-      int64_t q;
-      wave_item(a, m, s, q);
-      if (q < 0 || q >= nit) continue;
-      const int op = a.op[s];
-      // at most kWaveLag items ahead of the publisher (its done counters are reused)
-      if (ii >= kWaveLag)
-        while (*published + kWaveLag <= (unsigned int)ii) {
-        }
-      if (s > 0)
-        wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, fronts + warp * kWaveMaxStages + (s - 1), wave_dep_block(a, q),
-                  a.nchunks, a.nblk, lane);
-      const double* xin = a.xin[s];
-      double* xout = a.xout[s];
-      const bool fresh = (s > 0);  // x produced inside this pass: read through L2
-      const bool sweep = (op == (int)WaveOp::Sweep || op == (int)WaveOp::SweepDot);
-      const int64_t c1 = min(kWaveItem * q + kWaveItem, a.nchunks);
-      for (int64_t k = kWaveItem * q; k < c1; ++k, ++it) {
-        const int st = (int)(it % kTmaStages);
-        const int64_t sl = k * kTmaSlices + warp;
-        const uint32_t i = (uint32_t)(sl * 32 + lane);
-        const uint32_t ic = (int64_t)i < a.n_rows ? i : 0u;
-        // the row's own x, issued before the gathers
-        const double xi = (sweep && sl < a.n_slices) ? (fresh ? __ldcg(xin + ic) : __ldg(xin + ic)) : 0.0;
-        mbar_wait(&full[st], (uint32_t)((it / kTmaStages) & 1));
-        const unsigned char* base = smem + st * kTmaStageBytes;
-        const double* vec = reinterpret_cast<const double*>(base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes);
-        if (sl < a.n_slices) {
-          const int rl = warp * 32 + lane;
-          double sum = 0.0;
-          if (op != (int)WaveOp::Scale) {
-            const int32_t* hs = reinterpret_cast<const int32_t*>(base);
-            const double* vs = reinterpret_cast<const double*>(base + kTmaHdrBytes);
-            const int32_t* cs = reinterpret_cast<const int32_t*>(base + kTmaHdrBytes + kTmaValBytes);
-            const int32_t h = lane < kHdr ? hs[warp * kHdr + lane] : 0;
-            const int32_t h0 = hs[0], h1 = hs[1], h2 = hs[2], h3 = hs[3];
-            const int64_t vbase = ((int64_t)(uint32_t)h1 << 32) | (uint32_t)h0;
-            const int64_t cbase = ((int64_t)(uint32_t)h3 << 32) | (uint32_t)h2;
-            const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
-                               (uint32_t)__shfl_sync(0xffffffffu, h, 0);
-            const int w = __shfl_sync(0xffffffffu, h, 4);
-            const bool dia = __shfl_sync(0xffffffffu, h, 5) == 1;
-            const double* v = vs + (vb - vbase) + lane;
-            double xv[kTmaMaxW];
-            if (dia) {
-#pragma unroll
-              for (int j = 0; j < kTmaMaxW; ++j) {
-                const uint32_t cj = i + (uint32_t)__shfl_sync(0xffffffffu, h, 6 + j);
-                const double* px = xin + (cj < nc ? cj : 0u);
-                xv[j] = (j < w) ? (fresh ? __ldcg(px) : __ldg(px)) : 0.0;
-              }
-            } else {
-              const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
-                                 (uint32_t)__shfl_sync(0xffffffffu, h, 2);
-              const int32_t* cc = cs + (cb - cbase) + lane;
-#pragma unroll
-              for (int j = 0; j < kTmaMaxW; ++j) {
-                const double* px = xin + (j < w ? cc[32 * j] : 0);
-                xv[j] = (j < w) ? (fresh ? __ldcg(px) : __ldg(px)) : 0.0;
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < kTmaMaxW; ++j)
-              if (j < w) sum = fma(v[32 * j], xv[j], sum);
-          }
-          if ((int64_t)i < a.n_rows) {
-            const double bi = vec[rl];
-            if (op == (int)WaveOp::Scale) {
-              xout[i] = vec[kTmaRows + rl] * bi;
-            } else if (op == (int)WaveOp::Resid) {
-              xout[i] = bi - sum;
-            } else {
-              const double xn = xi + vec[kTmaRows + rl] * (bi - sum);
-              xout[i] = xn;
-              if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-      }
-      if (lane == 0) {
-        __threadfence_block();  // this warp's stores of the item before its count (CTA-scope release)
-        atomicAdd(done + (ii % kWaveLag), 1u);
-      }
-      ++ii;
-    }
-  }
-  pdl_exit();
-  if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
-}
-
-// Direct-load form of the wavefront pass for slices of any width (A_1, A_2):
-// no TMA ring, 8 consumer warps (warp w takes slice 8k + w of every chunk of an
-// item, streamed with the batched loads of sell_row_sum) + a publisher warp.
-constexpr int kWaveDirectThreads = (kTmaSlices + 1) * 32;
-
-__global__ void __launch_bounds__(kWaveDirectThreads, 2) sell_wave_direct(WaveArgs a) {
-  pdl_enter();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ unsigned int fronts[kTmaSlices * kWaveMaxStages];
-  __shared__ unsigned int done[kWaveLag];
-  __shared__ unsigned int published_s;
-  volatile unsigned int* published = &published_s;
-  if (threadIdx.x < kTmaSlices * kWaveMaxStages) fronts[threadIdx.x] = 0;
-  if (threadIdx.x < kWaveLag) done[threadIdx.x] = 0;
-  if (threadIdx.x == 0) published_s = 0;
-  __syncthreads();
-  const int64_t nit = wave_nitems(a);
-  const int64_t total = (int64_t)a.nst * (nit + a.G * (a.nst - 1));
-  double acc[1] = {0.0};
-  if (warp == kTmaSlices) {
-    if (lane == 0) wave_publisher(a, total, done, published);
-  } else {
-    int64_t ii = 0;
-    for (int64_t m = blockIdx.x; m < total; m += gridDim.x) {
-      int s;
-      int64_t q;
-      wave_item(a, m, s, q);
-      if (q < 0 || q >= nit) continue;
-      if (ii >= kWaveLag)
-        while (*published + kWaveLag <= (unsigned int)ii) {
-        }
-      const int op = a.op[s];
-      const bool keep = (s + 1 < a.nst);  // a later stage re-reads the slice: normal caching, else stream
-      if (s > 0)
-        wave_wait(a.flags + (int64_t)(s - 1) * a.nblk, fronts + warp * kWaveMaxStages + (s - 1), wave_dep_block(a, q),
-                  a.nchunks, a.nblk, lane);
-      const double* xin = a.xin[s];
-      double* xout = a.xout[s];
-      const bool sweep = (op == (int)WaveOp::Sweep || op == (int)WaveOp::SweepDot);
-      const int64_t c1 = min(kWaveItem * q + kWaveItem, a.nchunks);
-      for (int64_t k = kWaveItem * q; k < c1; ++k) {
-        const int64_t sl = k * kTmaSlices + warp;
-        if (sl >= a.n_slices) continue;
-        const int32_t h = (op != (int)WaveOp::Scale) ? load_hdr(a.hdr, sl, lane) : 0;
-        const int64_t i = sl * 32 + lane;
-        const int64_t ic = i < a.n_rows ? i : 0;
-        const double bi = ldm(a.b + ic, keep);
-        const double di = (op != (int)WaveOp::Resid) ? ldm(a.dinv + ic, keep) : 0.0;
-        const double xi = sweep ? ((s > 0) ? __ldcg(xin + ic) : __ldg(xin + ic)) : 0.0;
-        double sum = 0.0;
-        if (op != (int)WaveOp::Scale)
-          sum = (s > 0) ? sell_row_sum<true>(h, sl, lane, a.col, a.val, xin, a.ncols, keep)
-                        : sell_row_sum<false>(h, sl, lane, a.col, a.val, xin, a.ncols, keep);
-        if (i < a.n_rows) {
-          if (op == (int)WaveOp::Scale) {
-            xout[i] = di * bi;
-          } else if (op == (int)WaveOp::Resid) {
-            xout[i] = bi - sum;
-          } else {
-            const double xn = xi + di * (bi - sum);
-            xout[i] = xn;
-            if (op == (int)WaveOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : bi) * xn;
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();  // this warp's stores before its count (CTA-scope release)
-        atomicAdd(done + (ii % kWaveLag), 1u);
-      }
-      ++ii;
-    }
-  }
-  pdl_exit();
-  if (a.reduce) grid_reduce<1>(acc, a.partials, a.ticket, a.red_out, 1);
-}
-
-bool wave_supported(const Sell& A) {
-  return A.lanes == 1 && A.hdr && A.n_units > 0 && A.n_cols_local == A.n_rows;
-}
-
-static bool wave_tma(const Sell& A) { return A.max_width <= kTmaMaxW && !env_int("PSC_WAVE_DIRECT", 0); }
-
-int64_t wave_chunks(const Sell& A) { return (A.n_units + kTmaSlices - 1) / kTmaSlices; }
-
-void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& in, cudaStream_t s) {
-  static int occ = -1, occ_d = -1;
-  if (occ < 0) {
-    PSC_CUDA(cudaFuncSetAttribute(sell_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, kWaveSmem));
-    PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sell_wave, kWaveThreads, kWaveSmem));
-    PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, sell_wave_direct, kWaveDirectThreads, 0));
-  }
-  const bool tma = wave_tma(A);
-  const int o = tma ? occ : occ_d;
-  PSC_REQUIRE(o >= 1, PSC_ERR_STATE, "sell_wave cannot be resident");
-  WaveArgs a = in;
-  a.ptr = A.ptr;
-  a.cptr = A.cptr;
-  a.hdr = A.hdr;
-  a.col = A.col;
-  a.val = A.val;
-  a.ncols = A.n_cols_local;
-  a.n_rows = A.n_rows;
-  a.n_slices = A.n_units;
-  a.nchunks = wave_chunks(A);
-  a.nblk = (a.nchunks + kWaveBlk - 1) / kWaveBlk;
-  // G (in items) must put every dependency of an item (whole blocks up to chunk
-  // 8q + 7 + h + kWaveBlk - 1 of the previous stage) at a smaller key
-  PSC_REQUIRE(a.G * kWaveItem >= a.h + kWaveBlk + kWaveItem, PSC_ERR_STATE,
-              "wave schedule: key skew below the dependency reach");
-  const int64_t total = (int64_t)a.nst * ((a.nchunks + kWaveItem - 1) / kWaveItem + a.G * (a.nst - 1));
-  // every CTA must be resident at once (items wait on other CTAs' items)
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)o * ctx->num_sms));
-  // round-robin dealing: a grid that is a multiple of the stage count would pin
-  // every CTA to one stage (only 1/nst of the CTAs streaming stage 0 from HBM)
-  while (grid > 1 && std::gcd(grid, a.nst) != 1) --grid;
-  PSC_REQUIRE(!a.reduce || grid <= a.red_grid, PSC_ERR_STATE, "reduction site too small");
-  PSC_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(unsigned int) * (size_t)a.nst * a.nblk, s));
-  if (tma) launch_k(sell_wave, grid, kWaveThreads, kWaveSmem, s, a);
-  else launch_k(sell_wave_direct, grid, kWaveDirectThreads, 0, s, a);
-  PSC_CUDA(cudaGetLastError());
-  ctx->launches++;
 }
 
 // ---------------------------------------------- TMA-staged row-group kernel
@@ -1438,7 +684,6 @@ constexpr int kRgSmem = kRgStages * kRgStageBytes + 2 * kRgStages * 8;
 
 template <RowOp OP, int G>
 __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunks) {
-  pdl_enter();
   constexpr int NR = NRed<OP>::value;
   constexpr int RU = 32 / G;
   constexpr int CR = kTmaSlices * RU;  // rows per chunk
@@ -1456,9 +701,6 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-#ifndef PSC_NO_FUSED_EX_CODE
-  if (a.ex.on) fused_exchange(a.ex, a.x);
-#endif
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     if (lane == 0) {
@@ -1554,7 +796,6 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
-  pdl_exit();
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
@@ -1581,15 +822,6 @@ static void rg_tma_dispatch(RowOp op, const RowKArgs& a, int grid, int64_t nchun
   }
 }
 
-// k-blocked TMA path: sliced ELL wider than the ring's 8 columns
-static bool tmak_ok(const Sell& A, const RowArgs& r, SliceSet set) {
-  // measured not faster than the header-prefetching plain kernel on the wide
-  // slices of 256^3 (A_1: 99 vs 93 us, R_0: 190 vs 178 us): opt-in (PSC_TMAK=1)
-  const int off = env_int("PSC_NO_TMA", 0) || !env_int("PSC_TMAK", 0);
-  return !off && A.lanes == 1 && A.max_width > kTmaMaxW && set == SliceSet::All && r.vec_padded && A.hdr &&
-         A.n_units > 0 && A.n_dict == 0;  // reads explicit int32 columns
-}
-
 static bool rg_tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
   const int off = env_int("PSC_NO_TMA", 0) || env_int("PSC_NO_RG_TMA", 0);
   return !off && A.lanes > 1 && A.max_chunk <= kRgCap && set == SliceSet::All && r.vec_padded && A.n_units > 0;
@@ -1607,10 +839,6 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   RowKArgs a;
   // matrices up to 48 MB stay in L2 (evict_last) across the 8-10 launches of their level
   a.keep_matrix = (A.padded * 12 + A.n_rows * 8) <= ((int64_t)env_int("PSC_KEEP_MB", 96) << 20) ? 1 : 0;
-  // on-the-fly 1/M_ii (no dinv stream) measured slower: 287 vs 242 us per level-0 sweep
-  // (FP64 reciprocal + |a_ij| sums in the consumer warps); opt-in PSC_DINV_FLY=1
-  a.dinv_fly = (A.all_dia_diag && (op == RowOp::Sweep || op == RowOp::SweepDot) && env_int("PSC_DINV_FLY", 0))
-                   ? 1 : 0;
   a.ptr = A.ptr;
   a.cptr = A.cptr;
   a.hdr = A.hdr;
@@ -1633,7 +861,6 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.ticket = r.red ? r.red->ticket : nullptr;
   a.red_out = r.red_out;
   a.red_stride = r.red_stride;
-  a.ex = r.ex;
   const bool needs_red = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
   if (tma_ok(A, r, set)) {
     const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
@@ -1647,23 +874,6 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
       case RowOp::Resid: tma_launch<RowOp::Resid>(a, grid, nchunks, A.n_units, s); break;
       case RowOp::ResidDot2: tma_launch<RowOp::ResidDot2>(a, grid, nchunks, A.n_units, s); break;
       case RowOp::PAdd: tma_launch<RowOp::PAdd>(a, grid, nchunks, A.n_units, s); break;
-    }
-    PSC_CUDA(cudaGetLastError());
-    ctx->launches++;
-    return;
-  }
-  if (tmak_ok(A, r, set)) {
-    const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
-    PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
-    switch (op) {
-      case RowOp::Spmv: tmak_launch<RowOp::Spmv>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::SpmvDot: tmak_launch<RowOp::SpmvDot>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::Sweep: tmak_launch<RowOp::Sweep>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::SweepDot: tmak_launch<RowOp::SweepDot>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::Resid: tmak_launch<RowOp::Resid>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::ResidDot2: tmak_launch<RowOp::ResidDot2>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::PAdd: tmak_launch<RowOp::PAdd>(a, grid, nchunks, A.n_units, s); break;
     }
     PSC_CUDA(cudaGetLastError());
     ctx->launches++;
@@ -1703,11 +913,9 @@ __device__ __forceinline__ double2 ld2(const double* p, int64_t j) { return rein
 __device__ __forceinline__ void st2(double* p, int64_t j, double2 v) { reinterpret_cast<double2*>(p)[j] = v; }
 
 __global__ void __launch_bounds__(kBlock) scale_kernel(int64_t n, const double* __restrict__ dinv,
-                                                       const double* __restrict__ b, double* __restrict__ x) {
-  pdl_enter();  // (16-byte form measured 57 vs 56 us: kept scalar)
+                                                       const double* __restrict__ b, double* __restrict__ x) {  // (16-byte form measured 57 vs 56 us: kept scalar)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = dinv[i] * b[i];
-  pdl_exit();
 }
 
 static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -1773,9 +981,7 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
                                                            const double* __restrict__ p, double* __restrict__ r,
                                                            const double* __restrict__ q, const double* g_pq,
                                                            const double* g_num, int num_ranks, int nranks,
-                                                           double* partials, unsigned int* ticket, double* out,
-                                                           const double* __restrict__ dinv, double* __restrict__ z0) {
-  pdl_enter();
+                                                           double* partials, unsigned int* ticket, double* out) {
   const double alpha = gsum(g_num, num_ranks) / gsum(g_pq, nranks);
   double acc[1] = {0.0};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
@@ -1788,10 +994,6 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
     rv.y = rv.y - alpha * qv.y;
     st2(x, j, xv);
     st2(r, j, rv);
-    if (z0) {  // first level-0 sweep of the next V-cycle, from zero
-      const double2 d = ld2(dinv, j);
-      st2(z0, j, make_double2(d.x * rv.x, d.y * rv.y));
-    }
     acc[0] += rv.x * rv.x;
     acc[0] += rv.y * rv.y;
   }
@@ -1800,21 +1002,19 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
     x[i] = x[i] + alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
-    if (z0) z0[i] = dinv[i] * ri;
     acc[0] += ri * ri;
   }
-  pdl_exit();
   grid_reduce<1>(acc, partials, ticket, out, 1);
 }
 
 void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
                       const double* g_pq, const double* g_num, int num_ranks, int nranks, const RedSite* red,
-                      double* red_out, cudaStream_t s, const double* dinv, double* z0) {
-  PSC_REQUIRE(al16(x) && al16(p) && al16(r) && al16(q) && al16(dinv) && al16(z0), PSC_ERR_STATE,
+                      double* red_out, cudaStream_t s) {
+  PSC_REQUIRE(al16(x) && al16(p) && al16(r) && al16(q), PSC_ERR_STATE,
               "vector kernels need 16-byte aligned buffers");
   const int g = std::min(vec_grid(ctx, n), red->grid);
   launch_k(cg_update_kernel, g, kBlock, 0, s, n, x, p, r, q, g_pq, g_num, num_ranks, nranks, red->partials,
-           red->ticket, red_out, dinv, z0);
+           red->ticket, red_out);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -1826,7 +1026,6 @@ __global__ void __launch_bounds__(kBlock) fcg_dir_kernel(int64_t n, const double
                                                          double* __restrict__ p, const double* __restrict__ r,
                                                          const double* g_zq, const double* g_pq, int nranks,
                                                          double* partials, unsigned int* ticket, double* out) {
-  pdl_enter();
   const double beta = gsum(g_zq, nranks) / gsum(g_pq, nranks);
   double acc[1] = {0.0};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
@@ -1844,7 +1043,6 @@ __global__ void __launch_bounds__(kBlock) fcg_dir_kernel(int64_t n, const double
     p[n - 1] = pi;
     acc[0] += pi * r[n - 1];
   }
-  pdl_exit();
   grid_reduce<1>(acc, partials, ticket, out, 1);
 }
 
@@ -1870,7 +1068,6 @@ __global__ void __launch_bounds__(kBlock) cpcg_init_kernel(int64_t n, const doub
                                                            double* __restrict__ r, double* __restrict__ z,
                                                            double* __restrict__ p, int* done, double* partials,
                                                            unsigned int* ticket, double* out, int stride) {
-  pdl_enter();
   if (blockIdx.x == 0 && threadIdx.x == 0) *done = 0;
   double acc[2] = {0.0, 0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1883,7 +1080,6 @@ __global__ void __launch_bounds__(kBlock) cpcg_init_kernel(int64_t n, const doub
     acc[0] += bi * zi;
     acc[1] += bi * bi;
   }
-  pdl_exit();
   grid_reduce<2>(acc, partials, ticket, out, stride);
 }
 
@@ -1893,7 +1089,6 @@ __global__ void __launch_bounds__(kBlock) cpcg_update_kernel(int64_t n, double* 
                                                              const double* __restrict__ dinv, const double* g_pq,
                                                              const double* g_rz, int nr, int* done, double* partials,
                                                              unsigned int* ticket, double* out, int stride) {
-  pdl_enter();
   if (ld_flag(done)) return;
   const double pq = gsum(g_pq, nr);
   if (!(pq > 0.0)) {  // breakdown (or b = 0): keep x
@@ -1911,7 +1106,6 @@ __global__ void __launch_bounds__(kBlock) cpcg_update_kernel(int64_t n, double* 
     acc[0] += ri * ri;
     acc[1] += ri * zi;
   }
-  pdl_exit();
   grid_reduce<2>(acc, partials, ticket, out, stride);
 }
 
@@ -1919,7 +1113,6 @@ __global__ void __launch_bounds__(kBlock) cpcg_dir_kernel(int64_t n, const doubl
                                                           double* __restrict__ p, const double* g_rr,
                                                           const double* g_bb, const double* g_rzn, const double* g_rz,
                                                           int nr, double tol, int* done) {
-  pdl_enter();
   if (ld_flag(done)) return;
   if (sqrt(gsum(g_rr, nr)) <= tol * sqrt(gsum(g_bb, nr))) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *done = 1;
@@ -1928,7 +1121,6 @@ __global__ void __launch_bounds__(kBlock) cpcg_dir_kernel(int64_t n, const doubl
   const double beta = gsum(g_rzn, nr) / gsum(g_rz, nr);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
-  pdl_exit();
 }
 
 void launch_cpcg_init(psc_ctx* ctx, int64_t n, const double* b, const double* dinv, double* x, double* r, double* z,
@@ -1959,13 +1151,11 @@ void launch_cpcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const 
 __global__ void __launch_bounds__(kBlock) xpby_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ p,
                                                       const double* g_rz, double* rz_old, int nranks,
                                                       unsigned int* ticket) {
-  pdl_enter();
   const double rz = gsum(g_rz, nranks);
   const double beta = rz / __ldcg(rz_old);
   // (16-byte form measured 66 vs 62 us: kept scalar; cg_update gains from it: 121 vs 164 us)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
-  pdl_exit();
   // rz_old := rz once every CTA has read the old value
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1989,11 +1179,9 @@ void launch_xpby(psc_ctx* ctx, int64_t n, const double* z, double* p, const doub
 __global__ void __launch_bounds__(kBlock) dot_kernel(int64_t n, const double* __restrict__ a,
                                                      const double* __restrict__ b, double* partials,
                                                      unsigned int* ticket, double* out) {
-  pdl_enter();
   double acc[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     acc[0] += a[i] * b[i];
-  pdl_exit();
   grid_reduce<1>(acc, partials, ticket, out, 1);
 }
 
@@ -2007,10 +1195,8 @@ void launch_dot(psc_ctx* ctx, int64_t n, const double* a, const double* b, const
 
 __global__ void pack_kernel(int64_t n, const int32_t* __restrict__ idx, const double* __restrict__ x,
                             double* __restrict__ out) {
-  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = x[idx[i]];
-  pdl_exit();
 }
 
 void launch_pack(psc_ctx* ctx, int64_t n, const int32_t* idx, const double* x, double* sendbuf, cudaStream_t s) {
@@ -2022,10 +1208,8 @@ void launch_pack(psc_ctx* ctx, int64_t n, const int32_t* idx, const double* x, d
 
 __global__ void gather_kernel(int64_t n, const int64_t* __restrict__ map, const double* __restrict__ in,
                               double* __restrict__ out) {
-  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = in[map[i]];
-  pdl_exit();
 }
 
 void launch_gather(psc_ctx* ctx, int64_t n, const int64_t* map, const double* in, double* out, cudaStream_t s) {
@@ -2062,7 +1246,6 @@ struct CoarseArgs {
 
 template <bool SELL, bool STAGE>
 __global__ void __launch_bounds__(kCoarseThreads) coarse_solve(CoarseArgs a) {
-  pdl_enter();
   extern __shared__ double sm[];
   const int64_t n = a.n;
   double* xa = sm;
@@ -2126,7 +1309,6 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve(CoarseArgs a) {
     xb = t;
   }
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a.xout[i] = xa[i];
-  pdl_exit();
 }
 
 template <bool SELL, bool STAGE>
@@ -2217,7 +1399,6 @@ __global__ void __launch_bounds__(kDenseWarps * 32, 1) coarse_dense(const double
                                                                   const double* __restrict__ dinv,
                                                                   const double* __restrict__ b,
                                                                   double* __restrict__ xout, int nsweeps, int gk_unused) {
-  pdl_enter();
   __shared__ double xs[2][32 * kCC];
   __shared__ double bs[32 * kCC], ds[32 * kCC];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -2259,7 +1440,6 @@ __global__ void __launch_bounds__(kDenseWarps * 32, 1) coarse_dense(const double
     cur ^= 1;
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xs[cur][i];
-  pdl_exit();
 }
 
 void launch_coarse_dense(psc_ctx* ctx, const double* Ad, int64_t n, const double* dinv, const double* b, double* x,
@@ -2288,7 +1468,6 @@ __global__ void __launch_bounds__(kDenseWarps * 32, 1) coarse_dense_pcg(const do
                                                                       const double* __restrict__ b,
                                                                       double* __restrict__ xout, int maxit,
                                                                       double tol) {
-  pdl_enter();
   constexpr int V = 32 * kCC;
   __shared__ double ps[V], qs[V], xs[V], rs[V], ds[V];
   __shared__ int stop_s;
@@ -2384,7 +1563,6 @@ __global__ void __launch_bounds__(kDenseWarps * 32, 1) coarse_dense_pcg(const do
     __syncthreads();
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xs[i];
-  pdl_exit();
 }
 
 void launch_coarse_dense_pcg(psc_ctx* ctx, const double* Ad, int64_t n, const double* dinv, const double* b,
@@ -2398,49 +1576,12 @@ void launch_coarse_dense_pcg(psc_ctx* ctx, const double* Ad, int64_t n, const do
 // Row bandwidth of a square matrix in the sliced-ELL layout: max |j - i| over
 // the stored entries (DIA slices: their offsets; ELL padding repeats a real
 // column of the row, an empty row pads with column 0 — conservative).
-__global__ void sell_bw_kernel(const int32_t* __restrict__ hdr, const int64_t* __restrict__ ptr,
-                               const int64_t* __restrict__ cptr, const int32_t* __restrict__ col, int64_t n_rows,
-                               int64_t n_slices, unsigned long long* out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_slices * 32) return;
-  const int64_t sl = i >> 5;
-  const int w = (int)((ptr[sl + 1] - ptr[sl]) >> 5);
-  const int64_t cb = cptr[sl];
-  const int kind = hdr[sl * kHdr + 5];
-  unsigned long long m = 0;
-  if (kind != kEll) {  // DIA offsets / DICT table
-    const int nt = kind == kDia ? w : hdr[sl * kHdr + 6];
-    if ((i & 31) == 0)
-      for (int k = 0; k < nt; ++k) m = max(m, (unsigned long long)llabs((long long)col[cb + k]));
-  } else if (i < n_rows) {
-    for (int k = 0; k < w; ++k) m = max(m, (unsigned long long)llabs((long long)col[cb + 32 * (int64_t)k + (i & 31)] - i));
-  }
-  if (m) atomicMax(out, m);
-}
-
-int64_t sell_bandwidth(psc_ctx* ctx, const Sell& A, cudaStream_t s) {
-  PSC_REQUIRE(A.lanes == 1, PSC_ERR_STATE, "bandwidth: sliced ELL only");
-  if (A.n_units == 0) return 0;
-  unsigned long long* d = dalloc<unsigned long long>(1);
-  PSC_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
-  const int64_t nt = A.n_units * 32;
-  sell_bw_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(A.hdr, A.ptr, A.cptr, A.col, A.n_rows, A.n_units, d);
-  PSC_CUDA(cudaGetLastError());
-  ctx->launches++;
-  unsigned long long hbw = 0;
-  PSC_CUDA(cudaMemcpyAsync(&hbw, d, sizeof(hbw), cudaMemcpyDeviceToHost, s));
-  PSC_CUDA(cudaStreamSynchronize(s));
-  dfree(d);
-  return (int64_t)hbw;
-}
-
 // -------------------------------------------------- dense suffix operator
 // y = D b for a dense row-major n x n operator (the V-cycle of the deepest
 // levels precomputed as a matrix, hier.cu): one warp per row, b staged in
 // shared memory, four accumulators over column blocks (fixed order), xor tree.
 __global__ void __launch_bounds__(256) dense_gemv_kernel(const double* __restrict__ D, int64_t n,
                                                          const double* __restrict__ b, double* __restrict__ y) {
-  pdl_enter();
   extern __shared__ double bs[];
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) bs[i] = b[i];
   __syncthreads();
@@ -2462,7 +1603,6 @@ __global__ void __launch_bounds__(256) dense_gemv_kernel(const double* __restric
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane == 0) y[row] = sum;
   }
-  pdl_exit();
 }
 
 int64_t dense_gemv_max_rows() { return 6144; }  // b in 48 KB of shared memory
@@ -2510,9 +1650,9 @@ __device__ __forceinline__ int32_t map_col(int64_t g, int64_t own_begin, int64_t
 // (8 B x 32 d value slots beat 12 B x 32 w value+column slots).
 __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_t* __restrict__ rowptr,
                                   const int64_t* __restrict__ colg, int64_t own_begin, int64_t n_own, int allow_dia,
-                                  int allow_dict, int64_t* __restrict__ vslots, int64_t* __restrict__ cslots,
+                                  int64_t* __restrict__ vslots, int64_t* __restrict__ cslots,
                                   int64_t* __restrict__ snnz, int32_t* __restrict__ bflag, int32_t* __restrict__ dia_d,
-                                  int32_t* __restrict__ dia_off, int32_t* __restrict__ dict_d) {
+                                  int32_t* __restrict__ dia_off) {
   const int lane = threadIdx.x & 31;
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= n_slices) return;
@@ -2553,34 +1693,13 @@ __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_
     }
     if (!ok || 2 * d > 3 * w) d = 0;
   }
-  // DICT: wide slice of owned columns with at most kMaxDict distinct offsets j - i
-  // (sorted, by the same merge of the rows' sorted offsets)
-  int dd = 0;
-  if (d == 0 && allow_dict && !off && w > kTmaMaxW) {
-    int q = 0, t = 0;
-    bool ok = true;
-    for (;;) {
-      const long long my = (q < len) ? (long long)(colg[b + q] - own_begin - i) : LLONG_MAX;
-      long long mn = my;
-      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      if (mn == LLONG_MAX) break;
-      if (t == kMaxDict) {
-        ok = false;
-        break;
-      }
-      ++t;
-      if (my == mn) ++q;
-    }
-    if (ok) dd = t;
-  }
   if (lane == 0) {
     vslots[s] = 32 * (int64_t)(d ? d : w);
-    // DIA: offsets, padded to 16 B; DICT: table + byte indices; ELL: int32 columns
-    cslots[s] = d ? (int64_t)((d + 3) & ~3) : (dd ? (int64_t)((dd + 3) & ~3) + 32 * (int64_t)((w + 3) / 4) : 32 * (int64_t)w);
+    // DIA: offsets, padded to 16 B; ELL: int32 columns
+    cslots[s] = d ? (int64_t)((d + 3) & ~3) : 32 * (int64_t)w;
     snnz[s] = tot;
     bflag[s] = off;
     dia_d[s] = d;
-    dict_d[s] = dd;
   }
 }
 
@@ -2590,7 +1709,7 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
                                  const int64_t* __restrict__ colg, const double* __restrict__ valcsr,
                                  const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
                                  const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
-                                 const int32_t* __restrict__ dict_d, int64_t own_begin, int64_t n_own,
+                                 int64_t own_begin, int64_t n_own,
                                  const int64_t* __restrict__ halo, int64_t nh, int32_t* __restrict__ col,
                                  double* __restrict__ val, int* err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2620,46 +1739,6 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
     if (lane == 0)
       for (int j = d; j < ((d + 3) & ~3); ++j) col[cb + j] = 0;
     if (q != e) *err = 2;
-    return;
-  }
-  const int dd = dict_d[s];
-  if (dd > 0) {  // DICT slice (warp = slice): table of sorted distinct offsets, byte indices
-    int32_t* tbl = col + cb;
-    uint32_t* iw = reinterpret_cast<uint32_t*>(col + cb + ((dd + 3) & ~3));
-    const int len = (int)(e - b);
-    int q = 0, t = 0, lastb = 0;
-    uint32_t word = 0;
-    for (;;) {
-      const long long my = (q < len) ? (long long)(colg[b + q] - own_begin - i) : LLONG_MAX;
-      long long mn = my;
-      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      if (mn == LLONG_MAX) break;
-      if (lane == 0 && t < dd) tbl[t] = (int32_t)mn;
-      if (my == mn) {
-        word |= (uint32_t)t << (8 * (q & 3));
-        val[vb + 32 * (int64_t)q + lane] = valcsr[b + q];
-        lastb = t;
-        if ((q & 3) == 3) {
-          iw[32 * (int64_t)(q >> 2) + lane] = word;
-          word = 0;
-        }
-        ++q;
-      }
-      ++t;
-    }
-    for (; q < 4 * ((w + 3) / 4); ++q) {  // padding: repeat the last column with value 0
-      if (q < w) {
-        word |= (uint32_t)lastb << (8 * (q & 3));
-        val[vb + 32 * (int64_t)q + lane] = 0.0;
-      }
-      if ((q & 3) == 3) {
-        iw[32 * (int64_t)(q >> 2) + lane] = word;
-        word = 0;
-      }
-    }
-    if (lane == 0)
-      for (int j = dd; j < ((dd + 3) & ~3); ++j) tbl[j] = 0;
-    if (t != dd) *err = 2;
     return;
   }
   int32_t last = 0;
@@ -2731,7 +1810,7 @@ int choose_lanes(int64_t n_rows, int64_t nnz) {
 
 __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
                                 const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
-                                const int32_t* __restrict__ dict_d, int32_t* __restrict__ hdr, int* all_dia_diag) {
+                                int32_t* __restrict__ hdr) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_slices) return;
   int32_t* h = hdr + s * kHdr;
@@ -2741,17 +1820,15 @@ __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ pt
   h[2] = (int32_t)(uint32_t)(cb & 0xffffffffu);
   h[3] = (int32_t)(uint32_t)((uint64_t)cb >> 32);
   h[4] = (int32_t)((ptr[s + 1] - vb) >> 5);
-  const int d = dia_d[s], dd = dict_d[s];
-  h[5] = d > 0 ? kDia : (dd > 0 ? kDict : kEll);
+  const int d = dia_d[s];
+  h[5] = d > 0 ? kDia : kEll;
   int j0 = -1;
   for (int j = 0; j < kMaxDia; ++j) {
     h[6 + j] = j < d ? dia_off[s * kMaxDia + j] : 0;
     if (j < d && dia_off[s * kMaxDia + j] == 0) j0 = j;
   }
-  if (dd > 0) h[6] = dd;
   h[14] = j0;  // DIA: slot of the diagonal (offset 0), -1 if none
   h[15] = 0;
-  if (j0 < 0) atomicAnd(all_dia_diag, 0);
 }
 
 void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg, const double* d_val,
@@ -2772,7 +1849,6 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
   std::vector<int32_t> flag;      // per unit (sell) or per row (row groups)
   std::vector<int64_t> hp;        // ptr on the host
   std::vector<int32_t> hdia;      // DIA widths per slice
-  std::vector<int32_t> hdict;     // DICT table sizes per slice
   std::vector<int64_t> hsnnz;     // nnz per slice
   size_t tmp_bytes = 0;
   if (sell) {
@@ -2782,17 +1858,12 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     int32_t* d_flag = dalloc<int32_t>(nu);
     int32_t* d_diad = dalloc<int32_t>(nu);
     int32_t* d_diaoff = dalloc<int32_t>((size_t)nu * kMaxDia);
-    int32_t* d_dictd = dalloc<int32_t>(nu);
-    // DICT slices cut A_1's bytes by 25% but its sweeps are latency-bound: measured
-    // 189 vs 152 us per level-1 sweep at 256^3 (the shuffle decode lengthens the
-    // gather chain); opt-in PSC_DICT=1
-    const bool allow_dict = env_int("PSC_DICT", 0) != 0;
     PSC_CUDA(cudaMemsetAsync(d_vs, 0, sizeof(int64_t) * (nu + 1), s));
     PSC_CUDA(cudaMemsetAsync(d_cs, 0, sizeof(int64_t) * (nu + 1), s));
     if (nu > 0) {
       sell_width_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
-          n_rows, nu, d_rowptr, d_colg, own_begin, n_own, allow_dia ? 1 : 0, allow_dict ? 1 : 0, d_vs, d_cs, d_snnz,
-          d_flag, d_diad, d_diaoff, d_dictd);
+          n_rows, nu, d_rowptr, d_colg, own_begin, n_own, allow_dia ? 1 : 0, d_vs, d_cs, d_snnz,
+          d_flag, d_diad, d_diaoff);
       PSC_CUDA(cudaGetLastError());
     }
     S.ptr = dalloc<int64_t>(nu + 1);
@@ -2812,28 +1883,17 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     S.hdr = dalloc<int32_t>((size_t)nu * kHdr);
     if (nu > 0) {
       sell_fill_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
-          n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, d_dictd, own_begin, n_own, d_halo,
+          n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, own_begin, n_own, d_halo,
           n_halo, S.col, S.val, d_err);
       PSC_CUDA(cudaGetLastError());
-      int* d_all = dalloc<int>(1);
-      const int one = 1;
-      PSC_CUDA(cudaMemcpyAsync(d_all, &one, sizeof(int), cudaMemcpyHostToDevice, s));
-      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, d_dictd, S.hdr,
-                                                                   d_all);
+      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, S.hdr);
       PSC_CUDA(cudaGetLastError());
-      int h_all = 0;
-      PSC_CUDA(cudaMemcpyAsync(&h_all, d_all, sizeof(int), cudaMemcpyDeviceToHost, s));
-      PSC_CUDA(cudaStreamSynchronize(s));
-      dfree(d_all);
-      S.all_dia_diag = (h_all != 0);
     }
     flag.resize(nu);
     hp.resize(nu + 1);
     hdia.resize(nu);
     hsnnz.resize(nu);
-    hdict.resize(nu);
     if (nu) {
-      PSC_CUDA(cudaMemcpyAsync(hdict.data(), d_dictd, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
       PSC_CUDA(cudaMemcpyAsync(flag.data(), d_flag, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
       PSC_CUDA(cudaMemcpyAsync(hdia.data(), d_diad, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
       PSC_CUDA(cudaMemcpyAsync(hsnnz.data(), d_snnz, sizeof(int64_t) * nu, cudaMemcpyDeviceToHost, s));
@@ -2844,7 +1904,6 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     dfree(d_flag);
     dfree(d_diad);
     dfree(d_diaoff);
-    dfree(d_dictd);
   } else {
     int64_t* d_len = dalloc<int64_t>(nptr);
     int32_t* d_flag = dalloc<int32_t>(n_rows);
@@ -2883,7 +1942,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
   PSC_CUDA(cudaStreamSynchronize(s));
   dfree(d_err);
   PSC_REQUIRE(h_err == 0, PSC_ERR_STATE,
-              h_err == 2 ? "DIA/DICT slice fill mismatch" : "column not in the owned block nor in the assembled halo");
+              h_err == 2 ? "DIA slice fill mismatch" : "column not in the owned block nor in the assembled halo");
   std::vector<int32_t> in, bd;
   S.nnz_ell = sell ? 0 : nnz;
   for (int64_t u = 0; u < nu; ++u) {
@@ -2892,7 +1951,6 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
       f = flag[u];
       S.max_width = std::max<int>(S.max_width, (int)((hp[u + 1] - hp[u]) / 32));
       if (hdia[u]) S.n_dia++;
-      else if (hdict[u]) S.n_dict++;
       else S.nnz_ell += hsnnz[u];
     } else {
       for (int64_t i = u * RU; i < std::min<int64_t>(n_rows, (u + 1) * RU); ++i) {

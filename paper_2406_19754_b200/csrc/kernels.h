@@ -19,31 +19,6 @@ enum class RowOp {
   PAdd,       // y += s                         (prolongation x_l += P x_{l+1})
 };
 
-// Halo exchange fused into the prologue of the row kernel that consumes the
-// exchanged vector (NVLink peer stores through CUDA IPC mappings, see p2p.cu):
-// every CTA stores its share of x[send_idx] into the neighbours' halo slots,
-// the last CTA (ticket) signals each neighbour with a per-pair generation
-// counter (st.release.sys), then every CTA waits for the neighbours' counters
-// (ld.acquire.sys) before the main loop reads halo values.  Row-kernel grids
-// are persistent (all CTAs resident), so waiting CTAs cannot starve a pusher.
-struct FusedExchange {
-  int on = 0;
-  int R = 0;
-  int64_t nsend = 0;
-  const int32_t* send_idx = nullptr;  // local owned indices, grouped by peer
-  const int64_t* soff = nullptr;      // [R+1]
-  double* const* dst = nullptr;       // [R] peer p's halo slots for this rank
-  const int32_t* nbr = nullptr;       // [R] exchange partners at this level
-  uint64_t* const* pflag = nullptr;   // [R] &flags_p[me]
-  const uint64_t* myflag = nullptr;   // [R]
-  uint64_t* gen = nullptr;            // [2R] sgen, rgen
-  unsigned int* ticket = nullptr;
-  // mode 1: only the signalling CTA polls the peers' flags (system scope) and then
-  // publishes the exchange's generation in `go` (GPU scope) for the other CTAs
-  int mode = 1;
-  uint64_t* go = nullptr;
-};
-
 struct RowArgs {
   double alpha = 1.0, beta = 0.0;
   const double* x = nullptr;
@@ -59,7 +34,6 @@ struct RowArgs {
   // all row vectors (b, dinv, x, y) are library buffers padded past n (TMA bulk
   // copies of the last chunk may read up to 8 bytes beyond the last row)
   bool vec_padded = false;
-  FusedExchange ex;  // halo exchange of x done by this kernel's prologue (ex.on)
 };
 
 // Which slices: all, interior only (no halo column), boundary only.
@@ -76,10 +50,9 @@ void launch_l1_dinv(psc_ctx* ctx, const Sell& A, double* dinv, cudaStream_t s);
 // gathered scalars: value of slot = sum over ranks of g[slot*nranks + r], in rank order
 // CG: alpha = num / pq ; x += alpha p ; r -= alpha q ; red(r.r)
 // num = sum of g_num[0..num_ranks-1] (PCG: rz_old, 1 entry; FCG: gathered (p, r))
-// (optionally z0 = dinv .* r: the first level-0 sweep of the next V-cycle)
 void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
                       const double* g_pq, const double* g_num, int num_ranks, int nranks, const RedSite* red,
-                      double* red_out, cudaStream_t s, const double* dinv = nullptr, double* z0 = nullptr);
+                      double* red_out, cudaStream_t s);
 // FCG(1) direction: beta = (z, q_old) / (p_old, q_old) (both gathered); p = z - beta p; red(p.r)
 void launch_fcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* r, const double* g_zq,
                     const double* g_pq, int nranks, const RedSite* red, double* red_out, cudaStream_t s);
@@ -123,51 +96,6 @@ void launch_cpcg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, dou
                         const RedSite* red, double* out, int stride, cudaStream_t s);
 void launch_cpcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rr, const double* g_bb,
                      const double* g_rzn, const double* g_rz, int nr, double tol, int* done, cudaStream_t s);
-
-// Wavefront multi-stage pass (sell_wave, kernels.cu): up to kWaveMaxStages
-// row-wise stages of one level over a square, halo-free, TMA-able matrix in one
-// persistent launch (A streamed from HBM once, re-read from L2 by later stages).
-enum class WaveOp : int {
-  Scale = 0,     // xout = dinv .* b          (first sweep from x = 0; no matrix)
-  Sweep = 1,     // xout = xin + dinv (b - A xin)
-  SweepDot = 2,  // Sweep; red += w_i xout_i (w = b if null)
-  Resid = 3,     // xout = b - A xin
-};
-constexpr int kWaveMaxStages = 6;
-constexpr int kWaveBlk = 16;  // chunks per completion counter
-struct WaveArgs {
-  // matrix (filled by launch_wave)
-  const int64_t* ptr = nullptr;
-  const int64_t* cptr = nullptr;
-  const int32_t* hdr = nullptr;
-  const int32_t* col = nullptr;
-  const double* val = nullptr;
-  int64_t ncols = 0, n_rows = 0, n_slices = 0, nchunks = 0;
-  // stages
-  const double* b = nullptr;
-  const double* dinv = nullptr;
-  const double* w = nullptr;  // SweepDot weight
-  int nst = 0;
-  int op[kWaveMaxStages] = {};
-  const double* xin[kWaveMaxStages] = {};
-  double* xout[kWaveMaxStages] = {};
-  // schedule: dependency reach h (chunks), key skew G (in items of kWaveItem = 8 chunks)
-  int64_t h = 0, G = 1;
-  unsigned int* flags = nullptr;  // per stage: nblk block counters (8 warp arrivals per chunk)
-  int64_t nblk = 0;
-  // SweepDot reduction
-  int reduce = 0;
-  double* partials = nullptr;
-  unsigned int* ticket = nullptr;
-  double* red_out = nullptr;
-  int red_grid = 0;
-};
-bool wave_supported(const Sell& A);
-int64_t wave_chunks(const Sell& A);   // 256-row chunks
-constexpr int64_t kWaveChunkRows = 256;
-int64_t sell_bandwidth(psc_ctx* ctx, const Sell& A, cudaStream_t s);  // max |j - i| (sliced ELL)
-// flags must hold kWaveMaxStages * ceil(wave_chunks(A) / kWaveBlk) counters; requires G >= h + kWaveBlk
-void launch_wave(psc_ctx* ctx, const Sell& A, const WaveArgs& a, cudaStream_t s);
 
 // y = D b, D dense row-major n x n (n <= dense_gemv_max_rows()); out = in^T (n x n)
 int64_t dense_gemv_max_rows();

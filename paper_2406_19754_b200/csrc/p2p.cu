@@ -41,8 +41,14 @@ struct PushArgs {
   uint64_t* gen;          // [2R] sgen[p], rgen[p]
   unsigned int* ticket;
   int R;
-  int dbg;  // timing experiments (PSC_DEBUG_EX): 1 gpu fence, 2 relaxed flags + one fence, 4 no wait
+  uint64_t timeout_ns;  // bound of the wait for a peer's flag (then __trap: a launch error, not a hang)
 };
+
+static __device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
   const int p = blockIdx.y;
@@ -56,35 +62,24 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (!(a.dbg & 1)) __threadfence_system();
-    else __threadfence();
+    __threadfence_system();
     const unsigned int t = atomicAdd(a.ticket, 1u);
     last = (t == gridDim.x * gridDim.y - 1);
   }
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
-  if (!(a.dbg & 1)) __threadfence_system();
+  __threadfence_system();
   for (int q = 0; q < a.R; ++q)
-    if (a.nbr[q]) {
-      if (a.dbg & 2) {
-        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(a.pflag[q]), "l"(++a.gen[q]) : "memory");
-      } else {
-        st_release_sys(a.pflag[q], ++a.gen[q]);
-      }
-    }
+    if (a.nbr[q]) st_release_sys(a.pflag[q], ++a.gen[q]);
+  const uint64_t t0 = globaltimer();
   for (int q = 0; q < a.R; ++q)
     if (a.nbr[q]) {
       const uint64_t target = ++a.gen[a.R + q];
-      if (a.dbg & 4) continue;  // timing only: do not wait
-      if (a.dbg & 2) {
-        uint64_t v;
-        do {
-          asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.myflag + q) : "memory");
-        } while (v < target);
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-      } else {
-        while (ld_acquire_sys(a.myflag + q) < target) {
-        }
+      while (ld_acquire_sys(a.myflag + q) < target) {
+        // a peer that never signals (crashed, or left the collective order) must not
+        // hang this GPU: after timeout_ns the kernel traps and the host call returns
+        // PSC_ERR_CUDA (the library then aborts the NCCL communicator)
+        if (globaltimer() - t0 > a.timeout_ns) __trap();
       }
     }
   __threadfence();
@@ -93,8 +88,10 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
 
 static void push(psc_ctx* ctx, P2P& P, const double* x, const int32_t* idx, const int64_t* soff, int64_t n,
                  int64_t max_per_peer, double* const* dst, const int32_t* nbr, cudaStream_t s) {
-  static const int dbg = getenv("PSC_DEBUG_EX") ? atoi(getenv("PSC_DEBUG_EX")) : 0;
-  PushArgs a{x, idx, soff, n, dst, nbr, P.d_pflag, P.flags, P.d_gen, P.d_ticket, ctx->nranks, dbg};
+  // PSC_SPIN_TIMEOUT_S: seconds a rank waits for a neighbour's flag (default 30)
+  static const uint64_t tmo =
+      (uint64_t)(1e9 * (getenv("PSC_SPIN_TIMEOUT_S") ? atof(getenv("PSC_SPIN_TIMEOUT_S")) : 30.0));
+  PushArgs a{x, idx, soff, n, dst, nbr, P.d_pflag, P.flags, P.d_gen, P.d_ticket, ctx->nranks, tmo};
   const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((max_per_peer + 255) / 256, 64));
   p2p_push_kernel<<<dim3((unsigned)bx, (unsigned)ctx->nranks), 256, 0, s>>>(a);
   PSC_CUDA(cudaGetLastError());
@@ -109,32 +106,6 @@ bool p2p_halo(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, cudaStream_t s
   const P2PLevel& L = P.levels[it->second.level];
   if (!L.any) return true;  // no neighbour at this level: nothing to exchange
   push(ctx, P, x, d->d_send_idx, L.d_soff, 0, L.max_send, it->second.d_dst, L.d_nbr, s);
-  return true;
-}
-
-bool p2p_fused(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, FusedExchange& ex) {
-  if (!P.on) return false;
-  auto it = P.bufs.find(x);
-  if (it == P.bufs.end()) return false;
-  const P2PLevel& L = P.levels[it->second.level];
-  ex = FusedExchange();
-  if (!L.any) return true;
-  PSC_REQUIRE(ctx->nranks <= 64, PSC_ERR_STATE, "fused exchange supports at most 64 ranks");
-  ex.on = 1;
-  ex.R = ctx->nranks;
-  ex.nsend = d->n_send;
-  ex.send_idx = d->d_send_idx;
-  ex.soff = L.d_soff;
-  ex.dst = it->second.d_dst;
-  ex.nbr = L.d_nbr;
-  ex.pflag = P.d_pflag;
-  ex.myflag = P.flags;
-  ex.gen = P.d_gen;
-  ex.ticket = P.d_ticket2;
-  ex.go = P.d_go;
-  static const int mode = getenv("PSC_EX_MODE") ? atoi(getenv("PSC_EX_MODE")) : 1;
-  ex.mode = mode;
-  ctx->collectives++;
   return true;
 }
 
@@ -158,7 +129,7 @@ static void allgather_bytes(psc_ctx* ctx, const void* mine, void* all, size_t by
   dfree(d);
 }
 
-static int allreduce_min(psc_ctx* ctx, int v) {
+int allreduce_min(psc_ctx* ctx, int v) {
   int* d = dalloc<int>(1);
   PSC_CUDA(cudaMemcpy(d, &v, sizeof(int), cudaMemcpyHostToDevice));
   PSC_NCCL(ncclAllReduce(d, d, 1, ncclInt, ncclMin, ctx->comm, ctx->stream));
@@ -282,10 +253,6 @@ void p2p_setup(psc_ctx* ctx, P2P& P, const std::vector<P2PBufSpec>& halo_bufs,
   PSC_CUDA(cudaMemset(P.d_gen, 0, sizeof(uint64_t) * 2 * R));
   P.d_ticket = dalloc<unsigned int>(1);
   PSC_CUDA(cudaMemset(P.d_ticket, 0, sizeof(unsigned int)));
-  P.d_ticket2 = dalloc<unsigned int>(1);
-  PSC_CUDA(cudaMemset(P.d_ticket2, 0, sizeof(unsigned int)));
-  P.d_go = dalloc<uint64_t>(1);
-  PSC_CUDA(cudaMemset(P.d_go, 0, sizeof(uint64_t)));
   PSC_CUDA(cudaDeviceSynchronize());
   allreduce_min(ctx, 1);  // nobody signals before everybody is set up
   P.on = true;
@@ -304,8 +271,6 @@ void p2p_free(psc_ctx* ctx, P2P& P) {
   dfree(P.d_pflag);
   dfree(P.d_gen);
   dfree(P.d_ticket);
-  dfree(P.d_ticket2);
-  dfree(P.d_go);
   P = P2P();
 }
 

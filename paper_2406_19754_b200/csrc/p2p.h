@@ -34,8 +34,6 @@ struct P2P {
   uint64_t** d_pflag = nullptr;
   uint64_t* d_gen = nullptr;
   unsigned int* d_ticket = nullptr;
-  unsigned int* d_ticket2 = nullptr;  // fused exchanges (row-kernel prologues)
-  uint64_t* d_go = nullptr;           // fused exchanges: GPU-scope release word (mode 1)
   int32_t* d_all = nullptr;
   std::vector<P2PLevel> levels;
   std::map<const double*, P2PBufDev> bufs;
@@ -47,11 +45,10 @@ void p2p_setup(psc_ctx* ctx, P2P& P, const std::vector<P2PBufSpec>& halo_bufs,
                const std::vector<P2PGatherSpec>& gathers, const std::vector<psc_desc*>& level_desc,
                int64_t flags_off);
 void p2p_free(psc_ctx* ctx, P2P& P);
+// collective: the minimum of v over all ranks (NCCL all-reduce on ctx's stream)
+int allreduce_min(psc_ctx* ctx, int v);
 // false: not handled (caller falls back to NCCL)
 bool p2p_halo(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, cudaStream_t s);
-// Fill a row kernel's FusedExchange for the halo exchange of x (level buffer);
-// false: not handled (caller uses the standalone exchange).
-bool p2p_fused(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, FusedExchange& ex);
 bool p2p_allgather(psc_ctx* ctx, P2P& P, const double* src, int64_t n, const double* dst_base_local,
                    cudaStream_t s);
 

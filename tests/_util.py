@@ -77,3 +77,10 @@ def random_spd_mixed(n, density, seed):
     C = sp.random(n, n, density=density, random_state=rng, data_rvs=lambda m: rng.standard_normal(m))
     C = C + sp.eye(n)
     return (C.T @ C + 0.05 * sp.eye(n)).tocsr()
+
+
+def ew_err(a, ref):
+    """Element-wise error scaled by the reference's magnitude: max_i |a_i - ref_i| / max_i |ref_i|
+    (every component is held to the bound, unlike a relative 2-norm)."""
+    a, ref = np.asarray(a), np.asarray(ref)
+    return float(np.max(np.abs(a - ref)) / np.max(np.abs(ref)))

@@ -16,6 +16,7 @@ torch = pytest.importorskip("torch")
 
 import oracle  # noqa: E402
 import pscgen  # noqa: E402
+from _util import ew_err  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -127,7 +128,7 @@ def test_smoother_sweeps_every_level(psc, nsweeps):
         x = torch.zeros(n, dtype=torch.float64, device="cuda")
         H.smooth(l, dev(b), x, nsweeps)
         ref = oracle.l1_sweeps_from_zero(h.levels[l].A, b, nsweeps)
-        err = np.linalg.norm(host(x) - ref) / np.linalg.norm(ref)
+        err = ew_err(host(x), ref)
         assert err <= 1e-13 * nsweeps, (l, err)
 
 
@@ -142,7 +143,7 @@ def test_vcycle(psc, grid, kw):
         z = torch.zeros(n, dtype=torch.float64, device="cuda")
         H.vcycle(dev(r), z)
         ref = oracle.vcycle(h, r, opts.get("pre", 4), opts.get("post", 4), opts.get("coarse", 30))
-        err = np.linalg.norm(host(z) - ref) / np.linalg.norm(ref)
+        err = ew_err(host(z), ref)
         assert err <= 1e-12, err
 
 
@@ -244,22 +245,13 @@ def test_breakdown_is_reported(psc):
 VARIANTS = [
     {},
     {"PSC_NO_TMA": "1"},
-    {"PSC_TMAK": "1"},
     {"PSC_NO_FUSED_SCALE": "1"},
-    {"PSC_Z0_FUSED": "1"},
-    {"PSC_DINV_FLY": "1"},
-    {"PSC_FUSED_EXCHANGE": "1"},
     {"PSC_NO_DIA": "1"},
     {"PSC_NO_RG_TMA": "1", "PSC_NO_DENSE_COARSE": "1"},
     {"PSC_LANES": "1", "PSC_NO_DENSE_COARSE": "1"},
     {"PSC_LANES": "8"},
     {"PSC_LANES": "32", "PSC_NO_TMA": "1"},
     {"PSC_RG_MIN": "4", "PSC_RG_DIV": "1"},
-    {"PSC_DICT": "1"},
-    {"PSC_DICT": "1", "PSC_NO_TMA": "1", "PSC_NO_DENSE_COARSE": "1"},
-    {"PSC_WAVE": "1"},
-    {"PSC_WAVE": "1", "PSC_WAVE_DIRECT": "1"},
-    {"PSC_WAVE": "1", "PSC_WAVE_SLACK": "0", "PSC_NO_FUSED_SCALE": "1"},
 ]
 
 
@@ -279,11 +271,11 @@ def test_variants_pcg_parity(psc, env, grid, monkeypatch):
         z = torch.zeros(h.levels[l].n, dtype=torch.float64, device="cuda")
         H.smooth(l, dev(r), z, 5)
         ref = oracle.l1_sweeps_from_zero(h.levels[l].A, r, 5)
-        assert np.linalg.norm(host(z) - ref) / np.linalg.norm(ref) <= 1e-12
+        assert ew_err(host(z), ref) <= 1e-12
     z = torch.zeros(n, dtype=torch.float64, device="cuda")
     H.vcycle(dev(b), z)
     zo = oracle.vcycle(h, b)
-    assert np.linalg.norm(host(z) - zo) / np.linalg.norm(zo) <= 1e-12
+    assert ew_err(host(z), zo) <= 1e-12
     xo, ito, sto, histo = oracle.pcg(h, b, tol=1e-8, maxit=100)
     x = torch.zeros(n, dtype=torch.float64, device="cuda")
     rc, st, hist = H.solve(dev(b), x, tol=1e-8, maxit=100)
@@ -313,7 +305,7 @@ def test_pcg_full_size_256cube_bench_config(psc):
     z = torch.zeros(n, dtype=torch.float64, device="cuda")
     H.vcycle(dev(r), z)
     zo = oracle.vcycle(h, r)
-    assert np.linalg.norm(host(z) - zo) / np.linalg.norm(zo) <= 1e-12
+    assert ew_err(host(z), zo) <= 1e-12
     xo, ito, sto, histo = oracle.pcg(h, b, tol=1e-8, maxit=200)
     assert rc == 0 and sto == 0 and abs(st["iters"] - ito) <= 1
     k = min(20, ito, st["iters"]) + 1

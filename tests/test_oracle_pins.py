@@ -526,3 +526,31 @@ def test_coarse_pcg_stop_rule_equals_first_k_below_tol(seed, tol):
     np.testing.assert_allclose(xo, xs[kstar - 1], rtol=0, atol=1e-10 * np.abs(xs[kstar - 1]).max())
     xo, it = oracle.coarse_pcg(A, b, maxit=kstar - 1, tol=tol)  # the cap wins when it comes first
     assert it == kstar - 1
+
+
+# ------------------------------------------------------ OpenMP build of the oracle
+def test_openmp_oracle_build_is_bitwise_identical():
+    """SURVEY.md §8(d) "Oracle timing": the OpenMP build (cpu_baseline on all host cores)
+    computes exactly what the serial build does (row-parallel loops, fixed-chunk dots)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path[:0] = [%r, %r]\n"
+        "import oracle, pscgen\n"
+        "t = oracle.set_threads(int(sys.argv[1]))\n"
+        "h = pscgen.poisson_hierarchy(24, 20, 16, coarse_target=40)\n"
+        "b = pscgen.rhs_random(5, 0, h.levels[0].n)\n"
+        "x, it, st, hist = oracle.pcg(h, b, tol=1e-10)\n"
+        "xf, itf, stf, hf = oracle.fcg(h, b, tol=1e-10, coarse_pcg=True, coarse_maxit=7, coarse_tol=1e-3)\n"
+        "np.save(sys.argv[2], np.concatenate([x, hist, xf, hf, [it, itf, t]]))\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        outs = []
+        for nt in (1, 4):
+            f = os.path.join(d, f"o{nt}.npy")
+            subprocess.check_call([sys.executable, "-c", code, str(nt), f])
+            outs.append(np.load(f))
+    assert outs[1][-1] == 4 and outs[0][-1] == 1
+    assert np.array_equal(outs[0][:-1], outs[1][:-1])
