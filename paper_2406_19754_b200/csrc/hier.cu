@@ -282,6 +282,9 @@ double* coarse_solve(psc_hier* h, LevelWS& W, const double* b, cudaStream_t s) {
 // first_done: x[0] = M^{-1} b was already written by the kernel that produced b
 // (the restriction, or the CG update at level 0).  Returns the buffer index of x.
 // timing: event pairs around level-0 sweeps (dominant kernel, measured live).
+// PSC_NO_FUSED_SCALE=1: every first sweep from zero is a stand-alone x = M^-1 b launch
+bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
+
 int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream_t s, bool timing,
                bool first_done = false) {
   psc_ctx* ctx = h->ctx;
@@ -289,9 +292,25 @@ int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream
     PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
     return 0;
   }
-  if (!first_done) launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
-  int cur = 0;
-  for (int k = 1; k < nsweeps; ++k) {
+  int cur = 0, k = 1;
+  if (!first_done) {
+    if (nsweeps >= 2 && W.nh == 0 && (h->ctx->nranks == 1 || !W.d) && fuse_first_sweep()) {
+      // the first two sweeps from zero in one pass (RowOp::Sweep0): x1 = M^-1 b is
+      // formed where it is gathered, never stored (no halo: single rank or replicated)
+      RowArgs a;
+      a.vec_padded = true;
+      a.x = W.x[0];  // scratch of the two-launch fallback
+      a.b = b;
+      a.dinv = W.dinv;
+      a.y = W.x[1];
+      launch_rows(ctx, W.A->S, RowOp::Sweep0, a, s);
+      cur = 1;
+      k = 2;
+    } else {
+      launch_scale(ctx, W.n, W.dinv, b, W.x[0], s);
+    }
+  }
+  for (; k < nsweeps; ++k) {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
@@ -310,7 +329,6 @@ int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream
   return cur;
 }
 
-bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
 
 // Smoothing sweeps at hierarchy level `glev`: the base count, doubled per level
 // for the variable V-cycle (P:330 footnote, reading R25).

@@ -17,6 +17,10 @@ enum class RowOp {
   Resid,      // y = b_i - s
   ResidDot2,  // y = b_i - s; red0 += y_i^2; red1 += b_i^2
   PAdd,       // y += s                         (prolongation x_l += P x_{l+1})
+  Sweep0,     // the first two l1-Jacobi sweeps from x = 0 in one pass:
+              // y = x1_i + dinv_i (b_i - sum_j a_ij x1_j) with x1 = dinv .* b formed on
+              // the fly (bit-identical to scale then Sweep); `x` is scratch, written
+              // (x = x1) only by the two-launch fallback of non-TMA layouts
 };
 
 struct RowArgs {

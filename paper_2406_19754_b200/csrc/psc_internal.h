@@ -85,10 +85,14 @@ struct Sell {
   int32_t* col = nullptr;  // col_slots
   // lanes == 1: per-slice 64-byte header read by the row kernels in one coalesced
   // half-warp load (prefetched one slice ahead): [0..1] value offset, [2..3] column
-  // offset, [4] width, [5] kind (0 ELL, 1 DIA, 2 DICT), [6..13] DIA offsets (DICT: [6] table
-  // size), [14] DIA slot of the diagonal.
+  // offset, [4] width, [5] kind (0 ELL, 1 DIA), [6..13] DIA offsets, [14] DIA slot of
+  // the diagonal.
   int32_t* hdr = nullptr;
   double* val = nullptr;   // padded
+  // SELL-C-sigma (sorted) layouts: slot -> row and row -> slot offsets inside each
+  // 256-row window (kernels.cu row_of_slot / slot_of_row); nullptr: natural order
+  uint8_t* perm = nullptr;
+  uint8_t* iperm = nullptr;
   // units whose columns are all owned (interior) and the others (boundary):
   // the interior ones can run while the halo exchange is in flight.
   int32_t* interior = nullptr;
