@@ -272,6 +272,7 @@ def main():
     ap.add_argument("--maxit", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernel-table", action="store_true")
     ap.add_argument("--krylov", default="pcg", choices=["pcg", "fcg"])
     ap.add_argument("--coarse-solver", default="sweeps", choices=["sweeps", "pcg"])
     ap.add_argument("--vbm", action="store_true", help="the paper's VBM solve: --krylov fcg --coarse-solver pcg")
@@ -407,6 +408,32 @@ def main():
             "share_of_step": (dom_s / dom_n * per_iter * sum(iters) / sum(s["solve_seconds"] for s in stats)
                               if dom_n else None)}
 
+    # per-kernel table (outside the timed region): one iteration graph with an event
+    # pair around every launch, replayed 5 times (psc_hier_kernel_profile)
+    ktab = None
+    if not args.no_kernel_table:
+        recs = H.kernel_profile(bs[0], iters=5, method=args.krylov)
+        ktab = []
+        for r in recs:
+            us = r["total_us"] / r["calls_per_iter"]
+            row = {"kernel": r["name"], "level": r["level"], "calls_per_iter": r["calls_per_iter"],
+                   "us_per_call": round(us, 2), "share_of_iter": None,
+                   "alg_bytes": r["alg_bytes"], "layout_bytes": r["layout_bytes"]}
+            if r["alg_bytes"] > 0 and us > 0:
+                row["alg_GBps"] = round(r["alg_bytes"] / us / 1e3, 1)
+                row["layout_GBps"] = round(r["layout_bytes"] / us / 1e3, 1)
+                row["alg_frac"] = round(r["alg_bytes"] / us / 1e3 / peak, 3)
+                row["layout_frac"] = round(r["layout_bytes"] / us / 1e3 / peak, 3)
+            ktab.append(row)
+        tot = sum(r["total_us"] for r in recs)
+        for row, r in zip(ktab, recs):
+            row["share_of_iter"] = round(r["total_us"] / tot, 4) if tot > 0 else None
+        ktab = {"iteration_us_sum": round(tot, 1), "peak_GBps": peak,
+                "note": "event pairs around every launch in a replayed one-iteration graph; bytes per call "
+                        "(alg = SURVEY §8(d) 12 B/nnz + 8 B/vector element; layout = as stored); levels >= 2 "
+                        "are L2-resident, so their fractions of the HBM peak are not roofline claims",
+                "rows": ktab}
+
     # end to end: host b / x through psc_pcg_solve_host, pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -465,7 +492,7 @@ def main():
                 "l2": "inputs larger than L2 (A_0 alone ~1.4 GB/GPU vs 126 MB L2)",
                 "setup_s": {"generate": round(t_gen, 2), "create_assemble_hier": round(t_build, 2)},
                 "model": "none (sparse solver)"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "kernel_table": ktab, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": sum(s["kernel_launches"] for s in stats),
             "launches_per_iteration": stats[0]["iter_graph_nodes"],
             "halo_path": {0: "single rank", 1: "NVLink peer stores (CUDA IPC)", 2: "NCCL"}[stats[0]["halo_path"]],

@@ -261,6 +261,30 @@ int psc_krylov_solve_host(psc_hier* h, int method, const double* b_host, double*
  * level-`level` vector, averaged over `reps` back-to-back exchanges (eager launches). */
 int psc_hier_exchange_bench(psc_hier* h, int level, int reps, double* us_per_exchange);
 
+/* One kernel (name, hierarchy level) of the Krylov iteration, as measured by
+ * psc_hier_kernel_profile.  level: hierarchy level of a V-cycle kernel, -1 for the
+ * Krylov-level kernels (q = A p, vector updates, exchanges of p).  Bytes per call:
+ * alg_bytes = SURVEY.md §8(d)'s algorithmic count (12 B per stored nonzero + 8 B per
+ * vector element read or written once); layout_bytes = the same vectors + the matrix
+ * as stored (value and column slots incl. padding, slice headers, row order). */
+typedef struct {
+  char name[64];       /* kernel family and epilogue, e.g. "sell_tma<Sweep>" */
+  int level;
+  int calls_per_iter;  /* launches of this (name, level) per Krylov iteration */
+  double total_us;     /* device time of those launches per iteration (event pairs) */
+  double alg_bytes, layout_bytes;  /* per call */
+} psc_kernel_rec;
+
+/* [collective] Per-kernel device timing: solves A x = b from x = 0
+ * for exactly `iters` iterations (no tolerance test; b on the device, n_owned(0))
+ * with a CUDA graph of one iteration in which every kernel launch is bracketed by
+ * an event pair, and returns up to max_recs records (grouped by name and level, in
+ * launch order) and their number in *n_recs.  The caller's b is not modified; the
+ * iterate is discarded.  Errors: PSC_ERR_ARG (iters < 1, null pointers, unknown
+ * method), PSC_ERR_BREAKDOWN. */
+int psc_hier_kernel_profile(psc_hier* h, int method, const double* b_dev, int iters, psc_kernel_rec* recs,
+                            int max_recs, int* n_recs);
+
 void psc_hier_destroy(psc_hier* h);
 
 #ifdef __cplusplus

@@ -200,3 +200,144 @@ def pcg(hier, b, x0=None, tol=1e-8, maxit=200, pre=4, post=4, coarse=30, **coars
     st = lib().or_pcg(ctypes.byref(hh.c), b.ctypes.data, x.ctypes.data, float(tol), int(maxit), hist.ctypes.data,
                       ctypes.byref(it))
     return x, it.value, st, hist[: it.value + 1]
+
+
+# ------------------------------------------------------------------ NEXT-1 set-up
+def _take_csr(nrows, ncols, pp, pc, pv):
+    """Copy a malloc'd CSR (int64 ptr/col, f64 val) into scipy and free it."""
+    import scipy.sparse as sp
+    L = lib()
+    ptr = np.ctypeslib.as_array(ctypes.cast(pp, ctypes.POINTER(ctypes.c_int64)), shape=(nrows + 1,)).copy()
+    nnz = int(ptr[-1])
+    col = (np.ctypeslib.as_array(ctypes.cast(pc, ctypes.POINTER(ctypes.c_int64)), shape=(nnz,)).copy()
+           if nnz else np.zeros(0, np.int64))
+    val = (np.ctypeslib.as_array(ctypes.cast(pv, ctypes.POINTER(ctypes.c_double)), shape=(nnz,)).copy()
+           if nnz else np.zeros(0))
+    for p in (pp, pc, pv):
+        L.or_free(p)
+    m = sp.csr_matrix((val, col, ptr), shape=(nrows, ncols))
+    m.has_sorted_indices = True  # rows are built with increasing columns
+    return m
+
+
+def _setup_sigs():
+    L = lib()
+    vp = ctypes.c_void_p
+    if getattr(L, "_setup_sigs", False):
+        return L
+    L.or_free.argtypes = [vp]
+    L.or_vmb_aggregate.argtypes = [vp, ctypes.c_int, vp, ctypes.c_double, vp, vp]
+    L.or_vmb_aggregate.restype = ctypes.c_int64
+    L.or_omega.argtypes = [vp]
+    L.or_omega.restype = ctypes.c_double
+    pp = ctypes.POINTER(vp)
+    L.or_smoothed_prolongator.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_double, pp, pp, pp]
+    L.or_transpose.argtypes = [vp, pp, pp, pp]
+    L.or_galerkin.argtypes = [vp, vp, vp, pp, pp, pp]
+    L._setup_sigs = True
+    return L
+
+
+def vmb_aggregate(A, theta=0.01, row_start=None):
+    """Decoupled VMB aggregation (readings R17, R18, R20, R26).
+    Returns (agg[n], root[n] (bool), n_aggregates)."""
+    L = _setup_sigs()
+    h = _CsrHolder(A)
+    n = h.c.nrows
+    rs = np.array([0, n] if row_start is None else row_start, np.int64)
+    agg = np.empty(n, np.int64)
+    root = np.zeros(n, np.int8)
+    nc = L.or_vmb_aggregate(ctypes.byref(h.c), len(rs) - 1, rs.ctypes.data, float(theta), agg.ctypes.data,
+                            root.ctypes.data)
+    if nc < 0:
+        raise RuntimeError("VMB phase 3 reached (a node farther than two strong edges from every root)")
+    return agg, root.astype(bool), int(nc)
+
+
+def omega(A) -> float:
+    """omega = 1 / ||D^-1 A||_inf (reading R21)."""
+    h = _CsrHolder(A)  # keeps the arrays alive during the call
+    return _setup_sigs().or_omega(ctypes.byref(h.c))
+
+
+def smoothed_prolongator(A, agg, nc, om):
+    """P = (I - omega D^-1 A) P^, P^ of Eq. (3) with w = 1."""
+    L = _setup_sigs()
+    h = _CsrHolder(A)
+    agg = _arr(agg, np.int64)
+    pp, pc, pv = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    L.or_smoothed_prolongator(ctypes.byref(h.c), agg.ctypes.data, int(nc), float(om), ctypes.byref(pp),
+                              ctypes.byref(pc), ctypes.byref(pv))
+    return _take_csr(h.c.nrows, int(nc), pp.value, pc.value, pv.value)
+
+
+def transpose(P):
+    """R = P^T, rows by increasing column (BASELINE.json north_star: explicit R)."""
+    L = _setup_sigs()
+    h = _CsrHolder(P)
+    pp, pc, pv = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    L.or_transpose(ctypes.byref(h.c), ctypes.byref(pp), ctypes.byref(pc), ctypes.byref(pv))
+    return _take_csr(h.c.ncols, h.c.nrows, pp.value, pc.value, pv.value)
+
+
+def galerkin(R, A, P):
+    """A_c = R A P."""
+    L = _setup_sigs()
+    hr, ha, hp = _CsrHolder(R), _CsrHolder(A), _CsrHolder(P)
+    pp, pc, pv = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    L.or_galerkin(ctypes.byref(hr.c), ctypes.byref(ha.c), ctypes.byref(hp.c), ctypes.byref(pp), ctypes.byref(pc),
+                  ctypes.byref(pv))
+    return _take_csr(hr.c.nrows, hp.c.ncols, pp.value, pc.value, pv.value)
+
+
+class SetupLevel:
+    def __init__(self, A, row_start):
+        self.A, self.P, self.R, self.agg, self.root = A, None, None, None, None
+        self.n = A.shape[0]
+        self.row_start = np.asarray(row_start, np.int64)
+        self.omega = None
+
+
+class SetupHierarchy:
+    """A hierarchy built by the oracle's set-up; usable by oracle.pcg / vcycle / fcg."""
+
+    def __init__(self, levels):
+        self.levels = levels
+
+    @property
+    def nlevels(self):
+        return len(self.levels)
+
+    def operator_complexity(self):
+        return sum(L.A.nnz for L in self.levels) / self.levels[0].A.nnz
+
+
+def amg_setup(A0, theta=0.01, max_levels=20, coarse_target=200, stall_ratio=0.75, row_start=None):
+    """The set-up of P:196-240 level by level (readings R17-R21, R26): aggregate, smooth
+    the tentative prolongator, R = P^T, A_{l+1} = R A_l P.  Stops when n_l <=
+    coarse_target, when an aggregation would leave more than stall_ratio * n_l
+    aggregates (R19), or at max_levels."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix(A0)
+    A.sort_indices()
+    n = A.shape[0]
+    rs = np.array([0, n] if row_start is None else row_start, np.int64)
+    levels = [SetupLevel(A, rs)]
+    while True:
+        L = levels[-1]
+        if L.n <= coarse_target or len(levels) >= max_levels:
+            break
+        agg, root, nc = vmb_aggregate(L.A, theta, L.row_start)
+        if nc > stall_ratio * L.n or nc >= L.n:
+            break
+        om = omega(L.A)
+        P = smoothed_prolongator(L.A, agg, nc, om)
+        R = transpose(P)
+        Ac = galerkin(R, L.A, P)
+        # coarse row blocks: the aggregates of each fine block (decoupled, ids block by block)
+        crs = np.zeros(len(L.row_start), np.int64)
+        for r in range(len(L.row_start) - 1):
+            crs[r + 1] = crs[r] + int(root[L.row_start[r]:L.row_start[r + 1]].sum())
+        L.P, L.R, L.agg, L.root, L.omega = P, R, agg, root, om
+        levels.append(SetupLevel(Ac, crs))
+    return SetupHierarchy(levels)

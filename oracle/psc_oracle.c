@@ -353,3 +353,216 @@ done:
   free_m(h, m);
   return status;
 }
+
+/* ======================================================================
+ * NEXT-1: the set-up the paper runs before the solve:
+ * decoupled Vanek-Mandel-Brezina aggregation (Sec. 2.3.1), the
+ * tentative prolongator of Eq. (3) with w = 1, its smoothing
+ * P = (I - omega D^-1 A) P^ with omega = 1/||D^-1 A||_inf, R = P^T and
+ * the Galerkin product A_{l+1} = P_l^T A_l P_l.  Readings: DESIGN.md
+ * R17-R21 (theta, phases, stop rule, decoupling, omega) and R26 (phase 1 visits the
+ * nodes in increasing global index).  Outputs are malloc'd CSR arrays the
+ * caller frees with or_free.
+ * ====================================================================== */
+
+void or_free(void* p) { free(p); }
+
+/* Decoupled VMB aggregation of A (square, global CSR) over the row blocks
+ * row_start[0..nranks]: aggregates never contain nodes of two blocks (P:214,
+ * "Decoupled"; strong couplings to another block are ignored).
+ *   strong(i, j): j != i, same block, |a_ij| >= theta sqrt(a_ii a_jj)
+ *   phase 1: visit the nodes in increasing global index (reading R26); i becomes a
+ *            root when neither i nor any strong neighbour of i is aggregated yet; its
+ *            aggregate is i and its strong neighbours (the VMB root rule)
+ *   numbering: aggregate ids = roots in increasing global index (block by block)
+ *   phase 2: "any remaining nodes are added to the nearest aggregates":
+ *            a node outside the phase-1 aggregates joins the phase-1 aggregate of its
+ *            strongest strong neighbour (largest |a_ij| / sqrt(a_ii a_jj)) that is in
+ *            one; ties go to the lowest aggregate id (reading R18)
+ *   phase 3: a node still unaggregated would start its own aggregate; this never
+ *            happens, because phase 1 leaves no node farther than two strong edges
+ *            from a root.
+ * agg[n]: aggregate of each node; root[n]: 1 for roots.  Returns the number of
+ * aggregates, or -1 if phase 3 was reached. */
+int64_t or_vmb_aggregate(const or_csr* A, int nranks, const int64_t* row_start, double theta, int64_t* agg,
+                         int8_t* root) {
+  const int64_t n = A->nrows;
+  double* d = dalloc(n);
+  int64_t* blk = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+  for (int r = 0; r < nranks; ++r)
+    for (int64_t i = row_start[r]; i < row_start[r + 1]; ++i) blk[i] = r;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k)
+      if (A->col[k] == i) d[i] = A->val[k];
+  /* strong flags per stored entry */
+  int8_t* st = (int8_t*)calloc((size_t)(A->ptr[n] > 0 ? A->ptr[n] : 1), 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) {
+      const int64_t j = A->col[k];
+      st[k] = (j != i && blk[j] == blk[i] && fabs(A->val[k]) >= theta * sqrt(d[i] * d[j])) ? 1 : 0;
+    }
+  int8_t* in1 = (int8_t*)calloc((size_t)(n > 0 ? n : 1), 1); /* aggregated in phase 1 */
+  int64_t* owner = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1)); /* root of the phase-1 aggregate */
+  for (int64_t i = 0; i < n; ++i) { /* phase 1 */
+    root[i] = 0;
+    if (in1[i]) continue;
+    int free_nb = 1;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k)
+      if (st[k] && in1[A->col[k]]) { free_nb = 0; break; }
+    if (!free_nb) continue;
+    root[i] = 1;
+    in1[i] = 1;
+    owner[i] = i;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k)
+      if (st[k]) { in1[A->col[k]] = 1; owner[A->col[k]] = i; }
+  }
+  /* aggregate ids: roots in increasing index */
+  int64_t* rid = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  int64_t nc = 0;
+  for (int64_t i = 0; i < n; ++i) rid[i] = root[i] ? nc++ : -1;
+  for (int64_t i = 0; i < n; ++i) agg[i] = in1[i] ? rid[owner[i]] : -1;
+  /* phase 2 from the phase-1 snapshot */
+  int64_t left = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (in1[i]) continue;
+    double best = -1.0;
+    int64_t ba = -1;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) {
+      const int64_t j = A->col[k];
+      if (!st[k] || !in1[j]) continue;
+      const double s = fabs(A->val[k]) / sqrt(d[i] * d[j]);
+      const int64_t a = rid[owner[j]];
+      if (s > best || (s == best && a < ba)) { best = s; ba = a; }
+    }
+    agg[i] = ba;
+    if (ba < 0) ++left;
+  }
+  free(d); free(blk); free(st); free(in1); free(owner); free(rid);
+  return left ? -1 : nc;
+}
+
+/* omega = 1 / ||D^-1 A||_inf = 1 / max_i sum_j |a_ij| / |a_ii|   (reading R21) */
+double or_omega(const or_csr* A) {
+  double mx = 0.0;
+  for (int64_t i = 0; i < A->nrows; ++i) {
+    double s = 0.0, dii = 0.0;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) {
+      s += fabs(A->val[k]);
+      if (A->col[k] == i) dii = A->val[k];
+    }
+    const double t = s / fabs(dii);
+    if (t > mx) mx = t;
+  }
+  return 1.0 / mx;
+}
+
+/* Smoothed prolongator P = (I - omega D^-1 A) P^ with the tentative P^ of
+ * Eq. (3), w = 1: P^_{iJ} = 1 if i in C_J.  Row i:
+ *   t_J = sum_{k in row i, agg(k) = J} a_ik (stored column order),  s = omega / a_ii,
+ *   P_iJ = 1 - s t_J if J = agg(i), else -s t_J;  one entry per aggregate J touched
+ * by row i, columns increasing.  Outputs malloc'd (ptr[n+1], col, val). */
+void or_smoothed_prolongator(const or_csr* A, const int64_t* agg, int64_t nc, double omega, int64_t** pptr,
+                             int64_t** pcol, double** pval) {
+  const int64_t n = A->nrows;
+  int64_t* ptr = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t* col = (int64_t*)malloc(sizeof(int64_t) * (size_t)(A->ptr[n] + 1));
+  double* val = (double*)malloc(sizeof(double) * (size_t)(A->ptr[n] + 1));
+  (void)nc;
+  int64_t o = 0;
+  ptr[0] = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t b = o;
+    double dii = 0.0;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k) {
+      if (A->col[k] == i) dii = A->val[k];
+      const int64_t J = agg[A->col[k]];
+      int64_t t = b;
+      while (t < o && col[t] != J) ++t;
+      if (t == o) { col[o] = J; val[o] = A->val[k]; ++o; }
+      else val[t] = val[t] + A->val[k];
+    }
+    const double s = omega / dii;
+    for (int64_t t = b; t < o; ++t) {
+      const double v = s * val[t];
+      val[t] = (col[t] == agg[i]) ? 1.0 - v : -v;
+    }
+    for (int64_t x = b + 1; x < o; ++x) { /* columns increasing */
+      const int64_t cc = col[x];
+      const double vv = val[x];
+      int64_t y = x - 1;
+      while (y >= b && col[y] > cc) { col[y + 1] = col[y]; val[y + 1] = val[y]; --y; }
+      col[y + 1] = cc;
+      val[y + 1] = vv;
+    }
+    ptr[i + 1] = o;
+  }
+  *pptr = ptr; *pcol = col; *pval = val;
+}
+
+/* R = P^T (explicit restriction, BASELINE.json north_star), rows by increasing column. */
+void or_transpose(const or_csr* P, int64_t** rptr, int64_t** rcol, double** rval) {
+  const int64_t n = P->nrows, nc = P->ncols, nnz = P->ptr[n];
+  int64_t* ptr = (int64_t*)calloc((size_t)(nc + 1), sizeof(int64_t));
+  int64_t* col = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nnz + 1));
+  double* val = (double*)malloc(sizeof(double) * (size_t)(nnz + 1));
+  for (int64_t k = 0; k < nnz; ++k) ptr[P->col[k] + 1]++;
+  for (int64_t c = 0; c < nc; ++c) ptr[c + 1] += ptr[c];
+  int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nc + 1));
+  memcpy(fill, ptr, sizeof(int64_t) * (size_t)(nc + 1));
+  for (int64_t i = 0; i < n; ++i) /* rows of P in increasing i: each R row comes out sorted */
+    for (int64_t k = P->ptr[i]; k < P->ptr[i + 1]; ++k) {
+      const int64_t o = fill[P->col[k]]++;
+      col[o] = i;
+      val[o] = P->val[k];
+    }
+  free(fill);
+  *rptr = ptr; *rcol = col; *rval = val;
+}
+
+/* Galerkin coarse operator A_c = R A P (R = P^T), row by row:
+ *   A_c[J, K] = sum_{i in R_J} sum_{k in A_i} (R_Ji a_ik) P_kK
+ * accumulated in that loop order (i, then k, then K increasing), columns increasing;
+ * every (J, K) reached is stored (also when the sum cancels). */
+void or_galerkin(const or_csr* R, const or_csr* A, const or_csr* P, int64_t** cptr, int64_t** ccol,
+                 double** cval) {
+  const int64_t nc = R->nrows;
+  double* acc = dalloc(P->ncols);
+  int64_t* mark = (int64_t*)malloc(sizeof(int64_t) * (size_t)(P->ncols > 0 ? P->ncols : 1));
+  int64_t* touched = (int64_t*)malloc(sizeof(int64_t) * (size_t)(P->ncols > 0 ? P->ncols : 1));
+  for (int64_t K = 0; K < P->ncols; ++K) mark[K] = -1;
+  int64_t cap = 1024, o = 0;
+  int64_t* ptr = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nc + 1));
+  int64_t* col = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  double* val = (double*)malloc(sizeof(double) * (size_t)cap);
+  ptr[0] = 0;
+  for (int64_t J = 0; J < nc; ++J) {
+    int64_t nt = 0;
+    for (int64_t a = R->ptr[J]; a < R->ptr[J + 1]; ++a) {
+      const int64_t i = R->col[a];
+      for (int64_t b = A->ptr[i]; b < A->ptr[i + 1]; ++b) {
+        const int64_t k = A->col[b];
+        const double ra = R->val[a] * A->val[b];
+        for (int64_t c = P->ptr[k]; c < P->ptr[k + 1]; ++c) {
+          const int64_t K = P->col[c];
+          if (mark[K] != J) { mark[K] = J; acc[K] = 0.0; touched[nt++] = K; }
+          acc[K] = acc[K] + ra * P->val[c];
+        }
+      }
+    }
+    for (int64_t x = 1; x < nt; ++x) { /* sort the touched columns */
+      const int64_t t = touched[x];
+      int64_t y = x - 1;
+      while (y >= 0 && touched[y] > t) { touched[y + 1] = touched[y]; --y; }
+      touched[y + 1] = t;
+    }
+    if (o + nt > cap) {
+      while (o + nt > cap) cap *= 2;
+      col = (int64_t*)realloc(col, sizeof(int64_t) * (size_t)cap);
+      val = (double*)realloc(val, sizeof(double) * (size_t)cap);
+    }
+    for (int64_t x = 0; x < nt; ++x) { col[o] = touched[x]; val[o] = acc[touched[x]]; ++o; }
+    ptr[J + 1] = o;
+  }
+  free(acc); free(mark); free(touched);
+  *cptr = ptr; *ccol = col; *cval = val;
+}

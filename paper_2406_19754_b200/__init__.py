@@ -43,6 +43,11 @@ class CycleOpts(ctypes.Structure):
                 ("coarse_maxit", _i32), ("coarse_tol", _f64), ("variable_v", _i32)]
 
 
+class KernelRec(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 64), ("level", _i32), ("calls_per_iter", _i32), ("total_us", _f64),
+                ("alg_bytes", _f64), ("layout_bytes", _f64)]
+
+
 class Stats(ctypes.Structure):
     _fields_ = [("iters", _i32), ("status", _i32), ("rel_res", _f64), ("solve_seconds", _f64),
                 ("kernel_launches", _i64), ("collectives", _i64), ("dom_kernel_seconds", _f64),
@@ -91,6 +96,7 @@ _sig("psc_pcg_solve_host", _i32, [_vp, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
 _sig("psc_krylov_solve", _i32, [_vp, _i32, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
 _sig("psc_krylov_solve_host", _i32, [_vp, _i32, _vp, _vp, _f64, _i32, _vp, _P(Stats)])
 _sig("psc_hier_exchange_bench", _i32, [_vp, _i32, _i32, _P(_f64)])
+_sig("psc_hier_kernel_profile", _i32, [_vp, _i32, _vp, _i32, _vp, _i32, _P(_i32)])
 _sig("psc_hier_destroy", None, [_vp])
 
 
@@ -338,6 +344,17 @@ class Hierarchy:
                                         int(maxit), hist.ctypes.data, ctypes.byref(st))
         _check(rc, self.ctx, ok=(PSC_OK, PSC_NOT_CONVERGED))
         return rc, st.as_dict(), hist[: st.iters + 1]
+
+    def kernel_profile(self, b, iters=5, method="pcg", max_recs=256):
+        """psc_hier_kernel_profile: per-(kernel, level) device time per iteration and bytes per call."""
+        if method not in _KRYLOV:
+            raise ValueError(f"method must be one of {sorted(_KRYLOV)}")
+        recs = (KernelRec * max_recs)()
+        n = _i32()
+        _check(_lib.psc_hier_kernel_profile(self.handle, _KRYLOV[method], _dev_ptr(b, self.n0, "b"), int(iters),
+                                            recs, max_recs, ctypes.byref(n)), self.ctx)
+        return [dict(name=r.name.decode(), level=r.level, calls_per_iter=r.calls_per_iter, total_us=r.total_us,
+                     alg_bytes=r.alg_bytes, layout_bytes=r.layout_bytes) for r in recs[: min(n.value, max_recs)]]
 
     def exchange_bench(self, level, reps=200):
         """Device microseconds per halo exchange of a level vector (collective)."""

@@ -94,6 +94,7 @@ struct psc_hier_s {
   const double* rz_weight = nullptr;
   // graph of one Krylov iteration, per method (PSC_KRYLOV_PCG, PSC_KRYLOV_FCG)
   cudaGraphExec_t iter_exec[2] = {nullptr, nullptr};
+  cudaGraphExec_t prof_exec[2] = {nullptr, nullptr};  // the same iteration with per-kernel event pairs
   int64_t iter_launches[2] = {0, 0}, iter_collectives[2] = {0, 0};
   double* z_ptr = nullptr;
   // dominant-kernel timing (level-0 l1-Jacobi sweep) inside the graph
@@ -361,6 +362,9 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
                    bool first_done, bool dist) {
   psc_ctx* ctx = h->ctx;
   const int Lend = (int)LV.size();
+  // hierarchy level of LV[l] (the replicated suffix starts at level rep.first)
+  const int glev = l + (&LV == &h->rep.lv ? h->rep.first : 0);
+  ctx->kt.level = glev;
   if (dist && h->rep.on && l == h->rep.first) return replicated_cycle(h, b, s);
   if (h->dsuf && &LV == h->dsuf_lv && l == h->dsuf_l) {  // the whole sub-cycle as one dense product
     launch_dense_gemv(ctx, h->dsuf, LV[l].n, b, LV[l].x[0], s);
@@ -373,8 +377,6 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   const bool next_replicated = dist && h->rep.on && l + 1 == h->rep.first;
   // (I - M^-1 A)^pre, then the coarse-grid correction (I - P B_{l+1} P^T A):
   // r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
-  // hierarchy level of LV[l] (the replicated suffix starts at level rep.first)
-  const int glev = l + (&LV == &h->rep.lv ? h->rep.first : 0);
   const int pre = level_sweeps(h, h->opt.pre_sweeps, glev);
   int cur = pre_smooth(h, W, b, pre, s, time_here, first_done);
   {
@@ -400,6 +402,7 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     run_rows(h, W.d, W.R->S, RowOp::Spmv, a, s);
   }
   double* xc = vcycle_rec(h, LV, l + 1, C.b, s, timing, fuse, dist);
+  ctx->kt.level = glev;
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -460,6 +463,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing, int method) {
   // the CG update of the previous iteration (or the eager start) wrote x_0 = M^{-1} r
   h->rz_weight = fcg ? h->q : nullptr;
   double* z = vcycle_level(h, 0, h->r_cg, s, timing);
+  ctx->kt.level = -1;  // Krylov vector ops and q = A p
   h->rz_weight = nullptr;
   h->z_ptr = z;
   allgather_slot(h, S_RZ, s);
@@ -486,25 +490,39 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing, int method) {
   PSC_CUDA(cudaMemcpyAsync(h->h_scal, h->d_scal, sizeof(double) * NSLOT * R, cudaMemcpyDeviceToHost, s));
 }
 
-void capture_iteration(psc_hier* h, int method) {
+void capture_iteration(psc_hier* h, int method, bool profile = false) {
   psc_ctx* ctx = h->ctx;
   cudaStream_t s = ctx->stream;
   const int64_t l0 = ctx->launches, c0 = ctx->collectives;
   cudaGraph_t g = nullptr;
+  const int dom_saved = h->dom_used;  // the timed solve graph's event pairs
   PSC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  if (profile) {
+    ctx->kt.on = true;
+    ctx->kt.recs.clear();
+    ctx->kt.used = 0;
+  }
   try {
-    record_iteration(h, s, true, method);
+    record_iteration(h, s, !profile, method);
+    ctx->kt.on = false;
   } catch (...) {
+    ctx->kt.on = false;
     h->rz_weight = nullptr;
     cudaStreamEndCapture(s, &g);
     if (g) cudaGraphDestroy(g);
     throw;
   }
   PSC_CUDA(cudaStreamEndCapture(s, &g));
-  PSC_CUDA(cudaGraphInstantiate(&h->iter_exec[method], g, 0));
+  cudaGraphExec_t& ex = profile ? h->prof_exec[method] : h->iter_exec[method];
+  if (ex) PSC_CUDA(cudaGraphExecDestroy(ex));
+  PSC_CUDA(cudaGraphInstantiate(&ex, g, 0));
   PSC_CUDA(cudaGraphDestroy(g));
-  h->iter_launches[method] = ctx->launches - l0;
-  h->iter_collectives[method] = ctx->collectives - c0;
+  if (profile) {
+    h->dom_used = dom_saved;
+  } else {
+    h->iter_launches[method] = ctx->launches - l0;
+    h->iter_collectives[method] = ctx->collectives - c0;
+  }
   ctx->launches = l0;
   ctx->collectives = c0;
 }
@@ -750,6 +768,8 @@ void free_hier(psc_hier* h) {
   red_free(h->red1);
   red_free(h->red2);
   dfree(h->d_done);
+  for (auto e : h->prof_exec)
+    if (e) cudaGraphExecDestroy(e);
   for (auto e : h->iter_exec)
     if (e) cudaGraphExecDestroy(e);
   for (auto e : h->ev_dom) cudaEventDestroy(e);
@@ -760,8 +780,14 @@ void free_hier(psc_hier* h) {
   delete h;
 }
 
+// per-kernel sums of a profiled solve (psc_hier_kernel_profile)
+struct KProf {
+  std::vector<double> ms;  // per KTrace record of the iteration graph
+  int iters = 0;
+};
+
 int solve_impl(psc_hier* h, int method, const double* b, double* x, double tol, int maxit, double* hist,
-               psc_stats* st, double extra_h2d) {
+               psc_stats* st, double extra_h2d, KProf* prof = nullptr) {
   psc_ctx* ctx = h->ctx;
   cudaStream_t s = ctx->stream;
   const int R = ctx->nranks;
@@ -816,10 +842,24 @@ int solve_impl(psc_hier* h, int method, const double* b, double* x, double tol, 
         const double one = 1.0;
         PSC_CUDA(cudaMemcpyAsync(rz_old(h), &one, sizeof(double), cudaMemcpyHostToDevice, s));
       }
-      if (!h->iter_exec[method]) capture_iteration(h, method);
+      if (prof) {
+        capture_iteration(h, method, true);
+        prof->ms.assign(ctx->kt.recs.size(), 0.0);
+      } else if (!h->iter_exec[method]) {
+        capture_iteration(h, method);
+      }
+      cudaGraphExec_t ex = prof ? h->prof_exec[method] : h->iter_exec[method];
       for (int k = 1; k <= maxit; ++k) {
-        PSC_CUDA(cudaGraphLaunch(h->iter_exec[method], s));
+        PSC_CUDA(cudaGraphLaunch(ex, s));
         PSC_CUDA(cudaStreamSynchronize(s));
+        if (prof) {
+          for (size_t q = 0; q < ctx->kt.recs.size(); ++q) {
+            float ms = 0.f;
+            PSC_CUDA(cudaEventElapsedTime(&ms, ctx->kt.recs[q].e0, ctx->kt.recs[q].e1));
+            prof->ms[q] += ms;
+          }
+          prof->iters = k;
+        }
         ctx->launches += h->iter_launches[method];
         ctx->collectives += h->iter_collectives[method];
         for (int e = 0; e + 1 < h->dom_used; e += 2) {
@@ -1081,6 +1121,53 @@ int psc_hier_smooth(psc_hier* h, int level, const double* b, double* x, int nswe
     PSC_CUDA(cudaStreamSynchronize(s));
     return PSC_OK;
   } catch (const Error& e) {
+    return hfail(ctx, e);
+  }
+}
+
+int psc_hier_kernel_profile(psc_hier* h, int method, const double* b, int iters, psc_kernel_rec* recs, int max_recs,
+                            int* n_recs) {
+  psc_ctx* ctx = h ? h->ctx : nullptr;
+  double* x = nullptr;
+  try {
+    PSC_REQUIRE(h && iters >= 1 && (b || h->lv[0].n == 0) && n_recs && (recs || max_recs == 0), PSC_ERR_ARG,
+                "bad argument");
+    PSC_REQUIRE(method == PSC_KRYLOV_PCG || method == PSC_KRYLOV_FCG, PSC_ERR_ARG, "unknown Krylov method");
+    enter(ctx);
+    x = dvec(h->lv[0].n + 1);
+    PSC_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (h->lv[0].n + 1), ctx->stream));
+    KProf prof;
+    solve_impl(h, method, b, x, 0.0, iters, nullptr, nullptr, 0.0, &prof);
+    dfree(x);
+    x = nullptr;
+    // group the iteration's launches by (name, level), in order of first appearance
+    std::vector<psc_kernel_rec> out;
+    const auto& R = ctx->kt.recs;
+    for (size_t q = 0; q < R.size(); ++q) {
+      if (!R[q].name) continue;
+      size_t o = 0;
+      while (o < out.size() && !(out[o].level == R[q].level && std::strcmp(out[o].name, R[q].name) == 0)) ++o;
+      if (o == out.size()) {
+        psc_kernel_rec r{};
+        std::snprintf(r.name, sizeof(r.name), "%s", R[q].name);
+        r.level = R[q].level;
+        out.push_back(r);
+      }
+      psc_kernel_rec& r = out[o];
+      r.calls_per_iter += 1;
+      r.total_us += 1e3 * prof.ms[q] / std::max(prof.iters, 1);
+      r.alg_bytes += R[q].alg_bytes;
+      r.layout_bytes += R[q].layout_bytes;
+    }
+    for (auto& r : out) {  // per call
+      r.alg_bytes /= r.calls_per_iter;
+      r.layout_bytes /= r.calls_per_iter;
+    }
+    *n_recs = (int)out.size();
+    for (int q = 0; q < std::min<int>(max_recs, (int)out.size()); ++q) recs[q] = out[q];
+    return PSC_OK;
+  } catch (const Error& e) {
+    dfree(x);
     return hfail(ctx, e);
   }
 }

@@ -8,6 +8,7 @@
 // to the SM count, and deterministic fixed-order reductions.
 #include <algorithm>
 #include <cub/cub.cuh>
+#include <deque>
 #include <numeric>
 
 #include "kernels.h"
@@ -864,6 +865,50 @@ static bool tma_ok(const Sell& A, const RowArgs& r, SliceSet set) {
          A.n_units > 0;
 }
 
+const char* kt_name(const std::string& n) {  // interned kernel label for KTrace
+  static std::deque<std::string> names;
+  for (const auto& x : names)
+    if (x == n) return x.c_str();
+  names.push_back(n);
+  return names.back().c_str();
+}
+
+static const char* op_name(RowOp op) {
+  switch (op) {
+    case RowOp::Spmv: return "Spmv";
+    case RowOp::SpmvDot: return "SpmvDot";
+    case RowOp::Sweep: return "Sweep";
+    case RowOp::SweepDot: return "SweepDot";
+    case RowOp::Resid: return "Resid";
+    case RowOp::ResidDot2: return "ResidDot2";
+    case RowOp::PAdd: return "PAdd";
+    case RowOp::Sweep0: return "Sweep0";
+  }
+  return "?";
+}
+
+// Bytes one launch must move: algorithmic = SURVEY.md §8(d)'s count,
+// 12 B per stored nonzero + 8 B per vector element read or written once (x counted
+// once over the column space); layout = the same vectors + the matrix as stored
+// (8 B per value slot incl. padding, 4 B per column slot, slice headers, row order).
+static void row_bytes(const Sell& A, RowOp op, const RowArgs& r, double& alg, double& lay) {
+  const double n = (double)A.n_rows, nc = (double)A.n_cols_local;
+  double vec = 8.0 * nc;  // x gathered (Sweep0: b, then dinv, as x1 = dinv .* b)
+  switch (op) {
+    case RowOp::Spmv: vec += 8.0 * n * (1 + (r.beta != 0.0) + (r.y2 ? 2 : 0)); break;
+    case RowOp::SpmvDot: vec += 8.0 * n; break;
+    case RowOp::Sweep: vec += 24.0 * n; break;
+    case RowOp::SweepDot: vec += 8.0 * n * (3 + (r.w ? 1 : 0)); break;
+    case RowOp::Resid: case RowOp::ResidDot2: vec += 16.0 * n; break;
+    case RowOp::PAdd: vec += 16.0 * n; break;
+    case RowOp::Sweep0: vec = 24.0 * n; break;
+  }
+  const double hdr = A.lanes == 1 ? 64.0 * (double)A.n_units + (A.perm ? 32.0 * (double)A.n_units : 0.0)
+                                  : 8.0 * (n + 1);
+  alg = 12.0 * (double)A.nnz + vec;
+  lay = 8.0 * (double)A.padded + 4.0 * (double)A.col_slots + hdr + vec;
+}
+
 void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaStream_t s, SliceSet set) {
   if (op == RowOp::Sweep0 && !tma_ok(A, r, set)) {
     // two launches: x = dinv .* b, then one sweep from x
@@ -871,6 +916,15 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
     launch_rows(ctx, A, RowOp::Sweep, r, s, set);
     return;
   }
+  double alg = 0.0, lay = 0.0;
+  const char* kname = nullptr;
+  if (ctx->kt.on) {
+    row_bytes(A, op, r, alg, lay);
+    const char* fam = tma_ok(A, r, set) ? "sell_tma" : (A.lanes == 1 ? "sell" : (rg_tma_ok(A, r, set) ? "rg_tma" : "rg"));
+    kname = kt_name(std::string(fam) + "<" + op_name(op) + (A.lanes > 1 ? "," + std::to_string(A.lanes) : "") +
+                    ">" + (A.perm ? " sorted" : "") + (set != SliceSet::All ? " subset" : ""));
+  }
+  KtScope kts(ctx, s, kname, alg, lay);
   RowKArgs a;
   // matrices up to 48 MB stay in L2 (evict_last) across the 8-10 launches of their level
   a.keep_matrix = (A.padded * 12 + A.n_rows * 8) <= ((int64_t)env_int("PSC_KEEP_MB", 96) << 20) ? 1 : 0;
@@ -958,6 +1012,7 @@ __global__ void __launch_bounds__(kBlock) scale_kernel(int64_t n, const double* 
 static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, double* x, cudaStream_t s) {
+  KtScope kts(ctx, s, "scale", 24.0 * n, 24.0 * n);
   PSC_REQUIRE(al16(dinv) && al16(b) && al16(x), PSC_ERR_STATE, "vector kernels need 16-byte aligned buffers");
   launch_k(scale_kernel, vec_grid(ctx, n), kBlock, 0, s, n, dinv, b, x);
   PSC_CUDA(cudaGetLastError());
@@ -1049,6 +1104,7 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(int64_t n, double* __
 void launch_cg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q,
                       const double* g_pq, const double* g_num, int num_ranks, int nranks, const RedSite* red,
                       double* red_out, cudaStream_t s) {
+  KtScope kts(ctx, s, "cg_update", 48.0 * n, 48.0 * n);
   PSC_REQUIRE(al16(x) && al16(p) && al16(r) && al16(q), PSC_ERR_STATE,
               "vector kernels need 16-byte aligned buffers");
   const int g = std::min(vec_grid(ctx, n), red->grid);
@@ -1087,6 +1143,7 @@ __global__ void __launch_bounds__(kBlock) fcg_dir_kernel(int64_t n, const double
 
 void launch_fcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* r, const double* g_zq,
                     const double* g_pq, int nranks, const RedSite* red, double* red_out, cudaStream_t s) {
+  KtScope kts(ctx, s, "fcg_dir", 32.0 * n, 32.0 * n);
   PSC_REQUIRE(al16(z) && al16(p) && al16(r), PSC_ERR_STATE, "vector kernels need 16-byte aligned buffers");
   const int g = std::min(vec_grid(ctx, n), red->grid);
   launch_k(fcg_dir_kernel, g, kBlock, 0, s, n, z, p, r, g_zq, g_pq, nranks, red->partials, red->ticket, red_out);
@@ -1164,6 +1221,7 @@ __global__ void __launch_bounds__(kBlock) cpcg_dir_kernel(int64_t n, const doubl
 
 void launch_cpcg_init(psc_ctx* ctx, int64_t n, const double* b, const double* dinv, double* x, double* r, double* z,
                       double* p, int* done, const RedSite* red, double* out, int stride, cudaStream_t s) {
+  KtScope kts(ctx, s, "cpcg_init", 40.0 * n, 40.0 * n);
   const int g = std::min(vec_grid(ctx, n), red->grid);
   launch_k(cpcg_init_kernel, g, kBlock, 0, s, n, b, dinv, x, r, z, p, done, red->partials, red->ticket, out, stride);
   PSC_CUDA(cudaGetLastError());
@@ -1173,6 +1231,7 @@ void launch_cpcg_init(psc_ctx* ctx, int64_t n, const double* b, const double* di
 void launch_cpcg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, double* r, const double* q, double* z,
                         const double* dinv, const double* g_pq, const double* g_rz, int nr, int* done,
                         const RedSite* red, double* out, int stride, cudaStream_t s) {
+  KtScope kts(ctx, s, "cpcg_update", 64.0 * n, 64.0 * n);
   const int g = std::min(vec_grid(ctx, n), red->grid);
   launch_k(cpcg_update_kernel, g, kBlock, 0, s, n, x, p, r, q, z, dinv, g_pq, g_rz, nr, done, red->partials,
            red->ticket, out, stride);
@@ -1182,6 +1241,7 @@ void launch_cpcg_update(psc_ctx* ctx, int64_t n, double* x, const double* p, dou
 
 void launch_cpcg_dir(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rr, const double* g_bb,
                      const double* g_rzn, const double* g_rz, int nr, double tol, int* done, cudaStream_t s) {
+  KtScope kts(ctx, s, "cpcg_dir", 24.0 * n, 24.0 * n);
   launch_k(cpcg_dir_kernel, vec_grid(ctx, n), kBlock, 0, s, n, z, p, g_rr, g_bb, g_rzn, g_rz, nr, tol, done);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
@@ -1209,6 +1269,7 @@ __global__ void __launch_bounds__(kBlock) xpby_kernel(int64_t n, const double* _
 
 void launch_xpby(psc_ctx* ctx, int64_t n, const double* z, double* p, const double* g_rz, double* rz_old, int nranks,
                  const RedSite* red, cudaStream_t s) {
+  KtScope kts(ctx, s, "xpby", 24.0 * n, 24.0 * n);
   PSC_REQUIRE(al16(z) && al16(p), PSC_ERR_STATE, "vector kernels need 16-byte aligned buffers");
   launch_k(xpby_kernel, vec_grid(ctx, n), kBlock, 0, s, n, z, p, g_rz, rz_old, nranks, red->ticket);
   PSC_CUDA(cudaGetLastError());
@@ -1226,6 +1287,7 @@ __global__ void __launch_bounds__(kBlock) dot_kernel(int64_t n, const double* __
 
 void launch_dot(psc_ctx* ctx, int64_t n, const double* a, const double* b, const RedSite* red, double* red_out,
                 cudaStream_t s) {
+  KtScope kts(ctx, s, "dot", 16.0 * n, 16.0 * n);
   const int g = std::min(vec_grid(ctx, n), red->grid);
   launch_k(dot_kernel, g, kBlock, 0, s, n, a, b, red->partials, red->ticket, red_out);
   PSC_CUDA(cudaGetLastError());
@@ -1252,6 +1314,7 @@ __global__ void gather_kernel(int64_t n, const int64_t* __restrict__ map, const 
 }
 
 void launch_gather(psc_ctx* ctx, int64_t n, const int64_t* map, const double* in, double* out, cudaStream_t s) {
+  KtScope kts(ctx, s, "gather", 24.0 * n, 24.0 * n);
   if (n == 0) return;
   launch_k(gather_kernel, vec_grid(ctx, n), kBlock, 0, s, n, map, in, out);
   PSC_CUDA(cudaGetLastError());
@@ -1376,6 +1439,8 @@ bool coarse_one_cta_fits(const Sell& A) {
 
 void launch_coarse_solve(psc_ctx* ctx, const Sell& A, const double* dinv, const double* b, double* x, int nsweeps,
                          cudaStream_t s) {
+  KtScope kts(ctx, s, "coarse_solve", 12.0 * (double)A.nnz + 24.0 * (double)A.n_rows,
+               8.0 * (double)A.padded + 4.0 * (double)A.col_slots + 24.0 * (double)A.n_rows);
   const int64_t n = A.n_rows;
   PSC_REQUIRE(n <= coarse_smem_rows(), PSC_ERR_STATE, "coarsest level too large for the one-CTA solver");
   PSC_REQUIRE(A.n_cols_local == n, PSC_ERR_STATE, "coarsest matrix must have no halo");
@@ -1486,6 +1551,7 @@ __global__ void __launch_bounds__(kDenseWarps * 32, 1) coarse_dense(const double
 
 void launch_coarse_dense(psc_ctx* ctx, const double* Ad, int64_t n, const double* dinv, const double* b, double* x,
                          int nsweeps, cudaStream_t s) {
+  KtScope kts(ctx, s, "coarse_dense", 8.0 * n * n + 24.0 * n, 8.0 * n * n + 24.0 * n);
   PSC_REQUIRE(n <= coarse_dense_max_rows(), PSC_ERR_STATE, "coarsest level too large for the dense solver");
   launch_k(coarse_dense, 1, kDenseWarps * 32, 0, s, Ad, (int)n, dinv, b, x, nsweeps, 0);
   PSC_CUDA(cudaGetLastError());
@@ -1609,6 +1675,7 @@ __global__ void __launch_bounds__(kDenseWarps * 32, 1) coarse_dense_pcg(const do
 
 void launch_coarse_dense_pcg(psc_ctx* ctx, const double* Ad, int64_t n, const double* dinv, const double* b,
                              double* x, int maxit, double tol, cudaStream_t s) {
+  KtScope kts(ctx, s, "coarse_dense_pcg", 8.0 * n * n + 24.0 * n, 8.0 * n * n + 24.0 * n);
   PSC_REQUIRE(n <= coarse_dense_max_rows(), PSC_ERR_STATE, "coarsest level too large for the dense solver");
   launch_k(coarse_dense_pcg, 1, kDenseWarps * 32, 0, s, Ad, (int)n, dinv, b, x, maxit, tol);
   PSC_CUDA(cudaGetLastError());
@@ -1650,6 +1717,7 @@ __global__ void __launch_bounds__(256) dense_gemv_kernel(const double* __restric
 int64_t dense_gemv_max_rows() { return 6144; }  // b in 48 KB of shared memory
 
 void launch_dense_gemv(psc_ctx* ctx, const double* D, int64_t n, const double* b, double* y, cudaStream_t s) {
+  KtScope kts(ctx, s, "dense_gemv", 8.0 * n * n + 16.0 * n, 8.0 * n * n + 16.0 * n);
   PSC_REQUIRE(n >= 1 && n <= dense_gemv_max_rows(), PSC_ERR_STATE, "dense operator too large");
   launch_k(dense_gemv_kernel, (unsigned)((n + 7) / 8), 256, (size_t)n * sizeof(double), s, D, n, b, y);
   PSC_CUDA(cudaGetLastError());
@@ -1865,6 +1933,17 @@ int choose_lanes(int64_t n_rows, int64_t nnz) {
   const int forced = env_int("PSC_LANES", 0);
   if (forced == 1 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
   const double mu = n_rows ? (double)nnz / (double)n_rows : 0.0;
+  // small (L2-resident) matrices with longer rows: thread-per-row slices leave too few
+  // warps per SM to cover the gather latency (level 2 of 256^3: 65,000 rows, 2,031
+  // warps for 148 SMs); row groups of G = mu / PSC_RG_SMALL_DIV lanes spread a row over
+  // a group (experiment: PSC_RG_SMALL_MB = size limit in MB, 0 = off)
+  const int small_mb = env_int("PSC_RG_SMALL_MB", 0);
+  if (small_mb > 0 && mu >= 16 && 12.0 * (double)nnz <= (double)small_mb * 1048576.0) {
+    const double t = mu / std::max(1, env_int("PSC_RG_SMALL_DIV", 8));
+    int G = 4;
+    while (G * 2 <= t && G < 32) G *= 2;
+    return G;
+  }
   if (mu < env_int("PSC_RG_MIN", 100)) return 1;
   const double t = mu / std::max(1, env_int("PSC_RG_DIV", 1));
   int G = 4;
@@ -1946,12 +2025,14 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
       dfree(d_tmp);
     };
     widths(allow_dia, nullptr);
-    // SELL-C-sigma: a matrix with no DIA slice whose slices pad more
-    // than 2% is re-laid out with its rows sorted by length inside 256-row windows
-    // (P_0 of 256^3: 1.36 -> 1.09 padded slots per stored value); PSC_NO_SORT=1 keeps
-    // the natural order
+    // SELL-C-sigma, opt-in PSC_SORT=1: a matrix with no DIA slice whose
+    // slices pad more than 2% is re-laid out with its rows sorted by length inside
+    // 256-row windows (P_0 of 256^3: 1.36 -> 1.09 padded slots per stored value).
+    // Measured slower on B200 (P_0 210 vs 203 us, level-1 sweep 159 vs 150 us): the
+    // sorted lanes no longer touch consecutive rows, so the x gathers and the row
+    // vectors lose their coalescing, which costs more than the padding saved.
     const bool any_dia = std::any_of(hdia.begin(), hdia.end(), [](int32_t d) { return d > 0; });
-    if (!any_dia && !env_int("PSC_NO_SORT", 0) && (double)S.padded > 1.02 * (double)nnz && nu > 0) {
+    if (!any_dia && env_int("PSC_SORT", 0) && (double)S.padded > 1.02 * (double)nnz && nu > 0) {
       const int64_t nwin = (nu * 32 + kSortWin - 1) / kSortWin;
       S.perm = dalloc<uint8_t>(nwin * kSortWin);
       S.iperm = dalloc<uint8_t>(nwin * kSortWin);

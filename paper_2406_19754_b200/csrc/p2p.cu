@@ -92,6 +92,7 @@ static void push(psc_ctx* ctx, P2P& P, const double* x, const int32_t* idx, cons
   static const uint64_t tmo =
       (uint64_t)(1e9 * (getenv("PSC_SPIN_TIMEOUT_S") ? atof(getenv("PSC_SPIN_TIMEOUT_S")) : 30.0));
   PushArgs a{x, idx, soff, n, dst, nbr, P.d_pflag, P.flags, P.d_gen, P.d_ticket, ctx->nranks, tmo};
+  KtScope kts(ctx, s, idx ? "p2p_halo" : "p2p_allgather", 0.0, 0.0);
   const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((max_per_peer + 255) / 256, 64));
   p2p_push_kernel<<<dim3((unsigned)bx, (unsigned)ctx->nranks), 256, 0, s>>>(a);
   PSC_CUDA(cudaGetLastError());

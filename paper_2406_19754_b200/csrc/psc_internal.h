@@ -113,6 +113,33 @@ struct RedSite {
 
 }  // namespace psc
 
+namespace psc {
+// Per-kernel device timing (psc_hier_kernel_profile): while `on`, every launcher
+// brackets its launch with an event pair (recorded as graph nodes when captured)
+// and files it under (name, level) with its algorithmic and layout bytes.
+struct KTrace {
+  struct Rec {
+    const char* name;
+    int level;
+    double alg_bytes, layout_bytes;
+    cudaEvent_t e0, e1;
+  };
+  bool on = false;
+  int level = -1;  // hierarchy level of the launches being recorded (-1: Krylov level-0 vector ops)
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+}  // namespace psc
+
 struct psc_ctx_s {
   int rank = 0, nranks = 1, device = 0;
   int num_sms = 148;
@@ -124,7 +151,27 @@ struct psc_ctx_s {
   std::string err;
   int64_t launches = 0;     // kernel launch counter (incremented by every launcher)
   int64_t collectives = 0;  // NCCL call counter
+  psc::KTrace kt;           // per-kernel timing (off unless profiling)
 };
+
+namespace psc {
+// RAII bracket of one launch for KTrace (no-op unless ctx->kt.on)
+struct KtScope {
+  psc_ctx* ctx;
+  cudaStream_t s;
+  bool on;
+  KtScope(psc_ctx* c, cudaStream_t st, const char* name, double alg, double layout) : ctx(c), s(st) {
+    on = c && c->kt.on;
+    if (!on) return;
+    KTrace::Rec r{name, c->kt.level, alg, layout, c->kt.get(), c->kt.get()};
+    PSC_CUDA(cudaEventRecordWithFlags(r.e0, s, cudaEventRecordExternal));
+    c->kt.recs.push_back(r);
+  }
+  ~KtScope() {
+    if (on) cudaEventRecordWithFlags(ctx->kt.recs.back().e1, s, cudaEventRecordExternal);
+  }
+};
+}  // namespace psc
 
 struct psc_desc_s {
   psc_ctx* ctx = nullptr;

@@ -31,14 +31,14 @@ def main():
     tot = sum(r[2] for r in body)
     agg = OrderedDict()
     for _, name, us, grid, blk in body:
-        key = name.split("(")[0]
+        key = name.split("(")[0] + (f" g{grid}" if "--by-grid" in sys.argv else "")
         a = agg.setdefault(key, [0, 0.0])
         a[0] += 1
         a[1] += us
     print(f"launches={len(body)} total_us={tot:.1f}")
-    print(f"{'kernel':40s} {'n':>6s} {'total_us':>10s} {'avg_us':>9s} {'share':>7s}")
+    print(f"{'kernel':52s} {'n':>6s} {'total_us':>10s} {'avg_us':>9s} {'share':>7s}")
     for k, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"{k:40s} {n:6d} {us:10.1f} {us / n:9.2f} {100 * us / tot:6.1f}%")
+        print(f"{k[:52]:52s} {n:6d} {us:10.1f} {us / n:9.2f} {100 * us / tot:6.1f}%")
 
 
 if __name__ == "__main__":

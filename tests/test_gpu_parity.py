@@ -252,6 +252,9 @@ VARIANTS = [
     {"PSC_LANES": "8"},
     {"PSC_LANES": "32", "PSC_NO_TMA": "1"},
     {"PSC_RG_MIN": "4", "PSC_RG_DIV": "1"},
+    {"PSC_SORT": "1"},
+    {"PSC_SORT": "1", "PSC_NO_TMA": "1", "PSC_NO_DENSE_COARSE": "1", "PSC_NO_DIA": "1"},
+    {"PSC_RG_SMALL_MB": "200"},
 ]
 
 
