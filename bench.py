@@ -273,6 +273,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-table", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="N > 1: skip the distributed parity check")
+    ap.add_argument("--setup", default="gpu", choices=["gpu", "host"],
+                    help="hierarchy set-up: on the device (psc_amg_build, one GPU) or the host generator")
     ap.add_argument("--krylov", default="pcg", choices=["pcg", "fcg"])
     ap.add_argument("--coarse-solver", default="sweeps", choices=["sweeps", "pcg"])
     ap.add_argument("--vbm", action="store_true", help="the paper's VBM solve: --krylov fcg --coarse-solver pcg")
@@ -315,12 +318,33 @@ def main():
         if G % px or G % py or G % pz:
             raise SystemExit(f"--global-grid {G} not divisible by the rank grid {(px, py, pz)}")
         grid = (G, G, G)
+    # N > 1: the distributed path checked against the oracle first (tests/dist_worker.py,
+    # test infrastructure; outside the timed region) on a small global grid with this
+    # run's rank-box layout (8 GPUs: 2 x 2 x 2), reported as "parity" in the line
+    parity = None
+    if N > 1 and not args.no_parity:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import dist_worker
+        pg = (16 * px, 16 * py, 16 * pz)
+        t_p = time.perf_counter()
+        ok, pout = dist_worker.check(pg, (px, py, pz), "poisson", "/dev/shm", rank, N, local, full=False)
+        parity = {"ok": ok, "grid": list(pg), "procs": [px, py, pz], "seconds": round(time.perf_counter() - t_p, 1),
+                  "check": "tests/dist_worker.py: SpMV of every level matrix, V-cycle, PCG (tol 1e-8) on the "
+                           "distributed GPU path vs the CPU oracle on the global hierarchy (north-star bar)"}
+        if rank == 0:
+            parity.update({k: pout.get(k) for k in ("vcycle_rel", "hist_rel", "x_rel", "iters_gpu", "iters_oracle",
+                                                      "hist_identical_across_ranks")})
+            parity["spmv_max_rel"] = max(v for k, v in pout.items() if k.startswith("spmv_"))
+
     t_setup0 = time.perf_counter()
     h = None
+    # one GPU: the hierarchy is built on the device from A_0 (psc_amg_build, NEXT-1);
+    # several GPUs (decoupled per-rank set-up) or --unsmoothed-p: the host generator
+    device_setup = (N == 1 and args.setup == "gpu" and not args.unsmoothed_p)
     if N == 1:
-        h = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem, smooth=not args.unsmoothed_p)
+        h = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem, smooth=not args.unsmoothed_p,
+                                     max_levels=1 if device_setup else 20)
         levels = pscgen.rank_levels(h, 0)
-        oc = h.operator_complexity()
     else:
         shm = (f"/dev/shm/psc_bench_{args.problem}_{grid[0]}x{grid[1]}x{grid[2]}_{px}{py}{pz}"
                + ("_tentP" if args.unsmoothed_p else ""))
@@ -341,7 +365,17 @@ def main():
         uid = obj[0]
     ctx = psc.Context(rank=rank, nranks=N, device=local, unique_id=uid)
     t1 = time.perf_counter()
-    H, descs, A, P, R = psc.build_hierarchy(ctx, levels, coarse_solver=args.coarse_solver, **_cycle_kw(args))
+    amg_info = None
+    if device_setup:
+        S = psc.AmgSetup(ctx, h.levels[0].A)
+        amg_info = S.info()
+        H = S.hierarchy(coarse_solver=args.coarse_solver, **_cycle_kw(args))
+        oc = sum(amg_info["nnz_A"]) / amg_info["nnz_A"][0]
+        h = None  # the oracle baseline below regenerates a host hierarchy
+    else:
+        H, descs, A, P, R = psc.build_hierarchy(ctx, levels, coarse_solver=args.coarse_solver, **_cycle_kw(args))
+        if N == 1:
+            oc = h.operator_complexity()
     t_build = time.perf_counter() - t1
     info = H.info()
     n_loc = info["n_owned"][0]
@@ -460,6 +494,8 @@ def main():
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         import oracle
         cores = oracle.set_threads(oracle_threads())
+        if h is None:  # same rules, host generator (equal to the device set-up up to rounding)
+            h = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem)
         bcpu = pscgen.rhs_poisson(grid, 0, n_global)
         s_it, tc = oracle_seconds_per_iteration(args, h, bcpu)
         cpu = {"value": n_global / s_it / 1e6, "unit": "Mdof*iters/s", "cores": cores, "kind": "oracle",
@@ -490,9 +526,13 @@ def main():
                 "solve_s_median": statistics.median(solve_s), "solve_s_per_step": solve_s,
                 "rhs": "b_k = (k+1) h^2 1, x0 = 0", "parallelism": f"dp{N} row-block",
                 "l2": "inputs larger than L2 (A_0 alone ~1.4 GB/GPU vs 126 MB L2)",
-                "setup_s": {"generate": round(t_gen, 2), "create_assemble_hier": round(t_build, 2)},
+                "setup_s": {"generate": round(t_gen, 2), "create_assemble_hier": round(t_build, 2),
+                            "where": "device (psc_amg_build)" if device_setup else "host generator (pscgen)",
+                            "device_amg": ({k: round(v, 3) for k, v in amg_info["seconds"].items()}
+                                           if amg_info else None),
+                            "phase1_rounds": amg_info["mis_rounds"] if amg_info else None},
                 "model": "none (sparse solver)"},
-            "roofline": roof, "kernel_table": ktab, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "kernel_table": ktab, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "gpu_launches": sum(s["kernel_launches"] for s in stats),
             "launches_per_iteration": stats[0]["iter_graph_nodes"],
             "halo_path": {0: "single rank", 1: "NVLink peer stores (CUDA IPC)", 2: "NCCL"}[stats[0]["halo_path"]],

@@ -287,6 +287,55 @@ int psc_hier_kernel_profile(psc_hier* h, int method, const double* b_dev, int it
 
 void psc_hier_destroy(psc_hier* h);
 
+/* ---------------------------------------------------------------------------------
+ * AMG set-up on the device.  The paper builds
+ * the hierarchy "mostly on the CPU side" and names GPU set-up as future
+ * work; here every step runs in CUDA kernels on ctx's device:
+ *   decoupled Vanek-Mandel-Brezina aggregation, strong set N_i(theta) =
+ *     {j != i : |a_ij| >= theta sqrt(a_ii a_jj)} (phase 1 = the VMB root rule
+ *     in increasing index, computed in parallel rounds (reading R26); phase 2 = the
+ *     strongest strong neighbour's aggregate (R18));
+ *   tentative prolongator of Eq. (3) with w = 1, smoothed
+ *     P = (I - omega D^-1 A) P^, omega = 1/||D^-1 A||_inf;
+ *   R = P^T; Galerkin A_{l+1} = R A_l P;
+ *   stop when n_l <= coarse_target, at max_levels, or when aggregation would keep
+ *     more than stall_ratio n_l nodes (R19).
+ * Each value is computed in the order the definitions state with one IEEE rounding per
+ * operation (no FMA contraction), so a sequential implementation reproduces it bit
+ * for bit. */
+typedef struct psc_amg_s psc_amg;
+typedef struct {
+  double theta;           /* strength threshold (R17: 0.01) */
+  int max_levels;         /* 20 */
+  int64_t coarse_target;  /* 200 */
+  double stall_ratio;     /* 0.75 */
+} psc_amg_opts;
+
+/* [one rank] Build the hierarchy of A_0 (n x n, host CSR: int64 row_ptr[n+1], int64
+ * col (strictly increasing per row, in [0, n)), f64 val; copied, the caller keeps
+ * its arrays).  opts may be NULL (defaults above).  Errors: PSC_ERR_ARG (malformed
+ * CSR, a row without a positive diagonal, bad options), PSC_ERR_STATE (nranks > 1),
+ * PSC_ERR_CUDA / PSC_ERR_NOMEM. */
+int psc_amg_build(psc_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                  const psc_amg_opts* opts, psc_amg** out);
+/* Sizes and timings.  Arrays (each may be NULL) hold >= *nlevels entries: rows,
+ * nnz(A_l), nnz(P_l) (0 at the coarsest), omega_l, phase-1 rounds; seconds[5] =
+ * aggregation, prolongator, transpose, Galerkin, total (host wall clock around the
+ * device work, synchronised). */
+int psc_amg_info(psc_amg* a, int* nlevels, int64_t* n, int64_t* nnz_A, int64_t* nnz_P, double* omega,
+                 int* mis_rounds, double* seconds);
+/* Copy level `level`'s matrix (kind 0 = A_l, 1 = P_l, 2 = R_l; P/R absent at the
+ * coarsest level: PSC_ERR_STATE) to host arrays sized from psc_amg_info (row_ptr:
+ * rows + 1; col, val: nnz).  Any pointer may be NULL. */
+int psc_amg_level_csr(psc_amg* a, int level, int kind, int64_t* row_ptr, int64_t* col, double* val);
+/* Aggregate of each node of level `level` (< nlevels - 1) and its root flags (1 = root). */
+int psc_amg_aggregates(psc_amg* a, int level, int64_t* agg, int8_t* root);
+/* Descriptors, assembled matrices and psc_hier_create over the set-up's levels
+ * (once per set-up).  The hierarchy uses matrices owned by `a`: destroy it before
+ * psc_amg_destroy. */
+int psc_amg_hier_create(psc_amg* a, const psc_cycle_opts* opts, psc_hier** out);
+void psc_amg_destroy(psc_amg* a);
+
 #ifdef __cplusplus
 }
 #endif

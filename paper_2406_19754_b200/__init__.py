@@ -100,6 +100,18 @@ _sig("psc_hier_kernel_profile", _i32, [_vp, _i32, _vp, _i32, _vp, _i32, _P(_i32)
 _sig("psc_hier_destroy", None, [_vp])
 
 
+class AmgOpts(ctypes.Structure):
+    _fields_ = [("theta", _f64), ("max_levels", _i32), ("coarse_target", _i64), ("stall_ratio", _f64)]
+
+
+_sig("psc_amg_build", _i32, [_vp, _i64, _vp, _vp, _vp, _P(AmgOpts), _P(_vp)])
+_sig("psc_amg_info", _i32, [_vp, _P(_i32), _vp, _vp, _vp, _vp, _vp, _vp])
+_sig("psc_amg_level_csr", _i32, [_vp, _i32, _i32, _vp, _vp, _vp])
+_sig("psc_amg_aggregates", _i32, [_vp, _i32, _vp, _vp])
+_sig("psc_amg_hier_create", _i32, [_vp, _P(CycleOpts), _P(_vp)])
+_sig("psc_amg_destroy", None, [_vp])
+
+
 class PscError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"{_lib.psc_status_string(code).decode()}: {msg}")
@@ -307,13 +319,17 @@ class Hierarchy:
         _check(_lib.psc_hier_vcycle(self.handle, _dev_ptr(r, self.n0, "r"), _dev_ptr(z, self.n0, "z")), self.ctx)
         return z
 
+    def _n(self, level):
+        ln = getattr(self, "_level_n", None)
+        return ln[level] if ln else self.A[level].rows.n_owned
+
     def dinv(self, level, out):
-        n = self.A[level].rows.n_owned
+        n = self._n(level)
         _check(_lib.psc_hier_dinv(self.handle, level, _dev_ptr(out, n, "out")), self.ctx)
         return out
 
     def smooth(self, level, b, x, nsweeps):
-        n = self.A[level].rows.n_owned
+        n = self._n(level)
         _check(_lib.psc_hier_smooth(self.handle, level, _dev_ptr(b, n, "b"), _dev_ptr(x, n, "x"), int(nsweeps)),
                self.ctx)
         return x
@@ -365,6 +381,87 @@ class Hierarchy:
     def close(self):
         if self.handle:
             _lib.psc_hier_destroy(self.handle)
+            self.handle = None
+
+
+class AmgSetup:
+    """psc_amg_build: the VMB set-up (aggregation, smoothed P, R = P^T, Galerkin RAP) on
+    the device from a host CSR A_0 (one rank).  hierarchy() -> Hierarchy over its levels."""
+
+    _MAXL = 64
+
+    def __init__(self, ctx: Context, A0, theta=0.01, max_levels=20, coarse_target=200, stall_ratio=0.75):
+        if hasattr(A0, "indptr"):
+            A0 = A0.tocsr()
+            A0.sort_indices()
+            ptr, col, val = A0.indptr, A0.indices, A0.data
+        else:
+            ptr, col, val = A0.ptr, A0.col, A0.val
+        ptr, col, val = _host(ptr, np.int64, "ptr"), _host(col, np.int64, "col"), _host(val, np.float64, "val")
+        o = AmgOpts(float(theta), int(max_levels), int(coarse_target), float(stall_ratio))
+        h = _vp()
+        _check(_lib.psc_amg_build(ctx.handle, len(ptr) - 1, ptr.ctypes.data, col.ctypes.data, val.ctypes.data,
+                                  ctypes.byref(o), ctypes.byref(h)), ctx)
+        self.ctx, self.handle = ctx, h.value
+        self._hier = None
+        ctx._children.append(self)
+
+    def info(self):
+        M = self._MAXL
+        nl = _i32()
+        n, nA, nP = (np.zeros(M, np.int64) for _ in range(3))
+        om = np.zeros(M)
+        rounds = np.zeros(M, np.int32)
+        secs = np.zeros(5)
+        _check(_lib.psc_amg_info(self.handle, ctypes.byref(nl), n.ctypes.data, nA.ctypes.data, nP.ctypes.data,
+                                 om.ctypes.data, rounds.ctypes.data, secs.ctypes.data), self.ctx)
+        L = nl.value
+        return dict(nlevels=L, n=n[:L].tolist(), nnz_A=nA[:L].tolist(), nnz_P=nP[:L].tolist(),
+                    omega=om[:L].tolist(), mis_rounds=rounds[:L].tolist(),
+                    seconds=dict(zip(("aggregate", "prolongator", "transpose", "galerkin", "total"), secs.tolist())))
+
+    def csr(self, level, kind):
+        """(ptr, col, val) of A_l (kind "A"), P_l ("P") or R_l ("R") copied to the host."""
+        k = {"A": 0, "P": 1, "R": 2}[kind]
+        inf = self.info()
+        n = inf["n"][level]
+        rows = {0: n, 1: n, 2: inf["n"][level + 1] if level + 1 < inf["nlevels"] else 0}[k]
+        ptr = np.zeros(rows + 1, np.int64)
+        _check(_lib.psc_amg_level_csr(self.handle, level, k, ptr.ctypes.data, None, None), self.ctx)
+        col = np.zeros(int(ptr[-1]), np.int64)
+        val = np.zeros(int(ptr[-1]))
+        _check(_lib.psc_amg_level_csr(self.handle, level, k, None, col.ctypes.data, val.ctypes.data), self.ctx)
+        return ptr, col, val
+
+    def aggregates(self, level):
+        n = self.info()["n"][level]
+        agg = np.zeros(n, np.int64)
+        root = np.zeros(n, np.int8)
+        _check(_lib.psc_amg_aggregates(self.handle, level, agg.ctypes.data, root.ctypes.data), self.ctx)
+        return agg, root.astype(bool)
+
+    def hierarchy(self, pre=4, post=4, coarse=30, coarse_solver="sweeps", coarse_maxit=40, coarse_tol=1e-10,
+                  variable_v=False) -> "Hierarchy":
+        if coarse_solver not in _COARSE:
+            raise ValueError(f"coarse_solver must be one of {sorted(_COARSE)}")
+        opts = CycleOpts(pre, post, coarse, _COARSE[coarse_solver], int(coarse_maxit), float(coarse_tol),
+                         1 if variable_v else 0)
+        h = _vp()
+        _check(_lib.psc_amg_hier_create(self.handle, ctypes.byref(opts), ctypes.byref(h)), self.ctx)
+        H = Hierarchy.__new__(Hierarchy)
+        H.ctx, H.handle, H.nlevels = self.ctx, h.value, self.info()["nlevels"]
+        H.A, H.P, H.R = [], [], []
+        H._level_n = self.info()["n"]
+        H.n0 = H._level_n[0]
+        self._hier = H
+        return H
+
+    def close(self):
+        if self.handle:
+            if self._hier is not None:
+                self._hier.close()
+                self._hier = None
+            _lib.psc_amg_destroy(self.handle)
             self.handle = None
 
 

@@ -370,7 +370,14 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     launch_dense_gemv(ctx, h->dsuf, LV[l].n, b, LV[l].x[0], s);
     return LV[l].x[0];
   }
-  if (l == Lend - 1) return coarse_solve(h, LV[l], b, s);
+  if (l == Lend - 1) {
+    double* xc = coarse_solve(h, LV[l], b, s);
+    // a one-level hierarchy: the coarsest solver is the whole V-cycle, so (r, z) of
+    // the Krylov iteration is reduced here (otherwise by the last level-0 post-sweep)
+    if (dist && l == 0)
+      launch_dot(ctx, LV[0].n, h->rz_weight ? h->rz_weight : b, xc, &h->red1, scal_mine(h, S_RZ), s);
+    return xc;
+  }
   LevelWS& W = LV[l];
   LevelWS& C = LV[l + 1];
   const bool time_here = timing && dist && l == 0;

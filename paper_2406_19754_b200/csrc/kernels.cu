@@ -95,7 +95,8 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NR], double* partials,
 }
 
 constexpr int kHdr = 16;     // int32 words per slice header
-constexpr int kMaxDia = 8;   // most diagonals a DIA slice may have (header words 6..13)
+constexpr int kMaxDiaHdr = 8;  // DIA offsets also held in the slice header (words 6..13)
+constexpr int kMaxDia = 64;    // most diagonals a DIA slice may have (all in its column region)
 enum SliceKind : int { kEll = 0, kDia = 1 };
 
 __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int64_t s, int lane) {
@@ -162,8 +163,33 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
       case 6: return dia_sum<6, CG>(h, i, v, x, nc, keep);
       case 7: return dia_sum<7, CG>(h, i, v, x, nc, keep);
       case 8: return dia_sum<8, CG>(h, i, v, x, nc, keep);
-      default: return 0.0;
+      default: break;
     }
+    // wide DIA slice (level-1 Galerkin operators): the offsets, shared by the warp,
+    // from the slice's column region (broadcast loads); the 32 lanes gather 32
+    // consecutive entries of x per diagonal (coalesced, unlike ELL's scattered columns)
+    const int64_t cbd = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
+                        (uint32_t)__shfl_sync(0xffffffffu, h, 2);
+    const int32_t* offs = col + cbd;
+    double sum = 0.0;
+    int k = 0;
+    for (; k + 8 <= w; k += 8) {
+      double vi[8], xv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) vi[j] = ldm(v + 32 * (k + j), keep);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t c = i + (uint32_t)__ldg(offs + k + j);
+        xv[j] = ldx<CG>(x + (c < nc ? c : 0u));
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum = fma(vi[j], xv[j], sum);
+    }
+    for (; k < w; ++k) {
+      const uint32_t c = i + (uint32_t)__ldg(offs + k);
+      sum = fma(ldm(v + 32 * k, keep), ldx<CG>(x + (c < nc ? c : 0u)), sum);
+    }
+    return sum;
   }
   const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
                      (uint32_t)__shfl_sync(0xffffffffu, h, 2);
@@ -1760,7 +1786,7 @@ __device__ __forceinline__ int32_t map_col(int64_t g, int64_t own_begin, int64_t
 // (8 B x 32 d value slots beat 12 B x 32 w value+column slots).
 __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_t* __restrict__ rowptr,
                                   const int64_t* __restrict__ colg, int64_t own_begin, int64_t n_own, int allow_dia,
-                                  const uint8_t* __restrict__ perm, int64_t* __restrict__ vslots,
+                                  int max_dia, const uint8_t* __restrict__ perm, int64_t* __restrict__ vslots,
                                   int64_t* __restrict__ cslots, int64_t* __restrict__ snnz, int32_t* __restrict__ bflag,
                                   int32_t* __restrict__ dia_d, int32_t* __restrict__ dia_off) {
   const int lane = threadIdx.x & 31;
@@ -1785,7 +1811,7 @@ __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_
   }
   off = __any_sync(0xffffffffu, off);
   int d = 0;
-  if (allow_dia && !off && w > 0 && w <= kMaxDia) {
+  if (allow_dia && !off && w > 0 && w <= max_dia) {
     int q = 0;
     bool ok = true;
     for (;;) {
@@ -1793,7 +1819,7 @@ __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_
       long long mn = my;
       for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
       if (mn == LLONG_MAX) break;
-      if (d == kMaxDia) {
+      if (d == max_dia) {
         ok = false;
         break;
       }
@@ -1966,10 +1992,9 @@ __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ pt
   const int d = dia_d[s];
   h[5] = d > 0 ? kDia : kEll;
   int j0 = -1;
-  for (int j = 0; j < kMaxDia; ++j) {
-    h[6 + j] = j < d ? dia_off[s * kMaxDia + j] : 0;
-    if (j < d && dia_off[s * kMaxDia + j] == 0) j0 = j;
-  }
+  for (int j = 0; j < kMaxDiaHdr; ++j) h[6 + j] = j < d ? dia_off[s * kMaxDia + j] : 0;
+  for (int j = 0; j < d; ++j)
+    if (dia_off[s * kMaxDia + j] == 0) j0 = j;
   h[14] = j0;  // DIA: slot of the diagonal (offset 0), -1 if none
   h[15] = 0;
 }
@@ -2001,13 +2026,18 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     int32_t* d_flag = dalloc<int32_t>(nu);
     int32_t* d_diad = dalloc<int32_t>(nu);
     int32_t* d_diaoff = dalloc<int32_t>((size_t)nu * kMaxDia);
+    // DIA slices with up to 8 diagonals (offsets in the slice header; A_0).  Wider DIA
+    // slices (up to kMaxDia, offsets in the column region) are opt-in, PSC_DIA_MAX=64:
+    // on the level-1 Galerkin operator of 256^3 they measured slower (175 vs 154 us per
+    // sweep: more gathers per row for the zeros of the diagonals than ELL's padding)
+    const int max_dia = std::max(1, std::min(kMaxDia, env_int("PSC_DIA_MAX", kMaxDiaHdr)));
     auto widths = [&](bool dia, const uint8_t* perm) {
       PSC_CUDA(cudaMemsetAsync(d_vs, 0, sizeof(int64_t) * (nu + 1), s));
       PSC_CUDA(cudaMemsetAsync(d_cs, 0, sizeof(int64_t) * (nu + 1), s));
       if (nu > 0) {
         sell_width_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
-            n_rows, nu, d_rowptr, d_colg, own_begin, n_own, dia ? 1 : 0, perm, d_vs, d_cs, d_snnz, d_flag, d_diad,
-            d_diaoff);
+            n_rows, nu, d_rowptr, d_colg, own_begin, n_own, dia ? 1 : 0, max_dia, perm, d_vs, d_cs, d_snnz, d_flag,
+            d_diad, d_diaoff);
         PSC_CUDA(cudaGetLastError());
       }
       if (!S.ptr) S.ptr = dalloc<int64_t>(nu + 1);

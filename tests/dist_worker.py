@@ -21,10 +21,6 @@ from _util import ew_err  # noqa: E402
 
 
 def main():
-    import bench
-    import paper_2406_19754_b200 as psc
-    import pscgen
-
     grid = tuple(int(v) for v in os.environ.get("PSC_TEST_GRID", "32,32,64").split(","))
     procs = tuple(int(v) for v in os.environ.get("PSC_TEST_PROCS", "1,1,2").split(","))
     problem = os.environ.get("PSC_TEST_PROBLEM", "poisson")
@@ -33,6 +29,22 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     shm = os.environ.get("PSC_TEST_SHM") or tempfile.gettempdir()
+    ok, out = check(grid, procs, problem, shm, rank, world, local, full=True)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+def check(grid, procs, problem, shm, rank, world, local, full=True):
+    """The distributed CUDA path against the oracle on the global hierarchy (rank 0
+    compares).  Needs an initialised torch.distributed process group; returns
+    (ok on every rank, result dict on rank 0).  full=False: SpMV, V-cycle and PCG
+    only (no VBM / variable-cycle legs)."""
+    import bench
+    import paper_2406_19754_b200 as psc
+    import pscgen
+
     d = os.path.join(shm, f"psc_dist_{grid[0]}x{grid[1]}x{grid[2]}_{procs}_{problem}".replace(" ", ""))
     h = None
     if rank == 0:
@@ -70,25 +82,27 @@ def main():
     rc, st, hist = H.solve(torch.from_numpy(b[r0:r1].copy()).cuda(), x, tol=1e-8, maxit=200)
     parts = [None] * world
     dist.all_gather_object(parts, (z.cpu().numpy(), x.cpu().numpy(), rc, st["iters"], hist))
-    # the paper's VBM solve (NEXT-2): coarsest PCG(<= 40) with l1-Jacobi + FCG, on
-    # the same matrices (a general-form coarse PCG with all-gathers when the
-    # coarsest level is distributed, PSC_REPL_ROWS=0)
-    H2 = psc.Hierarchy(ctx, A, P, R, coarse_solver="pcg")
-    z2 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
-    H2.vcycle(torch.from_numpy(b[r0:r1].copy()).cuda(), z2)
-    x2 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
-    rc2, st2, hist2 = H2.solve(torch.from_numpy(b[r0:r1].copy()).cuda(), x2, tol=1e-8, maxit=200, method="fcg")
-    parts2 = [None] * world
-    dist.all_gather_object(parts2, (z2.cpu().numpy(), x2.cpu().numpy(), rc2, st2["iters"], hist2))
-    H2.close()
-    # the variable V-cycle (P:330 footnote): 2 sweeps at level 0, doubled per level,
-    # through the distributed levels and the replicated suffix alike
-    H3 = psc.Hierarchy(ctx, A, P, R, pre=2, post=2, variable_v=True)
-    z3 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
-    H3.vcycle(torch.from_numpy(b[r0:r1].copy()).cuda(), z3)
-    parts3 = [None] * world
-    dist.all_gather_object(parts3, z3.cpu().numpy())
-    H3.close()
+    parts2 = parts3 = None
+    if full:
+        # the paper's VBM solve (NEXT-2): coarsest PCG(<= 40) with l1-Jacobi + FCG, on
+        # the same matrices (a general-form coarse PCG with all-gathers when the
+        # coarsest level is distributed, PSC_REPL_ROWS=0)
+        H2 = psc.Hierarchy(ctx, A, P, R, coarse_solver="pcg")
+        z2 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+        H2.vcycle(torch.from_numpy(b[r0:r1].copy()).cuda(), z2)
+        x2 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+        rc2, st2, hist2 = H2.solve(torch.from_numpy(b[r0:r1].copy()).cuda(), x2, tol=1e-8, maxit=200, method="fcg")
+        parts2 = [None] * world
+        dist.all_gather_object(parts2, (z2.cpu().numpy(), x2.cpu().numpy(), rc2, st2["iters"], hist2))
+        H2.close()
+        # the variable V-cycle (P:330 footnote): 2 sweeps at level 0, doubled per level,
+        # through the distributed levels and the replicated suffix alike
+        H3 = psc.Hierarchy(ctx, A, P, R, pre=2, post=2, variable_v=True)
+        z3 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+        H3.vcycle(torch.from_numpy(b[r0:r1].copy()).cuda(), z3)
+        parts3 = [None] * world
+        dist.all_gather_object(parts3, z3.cpu().numpy())
+        H3.close()
     ok = True
     if rank == 0:
         import oracle
@@ -118,30 +132,30 @@ def main():
         out["hist_identical_across_ranks"] = same_hist
         ok &= (len(its) == 1 and abs(parts[0][3] - ito) <= 1 and all(p[2] == 0 for p in parts)
                and out["hist_rel"] <= 1e-9 and out["x_rel"] <= 1e-7 and same_hist)
-        zg2 = np.concatenate([p[0] for p in parts2])
-        zo2 = oracle.vcycle(h, b, coarse_pcg=True)
-        out["vbm_vcycle_rel"] = float(ew_err(zg2, zo2))
-        xg2 = np.concatenate([p[1] for p in parts2])
-        xo2, ito2, sto2, histo2 = oracle.fcg(h, b, tol=1e-8, maxit=200, coarse_pcg=True)
-        its2 = {p[3] for p in parts2}
-        k2 = min(20, ito2, parts2[0][3]) + 1
-        out.update(vbm_iters_gpu=sorted(its2), vbm_iters_oracle=ito2,
-                   vbm_hist_rel=float(np.max(np.abs(parts2[0][4][:k2] - histo2[:k2]) / histo2[:k2])),
-                   vbm_x_rel=float(np.linalg.norm(xg2 - xo2) / np.linalg.norm(xo2)))
-        ok &= (out["vbm_vcycle_rel"] <= 1e-9 and len(its2) == 1 and abs(parts2[0][3] - ito2) <= 1
-               and all(p[2] == 0 for p in parts2) and out["vbm_hist_rel"] <= 1e-9 and out["vbm_x_rel"] <= 1e-7
-               and all(np.array_equal(parts2[0][4], p[4]) for p in parts2))
-        zg3 = np.concatenate(parts3)
-        zo3 = oracle.vcycle(h, b, 2, 2, 30, variable_v=True)
-        out["varv_vcycle_rel"] = float(ew_err(zg3, zo3))
-        ok &= out["varv_vcycle_rel"] <= 1e-12
+        if full:
+            zg2 = np.concatenate([p[0] for p in parts2])
+            zo2 = oracle.vcycle(h, b, coarse_pcg=True)
+            out["vbm_vcycle_rel"] = float(ew_err(zg2, zo2))
+            xg2 = np.concatenate([p[1] for p in parts2])
+            xo2, ito2, sto2, histo2 = oracle.fcg(h, b, tol=1e-8, maxit=200, coarse_pcg=True)
+            its2 = {p[3] for p in parts2}
+            k2 = min(20, ito2, parts2[0][3]) + 1
+            out.update(vbm_iters_gpu=sorted(its2), vbm_iters_oracle=ito2,
+                       vbm_hist_rel=float(np.max(np.abs(parts2[0][4][:k2] - histo2[:k2]) / histo2[:k2])),
+                       vbm_x_rel=float(np.linalg.norm(xg2 - xo2) / np.linalg.norm(xo2)))
+            ok &= (out["vbm_vcycle_rel"] <= 1e-9 and len(its2) == 1 and abs(parts2[0][3] - ito2) <= 1
+                   and all(p[2] == 0 for p in parts2) and out["vbm_hist_rel"] <= 1e-9 and out["vbm_x_rel"] <= 1e-7
+                   and all(np.array_equal(parts2[0][4], p[4]) for p in parts2))
+            zg3 = np.concatenate(parts3)
+            zo3 = oracle.vcycle(h, b, 2, 2, 30, variable_v=True)
+            out["varv_vcycle_rel"] = float(ew_err(zg3, zo3))
+            ok &= out["varv_vcycle_rel"] <= 1e-12
         out["ok"] = bool(ok)
-        print(json.dumps(out), flush=True)
     flag = [ok]
     dist.broadcast_object_list(flag, src=0)
+    H.close()
     ctx.close()
-    dist.destroy_process_group()
-    sys.exit(0 if flag[0] else 1)
+    return bool(flag[0]), out
 
 
 if __name__ == "__main__":

@@ -33,7 +33,8 @@ def test_binding_names_match_header():
     import paper_2406_19754_b200 as psc
     for s in declared_symbols():
         assert getattr(psc._lib, s).restype is not None or s in ("psc_finalize", "psc_desc_destroy",
-                                                                  "psc_mat_destroy", "psc_hier_destroy")
+                                                                  "psc_mat_destroy", "psc_hier_destroy",
+                                                                  "psc_amg_destroy")
 
 
 def test_status_strings_and_version():

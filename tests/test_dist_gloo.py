@@ -88,9 +88,15 @@ def _worker(rank, world, port, shm, grid, procs, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("grid,procs", [((8, 8, 8), (1, 1, 2)), ((12, 8, 8), (2, 1, 1))])
-def test_two_rank_gloo_halo_plan_and_bench_inputs(grid, procs):
-    world = 2
+@pytest.mark.parametrize("grid,procs", [((8, 8, 8), (1, 1, 2)), ((12, 8, 8), (2, 1, 1)), ((8, 8, 8), (1, 2, 2)),
+                                        ((8, 8, 8), (2, 2, 2))],
+                         ids=["2ranks_z", "2ranks_x", "4ranks", "8ranks_2x2x2"])
+def test_multi_rank_gloo_halo_plan_and_bench_inputs(grid, procs):
+    """2, 4 and 8 processes (the 8-GPU layout 2 x 2 x 2 of bench.py, where every level-0
+    rank box has 3 neighbours and an x split)."""
+    world = procs[0] * procs[1] * procs[2]
+    import bench
+    assert bench.procs_for(world) == procs or world == 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     with tempfile.TemporaryDirectory() as shm:
@@ -101,7 +107,7 @@ def test_two_rank_gloo_halo_plan_and_bench_inputs(grid, procs):
         for p in ps:
             p.join(timeout=240)
         res = dict(q.get(timeout=5) for _ in range(world))
-    assert res == {0: "ok", 1: "ok"}, res
+    assert res == {r: "ok" for r in range(world)}, res
 
 
 def test_spec_descriptor_example_1d_laplacian():
