@@ -181,7 +181,16 @@ typedef struct {
   int coarse_maxit;
   double coarse_tol;
   int variable_v;     /* 0 = V-cycle, 1 = variable V-cycle (P:330 footnote) */
+  int smoother;       /* PSC_SMOOTHER_L1JACOBI (0) or PSC_SMOOTHER_AINV (1) on the levels < L-1 */
+  double ainv_drop;   /* AINV drop tolerance (entries |z_kj| < ainv_drop dropped; reading R27) */
 } psc_cycle_opts;
+
+/* Smoothers (Sec. 2.3.2).  AINV: M^-1 = Z D^-1 Z^T from an incomplete
+ * A-biconjugation of A_l (W = Z for SPD A, reading R27), built on the host from the
+ * matrix's host copy and applied on the device as two SpMVs (Z^T, then Z): a sweep
+ * is r = b - A x, u = D^-1 Z^T r, x += Z u.  One rank (the paper's block-Jacobi form
+ * across ranks is not built: PSC_ERR_STATE). */
+enum { PSC_SMOOTHER_L1JACOBI = 0, PSC_SMOOTHER_AINV = 1 };
 
 /* [collective] AMG hierarchy handle over given level matrices (D10/D11 in
  * SURVEY.md): A[0..nlevels-1], P[0..nlevels-2], R[0..nlevels-2] (R_l = P_l^T given
@@ -286,6 +295,23 @@ int psc_hier_kernel_profile(psc_hier* h, int method, const double* b_dev, int it
                             int max_recs, int* n_recs);
 
 void psc_hier_destroy(psc_hier* h);
+
+/* Structure-preserving coefficient update ("interfaces that allow to update
+ * data coefficients in an existing matrix if the structure is preserved"): val_host
+ * holds nnz values in the CSR order the matrix was created with (same row_ptr and
+ * columns).  Before assembly the staged values are replaced; after assembly the
+ * device sliced-ELL values (and the host copy, if kept) are.  Hierarchies using the
+ * matrix see the new values at their next kernel; their smoothers do not change until
+ * psc_hier_rebuild_smoothers.  Errors: PSC_ERR_ARG. */
+int psc_mat_update_values(psc_mat* m, const double* val_host);
+
+/* [collective] Rebuild every level's smoother from the current values of A_l (the
+ * second step of the split build: "the construction of the smoothers ...
+ * can be executed multiple times reusing an already assembled hierarchy"): l1
+ * diagonals, AINV factors, the dense coarsest copy and the dense suffix operator; the
+ * hierarchy (A_l, P_l, R_l) is reused as it is.  A replicated coarse suffix (several
+ * ranks) keeps its copies: PSC_ERR_STATE. */
+int psc_hier_rebuild_smoothers(psc_hier* h);
 
 /* ---------------------------------------------------------------------------------
  * AMG set-up on the device.  The paper builds

@@ -62,7 +62,8 @@ class _Hier(ctypes.Structure):
     _fields_ = [("nlevels", ctypes.c_int), ("A", ctypes.POINTER(_CSR)), ("P", ctypes.POINTER(_CSR)),
                 ("R", ctypes.POINTER(_CSR)), ("pre", ctypes.c_int), ("post", ctypes.c_int),
                 ("coarse", ctypes.c_int), ("coarse_pcg", ctypes.c_int), ("coarse_maxit", ctypes.c_int),
-                ("coarse_tol", ctypes.c_double), ("variable_v", ctypes.c_int)]
+                ("coarse_tol", ctypes.c_double), ("variable_v", ctypes.c_int), ("smoother", ctypes.c_int),
+                ("ainv_drop", ctypes.c_double)]
 
 
 def lib():
@@ -110,7 +111,7 @@ class _CsrHolder:
 
 class _HierHolder:
     def __init__(self, hier, pre=4, post=4, coarse=30, coarse_pcg=False, coarse_maxit=40, coarse_tol=1e-10,
-                 variable_v=False):
+                 variable_v=False, smoother="l1", ainv_drop=0.1):
         L = hier.nlevels
         self.A = [_CsrHolder(hier.levels[l].A) for l in range(L)]
         self.P = [_CsrHolder(hier.levels[l].P) for l in range(L - 1)]
@@ -118,8 +119,10 @@ class _HierHolder:
         self.Aa = (_CSR * L)(*[h.c for h in self.A])
         self.Pa = (_CSR * max(L - 1, 1))(*[h.c for h in self.P])
         self.Ra = (_CSR * max(L - 1, 1))(*[h.c for h in self.R])
+        if smoother not in ("l1", "ainv"):
+            raise ValueError("smoother must be 'l1' or 'ainv'")
         self.c = _Hier(L, self.Aa, self.Pa, self.Ra, pre, post, coarse, 1 if coarse_pcg else 0, coarse_maxit,
-                       coarse_tol, 1 if variable_v else 0)
+                       coarse_tol, 1 if variable_v else 0, 1 if smoother == "ainv" else 0, float(ainv_drop))
 
 
 def spmv(A, x) -> np.ndarray:
@@ -341,3 +344,28 @@ def amg_setup(A0, theta=0.01, max_levels=20, coarse_target=200, stall_ratio=0.75
         L.P, L.R, L.agg, L.root, L.omega = P, R, agg, root, om
         levels.append(SetupLevel(Ac, crs))
     return SetupHierarchy(levels)
+
+
+# ------------------------------------------------------------------ NEXT-4 AINV
+def ainv(A, drop_tol=0.1, row_start=None):
+    """AINV factors (reading R27): A^-1 ~ Z D^-1 Z^T, Z unit upper triangular
+    (returned as scipy CSC, columns z_j), D = diag(p).  Block-Jacobi over row_start."""
+    import scipy.sparse as sp
+    L = _setup_sigs()
+    if not getattr(L, "_ainv_sig", False):
+        pp = ctypes.POINTER(ctypes.c_void_p)
+        L.or_ainv.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_double, pp, pp, pp,
+                              ctypes.c_void_p]
+        L.or_ainv.restype = ctypes.c_int
+        L._ainv_sig = True
+    h = _CsrHolder(A)
+    n = h.c.nrows
+    rs = np.array([0, n] if row_start is None else row_start, np.int64)
+    p = np.zeros(n)
+    zp, zr, zv = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    st = L.or_ainv(ctypes.byref(h.c), len(rs) - 1, rs.ctypes.data, float(drop_tol), ctypes.byref(zp),
+                   ctypes.byref(zr), ctypes.byref(zv), p.ctypes.data)
+    Zt = _take_csr(n, n, zp.value, zr.value, zv.value)  # rows of Zt = columns of Z
+    if st != 0:
+        raise RuntimeError(f"AINV breakdown: pivot {-1 - st} <= 0")
+    return sp.csc_matrix((Zt.data, Zt.indices, Zt.indptr), shape=(n, n)), p

@@ -61,7 +61,12 @@ typedef struct {
   int coarse_maxit; /* its iteration cap ("at most 40 iterations") */
   double coarse_tol;/* its relative-residual tolerance (reading R23) */
   int variable_v;   /* 1: variable V-cycle, pre/post sweeps doubled per level (P:330 footnote, R25) */
+  int smoother;     /* 0: l1-Jacobi; 1: AINV (reading R27) on levels < L-1 */
+  double ainv_drop; /* AINV drop tolerance */
 } or_hier;
+
+int or_ainv(const or_csr* A, int nranks, const int64_t* row_start, double drop_tol, int64_t** zptr,
+            int64_t** zrow, double** zval, double* p);
 
 /* y = A x.  Row sums in stored column order. */
 void or_spmv(const or_csr* A, const double* x, double* y) {
@@ -175,6 +180,51 @@ int or_coarse_pcg(const or_csr* A, const double* m, const double* b, double* x, 
   return k;
 }
 
+/* Smoother of one level: l1-Jacobi (m) or AINV (Z by columns, pivots p). */
+typedef struct {
+  double* m;
+  int64_t *zp, *zr;
+  double *zv, *p;
+} or_smoother;
+
+/* x_new = x + M^-1 (b - A x) with the level's smoother (Eq. (2) factor I - M^-1 A);
+ * AINV: M^-1 = Z D^-1 Z^T, D = diag(p) (reading R27) */
+static void smooth_sweep(const or_hier* h, const or_smoother* sm, const or_csr* A, const double* b, const double* x,
+                         double* xnew) {
+  const int64_t n = A->nrows;
+  if (!h->smoother) {
+    or_l1_sweep(A, sm->m, b, x, xnew);
+    return;
+  }
+  double* r = dalloc(n);
+  double* u = dalloc(n);
+  or_spmv(A, x, r);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
+  for (int64_t j = 0; j < n; ++j) { /* u = D^-1 Z^T r */
+    double t = 0.0;
+    for (int64_t q = sm->zp[j]; q < sm->zp[j + 1]; ++q) t += sm->zv[q] * r[sm->zr[q]];
+    u[j] = t / sm->p[j];
+  }
+  for (int64_t k = 0; k < n; ++k) xnew[k] = 0.0; /* Z u, column by column */
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t q = sm->zp[j]; q < sm->zp[j + 1]; ++q) xnew[sm->zr[q]] += sm->zv[q] * u[j];
+  for (int64_t k = 0; k < n; ++k) xnew[k] = x[k] + xnew[k];
+  free(r); free(u);
+}
+
+/* nsweeps smoothing sweeps from x = 0 (reading R6) */
+static void smooth_from_zero(const or_hier* h, const or_smoother* sm, const or_csr* A, const double* b, int nsweeps,
+                             double* x) {
+  const int64_t n = A->nrows;
+  double* w = dalloc(n);
+  memset(x, 0, sizeof(double) * (size_t)n);
+  for (int s = 0; s < nsweeps; ++s) {
+    smooth_sweep(h, sm, A, b, x, w);
+    memcpy(x, w, sizeof(double) * (size_t)n);
+  }
+  free(w);
+}
+
 /* x = B_l b, the V-cycle of Eq. (2) (Sec. 2.3):
  *   I - B_l A_l = (I - M_l^{-T} A_l)(I - P_l B_{l+1} P_l^T A_l)(I - M_l^{-1} A_l),
  * applied to b with x = 0 on entry, i.e. right to left:
@@ -182,13 +232,13 @@ int or_coarse_pcg(const or_csr* A, const double* m, const double* b, double* x, 
  *   coarse: x <- x + P B_{l+1} R (b - A x), R = P^T              (middle factor)
  *   post:   x <- x + M^{-T}(b - A x), `post` times; M diagonal so M^{-T} = M^{-1} (R9)
  * and B_ell at the coarsest level = `coarse` sweeps from zero. */
-static void vcycle_level(const or_hier* h, double* const* m, int l, const double* b, double* x) {
+static void vcycle_level(const or_hier* h, const or_smoother* sm, int l, const double* b, double* x) {
   const or_csr* A = &h->A[l];
   const int64_t n = A->nrows;
   double* w = dalloc(n);
   if (l == h->nlevels - 1) {
-    if (h->coarse_pcg) or_coarse_pcg(A, m[l], b, x, h->coarse_maxit, h->coarse_tol);
-    else or_l1_sweeps_from_zero(A, m[l], b, h->coarse, x, w);
+    if (h->coarse_pcg) or_coarse_pcg(A, sm[l].m, b, x, h->coarse_maxit, h->coarse_tol);
+    else or_l1_sweeps_from_zero(A, sm[l].m, b, h->coarse, x, w);
     free(w);
     return;
   }
@@ -197,7 +247,7 @@ static void vcycle_level(const or_hier* h, double* const* m, int l, const double
    * level l = pre/post * 2^l (reading R25: both pre and post double) */
   const int pre = h->variable_v ? h->pre << l : h->pre;
   const int post = h->variable_v ? h->post << l : h->post;
-  or_l1_sweeps_from_zero(A, m[l], b, pre, x, w);
+  smooth_from_zero(h, &sm[l], A, b, pre, x);
   /* coarse-grid correction */
   const or_csr* R = &h->R[l];
   const or_csr* P = &h->P[l];
@@ -209,7 +259,7 @@ static void vcycle_level(const or_hier* h, double* const* m, int l, const double
   OR_PAR
   for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
   or_spmv(R, r, bc);
-  vcycle_level(h, m, l + 1, bc, xc);
+  vcycle_level(h, sm, l + 1, bc, xc);
   or_spmv(P, xc, r);
   OR_PAR
   for (int64_t i = 0; i < n; ++i) x[i] = x[i] + r[i];
@@ -217,28 +267,37 @@ static void vcycle_level(const or_hier* h, double* const* m, int l, const double
   free(bc);
   free(xc);
   for (int s = 0; s < post; ++s) {
-    or_l1_sweep(A, m[l], b, x, w);
+    smooth_sweep(h, &sm[l], A, b, x, w);
     memcpy(x, w, sizeof(double) * (size_t)n);
   }
   free(w);
 }
 
-static double** make_m(const or_hier* h) {
-  double** m = (double**)calloc((size_t)h->nlevels, sizeof(double*));
+/* the smoothers of every level: l1 diagonal (all levels: also the coarsest solver's),
+ * and AINV factors of the levels < L-1 when h->smoother == 1 (block of one rank) */
+static or_smoother* make_m(const or_hier* h) {
+  or_smoother* sm = (or_smoother*)calloc((size_t)h->nlevels, sizeof(or_smoother));
   for (int l = 0; l < h->nlevels; ++l) {
-    m[l] = dalloc(h->A[l].nrows);
-    or_l1_diag(&h->A[l], m[l]);
+    sm[l].m = dalloc(h->A[l].nrows);
+    or_l1_diag(&h->A[l], sm[l].m);
+    if (h->smoother == 1 && l < h->nlevels - 1) {
+      const int64_t rs[2] = {0, h->A[l].nrows};
+      sm[l].p = dalloc(h->A[l].nrows);
+      or_ainv(&h->A[l], 1, rs, h->ainv_drop, &sm[l].zp, &sm[l].zr, &sm[l].zv, sm[l].p);
+    }
   }
-  return m;
+  return sm;
 }
-static void free_m(const or_hier* h, double** m) {
-  for (int l = 0; l < h->nlevels; ++l) free(m[l]);
-  free(m);
+static void free_m(const or_hier* h, or_smoother* sm) {
+  for (int l = 0; l < h->nlevels; ++l) {
+    free(sm[l].m); free(sm[l].zp); free(sm[l].zr); free(sm[l].zv); free(sm[l].p);
+  }
+  free(sm);
 }
 
 /* z = B_0 r (one V-cycle from x = 0). */
 void or_vcycle(const or_hier* h, const double* r, double* z) {
-  double** m = make_m(h);
+  or_smoother* m = make_m(h);
   vcycle_level(h, m, 0, r, z);
   free_m(h, m);
 }
@@ -259,7 +318,7 @@ int or_pcg(const or_hier* h, const double* b, double* x, double tol, int maxit, 
     hist[0] = 0.0;
     return 0;
   }
-  double** m = make_m(h);
+  or_smoother* m = make_m(h);
   double* r = dalloc(n);
   double* z = dalloc(n);
   double* p = dalloc(n);
@@ -315,7 +374,7 @@ int or_fcg(const or_hier* h, const double* b, double* x, double tol, int maxit, 
     hist[0] = 0.0;
     return 0;
   }
-  double** m = make_m(h);
+  or_smoother* m = make_m(h);
   double* r = dalloc(n);
   double* z = dalloc(n);
   double* p = dalloc(n);
@@ -565,4 +624,67 @@ void or_galerkin(const or_csr* R, const or_csr* A, const or_csr* P, int64_t** cp
   }
   free(acc); free(mark); free(touched);
   *cptr = ptr; *ccol = col; *cval = val;
+}
+
+/* ======================================================================
+ * NEXT-4: the AINV smoother (Sec. 2.3.2): "an approximate inverse of A
+ * ... an incomplete biconjugation, approximating A_l^-1 as a product of two sparse
+ * triangular matrices Z and W ... on GPUs ... only sparse matrix-vector products
+ * with Z and W".  Reading R27: A symmetric positive definite, so W = Z and
+ * A^-1 ~ Z D^-1 Z^T; right-looking biconjugation (Benzi-Meyer-Tuma):
+ *   z_j = e_j (j = 0..n-1)
+ *   for i = 0..n-1:  p_i = a_i^T z_i
+ *       for j = i+1..n-1:  p_j = a_i^T z_j;  if p_j != 0: z_j = z_j - (p_j / p_i) z_i,
+ *                          then drop the entries of z_j with |z_kj| < drop_tol (k != j)
+ *   D = diag(p)
+ * (a_i = row i of A; a_i^T z = sum over row i's entries in column order).  In the
+ * distributed setting the paper's AINV inverts diagonal blocks (block-Jacobi): only
+ * the columns of row_start's block of i are used.  The smoother M^-1 = Z D^-1 Z^T
+ * replaces the l1-Jacobi M^-1 in Eq. (2).  Returns 0, or -1 - i if pivot p_i <= 0.
+ * Z is returned by columns (zptr[n+1], zrow (increasing), zval) and p[n]. */
+int or_ainv(const or_csr* A, int nranks, const int64_t* row_start, double drop_tol, int64_t** zptr,
+            int64_t** zrow, double** zval, double* p) {
+  const int64_t n = A->nrows;
+  /* dense columns are the plain form of "z_j" for the small matrices the oracle sees */
+  double* Z = (double*)calloc((size_t)(n * n > 0 ? n * n : 1), sizeof(double)); /* Z[k*n + j] = z_kj */
+  int64_t* blk = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+  for (int r = 0; r < nranks; ++r)
+    for (int64_t i = row_start[r]; i < row_start[r + 1]; ++i) blk[i] = r;
+  for (int64_t j = 0; j < n; ++j) Z[j * n + j] = 1.0;
+  int status = 0;
+  for (int64_t i = 0; i < n && status == 0; ++i) {
+    double pi = 0.0;
+    for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k)
+      if (blk[A->col[k]] == blk[i]) pi += A->val[k] * Z[A->col[k] * n + i];
+    p[i] = pi;
+    if (!(pi > 0.0)) { status = (int)(-1 - i); break; }
+    for (int64_t j = i + 1; j < n; ++j) {
+      if (blk[j] != blk[i]) continue;
+      double pj = 0.0;
+      for (int64_t k = A->ptr[i]; k < A->ptr[i + 1]; ++k)
+        if (blk[A->col[k]] == blk[i]) pj += A->val[k] * Z[A->col[k] * n + j];
+      if (pj == 0.0) continue;
+      const double f = pj / pi;
+      for (int64_t k = 0; k <= i; ++k)
+        if (Z[k * n + i] != 0.0) {
+          Z[k * n + j] = Z[k * n + j] - f * Z[k * n + i];
+          if (k != j && fabs(Z[k * n + j]) < drop_tol) Z[k * n + j] = 0.0;
+        }
+    }
+  }
+  int64_t nz = 0;
+  for (int64_t q = 0; q < n * n; ++q) nz += Z[q] != 0.0;
+  int64_t* cp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t* rr = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nz + 1));
+  double* vv = (double*)malloc(sizeof(double) * (size_t)(nz + 1));
+  int64_t o = 0;
+  cp[0] = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    for (int64_t k = 0; k < n; ++k)
+      if (Z[k * n + j] != 0.0) { rr[o] = k; vv[o] = Z[k * n + j]; ++o; }
+    cp[j + 1] = o;
+  }
+  free(Z); free(blk);
+  *zptr = cp; *zrow = rr; *zval = vv;
+  return status;
 }

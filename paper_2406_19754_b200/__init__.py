@@ -40,7 +40,8 @@ _KRYLOV = {"pcg": PSC_KRYLOV_PCG, "fcg": PSC_KRYLOV_FCG}
 
 class CycleOpts(ctypes.Structure):
     _fields_ = [("pre_sweeps", _i32), ("post_sweeps", _i32), ("coarse_sweeps", _i32), ("coarse_solver", _i32),
-                ("coarse_maxit", _i32), ("coarse_tol", _f64), ("variable_v", _i32)]
+                ("coarse_maxit", _i32), ("coarse_tol", _f64), ("variable_v", _i32), ("smoother", _i32),
+                ("ainv_drop", _f64)]
 
 
 class KernelRec(ctypes.Structure):
@@ -98,6 +99,8 @@ _sig("psc_krylov_solve_host", _i32, [_vp, _i32, _vp, _vp, _f64, _i32, _vp, _P(St
 _sig("psc_hier_exchange_bench", _i32, [_vp, _i32, _i32, _P(_f64)])
 _sig("psc_hier_kernel_profile", _i32, [_vp, _i32, _vp, _i32, _vp, _i32, _P(_i32)])
 _sig("psc_hier_destroy", None, [_vp])
+_sig("psc_mat_update_values", _i32, [_vp, _vp])
+_sig("psc_hier_rebuild_smoothers", _i32, [_vp])
 
 
 class AmgOpts(ctypes.Structure):
@@ -271,6 +274,11 @@ class Matrix:
                                  ctypes.byref(e)), self.ctx)
         return dict(nnz=a.value, padded=b.value, n_units=c.value, n_rows=d.value, lanes=e.value)
 
+    def update_values(self, val):
+        """psc_mat_update_values: new values, same CSR structure as at creation."""
+        v = _host(val, np.float64, "val")
+        _check(_lib.psc_mat_update_values(self.handle, v.ctypes.data), self.ctx)
+
     def spmv(self, x, y, alpha=1.0, beta=0.0):
         """y = alpha A x + beta y (device tensors; owned parts)."""
         _check(_lib.psc_mat_spmv(self.handle, float(alpha), _dev_ptr(x, self.cols.n_owned, "x"), float(beta),
@@ -283,29 +291,46 @@ class Matrix:
             self.handle = None
 
 
+_SMOOTHER = {"l1": 0, "ainv": 1}
+
+
+def _cycle_opts(pre, post, coarse, coarse_solver, coarse_maxit, coarse_tol, variable_v, smoother, ainv_drop):
+    if coarse_solver not in _COARSE:
+        raise ValueError(f"coarse_solver must be one of {sorted(_COARSE)}")
+    if smoother not in _SMOOTHER:
+        raise ValueError(f"smoother must be one of {sorted(_SMOOTHER)}")
+    return CycleOpts(pre, post, coarse, _COARSE[coarse_solver], int(coarse_maxit), float(coarse_tol),
+                     1 if variable_v else 0, _SMOOTHER[smoother], float(ainv_drop))
+
+
 class Hierarchy:
     """psc_hier_create over given level matrices A[l], P[l], R[l]; V-cycle + PCG / FCG.
 
     coarse_solver: "sweeps" (`coarse` l1-Jacobi sweeps) or "pcg" (PCG with
     l1-Jacobi, at most coarse_maxit iterations to coarse_tol).
-    variable_v: variable V-cycle, pre/post sweeps doubled per level (P:330 footnote)."""
+    variable_v: variable V-cycle, pre/post sweeps doubled per level (P:330 footnote).
+    smoother: "l1" (l1-Jacobi) or "ainv" (AINV with drop tolerance ainv_drop,
+    P:273-279)."""
 
     def __init__(self, ctx: Context, A, P, R, pre=4, post=4, coarse=30, coarse_solver="sweeps", coarse_maxit=40,
-                 coarse_tol=1e-10, variable_v=False):
+                 coarse_tol=1e-10, variable_v=False, smoother="l1", ainv_drop=0.1):
         L = len(A)
         Aa = (_vp * L)(*[m.handle for m in A])
         Pa = (_vp * max(L - 1, 1))(*[m.handle for m in P])
         Ra = (_vp * max(L - 1, 1))(*[m.handle for m in R])
         if coarse_solver not in _COARSE:
             raise ValueError(f"coarse_solver must be one of {sorted(_COARSE)}")
-        opts = CycleOpts(pre, post, coarse, _COARSE[coarse_solver], int(coarse_maxit), float(coarse_tol),
-                         1 if variable_v else 0)
+        opts = _cycle_opts(pre, post, coarse, coarse_solver, coarse_maxit, coarse_tol, variable_v, smoother, ainv_drop)
         h = _vp()
         _check(_lib.psc_hier_create(ctx.handle, L, Aa, Pa, Ra, ctypes.byref(opts), ctypes.byref(h)), ctx)
         self.ctx, self.handle, self.nlevels = ctx, h.value, L
         self.A, self.P, self.R = list(A), list(P), list(R)
         self.n0 = A[0].rows.n_owned
         ctx._children.append(self)
+
+    def rebuild_smoothers(self):
+        """psc_hier_rebuild_smoothers: smoothers from the current A_l values."""
+        _check(_lib.psc_hier_rebuild_smoothers(self.handle), self.ctx)
 
     def info(self):
         L = self.nlevels
@@ -441,11 +466,8 @@ class AmgSetup:
         return agg, root.astype(bool)
 
     def hierarchy(self, pre=4, post=4, coarse=30, coarse_solver="sweeps", coarse_maxit=40, coarse_tol=1e-10,
-                  variable_v=False) -> "Hierarchy":
-        if coarse_solver not in _COARSE:
-            raise ValueError(f"coarse_solver must be one of {sorted(_COARSE)}")
-        opts = CycleOpts(pre, post, coarse, _COARSE[coarse_solver], int(coarse_maxit), float(coarse_tol),
-                         1 if variable_v else 0)
+                  variable_v=False, smoother="l1", ainv_drop=0.1) -> "Hierarchy":
+        opts = _cycle_opts(pre, post, coarse, coarse_solver, coarse_maxit, coarse_tol, variable_v, smoother, ainv_drop)
         h = _vp()
         _check(_lib.psc_amg_hier_create(self.handle, ctypes.byref(opts), ctypes.byref(h)), self.ctx)
         H = Hierarchy.__new__(Hierarchy)

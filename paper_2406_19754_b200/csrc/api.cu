@@ -391,7 +391,7 @@ int psc_mat_create_csr(psc_ctx* ctx, psc_desc* rows, psc_desc* cols, int64_t n_l
     PSC_CUDA(cudaMemcpy(m->d_valcsr, val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
   }
   // small matrices keep a host copy (replicated coarse levels)
-  if (nnz <= (int64_t)8 << 20) {
+  if (nnz <= (int64_t)1 << 27) {
     m->h_rowptr.assign(row_ptr, row_ptr + n_local_rows + 1);
     m->h_colg.assign(col_global, col_global + nnz);
     m->h_val.assign(val, val + nnz);
@@ -455,6 +455,35 @@ int psc_mat_spmv(psc_mat* m, double alpha, const double* x, double beta, double*
   dfree(xh);
   return PSC_OK;
   API_END(ctx)
+}
+
+int psc_mat_update_values(psc_mat* m, const double* val) {
+  psc_ctx* ctx = m ? m->ctx : nullptr;
+  double* d = nullptr;
+  API_BEGIN
+  PSC_REQUIRE(m && (val || m->nnz == 0), PSC_ERR_ARG, "null argument");
+  PSC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  if (!m->assembled) {
+    if (m->nnz) PSC_CUDA(cudaMemcpyAsync(m->d_valcsr, val, sizeof(double) * m->nnz, cudaMemcpyHostToDevice, s));
+  } else if (m->nnz) {
+    d = dalloc<double>(m->nnz);
+    PSC_CUDA(cudaMemcpyAsync(d, val, sizeof(double) * m->nnz, cudaMemcpyHostToDevice, s));
+    sell_update_values(ctx, m->S, d, s);
+  }
+  if (!m->h_val.empty()) m->h_val.assign(val, val + m->nnz);
+  PSC_CUDA(cudaStreamSynchronize(s));
+  dfree(d);
+  return PSC_OK;
+  }
+  catch (const Error& e) {
+    dfree(d);
+    return fail(ctx, e);
+  }
+  catch (const std::exception& e) {
+    dfree(d);
+    return fail(ctx, e);
+  }
 }
 
 void psc_mat_destroy(psc_mat* m) {

@@ -44,6 +44,12 @@ struct LevelWS {
   bool one_cta = false;       // sparse one-CTA solver applies
   double* cz = nullptr;       // general coarsest PCG: z and q = A p (n)
   double* cq = nullptr;
+  // AINV smoother: M^-1 = Z D^-1 Z^T; Z and Z^T as sliced ELL, 1/p, scratch
+  bool ainv = false;
+  Sell Z, Zt;
+  double* ainv_dinv = nullptr;
+  double* az_t = nullptr;
+  double* az_u = nullptr;
 };
 
 // Replicated suffix (nranks > 1): levels first..L-1 are held whole on every
@@ -283,6 +289,184 @@ double* coarse_solve(psc_hier* h, LevelWS& W, const double* b, cudaStream_t s) {
 // first_done: x[0] = M^{-1} b was already written by the kernel that produced b
 // (the restriction, or the CG update at level 0).  Returns the buffer index of x.
 // timing: event pairs around level-0 sweeps (dominant kernel, measured live).
+void free_ainv(LevelWS& W) {
+  sell_free(W.Z);
+  sell_free(W.Zt);
+  dfree(W.ainv_dinv);
+  dfree(W.az_t);
+  dfree(W.az_u);
+  W.ainv_dinv = W.az_t = W.az_u = nullptr;
+  W.ainv = false;
+}
+
+// ------------------------------------------------------------ AINV smoother
+// Incomplete A-biconjugation (reading R27): A symmetric positive definite,
+// W = Z, A^-1 ~ Z D^-1 Z^T.  Right-looking: z_j = e_j; for i = 0..n-1: p_i = a_i^T z_i,
+// and for every j > i with p_j = a_i^T z_j != 0: z_j -= (p_j / p_i) z_i, dropping the
+// updated entries below drop_tol (never z_jj).  Only columns j whose z_j has an entry
+// in the pattern of row i can have p_j != 0, so the candidates come from a row ->
+// columns index of Z.  Sums run over row i's entries in column order; one rounding
+// per operation (host code built with -ffp-contract=off).  Host work at set-up.
+void ainv_factor(int64_t n, const int64_t* ptr, const int64_t* col, const double* val, double drop,
+                 std::vector<int64_t>& zptr, std::vector<int64_t>& zrow, std::vector<double>& zval,
+                 std::vector<double>& p) {
+  std::vector<std::vector<std::pair<int64_t, double>>> z(n);  // column j: (row k, z_kj), rows increasing
+  std::vector<std::vector<int64_t>> cols_at(n);                // row k -> columns j with z_kj present (or once)
+  for (int64_t j = 0; j < n; ++j) {
+    z[j].push_back({j, 1.0});
+    cols_at[j].push_back(j);
+  }
+  p.assign(n, 0.0);
+  auto dot_row = [&](int64_t i, const std::vector<std::pair<int64_t, double>>& zj) {
+    double s = 0.0;
+    size_t q = 0;
+    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {  // row i in column order
+      const int64_t c = col[k];
+      while (q < zj.size() && zj[q].first < c) ++q;
+      if (q < zj.size() && zj[q].first == c) s = s + val[k] * zj[q].second;
+    }
+    return s;
+  };
+  std::vector<int64_t> cand;
+  std::vector<std::pair<int64_t, double>> merged;
+  for (int64_t i = 0; i < n; ++i) {
+    const double pi = dot_row(i, z[i]);
+    PSC_REQUIRE(pi > 0.0, PSC_ERR_STATE, "AINV breakdown: pivot " + std::to_string(i) + " <= 0");
+    p[i] = pi;
+    cand.clear();
+    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k)
+      for (int64_t j : cols_at[col[k]])
+        if (j > i) cand.push_back(j);
+    std::sort(cand.begin(), cand.end());
+    cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+    const auto& zi = z[i];
+    for (int64_t j : cand) {
+      const double pj = dot_row(i, z[j]);
+      if (pj == 0.0) continue;
+      const double f = pj / pi;
+      // z_j - f z_i over the rows of z_i (z_i has rows <= i < j, so z_jj stays 1)
+      merged.clear();
+      const auto& zj = z[j];
+      size_t a = 0, b = 0;
+      while (a < zj.size() || b < zi.size()) {
+        if (b == zi.size() || (a < zj.size() && zj[a].first < zi[b].first)) {
+          merged.push_back(zj[a++]);
+        } else {
+          const int64_t k = zi[b].first;
+          const bool have = a < zj.size() && zj[a].first == k;
+          const double v = (have ? zj[a].second : 0.0) - f * zi[b].second;
+          if (have) ++a;
+          ++b;
+          if (k == j || std::fabs(v) >= drop) {
+            merged.push_back({k, v});
+            if (!have) cols_at[k].push_back(j);
+          }
+        }
+      }
+      z[j].swap(merged);
+    }
+  }
+  zptr.assign(n + 1, 0);  // Z by rows: (k, j)
+  for (int64_t j = 0; j < n; ++j)
+    for (auto& e : z[j]) zptr[e.first + 1]++;
+  for (int64_t k = 0; k < n; ++k) zptr[k + 1] += zptr[k];
+  zrow.assign(zptr[n], 0);
+  zval.assign(zptr[n], 0.0);
+  std::vector<int64_t> fill(zptr.begin(), zptr.end() - 1);
+  for (int64_t j = 0; j < n; ++j)  // columns in increasing j: each row of Z comes out sorted
+    for (auto& e : z[j]) {
+      const int64_t o = fill[e.first]++;
+      zrow[o] = j;
+      zval[o] = e.second;
+    }
+}
+
+// device copy of a host CSR (local columns) as sliced ELL
+void sell_from_host(psc_ctx* ctx, int64_t n, int64_t ncols, const std::vector<int64_t>& ptr,
+                    const std::vector<int64_t>& col, const std::vector<double>& val, Sell& S) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nnz = ptr[n];
+  int64_t* dp = dalloc<int64_t>(n + 1);
+  int64_t* dc = dalloc<int64_t>(nnz);
+  double* dv = dalloc<double>(nnz);
+  PSC_CUDA(cudaMemcpyAsync(dp, ptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+  if (nnz) {
+    PSC_CUDA(cudaMemcpyAsync(dc, col.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+    PSC_CUDA(cudaMemcpyAsync(dv, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+  }
+  sell_from_csr(ctx, n, dp, dc, dv, nnz, 0, ncols, nullptr, 0, S, s, 0, false);
+  PSC_CUDA(cudaStreamSynchronize(s));
+  dfree(dp);
+  dfree(dc);
+  dfree(dv);
+}
+
+// AINV factors of level W from its matrix's host copy (one rank: the owned block is
+// the whole matrix; columns are local = global)
+void build_ainv(psc_hier* h, LevelWS& W) {
+  psc_ctx* ctx = h->ctx;
+  psc_mat* A = W.A;
+  PSC_REQUIRE(ctx->nranks == 1, PSC_ERR_STATE, "AINV smoother: one rank only");
+  PSC_REQUIRE((int64_t)A->h_rowptr.size() == A->n_rows + 1, PSC_ERR_STATE,
+              "AINV smoother needs the matrix's host copy (nnz <= 2^27)");
+  free_ainv(W);
+  const int64_t n = W.n;
+  std::vector<int64_t> zp, zr, tp, tr;
+  std::vector<double> zv, tv, pv;
+  ainv_factor(n, A->h_rowptr.data(), A->h_colg.data(), A->h_val.data(), h->opt.ainv_drop, zp, zr, zv, pv);
+  // Z^T by rows (= columns of Z)
+  tp.assign(n + 1, 0);
+  for (int64_t q = 0; q < zp[n]; ++q) tp[zr[q] + 1]++;
+  for (int64_t j = 0; j < n; ++j) tp[j + 1] += tp[j];
+  tr.assign(zp[n], 0);
+  tv.assign(zp[n], 0.0);
+  std::vector<int64_t> fill(tp.begin(), tp.end() - 1);
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t q = zp[k]; q < zp[k + 1]; ++q) {
+      const int64_t o = fill[zr[q]]++;
+      tr[o] = k;
+      tv[o] = zv[q];
+    }
+  sell_from_host(ctx, n, n, zp, zr, zv, W.Z);
+  sell_from_host(ctx, n, n, tp, tr, tv, W.Zt);
+  std::vector<double> dinv(n);
+  for (int64_t i = 0; i < n; ++i) dinv[i] = 1.0 / pv[i];
+  W.ainv_dinv = dvec(n);
+  W.az_t = dvec(n);
+  W.az_u = dvec(n);
+  PSC_CUDA(cudaMemcpy(W.ainv_dinv, dinv.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+  W.ainv = true;
+}
+
+// One AINV sweep in place: x += Z D^-1 Z^T (b - A x); from_zero: x = Z D^-1 Z^T b
+void ainv_sweep(psc_hier* h, LevelWS& W, const double* b, double* x, bool from_zero, cudaStream_t s) {
+  psc_ctx* ctx = h->ctx;
+  const double* r = b;
+  if (!from_zero) {
+    RowArgs a;
+    a.vec_padded = true;
+    a.x = x;
+    a.b = b;
+    a.y = W.r;
+    run_rows(h, W.d, W.A->S, RowOp::Resid, a, s);
+    r = W.r;
+  }
+  {  // u = D^-1 Z^T r  (the Spmv epilogue's second output y2 = dinv2 .* y)
+    RowArgs a;
+    a.vec_padded = true;
+    a.x = r;
+    a.y = W.az_t;
+    a.y2 = W.az_u;
+    a.dinv2 = W.ainv_dinv;
+    launch_rows(ctx, W.Zt, RowOp::Spmv, a, s);
+  }
+  RowArgs a;
+  a.vec_padded = true;
+  a.x = W.az_u;
+  a.y = x;
+  launch_rows(ctx, W.Z, from_zero ? RowOp::Spmv : RowOp::PAdd, a, s);
+}
+
 // PSC_NO_FUSED_SCALE=1: every first sweep from zero is a stand-alone x = M^-1 b launch
 bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
 
@@ -291,6 +475,10 @@ int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream
   psc_ctx* ctx = h->ctx;
   if (nsweeps <= 0) {
     PSC_CUDA(cudaMemsetAsync(W.x[0], 0, sizeof(double) * (W.n + W.nh), s));
+    return 0;
+  }
+  if (W.ainv) {  // AINV sweeps in place in x[0] (first_done never set for AINV levels)
+    for (int k = 0; k < nsweeps; ++k) ainv_sweep(h, W, b, W.x[0], k == 0, s);
     return 0;
   }
   int cur = 0, k = 1;
@@ -396,7 +584,8 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   }
   // fused: the next level's first sweep from zero, x_{l+1} = M^{-1} b_{l+1}
   const bool next_dense = h->dsuf && &LV == h->dsuf_lv && l + 1 == h->dsuf_l;
-  const bool fuse = fuse_first_sweep() && l + 1 < Lend - 1 && h->opt.pre_sweeps > 0 && !next_replicated && !next_dense;
+  const bool fuse = fuse_first_sweep() && l + 1 < Lend - 1 && h->opt.pre_sweeps > 0 && !next_replicated &&
+                    !next_dense && !C.ainv;
   {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
@@ -421,6 +610,12 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
   const int post = level_sweeps(h, h->opt.post_sweeps, glev);
   const bool level0 = dist && l == 0;
+  if (W.ainv) {
+    for (int k = 0; k < post; ++k) ainv_sweep(h, W, b, W.x[cur], false, s);
+    if (level0)
+      launch_dot(ctx, W.n, h->rz_weight ? h->rz_weight : b, W.x[cur], &h->red1, scal_mine(h, S_RZ), s);
+    return W.x[cur];
+  }
   for (int k = 0; k < post; ++k) {
     const bool last0 = (level0 && k == post - 1);
     RowArgs a;
@@ -741,6 +936,7 @@ void free_hier(psc_hier* h) {
   if (h->ctx->stream) cudaStreamSynchronize(h->ctx->stream);
   p2p_free(h->ctx, h->p2p);
   for (auto& W : h->lv) {
+    free_ainv(W);
     dfree(W.dinv);
     if (&W != &h->lv[0]) dfree(W.b);
     dfree(W.cz);
@@ -944,6 +1140,10 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
     PSC_REQUIRE(h->opt.coarse_maxit >= 0 && h->opt.coarse_tol >= 0.0 && std::isfinite(h->opt.coarse_tol), PSC_ERR_ARG,
                 "coarse_maxit / coarse_tol must be non-negative");
     PSC_REQUIRE(h->opt.variable_v == 0 || h->opt.variable_v == 1, PSC_ERR_ARG, "variable_v must be 0 or 1");
+    PSC_REQUIRE(h->opt.smoother == PSC_SMOOTHER_L1JACOBI || h->opt.smoother == PSC_SMOOTHER_AINV, PSC_ERR_ARG,
+                "unknown smoother");
+    PSC_REQUIRE(h->opt.smoother != PSC_SMOOTHER_AINV || (h->opt.ainv_drop >= 0.0 && std::isfinite(h->opt.ainv_drop)),
+                PSC_ERR_ARG, "ainv_drop must be a finite non-negative number");
     PSC_REQUIRE(!h->opt.variable_v || nlevels < 2 ||
                     (nlevels - 2 <= 20 && ((int64_t)std::max(h->opt.pre_sweeps, h->opt.post_sweeps) << (nlevels - 2)) <= (1 << 20)),
                 PSC_ERR_ARG, "variable V-cycle: more than 2^20 sweeps at a level");
@@ -1001,6 +1201,7 @@ int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const
       W.dinv = dvec(W.n);
       launch_l1_dinv(ctx, W.A->S, W.dinv, s);  // smoother build
       if (l > 0) W.b = dvec(W.n);
+      if (h->opt.smoother == PSC_SMOOTHER_AINV && l + 1 < nlevels) build_ainv(h, W);
     }
     h->r_cg = dvec(W0.n);
     h->q = dvec(W0.n);
@@ -1248,6 +1449,45 @@ int psc_hier_exchange_bench(psc_hier* h, int level, int reps, double* us_per_exc
     float ms = 0.f;
     PSC_CUDA(cudaEventElapsedTime(&ms, h->ev_t0, h->ev_t1));
     *us_per_exchange = 1e3 * ms / reps;
+    return PSC_OK;
+  } catch (const Error& e) {
+    return hfail(ctx, e);
+  }
+}
+
+int psc_hier_rebuild_smoothers(psc_hier* h) {
+  psc_ctx* ctx = h ? h->ctx : nullptr;
+  try {
+    PSC_REQUIRE(h, PSC_ERR_ARG, "null hierarchy");
+    PSC_REQUIRE(!h->rep.on, PSC_ERR_STATE, "rebuild_smoothers: the replicated coarse suffix keeps its own copies");
+    enter(ctx);
+    cudaStream_t s = ctx->stream;
+    PSC_CUDA(cudaStreamSynchronize(s));
+    for (int l = 0; l < h->L; ++l) {
+      LevelWS& W = h->lv[l];
+      launch_l1_dinv(ctx, W.A->S, W.dinv, s);
+      if (W.dense) dense_from_sell(ctx, W.A->S, W.dense, s);
+      if (h->opt.smoother == PSC_SMOOTHER_AINV && l + 1 < h->L) build_ainv(h, W);
+    }
+    if (h->dsuf) {  // the dense suffix operator is a function of the smoothers
+      dfree(h->dsuf);
+      h->dsuf = nullptr;
+      h->dsuf_lv = nullptr;
+      h->dsuf_l = -1;
+      build_dense_suffix(h);
+    }
+    // the captured iterations may hold buffers that were reallocated (AINV factors)
+    for (auto& e : h->iter_exec)
+      if (e) {
+        PSC_CUDA(cudaGraphExecDestroy(e));
+        e = nullptr;
+      }
+    for (auto& e : h->prof_exec)
+      if (e) {
+        PSC_CUDA(cudaGraphExecDestroy(e));
+        e = nullptr;
+      }
+    PSC_CUDA(cudaStreamSynchronize(s));
     return PSC_OK;
   } catch (const Error& e) {
     return hfail(ctx, e);

@@ -1847,7 +1847,8 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
                                  const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
                                  int64_t own_begin, int64_t n_own,
                                  const int64_t* __restrict__ halo, int64_t nh, const uint8_t* __restrict__ perm,
-                                 int32_t* __restrict__ col, double* __restrict__ val, int* err) {
+                                 int32_t* __restrict__ col, double* __restrict__ val, int64_t* __restrict__ slot,
+                                 int* err) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // slot
   if (t >= n_slices * 32) return;
   const int64_t s = t >> 5;
@@ -1868,6 +1869,7 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
       double v = 0.0;
       if (q < e && colg[q] - own_begin == i + o) {
         v = valcsr[q];
+        if (slot) slot[q] = vb + 32 * (int64_t)j + lane;
         ++q;
       }
       val[vb + 32 * (int64_t)j + lane] = v;
@@ -1885,6 +1887,7 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
       last = map_col(colg[b + k], own_begin, n_own, halo, nh, err);
       col[cb + o] = last;
       val[vb + o] = valcsr[b + k];
+      if (slot) slot[b + k] = vb + o;
     } else {
       col[cb + o] = last;
       val[vb + o] = 0.0;
@@ -1932,7 +1935,7 @@ __global__ void rg_len_kernel(int64_t n_rows, int G, const int64_t* __restrict__
 __global__ void rg_fill_kernel(int64_t n_rows, const int64_t* __restrict__ rowptr, const int64_t* __restrict__ colg,
                                const double* __restrict__ valcsr, const int64_t* __restrict__ ptr, int64_t own_begin,
                                int64_t n_own, const int64_t* __restrict__ halo, int64_t nh, int32_t* __restrict__ col,
-                               double* __restrict__ val, int* err) {
+                               double* __restrict__ val, int64_t* __restrict__ slot, int* err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_rows) return;
   const int64_t b = rowptr[i], e = rowptr[i + 1];
@@ -1943,6 +1946,7 @@ __global__ void rg_fill_kernel(int64_t n_rows, const int64_t* __restrict__ rowpt
       last = map_col(colg[b + k], own_begin, n_own, halo, nh, err);
       col[o0 + k] = last;
       val[o0 + k] = valcsr[b + k];
+      if (slot) slot[b + k] = o0 + k;
     } else {
       col[o0 + k] = last;
       val[o0 + k] = 0.0;
@@ -2005,6 +2009,8 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
   S.n_rows = n_rows;
   S.n_cols_local = n_own + n_halo;
   S.nnz = nnz;
+  // value slot of every CSR entry (psc_mat_update_values: same structure, new values)
+  S.slot = dalloc<int64_t>(nnz);
   S.lanes = lanes > 0 ? lanes : choose_lanes(n_rows, nnz);
   if (env_int("PSC_NO_DIA", 0)) allow_dia = false;
   const int RU = S.rows_per_unit();
@@ -2076,7 +2082,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     if (nu > 0) {
       sell_fill_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
           n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, own_begin, n_own, d_halo,
-          n_halo, S.perm, S.col, S.val, d_err);
+          n_halo, S.perm, S.col, S.val, S.slot, d_err);
       PSC_CUDA(cudaGetLastError());
       sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, S.hdr);
       PSC_CUDA(cudaGetLastError());
@@ -2117,7 +2123,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     if (n_rows > 0) {
       rg_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, d_rowptr, d_colg, d_val, S.ptr,
                                                                        own_begin, n_own, d_halo, n_halo, S.col,
-                                                                       S.val, d_err);
+                                                                       S.val, S.slot, d_err);
       PSC_CUDA(cudaGetLastError());
     }
     flag.resize(n_rows);
@@ -2175,6 +2181,7 @@ void sell_free(Sell& S) {
   dfree(S.boundary);
   dfree(S.perm);
   dfree(S.iperm);
+  dfree(S.slot);
   S = Sell();
 }
 
@@ -2193,4 +2200,18 @@ void red_free(RedSite& r) {
   r = RedSite();
 }
 
+}  // namespace psc
+
+namespace psc {
+__global__ void scatter_values_kernel(int64_t nnz, const int64_t* __restrict__ slot, const double* __restrict__ v,
+                                      double* __restrict__ val) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nnz) val[slot[k]] = v[k];
+}
+void sell_update_values(psc_ctx* ctx, Sell& S, const double* d_newval, cudaStream_t s) {
+  if (S.nnz == 0) return;
+  scatter_values_kernel<<<(unsigned)((S.nnz + 255) / 256), 256, 0, s>>>(S.nnz, S.slot, d_newval, S.val);
+  PSC_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
 }  // namespace psc

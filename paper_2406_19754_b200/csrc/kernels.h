@@ -113,6 +113,8 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
                    const double* d_val, int64_t nnz, int64_t own_begin, int64_t n_own, const int64_t* d_halo,
                    int64_t n_halo, Sell& S, cudaStream_t s, int lanes = 0, bool allow_dia = false);
 void sell_free(Sell& S);
+// new values in the CSR order of the assembled matrix (device array of S.nnz)
+void sell_update_values(psc_ctx* ctx, Sell& S, const double* d_newval, cudaStream_t s);
 
 RedSite red_alloc(int num_sms, int nred);
 void red_free(RedSite& r);

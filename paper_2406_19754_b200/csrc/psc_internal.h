@@ -93,6 +93,7 @@ struct Sell {
   // 256-row window (kernels.cu row_of_slot / slot_of_row); nullptr: natural order
   uint8_t* perm = nullptr;
   uint8_t* iperm = nullptr;
+  int64_t* slot = nullptr;  // nnz: value slot of each CSR entry (structure-preserving updates)
   // units whose columns are all owned (interior) and the others (boundary):
   // the interior ones can run while the halo exchange is in flight.
   int32_t* interior = nullptr;

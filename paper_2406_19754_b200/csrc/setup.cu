@@ -521,6 +521,86 @@ DCsr transpose(psc_ctx* ctx, const DCsr& P) {
   return R;
 }
 
+// rap_kernel with the per-thread tables in shared memory (kSmallT slots, 32-bit keys:
+// K < 2^31 on one rank), interleaved [slot][thread] so the threads of a warp hitting
+// the same slot index fall in different banks.  Same semantics as rap_kernel.
+constexpr int kSmallT = 64;
+constexpr int kRapThreads = 128;
+constexpr int kRapSmem = kRapThreads * kSmallT * (4 + 8 + 1);
+__global__ void __launch_bounds__(kRapThreads) rap_smem_kernel(DCsr R, DCsr A, DCsr P, int64_t* __restrict__ cnt,
+                                                               const int64_t* __restrict__ cptr,
+                                                               int64_t* __restrict__ ccol, double* __restrict__ cval) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* acc = reinterpret_cast<double*>(sm);
+  int32_t* key = reinterpret_cast<int32_t*>(sm + kRapThreads * kSmallT * 8);
+  uint8_t* tl = sm + kRapThreads * kSmallT * 12;
+  const int t = threadIdx.x;
+  constexpr int cap = kSmallT - kSmallT / 4;
+  for (int h = 0; h < kSmallT; ++h) key[h * kRapThreads + t] = -1;
+  for (int64_t J = (int64_t)blockIdx.x * blockDim.x + t; J < R.n; J += (int64_t)gridDim.x * blockDim.x) {
+    if (cptr && cnt[J] < 0) continue;
+    int nt = 0;
+    bool over = false;
+    for (int64_t a = R.ptr[J]; a < R.ptr[J + 1] && !over; ++a) {
+      const int64_t i = R.col[a];
+      const double rv = R.val[a];
+      for (int64_t b = A.ptr[i]; b < A.ptr[i + 1] && !over; ++b) {
+        const int64_t k = A.col[b];
+        const double ra = __dmul_rn(rv, A.val[b]);
+        for (int64_t c = P.ptr[k]; c < P.ptr[k + 1]; ++c) {
+          const int32_t K = (int32_t)P.col[c];
+          uint32_t h = hslot(K, kSmallT - 1);
+          while (key[h * kRapThreads + t] != -1 && key[h * kRapThreads + t] != K) h = (h + 1) & (kSmallT - 1);
+          const int s = h * kRapThreads + t;
+          if (key[s] == -1) {
+            if (nt == cap) {
+              over = true;
+              break;
+            }
+            key[s] = K;
+            acc[s] = 0.0;
+            tl[nt * kRapThreads + t] = (uint8_t)h;
+            ++nt;
+          }
+          acc[s] = __dadd_rn(acc[s], __dmul_rn(ra, P.val[c]));
+        }
+      }
+    }
+    if (!cptr) {
+      cnt[J] = over ? -1 : nt;
+    } else {
+      const int64_t q0 = cptr[J];
+      for (int x = 0; x < nt; ++x) {  // insertion by increasing K
+        const int s = tl[x * kRapThreads + t] * kRapThreads + t;
+        const int64_t K = key[s];
+        const double v = acc[s];
+        int64_t y = q0 + x - 1;
+        while (y >= q0 && ccol[y] > K) {
+          ccol[y + 1] = ccol[y];
+          cval[y + 1] = cval[y];
+          --y;
+        }
+        ccol[y + 1] = K;
+        cval[y + 1] = v;
+      }
+    }
+    for (int x = 0; x < nt; ++x) key[tl[x * kRapThreads + t] * kRapThreads + t] = -1;
+  }
+}
+
+void rap_smem_launch(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P, int64_t* cnt, const int64_t* cptr,
+                     int64_t* ccol, double* cval, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PSC_CUDA(cudaFuncSetAttribute(rap_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRapSmem));
+    attr = true;
+  }
+  const int64_t need = (R.n + kRapThreads - 1) / kRapThreads;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * 2));
+  rap_smem_kernel<<<grid, kRapThreads, kRapSmem, s>>>(R, A, P, cnt, cptr, ccol, cval);
+  PSC_CUDA(cudaGetLastError());
+}
+
 // per-thread tables for rap_kernel: T slots (3 words each) for nth threads
 struct RapTables {
   int64_t T = 0, nth = 0;
@@ -552,11 +632,9 @@ DCsr galerkin(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P) {
   cudaStream_t s = ctx->stream;
   const int64_t nc = R.n;
   int64_t* cnt = dalloc<int64_t>(nc);
-  const int64_t T0 = 64;
-  RapTables small(ctx, T0, nc, s);
-  rap_kernel<<<small.grid(), kT, 0, s>>>(R, A, P, (uint32_t)(T0 - 1), small.keys, small.vals, small.tl, cnt, nullptr,
-                                         nc, nullptr, nullptr, nullptr);
-  PSC_CUDA(cudaGetLastError());
+  const int64_t T0 = kSmallT;
+  PSC_REQUIRE(P.ncols < INT32_MAX, PSC_ERR_STATE, "Galerkin: more than 2^31 coarse columns");
+  rap_smem_launch(ctx, R, A, P, cnt, nullptr, nullptr, nullptr, s);
   std::vector<int64_t> hc(nc);
   PSC_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int64_t) * nc, cudaMemcpyDeviceToHost, s));
   PSC_CUDA(cudaStreamSynchronize(s));
@@ -598,8 +676,7 @@ DCsr galerkin(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P) {
   // fill: the small tables skip the big rows (cnt < 0 marks them only in the count
   // pass, so mark them again), the large tables do just those
   if (!big.empty()) mark_kernel<<<blocks((int64_t)big.size()), kT, 0, s>>>((int64_t)big.size(), d_big, cnt);
-  rap_kernel<<<small.grid(), kT, 0, s>>>(R, A, P, (uint32_t)(T0 - 1), small.keys, small.vals, small.tl, cnt, nullptr,
-                                         nc, C.ptr, C.col, C.val);
+  rap_smem_launch(ctx, R, A, P, cnt, C.ptr, C.col, C.val, s);
   if (!big.empty()) {
     unmark_kernel<<<blocks((int64_t)big.size()), kT, 0, s>>>((int64_t)big.size(), d_big, cnt);
     rap_kernel<<<large->grid(), kT, 0, s>>>(R, A, P, (uint32_t)(large->T - 1), large->keys, large->vals, large->tl,
