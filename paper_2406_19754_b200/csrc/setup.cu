@@ -274,18 +274,6 @@ __global__ void rowsort_kernel(DCsr M) {
 }
 
 // ------------------------------------------------------------ Galerkin R A P
-// products reached by row J: sum over i in R_J, k in A_i of |P_k| (table size bound)
-__global__ void rap_bound_kernel(DCsr R, DCsr A, DCsr P, int64_t* __restrict__ bound) {
-  const int64_t J = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (J >= R.n) return;
-  int64_t s = 0;
-  for (int64_t a = R.ptr[J]; a < R.ptr[J + 1]; ++a) {
-    const int64_t i = R.col[a];
-    for (int64_t b = A.ptr[i]; b < A.ptr[i + 1]; ++b) s += P.ptr[A.col[b] + 1] - P.ptr[A.col[b]];
-  }
-  bound[J] = s;
-}
-
 __device__ __forceinline__ uint32_t hslot(int64_t K, uint32_t mask) {
   return (uint32_t)(((uint64_t)K * 0x9E3779B97F4A7C15ull) >> 32) & mask;
 }
@@ -366,16 +354,6 @@ __global__ void mark_kernel(int64_t n, const int64_t* __restrict__ rows, int64_t
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) cnt[rows[q]] = -1;
 }
-__global__ void unmark_kernel(int64_t n, const int64_t* __restrict__ rows, int64_t* __restrict__ cnt) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n) cnt[rows[q]] = 0;  // any value >= 0: the fill pass does the row
-}
-
-__global__ void max_kernel(int64_t n, const int64_t* __restrict__ v, unsigned long long* __restrict__ mx) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) atomicMax(mx, (unsigned long long)v[i]);
-}
-
 double secs_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -625,46 +603,44 @@ struct RapTables {
   unsigned grid() const { return (unsigned)(nth / kT); }
 };
 
-// Galerkin A_c = R A P.  Every row first with small tables (64 slots: the rows of the
-// level-1 operator of a 7-point problem have <= ~50 entries); the rows that do not fit
-// are redone with tables sized from their product count.
+// Galerkin A_c = R A P.  Every row first with small shared-memory tables (64 slots:
+// the rows of the level-1 operator of a 7-point problem have <= ~50 entries); the rows
+// that do not fit are redone with global-memory tables of 512, 4096, ... slots (the
+// product count is a poor bound on a row's distinct columns: ~35,000 products for
+// ~120 columns on level 2 of 256^3).
 DCsr galerkin(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P) {
   cudaStream_t s = ctx->stream;
   const int64_t nc = R.n;
-  int64_t* cnt = dalloc<int64_t>(nc);
-  const int64_t T0 = kSmallT;
   PSC_REQUIRE(P.ncols < INT32_MAX, PSC_ERR_STATE, "Galerkin: more than 2^31 coarse columns");
+  int64_t* cnt = dalloc<int64_t>(nc);
   rap_smem_launch(ctx, R, A, P, cnt, nullptr, nullptr, nullptr, s);
+  // escalation stages: rows still at cnt < 0 after a stage go to the next one
+  struct Stage {
+    std::unique_ptr<RapTables> tab;
+    int64_t* rows = nullptr;
+    int64_t nrows = 0;
+  };
+  std::vector<Stage> stages;
   std::vector<int64_t> hc(nc);
-  PSC_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int64_t) * nc, cudaMemcpyDeviceToHost, s));
-  PSC_CUDA(cudaStreamSynchronize(s));
-  std::vector<int64_t> big;
-  for (int64_t J = 0; J < nc; ++J)
-    if (hc[J] < 0) big.push_back(J);
-  int64_t* d_big = nullptr;
-  std::unique_ptr<RapTables> large;
-  if (!big.empty()) {
-    d_big = dalloc<int64_t>(big.size());
-    PSC_CUDA(cudaMemcpyAsync(d_big, big.data(), sizeof(int64_t) * big.size(), cudaMemcpyHostToDevice, s));
-    int64_t* bound = dalloc<int64_t>(nc);
-    rap_bound_kernel<<<blocks(nc), kT, 0, s>>>(R, A, P, bound);
-    unsigned long long* mx = dalloc<unsigned long long>(1);
-    PSC_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), s));
-    max_kernel<<<blocks(nc), kT, 0, s>>>(nc, bound, mx);
-    PSC_CUDA(cudaGetLastError());
-    unsigned long long mb = 0;
-    PSC_CUDA(cudaMemcpyAsync(&mb, mx, sizeof(mb), cudaMemcpyDeviceToHost, s));
+  int64_t T = 512;
+  for (;;) {
+    PSC_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int64_t) * nc, cudaMemcpyDeviceToHost, s));
     PSC_CUDA(cudaStreamSynchronize(s));
-    dfree(mx);
-    dfree(bound);
-    // at most P.ncols distinct columns; T with a 3/4 load limit above the bound
-    const int64_t need = std::max<int64_t>(1, std::min<int64_t>((int64_t)mb, P.ncols));
-    int64_t T = 2 * T0;
-    while (T - T / 4 < need + 1) T *= 2;
-    large.reset(new RapTables(ctx, T, (int64_t)big.size(), s));
-    rap_kernel<<<large->grid(), kT, 0, s>>>(R, A, P, (uint32_t)(T - 1), large->keys, large->vals, large->tl, cnt,
-                                            d_big, (int64_t)big.size(), nullptr, nullptr, nullptr);
+    std::vector<int64_t> big;
+    for (int64_t J = 0; J < nc; ++J)
+      if (hc[J] < 0) big.push_back(J);
+    if (big.empty()) break;
+    PSC_REQUIRE(T <= ((int64_t)1 << 31), PSC_ERR_STATE, "Galerkin: row too long");
+    Stage st;
+    st.nrows = (int64_t)big.size();
+    st.rows = dalloc<int64_t>(big.size());
+    PSC_CUDA(cudaMemcpyAsync(st.rows, big.data(), sizeof(int64_t) * big.size(), cudaMemcpyHostToDevice, s));
+    st.tab.reset(new RapTables(ctx, T, st.nrows, s));
+    rap_kernel<<<st.tab->grid(), kT, 0, s>>>(R, A, P, (uint32_t)(T - 1), st.tab->keys, st.tab->vals, st.tab->tl,
+                                             cnt, st.rows, st.nrows, nullptr, nullptr, nullptr);
     PSC_CUDA(cudaGetLastError());
+    stages.push_back(std::move(st));
+    T *= 8;
   }
   DCsr C;
   C.n = nc;
@@ -673,19 +649,25 @@ DCsr galerkin(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P) {
   C.nnz = scan(cnt, C.ptr, nc, s);
   C.col = dalloc<int64_t>(C.nnz);
   C.val = dalloc<double>(C.nnz);
-  // fill: the small tables skip the big rows (cnt < 0 marks them only in the count
-  // pass, so mark them again), the large tables do just those
-  if (!big.empty()) mark_kernel<<<blocks((int64_t)big.size()), kT, 0, s>>>((int64_t)big.size(), d_big, cnt);
-  rap_smem_launch(ctx, R, A, P, cnt, C.ptr, C.col, C.val, s);
-  if (!big.empty()) {
-    unmark_kernel<<<blocks((int64_t)big.size()), kT, 0, s>>>((int64_t)big.size(), d_big, cnt);
-    rap_kernel<<<large->grid(), kT, 0, s>>>(R, A, P, (uint32_t)(large->T - 1), large->keys, large->vals, large->tl,
-                                            cnt, d_big, (int64_t)big.size(), C.ptr, C.col, C.val);
+  // fill: each row by the stage whose table held it (the others skip it: cnt < 0)
+  for (size_t q = 0; q <= stages.size(); ++q) {
+    // rows escalated past stage q (the lists are nested, so marking every later list
+    // marks exactly them) are skipped; stage q does the rest of its rows
+    PSC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * nc, s));
+    for (size_t r = q; r < stages.size(); ++r)
+      mark_kernel<<<blocks(stages[r].nrows), kT, 0, s>>>(stages[r].nrows, stages[r].rows, cnt);
+    if (q == 0) {
+      rap_smem_launch(ctx, R, A, P, cnt, C.ptr, C.col, C.val, s);
+    } else {
+      const Stage& st = stages[q - 1];
+      rap_kernel<<<st.tab->grid(), kT, 0, s>>>(R, A, P, (uint32_t)(st.tab->T - 1), st.tab->keys, st.tab->vals,
+                                               st.tab->tl, cnt, st.rows, st.nrows, C.ptr, C.col, C.val);
+    }
+    PSC_CUDA(cudaGetLastError());
   }
-  PSC_CUDA(cudaGetLastError());
   PSC_CUDA(cudaStreamSynchronize(s));
-  large.reset();
-  dfree(d_big);
+  for (auto& st : stages) dfree(st.rows);
+  stages.clear();
   dfree(cnt);
   return C;
 }

@@ -11,7 +11,7 @@ The hierarchy follows PSCToolkit's VBM set-up (Sec.
 2.3.1): decoupled Vanek-Mandel-Brezina aggregation, tentative prolongator
 Eq. (3) with w = 1, prolongator smoothing P = (I - omega D^-1 A) P^ with
 omega = 1/||D^-1 A||_inf, R = P^T, Galerkin A_{l+1} = P^T A P.
-The C++ builder is ``gen/pscgen.cpp``; input recipe and readings in DESIGN.md.
+The C++ builder is ``pscgen/pscgen.cpp``; input recipe and readings in DESIGN.md.
 """
 from __future__ import annotations
 
@@ -28,7 +28,7 @@ _lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile gen/pscgen.cpp -> gen/libpscgen.so (host C++, OpenMP)."""
+    """Compile pscgen/pscgen.cpp -> pscgen/libpscgen.so (host C++, OpenMP)."""
     src = os.path.join(_HERE, "pscgen.cpp")
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
         tmp = _SO + f".tmp{os.getpid()}"
@@ -45,9 +45,12 @@ def lib():
         L = ctypes.CDLL(_SO)
         i64, i32, f64, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
         L.pscgen_build_grid.restype = vp
-        L.pscgen_build_grid.argtypes = [i64, i64, i64, i32, i32, i32, i32, f64, i64, f64, i32, i64, f64, i32]
+        L.pscgen_build_grid.argtypes = [i64, i64, i64, i32, i32, i32, i32, f64, i64, f64, i32, i64, f64, i32, i32,
+                                        i32]
         L.pscgen_build_csr.restype = vp
-        L.pscgen_build_csr.argtypes = [i64, vp, vp, vp, i32, vp, f64, i32, i64, f64, i32]
+        L.pscgen_build_csr.argtypes = [i64, vp, vp, vp, i32, vp, f64, i32, i64, f64, i32, i32, i32]
+        L.pscgen_match.restype = i64
+        L.pscgen_match.argtypes = [i64, vp, vp, vp, vp, i32, vp, vp]
         L.pscgen_nlevels.restype = i32
         L.pscgen_nlevels.argtypes = [vp]
         L.pscgen_nranks.restype = i32
@@ -185,29 +188,37 @@ def _wrap(handle, meta) -> Hierarchy:
 def poisson_hierarchy(nx: int, ny: int | None = None, nz: int | None = None, procs=(1, 1, 1), *,
                       problem: str = "poisson", jump: float = 1e4, cube: int = 32, theta: float = 0.01,
                       max_levels: int = 20, coarse_target: int = 200, stall_ratio: float = 0.75,
-                      smooth: bool = True, threads: int = 0) -> Hierarchy:
+                      smooth: bool = True, threads: int = 0, aggregation: str = "vmb",
+                      match_sweeps: int = 3) -> Hierarchy:
     """7-point 3D problem on an nx*ny*nz grid split in procs=(px,py,pz) rank boxes.
 
     problem="poisson": -lap u = 1; "jump": BASELINE.json config 5
     (coefficient `jump` on a checkerboard of `cube`^3 cubes; reading R22).
+    aggregation="vmb": decoupled VMB; "matching": compatible weighted matching
+    with match_sweeps sweeps, aggregates of at most 2^k nodes (SMATCH/VMATCH,
+    P:329-330, reading R29).
     """
     ny = nx if ny is None else ny
     nz = nx if nz is None else nz
     px, py, pz = procs
     if threads:
         lib().pscgen_set_threads(threads)
+    if aggregation not in ("vmb", "matching"):
+        raise ValueError("aggregation must be 'vmb' or 'matching'")
     h = lib().pscgen_build_grid(nx, ny, nz, px, py, pz, 0 if problem == "poisson" else 1, jump, cube, theta,
-                                max_levels, coarse_target, stall_ratio, 1 if smooth else 0)
+                                max_levels, coarse_target, stall_ratio, 1 if smooth else 0,
+                                1 if aggregation == "matching" else 0, match_sweeps)
     if not h:
         raise ValueError("grid not divisible by the process grid")
     meta = dict(problem=problem, grid=(nx, ny, nz), procs=tuple(procs), theta=theta, max_levels=max_levels,
-                coarse_target=coarse_target, stall_ratio=stall_ratio, smooth=smooth,
+                coarse_target=coarse_target, stall_ratio=stall_ratio, smooth=smooth, aggregation=aggregation,
                 jump=jump if problem != "poisson" else None, cube=cube if problem != "poisson" else None)
     return _wrap(h, meta)
 
 
 def csr_hierarchy(A, row_start=None, *, theta: float = 0.01, max_levels: int = 20, coarse_target: int = 200,
-                  stall_ratio: float = 0.75, smooth: bool = True) -> Hierarchy:
+                  stall_ratio: float = 0.75, smooth: bool = True, aggregation: str = "vmb",
+                  match_sweeps: int = 3) -> Hierarchy:
     """Hierarchy from a user SPD matrix (scipy.sparse or dense ndarray), row blocks row_start."""
     import scipy.sparse as sp
     A = sp.csr_matrix(A)
@@ -221,7 +232,7 @@ def csr_hierarchy(A, row_start=None, *, theta: float = 0.01, max_levels: int = 2
     val = np.ascontiguousarray(A.data, dtype=np.float64)
     h = lib().pscgen_build_csr(n, ptr.ctypes.data, col.ctypes.data, val.ctypes.data, len(row_start) - 1,
                                row_start.ctypes.data, theta, max_levels, coarse_target, stall_ratio,
-                               1 if smooth else 0)
+                               1 if smooth else 0, 1 if aggregation == "matching" else 0, match_sweeps)
     return _wrap(h, dict(problem="csr", theta=theta, max_levels=max_levels, coarse_target=coarse_target))
 
 
@@ -268,3 +279,21 @@ def rank_levels(h: Hierarchy, r: int) -> list:
             d["R"] = (R.ptr, R.col, R.val)
         out.append(d)
     return out
+
+
+def match(A, w=None, k=1):
+    """One matching aggregation (reading R29) of a square matrix with near-kernel
+    vector w (default 1): returns (agg, values of P^ per node, number of aggregates)."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    n = A.shape[0]
+    w = np.ones(n) if w is None else np.ascontiguousarray(w, dtype=np.float64)
+    ptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    col = np.ascontiguousarray(A.indices, dtype=np.int64)
+    val = np.ascontiguousarray(A.data, dtype=np.float64)
+    agg = np.zeros(n, np.int64)
+    ph = np.zeros(n)
+    nc = lib().pscgen_match(n, ptr.ctypes.data, col.ctypes.data, val.ctypes.data, w.ctypes.data, int(k),
+                            agg.ctypes.data, ph.ctypes.data)
+    return agg, ph, int(nc)

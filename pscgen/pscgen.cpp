@@ -38,6 +38,14 @@
 #include <omp.h>
 #include <cstdio>
 
+#define PSC_GEN_CHECK(c)                                                               \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      fprintf(stderr, "pscgen: check failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);  \
+      abort();                                                                         \
+    }                                                                                  \
+  } while (0)
+
 namespace {
 
 template <class T>
@@ -63,6 +71,7 @@ struct Level {
   std::vector<int64_t> row_start;  // nranks+1
   CSR A, P, R;                     // P: n x n_next, R: n_next x n (absent at coarsest)
   std::vector<int64_t> agg;        // fine node -> global coarse id (absent at coarsest)
+  std::vector<double> w, ph;       // matching: near-kernel vector of the level, tentative P^ values
 };
 
 struct Hier {
@@ -265,6 +274,128 @@ int64_t vmb_aggregate_rank(const CSR& A, const double* diag, int64_t r0, int64_t
   return nagg;
 }
 
+// ------------------------------------------------- matching-based aggregation
+// Coupled aggregation based on compatible weighted matching (Sec. 2.3.1;
+// SPEC S:251-285), restricted to each rank's block here (reading R29):
+//   edge weights c_ij = 1 - 2 a_ij w_i w_j / (a_ii w_i^2 + a_jj w_j^2) on the
+//     off-diagonal pattern (usable when the denominator is non-zero and c_ij > 0);
+//   approximate maximum weight matching: the locally dominant greedy -- repeatedly the
+//     heaviest remaining edge (ties: lexicographically smallest (i, j)), its endpoints
+//     removed (weight >= 1/2 of the optimum);
+//   Eq. (4): a matched pair e = {i, j} gets the column w_e = (w_i, w_j) / ||(w_i, w_j)||,
+//     an unmatched vertex s the column w_s / |w_s|; the coarse near-kernel vector is
+//     P^_1^T w (||w_e|| for a pair, |w_s| for a singleton);
+//   k sweeps ("aggregates of size 2^k"): sweep t matches the unsmoothed Galerkin
+//     matrix of sweep t-1 and the composed P^ = P^_1 P^_2 ... P^_k has one entry per row.
+// Returns the number of aggregates; agg[i] local aggregate, ph[i] = P^_{i, agg(i)}.
+int64_t match_aggregate_rank(const CSR& A, int64_t r0, int64_t r1, const double* w0, int k, int64_t* agg_out,
+                             double* ph_out) {
+  const int64_t nloc = r1 - r0;
+  // current level: local CSR (rows/cols 0..m-1), near-kernel vector
+  std::vector<int64_t> ptr(nloc + 1, 0), col;
+  std::vector<double> val, w(w0, w0 + nloc);
+  for (int64_t i = r0; i < r1; ++i) {
+    for (int64_t q = A.ptr[i]; q < A.ptr[i + 1]; ++q) {
+      const int64_t j = A.col[q];
+      if (j < r0 || j >= r1) continue;  // decoupled per rank block
+      col.push_back(j - r0);
+      val.push_back(A.val[q]);
+    }
+    ptr[i - r0 + 1] = (int64_t)col.size();
+  }
+  std::vector<int64_t> agg(nloc);
+  std::vector<double> ph(nloc, 1.0);
+  for (int64_t i = 0; i < nloc; ++i) agg[i] = i;
+  int64_t m = nloc;
+  for (int sweep = 0; sweep < k && m > 1; ++sweep) {
+    std::vector<double> d(m, 0.0);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q)
+        if (col[q] == i) d[i] = val[q];
+    struct Edge {
+      double c;
+      int64_t i, j;
+    };
+    std::vector<Edge> E;
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) {
+        const int64_t j = col[q];
+        if (j <= i) continue;
+        const double den = d[i] * w[i] * w[i] + d[j] * w[j] * w[j];
+        if (den == 0.0) continue;
+        const double c = 1.0 - 2.0 * val[q] * w[i] * w[j] / den;
+        if (c > 0.0) E.push_back({c, i, j});
+      }
+    std::stable_sort(E.begin(), E.end(), [](const Edge& a, const Edge& b) {
+      if (a.c != b.c) return a.c > b.c;
+      if (a.i != b.i) return a.i < b.i;
+      return a.j < b.j;
+    });
+    std::vector<int64_t> mate(m, -1);
+    for (const Edge& e : E)
+      if (mate[e.i] < 0 && mate[e.j] < 0) {
+        mate[e.i] = e.j;
+        mate[e.j] = e.i;
+      }
+    // coarse numbering in increasing index of each pair's (or singleton's) first node
+    std::vector<int64_t> cid(m, -1);
+    std::vector<double> cval(m), wc;
+    int64_t mc = 0;
+    for (int64_t i = 0; i < m; ++i) {
+      if (cid[i] >= 0) continue;
+      const int64_t j = mate[i];
+      if (j < 0) {  // singleton: w_s / |w_s|, coarse w = |w_s|
+        PSC_GEN_CHECK(w[i] != 0.0);
+        cid[i] = mc;
+        cval[i] = w[i] / std::fabs(w[i]);
+        wc.push_back(std::fabs(w[i]));
+      } else {  // pair: (w_i, w_j) / ||.||, coarse w = ||.||
+        const double nrm = std::sqrt(w[i] * w[i] + w[j] * w[j]);
+        PSC_GEN_CHECK(nrm != 0.0);
+        cid[i] = cid[j] = mc;
+        cval[i] = w[i] / nrm;
+        cval[j] = w[j] / nrm;
+        wc.push_back(nrm);
+      }
+      ++mc;
+    }
+    // compose the fine assignment and its value
+    for (int64_t f = 0; f < nloc; ++f) {
+      ph[f] *= cval[agg[f]];
+      agg[f] = cid[agg[f]];
+    }
+    // unsmoothed Galerkin of this sweep: A_c[I, J] = sum cval_i a_ij cval_j
+    std::vector<std::vector<std::pair<int64_t, double>>> rows(mc);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) {
+        const int64_t j = col[q];
+        rows[cid[i]].push_back({cid[j], cval[i] * val[q] * cval[j]});
+      }
+    std::vector<int64_t> nptr(mc + 1, 0), ncol;
+    std::vector<double> nval;
+    for (int64_t I = 0; I < mc; ++I) {
+      auto& r = rows[I];
+      std::stable_sort(r.begin(), r.end(), [](const std::pair<int64_t, double>& a,
+                                              const std::pair<int64_t, double>& b) { return a.first < b.first; });
+      for (size_t t = 0; t < r.size(); ++t) {
+        if (!ncol.empty() && (int64_t)ncol.size() > nptr[I] && ncol.back() == r[t].first) nval.back() += r[t].second;
+        else { ncol.push_back(r[t].first); nval.push_back(r[t].second); }
+      }
+      nptr[I + 1] = (int64_t)ncol.size();
+    }
+    ptr.swap(nptr);
+    col.swap(ncol);
+    val.swap(nval);
+    w.swap(wc);
+    m = mc;
+  }
+  for (int64_t f = 0; f < nloc; ++f) {
+    agg_out[f] = agg[f];
+    ph_out[f] = ph[f];
+  }
+  return m;
+}
+
 // ---------------------------------------------------------- prolongator
 struct SmoothedPRow {
   const CSR* A;
@@ -272,19 +403,21 @@ struct SmoothedPRow {
   const int64_t* agg;
   double omega;
   bool smooth;
+  const double* ph = nullptr;  // tentative value of each node (nullptr: 1, Eq. (3) with w = 1)
   int make_state() const { return 0; }
   void operator()(int&, int64_t i, std::vector<int64_t>& col, std::vector<double>& val) const {
-    if (!smooth) {  // tentative prolongator, Eq. (3) with w = 1
+    const double phi = ph ? ph[i] : 1.0;
+    if (!smooth) {  // tentative prolongator: Eq. (3) with w = 1, or Eq. (4) (matching)
       col.push_back(agg[i]);
-      val.push_back(1.0);
+      val.push_back(phi);
       return;
     }
-    // P_i. = e_{agg(i)} - (omega / a_ii) * sum_k a_ik e_{agg(k)}
+    // P_i. = P^_i. - (omega / a_ii) * sum_k a_ik P^_k.
     const int64_t k0 = A->ptr[i], k1 = A->ptr[i + 1];
     const size_t base = col.size();
     for (int64_t k = k0; k < k1; ++k) {
       int64_t J = agg[A->col[k]];
-      double a = A->val[k];
+      double a = ph ? A->val[k] * ph[A->col[k]] : A->val[k];
       size_t t = base;
       while (t < col.size() && col[t] != J) ++t;
       if (t == col.size()) { col.push_back(J); val.push_back(a); }
@@ -294,10 +427,10 @@ struct SmoothedPRow {
     bool have_own = false;
     for (size_t t = base; t < col.size(); ++t) {
       double v = -s * val[t];
-      if (col[t] == agg[i]) { v = 1.0 + v; have_own = true; }
+      if (col[t] == agg[i]) { v = phi + v; have_own = true; }
       val[t] = v;
     }
-    if (!have_own) { col.push_back(agg[i]); val.push_back(1.0); }
+    if (!have_own) { col.push_back(agg[i]); val.push_back(phi); }
     // sort the row by column
     const size_t m = col.size() - base;
     for (size_t a = 1; a < m; ++a) {
@@ -427,6 +560,8 @@ struct Params {
   int64_t coarse_target = 200;
   double stall_ratio = 0.75;
   int smooth = 1;
+  int aggr = 0;          // 0: decoupled VMB; 1: matching
+  int match_sweeps = 3;  // matching: k sweeps, aggregates of at most 2^k nodes ("maximum size 8")
 };
 
 void diag_of(const CSR& A, std::vector<double>& d) {
@@ -459,10 +594,23 @@ void build_levels(Hier* h, const Params& prm) {
     // decoupled aggregation, independently per rank
     std::vector<int64_t> agg_local(L.n);
     std::vector<int64_t> nagg(h->nranks);
+    L.ph.clear();
+    if (prm.aggr == 1) {
+      // near-kernel vector w = 1 at level 0; at coarser levels P^_{l-1}^T w_{l-1} is
+      // carried as the level's w (the unit vector's coarse image)
+      if (L.w.empty()) L.w.assign(L.n, 1.0);
+      L.ph.assign(L.n, 1.0);
 #pragma omp parallel for schedule(dynamic, 1)
-    for (int r = 0; r < h->nranks; ++r)
-      nagg[r] = vmb_aggregate_rank(L.A, diag.data(), L.row_start[r], L.row_start[r + 1], prm.theta,
-                                   agg_local.data() + L.row_start[r]);
+      for (int r = 0; r < h->nranks; ++r)
+        nagg[r] = match_aggregate_rank(L.A, L.row_start[r], L.row_start[r + 1], L.w.data() + L.row_start[r],
+                                       prm.match_sweeps, agg_local.data() + L.row_start[r],
+                                       L.ph.data() + L.row_start[r]);
+    } else {
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int r = 0; r < h->nranks; ++r)
+        nagg[r] = vmb_aggregate_rank(L.A, diag.data(), L.row_start[r], L.row_start[r + 1], prm.theta,
+                                     agg_local.data() + L.row_start[r]);
+    }
     TLOG("aggregate");
     std::vector<int64_t> crs(h->nranks + 1, 0);
     for (int r = 0; r < h->nranks; ++r) crs[r + 1] = crs[r] + nagg[r];
@@ -484,7 +632,8 @@ void build_levels(Hier* h, const Params& prm) {
     }
     const double omega = 1.0 / nrm;
     h->omega.push_back(prm.smooth ? omega : 0.0);
-    SmoothedPRow prow{&L.A, diag.data(), L.agg.data(), omega, prm.smooth != 0};
+    SmoothedPRow prow{&L.A, diag.data(), L.agg.data(), omega, prm.smooth != 0,
+                      L.ph.empty() ? nullptr : L.ph.data()};
     build_csr_chunked(L.P, L.n, nc, prow);
     TLOG("prolongator");
     transpose(L.P, L.R);
@@ -492,6 +641,10 @@ void build_levels(Hier* h, const Params& prm) {
     Level NL;
     NL.n = nc;
     NL.row_start = crs;
+    if (prm.aggr == 1) {  // coarse near-kernel vector P^^T w: sum over each aggregate of ph_i w_i
+      NL.w.assign(nc, 0.0);
+      for (int64_t i = 0; i < L.n; ++i) NL.w[L.agg[i]] += L.ph[i] * L.w[i];
+    }
     if (L.A.nnz() <= 8 * L.n) {  // stencil-like A: direct triple product
       RAPRow rrow{&L.R, &L.A, &L.P, nc};
       build_csr_chunked(NL.A, nc, nc, rrow);
@@ -515,7 +668,7 @@ extern "C" {
 // px*py*pz rank boxes.  problem: 0 = Poisson, 1 = jump diffusion.
 void* pscgen_build_grid(int64_t nx, int64_t ny, int64_t nz, int px, int py, int pz, int problem,
                         double jump, int64_t cube, double theta, int max_levels, int64_t coarse_target,
-                        double stall_ratio, int smooth) {
+                        double stall_ratio, int smooth, int aggr, int match_sweeps) {
   if (nx % px || ny % py || nz % pz) return nullptr;
   Grid g{nx, ny, nz, px, py, pz, nx / px, ny / py, nz / pz};
   Coef cf{problem, jump, cube};
@@ -534,6 +687,8 @@ void* pscgen_build_grid(int64_t nx, int64_t ny, int64_t nz, int px, int py, int 
   prm.coarse_target = coarse_target;
   prm.stall_ratio = stall_ratio;
   prm.smooth = smooth;
+  prm.aggr = aggr;
+  prm.match_sweeps = match_sweeps;
   build_levels(h, prm);
   return h;
 }
@@ -542,7 +697,7 @@ void* pscgen_build_grid(int64_t nx, int64_t ny, int64_t nz, int px, int py, int 
 // contiguous row partition row_start[0..nranks].
 void* pscgen_build_csr(int64_t n, const int64_t* ptr, const int64_t* col, const double* val, int nranks,
                        const int64_t* row_start, double theta, int max_levels, int64_t coarse_target,
-                       double stall_ratio, int smooth) {
+                       double stall_ratio, int smooth, int aggr, int match_sweeps) {
   Hier* h = new Hier();
   h->nranks = nranks;
   Level L0;
@@ -564,8 +719,25 @@ void* pscgen_build_csr(int64_t n, const int64_t* ptr, const int64_t* col, const 
   prm.coarse_target = coarse_target;
   prm.stall_ratio = stall_ratio;
   prm.smooth = smooth;
+  prm.aggr = aggr;
+  prm.match_sweeps = match_sweeps;
   build_levels(h, prm);
   return h;
+}
+
+// One matching aggregation (k sweeps) of an n x n CSR with near-kernel vector w
+// (tests: SPEC S:260-285 examples).  Returns the number of aggregates.
+int64_t pscgen_match(int64_t n, const int64_t* ptr, const int64_t* col, const double* val, const double* w, int k,
+                     int64_t* agg, double* ph) {
+  CSR A;
+  A.nrows = A.ncols = n;
+  A.ptr.alloc(n + 1);
+  std::memcpy(A.ptr.data(), ptr, (n + 1) * sizeof(int64_t));
+  A.col.alloc(ptr[n]);
+  A.val.alloc(ptr[n]);
+  std::memcpy(A.col.data(), col, ptr[n] * sizeof(int64_t));
+  std::memcpy(A.val.data(), val, ptr[n] * sizeof(double));
+  return match_aggregate_rank(A, 0, n, w, k, agg, ph);
 }
 
 int pscgen_nlevels(void* hp) { return (int)((Hier*)hp)->lv.size(); }

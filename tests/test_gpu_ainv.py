@@ -99,10 +99,11 @@ def test_update_values_and_rebuild_smoothers(psc, smoother):
     H, descs, A, P, R = psc.build_hierarchy(ctx, pscgen.rank_levels(h, 0), smoother=smoother, ainv_drop=0.1,
                                             pre=1 if smoother == "ainv" else 4, post=1 if smoother == "ainv" else 4)
     b = pscgen.rhs_random(2, 0, n)
-    # new coefficients: a variable diagonal shift and scaled couplings, same pattern
+    # new coefficients on the same pattern, still SPD (diagonally dominant): a variable
+    # diagonal and scaled couplings
     A0 = h.levels[0].A.to_scipy().tocsr()
     rows = np.repeat(np.arange(n), np.diff(A0.indptr))
-    newval = np.where(A0.indices == rows, A0.data * (1.0 + 0.3 * np.sin(rows)), 1.2 * A0.data)
+    newval = np.where(A0.indices == rows, A0.data * (1.1 + 0.2 * np.sin(rows)), 0.9 * A0.data)
     A[0].update_values(newval)
     # the matrix itself changed at once
     xr = pscgen.rhs_random(5, 0, n)

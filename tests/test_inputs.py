@@ -145,3 +145,105 @@ def test_csr_arrays_outlive_the_hierarchy_object():
     assert S.indptr[0] == 0 and S.shape == (125, 125) and S.nnz == 725
     np.testing.assert_array_equal(S.diagonal(), np.full(125, 6.0))
     del junk
+
+
+# ------------------------------------------ matching-based hierarchies (NEXT-3 set-up)
+def test_matching_spec_examples():
+    """SPEC S:263-278 (approx_max_weight_matching, matching_aggregate) with w = 1 and unit
+    diagonals, so c_ij = 1 - a_ij (weights set through the couplings)."""
+    import scipy.sparse as sp
+    from _util import tridiag
+    # path a-b-c with weights 1.2 then 1.5 -> (b, c) matched, a unmatched
+    A = sp.csr_matrix(np.array([[1.0, -0.2, 0.0], [-0.2, 1.0, -0.5], [0.0, -0.5, 1.0]]))
+    agg, ph, nc = pscgen.match(A, k=1)
+    assert nc == 2 and agg[1] == agg[2] and agg[0] != agg[1]
+    # triangle with equal weights -> exactly one edge (the lexicographically smallest), one vertex free
+    T = sp.csr_matrix(np.array([[1.0, -0.3, -0.3], [-0.3, 1.0, -0.3], [-0.3, -0.3, 1.0]]))
+    agg, ph, nc = pscgen.match(T, k=1)
+    assert nc == 2 and agg[0] == agg[1] and agg[2] != agg[0]
+    # 4-node path, uniform weights: k = 1 -> 2 pairs; k = 2 -> one aggregate of 4 (S:273-274)
+    agg, ph, nc = pscgen.match(tridiag(4), k=1)
+    assert nc == 2 and np.array_equal(agg, [0, 0, 1, 1])
+    np.testing.assert_allclose(ph, np.full(4, 1 / np.sqrt(2)), rtol=1e-15)  # Eq. (4): (1,1)/sqrt(2)
+    agg, ph, nc = pscgen.match(tridiag(4), k=2)
+    assert nc == 1 and np.array_equal(agg, [0, 0, 0, 0])
+    np.testing.assert_allclose(ph, np.full(4, 0.5), rtol=1e-15)
+    # isolated vertex with w_s = 2 -> singleton, column entry 2/|2| = 1 (S:275, Eq. (4) W)
+    agg, ph, nc = pscgen.match(sp.csr_matrix(np.array([[3.0]])), w=np.array([2.0]), k=1)
+    assert nc == 1 and ph[0] == 1.0
+
+
+def _brute_max_matching(n, edges):
+    """Exact maximum weight matching by exhaustive recursion on the lowest free vertex."""
+    wt = {}
+    for c, i, j in edges:
+        wt[(i, j)] = wt[(j, i)] = c
+
+    def best(free):
+        if not free:
+            return 0.0
+        v, rest = free[0], free[1:]
+        b = best(rest)  # v unmatched
+        for u in rest:
+            if (v, u) in wt:
+                b = max(b, wt[(v, u)] + best(tuple(x for x in rest if x != u)))
+        return b
+
+    return best(tuple(range(n)))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_matching_half_approximation_and_orthonormal_prolongator(seed):
+    """The greedy matching is a valid matching with weight >= 1/2 of the optimum (brute
+    force on small graphs); P^ of Eq. (4) has orthonormal columns and w in its range."""
+    import scipy.sparse as sp
+    from _util import random_spd_mixed
+    A = random_spd_mixed(9, 0.25, seed)
+    w = 1.0 + np.random.default_rng(seed).random(9)
+    agg, ph, nc = pscgen.match(A, w=w, k=1)
+    Ad = A.toarray()
+    d = np.diag(Ad)
+    edges = []
+    for i in range(9):
+        for j in range(i + 1, 9):
+            if Ad[i, j] != 0.0:
+                c = 1.0 - 2.0 * Ad[i, j] * w[i] * w[j] / (d[i] * w[i] ** 2 + d[j] * w[j] ** 2)
+                if c > 0:
+                    edges.append((c, i, j))
+    pairs = [np.flatnonzero(agg == a) for a in range(nc)]
+    assert all(len(p) <= 2 for p in pairs)
+    got = 0.0
+    for p in pairs:
+        if len(p) == 2:
+            c = [e[0] for e in edges if e[1] == p[0] and e[2] == p[1]]
+            assert c, p  # matched along a usable edge
+            got += c[0]
+    assert got >= 0.5 * _brute_max_matching(9, edges) - 1e-12
+    P = sp.csr_matrix((ph, (np.arange(9), agg)), shape=(9, nc)).toarray()
+    np.testing.assert_allclose(P.T @ P, np.eye(nc), rtol=0, atol=1e-14)
+    np.testing.assert_allclose(P @ (P.T @ w), w, rtol=1e-14)
+
+
+def test_matching_hierarchies_vs_paper_fig2_fig3():
+    """SMATCH / VMATCH: aggregates of at most 8 = 2^3 nodes, smoothed / un-
+    smoothed prolongators.  Operator complexity near Fig. 3's 1 GPU values (SMATCH 1.894,
+    VMATCH 1.142; loose: the paper's matrix is 200^3, ours 64^3) and the
+    iteration order of Fig. 2 at 1 GPU (SMATCH 9 < VBM 18 < VMATCH 28, P:380, P:399, P:418;
+    FCG + coarsest PCG(40) to 1e-6 as in the paper's configurations)."""
+    import oracle
+    g = 64
+    hs = pscgen.poisson_hierarchy(g, aggregation="matching", smooth=True)
+    hv = pscgen.poisson_hierarchy(g, aggregation="matching", smooth=False)
+    hb = pscgen.poisson_hierarchy(g)
+    assert abs(hs.operator_complexity() - 1.894) <= 0.1
+    assert abs(hv.operator_complexity() - 1.142) <= 0.01
+    for h in (hs, hv):
+        for l in range(h.nlevels - 1):
+            assert h.levels[l].n <= 8 * h.levels[l + 1].n
+    b = pscgen.rhs_poisson((g,) * 3, 0, g ** 3)
+    kw = dict(coarse_pcg=True, coarse_maxit=40, coarse_tol=1e-10)
+    its = oracle.fcg(hs, b, tol=1e-6, **kw)[1]
+    itv = oracle.fcg(hv, b, tol=1e-6, pre=2, post=2, variable_v=True, **kw)[1]
+    itb = oracle.fcg(hb, b, tol=1e-6, **kw)[1]
+    assert abs(its - 9) <= 3
+    assert its < itb < itv
