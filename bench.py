@@ -182,7 +182,8 @@ def run_reference(args, rank, world, out=sys.stdout):
     import pscgen
     cores = oracle.set_threads(oracle_threads())
     g = args.grid
-    h = pscgen.poisson_hierarchy(g, g, g, (1, 1, 1), problem=args.problem, smooth=not args.unsmoothed_p)
+    h = pscgen.poisson_hierarchy(g, g, g, (1, 1, 1), problem=args.problem, smooth=not args.unsmoothed_p,
+                                 aggregation=_aggregation(args))
     n = h.levels[0].n
     b = pscgen.rhs_poisson((g, g, g), 0, n)
     per_it = []
@@ -220,7 +221,13 @@ def _metric(args):
         var += ", un-smoothed P"
     if args.coarse_solver == "pcg":
         var += ", coarsest PCG"
+    if args.hierarchy != "vmb":
+        var += f", {args.hierarchy.upper()} hierarchy"
     return f"AMG-{args.krylov.upper()} Mdof*iters/s (3D {args.problem}, {scope}, tol {args.tol:g}{var})"
+
+
+def _aggregation(args):
+    return "matching" if args.hierarchy in ("smatch", "vmatch") else "vmb"
 
 
 def _oracle_solve(args):
@@ -243,7 +250,9 @@ def _solver_desc(args):
               else "30 coarsest l1-Jacobi sweeps")
     cyc = "variable V(2*2^l,2*2^l)" if args.variable_v else "V(4,4)"
     prol = ", un-smoothed P" if args.unsmoothed_p else ""
-    return f"{args.krylov.upper()}, {cyc} l1-Jacobi, {coarse}{prol}"
+    hier = {"vmb": "decoupled VMB", "smatch": "matching (<= 8), smoothed P",
+            "vmatch": "matching (<= 8)"}[args.hierarchy]
+    return f"{args.krylov.upper()}, {cyc} l1-Jacobi, {coarse}{prol}, {hier} aggregation"
 
 
 # ------------------------------------------------------------------- main
@@ -281,11 +290,16 @@ def main():
     ap.add_argument("--vbm", action="store_true", help="the paper's VBM solve: --krylov fcg --coarse-solver pcg")
     ap.add_argument("--variable-v", action="store_true",
                     help="variable V-cycle (P:330 footnote): 2 sweeps at level 0, doubled per level")
+    ap.add_argument("--hierarchy", default="vmb", choices=["vmb", "smatch", "vmatch"],
+                    help="aggregation (P:328-330): decoupled VMB; matching with aggregates <= 8 and smoothed "
+                         "(SMATCH) or tentative (VMATCH, implies --unsmoothed-p --variable-v) prolongators")
     ap.add_argument("--unsmoothed-p", action="store_true",
                     help="tentative (un-smoothed) prolongators, as VMATCH (P:330), on the same aggregates")
     args = ap.parse_args()
     if args.vbm:
         args.krylov, args.coarse_solver = "fcg", "pcg"
+    if args.hierarchy == "vmatch":
+        args.unsmoothed_p, args.variable_v = True, True
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -340,17 +354,17 @@ def main():
     h = None
     # one GPU: the hierarchy is built on the device from A_0 (psc_amg_build, NEXT-1);
     # several GPUs (decoupled per-rank set-up) or --unsmoothed-p: the host generator
-    device_setup = (N == 1 and args.setup == "gpu" and not args.unsmoothed_p)
+    device_setup = (N == 1 and args.setup == "gpu" and not args.unsmoothed_p and args.hierarchy == "vmb")
     if N == 1:
         h = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem, smooth=not args.unsmoothed_p,
-                                     max_levels=1 if device_setup else 20)
+                                     max_levels=1 if device_setup else 20, aggregation=_aggregation(args))
         levels = pscgen.rank_levels(h, 0)
     else:
         shm = (f"/dev/shm/psc_bench_{args.problem}_{grid[0]}x{grid[1]}x{grid[2]}_{px}{py}{pz}"
-               + ("_tentP" if args.unsmoothed_p else ""))
+               + ("_tentP" if args.unsmoothed_p else "") + f"_{args.hierarchy}")
         if rank == 0 and not os.path.exists(os.path.join(shm, "meta.json")):
             hh = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem,
-                                          smooth=not args.unsmoothed_p)
+                                          smooth=not args.unsmoothed_p, aggregation=_aggregation(args))
             save_rank_levels(shm, hh, N)
             del hh
         dist.barrier()
@@ -494,7 +508,7 @@ def main():
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         import oracle
         cores = oracle.set_threads(oracle_threads())
-        if h is None:  # same rules, host generator (equal to the device set-up up to rounding)
+        if h is None or h.nlevels == 1:  # same rules, host generator (equal to the device set-up up to rounding)
             h = pscgen.poisson_hierarchy(*grid, procs=(px, py, pz), problem=args.problem)
         bcpu = pscgen.rhs_poisson(grid, 0, n_global)
         s_it, tc = oracle_seconds_per_iteration(args, h, bcpu)
