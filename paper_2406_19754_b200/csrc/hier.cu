@@ -146,6 +146,12 @@ void allgather_slot(psc_hier* h, Slot s, cudaStream_t st) {
 void exchange(psc_hier* h, psc_desc* d, double* x, cudaStream_t s) {
   psc_ctx* ctx = h->ctx;
   if (ctx->nranks == 1) return;
+  // TEST HOOK ("halo freshness"): PSC_DEBUG_POISON_HALO=1 fills the halo
+  // slots with NaN (all-ones bytes) right before every exchange; a slot the exchange
+  // failed to refresh would carry the NaN into the owned results
+  static const bool poison = getenv("PSC_DEBUG_POISON_HALO") != nullptr;
+  if (poison && d->n_halo() > 0)
+    PSC_CUDA(cudaMemsetAsync(x + d->n_own, 0xFF, sizeof(double) * d->n_halo(), s));
   if (p2p_halo(ctx, h->p2p, d, x, s)) return;
   halo_exchange(ctx, d, x, s);
 }
@@ -693,6 +699,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing, int method) {
 }
 
 void capture_iteration(psc_hier* h, int method, bool profile = false) {
+  NvtxRange nv("psc_capture_iteration");
   psc_ctx* ctx = h->ctx;
   cudaStream_t s = ctx->stream;
   const int64_t l0 = ctx->launches, c0 = ctx->collectives;
@@ -991,6 +998,7 @@ struct KProf {
 
 int solve_impl(psc_hier* h, int method, const double* b, double* x, double tol, int maxit, double* hist,
                psc_stats* st, double extra_h2d, KProf* prof = nullptr) {
+  NvtxRange nv(method == PSC_KRYLOV_FCG ? "psc_fcg_solve" : "psc_pcg_solve");
   psc_ctx* ctx = h->ctx;
   cudaStream_t s = ctx->stream;
   const int R = ctx->nranks;
@@ -1123,6 +1131,7 @@ extern "C" {
 
 int psc_hier_create(psc_ctx* ctx, int nlevels, psc_mat* const* A, psc_mat* const* P, psc_mat* const* R,
                     const psc_cycle_opts* opts, psc_hier** out) {
+  NvtxRange nv("psc_hier_create");
   psc_hier* h = nullptr;
   try {
     PSC_REQUIRE(ctx && out && A && nlevels >= 1, PSC_ERR_ARG, "bad argument");

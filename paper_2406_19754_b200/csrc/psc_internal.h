@@ -11,6 +11,8 @@
 
 #include "psc.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace psc {
 
 constexpr int kSlice = 32;        // rows per sliced-ELL slice = warp size ("based on the size of a warp")
@@ -115,6 +117,13 @@ struct RedSite {
 }  // namespace psc
 
 namespace psc {
+// NVTX range for the host phases (visible in nsys / ncu --nvtx): set-up steps, graph
+// capture, each solve
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 // Per-kernel device timing (psc_hier_kernel_profile): while `on`, every launcher
 // brackets its launch with an event pair (recorded as graph nodes when captured)
 // and files it under (name, level) with its algorithmic and layout bytes.

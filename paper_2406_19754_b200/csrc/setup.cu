@@ -386,6 +386,7 @@ namespace {
 
 // decoupled VMB aggregation of one level (one rank): returns the number of aggregates
 int64_t aggregate(psc_ctx* ctx, AmgLevel& L, double theta) {
+  NvtxRange nv("psc_amg_aggregate");
   cudaStream_t s = ctx->stream;
   const DCsr& A = L.A;
   const int64_t n = A.n;
@@ -609,6 +610,7 @@ struct RapTables {
 // product count is a poor bound on a row's distinct columns: ~35,000 products for
 // ~120 columns on level 2 of 256^3).
 DCsr galerkin(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P) {
+  NvtxRange nv("psc_amg_galerkin");
   cudaStream_t s = ctx->stream;
   const int64_t nc = R.n;
   PSC_REQUIRE(P.ncols < INT32_MAX, PSC_ERR_STATE, "Galerkin: more than 2^31 coarse columns");

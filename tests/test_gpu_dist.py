@@ -43,10 +43,12 @@ def test_four_gpu_parity():
     _run(4, (32, 32, 32), (1, 2, 2))
 
 
-@pytest.mark.parametrize("env", [{"PSC_REPL_ROWS": "0"}, {"PSC_REPL_ROWS": "100000000"},
+@pytest.mark.parametrize("env", [{"PSC_DEBUG_POISON_HALO": "1"}, {"PSC_DEBUG_POISON_HALO": "1", "PSC_NO_P2P": "1"},
+                                 {"PSC_REPL_ROWS": "0"}, {"PSC_REPL_ROWS": "100000000"},
                                  {"PSC_NO_P2P": "1"}, {"PSC_OVERLAP": "1"}, {"PSC_OVERLAP": "1", "PSC_NO_P2P": "1"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_two_gpu_exchange_and_replication_variants(env):
-    """Replicated suffix from the coarsest level only / from level 1; NVLink and
-    NCCL halo exchanges; exchange / interior overlap: all must match the oracle."""
+    """Halo slots poisoned with NaN before every exchange (no NaN may leak
+    into owned results); replicated suffix from the coarsest level only / from level 1;
+    NVLink and NCCL halo exchanges; exchange / interior overlap: all must match the oracle."""
     _run(2, (32, 32, 64), (1, 1, 2), env_extra=env)
