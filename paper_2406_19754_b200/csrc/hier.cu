@@ -476,14 +476,12 @@ void ainv_sweep(psc_hier* h, LevelWS& W, const double* b, double* x, bool from_z
 // A smoothing phase of this level as one cooperative launch (launch_coop_sweeps): the
 // matrix stays in L2 across the sweeps (sliced ELL, natural row order, at most
 // PSC_COOP_MB = 96 MB of values and columns), no halo (one rank or the replicated
-// suffix), l1-Jacobi.  Opt-in (PSC_COOP=1): on level 2 of 256^3 (65,000 rows, 62 MB)
-// a grid-synchronised stage took ~23 us against ~19.5 us per stand-alone launch
-// (94 vs 78 us per four-stage phase; 3719 vs 3793 Mdof*iters/s on one box).
+// suffix), l1-Jacobi.  PSC_NO_COOP=1: stage by stage.
 bool coop_ok(const psc_hier* h, const LevelWS& W, int nsweeps) {
-  static const bool off = getenv("PSC_COOP") == nullptr;
+  static const bool off = getenv("PSC_NO_COOP") != nullptr;
   static const int64_t lim = (getenv("PSC_COOP_MB") ? atoll(getenv("PSC_COOP_MB")) : 96) << 20;
   const Sell& S = W.A->S;
-  return !off && nsweeps >= 1 && !W.ainv && S.lanes == 1 && !S.c8 && !S.perm && W.nh == 0 && (h->ctx->nranks == 1 || !W.d) &&
+  return !off && nsweeps >= 1 && !W.ainv && S.lanes == 1 && !S.perm && W.nh == 0 && (h->ctx->nranks == 1 || !W.d) &&
          S.padded * 8 + S.col_slots * 4 <= lim && S.n_units > 0;
 }
 

@@ -113,14 +113,10 @@ __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int
 __device__ __forceinline__ double ldm(const double* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
 __device__ __forceinline__ int32_t ldm(const int32_t* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
 
-// x gathers: read-only texture path, or (CG) a coherent L1-cached load for vectors
-// written earlier in the same cooperative launch (sell_coop_sweeps): the grid barrier's
-// acquire fence invalidates the SM's L1, so after it ld.ca sees the other CTAs' writes
-// while neighbouring rows still share the L1 lines (ld.cg, L2 only, took 27 vs 19 us
-// per level-2 stage at 256^3)
+// x gathers: read-only texture path, or (CG) through L2 only
 template <bool CG>
 __device__ __forceinline__ double ldx(const double* p) {
-  if constexpr (CG) return __ldca(p);
+  if constexpr (CG) return __ldcg(p);
   else return __ldg(p);
 }
 
@@ -408,55 +404,6 @@ __device__ __forceinline__ void sell_body(const RowKArgs& a) {
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
-// SELL-8: a warp takes four 8-row units (lanes 8q..8q+7 unit q), one thread per row;
-// each lane loops over its own unit's width (the row sum in stored order, as ELL)
-template <RowOp OP>
-__device__ __forceinline__ void sell8_body(const RowKArgs& a) {
-  constexpr int NR = NRed<OP>::value;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int64_t stride = (int64_t)gridDim.x * kWarpsPerBlock * 4;
-  const bool keep = a.keep_matrix != 0;
-  double acc[NR > 0 ? NR : 1] = {};
-  for (int64_t t = ((int64_t)blockIdx.x * kWarpsPerBlock + warp) * 4 + (lane >> 3); t - (lane >> 3) < a.nlist;
-       t += stride) {
-    const bool has = t < a.nlist;
-    const int64_t u = has ? (a.list ? (int64_t)a.list[t] : t) : 0;
-    const int64_t i = u * 8 + (lane & 7);
-    const bool live = has && i < a.n_rows;
-    double sum = 0.0;
-    EpiIn e{0.0, 0.0, 0.0};
-    if (live) {
-      e = epi_load<OP>(a, i);
-      const int64_t b0 = __ldg(a.ptr + u);
-      const int w = (int)((__ldg(a.ptr + u + 1) - b0) >> 3);
-      const int32_t* c = a.col + b0 + (lane & 7);
-      const double* v = a.val + b0 + (lane & 7);
-      int k = 0;
-      for (; k + 8 <= w; k += 8) {
-        int ci[8];
-        double vi[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          ci[j] = ldm(c + 8 * j, keep);
-          vi[j] = ldm(v + 8 * j, keep);
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sum = fma(vi[j], __ldg(a.x + ci[j]), sum);
-        c += 64;
-        v += 64;
-      }
-      for (; k < w; ++k) {
-        sum = fma(ldm(v, keep), __ldg(a.x + ldm(c, keep)), sum);
-        c += 8;
-        v += 8;
-      }
-      epi_store<OP>(a, i, sum, e, acc);
-    }
-  }
-  if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
-}
-
 // row groups: one warp per unit of 32/G rows, G lanes per row, fixed shuffle tree
 template <RowOp OP, int G>
 __device__ __forceinline__ void rg_body(const RowKArgs& a) {
@@ -487,7 +434,6 @@ __device__ __forceinline__ void rg_body(const RowKArgs& a) {
 // One named kernel per (layout, epilogue): readable launch lists and ncu filters.
 #define PSC_ROW_KERNELS(name, OP)                                                                         \
   __global__ void __launch_bounds__(kBlock, PSC_SELL_MINB) sell_##name(RowKArgs a) { sell_body<OP>(a); }  \
-  __global__ void __launch_bounds__(kBlock, PSC_SELL_MINB) sell8_##name(RowKArgs a) { sell8_body<OP>(a); } \
   template <int G>                                                                                        \
   __global__ void __launch_bounds__(kBlock) rg_##name(RowKArgs a) {                                      \
     rg_body<OP, G>(a);                                                                                    \
@@ -513,20 +459,6 @@ static RowKernel rg_kernel(RowOp op) {
     case RowOp::Resid: return rg_resid<G>;
     case RowOp::ResidDot2: return rg_resid_dot2<G>;
     case RowOp::PAdd: return rg_padd<G>;
-    case RowOp::Sweep0: break;
-  }
-  return nullptr;
-}
-
-static RowKernel sell8_kernel(RowOp op) {
-  switch (op) {
-    case RowOp::Spmv: return sell8_spmv;
-    case RowOp::SpmvDot: return sell8_spmv_dot;
-    case RowOp::Sweep: return sell8_sweep;
-    case RowOp::SweepDot: return sell8_sweep_dot;
-    case RowOp::Resid: return sell8_resid;
-    case RowOp::ResidDot2: return sell8_resid_dot2;
-    case RowOp::PAdd: return sell8_padd;
     case RowOp::Sweep0: break;
   }
   return nullptr;
@@ -998,9 +930,8 @@ static void row_bytes(const Sell& A, RowOp op, const RowArgs& r, double& alg, do
     case RowOp::PAdd: vec += 16.0 * n; break;
     case RowOp::Sweep0: vec = 24.0 * n; break;
   }
-  const double hdr = A.c8 ? 8.0 * (double)(A.n_units + 1)
-                  : (A.lanes == 1 ? 64.0 * (double)A.n_units + (A.perm ? 32.0 * (double)A.n_units : 0.0)
-                                  : 8.0 * (n + 1));
+  const double hdr = A.lanes == 1 ? 64.0 * (double)A.n_units + (A.perm ? 32.0 * (double)A.n_units : 0.0)
+                                  : 8.0 * (n + 1);
   alg = 12.0 * (double)A.nnz + vec;
   lay = 8.0 * (double)A.padded + 4.0 * (double)A.col_slots + hdr + vec;
 }
@@ -1016,8 +947,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   const char* kname = nullptr;
   if (ctx->kt.on) {
     row_bytes(A, op, r, alg, lay);
-    const char* fam = tma_ok(A, r, set) ? "sell_tma"
-                      : (A.lanes == 1 ? (A.c8 ? "sell8" : "sell") : (rg_tma_ok(A, r, set) ? "rg_tma" : "rg"));
+    const char* fam = tma_ok(A, r, set) ? "sell_tma" : (A.lanes == 1 ? "sell" : (rg_tma_ok(A, r, set) ? "rg_tma" : "rg"));
     kname = kt_name(std::string(fam) + "<" + op_name(op) + (A.lanes > 1 ? "," + std::to_string(A.lanes) : "") +
                     ">" + (A.perm ? " sorted" : "") + (set != SliceSet::All ? " subset" : ""));
   }
@@ -1081,15 +1011,6 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
     ctx->launches++;
     return;
   }
-  if (A.c8) {  // four units per warp
-    const int64_t need = (set_count(A, set) + 4 * kWarpsPerBlock - 1) / (4 * kWarpsPerBlock);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * PSC_SELL_MINB));
-    PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
-    launch_k(sell8_kernel(op), grid, kBlock, 0, s, a);
-    PSC_CUDA(cudaGetLastError());
-    ctx->launches++;
-    return;
-  }
   const int grid = row_grid(A, op, ctx->num_sms, set);
   PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
   launch_k(kernel_of(op, A.lanes), grid, kBlock, 0, s, a);
@@ -1136,7 +1057,7 @@ __global__ void __launch_bounds__(kBlock) sell_coop_sweeps(CoopArgs c) {
       const int32_t h = load_hdr(a.hdr, s, lane);
       const int64_t i = s * kSlice + lane;
       const double sum = sell_row_sum<true>(h, s, lane, a.col, a.val, x, a.ncols, a.keep_matrix != 0);
-      if (i < a.n_rows) y[i] = resid ? a.b[i] - sum : __ldca(x + i) + a.dinv[i] * (a.b[i] - sum);
+      if (i < a.n_rows) y[i] = resid ? a.b[i] - sum : x[i] + a.dinv[i] * (a.b[i] - sum);
     }
     if (!resid) cur ^= 1;
     grid.sync();
@@ -1220,20 +1141,7 @@ __global__ void __launch_bounds__(kBlock) l1_dinv_kernel(const int32_t* __restri
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double aii = 0.0, off = 0.0;
     bool found = false;
-    if (lanes == 8) {  // SELL-8 (see Sell::c8)
-      const int64_t u = i >> 3;
-      const int64_t vb = ptr[u] + (i & 7);
-      const int w = (int)((ptr[u + 1] - ptr[u]) >> 3);
-      for (int k = 0; k < w; ++k) {
-        const double v = val[vb + 8 * (int64_t)k];
-        if (col[vb + 8 * (int64_t)k] == (int32_t)i && !found) {
-          aii = v;
-          found = true;
-        } else {
-          off += fabs(v);
-        }
-      }
-    } else if (lanes == 1) {
+    if (lanes == 1) {
       const int64_t t = slot_of_row(iperm, i);
       const int64_t s = t >> 5;
       const int64_t vb = ptr[s] + (t & 31);
@@ -1266,7 +1174,7 @@ __global__ void __launch_bounds__(kBlock) l1_dinv_kernel(const int32_t* __restri
 void launch_l1_dinv(psc_ctx* ctx, const Sell& A, double* dinv, cudaStream_t s) {
   if (A.n_rows == 0) return;
   l1_dinv_kernel<<<vec_grid(ctx, A.n_rows), kBlock, 0, s>>>(A.hdr, A.ptr, A.cptr, A.col, A.val, A.n_rows, A.n_cols_local,
-                                                            A.c8 ? 8 : A.lanes, A.iperm, dinv);
+                                                            A.lanes, A.iperm, dinv);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -1629,7 +1537,6 @@ static void coarse_launch(const CoarseArgs& a, size_t smem, cudaStream_t s) {
 // larger coarsest level (e.g. 602 rows x ~600 nnz on the 1e4-jump problem:
 // 11 ms per call from L2 in one CTA) runs as full-grid sweep launches instead.
 bool coarse_one_cta_fits(const Sell& A) {
-  if (A.c8) return false;
   const int64_t n = A.n_rows;
   const int64_t nptr = A.lanes == 1 ? A.n_units + 1 : n + 1;
   const size_t vec = (size_t)std::max<int64_t>(n, 1) * 4 * sizeof(double);
@@ -1689,7 +1596,6 @@ __global__ void dense_from_sell_kernel(const int32_t* __restrict__ hdr, const in
 }
 
 void dense_from_sell(psc_ctx* ctx, const Sell& A, double* dense, cudaStream_t s) {
-  PSC_REQUIRE(!A.c8, PSC_ERR_STATE, "dense copy of a SELL-8 matrix");
   const int64_t n = A.n_rows;
   PSC_CUDA(cudaMemsetAsync(dense, 0, sizeof(double) * n * n, s));
   if (n == 0) return;
@@ -2179,103 +2085,6 @@ __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ pt
   h[15] = 0;
 }
 
-// SELL-8: 8-row slices, four per warp (c8_*).  Unit u holds rows 8u..8u+7; its width
-// w_u = max row length; value k of row 8u + r at ptr[u] + 8k + r (columns the same
-// slots: no header, cptr unused).
-__global__ void c8_width_kernel(int64_t n_rows, int64_t nu, const int64_t* __restrict__ rowptr,
-                                const int64_t* __restrict__ colg, int64_t own_begin, int64_t n_own,
-                                int64_t* __restrict__ vs, int32_t* __restrict__ flag) {
-  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= nu) return;
-  int64_t w = 0;
-  int off = 0;
-  for (int64_t i = u * 8; i < min(n_rows, u * 8 + 8); ++i) {
-    w = max(w, rowptr[i + 1] - rowptr[i]);
-    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) off |= (colg[k] < own_begin || colg[k] >= own_begin + n_own);
-  }
-  vs[u] = 8 * w;
-  flag[u] = off;
-}
-__global__ void c8_fill_kernel(int64_t n_rows, const int64_t* __restrict__ rowptr, const int64_t* __restrict__ colg,
-                               const double* __restrict__ valcsr, const int64_t* __restrict__ ptr, int64_t own_begin,
-                               int64_t n_own, const int64_t* __restrict__ halo, int64_t nh, int32_t* __restrict__ col,
-                               double* __restrict__ val, int64_t* __restrict__ slot, int* err) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_rows) return;
-  const int64_t u = i >> 3, r = i & 7;
-  const int64_t vb = ptr[u] + r, w = (ptr[u + 1] - ptr[u]) >> 3;
-  const int64_t b = rowptr[i], e = rowptr[i + 1];
-  int32_t last = 0;
-  for (int64_t k = 0; k < w; ++k) {
-    const int64_t o = vb + 8 * k;
-    if (b + k < e) {
-      last = map_col(colg[b + k], own_begin, n_own, halo, nh, err);
-      col[o] = last;
-      val[o] = valcsr[b + k];
-      if (slot) slot[b + k] = o;
-    } else {
-      col[o] = last;
-      val[o] = 0.0;
-    }
-  }
-}
-
-static void sell8_build(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg,
-                        const double* d_val, int64_t own_begin, int64_t n_own, const int64_t* d_halo, int64_t n_halo,
-                        Sell& S, cudaStream_t s) {
-  const int64_t nu = (n_rows + 7) / 8;
-  S.c8 = true;
-  S.n_units = nu;
-  int64_t* d_vs = dalloc<int64_t>(nu + 1);
-  int32_t* d_flag = dalloc<int32_t>(nu);
-  int* d_err = dalloc<int>(1);
-  PSC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-  c8_width_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(n_rows, nu, d_rowptr, d_colg, own_begin, n_own, d_vs,
-                                                                  d_flag);
-  PSC_CUDA(cudaGetLastError());
-  S.ptr = dalloc<int64_t>(nu + 1);
-  PSC_CUDA(cudaMemsetAsync(S.ptr, 0, sizeof(int64_t), s));
-  size_t tb = 0;
-  PSC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, d_vs, S.ptr + 1, nu, s));
-  void* tmp = dalloc<char>(tb);
-  PSC_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, d_vs, S.ptr + 1, nu, s));
-  PSC_CUDA(cudaMemcpyAsync(&S.padded, S.ptr + nu, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  PSC_CUDA(cudaStreamSynchronize(s));
-  dfree(tmp);
-  S.col_slots = S.padded;
-  S.col = dalloc<int32_t>(S.padded);
-  S.val = dalloc<double>(S.padded);
-  c8_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, d_rowptr, d_colg, d_val, S.ptr, own_begin,
-                                                                   n_own, d_halo, n_halo, S.col, S.val, S.slot, d_err);
-  PSC_CUDA(cudaGetLastError());
-  std::vector<int64_t> hp(nu + 1);
-  std::vector<int32_t> flag(nu);
-  int h_err = 0;
-  PSC_CUDA(cudaMemcpyAsync(hp.data(), S.ptr, sizeof(int64_t) * (nu + 1), cudaMemcpyDeviceToHost, s));
-  PSC_CUDA(cudaMemcpyAsync(flag.data(), d_flag, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
-  PSC_CUDA(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
-  PSC_CUDA(cudaStreamSynchronize(s));
-  dfree(d_vs);
-  dfree(d_flag);
-  dfree(d_err);
-  PSC_REQUIRE(h_err == 0, PSC_ERR_STATE, "column not in the owned block nor in the assembled halo");
-  std::vector<int32_t> in, bd;
-  S.nnz_ell = S.nnz;
-  for (int64_t u = 0; u < nu; ++u) {
-    S.max_width = std::max<int>(S.max_width, (int)((hp[u + 1] - hp[u]) / 8));
-    (flag[u] ? bd : in).push_back((int32_t)u);
-  }
-  S.n_interior = (int64_t)in.size();
-  S.n_boundary = (int64_t)bd.size();
-  S.interior = dalloc<int32_t>(in.size());
-  S.boundary = dalloc<int32_t>(bd.size());
-  if (!in.empty())
-    PSC_CUDA(cudaMemcpyAsync(S.interior, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s));
-  if (!bd.empty())
-    PSC_CUDA(cudaMemcpyAsync(S.boundary, bd.data(), sizeof(int32_t) * bd.size(), cudaMemcpyHostToDevice, s));
-  PSC_CUDA(cudaStreamSynchronize(s));
-}
-
 void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg, const double* d_val,
                    int64_t nnz, int64_t own_begin, int64_t n_own, const int64_t* d_halo, int64_t n_halo, Sell& S,
                    cudaStream_t s, int lanes, bool allow_dia) {
@@ -2334,39 +2143,6 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
       dfree(d_tmp);
     };
     widths(allow_dia, nullptr);
-    // SELL-8: long ELL-only matrices whose 32-row slices pad > 3% (A_1,
-    // R_0, P_1 of 256^3: 1.12 / 1.14 / 1.40 padded slots per value -> 1.06 / 1.07 / 1.27
-    // with 8-row slices); PSC_NO_SELL8=1 keeps 32-row slices
-    {
-      const bool any_dia8 = std::any_of(hdia.begin(), hdia.end(), [](int32_t d) { return d > 0; });
-      const char* pe = getenv("PSC_SELL8_PAD");
-      const double pad_min = pe ? atof(pe) : 1.03;
-      bool eligible = !any_dia8 && !env_int("PSC_NO_SELL8", 0) && !env_int("PSC_SORT", 0) &&
-                      n_rows >= env_int("PSC_SELL8_MIN_ROWS", 65536) && (double)S.padded > pad_min * (double)nnz;
-      if (eligible) {  // only slices too wide for the TMA ring (those take the plain kernel anyway)
-        std::vector<int64_t> hv(nu);
-        PSC_CUDA(cudaMemcpyAsync(hv.data(), d_vs, sizeof(int64_t) * nu, cudaMemcpyDeviceToHost, s));
-        PSC_CUDA(cudaStreamSynchronize(s));
-        int64_t mw = 0;
-        for (int64_t v : hv) mw = std::max(mw, v / 32);
-        eligible = mw > kTmaMaxW;
-      }
-      if (eligible) {
-        dfree(S.ptr);
-        dfree(S.cptr);
-        S.ptr = S.cptr = nullptr;
-        dfree(d_vs);
-        dfree(d_cs);
-        dfree(d_snnz);
-        dfree(d_flag);
-        dfree(d_diad);
-        dfree(d_diaoff);
-        dfree(d_err);
-        S.padded = S.col_slots = 0;
-        sell8_build(ctx, n_rows, d_rowptr, d_colg, d_val, own_begin, n_own, d_halo, n_halo, S, s);
-        return;
-      }
-    }
     // SELL-C-sigma, opt-in PSC_SORT=1: a matrix with no DIA slice whose
     // slices pad more than 2% is re-laid out with its rows sorted by length inside
     // 256-row windows (P_0 of 256^3: 1.36 -> 1.09 padded slots per stored value).

@@ -96,9 +96,6 @@ struct Sell {
   uint8_t* perm = nullptr;
   uint8_t* iperm = nullptr;
   int64_t* slot = nullptr;  // nnz: value slot of each CSR entry (structure-preserving updates)
-  // SELL-8 (lanes == 1): 8-row slices ("units"), four per warp, no headers; value k of
-  // row 8u + r at ptr[u] + 8k + r, columns in the same slots
-  bool c8 = false;
   // units whose columns are all owned (interior) and the others (boundary):
   // the interior ones can run while the halo exchange is in flight.
   int32_t* interior = nullptr;
@@ -106,7 +103,7 @@ struct Sell {
   int64_t n_interior = 0, n_boundary = 0;
   int max_width = 0;  // longest (padded) row
   int64_t max_chunk = 0;  // row groups: most entries in one chunk of 8 units (TMA ring capacity check)
-  int rows_per_unit() const { return lanes == 1 ? (c8 ? 8 : 32) : 32 / lanes; }
+  int rows_per_unit() const { return lanes == 1 ? 32 : 32 / lanes; }
 };
 
 // Per-reduction-site scratch: block partials, a ticket counter, and the slot of
