@@ -473,18 +473,6 @@ void ainv_sweep(psc_hier* h, LevelWS& W, const double* b, double* x, bool from_z
   launch_rows(ctx, W.Z, from_zero ? RowOp::Spmv : RowOp::PAdd, a, s);
 }
 
-// A smoothing phase of this level as one cooperative launch (launch_coop_sweeps): the
-// matrix stays in L2 across the sweeps (sliced ELL, natural row order, at most
-// PSC_COOP_MB = 96 MB of values and columns), no halo (one rank or the replicated
-// suffix), l1-Jacobi.  PSC_NO_COOP=1: stage by stage.
-bool coop_ok(const psc_hier* h, const LevelWS& W, int nsweeps) {
-  static const bool off = getenv("PSC_NO_COOP") != nullptr;
-  static const int64_t lim = (getenv("PSC_COOP_MB") ? atoll(getenv("PSC_COOP_MB")) : 96) << 20;
-  const Sell& S = W.A->S;
-  return !off && nsweeps >= 1 && !W.ainv && S.lanes == 1 && !S.perm && W.nh == 0 && (h->ctx->nranks == 1 || !W.d) &&
-         S.padded * 8 + S.col_slots * 4 <= lim && S.n_units > 0;
-}
-
 // PSC_NO_FUSED_SCALE=1: every first sweep from zero is a stand-alone x = M^-1 b launch
 bool fuse_first_sweep() { return getenv("PSC_NO_FUSED_SCALE") == nullptr; }
 
@@ -591,11 +579,8 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   // (I - M^-1 A)^pre, then the coarse-grid correction (I - P B_{l+1} P^T A):
   // r = b - A x ; b_c = R r ; x += P B_{l+1} b_c
   const int pre = level_sweeps(h, h->opt.pre_sweeps, glev);
-  int cur;
-  if (!time_here && coop_ok(h, W, pre)) {  // pre-smoothing and the residual in one launch
-    cur = launch_coop_sweeps(ctx, W.A->S, b, W.dinv, W.x[0], W.x[1], 0, !first_done, pre - 1, W.r, s);
-  } else {
-    cur = pre_smooth(h, W, b, pre, s, time_here, first_done);
+  int cur = pre_smooth(h, W, b, pre, s, time_here, first_done);
+  {
     RowArgs a;
     a.vec_padded = true;  // library buffers, padded (dvec)
     a.x = W.x[cur];
@@ -631,8 +616,6 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
   const int post = level_sweeps(h, h->opt.post_sweeps, glev);
   const bool level0 = dist && l == 0;
-  if (!level0 && coop_ok(h, W, post))  // post-smoothing in one launch
-    return W.x[launch_coop_sweeps(ctx, W.A->S, b, W.dinv, W.x[0], W.x[1], cur, false, post, nullptr, s)];
   if (W.ainv) {
     for (int k = 0; k < post; ++k) ainv_sweep(h, W, b, W.x[cur], false, s);
     if (level0)

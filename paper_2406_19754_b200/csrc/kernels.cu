@@ -7,7 +7,6 @@
 // cached gathers of x (__ldg, kept in the 126 MB L2), grid-stride loops sized
 // to the SM count, and deterministic fixed-order reductions.
 #include <algorithm>
-#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <deque>
 #include <numeric>
@@ -1016,87 +1015,6 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   launch_k(kernel_of(op, A.lanes), grid, kBlock, 0, s, a);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
-}
-
-// ----------------------------------------- several sweeps of an L2-resident level
-// One cooperative launch runs a whole smoothing phase of a small level (its matrix
-// stays in L2 across the sweeps): [x0 = M^-1 b,] `nsweeps` Jacobi sweeps alternating
-// x[0] / x[1], [r = b - A x]; grid-wide barriers between the stages replace the kernel
-// boundaries.  Each row's arithmetic is the stand-alone kernels' (same row sums, same
-// epilogues), so the result is bit-identical to launching the stages one by one.
-struct CoopArgs {
-  RowKArgs a;          // matrix, b, dinv
-  double* x[2];
-  double* r;           // residual output, nullptr: none
-  int nsweeps;         // sweeps after the start
-  int from_zero;       // 1: start with x[0] = dinv .* b
-  int start;           // buffer holding x when !from_zero
-};
-
-__global__ void __launch_bounds__(kBlock) sell_coop_sweeps(CoopArgs c) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  const RowKArgs& a = c.a;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nw = (int64_t)gridDim.x * kWarpsPerBlock;
-  const int64_t w0 = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
-  int cur = c.start;
-  if (c.from_zero) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_rows;
-         i += (int64_t)gridDim.x * blockDim.x)
-      c.x[0][i] = a.dinv[i] * a.b[i];
-    cur = 0;
-    grid.sync();
-  }
-  for (int k = 0; k <= c.nsweeps; ++k) {
-    const bool resid = (k == c.nsweeps);
-    if (resid && !c.r) break;
-    const double* x = c.x[cur];
-    double* y = resid ? c.r : c.x[cur ^ 1];
-    for (int64_t s = w0; s < a.nlist; s += nw) {
-      const int32_t h = load_hdr(a.hdr, s, lane);
-      const int64_t i = s * kSlice + lane;
-      const double sum = sell_row_sum<true>(h, s, lane, a.col, a.val, x, a.ncols, a.keep_matrix != 0);
-      if (i < a.n_rows) y[i] = resid ? a.b[i] - sum : x[i] + a.dinv[i] * (a.b[i] - sum);
-    }
-    if (!resid) cur ^= 1;
-    grid.sync();
-  }
-}
-
-int launch_coop_sweeps(psc_ctx* ctx, const Sell& A, const double* b, const double* dinv, double* x0, double* x1,
-                       int start, bool from_zero, int nsweeps, double* r, cudaStream_t s) {
-  static int occ = -1;
-  if (occ < 0) {
-    PSC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sell_coop_sweeps, kBlock, 0));
-    occ = std::max(occ, 1);
-  }
-  const int64_t need = (A.n_units + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * occ));
-  CoopArgs c{};
-  c.a.keep_matrix = 1;
-  c.a.ptr = A.ptr;
-  c.a.cptr = A.cptr;
-  c.a.hdr = A.hdr;
-  c.a.ncols = A.n_cols_local;
-  c.a.col = A.col;
-  c.a.val = A.val;
-  c.a.n_rows = A.n_rows;
-  c.a.nlist = A.n_units;
-  c.a.b = b;
-  c.a.dinv = dinv;
-  c.x[0] = x0;
-  c.x[1] = x1;
-  c.r = r;
-  c.nsweeps = nsweeps;
-  c.from_zero = from_zero ? 1 : 0;
-  c.start = start;
-  KtScope kts(ctx, s, "sell_coop<Sweeps>", 0.0, 0.0);
-  void* args[] = {&c};
-  PSC_CUDA(cudaLaunchCooperativeKernel((void*)sell_coop_sweeps, grid, kBlock, args, 0, s));
-  ctx->launches++;
-  // the buffer holding the smoothed x
-  return from_zero ? (nsweeps & 1) : (start ^ (nsweeps & 1));
 }
 
 // ------------------------------------------------------------ vector kernels

@@ -47,13 +47,6 @@ int row_grid(const Sell& A, RowOp op, int num_sms, SliceSet set = SliceSet::All)
 void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& a, cudaStream_t s,
                  SliceSet set = SliceSet::All);
 
-// A whole smoothing phase of an L2-resident sliced-ELL level (no halo) in one
-// cooperative launch: [x0 = dinv .* b (from_zero),] nsweeps Jacobi sweeps alternating
-// x0 / x1 from buffer `start`, [r = b - A x]; bit-identical to the stage-by-stage
-// kernels.  Returns the index of the buffer holding x.
-int launch_coop_sweeps(psc_ctx* ctx, const Sell& A, const double* b, const double* dinv, double* x0, double* x1,
-                       int start, bool from_zero, int nsweeps, double* r, cudaStream_t s);
-
 // x = dinv .* b  (first sweep from x = 0: x + M^-1 (b - A 0) = M^-1 b)
 void launch_scale(psc_ctx* ctx, int64_t n, const double* dinv, const double* b, double* x, cudaStream_t s);
 // m_i = a_ii + sum_{j != i} |a_ij| over the stored row;  dinv_i = 1 / m_i

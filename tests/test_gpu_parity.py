@@ -256,8 +256,6 @@ VARIANTS = [
     {"PSC_SORT": "1", "PSC_NO_TMA": "1", "PSC_NO_DENSE_COARSE": "1", "PSC_NO_DIA": "1"},
     {"PSC_RG_SMALL_MB": "200"},
     {"PSC_DIA_MAX": "64"},
-    {"PSC_NO_COOP": "1"},
-    {"PSC_COOP_MB": "100000", "PSC_DENSE_SUFFIX_ROWS": "0"},
     {"PSC_NO_FUSED_SCALE": "1", "PSC_NO_DIA": "1", "PSC_NO_TMA": "1"},
 ]
 
