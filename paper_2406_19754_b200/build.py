@@ -87,5 +87,15 @@ def _build(force, verbose, LIB, defines):
     return LIB
 
 
+def build_checked(force: bool = False) -> str:
+    """libpsc_checked.so: the same sources with device-side bounds checks (-DPSC_CHECKS),
+    for test runs with PSC_LIB pointing at it (compute-sanitizer is not available on the
+    GPU pool)."""
+    return build(force=force, out=os.path.join(HERE, "libpsc_checked.so"), defines=["-DPSC_CHECKS"])
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

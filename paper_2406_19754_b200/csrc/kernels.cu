@@ -203,6 +203,7 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
     for (int j = 0; j < 8; ++j) {
       ci[j] = ldm(c + 32 * j, keep);
       vi[j] = ldm(v + 32 * j, keep);
+      PSC_DASSERT((uint64_t)ci[j] < (uint64_t)ncols);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) sum = fma(vi[j], ldx<CG>(x + ci[j]), sum);
@@ -627,6 +628,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
         const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) +
                               ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0);
+        PSC_DASSERT(vbytes <= (uint32_t)kTmaValBytes && cbytes <= (uint32_t)kTmaColBytes &&
+                    rbytes <= (uint32_t)kTmaVecBytes && hb <= (uint32_t)kTmaHdrBytes);
         mbar_expect_tx(&full[st], hb + vbytes + cbytes + nvec * rbytes);
         bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol_keep);
         if (vbytes) bulk_g2s(base + kTmaHdrBytes, a.val + vb0, vbytes, &full[st], pol_mat);
@@ -683,6 +686,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
           const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
                              (uint32_t)__shfl_sync(0xffffffffu, h, 2);
           const int32_t* cc = cs + (cb - cbase) + lane;
+#pragma unroll
+          for (int j = 0; j < kTmaMaxW; ++j) PSC_DASSERT(j >= w || (uint32_t)cc[32 * j] < nc);
 #pragma unroll
           for (int j = 0; j < kTmaMaxW; ++j) xv[j] = (j < w) ? gx((uint32_t)cc[32 * j]) : 0.0;
         }
@@ -785,6 +790,7 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
         const uint32_t cbytes = (uint32_t)(e1 - e0) * 4;
         const uint32_t rbytes = (uint32_t)(((r1 - r0) * 8 + 15) & ~15);
         const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D ? 1 : 0) + (EV::X ? 1 : 0) + (readY ? 1 : 0);
+        PSC_DASSERT(e1 - e0 <= kRgCap && pbytes <= (uint32_t)kRgPtrBytes && r1 - r0 <= kRgMaxRows);
         mbar_expect_tx(&full[st], pbytes + vbytes + cbytes + nvec * rbytes);
         bulk_g2s(base + kRgValBytes + kRgColBytes, a.ptr + r0, pbytes, &full[st], pol_keep);
         if (vbytes) {

@@ -41,6 +41,18 @@ struct Error : std::runtime_error {
                                            ":" + std::to_string(__LINE__));                               \
   } while (0)
 
+// Device-side bounds checks of the checked build (build.py: libpsc_checked.so with
+// -DPSC_CHECKS; compute-sanitizer is not available on the GPU pool): a failed check
+// traps, the launch fails and the host call returns PSC_ERR_CUDA.
+#ifdef PSC_CHECKS
+#define PSC_DASSERT(c)     \
+  do {                     \
+    if (!(c)) __trap();    \
+  } while (0)
+#else
+#define PSC_DASSERT(c) ((void)0)
+#endif
+
 #define PSC_REQUIRE(cond, code, msg)                 \
   do {                                               \
     if (!(cond)) throw ::psc::Error((code), (msg)); \
