@@ -98,6 +98,10 @@ struct psc_hier_s {
   // weight of the (., z) reduction in the last level-0 post-sweep while an FCG
   // iteration is recorded (q = A p_old); nullptr: r (PCG)
   const double* rz_weight = nullptr;
+  // fused push: the vector whose halo the last row kernel pushed, and the launch count
+  // right after it (the push is consumed only by the immediately next launch)
+  const double* pushed = nullptr;
+  int64_t pushed_at = -1;
   // graph of one Krylov iteration, per method (PSC_KRYLOV_PCG, PSC_KRYLOV_FCG)
   cudaGraphExec_t iter_exec[2] = {nullptr, nullptr};
   cudaGraphExec_t prof_exec[2] = {nullptr, nullptr};  // the same iteration with per-kernel event pairs
@@ -180,8 +184,24 @@ void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
 // Opt-in (PSC_OVERLAP=1): measured slower on 2 B200 (6122 vs 6555 Mdof*iters/s at
 // 256^3/GPU): the split adds a launch and a join per kernel (92 -> 120 launches per
 // iteration), which costs more than the ~10 us exchange it hides.
-void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cudaStream_t s) {
+// Fused push (PSC_PUSH=1): a producer row kernel pushes its output's
+// boundary rows into the neighbours' halo slots and signals; the next launch, when it
+// is the row kernel reading that vector's halo, waits instead of a stand-alone
+// exchange.  push_d: the output's row space when the caller's next launch reads the
+// output's halo (nullptr: no push).
+bool fused_push_on() {
+  static const bool on = getenv("PSC_PUSH") != nullptr && getenv("PSC_OVERLAP") == nullptr &&
+                         getenv("PSC_DEBUG_SKIP_HALO") == nullptr && getenv("PSC_DEBUG_DOUBLE_HALO") == nullptr &&
+                         getenv("PSC_DEBUG_POISON_HALO") == nullptr;
+  return on;
+}
+
+void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cudaStream_t s,
+              psc_desc* push_d = nullptr) {
   psc_ctx* ctx = h->ctx;
+  // a pushed halo is only valid for the immediately following launch
+  const bool pushed_here = h->pushed && h->pushed == a.x && h->pushed_at == ctx->launches + ctx->collectives;
+  h->pushed = nullptr;
   static const bool no_overlap = getenv("PSC_OVERLAP") == nullptr || getenv("PSC_DEBUG_SKIP_HALO") != nullptr ||
                                  getenv("PSC_DEBUG_SKIP_HALO_FROM") != nullptr ||
                                  getenv("PSC_DEBUG_DOUBLE_HALO") != nullptr;
@@ -196,8 +216,14 @@ void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cud
     launch_rows(ctx, S, op, a, s, SliceSet::Boundary);
     return;
   }
-  prep(h, d, a, s);
+  if (!(pushed_here && d && rows_can_push(S, a) && p2p_wait_spec(ctx, h->p2p, a.x, a.wait))) prep(h, d, a, s);
+  const bool push = fused_push_on() && push_d && ctx->nranks > 1 && rows_can_push(S, a) &&
+                    p2p_push_spec(ctx, h->p2p, push_d, a.y, a.push);
   launch_rows(ctx, S, op, a, s);
+  if (push) {
+    h->pushed = a.y;
+    h->pushed_at = ctx->launches + ctx->collectives;
+  }
 }
 
 // ------------------------------------------------------------ coarsest level
@@ -514,7 +540,8 @@ int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream
     a.y = W.x[cur ^ 1];
     const bool t = timing && h->dom_used + 2 <= (int)h->ev_dom.size();
     if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
-    run_rows(h, W.d, W.A->S, RowOp::Sweep, a, s);
+    // output read next by the following sweep or by the residual (both row kernels)
+    run_rows(h, W.d, W.A->S, RowOp::Sweep, a, s, W.d);
     if (t) {
       PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
       h->dom_used += 2;
@@ -586,7 +613,9 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     a.x = W.x[cur];
     a.b = b;
     a.y = W.r;
-    run_rows(h, W.d, W.A->S, RowOp::Resid, a, s);
+    RowArgs ra;  // the restriction, which reads r's halo next
+    ra.vec_padded = true;
+    run_rows(h, W.d, W.A->S, RowOp::Resid, a, s, rows_can_push(W.R->S, ra) ? W.d : nullptr);
   }
   // fused: the next level's first sweep from zero, x_{l+1} = M^{-1} b_{l+1}
   const bool next_dense = h->dsuf && &LV == h->dsuf_lv && l + 1 == h->dsuf_l;
@@ -611,7 +640,7 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     a.x = xc;
     a.y = W.x[cur];
     if (next_replicated) launch_rows(ctx, W.P->S, RowOp::PAdd, a, s);  // the replicated cycle filled xc's halo
-    else run_rows(h, C.d, W.P->S, RowOp::PAdd, a, s);
+    else run_rows(h, C.d, W.P->S, RowOp::PAdd, a, s, W.d);  // x's halo read next by the first post-sweep
   }
   // (I - M^-T A)^post ; M diagonal so M^-T = M^-1
   const int post = level_sweeps(h, h->opt.post_sweeps, glev);
@@ -637,7 +666,12 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
     }
     const bool t = time_here && h->dom_used + 2 <= (int)h->ev_dom.size();
     if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
-    run_rows(h, W.d, W.A->S, last0 ? RowOp::SweepDot : RowOp::Sweep, a, s);
+    // the output's halo is read next by the following post-sweep, or (last sweep,
+    // level >= 1) by the prolongation of the level above
+    RowArgs pa;
+    pa.vec_padded = true;
+    const bool consumer_waits = (k + 1 < post) || (l > 0 && rows_can_push(LV[l - 1].P->S, pa));
+    run_rows(h, W.d, W.A->S, last0 ? RowOp::SweepDot : RowOp::Sweep, a, s, (!last0 && consumer_waits) ? W.d : nullptr);
     if (t) {
       PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
       h->dom_used += 2;

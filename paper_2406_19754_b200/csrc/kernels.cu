@@ -301,6 +301,8 @@ struct RowKArgs {
   unsigned int* ticket;
   double* red_out;
   int red_stride;
+  PushSpec push;
+  WaitSpec wait;
 };
 
 template <RowOp OP>
@@ -308,6 +310,58 @@ struct NRed {
   static constexpr int value =
       (OP == RowOp::SpmvDot || OP == RowOp::SweepDot) ? 1 : (OP == RowOp::ResidDot2 ? 2 : 0);
 };
+
+// ------------------------------------------------------------ fused push
+static __device__ __forceinline__ void fp_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+static __device__ __forceinline__ uint64_t fp_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// consumer: before any thread of the CTA reads x's halo, thread 0 waits until every
+// neighbour's flag reached this rank's generation (the producer on each side signalled)
+__device__ __forceinline__ void wait_halo(const WaitSpec& w) {
+  if (threadIdx.x == 0) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    for (int q = 0; q < w.R; ++q)
+      if (w.nbr[q]) {
+        const uint64_t target = __ldcg(w.gen + q);
+        while (fp_acquire_sys(w.myflag + q) < target) {
+          uint64_t t;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+          if (t - t0 > w.timeout_ns) __trap();  // a peer that never signals: launch error, no hang
+        }
+      }
+  }
+  __syncthreads();
+}
+// producer epilogue: row i's new value into every neighbour slot it feeds
+__device__ __forceinline__ void push_row(const PushSpec& p, int64_t i, double v) {
+  for (int t = __ldg(p.iptr + i); t < __ldg(p.iptr + i + 1); ++t) p.dst[__ldg(p.iq + t)][__ldg(p.ipos + t)] = v;
+}
+// producer end: the last CTA signals every neighbour once all CTAs' stores are visible
+__device__ __forceinline__ void push_signal(const PushSpec& p) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < p.R; ++q)
+      if (p.nbr[q]) {
+        const uint64_t g = p.gen[q] + 1;
+        p.gen[q] = g;
+        fp_release_sys(p.pflag[q], g);
+      }
+    *p.ticket = 0u;
+  }
+}
 
 // Fused epilogue of row i with row sum `sum`, split in two: the row's vector
 // operands are loaded by epi_load BEFORE the row sum (so they travel with the
@@ -341,6 +395,7 @@ __device__ __forceinline__ void epi_store(const RowKArgs& a, int64_t i, double s
   if constexpr (OP == RowOp::Spmv) {
     const double v = (a.beta == 0.0) ? a.alpha * sum : a.alpha * sum + a.beta * e.x;
     a.y[i] = v;
+    if (a.push.on) push_row(a.push, i, v);
     if (a.y2) a.y2[i] = a.dinv2[i] * v;
   } else if constexpr (OP == RowOp::SpmvDot) {
     a.y[i] = sum;
@@ -348,9 +403,11 @@ __device__ __forceinline__ void epi_store(const RowKArgs& a, int64_t i, double s
   } else if constexpr (OP == RowOp::Sweep || OP == RowOp::SweepDot || OP == RowOp::Sweep0) {
     const double xn = e.x + e.d * (e.b - sum);
     a.y[i] = xn;
+    if (a.push.on) push_row(a.push, i, xn);
     if constexpr (OP == RowOp::SweepDot) acc[0] += (a.w ? __ldg(a.w + i) : e.b) * xn;
   } else if constexpr (OP == RowOp::Resid) {
     a.y[i] = e.b - sum;
+    if (a.push.on) push_row(a.push, i, e.b - sum);
   } else if constexpr (OP == RowOp::ResidDot2) {
     const double r = e.b - sum;
     a.y[i] = r;
@@ -358,6 +415,7 @@ __device__ __forceinline__ void epi_store(const RowKArgs& a, int64_t i, double s
     acc[1] += e.b * e.b;
   } else if constexpr (OP == RowOp::PAdd) {
     a.y[i] = e.x + sum;
+    if (a.push.on) push_row(a.push, i, e.x + sum);
   }
 }
 
@@ -371,6 +429,7 @@ __device__ __forceinline__ void epilogue(const RowKArgs& a, int64_t i, double su
 // less per slice)
 template <RowOp OP>
 __device__ __forceinline__ void sell_body(const RowKArgs& a) {
+  if (a.wait.on) wait_halo(a.wait);
   constexpr int NR = NRed<OP>::value;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -401,6 +460,7 @@ __device__ __forceinline__ void sell_body(const RowKArgs& a) {
     s = sn;
     h = hn;
   }
+  if (a.push.on) push_signal(a.push);
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
@@ -595,6 +655,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (a.wait.on) wait_halo(a.wait);
   double acc[NR > 0 ? NR : 1] = {};
   if (warp == kTmaSlices) {
     // ---------------- producer (one lane)
@@ -713,6 +774,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
+  if (a.push.on) push_signal(a.push);
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
@@ -941,6 +1003,10 @@ static void row_bytes(const Sell& A, RowOp op, const RowArgs& r, double& alg, do
   lay = 8.0 * (double)A.padded + 4.0 * (double)A.col_slots + hdr + vec;
 }
 
+bool rows_can_push(const Sell& A, const RowArgs& r) {
+  return A.lanes == 1 && !A.perm && (tma_ok(A, r, SliceSet::All) || A.hdr != nullptr);
+}
+
 void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaStream_t s, SliceSet set) {
   if (op == RowOp::Sweep0 && !tma_ok(A, r, set)) {
     // two launches: x = dinv .* b, then one sweep from x
@@ -983,6 +1049,10 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   a.ticket = r.red ? r.red->ticket : nullptr;
   a.red_out = r.red_out;
   a.red_stride = r.red_stride;
+  a.push = r.push;
+  a.wait = r.wait;
+  PSC_REQUIRE(!(r.push.on || r.wait.on) || (set == SliceSet::All && rows_can_push(A, r)), PSC_ERR_STATE,
+              "fused push / wait on a row kernel without them");
   const bool needs_red = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
   if (tma_ok(A, r, set)) {
     const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;

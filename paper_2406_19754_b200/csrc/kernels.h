@@ -23,6 +23,32 @@ enum class RowOp {
               // (x = x1) only by the two-launch fallback of non-TMA layouts
 };
 
+// Halo exchange folded into the producer ("fused push"): a row kernel
+// whose output y is a halo-bearing vector stores each boundary row's value straight
+// into the neighbours' halo slots (NVLink peer stores) from its epilogue, and its last
+// CTA release-stores one generation flag per neighbour; the kernel that next reads
+// y's halo waits for those flags before its first gather (WaitSpec).
+struct PushSpec {
+  int on = 0;
+  int R = 0;
+  const int32_t* iptr = nullptr;  // [n_own+1]: sends of owned row i at [iptr[i], iptr[i+1])
+  const int32_t* iq = nullptr;    // peer of each send
+  const int32_t* ipos = nullptr;  // slot in that peer's block of y's halo
+  double* const* dst = nullptr;   // [R] peer p's halo slots for this rank's block of y
+  const int32_t* nbr = nullptr;   // [R] neighbours at y's level
+  uint64_t* const* pflag = nullptr;
+  uint64_t* gen = nullptr;        // [R] signals sent to each peer (generation)
+  unsigned int* ticket = nullptr;
+};
+struct WaitSpec {
+  int on = 0;
+  int R = 0;
+  const int32_t* nbr = nullptr;   // [R] neighbours at x's level
+  const uint64_t* myflag = nullptr;
+  const uint64_t* gen = nullptr;  // wait until every neighbour's flag reaches my generation
+  uint64_t timeout_ns = 0;
+};
+
 struct RowArgs {
   double alpha = 1.0, beta = 0.0;
   const double* x = nullptr;
@@ -38,7 +64,11 @@ struct RowArgs {
   // all row vectors (b, dinv, x, y) are library buffers padded past n (TMA bulk
   // copies of the last chunk may read up to 8 bytes beyond the last row)
   bool vec_padded = false;
+  PushSpec push;  // y's halo pushed by this kernel (push.on)
+  WaitSpec wait;  // x's halo was pushed by the previous kernel: wait for it (wait.on)
 };
+// row kernels that implement PushSpec / WaitSpec (sliced ELL: TMA ring or plain)
+bool rows_can_push(const Sell& A, const RowArgs& r);
 
 // Which slices: all, interior only (no halo column), boundary only.
 enum class SliceSet { All, Interior, Boundary };

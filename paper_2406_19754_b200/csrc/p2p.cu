@@ -71,10 +71,13 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
   __threadfence_system();
   for (int q = 0; q < a.R; ++q)
     if (a.nbr[q]) st_release_sys(a.pflag[q], ++a.gen[q]);
+  // wait until every neighbour has signalled as often as this rank has (the signal
+  // counts of a pair advance in the same collective order on both sides; fused
+  // pushes in row kernels signal without a standalone exchange, PushSpec)
   const uint64_t t0 = globaltimer();
   for (int q = 0; q < a.R; ++q)
     if (a.nbr[q]) {
-      const uint64_t target = ++a.gen[a.R + q];
+      const uint64_t target = a.gen[q];
       while (ld_acquire_sys(a.myflag + q) < target) {
         // a peer that never signals (crashed, or left the collective order) must not
         // hang this GPU: after timeout_ns the kernel traps and the host call returns
@@ -86,11 +89,16 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
   *a.ticket = 0u;
 }
 
-static void push(psc_ctx* ctx, P2P& P, const double* x, const int32_t* idx, const int64_t* soff, int64_t n,
-                 int64_t max_per_peer, double* const* dst, const int32_t* nbr, cudaStream_t s) {
-  // PSC_SPIN_TIMEOUT_S: seconds a rank waits for a neighbour's flag (default 30)
+// PSC_SPIN_TIMEOUT_S: seconds a rank waits for a neighbour's flag (default 30)
+static uint64_t spin_timeout_ns() {
   static const uint64_t tmo =
       (uint64_t)(1e9 * (getenv("PSC_SPIN_TIMEOUT_S") ? atof(getenv("PSC_SPIN_TIMEOUT_S")) : 30.0));
+  return tmo;
+}
+
+static void push(psc_ctx* ctx, P2P& P, const double* x, const int32_t* idx, const int64_t* soff, int64_t n,
+                 int64_t max_per_peer, double* const* dst, const int32_t* nbr, cudaStream_t s) {
+  const uint64_t tmo = spin_timeout_ns();
   PushArgs a{x, idx, soff, n, dst, nbr, P.d_pflag, P.flags, P.d_gen, P.d_ticket, ctx->nranks, tmo};
   KtScope kts(ctx, s, idx ? "p2p_halo" : "p2p_allgather", 0.0, 0.0);
   const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((max_per_peer + 255) / 256, 64));
@@ -107,6 +115,42 @@ bool p2p_halo(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, cudaStream_t s
   const P2PLevel& L = P.levels[it->second.level];
   if (!L.any) return true;  // no neighbour at this level: nothing to exchange
   push(ctx, P, x, d->d_send_idx, L.d_soff, 0, L.max_send, it->second.d_dst, L.d_nbr, s);
+  return true;
+}
+
+bool p2p_push_spec(psc_ctx* ctx, P2P& P, psc_desc* d, const double* y, PushSpec& ps) {
+  ps = PushSpec();
+  if (!P.on) return false;
+  auto it = P.bufs.find(y);
+  if (it == P.bufs.end()) return false;
+  const P2PLevel& L = P.levels[it->second.level];
+  if (!L.any || !L.d_iptr || d->n_own + d->n_halo() <= 0) return false;
+  ps.on = 1;
+  ps.R = ctx->nranks;
+  ps.iptr = L.d_iptr;
+  ps.iq = L.d_iq;
+  ps.ipos = L.d_ipos;
+  ps.dst = it->second.d_dst;
+  ps.nbr = L.d_nbr;
+  ps.pflag = P.d_pflag;
+  ps.gen = P.d_gen;
+  ps.ticket = P.d_ticket_push;
+  ctx->collectives++;
+  return true;
+}
+
+bool p2p_wait_spec(psc_ctx* ctx, P2P& P, const double* x, WaitSpec& ws) {
+  ws = WaitSpec();
+  if (!P.on) return false;
+  auto it = P.bufs.find(x);
+  if (it == P.bufs.end()) return false;
+  const P2PLevel& L = P.levels[it->second.level];
+  ws.on = L.any ? 1 : 0;
+  ws.R = ctx->nranks;
+  ws.nbr = L.d_nbr;
+  ws.myflag = P.flags;
+  ws.gen = P.d_gen;
+  ws.timeout_ns = spin_timeout_ns();
   return true;
 }
 
@@ -210,6 +254,27 @@ void p2p_setup(psc_ctx* ctx, P2P& P, const std::vector<P2PBufSpec>& halo_bufs,
     Lv.d_soff = dalloc<int64_t>(R + 1);
     PSC_CUDA(cudaMemcpy(Lv.d_nbr, nbr.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice));
     PSC_CUDA(cudaMemcpy(Lv.d_soff, d->soff.data(), sizeof(int64_t) * (R + 1), cudaMemcpyHostToDevice));
+    // fused push: owned row -> (peer, position in my block of that peer's halo)
+    if (d->n_send > 0) {
+      std::vector<int32_t> sidx(d->n_send);
+      PSC_CUDA(cudaMemcpy(sidx.data(), d->d_send_idx, sizeof(int32_t) * d->n_send, cudaMemcpyDeviceToHost));
+      std::vector<int32_t> iptr(d->n_own + 1, 0), iq(d->n_send), ipos(d->n_send);
+      for (int64_t k = 0; k < d->n_send; ++k) iptr[sidx[k] + 1]++;
+      for (int64_t i = 0; i < d->n_own; ++i) iptr[i + 1] += iptr[i];
+      std::vector<int32_t> fill(iptr.begin(), iptr.end() - 1);
+      for (int p = 0; p < R; ++p)
+        for (int64_t k = d->soff[p]; k < d->soff[p + 1]; ++k) {
+          const int32_t o = fill[sidx[k]]++;
+          iq[o] = p;
+          ipos[o] = (int32_t)(k - d->soff[p]);
+        }
+      Lv.d_iptr = dalloc<int32_t>(d->n_own + 1);
+      Lv.d_iq = dalloc<int32_t>(d->n_send);
+      Lv.d_ipos = dalloc<int32_t>(d->n_send);
+      PSC_CUDA(cudaMemcpy(Lv.d_iptr, iptr.data(), sizeof(int32_t) * (d->n_own + 1), cudaMemcpyHostToDevice));
+      PSC_CUDA(cudaMemcpy(Lv.d_iq, iq.data(), sizeof(int32_t) * d->n_send, cudaMemcpyHostToDevice));
+      PSC_CUDA(cudaMemcpy(Lv.d_ipos, ipos.data(), sizeof(int32_t) * d->n_send, cudaMemcpyHostToDevice));
+    }
   }
   for (size_t b = 0; b < halo_bufs.size(); ++b) {
     const int l = halo_bufs[b].level;
@@ -254,6 +319,8 @@ void p2p_setup(psc_ctx* ctx, P2P& P, const std::vector<P2PBufSpec>& halo_bufs,
   PSC_CUDA(cudaMemset(P.d_gen, 0, sizeof(uint64_t) * 2 * R));
   P.d_ticket = dalloc<unsigned int>(1);
   PSC_CUDA(cudaMemset(P.d_ticket, 0, sizeof(unsigned int)));
+  P.d_ticket_push = dalloc<unsigned int>(1);
+  PSC_CUDA(cudaMemset(P.d_ticket_push, 0, sizeof(unsigned int)));
   PSC_CUDA(cudaDeviceSynchronize());
   allreduce_min(ctx, 1);  // nobody signals before everybody is set up
   P.on = true;
@@ -267,11 +334,15 @@ void p2p_free(psc_ctx* ctx, P2P& P) {
   for (auto& Lv : P.levels) {
     dfree(Lv.d_nbr);
     dfree(Lv.d_soff);
+    dfree(Lv.d_iptr);
+    dfree(Lv.d_iq);
+    dfree(Lv.d_ipos);
   }
   dfree(P.d_all);
   dfree(P.d_pflag);
   dfree(P.d_gen);
   dfree(P.d_ticket);
+  dfree(P.d_ticket_push);
   P = P2P();
 }
 

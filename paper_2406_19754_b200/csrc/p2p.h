@@ -25,6 +25,10 @@ struct P2PLevel {
   int64_t max_send = 0;
   int32_t* d_nbr = nullptr;
   int64_t* d_soff = nullptr;
+  // fused push: for each owned row, its sends (peer, slot in the peer's block)
+  int32_t* d_iptr = nullptr;
+  int32_t* d_iq = nullptr;
+  int32_t* d_ipos = nullptr;
 };
 struct P2P {
   bool on = false;
@@ -34,6 +38,7 @@ struct P2P {
   uint64_t** d_pflag = nullptr;
   uint64_t* d_gen = nullptr;
   unsigned int* d_ticket = nullptr;
+  unsigned int* d_ticket_push = nullptr;  // fused pushes (producer row kernels)
   int32_t* d_all = nullptr;
   std::vector<P2PLevel> levels;
   std::map<const double*, P2PBufDev> bufs;
@@ -49,6 +54,11 @@ void p2p_free(psc_ctx* ctx, P2P& P);
 int allreduce_min(psc_ctx* ctx, int v);
 // false: not handled (caller falls back to NCCL)
 bool p2p_halo(psc_ctx* ctx, P2P& P, psc_desc* d, const double* x, cudaStream_t s);
+// Fused push of a row kernel's output y (a registered halo-bearing vector of the row
+// space d) / wait in the kernel that next reads x's halo.  false: not possible (the
+// caller exchanges with p2p_halo).  See PushSpec / WaitSpec (kernels.h).
+bool p2p_push_spec(psc_ctx* ctx, P2P& P, psc_desc* d, const double* y, PushSpec& ps);
+bool p2p_wait_spec(psc_ctx* ctx, P2P& P, const double* x, WaitSpec& ws);
 bool p2p_allgather(psc_ctx* ctx, P2P& P, const double* src, int64_t n, const double* dst_base_local,
                    cudaStream_t s);
 

@@ -43,7 +43,8 @@ def test_four_gpu_parity():
     _run(4, (32, 32, 32), (1, 2, 2))
 
 
-@pytest.mark.parametrize("env", [{"PSC_DEBUG_POISON_HALO": "1"}, {"PSC_DEBUG_POISON_HALO": "1", "PSC_NO_P2P": "1"},
+@pytest.mark.parametrize("env", [{"PSC_PUSH": "1"}, {"PSC_PUSH": "1", "PSC_REPL_ROWS": "0"},
+                                 {"PSC_DEBUG_POISON_HALO": "1"}, {"PSC_DEBUG_POISON_HALO": "1", "PSC_NO_P2P": "1"},
                                  {"PSC_REPL_ROWS": "0"}, {"PSC_REPL_ROWS": "100000000"},
                                  {"PSC_NO_P2P": "1"}, {"PSC_OVERLAP": "1"}, {"PSC_OVERLAP": "1", "PSC_NO_P2P": "1"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
