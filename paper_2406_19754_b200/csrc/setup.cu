@@ -22,6 +22,7 @@
 #include <chrono>
 #include <memory>
 #include <climits>
+#include <cstdio>
 #include <cstring>
 
 #include "kernels.h"
@@ -756,6 +757,10 @@ int psc_amg_build(psc_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t
       AmgLevel N;
       N.A = galerkin(ctx, L.R, L.A, L.P);
       a->t_galerkin += secs_since(t);
+      if (getenv("PSC_AMG_VERBOSE"))
+        fprintf(stderr, "[psc_amg] level %d: n %lld nnz %lld -> %lld rows, %lld nnz; rounds %d, galerkin %.3f s\n",
+                (int)a->lv.size() - 1, (long long)L.A.n, (long long)L.A.nnz, (long long)N.A.n, (long long)N.A.nnz,
+                L.mis_rounds, secs_since(t));
       a->lv.push_back(N);
     }
     a->t_total = secs_since(t0);
