@@ -184,10 +184,11 @@ void prep(psc_hier* h, psc_desc* d, RowArgs& a, cudaStream_t s) {
 // Opt-in (PSC_OVERLAP=1): measured slower on 2 B200 (6122 vs 6555 Mdof*iters/s at
 // 256^3/GPU): the split adds a launch and a join per kernel (92 -> 120 launches per
 // iteration), which costs more than the ~10 us exchange it hides.
-// Fused push (PSC_PUSH=1): a producer row kernel pushes its output's
-// boundary rows into the neighbours' halo slots and signals; the next launch, when it
-// is the row kernel reading that vector's halo, waits instead of a stand-alone
-// exchange.  push_d: the output's row space when the caller's next launch reads the
+// Fused push (opt-in PSC_PUSH=1): a producer row kernel pushes its
+// output's boundary rows into the neighbours' halo slots and signals; the next launch,
+// when it is the row kernel reading that vector's halo, waits instead of a stand-alone
+// exchange.  Measured slower on 2 B200 (6670 vs 7050 Mdof*iters/s): producer-end
+// system fences and consumer-start waits serialise the kernels on NVLink latency.  push_d: the output's row space when the caller's next launch reads the
 // output's halo (nullptr: no push).
 bool fused_push_on() {
   static const bool on = getenv("PSC_PUSH") != nullptr && getenv("PSC_OVERLAP") == nullptr &&

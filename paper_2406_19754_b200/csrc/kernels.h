@@ -31,6 +31,7 @@ enum class RowOp {
 struct PushSpec {
   int on = 0;
   int R = 0;
+  const uint8_t* sslice = nullptr; // [n_own/32]: 1 if a row of the 32-row slice is sent
   const int32_t* iptr = nullptr;  // [n_own+1]: sends of owned row i at [iptr[i], iptr[i+1])
   const int32_t* iq = nullptr;    // peer of each send
   const int32_t* ipos = nullptr;  // slot in that peer's block of y's halo

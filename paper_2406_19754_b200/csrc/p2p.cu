@@ -127,6 +127,7 @@ bool p2p_push_spec(psc_ctx* ctx, P2P& P, psc_desc* d, const double* y, PushSpec&
   if (!L.any || !L.d_iptr || d->n_own + d->n_halo() <= 0) return false;
   ps.on = 1;
   ps.R = ctx->nranks;
+  ps.sslice = L.d_sslice;
   ps.iptr = L.d_iptr;
   ps.iq = L.d_iq;
   ps.ipos = L.d_ipos;
@@ -268,6 +269,11 @@ void p2p_setup(psc_ctx* ctx, P2P& P, const std::vector<P2PBufSpec>& halo_bufs,
           iq[o] = p;
           ipos[o] = (int32_t)(k - d->soff[p]);
         }
+      std::vector<uint8_t> ss((d->n_own + 31) / 32, 0);
+      for (int64_t i = 0; i < d->n_own; ++i)
+        if (iptr[i + 1] > iptr[i]) ss[i >> 5] = 1;
+      Lv.d_sslice = dalloc<uint8_t>(ss.size());
+      PSC_CUDA(cudaMemcpy(Lv.d_sslice, ss.data(), ss.size(), cudaMemcpyHostToDevice));
       Lv.d_iptr = dalloc<int32_t>(d->n_own + 1);
       Lv.d_iq = dalloc<int32_t>(d->n_send);
       Lv.d_ipos = dalloc<int32_t>(d->n_send);
@@ -335,6 +341,7 @@ void p2p_free(psc_ctx* ctx, P2P& P) {
     dfree(Lv.d_nbr);
     dfree(Lv.d_soff);
     dfree(Lv.d_iptr);
+    dfree(Lv.d_sslice);
     dfree(Lv.d_iq);
     dfree(Lv.d_ipos);
   }

@@ -27,6 +27,7 @@ struct P2PLevel {
   int64_t* d_soff = nullptr;
   // fused push: for each owned row, its sends (peer, slot in the peer's block)
   int32_t* d_iptr = nullptr;
+  uint8_t* d_sslice = nullptr;
   int32_t* d_iq = nullptr;
   int32_t* d_ipos = nullptr;
 };
