@@ -150,12 +150,7 @@ void allgather_slot(psc_hier* h, Slot s, cudaStream_t st) {
 void exchange(psc_hier* h, psc_desc* d, double* x, cudaStream_t s) {
   psc_ctx* ctx = h->ctx;
   if (ctx->nranks == 1) return;
-  // TEST HOOK ("halo freshness"): PSC_DEBUG_POISON_HALO=1 fills the halo
-  // slots with NaN (all-ones bytes) right before every exchange; a slot the exchange
-  // failed to refresh would carry the NaN into the owned results
-  static const bool poison = getenv("PSC_DEBUG_POISON_HALO") != nullptr;
-  if (poison && d->n_halo() > 0)
-    PSC_CUDA(cudaMemsetAsync(x + d->n_own, 0xFF, sizeof(double) * d->n_halo(), s));
+
   if (p2p_halo(ctx, h->p2p, d, x, s)) return;
   halo_exchange(ctx, d, x, s);
 }
@@ -197,6 +192,17 @@ bool fused_push_on() {
   return on;
 }
 
+// TEST HOOK ("halo freshness"): PSC_DEBUG_POISON_HALO=1 fills the halo slots
+// of x with NaN (all-ones bytes) right after every kernel that read them; a later kernel
+// reading them without a new exchange would carry the NaN into the owned results.
+// (After the read, not before the exchange: a peer may push into the halo before this
+// rank's own exchange kernel starts.)
+void poison_halo(psc_hier* h, psc_desc* d, const double* x, cudaStream_t s) {
+  static const bool poison = getenv("PSC_DEBUG_POISON_HALO") != nullptr;
+  if (poison && h->ctx->nranks > 1 && d && d->n_halo() > 0)
+    PSC_CUDA(cudaMemsetAsync(const_cast<double*>(x) + d->n_own, 0xFF, sizeof(double) * d->n_halo(), s));
+}
+
 void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cudaStream_t s,
               psc_desc* push_d = nullptr) {
   psc_ctx* ctx = h->ctx;
@@ -215,6 +221,7 @@ void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cud
     launch_rows(ctx, S, op, a, s, SliceSet::Interior);
     PSC_CUDA(cudaStreamWaitEvent(s, h->ev_join, 0));
     launch_rows(ctx, S, op, a, s, SliceSet::Boundary);
+    poison_halo(h, d, a.x, s);
     return;
   }
   if (!(pushed_here && d && rows_can_push(S, a) && p2p_wait_spec(ctx, h->p2p, a.x, a.wait))) prep(h, d, a, s);
@@ -225,6 +232,7 @@ void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cud
     h->pushed = a.y;
     h->pushed_at = ctx->launches + ctx->collectives;
   }
+  poison_halo(h, d, a.x, s);
 }
 
 // ------------------------------------------------------------ coarsest level
@@ -298,6 +306,7 @@ double* coarse_pcg(psc_hier* h, LevelWS& W, const double* b, cudaStream_t s) {
       a.red_out = scal_mine(h, S_CPQ);
       prep(h, W.d, a, s);
       launch_rows(ctx, W.A->S, RowOp::SpmvDot, a, s);
+      poison_halo(h, W.d, a.x, s);
     }
     if (dist) allgather_slot(h, S_CPQ, s);
     launch_cpcg_update(ctx, W.n, x, p, r, q, z, W.dinv, g(S_CPQ), g(zo), nr, h->d_done, &h->red2,
@@ -725,6 +734,7 @@ void record_iteration(psc_hier* h, cudaStream_t s, bool timing, int method) {
     a.red_out = scal_mine(h, S_PQ);
     prep(h, W.d, a, s);
     launch_rows(ctx, W.A->S, RowOp::SpmvDot, a, s);
+    poison_halo(h, W.d, a.x, s);
   }
   allgather_slot(h, S_PQ, s);
   launch_cg_update(ctx, W.n, h->x_int, h->p, h->r_cg, h->q, scal(h, S_PQ), fcg ? scal(h, S_PR) : rz_old(h),
@@ -1053,6 +1063,7 @@ int solve_impl(psc_hier* h, int method, const double* b, double* x, double tol, 
     a.red_stride = (int)((size_t)(S_BB - S_RR) * R);
     prep(h, W.d, a, s);
     launch_rows(ctx, W.A->S, RowOp::ResidDot2, a, s);
+    poison_halo(h, W.d, a.x, s);
   }
   allgather_slot(h, S_RR, s);
   allgather_slot(h, S_BB, s);

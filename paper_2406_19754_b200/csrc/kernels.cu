@@ -698,8 +698,12 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         if (cbytes) bulk_g2s(base + kTmaHdrBytes + kTmaValBytes, a.col + cb0, cbytes, &full[st], pol_mat);
         unsigned char* vec = base + kTmaHdrBytes + kTmaValBytes + kTmaColBytes;
         if (rbytes) {
-          if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], pol_stream);
-          if constexpr (EV::D_SELL) bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
+          // Sweep0 gathers b and 1/M of the neighbouring rows too (x1 = M^-1 b on the fly):
+          // keep the chunk's b / 1/M in L2 for them instead of evicting them first
+          constexpr bool kGatherBD = (OP == RowOp::Sweep0);
+          if constexpr (EV::B) bulk_g2s(vec, a.b + r0, rbytes, &full[st], kGatherBD ? pol_keep : pol_stream);
+          if constexpr (EV::D_SELL)
+            bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], kGatherBD ? pol_keep : pol_stream);
           if constexpr (EV::X || EV::XPRE) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
           if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
         }

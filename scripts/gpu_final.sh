@@ -6,7 +6,7 @@ python __graft_entry__.py smoke > gpurun_out/${TAG}_smoke.log 2>&1; echo smoke_r
 timeout 2400 python -m pytest tests/ -q -m gpu > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo tests_rc=$?
 tail -2 gpurun_out/${TAG}_gpu_tests.log
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > gpurun_out/${TAG}_gpu.txt
-timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench_rc=$?
+PSC_AMG_VERBOSE=1 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench_rc=$?; grep psc_amg gpurun_out/${TAG}_bench.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err; echo ref_rc=$?
 B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-kernel-table"
 for cfg in "--vbm" "--vbm --hierarchy smatch" "--vbm --hierarchy vmatch" "--variable-v" "--problem jump" "--grid 128" "--setup host"; do
