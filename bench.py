@@ -413,6 +413,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    barrier()  # ranks finish their host-side set-up at different times
     for k in range(args.warmup):
         H.solve(bs[k], xs[k], tol=args.tol, maxit=args.maxit, method=args.krylov)
 

@@ -89,10 +89,12 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
   *a.ticket = 0u;
 }
 
-// PSC_SPIN_TIMEOUT_S: seconds a rank waits for a neighbour's flag (default 30)
+// PSC_SPIN_TIMEOUT_S: seconds a rank waits for a neighbour's flag (default 300: ranks can
+// legitimately drift apart by tens of seconds on large set-ups, e.g. 512^3 over 4 GPUs
+// with host-side inputs, where a 30 s bound tripped)
 static uint64_t spin_timeout_ns() {
   static const uint64_t tmo =
-      (uint64_t)(1e9 * (getenv("PSC_SPIN_TIMEOUT_S") ? atof(getenv("PSC_SPIN_TIMEOUT_S")) : 30.0));
+      (uint64_t)(1e9 * (getenv("PSC_SPIN_TIMEOUT_S") ? atof(getenv("PSC_SPIN_TIMEOUT_S")) : 300.0));
   return tmo;
 }
 
