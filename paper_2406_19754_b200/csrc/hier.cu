@@ -203,8 +203,10 @@ void poison_halo(psc_hier* h, psc_desc* d, const double* x, cudaStream_t s) {
     PSC_CUDA(cudaMemsetAsync(const_cast<double*>(x) + d->n_own, 0xFF, sizeof(double) * d->n_halo(), s));
 }
 
+// tev: optional event pair recorded around the row kernel alone (after its halo
+// exchange: the dominant-kernel timing must not include the wait for the neighbours)
 void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cudaStream_t s,
-              psc_desc* push_d = nullptr) {
+              psc_desc* push_d = nullptr, cudaEvent_t* tev = nullptr) {
   psc_ctx* ctx = h->ctx;
   // a pushed halo is only valid for the immediately following launch
   const bool pushed_here = h->pushed && h->pushed == a.x && h->pushed_at == ctx->launches + ctx->collectives;
@@ -218,16 +220,20 @@ void run_rows(psc_hier* h, psc_desc* d, const Sell& S, RowOp op, RowArgs& a, cud
     PSC_CUDA(cudaStreamWaitEvent(ctx->comm_stream, h->ev_fork, 0));
     exchange(h, d, const_cast<double*>(a.x), ctx->comm_stream);
     PSC_CUDA(cudaEventRecord(h->ev_join, ctx->comm_stream));
+    if (tev) PSC_CUDA(cudaEventRecordWithFlags(tev[0], s, cudaEventRecordExternal));
     launch_rows(ctx, S, op, a, s, SliceSet::Interior);
     PSC_CUDA(cudaStreamWaitEvent(s, h->ev_join, 0));
     launch_rows(ctx, S, op, a, s, SliceSet::Boundary);
+    if (tev) PSC_CUDA(cudaEventRecordWithFlags(tev[1], s, cudaEventRecordExternal));
     poison_halo(h, d, a.x, s);
     return;
   }
   if (!(pushed_here && d && rows_can_push(S, a) && p2p_wait_spec(ctx, h->p2p, a.x, a.wait))) prep(h, d, a, s);
   const bool push = fused_push_on() && push_d && ctx->nranks > 1 && rows_can_push(S, a) &&
                     p2p_push_spec(ctx, h->p2p, push_d, a.y, a.push);
+  if (tev) PSC_CUDA(cudaEventRecordWithFlags(tev[0], s, cudaEventRecordExternal));
   launch_rows(ctx, S, op, a, s);
+  if (tev) PSC_CUDA(cudaEventRecordWithFlags(tev[1], s, cudaEventRecordExternal));
   if (push) {
     h->pushed = a.y;
     h->pushed_at = ctx->launches + ctx->collectives;
@@ -549,13 +555,9 @@ int pre_smooth(psc_hier* h, LevelWS& W, const double* b, int nsweeps, cudaStream
     a.dinv = W.dinv;
     a.y = W.x[cur ^ 1];
     const bool t = timing && h->dom_used + 2 <= (int)h->ev_dom.size();
-    if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
     // output read next by the following sweep or by the residual (both row kernels)
-    run_rows(h, W.d, W.A->S, RowOp::Sweep, a, s, W.d);
-    if (t) {
-      PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
-      h->dom_used += 2;
-    }
+    run_rows(h, W.d, W.A->S, RowOp::Sweep, a, s, W.d, t ? &h->ev_dom[h->dom_used] : nullptr);
+    if (t) h->dom_used += 2;
     cur ^= 1;
   }
   return cur;
@@ -675,17 +677,14 @@ double* vcycle_rec(psc_hier* h, std::vector<LevelWS>& LV, int l, const double* b
       a.w = h->rz_weight;
     }
     const bool t = time_here && h->dom_used + 2 <= (int)h->ev_dom.size();
-    if (t) PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used], s, cudaEventRecordExternal));
     // the output's halo is read next by the following post-sweep, or (last sweep,
     // level >= 1) by the prolongation of the level above
     RowArgs pa;
     pa.vec_padded = true;
     const bool consumer_waits = (k + 1 < post) || (l > 0 && rows_can_push(LV[l - 1].P->S, pa));
-    run_rows(h, W.d, W.A->S, last0 ? RowOp::SweepDot : RowOp::Sweep, a, s, (!last0 && consumer_waits) ? W.d : nullptr);
-    if (t) {
-      PSC_CUDA(cudaEventRecordWithFlags(h->ev_dom[h->dom_used + 1], s, cudaEventRecordExternal));
-      h->dom_used += 2;
-    }
+    run_rows(h, W.d, W.A->S, last0 ? RowOp::SweepDot : RowOp::Sweep, a, s, (!last0 && consumer_waits) ? W.d : nullptr,
+             t ? &h->ev_dom[h->dom_used] : nullptr);
+    if (t) h->dom_used += 2;
     cur ^= 1;
   }
   if (level0 && post == 0)
