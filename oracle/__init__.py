@@ -63,7 +63,7 @@ class _Hier(ctypes.Structure):
                 ("R", ctypes.POINTER(_CSR)), ("pre", ctypes.c_int), ("post", ctypes.c_int),
                 ("coarse", ctypes.c_int), ("coarse_pcg", ctypes.c_int), ("coarse_maxit", ctypes.c_int),
                 ("coarse_tol", ctypes.c_double), ("variable_v", ctypes.c_int), ("smoother", ctypes.c_int),
-                ("ainv_drop", ctypes.c_double)]
+                ("ainv_drop", ctypes.c_double), ("ainv_nb", ctypes.c_void_p), ("ainv_rs", ctypes.c_void_p)]
 
 
 def lib():
@@ -111,7 +111,7 @@ class _CsrHolder:
 
 class _HierHolder:
     def __init__(self, hier, pre=4, post=4, coarse=30, coarse_pcg=False, coarse_maxit=40, coarse_tol=1e-10,
-                 variable_v=False, smoother="l1", ainv_drop=0.1):
+                 variable_v=False, smoother="l1", ainv_drop=0.1, ainv_blocks=None):
         L = hier.nlevels
         self.A = [_CsrHolder(hier.levels[l].A) for l in range(L)]
         self.P = [_CsrHolder(hier.levels[l].P) for l in range(L - 1)]
@@ -121,8 +121,20 @@ class _HierHolder:
         self.Ra = (_CSR * max(L - 1, 1))(*[h.c for h in self.R])
         if smoother not in ("l1", "ainv"):
             raise ValueError("smoother must be 'l1' or 'ainv'")
+        # AINV block structure per level (None: the whole level matrix)
+        nb = np.zeros(L, np.int32)
+        self._rs = [None] * L
+        rsp = (ctypes.c_void_p * L)()
+        for l in range(L):
+            blk = ainv_blocks[l] if ainv_blocks is not None and l < len(ainv_blocks) else None
+            if blk is not None:
+                self._rs[l] = _arr(blk, np.int64)
+                nb[l] = len(self._rs[l]) - 1
+                rsp[l] = self._rs[l].ctypes.data
+        self._nb, self._rsp = nb, rsp
         self.c = _Hier(L, self.Aa, self.Pa, self.Ra, pre, post, coarse, 1 if coarse_pcg else 0, coarse_maxit,
-                       coarse_tol, 1 if variable_v else 0, 1 if smoother == "ainv" else 0, float(ainv_drop))
+                       coarse_tol, 1 if variable_v else 0, 1 if smoother == "ainv" else 0, float(ainv_drop),
+                       nb.ctypes.data, ctypes.cast(rsp, ctypes.c_void_p).value)
 
 
 def spmv(A, x) -> np.ndarray:

@@ -63,6 +63,10 @@ typedef struct {
   int variable_v;   /* 1: variable V-cycle, pre/post sweeps doubled per level (P:330 footnote, R25) */
   int smoother;     /* 0: l1-Jacobi; 1: AINV (reading R27) on levels < L-1 */
   double ainv_drop; /* AINV drop tolerance */
+  /* AINV blocks per level (block-Jacobi across ranks): ainv_nb[l] blocks with
+   * row starts ainv_rs[l][0..nb]; NULL (or nb <= 1): the whole matrix */
+  const int* ainv_nb;
+  const int64_t* const* ainv_rs;
 } or_hier;
 
 int or_ainv(const or_csr* A, int nranks, const int64_t* row_start, double drop_tol, int64_t** zptr,
@@ -281,9 +285,11 @@ static or_smoother* make_m(const or_hier* h) {
     sm[l].m = dalloc(h->A[l].nrows);
     or_l1_diag(&h->A[l], sm[l].m);
     if (h->smoother == 1 && l < h->nlevels - 1) {
-      const int64_t rs[2] = {0, h->A[l].nrows};
+      const int64_t whole[2] = {0, h->A[l].nrows};
+      const int blocked = h->ainv_nb && h->ainv_rs && h->ainv_nb[l] > 1 && h->ainv_rs[l];
       sm[l].p = dalloc(h->A[l].nrows);
-      or_ainv(&h->A[l], 1, rs, h->ainv_drop, &sm[l].zp, &sm[l].zr, &sm[l].zv, sm[l].p);
+      or_ainv(&h->A[l], blocked ? h->ainv_nb[l] : 1, blocked ? h->ainv_rs[l] : whole, h->ainv_drop, &sm[l].zp,
+              &sm[l].zr, &sm[l].zv, sm[l].p);
     }
   }
   return sm;

@@ -449,19 +449,30 @@ void sell_from_host(psc_ctx* ctx, int64_t n, int64_t ncols, const std::vector<in
   dfree(dv);
 }
 
-// AINV factors of level W from its matrix's host copy (one rank: the owned block is
-// the whole matrix; columns are local = global)
+// AINV factors of level W from its matrix's host copy.  Distributed level: the owned
+// diagonal block (columns outside this rank's rows dropped: the paper's block-Jacobi
+// form); replicated level or one rank: the whole matrix.
 void build_ainv(psc_hier* h, LevelWS& W) {
-  psc_ctx* ctx = h->ctx;
   psc_mat* A = W.A;
-  PSC_REQUIRE(ctx->nranks == 1, PSC_ERR_STATE, "AINV smoother: one rank only");
   PSC_REQUIRE((int64_t)A->h_rowptr.size() == A->n_rows + 1, PSC_ERR_STATE,
               "AINV smoother needs the matrix's host copy (nnz <= 2^27)");
   free_ainv(W);
   const int64_t n = W.n;
+  const int64_t ob = W.d ? W.d->own_begin : 0;
+  std::vector<int64_t> bp(n + 1, 0), bc;
+  std::vector<double> bv;
+  for (int64_t i = 0; i < n; ++i) {  // the block in local numbering, columns in order
+    for (int64_t k = A->h_rowptr[i]; k < A->h_rowptr[i + 1]; ++k) {
+      const int64_t c = A->h_colg[k] - ob;
+      if (c < 0 || c >= n) continue;
+      bc.push_back(c);
+      bv.push_back(A->h_val[k]);
+    }
+    bp[i + 1] = (int64_t)bc.size();
+  }
   std::vector<int64_t> zp, zr, tp, tr;
   std::vector<double> zv, tv, pv;
-  ainv_factor(n, A->h_rowptr.data(), A->h_colg.data(), A->h_val.data(), h->opt.ainv_drop, zp, zr, zv, pv);
+  ainv_factor(n, bp.data(), bc.data(), bv.data(), h->opt.ainv_drop, zp, zr, zv, pv);
   // Z^T by rows (= columns of Z)
   tp.assign(n + 1, 0);
   for (int64_t q = 0; q < zp[n]; ++q) tp[zr[q] + 1]++;
@@ -475,8 +486,8 @@ void build_ainv(psc_hier* h, LevelWS& W) {
       tr[o] = k;
       tv[o] = zv[q];
     }
-  sell_from_host(ctx, n, n, zp, zr, zv, W.Z);
-  sell_from_host(ctx, n, n, tp, tr, tv, W.Zt);
+  sell_from_host(h->ctx, n, n, zp, zr, zv, W.Z);
+  sell_from_host(h->ctx, n, n, tp, tr, tv, W.Zt);
   std::vector<double> dinv(n);
   for (int64_t i = 0; i < n; ++i) dinv[i] = 1.0 / pv[i];
   W.ainv_dinv = dvec(n);
@@ -841,6 +852,9 @@ psc_mat* replicate_matrix(psc_ctx* ctx, psc_mat* A, int64_t n_rows_global, int64
   m->ctx = ctx;
   m->n_rows = n_rows_global;
   m->nnz = totnnz;
+  m->h_rowptr.swap(rp_all);  // host copy (AINV factors of the replicated levels)
+  m->h_colg.swap(col_all);
+  m->h_val.swap(val_all);
   try {
     sell_from_csr(ctx, n_rows_global, drp, dcol, dval, totnnz, 0, n_cols_global, nullptr, 0, m->S, s, 0, allow_dia);
   } catch (...) {
@@ -958,6 +972,7 @@ void build_replica(psc_hier* h, int first) {
       *b = dvec(W.n);
       PSC_CUDA(cudaMemsetAsync(*b, 0, sizeof(double) * W.n, s));
     }
+    if (h->opt.smoother == PSC_SMOOTHER_AINV && k + 1 < L) build_ainv(h, W);
     if (k == L - 1) level_coarse_solver(h, W);
     rp.lv.push_back(W);
   }
@@ -995,6 +1010,7 @@ void free_hier(psc_hier* h) {
   }
   Replica& rp = h->rep;
   for (auto& W : rp.lv) {
+    free_ainv(W);
     dfree(W.dinv);
     dfree(W.x[0]);
     dfree(W.x[1]);

@@ -103,6 +103,17 @@ def check(grid, procs, problem, shm, rank, world, local, full=True):
         parts3 = [None] * world
         dist.all_gather_object(parts3, z3.cpu().numpy())
         H3.close()
+        # NEXT-4: the AINV smoother, block-Jacobi across ranks on the distributed levels
+        # (each rank factors its diagonal block), whole-matrix factors on the
+        # replicated suffix
+        H4 = psc.Hierarchy(ctx, A, P, R, pre=1, post=1, smoother="ainv", ainv_drop=0.1)
+        z4 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+        H4.vcycle(torch.from_numpy(b[r0:r1].copy()).cuda(), z4)
+        x4 = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+        rc4, st4, hist4 = H4.solve(torch.from_numpy(b[r0:r1].copy()).cuda(), x4, tol=1e-8, maxit=200)
+        parts4 = [None] * world
+        dist.all_gather_object(parts4, (z4.cpu().numpy(), x4.cpu().numpy(), rc4, st4["iters"], hist4))
+        H4.close()
     ok = True
     if rank == 0:
         import oracle
@@ -146,6 +157,27 @@ def check(grid, procs, problem, shm, rank, world, local, full=True):
             ok &= (out["vbm_vcycle_rel"] <= 1e-9 and len(its2) == 1 and abs(parts2[0][3] - ito2) <= 1
                    and all(p[2] == 0 for p in parts2) and out["vbm_hist_rel"] <= 1e-9 and out["vbm_x_rel"] <= 1e-7
                    and all(np.array_equal(parts2[0][4], p[4]) for p in parts2))
+            # AINV blocks as the library forms them: the rank row blocks on distributed
+            # levels, the whole matrix from the first replicated level (hier.cu
+            # replica_first: first level >= 1 with at most PSC_REPL_ROWS global rows)
+            lim = int(os.environ.get("PSC_REPL_ROWS", "50000"))
+            L = meta["nlevels"]
+            first = next((l for l in range(1, L) if lim and int(levels[l]["n_global"]) <= lim), L)
+            blocks = [np.asarray(levels[l]["row_start"], np.int64) if l < first and world > 1 else None
+                      for l in range(L)]
+            akw = dict(pre=1, post=1, smoother="ainv", ainv_drop=0.1, ainv_blocks=blocks)
+            zg4 = np.concatenate([p[0] for p in parts4])
+            out["ainv_vcycle_rel"] = float(ew_err(zg4, oracle.vcycle(h, b, **akw)))
+            xo4, ito4, sto4, histo4 = oracle.pcg(h, b, tol=1e-8, maxit=200, **akw)
+            xg4 = np.concatenate([p[1] for p in parts4])
+            k4 = min(20, ito4, parts4[0][3]) + 1
+            out.update(ainv_first_replicated=first, ainv_iters_gpu=sorted({p[3] for p in parts4}),
+                       ainv_iters_oracle=ito4,
+                       ainv_hist_rel=float(np.max(np.abs(parts4[0][4][:k4] - histo4[:k4]) / histo4[:k4])),
+                       ainv_x_rel=float(np.linalg.norm(xg4 - xo4) / np.linalg.norm(xo4)))
+            ok &= (out["ainv_vcycle_rel"] <= 1e-12 and len({p[3] for p in parts4}) == 1
+                   and abs(parts4[0][3] - ito4) <= 1 and all(p[2] == 0 for p in parts4)
+                   and out["ainv_hist_rel"] <= 1e-9 and out["ainv_x_rel"] <= 1e-7)
             zg3 = np.concatenate(parts3)
             zo3 = oracle.vcycle(h, b, 2, 2, 30, variable_v=True)
             out["varv_vcycle_rel"] = float(ew_err(zg3, zo3))
