@@ -584,34 +584,30 @@ void or_transpose(const or_csr* P, int64_t** rptr, int64_t** rcol, double** rval
   *rptr = ptr; *rcol = col; *rval = val;
 }
 
-/* Galerkin coarse operator A_c = R A P (R = P^T), row by row:
- *   A_c[J, K] = sum_{i in R_J} sum_{k in A_i} (R_Ji a_ik) P_kK
- * accumulated in that loop order (i, then k, then K increasing), columns increasing;
- * every (J, K) reached is stored (also when the sum cancels). */
-void or_galerkin(const or_csr* R, const or_csr* A, const or_csr* P, int64_t** cptr, int64_t** ccol,
-                 double** cval) {
-  const int64_t nc = R->nrows;
-  double* acc = dalloc(P->ncols);
-  int64_t* mark = (int64_t*)malloc(sizeof(int64_t) * (size_t)(P->ncols > 0 ? P->ncols : 1));
-  int64_t* touched = (int64_t*)malloc(sizeof(int64_t) * (size_t)(P->ncols > 0 ? P->ncols : 1));
-  for (int64_t K = 0; K < P->ncols; ++K) mark[K] = -1;
+/* Sparse product Z = X Y row by row (Gustavson):
+ *   Z[i, K] = sum_{k in X_i} X_ik Y_kK
+ * accumulated in that loop order (k, then K increasing), columns increasing; every
+ * (i, K) reached is stored (also when the sum cancels). */
+static void or_spgemm(const or_csr* X, const or_csr* Y, or_csr* Z) {
+  const int64_t n = X->nrows, m = Y->ncols;
+  double* acc = dalloc(m);
+  int64_t* mark = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
+  int64_t* touched = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
+  for (int64_t K = 0; K < m; ++K) mark[K] = -1;
   int64_t cap = 1024, o = 0;
-  int64_t* ptr = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nc + 1));
+  int64_t* ptr = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
   int64_t* col = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
   double* val = (double*)malloc(sizeof(double) * (size_t)cap);
   ptr[0] = 0;
-  for (int64_t J = 0; J < nc; ++J) {
+  for (int64_t i = 0; i < n; ++i) {
     int64_t nt = 0;
-    for (int64_t a = R->ptr[J]; a < R->ptr[J + 1]; ++a) {
-      const int64_t i = R->col[a];
-      for (int64_t b = A->ptr[i]; b < A->ptr[i + 1]; ++b) {
-        const int64_t k = A->col[b];
-        const double ra = R->val[a] * A->val[b];
-        for (int64_t c = P->ptr[k]; c < P->ptr[k + 1]; ++c) {
-          const int64_t K = P->col[c];
-          if (mark[K] != J) { mark[K] = J; acc[K] = 0.0; touched[nt++] = K; }
-          acc[K] = acc[K] + ra * P->val[c];
-        }
+    for (int64_t b = X->ptr[i]; b < X->ptr[i + 1]; ++b) {
+      const int64_t k = X->col[b];
+      const double xv = X->val[b];
+      for (int64_t c = Y->ptr[k]; c < Y->ptr[k + 1]; ++c) {
+        const int64_t K = Y->col[c];
+        if (mark[K] != i) { mark[K] = i; acc[K] = 0.0; touched[nt++] = K; }
+        acc[K] = acc[K] + xv * Y->val[c];
       }
     }
     for (int64_t x = 1; x < nt; ++x) { /* sort the touched columns */
@@ -626,10 +622,25 @@ void or_galerkin(const or_csr* R, const or_csr* A, const or_csr* P, int64_t** cp
       val = (double*)realloc(val, sizeof(double) * (size_t)cap);
     }
     for (int64_t x = 0; x < nt; ++x) { col[o] = touched[x]; val[o] = acc[touched[x]]; ++o; }
-    ptr[J + 1] = o;
+    ptr[i + 1] = o;
   }
   free(acc); free(mark); free(touched);
-  *cptr = ptr; *ccol = col; *cval = val;
+  Z->nrows = n; Z->ncols = m; Z->ptr = ptr; Z->col = col; Z->val = val;
+}
+
+/* Galerkin coarse operator A_c = R A P (R = P^T), reading R31: associated
+ * as R (A P), two sparse products in Gustavson's row order:
+ *   (AP)[i, K] = sum_{k in A_i} a_ik P_kK,   A_c[J, K] = sum_{i in R_J} R_Ji (AP)[i, K]
+ * (work nnz(A) * |P row| + nnz(R) * |AP row| instead of the triple product's
+ * nnz(R) * |A row| * |P row|).  Same pattern as the triple product: every (J, K)
+ * reached is stored. */
+void or_galerkin(const or_csr* R, const or_csr* A, const or_csr* P, int64_t** cptr, int64_t** ccol,
+                 double** cval) {
+  or_csr AP, C;
+  or_spgemm(A, P, &AP);
+  or_spgemm(R, &AP, &C);
+  free((void*)AP.ptr); free((void*)AP.col); free((void*)AP.val);
+  *cptr = (int64_t*)C.ptr; *ccol = (int64_t*)C.col; *cval = (double*)C.val;
 }
 
 /* ======================================================================

@@ -97,7 +97,9 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NR], double* partials,
 constexpr int kHdr = 16;     // int32 words per slice header
 constexpr int kMaxDiaHdr = 8;  // DIA offsets also held in the slice header (words 6..13)
 constexpr int kMaxDia = 64;    // most diagonals a DIA slice may have (all in its column region)
-enum SliceKind : int { kEll = 0, kDia = 1 };
+// kEll16: ELL slice whose columns span less than 2^16 (all owned): stored as uint16
+// offsets from a per-slice base column (header word 6), 2 bytes per slot instead of 4
+enum SliceKind : int { kEll = 0, kDia = 1, kEll16 = 2 };
 
 __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int64_t s, int lane) {
   return lane < kHdr ? __ldg(hdr + s * kHdr + lane) : 0;
@@ -111,6 +113,10 @@ __device__ __forceinline__ int32_t load_hdr(const int32_t* __restrict__ hdr, int
 // matrix-stream load: evict-first unless the matrix is small enough to stay in L2
 __device__ __forceinline__ double ldm(const double* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
 __device__ __forceinline__ int32_t ldm(const int32_t* p, bool keep) { return keep ? __ldg(p) : __ldcs(p); }
+__device__ __forceinline__ int32_t ldm(const uint16_t* p, bool keep) {
+  return (int32_t)(keep ? __ldg(reinterpret_cast<const unsigned short*>(p))
+                        : __ldcs(reinterpret_cast<const unsigned short*>(p)));
+}
 
 // x gathers: read-only texture path, or (CG) through L2 only
 template <bool CG>
@@ -134,6 +140,44 @@ __device__ __forceinline__ double dia_sum(int32_t h, uint32_t i, const double* _
   double sum = 0.0;
 #pragma unroll
   for (int j = 0; j < W; ++j) sum = fma(vi[j], xv[j], sum);
+  return sum;
+}
+
+// ELL part of a row sum: columns c[32 k] (+ base: kEll16 offsets), batches of 8
+// (value, column) loads issued before the dependent gathers
+template <bool CG, typename CT>
+__device__ __forceinline__ double ell_sum(const CT* __restrict__ c, int32_t base, int w, const double* __restrict__ v,
+                                          const double* __restrict__ x, int64_t ncols, bool keep) {
+  double sum = 0.0;
+  int k = 0;
+  for (; k + 8 <= w; k += 8) {
+    int ci[8];
+    double vi[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      ci[j] = base + ldm(c + 32 * j, keep);
+      vi[j] = ldm(v + 32 * j, keep);
+      PSC_DASSERT((uint64_t)ci[j] < (uint64_t)ncols);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sum = fma(vi[j], ldx<CG>(x + ci[j]), sum);
+    c += 256;
+    v += 256;
+  }
+  const int rem = w - k;
+  if (rem > 0) {
+    int ci[8];
+    double vi[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < rem) {
+        ci[j] = base + ldm(c + 32 * j, keep);
+        vi[j] = ldm(v + 32 * j, keep);
+      }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < rem) sum = fma(vi[j], ldx<CG>(x + ci[j]), sum);
+  }
   return sum;
 }
 
@@ -193,38 +237,10 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
   }
   const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
                      (uint32_t)__shfl_sync(0xffffffffu, h, 2);
-  const int32_t* c = col + cb + lane;
-  double sum = 0.0;
-  int k = 0;
-  for (; k + 8 <= w; k += 8) {
-    int ci[8];
-    double vi[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      ci[j] = ldm(c + 32 * j, keep);
-      vi[j] = ldm(v + 32 * j, keep);
-      PSC_DASSERT((uint64_t)ci[j] < (uint64_t)ncols);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) sum = fma(vi[j], ldx<CG>(x + ci[j]), sum);
-    c += 256;
-    v += 256;
-  }
-  const int rem = w - k;
-  if (rem > 0) {
-    int ci[8];
-    double vi[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < rem) {
-        ci[j] = ldm(c + 32 * j, keep);
-        vi[j] = ldm(v + 32 * j, keep);
-      }
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < rem) sum = fma(vi[j], ldx<CG>(x + ci[j]), sum);
-  }
-  return sum;
+  if (__shfl_sync(0xffffffffu, h, 5) == kEll16)
+    return ell_sum<CG>(reinterpret_cast<const uint16_t*>(col + cb) + lane, __shfl_sync(0xffffffffu, h, 6), w, v,
+                       x, ncols, keep);
+  return ell_sum<CG>(col + cb + lane, 0, w, v, x, ncols, keep);
 }
 
 // Column of entry k of local row i, stored in lane `lane` of slice s; -1 if a DIA
@@ -238,6 +254,8 @@ __device__ __forceinline__ int64_t sell_col(const int32_t* __restrict__ hdr, con
     const int64_t c = i + col[cb + k];
     return ((uint64_t)c < (uint64_t)ncols) ? c : -1;
   }
+  if (kind == kEll16)
+    return (int64_t)hdr[s * kHdr + 6] + reinterpret_cast<const uint16_t*>(col + cb)[32 * (int64_t)k + lane];
   return col[cb + 32 * (int64_t)k + lane];
 }
 
@@ -732,7 +750,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const int64_t vb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 1) << 32) |
                            (uint32_t)__shfl_sync(0xffffffffu, h, 0);
         const int w = __shfl_sync(0xffffffffu, h, 4);
-        const bool dia = __shfl_sync(0xffffffffu, h, 5) == 1;
+        const int kind = __shfl_sync(0xffffffffu, h, 5);
+        const bool dia = kind == kDia;
         const double* v = vs + (vb - vbase) + lane;
         const uint32_t i = (uint32_t)(s * 32 + lane);
         // x_j; Sweep0: x1_j = dinv_j b_j, the first sweep from zero (a correctly
@@ -751,11 +770,20 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         } else {
           const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
                              (uint32_t)__shfl_sync(0xffffffffu, h, 2);
-          const int32_t* cc = cs + (cb - cbase) + lane;
+          if (kind == kEll16) {
+            const uint16_t* cc = reinterpret_cast<const uint16_t*>(cs + (cb - cbase)) + lane;
+            const uint32_t base = (uint32_t)__shfl_sync(0xffffffffu, h, 6);
 #pragma unroll
-          for (int j = 0; j < kTmaMaxW; ++j) PSC_DASSERT(j >= w || (uint32_t)cc[32 * j] < nc);
+            for (int j = 0; j < kTmaMaxW; ++j) PSC_DASSERT(j >= w || base + cc[32 * j] < nc);
 #pragma unroll
-          for (int j = 0; j < kTmaMaxW; ++j) xv[j] = (j < w) ? gx((uint32_t)cc[32 * j]) : 0.0;
+            for (int j = 0; j < kTmaMaxW; ++j) xv[j] = (j < w) ? gx(base + cc[32 * j]) : 0.0;
+          } else {
+            const int32_t* cc = cs + (cb - cbase) + lane;
+#pragma unroll
+            for (int j = 0; j < kTmaMaxW; ++j) PSC_DASSERT(j >= w || (uint32_t)cc[32 * j] < nc);
+#pragma unroll
+            for (int j = 0; j < kTmaMaxW; ++j) xv[j] = (j < w) ? gx((uint32_t)cc[32 * j]) : 0.0;
+          }
         }
         double sum = 0.0;
 #pragma unroll
@@ -1867,9 +1895,10 @@ __device__ __forceinline__ int32_t map_col(int64_t g, int64_t own_begin, int64_t
 // (8 B x 32 d value slots beat 12 B x 32 w value+column slots).
 __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_t* __restrict__ rowptr,
                                   const int64_t* __restrict__ colg, int64_t own_begin, int64_t n_own, int allow_dia,
-                                  int max_dia, const uint8_t* __restrict__ perm, int64_t* __restrict__ vslots,
-                                  int64_t* __restrict__ cslots, int64_t* __restrict__ snnz, int32_t* __restrict__ bflag,
-                                  int32_t* __restrict__ dia_d, int32_t* __restrict__ dia_off) {
+                                  int max_dia, int allow16, const uint8_t* __restrict__ perm,
+                                  int64_t* __restrict__ vslots, int64_t* __restrict__ cslots,
+                                  int64_t* __restrict__ snnz, int32_t* __restrict__ bflag, int32_t* __restrict__ dia_d,
+                                  int32_t* __restrict__ dia_off, int32_t* __restrict__ e16) {
   const int lane = threadIdx.x & 31;
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= n_slices) return;
@@ -1910,10 +1939,26 @@ __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_
     }
     if (!ok || 2 * d > 3 * w) d = 0;
   }
+  // ELL slice of owned columns spanning < 2^16: uint16 offsets from the smallest
+  int base = -1;
+  if (allow16 && d == 0 && !off && w > 0) {
+    long long mn = LLONG_MAX, mx = LLONG_MIN;
+    for (int q = 0; q < len; ++q) {
+      const long long c = (long long)(colg[b + q] - own_begin);
+      mn = min(mn, c);
+      mx = max(mx, c);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (mx - mn < 65536) base = (int)mn;
+  }
   if (lane == 0) {
     vslots[s] = 32 * (int64_t)(d ? d : w);
-    // DIA: offsets, padded to 16 B; ELL: int32 columns
-    cslots[s] = d ? (int64_t)((d + 3) & ~3) : 32 * (int64_t)w;
+    // DIA: offsets, padded to 16 B; ELL: int32 columns; ELL16: uint16 columns
+    cslots[s] = d ? (int64_t)((d + 3) & ~3) : (base >= 0 ? 16 * (int64_t)w : 32 * (int64_t)w);
+    e16[s] = base;
     snnz[s] = tot;
     bflag[s] = off;
     dia_d[s] = d;
@@ -1926,7 +1971,7 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
                                  const int64_t* __restrict__ colg, const double* __restrict__ valcsr,
                                  const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
                                  const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
-                                 int64_t own_begin, int64_t n_own,
+                                 const int32_t* __restrict__ e16, int64_t own_begin, int64_t n_own,
                                  const int64_t* __restrict__ halo, int64_t nh, const uint8_t* __restrict__ perm,
                                  int32_t* __restrict__ col, double* __restrict__ val, int64_t* __restrict__ slot,
                                  int* err) {
@@ -1959,6 +2004,25 @@ __global__ void sell_fill_kernel(int64_t n_rows, int64_t n_slices, const int64_t
     if (lane == 0)
       for (int j = d; j < ((d + 3) & ~3); ++j) col[cb + j] = 0;
     if (q != e) *err = 2;
+    return;
+  }
+  const int32_t base = e16[s];
+  if (base >= 0) {  // kEll16 (every column owned: col - own_begin - base in [0, 2^16))
+    uint16_t* c16 = reinterpret_cast<uint16_t*>(col + cb);
+    uint16_t last = 0;
+    for (int k = 0; k < w; ++k) {
+      const int64_t o = 32 * (int64_t)k + lane;
+      if (b + k < e) {
+        const int64_t c = colg[b + k] - own_begin - base;
+        if (c < 0 || c > 65535) *err = 1;
+        last = (uint16_t)c;
+        val[vb + o] = valcsr[b + k];
+        if (slot) slot[b + k] = vb + o;
+      } else {
+        val[vb + o] = 0.0;
+      }
+      c16[o] = last;
+    }
     return;
   }
   int32_t last = 0;
@@ -2064,7 +2128,7 @@ int choose_lanes(int64_t n_rows, int64_t nnz) {
 
 __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ ptr, const int64_t* __restrict__ cptr,
                                 const int32_t* __restrict__ dia_d, const int32_t* __restrict__ dia_off,
-                                int32_t* __restrict__ hdr) {
+                                const int32_t* __restrict__ e16, int32_t* __restrict__ hdr) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_slices) return;
   int32_t* h = hdr + s * kHdr;
@@ -2082,6 +2146,10 @@ __global__ void sell_hdr_kernel(int64_t n_slices, const int64_t* __restrict__ pt
     if (dia_off[s * kMaxDia + j] == 0) j0 = j;
   h[14] = j0;  // DIA: slot of the diagonal (offset 0), -1 if none
   h[15] = 0;
+  if (d == 0 && e16[s] >= 0) {
+    h[5] = kEll16;
+    h[6] = e16[s];  // base column
+  }
 }
 
 void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const int64_t* d_colg, const double* d_val,
@@ -2113,6 +2181,9 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     int32_t* d_flag = dalloc<int32_t>(nu);
     int32_t* d_diad = dalloc<int32_t>(nu);
     int32_t* d_diaoff = dalloc<int32_t>((size_t)nu * kMaxDia);
+    int32_t* d_e16 = dalloc<int32_t>(nu);
+    // ELL slices with 16-bit column offsets (PSC_COL16=0: 32-bit columns everywhere)
+    const int allow16 = env_int("PSC_COL16", 1) ? 1 : 0;
     // DIA slices with up to 8 diagonals (offsets in the slice header; A_0).  Wider DIA
     // slices (up to kMaxDia, offsets in the column region) are opt-in, PSC_DIA_MAX=64:
     // on the level-1 Galerkin operator of 256^3 they measured slower (175 vs 154 us per
@@ -2123,8 +2194,8 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
       PSC_CUDA(cudaMemsetAsync(d_cs, 0, sizeof(int64_t) * (nu + 1), s));
       if (nu > 0) {
         sell_width_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
-            n_rows, nu, d_rowptr, d_colg, own_begin, n_own, dia ? 1 : 0, max_dia, perm, d_vs, d_cs, d_snnz, d_flag,
-            d_diad, d_diaoff);
+            n_rows, nu, d_rowptr, d_colg, own_begin, n_own, dia ? 1 : 0, max_dia, allow16, perm, d_vs, d_cs, d_snnz,
+            d_flag, d_diad, d_diaoff, d_e16);
         PSC_CUDA(cudaGetLastError());
       }
       if (!S.ptr) S.ptr = dalloc<int64_t>(nu + 1);
@@ -2162,10 +2233,11 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     S.hdr = dalloc<int32_t>((size_t)nu * kHdr);
     if (nu > 0) {
       sell_fill_kernel<<<(unsigned)((nu * 32 + 255) / 256), 256, 0, s>>>(
-          n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, own_begin, n_own, d_halo,
+          n_rows, nu, d_rowptr, d_colg, d_val, S.ptr, S.cptr, d_diad, d_diaoff, d_e16, own_begin, n_own, d_halo,
           n_halo, S.perm, S.col, S.val, S.slot, d_err);
       PSC_CUDA(cudaGetLastError());
-      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, S.hdr);
+      sell_hdr_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, s>>>(nu, S.ptr, S.cptr, d_diad, d_diaoff, d_e16,
+                                                                     S.hdr);
       PSC_CUDA(cudaGetLastError());
     }
     flag.resize(nu);
@@ -2181,6 +2253,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     dfree(d_flag);
     dfree(d_diad);
     dfree(d_diaoff);
+    dfree(d_e16);
   } else {
     int64_t* d_len = dalloc<int64_t>(nptr);
     int32_t* d_flag = dalloc<int32_t>(n_rows);

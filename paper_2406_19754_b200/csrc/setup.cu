@@ -14,7 +14,7 @@
 // roots equal those of the sequential sweep in increasing index.
 //
 // Every floating-point result is computed in the order the definitions state (row
-// sums in column order, the Galerkin loop i -> k -> K) with one rounding per
+// sums in column order, the Galerkin products k -> K row by row) with one rounding per
 // operation and no FMA contraction (__dmul_rn / __dadd_rn), so the set-up is
 // reproducible bit for bit by a plain sequential implementation.  One rank.
 #include <cub/cub.cuh>
@@ -279,78 +279,6 @@ __device__ __forceinline__ uint32_t hslot(int64_t K, uint32_t mask) {
   return (uint32_t)(((uint64_t)K * 0x9E3779B97F4A7C15ull) >> 32) & mask;
 }
 
-// Row J of A_c = R A P, accumulated exactly in the definition's loop order (i, then k,
-// then K increasing; acc = acc + (r a) p, no FMA) in a per-thread open-addressing
-// table (keys/vals, T = mask + 1 slots, key -1 = empty) plus the list of touched keys
-// in insertion order.  Count pass (cptr == nullptr): cnt[J] = distinct K, or -1 when
-// the row does not fit 3/4 of the table (then it is redone with a larger table).
-// Fill pass: the row's (K, acc) sorted by K into the output.  rows: the rows to do
-// (nullptr: all R.n); rows whose cnt is -1 are skipped by the fill pass.
-__global__ void rap_kernel(DCsr R, DCsr A, DCsr P, uint32_t mask, int64_t* __restrict__ keys,
-                           double* __restrict__ vals, int64_t* __restrict__ touched, int64_t* __restrict__ cnt,
-                           const int64_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ cptr,
-                           int64_t* __restrict__ ccol, double* __restrict__ cval) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t T = (int64_t)mask + 1;
-  const int64_t cap = T - T / 4;
-  int64_t* key = keys + tid * T;
-  double* acc = vals + tid * T;
-  int64_t* tl = touched + tid * T;
-  for (int64_t q = tid; q < nrows; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t J = rows ? rows[q] : q;
-    if (cptr && cnt[J] < 0) continue;
-    int64_t nt = 0;
-    bool over = false;
-    for (int64_t a = R.ptr[J]; a < R.ptr[J + 1] && !over; ++a) {
-      const int64_t i = R.col[a];
-      const double rv = R.val[a];
-      for (int64_t b = A.ptr[i]; b < A.ptr[i + 1]; ++b) {
-        const int64_t k = A.col[b];
-        const double ra = __dmul_rn(rv, A.val[b]);
-        for (int64_t c = P.ptr[k]; c < P.ptr[k + 1]; ++c) {
-          const int64_t K = P.col[c];
-          uint32_t h = hslot(K, mask);
-          while (key[h] != -1 && key[h] != K) h = (h + 1) & mask;
-          if (key[h] == -1) {
-            if (nt == cap) {
-              over = true;
-              break;
-            }
-            key[h] = K;
-            acc[h] = 0.0;
-            tl[nt++] = h;
-          }
-          acc[h] = __dadd_rn(acc[h], __dmul_rn(ra, P.val[c]));
-        }
-        if (over) break;
-      }
-    }
-    if (!cptr) {
-      cnt[J] = over ? -1 : nt;
-    } else {
-      const int64_t q0 = cptr[J];
-      for (int64_t x = 0; x < nt; ++x) {  // insertion by increasing K
-        const int64_t K = key[tl[x]];
-        const double v = acc[tl[x]];
-        int64_t y = q0 + x - 1;
-        while (y >= q0 && ccol[y] > K) {
-          ccol[y + 1] = ccol[y];
-          cval[y + 1] = cval[y];
-          --y;
-        }
-        ccol[y + 1] = K;
-        cval[y + 1] = v;
-      }
-    }
-    for (int64_t x = 0; x < nt; ++x) key[tl[x]] = -1;
-  }
-}
-
-__global__ void fill_i64_kernel(int64_t n, int64_t* __restrict__ p, int64_t v) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
-}
-
 __global__ void mark_kernel(int64_t n, const int64_t* __restrict__ rows, int64_t* __restrict__ cnt) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) cnt[rows[q]] = -1;
@@ -501,57 +429,63 @@ DCsr transpose(psc_ctx* ctx, const DCsr& P) {
   return R;
 }
 
-// rap_kernel with the per-thread tables in shared memory (kSmallT slots, 32-bit keys:
-// K < 2^31 on one rank), interleaved [slot][thread] so the threads of a warp hitting
-// the same slot index fall in different banks.  Same semantics as rap_kernel.
+// ------------------------------------------------------------ sparse products
+// Z = X Y row by row (Gustavson), every Z[i, K] accumulated exactly in the order of
+// the definition (k along X's row i, then K along Y's row k; acc = acc + x y with one
+// rounding per operation, no FMA), so the result is bit-identical to a sequential
+// implementation.  A row is first tried in a small per-thread table; the rows that do
+// not fit go to one warp per row with a larger table (shared, then global memory).
+// Every stage has a count pass (cnt[i] = distinct K, or -1: redo at the next stage)
+// and a fill pass (columns increasing) over the rows it holds.
+
+// stage 0: thread per row, kSmallT-slot open-addressing table in shared memory (32-bit
+// keys: K < 2^31 on one rank), interleaved [slot][thread] so that the threads of a warp
+// probing the same slot index hit different banks
 constexpr int kSmallT = 64;
-constexpr int kRapThreads = 128;
-constexpr int kRapSmem = kRapThreads * kSmallT * (4 + 8 + 1);
-__global__ void __launch_bounds__(kRapThreads) rap_smem_kernel(DCsr R, DCsr A, DCsr P, int64_t* __restrict__ cnt,
-                                                               const int64_t* __restrict__ cptr,
-                                                               int64_t* __restrict__ ccol, double* __restrict__ cval) {
+constexpr int kProdThreads = 128;
+constexpr int kProdSmem = kProdThreads * kSmallT * (4 + 8 + 1);
+__global__ void __launch_bounds__(kProdThreads) prod_thread_kernel(DCsr X, DCsr Y, int64_t* __restrict__ cnt,
+                                                                   const int64_t* __restrict__ cptr,
+                                                                   int64_t* __restrict__ ccol,
+                                                                   double* __restrict__ cval) {
   extern __shared__ __align__(16) unsigned char sm[];
   double* acc = reinterpret_cast<double*>(sm);
-  int32_t* key = reinterpret_cast<int32_t*>(sm + kRapThreads * kSmallT * 8);
-  uint8_t* tl = sm + kRapThreads * kSmallT * 12;
+  int32_t* key = reinterpret_cast<int32_t*>(sm + kProdThreads * kSmallT * 8);
+  uint8_t* tl = sm + kProdThreads * kSmallT * 12;
   const int t = threadIdx.x;
   constexpr int cap = kSmallT - kSmallT / 4;
-  for (int h = 0; h < kSmallT; ++h) key[h * kRapThreads + t] = -1;
-  for (int64_t J = (int64_t)blockIdx.x * blockDim.x + t; J < R.n; J += (int64_t)gridDim.x * blockDim.x) {
-    if (cptr && cnt[J] < 0) continue;
+  for (int h = 0; h < kSmallT; ++h) key[h * kProdThreads + t] = -1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + t; i < X.n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (cptr && cnt[i] < 0) continue;
     int nt = 0;
     bool over = false;
-    for (int64_t a = R.ptr[J]; a < R.ptr[J + 1] && !over; ++a) {
-      const int64_t i = R.col[a];
-      const double rv = R.val[a];
-      for (int64_t b = A.ptr[i]; b < A.ptr[i + 1] && !over; ++b) {
-        const int64_t k = A.col[b];
-        const double ra = __dmul_rn(rv, A.val[b]);
-        for (int64_t c = P.ptr[k]; c < P.ptr[k + 1]; ++c) {
-          const int32_t K = (int32_t)P.col[c];
-          uint32_t h = hslot(K, kSmallT - 1);
-          while (key[h * kRapThreads + t] != -1 && key[h * kRapThreads + t] != K) h = (h + 1) & (kSmallT - 1);
-          const int s = h * kRapThreads + t;
-          if (key[s] == -1) {
-            if (nt == cap) {
-              over = true;
-              break;
-            }
-            key[s] = K;
-            acc[s] = 0.0;
-            tl[nt * kRapThreads + t] = (uint8_t)h;
-            ++nt;
+    for (int64_t b = X.ptr[i]; b < X.ptr[i + 1] && !over; ++b) {
+      const int64_t k = X.col[b];
+      const double xv = X.val[b];
+      for (int64_t c = Y.ptr[k]; c < Y.ptr[k + 1]; ++c) {
+        const int32_t K = (int32_t)Y.col[c];
+        uint32_t h = hslot(K, kSmallT - 1);
+        while (key[h * kProdThreads + t] != -1 && key[h * kProdThreads + t] != K) h = (h + 1) & (kSmallT - 1);
+        const int s = h * kProdThreads + t;
+        if (key[s] == -1) {
+          if (nt == cap) {
+            over = true;
+            break;
           }
-          acc[s] = __dadd_rn(acc[s], __dmul_rn(ra, P.val[c]));
+          key[s] = K;
+          acc[s] = 0.0;
+          tl[nt * kProdThreads + t] = (uint8_t)h;
+          ++nt;
         }
+        acc[s] = __dadd_rn(acc[s], __dmul_rn(xv, Y.val[c]));
       }
     }
     if (!cptr) {
-      cnt[J] = over ? -1 : nt;
+      cnt[i] = over ? -1 : nt;
     } else {
-      const int64_t q0 = cptr[J];
+      const int64_t q0 = cptr[i];
       for (int x = 0; x < nt; ++x) {  // insertion by increasing K
-        const int s = tl[x * kRapThreads + t] * kRapThreads + t;
+        const int s = tl[x * kProdThreads + t] * kProdThreads + t;
         const int64_t K = key[s];
         const double v = acc[s];
         int64_t y = q0 + x - 1;
@@ -564,114 +498,238 @@ __global__ void __launch_bounds__(kRapThreads) rap_smem_kernel(DCsr R, DCsr A, D
         cval[y + 1] = v;
       }
     }
-    for (int x = 0; x < nt; ++x) key[tl[x * kRapThreads + t] * kRapThreads + t] = -1;
+    for (int x = 0; x < nt; ++x) key[tl[x * kProdThreads + t] * kProdThreads + t] = -1;
   }
 }
 
-void rap_smem_launch(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P, int64_t* cnt, const int64_t* cptr,
-                     int64_t* ccol, double* cval, cudaStream_t s) {
+// stages >= 1: one warp per row.  The warp walks X's row i in order and spreads each
+// Y row k over its lanes: the K of one Y row are distinct, so every acc[K] still
+// receives its terms in the sequential order.  The table (T slots, keys / values,
+// plus the compaction list used by the fill pass) is in shared memory (T = kWT) or in
+// a per-warp slice of global memory (larger T).
+constexpr int kWT = 1024;
+constexpr int kWCap = 768;
+constexpr int kProdWarps = 4;
+constexpr int kProdWarpSmem = kProdWarps * kWT * (4 + 8 + 4 + 8);
+struct WarpTab {
+  int32_t* key;
+  double* val;
+  int32_t* lk;
+  double* lv;
+};
+__global__ void __launch_bounds__(kProdWarps * 32) prod_warp_kernel(DCsr X, DCsr Y, int64_t* __restrict__ cnt,
+                                                                    const int64_t* __restrict__ rows, int64_t nrows,
+                                                                    int T, int wcap, unsigned char* gtab,
+                                                                    const int64_t* __restrict__ cptr,
+                                                                    int64_t* __restrict__ ccol,
+                                                                    double* __restrict__ cval) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int tcnt[kProdWarps];
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kProdWarps + wi;
+  unsigned char* base = gtab ? gtab + (size_t)gw * T * 24 : sm + (size_t)wi * T * 24;
+  WarpTab tb{reinterpret_cast<int32_t*>(base), reinterpret_cast<double*>(base + (size_t)T * 4),
+             reinterpret_cast<int32_t*>(base + (size_t)T * 12), reinterpret_cast<double*>(base + (size_t)T * 16)};
+  volatile int32_t* vkey = tb.key;
+  volatile int* vcnt = &tcnt[wi];
+  const uint32_t mask = (uint32_t)T - 1;
+  for (int h = lane; h < T; h += 32) tb.key[h] = -1;
+  if (lane == 0) tcnt[wi] = 0;
+  __syncwarp();
+  const int64_t nw = (int64_t)gridDim.x * kProdWarps;
+  for (int64_t q = gw; q < nrows; q += nw) {
+    const int64_t i = rows ? rows[q] : q;
+    if (cptr && cnt[i] < 0) continue;
+    bool over = false;
+    const int64_t b1 = X.ptr[i + 1];
+    for (int64_t bb = X.ptr[i]; bb < b1 && !over; bb += 32) {
+      // lane j holds (x, Y row range) of entry bb + j of X's row
+      int64_t pb = 0, pe = 0;
+      double xl = 0.0;
+      if (bb + lane < b1) {
+        const int64_t k = X.col[bb + lane];
+        xl = X.val[bb + lane];
+        pb = Y.ptr[k];
+        pe = Y.ptr[k + 1];
+      }
+      const int np = (int)(b1 - bb < 32 ? b1 - bb : 32);
+      for (int j = 0; j < np && !over; ++j) {
+        const int64_t cb = __shfl_sync(kFull, pb, j);
+        const int64_t ce = __shfl_sync(kFull, pe, j);
+        const double xv = __shfl_sync(kFull, xl, j);
+        for (int64_t c0 = cb; c0 < ce; c0 += 32) {
+          const int64_t c = c0 + lane;
+          if (c < ce) {
+            const int32_t K = (int32_t)Y.col[c];
+            const double v = __dmul_rn(xv, Y.val[c]);
+            uint32_t h = hslot(K, mask);
+            for (;;) {
+              int32_t cur = vkey[h];
+              if (cur == -1) {
+                cur = atomicCAS(&tb.key[h], -1, K);
+                if (cur == -1) {
+                  atomicAdd(&tcnt[wi], 1);
+                  tb.val[h] = 0.0;
+                  break;
+                }
+              }
+              if (cur == K) break;
+              h = (h + 1) & mask;
+            }
+            tb.val[h] = __dadd_rn(tb.val[h], v);
+          }
+          __syncwarp();
+          // at most 32 inserts per step: a table past wcap (<= 3/4 T) still has room
+          if (*vcnt > wcap) {
+            over = true;
+            break;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (!cptr) {
+      if (lane == 0) cnt[i] = over ? -1 : *vcnt;
+    } else {
+      // compact the occupied slots, then place each by its rank among the keys
+      int nt = 0;
+      for (int b = 0; b < T; b += 32) {
+        const int32_t K = tb.key[b + lane];
+        const unsigned m = __ballot_sync(kFull, K != -1);
+        if (K != -1) {
+          const int pos = nt + __popc(m & ((1u << lane) - 1u));
+          tb.lk[pos] = K;
+          tb.lv[pos] = tb.val[b + lane];
+        }
+        nt += __popc(m);
+      }
+      __syncwarp();
+      const int64_t q0 = cptr[i];
+      for (int x = lane; x < nt; x += 32) {
+        const int32_t K = tb.lk[x];
+        int rank = 0;
+        for (int y = 0; y < nt; ++y) rank += tb.lk[y] < K;
+        ccol[q0 + rank] = K;
+        cval[q0 + rank] = tb.lv[x];
+      }
+    }
+    __syncwarp();
+    for (int h = lane; h < T; h += 32) tb.key[h] = -1;
+    if (lane == 0) tcnt[wi] = 0;
+    __syncwarp();
+  }
+}
+
+// one escalation stage of the warp kernel: table size, the rows it holds, and (global
+// stages) the per-warp tables
+struct ProdStage {
+  int T = 0;
+  int64_t* rows = nullptr;
+  int64_t nrows = 0;
+  unsigned char* gtab = nullptr;
+  unsigned grid = 1;
+};
+
+// PSC_RAP_WCAP lowers the shared-memory warp stage's row capacity (tests: reach the
+// global stages on small problems)
+int warp_cap() {
+  const char* e = getenv("PSC_RAP_WCAP");
+  const int v = e ? atoi(e) : kWCap;
+  return v >= 1 && v <= kWCap ? v : kWCap;
+}
+
+void prod_thread_launch(psc_ctx* ctx, const DCsr& X, const DCsr& Y, int64_t* cnt, const int64_t* cptr,
+                        int64_t* ccol, double* cval, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    PSC_CUDA(cudaFuncSetAttribute(rap_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRapSmem));
+    PSC_CUDA(cudaFuncSetAttribute(prod_thread_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kProdSmem));
     attr = true;
   }
-  const int64_t need = (R.n + kRapThreads - 1) / kRapThreads;
+  const int64_t need = (X.n + kProdThreads - 1) / kProdThreads;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * 2));
-  rap_smem_kernel<<<grid, kRapThreads, kRapSmem, s>>>(R, A, P, cnt, cptr, ccol, cval);
+  prod_thread_kernel<<<grid, kProdThreads, kProdSmem, s>>>(X, Y, cnt, cptr, ccol, cval);
   PSC_CUDA(cudaGetLastError());
 }
 
-// per-thread tables for rap_kernel: T slots (3 words each) for nth threads
-struct RapTables {
-  int64_t T = 0, nth = 0;
-  int64_t* keys = nullptr;
-  double* vals = nullptr;
-  int64_t* tl = nullptr;
-  RapTables(psc_ctx* ctx, int64_t T_, int64_t rows, cudaStream_t s) : T(T_) {
-    // as many threads as fit ~1.5 GB of tables, at most 2048 per SM and one per row
-    nth = std::min<int64_t>(((int64_t)3 << 29) / (24 * T), (int64_t)ctx->num_sms * 2048);
-    nth = std::min<int64_t>(nth, ((rows + kT - 1) / kT) * kT);
-    nth = std::max<int64_t>(kT, (nth / kT) * kT);
-    keys = dalloc<int64_t>(nth * T);
-    vals = dalloc<double>(nth * T);
-    tl = dalloc<int64_t>(nth * T);
-    fill_i64_kernel<<<blocks(nth * T), kT, 0, s>>>(nth * T, keys, -1);
+void prod_warp_launch(const DCsr& X, const DCsr& Y, int64_t* cnt, const ProdStage& st, const int64_t* cptr,
+                      int64_t* ccol, double* cval, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PSC_CUDA(cudaFuncSetAttribute(prod_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kProdWarpSmem));
+    attr = true;
   }
-  ~RapTables() {
-    dfree(keys);
-    dfree(vals);
-    dfree(tl);
-  }
-  unsigned grid() const { return (unsigned)(nth / kT); }
-};
+  const int wcap = st.gtab ? st.T - st.T / 4 : warp_cap();
+  prod_warp_kernel<<<st.grid, kProdWarps * 32, st.gtab ? 0 : kProdWarpSmem, s>>>(X, Y, cnt, st.rows, st.nrows, st.T,
+                                                                                wcap, st.gtab, cptr, ccol, cval);
+  PSC_CUDA(cudaGetLastError());
+}
 
-// Galerkin A_c = R A P.  Every row first with small shared-memory tables (64 slots:
-// the rows of the level-1 operator of a 7-point problem have <= ~50 entries); the rows
-// that do not fit are redone with global-memory tables of 512, 4096, ... slots (the
-// product count is a poor bound on a row's distinct columns: ~35,000 products for
-// ~120 columns on level 2 of 256^3).
-DCsr galerkin(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P) {
-  NvtxRange nv("psc_amg_galerkin");
+// Z = X Y (X.n rows, Y.ncols columns, columns increasing per row)
+DCsr spgemm(psc_ctx* ctx, const DCsr& X, const DCsr& Y) {
   cudaStream_t s = ctx->stream;
-  const int64_t nc = R.n;
-  PSC_REQUIRE(P.ncols < INT32_MAX, PSC_ERR_STATE, "Galerkin: more than 2^31 coarse columns");
-  int64_t* cnt = dalloc<int64_t>(nc);
-  rap_smem_launch(ctx, R, A, P, cnt, nullptr, nullptr, nullptr, s);
-  // escalation stages: rows still at cnt < 0 after a stage go to the next one
-  struct Stage {
-    std::unique_ptr<RapTables> tab;
-    int64_t* rows = nullptr;
-    int64_t nrows = 0;
-  };
-  std::vector<Stage> stages;
-  std::vector<int64_t> hc(nc);
-  int64_t T = 512;
+  const int64_t n = X.n;
+  PSC_REQUIRE(Y.ncols < INT32_MAX, PSC_ERR_STATE, "sparse product: more than 2^31 columns");
+  int64_t* cnt = dalloc<int64_t>(std::max<int64_t>(n, 1));
+  prod_thread_launch(ctx, X, Y, cnt, nullptr, nullptr, nullptr, s);
+  std::vector<ProdStage> stages;
+  std::vector<int64_t> hc(n);
   for (;;) {
-    PSC_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int64_t) * nc, cudaMemcpyDeviceToHost, s));
+    if (n) PSC_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
     PSC_CUDA(cudaStreamSynchronize(s));
     std::vector<int64_t> big;
-    for (int64_t J = 0; J < nc; ++J)
-      if (hc[J] < 0) big.push_back(J);
+    for (int64_t i = 0; i < n; ++i)
+      if (hc[i] < 0) big.push_back(i);
     if (big.empty()) break;
-    PSC_REQUIRE(T <= ((int64_t)1 << 31), PSC_ERR_STATE, "Galerkin: row too long");
-    Stage st;
+    ProdStage st;
+    st.T = stages.empty() ? kWT : (stages.size() == 1 ? 8192 : stages.back().T * 8);
+    PSC_REQUIRE(st.T <= (1 << 30) && st.T <= 4 * Y.ncols + 8192, PSC_ERR_STATE, "sparse product: row too long");
     st.nrows = (int64_t)big.size();
     st.rows = dalloc<int64_t>(big.size());
     PSC_CUDA(cudaMemcpyAsync(st.rows, big.data(), sizeof(int64_t) * big.size(), cudaMemcpyHostToDevice, s));
-    st.tab.reset(new RapTables(ctx, T, st.nrows, s));
-    rap_kernel<<<st.tab->grid(), kT, 0, s>>>(R, A, P, (uint32_t)(T - 1), st.tab->keys, st.tab->vals, st.tab->tl,
-                                             cnt, st.rows, st.nrows, nullptr, nullptr, nullptr);
-    PSC_CUDA(cudaGetLastError());
-    stages.push_back(std::move(st));
-    T *= 8;
+    int64_t nwarps = std::min<int64_t>(st.nrows, (int64_t)ctx->num_sms * 16);
+    if (!stages.empty()) {  // global tables: at most ~1.5 GB of them
+      nwarps = std::min<int64_t>(nwarps, std::max<int64_t>(kProdWarps, ((int64_t)3 << 29) / (24 * (int64_t)st.T)));
+      nwarps = (nwarps + kProdWarps - 1) / kProdWarps * kProdWarps;
+      st.gtab = dalloc<unsigned char>((size_t)nwarps * st.T * 24);  // keys cleared by the kernel
+    }
+    st.grid = (unsigned)std::max<int64_t>(1, (nwarps + kProdWarps - 1) / kProdWarps);
+    prod_warp_launch(X, Y, cnt, st, nullptr, nullptr, nullptr, s);
+    stages.push_back(st);
   }
-  DCsr C;
-  C.n = nc;
-  C.ncols = P.ncols;
-  C.ptr = dalloc<int64_t>(nc + 1);
-  C.nnz = scan(cnt, C.ptr, nc, s);
-  C.col = dalloc<int64_t>(C.nnz);
-  C.val = dalloc<double>(C.nnz);
+  DCsr Z;
+  Z.n = n;
+  Z.ncols = Y.ncols;
+  Z.ptr = dalloc<int64_t>(n + 1);
+  Z.nnz = scan(cnt, Z.ptr, n, s);
+  Z.col = dalloc<int64_t>(std::max<int64_t>(Z.nnz, 1));
+  Z.val = dalloc<double>(std::max<int64_t>(Z.nnz, 1));
   // fill: each row by the stage whose table held it (the others skip it: cnt < 0)
   for (size_t q = 0; q <= stages.size(); ++q) {
     // rows escalated past stage q (the lists are nested, so marking every later list
     // marks exactly them) are skipped; stage q does the rest of its rows
-    PSC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * nc, s));
+    PSC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * n, s));
     for (size_t r = q; r < stages.size(); ++r)
       mark_kernel<<<blocks(stages[r].nrows), kT, 0, s>>>(stages[r].nrows, stages[r].rows, cnt);
-    if (q == 0) {
-      rap_smem_launch(ctx, R, A, P, cnt, C.ptr, C.col, C.val, s);
-    } else {
-      const Stage& st = stages[q - 1];
-      rap_kernel<<<st.tab->grid(), kT, 0, s>>>(R, A, P, (uint32_t)(st.tab->T - 1), st.tab->keys, st.tab->vals,
-                                               st.tab->tl, cnt, st.rows, st.nrows, C.ptr, C.col, C.val);
-    }
+    if (q == 0) prod_thread_launch(ctx, X, Y, cnt, Z.ptr, Z.col, Z.val, s);
+    else prod_warp_launch(X, Y, cnt, stages[q - 1], Z.ptr, Z.col, Z.val, s);
     PSC_CUDA(cudaGetLastError());
   }
   PSC_CUDA(cudaStreamSynchronize(s));
-  for (auto& st : stages) dfree(st.rows);
-  stages.clear();
+  for (auto& st : stages) {
+    dfree(st.rows);
+    dfree(st.gtab);
+  }
   dfree(cnt);
+  return Z;
+}
+
+// Galerkin A_c = R A P, reading R31: R (A P), two sparse products.
+DCsr galerkin(psc_ctx* ctx, const DCsr& R, const DCsr& A, const DCsr& P) {
+  NvtxRange nv("psc_amg_galerkin");
+  DCsr AP = spgemm(ctx, A, P);
+  DCsr C = spgemm(ctx, R, AP);
+  dcsr_free(AP);
   return C;
 }
 

@@ -518,20 +518,25 @@ struct SpGEMMRow {
   }
 };
 
-// Direct Galerkin rows: A_c[J,:] = sum_i R[J,i] sum_k A[i,k] P[k,:] (cheapest when
-// A is a short-row stencil: no intermediate AP).
+// Galerkin rows A_c[J,:] = sum_i R[J,i] (AP)[i,:] with (AP)[i,:] = sum_k A[i,k] P[k,:]
+// (the association R (A P) of SpGEMMRow, bit for bit: each (AP)[i,K] is summed in k
+// order, then added to A_c[J,K] in i order) without storing AP: row i of AP is
+// recomputed for every J that needs it (the stencil-like fine levels, where AP would
+// be as large as A times the prolongator's row length).
 struct RAPRow {
   const CSR *R, *A, *P;
   int64_t nc;
   struct State {
-    std::vector<double> acc;
-    std::vector<int64_t> mark;
-    std::vector<int64_t> touched;
+    std::vector<double> acc, acc2;
+    std::vector<int64_t> mark, mark2;
+    std::vector<int64_t> touched, touched2;
   };
   State make_state() const {
     State s;
     s.acc.assign(nc, 0.0);
     s.mark.assign(nc, -1);
+    s.acc2.assign(nc, 0.0);
+    s.mark2.assign(nc, -1);
     return s;
   }
   void operator()(State& s, int64_t J, std::vector<int64_t>& col, std::vector<double>& val) const {
@@ -539,14 +544,20 @@ struct RAPRow {
     for (int64_t a = R->ptr[J]; a < R->ptr[J + 1]; ++a) {
       const int64_t i = R->col[a];
       const double rv = R->val[a];
+      // row i of AP (mark2 keyed by the R entry a: unique per (J, i))
+      s.touched2.clear();
       for (int64_t b = A->ptr[i]; b < A->ptr[i + 1]; ++b) {
         const int64_t k = A->col[b];
-        const double ra = rv * A->val[b];
+        const double av = A->val[b];
         for (int64_t c = P->ptr[k]; c < P->ptr[k + 1]; ++c) {
           const int64_t K = P->col[c];
-          if (s.mark[K] != J) { s.mark[K] = J; s.acc[K] = 0.0; s.touched.push_back(K); }
-          s.acc[K] += ra * P->val[c];
+          if (s.mark2[K] != a) { s.mark2[K] = a; s.acc2[K] = 0.0; s.touched2.push_back(K); }
+          s.acc2[K] += av * P->val[c];
         }
+      }
+      for (int64_t K : s.touched2) {
+        if (s.mark[K] != J) { s.mark[K] = J; s.acc[K] = 0.0; s.touched.push_back(K); }
+        s.acc[K] += rv * s.acc2[K];
       }
     }
     std::sort(s.touched.begin(), s.touched.end());
@@ -645,7 +656,7 @@ void build_levels(Hier* h, const Params& prm) {
       NL.w.assign(nc, 0.0);
       for (int64_t i = 0; i < L.n; ++i) NL.w[L.agg[i]] += L.ph[i] * L.w[i];
     }
-    if (L.A.nnz() <= 8 * L.n) {  // stencil-like A: direct triple product
+    if (L.A.nnz() <= 8 * L.n) {  // stencil-like A: AP rows recomputed, not stored
       RAPRow rrow{&L.R, &L.A, &L.P, nc};
       build_csr_chunked(NL.A, nc, nc, rrow);
     } else {  // denser A: AP first, then R (AP)

@@ -76,6 +76,36 @@ def test_spmv_all_level_matrices(psc, grid):
             assert np.all(err <= tol), (name, l, float((err / tol).max()))
 
 
+@pytest.mark.parametrize("env", [{}, {"PSC_NO_DIA": "1"}, {"PSC_NO_DIA": "1", "PSC_NO_TMA": "1"},
+                                 {"PSC_COL16": "0", "PSC_NO_DIA": "1"}], ids=["default", "ell", "ell-notma", "col32"])
+def test_spmv_mixed_column_spans(psc, env, monkeypatch):
+    """Slices whose columns span less than 2^16 store 16-bit column offsets (kEll16),
+    the others 32-bit columns: a tridiagonal matrix plus far couplings every 97th row
+    (span ~10^5) mixes both kinds; SpMV and the l1 diagonal against the oracle."""
+    import scipy.sparse as sp
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    n = 200_003
+    i = np.arange(0, n, 97)
+    j = (i + 100_003) % n
+    far = sp.coo_matrix((np.full(len(i), -0.25), (i, j)), shape=(n, n))
+    A = (sp.diags([-np.ones(n - 1), 4 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1]) + far + far.T).tocsr()
+    A.sum_duplicates()
+    A.sort_indices()
+    ctx = psc.Context()
+    d = psc.Descriptor(ctx, n, [0, n])
+    M = psc.Matrix(ctx, d, d, A.indptr, A.indices, A.data)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(n)
+    y = dev(np.zeros(n))
+    M.spmv(dev(x), y)
+    h = pscgen.csr_hierarchy(A, max_levels=1)
+    ref = oracle.spmv(h.levels[0].A, x)
+    err = np.abs(host(y) - ref)
+    assert np.all(err <= 1e-14 * (abs(A) @ np.abs(x)) + 1e-300)
+    ctx.close()
+
+
 def _check_layout(M, info):
     lens = np.diff(M.ptr)
     n = len(lens)
@@ -257,6 +287,8 @@ VARIANTS = [
     {"PSC_RG_SMALL_MB": "200"},
     {"PSC_DIA_MAX": "64"},
     {"PSC_NO_FUSED_SCALE": "1", "PSC_NO_DIA": "1", "PSC_NO_TMA": "1"},
+    {"PSC_COL16": "0"},
+    {"PSC_COL16": "0", "PSC_NO_DIA": "1", "PSC_NO_TMA": "1"},
 ]
 
 

@@ -68,6 +68,18 @@ def test_setup_bit_exact_vs_oracle(psc, name):
     ctx.close()
 
 
+@pytest.mark.parametrize("wcap", ["768", "24"])
+def test_setup_galerkin_stages(psc, wcap, monkeypatch):
+    """Every stage of the Galerkin products (per-thread shared tables, one warp per row
+    with a shared table, one warp per row with a global table) bit-exact:
+    PSC_RAP_WCAP=24 sends the rows with more than 24 columns past the shared warp
+    stage to the global tables."""
+    monkeypatch.setenv("PSC_RAP_WCAP", wcap)
+    for name in ("poisson16", "random_spd"):
+        H, ctx, S, info = _compare(psc, _A0(name))
+        ctx.close()
+
+
 @pytest.mark.parametrize("kw", [dict(theta=0.25), dict(max_levels=2), dict(coarse_target=1000), dict(stall_ratio=0.05)],
                          ids=["theta0.25", "2levels", "target1000", "stall"])
 def test_setup_options(psc, kw):
