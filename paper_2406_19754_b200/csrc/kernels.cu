@@ -1939,9 +1939,12 @@ __global__ void sell_width_kernel(int64_t n_rows, int64_t n_slices, const int64_
     }
     if (!ok || 2 * d > 3 * w) d = 0;
   }
-  // ELL slice of owned columns spanning < 2^16: uint16 offsets from the smallest
+  // ELL slice of at most kTmaMaxW columns, all owned, spanning < 2^16: uint16 offsets
+  // from the smallest.  (Wider slices keep int32 columns: on the level-1 operator of
+  // 256^3, ~31 per row, 16-bit offsets made the thread-per-row sweep slower, 166 vs
+  // 161 us, while P_0 in the TMA kernel gained 204 vs 215 us.)
   int base = -1;
-  if (allow16 && d == 0 && !off && w > 0) {
+  if (allow16 && d == 0 && !off && w > 0 && w <= kTmaMaxW) {
     long long mn = LLONG_MAX, mx = LLONG_MIN;
     for (int q = 0; q < len; ++q) {
       const long long c = (long long)(colg[b + q] - own_begin);

@@ -42,7 +42,13 @@ struct PushArgs {
   unsigned int* ticket;
   int R;
   uint64_t timeout_ns;  // bound of the wait for a peer's flag (then __trap: a launch error, not a hang)
+  int fence;            // 0: fence.sc.sys per CTA; 1: fence.acq_rel.sys (PSC_P2P_FENCE)
 };
+
+static __device__ __forceinline__ void fence_sys(int mode) {
+  if (mode == 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else __threadfence_system();
+}
 
 static __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -62,13 +68,13 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(PushArgs a) {
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    fence_sys(a.fence);
     const unsigned int t = atomicAdd(a.ticket, 1u);
     last = (t == gridDim.x * gridDim.y - 1);
   }
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
-  __threadfence_system();
+  fence_sys(a.fence);
   for (int q = 0; q < a.R; ++q)
     if (a.nbr[q]) st_release_sys(a.pflag[q], ++a.gen[q]);
   // wait until every neighbour has signalled as often as this rank has (the signal
@@ -101,9 +107,12 @@ static uint64_t spin_timeout_ns() {
 static void push(psc_ctx* ctx, P2P& P, const double* x, const int32_t* idx, const int64_t* soff, int64_t n,
                  int64_t max_per_peer, double* const* dst, const int32_t* nbr, cudaStream_t s) {
   const uint64_t tmo = spin_timeout_ns();
-  PushArgs a{x, idx, soff, n, dst, nbr, P.d_pflag, P.flags, P.d_gen, P.d_ticket, ctx->nranks, tmo};
+  static const int fence = getenv("PSC_P2P_FENCE") ? atoi(getenv("PSC_P2P_FENCE")) : 0;
+  static const int64_t bxmax = getenv("PSC_P2P_BX") ? std::max(1, atoi(getenv("PSC_P2P_BX"))) : 64;
+  static const int64_t per_cta = getenv("PSC_P2P_PER_CTA") ? std::max(32, atoi(getenv("PSC_P2P_PER_CTA"))) : 256;
+  PushArgs a{x, idx, soff, n, dst, nbr, P.d_pflag, P.flags, P.d_gen, P.d_ticket, ctx->nranks, tmo, fence};
   KtScope kts(ctx, s, idx ? "p2p_halo" : "p2p_allgather", 0.0, 0.0);
-  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((max_per_peer + 255) / 256, 64));
+  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((max_per_peer + per_cta - 1) / per_cta, bxmax));
   p2p_push_kernel<<<dim3((unsigned)bx, (unsigned)ctx->nranks), 256, 0, s>>>(a);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;

@@ -79,9 +79,9 @@ def test_spmv_all_level_matrices(psc, grid):
 @pytest.mark.parametrize("env", [{}, {"PSC_NO_DIA": "1"}, {"PSC_NO_DIA": "1", "PSC_NO_TMA": "1"},
                                  {"PSC_COL16": "0", "PSC_NO_DIA": "1"}], ids=["default", "ell", "ell-notma", "col32"])
 def test_spmv_mixed_column_spans(psc, env, monkeypatch):
-    """Slices whose columns span less than 2^16 store 16-bit column offsets (kEll16),
-    the others 32-bit columns: a tridiagonal matrix plus far couplings every 97th row
-    (span ~10^5) mixes both kinds; SpMV and the l1 diagonal against the oracle."""
+    """Slices of at most 8 columns whose columns span less than 2^16 store 16-bit column
+    offsets (kEll16), the others 32-bit columns: a tridiagonal matrix plus far couplings
+    every 97th row (span ~10^5) mixes both kinds; SpMV against the oracle."""
     import scipy.sparse as sp
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -95,6 +95,8 @@ def test_spmv_mixed_column_spans(psc, env, monkeypatch):
     ctx = psc.Context()
     d = psc.Descriptor(ctx, n, [0, n])
     M = psc.Matrix(ctx, d, d, A.indptr, A.indices, A.data)
+    d.assemble()
+    M.assemble()
     rng = np.random.default_rng(5)
     x = rng.standard_normal(n)
     y = dev(np.zeros(n))
