@@ -223,6 +223,8 @@ def _metric(args):
         var += ", coarsest PCG"
     if args.hierarchy != "vmb":
         var += f", {args.hierarchy.upper()} hierarchy"
+    if args.smoother == "ainv":
+        var += f", AINV({args.ainv_drop:g}) smoother"
     return f"AMG-{args.krylov.upper()} Mdof*iters/s (3D {args.problem}, {scope}, tol {args.tol:g}{var})"
 
 
@@ -236,8 +238,14 @@ def _oracle_solve(args):
 
 
 def _cycle_kw(args):
-    """Variable V-cycle (--variable-v, P:330 footnote): 2 sweeps at level 0, doubled per level."""
-    return dict(pre=2, post=2, variable_v=True) if args.variable_v else {}
+    """Variable V-cycle (--variable-v, P:330 footnote): 2 sweeps at level 0, doubled per
+    level.  --smoother ainv (NEXT-4): one AINV sweep per side, V(1,1)."""
+    kw = dict(pre=2, post=2, variable_v=True) if args.variable_v else {}
+    if args.smoother == "ainv":
+        kw.update(smoother="ainv", ainv_drop=args.ainv_drop)
+        if not args.variable_v:
+            kw.update(pre=1, post=1)
+    return kw
 
 
 def _oracle_kw(args):
@@ -248,11 +256,15 @@ def _oracle_kw(args):
 def _solver_desc(args):
     coarse = ("coarsest PCG(<=40, 1e-10) with l1-Jacobi" if args.coarse_solver == "pcg"
               else "30 coarsest l1-Jacobi sweeps")
-    cyc = "variable V(2*2^l,2*2^l)" if args.variable_v else "V(4,4)"
+    cyc = "variable V(2*2^l,2*2^l)" if args.variable_v else ("V(1,1)" if args.smoother == "ainv" else "V(4,4)")
+    if args.smoother == "ainv":
+        cyc += f" AINV(drop {args.ainv_drop:g}, block-Jacobi over ranks)"
+    else:
+        cyc += " l1-Jacobi"
     prol = ", un-smoothed P" if args.unsmoothed_p else ""
     hier = {"vmb": "decoupled VMB", "smatch": "matching (<= 8), smoothed P",
             "vmatch": "matching (<= 8)"}[args.hierarchy]
-    return f"{args.krylov.upper()}, {cyc} l1-Jacobi, {coarse}{prol}, {hier} aggregation"
+    return f"{args.krylov.upper()}, {cyc}, {coarse}{prol}, {hier} aggregation"
 
 
 # ------------------------------------------------------------------- main
@@ -293,6 +305,9 @@ def main():
     ap.add_argument("--hierarchy", default="vmb", choices=["vmb", "smatch", "vmatch"],
                     help="aggregation (P:328-330): decoupled VMB; matching with aggregates <= 8 and smoothed "
                          "(SMATCH) or tentative (VMATCH, implies --unsmoothed-p --variable-v) prolongators")
+    ap.add_argument("--smoother", default="l1", choices=["l1", "ainv"],
+                    help="level smoother: l1-Jacobi (P:269-272) or AINV (P:273-279; V(1,1) unless --variable-v)")
+    ap.add_argument("--ainv-drop", type=float, default=0.1, help="AINV drop tolerance")
     ap.add_argument("--unsmoothed-p", action="store_true",
                     help="tentative (un-smoothed) prolongators, as VMATCH (P:330), on the same aggregates")
     args = ap.parse_args()
@@ -311,6 +326,12 @@ def main():
         raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
 
     if args.impl == "reference":
+        if args.smoother == "ainv":  # the oracle's AINV factors are dense (n x n): test sizes only
+            if rank == 0:
+                print(json.dumps({"impl": "reference",
+                                  "unavailable": "the oracle's AINV is a dense n x n factorisation (tests only)"}),
+                      file=out, flush=True)
+            return
         run_reference(args, rank, N, out)
         return
 
@@ -482,6 +503,15 @@ def main():
                         "(alg = SURVEY §8(d) 12 B/nnz + 8 B/vector element; layout = as stored); levels >= 2 "
                         "are L2-resident, so their fractions of the HBM peak are not roofline claims",
                 "rows": ktab}
+    if roof["achieved"] is None and ktab:
+        # no l1-Jacobi level-0 sweep in this cycle (AINV smoother): the kernel with the
+        # largest share of the iteration, from the per-kernel table
+        top = max((r for r in ktab["rows"] if r.get("alg_GBps")), key=lambda r: r["share_of_iter"] or 0.0)
+        roof.update(kernel=f"{top['kernel']} (level {top['level']}, largest share of the iteration)",
+                    achieved=top["alg_GBps"], frac=top["alg_frac"], traffic=None,
+                    algorithmic_bytes_per_launch=top["alg_bytes"], launches_per_iteration=top["calls_per_iter"],
+                    launches_timed=None, avg_launch_us=top["us_per_call"], share_of_step=top["share_of_iter"],
+                    source="kernel_table (psc_hier_kernel_profile)")
 
     # end to end: host b / x through psc_pcg_solve_host, pinned host buffers
     e2e = None
@@ -506,7 +536,7 @@ def main():
                "api": "psc_krylov_solve_host"}
 
     cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+    if rank == 0 and N == 1 and not args.no_cpu_baseline and args.smoother == "l1":
         import oracle
         cores = oracle.set_threads(oracle_threads())
         if h is None or h.nlevels == 1:  # same rules, host generator (equal to the device set-up up to rounding)
