@@ -185,7 +185,10 @@ __device__ __forceinline__ double ell_sum(const CT* __restrict__ c, int32_t base
 // lane holds: s = sum_k val[k] * x[col[k]], k in stored order (padding adds
 // fma(0, x, s) = s).  DIA slices: dia_sum<W>.  ELL slices: explicit columns,
 // batches of 8 (value, column) loads issued before the dependent gathers.
-template <bool CG = false>
+// E16: the matrix has kEll16 slices.  The thread-per-row kernels come in two
+// instantiations: without the kEll16 branch (116 registers for sell_sweep; the branch
+// alone raised it to 128 and slowed the level-1 sweep) and with it.
+template <bool CG = false, bool E16 = true>
 __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, const int32_t* __restrict__ col,
                                                const double* __restrict__ val, const double* __restrict__ x,
                                                int64_t ncols, bool keep) {
@@ -237,9 +240,11 @@ __device__ __forceinline__ double sell_row_sum(int32_t h, int64_t s, int lane, c
   }
   const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
                      (uint32_t)__shfl_sync(0xffffffffu, h, 2);
-  if (__shfl_sync(0xffffffffu, h, 5) == kEll16)
-    return ell_sum<CG>(reinterpret_cast<const uint16_t*>(col + cb) + lane, __shfl_sync(0xffffffffu, h, 6), w, v,
-                       x, ncols, keep);
+  if constexpr (E16) {
+    if (__shfl_sync(0xffffffffu, h, 5) == kEll16)
+      return ell_sum<CG>(reinterpret_cast<const uint16_t*>(col + cb) + lane, __shfl_sync(0xffffffffu, h, 6), w, v,
+                         x, ncols, keep);
+  }
   return ell_sum<CG>(col + cb + lane, 0, w, v, x, ncols, keep);
 }
 
@@ -446,7 +451,7 @@ __device__ __forceinline__ void epilogue(const RowKArgs& a, int64_t i, double su
 // sliced ELL: one warp per slice, one thread per row; the next slice's header
 // is loaded before the current slice is processed (one dependent round trip
 // less per slice)
-template <RowOp OP>
+template <RowOp OP, bool E16>
 __device__ __forceinline__ void sell_body(const RowKArgs& a) {
   if (a.wait.on) wait_halo(a.wait);
   constexpr int NR = NRed<OP>::value;
@@ -473,7 +478,7 @@ __device__ __forceinline__ void sell_body(const RowKArgs& a) {
     const bool live = i < a.n_rows;
     EpiIn e{0.0, 0.0, 0.0};
     if (live) e = epi_load<OP>(a, i);
-    const double sum = sell_row_sum(h, s, lane, a.col, a.val, a.x, a.ncols, a.keep_matrix != 0);
+    const double sum = sell_row_sum<false, E16>(h, s, lane, a.col, a.val, a.x, a.ncols, a.keep_matrix != 0);
     if (live) epi_store<OP>(a, i, sum, e, acc);
     t = tn;
     s = sn;
@@ -512,7 +517,12 @@ __device__ __forceinline__ void rg_body(const RowKArgs& a) {
 
 // One named kernel per (layout, epilogue): readable launch lists and ncu filters.
 #define PSC_ROW_KERNELS(name, OP)                                                                         \
-  __global__ void __launch_bounds__(kBlock, PSC_SELL_MINB) sell_##name(RowKArgs a) { sell_body<OP>(a); }  \
+  __global__ void __launch_bounds__(kBlock, PSC_SELL_MINB) sell_##name(RowKArgs a) {                    \
+    sell_body<OP, false>(a);                                                                              \
+  }                                                                                                       \
+  __global__ void __launch_bounds__(kBlock, PSC_SELL_MINB) sell16_##name(RowKArgs a) {                  \
+    sell_body<OP, true>(a);                                                                               \
+  }                                                                                                       \
   template <int G>                                                                                        \
   __global__ void __launch_bounds__(kBlock) rg_##name(RowKArgs a) {                                      \
     rg_body<OP, G>(a);                                                                                    \
@@ -543,7 +553,20 @@ static RowKernel rg_kernel(RowOp op) {
   return nullptr;
 }
 
-static RowKernel kernel_of(RowOp op, int lanes) {
+static RowKernel kernel_of(RowOp op, int lanes, bool e16 = false) {
+  if (lanes == 1 && e16) {
+    switch (op) {
+      case RowOp::Spmv: return sell16_spmv;
+      case RowOp::SpmvDot: return sell16_spmv_dot;
+      case RowOp::Sweep: return sell16_sweep;
+      case RowOp::SweepDot: return sell16_sweep_dot;
+      case RowOp::Resid: return sell16_resid;
+      case RowOp::ResidDot2: return sell16_resid_dot2;
+      case RowOp::PAdd: return sell16_padd;
+      case RowOp::Sweep0: break;
+    }
+    return nullptr;
+  }
   switch (lanes) {
     case 4: return rg_kernel<4>(op);
     case 8: return rg_kernel<8>(op);
@@ -566,14 +589,15 @@ static RowKernel kernel_of(RowOp op, int lanes) {
 
 static int lanes_slot(int lanes) { return lanes == 1 ? 0 : (lanes == 4 ? 1 : (lanes == 8 ? 2 : (lanes == 16 ? 3 : 4))); }
 
-static int occ_for(RowOp op, int lanes) {
-  static int occ[5][8] = {{-1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1},
+static int occ_for(RowOp op, int lanes, bool e16 = false) {
+  static int occ[6][8] = {{-1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1},
                           {-1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1},
-                          {-1, -1, -1, -1, -1, -1, -1, -1}};
-  int& o = occ[lanes_slot(lanes)][(int)op];
+                          {-1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1}};
+  const bool e = e16 && lanes == 1;
+  int& o = occ[e ? 5 : lanes_slot(lanes)][(int)op];
   if (o < 0) {
     int v = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel_of(op, lanes), kBlock, 0) != cudaSuccess || v < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel_of(op, lanes, e), kBlock, 0) != cudaSuccess || v < 1)
       v = 1;
     o = v;
   }
@@ -587,7 +611,7 @@ static int64_t set_count(const Sell& A, SliceSet set) {
 int row_grid(const Sell& A, RowOp op, int num_sms, SliceSet set) {
   const int64_t n = set_count(A, set);
   const int64_t need = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const int64_t cap = (int64_t)num_sms * occ_for(op, A.lanes);
+  const int64_t cap = (int64_t)num_sms * occ_for(op, A.lanes, A.n_e16 > 0);
   return (int)std::max<int64_t>(1, std::min(need, cap));
 }
 
@@ -1121,7 +1145,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   }
   const int grid = row_grid(A, op, ctx->num_sms, set);
   PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
-  launch_k(kernel_of(op, A.lanes), grid, kBlock, 0, s, a);
+  launch_k(kernel_of(op, A.lanes, A.n_e16 > 0), grid, kBlock, 0, s, a);
   PSC_CUDA(cudaGetLastError());
   ctx->launches++;
 }
@@ -2246,12 +2270,15 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     flag.resize(nu);
     hp.resize(nu + 1);
     hsnnz.resize(nu);
+    std::vector<int32_t> he16(nu);
     if (nu) {
+      PSC_CUDA(cudaMemcpyAsync(he16.data(), d_e16, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
       PSC_CUDA(cudaMemcpyAsync(flag.data(), d_flag, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
       PSC_CUDA(cudaMemcpyAsync(hsnnz.data(), d_snnz, sizeof(int64_t) * nu, cudaMemcpyDeviceToHost, s));
     }
     PSC_CUDA(cudaMemcpyAsync(hp.data(), S.ptr, sizeof(int64_t) * (nu + 1), cudaMemcpyDeviceToHost, s));
     PSC_CUDA(cudaStreamSynchronize(s));
+    S.n_e16 = std::count_if(he16.begin(), he16.end(), [&](int32_t b) { return b >= 0; });
     dfree(d_snnz);
     dfree(d_flag);
     dfree(d_diad);

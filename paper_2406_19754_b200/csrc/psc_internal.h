@@ -96,6 +96,7 @@ struct Sell {
   int64_t col_slots = 0;   // entries of `col`
   int64_t nnz_ell = 0;     // stored nonzeros whose column index is explicit (ELL slices / row groups)
   int64_t n_dia = 0;       // DIA slices
+  int64_t n_e16 = 0;       // ELL slices with 16-bit column offsets (kEll16)
   int32_t* col = nullptr;  // col_slots
   // lanes == 1: per-slice 64-byte header read by the row kernels in one coalesced
   // half-warp load (prefetched one slice ahead): [0..1] value offset, [2..3] column

@@ -931,6 +931,23 @@ int psc_amg_hier_create(psc_amg* a, const psc_cycle_opts* copts, psc_hier** out)
     };
     std::vector<psc_mat*> A(L), P(std::max(L - 1, 1)), R(std::max(L - 1, 1));
     for (int l = 0; l < L; ++l) A[l] = mk(a->lv[l].A, a->descs[l], a->descs[l]);
+    // the AINV factorisation runs on the host (hier.cu ainv_factor): host copies of the
+    // smoothed levels' operators, as psc_mat_create_csr keeps them (nnz <= 2^27)
+    if (copts && copts->smoother == PSC_SMOOTHER_AINV)
+      for (int l = 0; l + 1 < L; ++l) {
+        const DCsr& M = a->lv[l].A;
+        if (M.nnz > ((int64_t)1 << 27)) continue;
+        psc_mat* m = A[l];
+        m->h_rowptr.resize(M.n + 1);
+        m->h_colg.resize(M.nnz);
+        m->h_val.resize(M.nnz);
+        PSC_CUDA(cudaMemcpyAsync(m->h_rowptr.data(), M.ptr, sizeof(int64_t) * (M.n + 1), cudaMemcpyDeviceToHost, s));
+        if (M.nnz) {
+          PSC_CUDA(cudaMemcpyAsync(m->h_colg.data(), M.col, sizeof(int64_t) * M.nnz, cudaMemcpyDeviceToHost, s));
+          PSC_CUDA(cudaMemcpyAsync(m->h_val.data(), M.val, sizeof(double) * M.nnz, cudaMemcpyDeviceToHost, s));
+        }
+      }
+    PSC_CUDA(cudaStreamSynchronize(s));
     for (int l = 0; l + 1 < L; ++l) {
       P[l] = mk(a->lv[l].P, a->descs[l], a->descs[l + 1]);
       R[l] = mk(a->lv[l].R, a->descs[l + 1], a->descs[l]);

@@ -105,6 +105,30 @@ def test_device_hierarchy_pcg_parity(psc, name):
     ctx.close()
 
 
+def test_device_hierarchy_ainv_smoother(psc):
+    """The device set-up's hierarchy with the AINV smoother (the library factors the
+    levels from host copies of the device-built operators): V-cycle and PCG against
+    the oracle's hierarchy with the same smoother."""
+    A0 = _A0("poisson16")
+    H, ctx, S, info = _compare(psc, A0)
+    n = A0.shape[0]
+    Hd = S.hierarchy(pre=1, post=1, smoother="ainv", ainv_drop=0.1)
+    okw = dict(pre=1, post=1, smoother="ainv", ainv_drop=0.1)
+    r = pscgen.rhs_random(4, 0, n)
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    Hd.vcycle(torch.from_numpy(r).cuda(), z)
+    zo = oracle.vcycle(H, r, **okw)
+    assert np.abs(z.cpu().numpy() - zo).max() <= 1e-12 * np.abs(zo).max()
+    b = pscgen.rhs_random(2, 0, n)
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    rc, st, hist = Hd.solve(torch.from_numpy(b).cuda(), x, tol=1e-8, maxit=200)
+    xo, ito, sto, histo = oracle.pcg(H, b, tol=1e-8, maxit=200, **okw)
+    assert rc == 0 and sto == 0 and abs(st["iters"] - ito) <= 1
+    k = min(20, ito, st["iters"]) + 1
+    np.testing.assert_allclose(hist[:k], histo[:k], rtol=1e-9, atol=0)
+    ctx.close()
+
+
 def test_setup_errors(psc):
     ctx = psc.Context()
     A = sp.csr_matrix(np.array([[1.0, 0.5], [0.5, -1.0]]))  # non-positive diagonal
