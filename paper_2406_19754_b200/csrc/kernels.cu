@@ -400,6 +400,7 @@ __device__ __forceinline__ EpiIn epi_load(const RowKArgs& a, int64_t i) {
   EpiIn e{0.0, 0.0, 0.0};
   if constexpr (OP == RowOp::Spmv) {
     if (a.beta != 0.0) e.x = a.y[i];
+    if (a.y2) e.d = __ldcs(a.dinv2 + i);  // before the row sum: off the critical path
   } else if constexpr (OP == RowOp::SpmvDot) {
     e.x = __ldg(a.x + i);
   } else if constexpr (OP == RowOp::Sweep || OP == RowOp::SweepDot) {
@@ -420,7 +421,7 @@ __device__ __forceinline__ void epi_store(const RowKArgs& a, int64_t i, double s
     const double v = (a.beta == 0.0) ? a.alpha * sum : a.alpha * sum + a.beta * e.x;
     a.y[i] = v;
     if (a.push.on) push_row(a.push, i, v);
-    if (a.y2) a.y2[i] = a.dinv2[i] * v;
+    if (a.y2) a.y2[i] = e.d * v;
   } else if constexpr (OP == RowOp::SpmvDot) {
     a.y[i] = sum;
     acc[0] += e.x * sum;
@@ -690,6 +691,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
   uint64_t* empty = full + kTmaStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool readY = EV::Y && !(OP == RowOp::Spmv && a.beta == 0.0);
+  // Spmv with y2 = dinv2 .* y (the next level's first sweep): dinv2 staged in slot 1
+  const bool readD2 = OP == RowOp::Spmv && a.y2 != nullptr;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kTmaStages; ++st) {
       mbar_init(&full[st], 1);
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const uint32_t cbytes = (uint32_t)(cb1 - cb0) * 4;
         const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
         const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) +
-                              ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0);
+                              ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0) + (readD2 ? 1 : 0);
         PSC_DASSERT(vbytes <= (uint32_t)kTmaValBytes && cbytes <= (uint32_t)kTmaColBytes &&
                     rbytes <= (uint32_t)kTmaVecBytes && hb <= (uint32_t)kTmaHdrBytes);
         mbar_expect_tx(&full[st], hb + vbytes + cbytes + nvec * rbytes);
@@ -748,6 +751,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
             bulk_g2s(vec + kTmaVecBytes, a.dinv + r0, rbytes, &full[st], kGatherBD ? pol_keep : pol_stream);
           if constexpr (EV::X || EV::XPRE) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
           if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
+          if (readD2) bulk_g2s(vec + kTmaVecBytes, a.dinv2 + r0, rbytes, &full[st], pol_stream);
         }
         vb0 = nvb0; vb1 = nvb1; cb0 = ncb0; cb1 = ncb1;
       }
@@ -823,6 +827,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
           if constexpr (EV::D) e.d = vec[kTmaRows + rl];
           if constexpr (EV::X) e.x = vec[2 * kTmaRows + rl];
           if (readY) e.x = vec[2 * kTmaRows + rl];
+          if (readD2) e.d = vec[kTmaRows + rl];
           if constexpr (OP == RowOp::Sweep0) e.x = __dmul_rn(e.d, e.b);  // x1_i
           epi_store<OP>(a, row, sum, e, acc);
         }
@@ -871,6 +876,7 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRgStages * kRgStageBytes);
   uint64_t* empty = full + kRgStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool readD2 = OP == RowOp::Spmv && a.y2 != nullptr;  // y2 = dinv2 .* y: dinv2 in slot 1
   const bool readY = EV::Y && !(OP == RowOp::Spmv && a.beta == 0.0);
   if (threadIdx.x == 0) {
     for (int st = 0; st < kRgStages; ++st) {
@@ -908,7 +914,7 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
         const uint32_t vbytes = (uint32_t)(e1 - e0) * 8;
         const uint32_t cbytes = (uint32_t)(e1 - e0) * 4;
         const uint32_t rbytes = (uint32_t)(((r1 - r0) * 8 + 15) & ~15);
-        const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D ? 1 : 0) + (EV::X ? 1 : 0) + (readY ? 1 : 0);
+        const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D ? 1 : 0) + (EV::X ? 1 : 0) + (readY ? 1 : 0) + (readD2 ? 1 : 0);
         PSC_DASSERT(e1 - e0 <= kRgCap && pbytes <= (uint32_t)kRgPtrBytes && r1 - r0 <= kRgMaxRows);
         mbar_expect_tx(&full[st], pbytes + vbytes + cbytes + nvec * rbytes);
         bulk_g2s(base + kRgValBytes + kRgColBytes, a.ptr + r0, pbytes, &full[st], pol_keep);
@@ -921,6 +927,7 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
         if constexpr (EV::D) bulk_g2s(vec + kRgVecBytes, a.dinv + r0, rbytes, &full[st], pol_stream);
         if constexpr (EV::X) bulk_g2s(vec + 2 * kRgVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
         if (readY) bulk_g2s(vec + 2 * kRgVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
+        if (readD2) bulk_g2s(vec + kRgVecBytes, a.dinv2 + r0, rbytes, &full[st], pol_stream);
         e0 = ne0;
         e1 = ne1;
       }
@@ -970,6 +977,7 @@ __global__ void __launch_bounds__(kTmaThreads) rg_tma(RowKArgs a, int64_t nchunk
         if constexpr (EV::D) ein.d = vec[kRgMaxRows + lr];
         if constexpr (EV::X) ein.x = vec[2 * kRgMaxRows + lr];
         if (readY) ein.x = vec[2 * kRgMaxRows + lr];
+        if (readD2) ein.d = vec[kRgMaxRows + lr];
         epi_store<OP>(a, i, sum, ein, acc);
       }
       __syncwarp();
