@@ -302,6 +302,8 @@ __device__ __forceinline__ double rg_row_sum(const int32_t* __restrict__ col, co
 
 struct RowKArgs {
   int keep_matrix;  // 1: matrix small enough to stay in L2 across the level's launches (evict_last)
+  int xpre;         // square matrix, Spmv / PAdd: the TMA kernel bulk-copies the rows' own x block
+                    // (evict_last) to bring the gathers' lines into L2 ahead of them
   const int64_t* ptr;
   const int64_t* cptr;
   const int32_t* hdr;
@@ -693,6 +695,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
   const bool readY = EV::Y && !(OP == RowOp::Spmv && a.beta == 0.0);
   // Spmv with y2 = dinv2 .* y (the next level's first sweep): dinv2 staged in slot 1
   const bool readD2 = OP == RowOp::Spmv && a.y2 != nullptr;
+  // square Spmv / PAdd (AINV's Z^T and Z): own x block prefetched into slot 0 (unused)
+  const bool xpre = (OP == RowOp::Spmv || OP == RowOp::PAdd) && a.xpre != 0;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kTmaStages; ++st) {
       mbar_init(&full[st], 1);
@@ -734,7 +738,8 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const uint32_t cbytes = (uint32_t)(cb1 - cb0) * 4;
         const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
         const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) +
-                              ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0) + (readD2 ? 1 : 0);
+                              ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0) + (readD2 ? 1 : 0) +
+                              (xpre ? 1 : 0);
         PSC_DASSERT(vbytes <= (uint32_t)kTmaValBytes && cbytes <= (uint32_t)kTmaColBytes &&
                     rbytes <= (uint32_t)kTmaVecBytes && hb <= (uint32_t)kTmaHdrBytes);
         mbar_expect_tx(&full[st], hb + vbytes + cbytes + nvec * rbytes);
@@ -752,6 +757,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
           if constexpr (EV::X || EV::XPRE) bulk_g2s(vec + 2 * kTmaVecBytes, a.x + r0, rbytes, &full[st], pol_keep);
           if (readY) bulk_g2s(vec + 2 * kTmaVecBytes, a.y + r0, rbytes, &full[st], pol_stream);
           if (readD2) bulk_g2s(vec + kTmaVecBytes, a.dinv2 + r0, rbytes, &full[st], pol_stream);
+          if (xpre) bulk_g2s(vec, a.x + r0, rbytes, &full[st], pol_keep);
         }
         vb0 = nvb0; vb1 = nvb1; cb0 = ncb0; cb1 = ncb1;
       }
@@ -1091,6 +1097,7 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   RowKArgs a;
   // matrices up to 48 MB stay in L2 (evict_last) across the 8-10 launches of their level
   a.keep_matrix = (A.padded * 12 + A.n_rows * 8) <= ((int64_t)env_int("PSC_KEEP_MB", 96) << 20) ? 1 : 0;
+  a.xpre = (A.n_rows == A.n_cols_local && (op == RowOp::Spmv || op == RowOp::PAdd) && !env_int("PSC_NO_XPRE", 0)) ? 1 : 0;
   a.perm = A.perm;
   a.ptr = A.ptr;
   a.cptr = A.cptr;
