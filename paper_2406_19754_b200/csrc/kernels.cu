@@ -638,8 +638,15 @@ constexpr int kTmaHdrBytes = kTmaSlices * kHdr * 4;                    // 512
 constexpr int kTmaValBytes = kTmaSlices * kTmaMaxW * 32 * 8;           // 16 KB
 constexpr int kTmaColBytes = kTmaSlices * kTmaMaxW * 32 * 4;           // 8 KB
 constexpr int kTmaVecBytes = kTmaRows * 8;                             // 2 KB per vector
-constexpr int kTmaStageBytes = kTmaHdrBytes + kTmaValBytes + kTmaColBytes + 3 * kTmaVecBytes;
-constexpr int kTmaSmem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
+// DIA-only matrices (every slice DIA with its offsets in the header: A_0 of a stencil):
+// no column region, so the same shared memory holds a 4-stage ring (more bytes in flight)
+template <bool DIAONLY>
+struct TmaRing {
+  static constexpr int kStages = DIAONLY ? 4 : kTmaStages;
+  static constexpr int kColBytes = DIAONLY ? 0 : kTmaColBytes;
+  static constexpr int kStageBytes = kTmaHdrBytes + kTmaValBytes + kColBytes + 3 * kTmaVecBytes;
+  static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -684,10 +691,14 @@ struct EpiVecs {  // which row vectors the epilogue reads: b, dinv, x(own), y
   static constexpr bool Y = (OP == RowOp::PAdd || OP == RowOp::Spmv);
 };
 
-template <RowOp OP>
+template <RowOp OP, bool DIAONLY>
 __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchunks, int64_t n_slices) {
   constexpr int NR = NRed<OP>::value;
   using EV = EpiVecs<OP>;
+  using RG = TmaRing<DIAONLY>;
+  constexpr int kTmaStages = RG::kStages;
+  constexpr int kTmaStageBytes = RG::kStageBytes;
+  constexpr int kTmaColBytes = RG::kColBytes;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaStageBytes);
   uint64_t* empty = full + kTmaStages;
@@ -735,12 +746,12 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         const int64_t r0 = s0 * 32, r1 = min(s1 * 32, a.n_rows);
         const uint32_t hb = (uint32_t)(s1 - s0) * kHdr * 4;
         const uint32_t vbytes = (uint32_t)(vb1 - vb0) * 8;
-        const uint32_t cbytes = (uint32_t)(cb1 - cb0) * 4;
+        const uint32_t cbytes = DIAONLY ? 0u : (uint32_t)(cb1 - cb0) * 4;  // DIA: offsets in the header
         const uint32_t rbytes = r1 > r0 ? (uint32_t)(((r1 - r0) * 8 + 15) & ~15) : 0u;
         const uint32_t nvec = (EV::B ? 1 : 0) + (EV::D_SELL ? 1 : 0) +
                               ((EV::X || EV::XPRE) ? 1 : 0) + (readY ? 1 : 0) + (readD2 ? 1 : 0) +
                               (xpre ? 1 : 0);
-        PSC_DASSERT(vbytes <= (uint32_t)kTmaValBytes && cbytes <= (uint32_t)kTmaColBytes &&
+        PSC_DASSERT(vbytes <= (uint32_t)kTmaValBytes && cbytes <= (uint32_t)(DIAONLY ? 0 : kTmaColBytes) &&
                     rbytes <= (uint32_t)kTmaVecBytes && hb <= (uint32_t)kTmaHdrBytes);
         mbar_expect_tx(&full[st], hb + vbytes + cbytes + nvec * rbytes);
         bulk_g2s(base, a.hdr + s0 * kHdr, hb, &full[st], pol_keep);
@@ -785,7 +796,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
                            (uint32_t)__shfl_sync(0xffffffffu, h, 0);
         const int w = __shfl_sync(0xffffffffu, h, 4);
         const int kind = __shfl_sync(0xffffffffu, h, 5);
-        const bool dia = kind == kDia;
+        const bool dia = DIAONLY || kind == kDia;
         const double* v = vs + (vb - vbase) + lane;
         const uint32_t i = (uint32_t)(s * 32 + lane);
         // x_j; Sweep0: x1_j = dinv_j b_j, the first sweep from zero (a correctly
@@ -846,14 +857,20 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
-template <RowOp OP>
-static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, cudaStream_t s) {
+template <RowOp OP, bool DIAONLY>
+static void tma_launch_t(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, cudaStream_t s) {
   static bool attr = false;
+  constexpr int smem = TmaRing<DIAONLY>::kSmem;
   if (!attr) {
-    PSC_CUDA(cudaFuncSetAttribute(sell_tma<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+    PSC_CUDA(cudaFuncSetAttribute(sell_tma<OP, DIAONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  launch_k(sell_tma<OP>, grid, kTmaThreads, kTmaSmem, s, a, nchunks, n_slices);
+  launch_k(sell_tma<OP, DIAONLY>, grid, kTmaThreads, smem, s, a, nchunks, n_slices);
+}
+template <RowOp OP>
+static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, bool diaonly, cudaStream_t s) {
+  if (diaonly) tma_launch_t<OP, true>(a, grid, nchunks, n_slices, s);
+  else tma_launch_t<OP, false>(a, grid, nchunks, n_slices, s);
 }
 
 // ---------------------------------------------- TMA-staged row-group kernel
@@ -1130,15 +1147,17 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
     const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
     PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
+    // every slice DIA (offsets in the header): the 4-stage ring without a column region
+    const bool dia4 = A.n_dia == A.n_units && A.max_width <= kMaxDiaHdr && !env_int("PSC_NO_TMA4", 0);
     switch (op) {
-      case RowOp::Spmv: tma_launch<RowOp::Spmv>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::SpmvDot: tma_launch<RowOp::SpmvDot>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::Sweep: tma_launch<RowOp::Sweep>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::SweepDot: tma_launch<RowOp::SweepDot>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::Resid: tma_launch<RowOp::Resid>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::ResidDot2: tma_launch<RowOp::ResidDot2>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::PAdd: tma_launch<RowOp::PAdd>(a, grid, nchunks, A.n_units, s); break;
-      case RowOp::Sweep0: tma_launch<RowOp::Sweep0>(a, grid, nchunks, A.n_units, s); break;
+      case RowOp::Spmv: tma_launch<RowOp::Spmv>(a, grid, nchunks, A.n_units, dia4, s); break;
+      case RowOp::SpmvDot: tma_launch<RowOp::SpmvDot>(a, grid, nchunks, A.n_units, dia4, s); break;
+      case RowOp::Sweep: tma_launch<RowOp::Sweep>(a, grid, nchunks, A.n_units, dia4, s); break;
+      case RowOp::SweepDot: tma_launch<RowOp::SweepDot>(a, grid, nchunks, A.n_units, dia4, s); break;
+      case RowOp::Resid: tma_launch<RowOp::Resid>(a, grid, nchunks, A.n_units, dia4, s); break;
+      case RowOp::ResidDot2: tma_launch<RowOp::ResidDot2>(a, grid, nchunks, A.n_units, dia4, s); break;
+      case RowOp::PAdd: tma_launch<RowOp::PAdd>(a, grid, nchunks, A.n_units, dia4, s); break;
+      case RowOp::Sweep0: tma_launch<RowOp::Sweep0>(a, grid, nchunks, A.n_units, dia4, s); break;
     }
     PSC_CUDA(cudaGetLastError());
     ctx->launches++;
