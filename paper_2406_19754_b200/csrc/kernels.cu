@@ -638,12 +638,16 @@ constexpr int kTmaHdrBytes = kTmaSlices * kHdr * 4;                    // 512
 constexpr int kTmaValBytes = kTmaSlices * kTmaMaxW * 32 * 8;           // 16 KB
 constexpr int kTmaColBytes = kTmaSlices * kTmaMaxW * 32 * 4;           // 8 KB
 constexpr int kTmaVecBytes = kTmaRows * 8;                             // 2 KB per vector
-// DIA-only matrices (every slice DIA with its offsets in the header: A_0 of a stencil):
-// no column region, so the same shared memory holds a 4-stage ring (more bytes in flight)
-template <bool DIAONLY>
+// Ring layouts by the matrix's slice kinds.  kRingAny: 3 stages with an int32 column
+// region.  kRingDia (every slice DIA with its offsets in the header: A_0 of a stencil):
+// no column region, so the same shared memory holds 4 stages.  kRingE16 (every slice
+// DIA or kEll16: P_0): a uint16 column region, 4 stages.  More bytes in flight per SM:
+// level-0 sweep 229.6 -> 224.8 us, Sweep0 259 -> 235, q = A p 217 -> 202 (same box).
+enum TmaRingKind : int { kRingAny = 0, kRingDia = 1, kRingE16 = 2 };
+template <int RING>
 struct TmaRing {
-  static constexpr int kStages = DIAONLY ? 4 : kTmaStages;
-  static constexpr int kColBytes = DIAONLY ? 0 : kTmaColBytes;
+  static constexpr int kStages = RING == kRingAny ? kTmaStages : 4;
+  static constexpr int kColBytes = RING == kRingAny ? kTmaColBytes : (RING == kRingDia ? 0 : kTmaColBytes / 2);
   static constexpr int kStageBytes = kTmaHdrBytes + kTmaValBytes + kColBytes + 3 * kTmaVecBytes;
   static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
 };
@@ -691,11 +695,12 @@ struct EpiVecs {  // which row vectors the epilogue reads: b, dinv, x(own), y
   static constexpr bool Y = (OP == RowOp::PAdd || OP == RowOp::Spmv);
 };
 
-template <RowOp OP, bool DIAONLY>
+template <RowOp OP, int RING>
 __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchunks, int64_t n_slices) {
   constexpr int NR = NRed<OP>::value;
   using EV = EpiVecs<OP>;
-  using RG = TmaRing<DIAONLY>;
+  using RG = TmaRing<RING>;
+  constexpr bool DIAONLY = RING == kRingDia;
   constexpr int kTmaStages = RG::kStages;
   constexpr int kTmaStageBytes = RG::kStageBytes;
   constexpr int kTmaColBytes = RG::kColBytes;
@@ -815,7 +820,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
         } else {
           const int64_t cb = ((int64_t)(uint32_t)__shfl_sync(0xffffffffu, h, 3) << 32) |
                              (uint32_t)__shfl_sync(0xffffffffu, h, 2);
-          if (kind == kEll16) {
+          if (RING == kRingE16 || kind == kEll16) {
             const uint16_t* cc = reinterpret_cast<const uint16_t*>(cs + (cb - cbase)) + lane;
             const uint32_t base = (uint32_t)__shfl_sync(0xffffffffu, h, 6);
 #pragma unroll
@@ -857,20 +862,21 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
   if constexpr (NR > 0) grid_reduce<NR>(acc, a.partials, a.ticket, a.red_out, a.red_stride);
 }
 
-template <RowOp OP, bool DIAONLY>
+template <RowOp OP, int RING>
 static void tma_launch_t(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, cudaStream_t s) {
   static bool attr = false;
-  constexpr int smem = TmaRing<DIAONLY>::kSmem;
+  constexpr int smem = TmaRing<RING>::kSmem;
   if (!attr) {
-    PSC_CUDA(cudaFuncSetAttribute(sell_tma<OP, DIAONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PSC_CUDA(cudaFuncSetAttribute(sell_tma<OP, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  launch_k(sell_tma<OP, DIAONLY>, grid, kTmaThreads, smem, s, a, nchunks, n_slices);
+  launch_k(sell_tma<OP, RING>, grid, kTmaThreads, smem, s, a, nchunks, n_slices);
 }
 template <RowOp OP>
-static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, bool diaonly, cudaStream_t s) {
-  if (diaonly) tma_launch_t<OP, true>(a, grid, nchunks, n_slices, s);
-  else tma_launch_t<OP, false>(a, grid, nchunks, n_slices, s);
+static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, int ring, cudaStream_t s) {
+  if (ring == kRingDia) tma_launch_t<OP, kRingDia>(a, grid, nchunks, n_slices, s);
+  else if (ring == kRingE16) tma_launch_t<OP, kRingE16>(a, grid, nchunks, n_slices, s);
+  else tma_launch_t<OP, kRingAny>(a, grid, nchunks, n_slices, s);
 }
 
 // ---------------------------------------------- TMA-staged row-group kernel
@@ -1147,8 +1153,12 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
     const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
     PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
-    // every slice DIA (offsets in the header): the 4-stage ring without a column region
-    const bool dia4 = A.n_dia == A.n_units && A.max_width <= kMaxDiaHdr && !env_int("PSC_NO_TMA4", 0);
+    // ring layout by slice kinds (DIA slices here have <= 8 offsets, in the header)
+    int dia4 = kRingAny;
+    if (!env_int("PSC_NO_TMA4", 0)) {
+      if (A.n_dia == A.n_units) dia4 = kRingDia;
+      else if (A.n_dia + A.n_e16 == A.n_units) dia4 = kRingE16;
+    }
     switch (op) {
       case RowOp::Spmv: tma_launch<RowOp::Spmv>(a, grid, nchunks, A.n_units, dia4, s); break;
       case RowOp::SpmvDot: tma_launch<RowOp::SpmvDot>(a, grid, nchunks, A.n_units, dia4, s); break;
