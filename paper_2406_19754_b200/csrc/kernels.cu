@@ -643,11 +643,16 @@ constexpr int kTmaVecBytes = kTmaRows * 8;                             // 2 KB p
 // no column region, so the same shared memory holds 4 stages.  kRingE16 (every slice
 // DIA or kEll16: P_0): a uint16 column region, 4 stages.  More bytes in flight per SM:
 // level-0 sweep 229.6 -> 224.8 us, Sweep0 259 -> 235, q = A p 217 -> 202 (same box).
-enum TmaRingKind : int { kRingAny = 0, kRingDia = 1, kRingE16 = 2 };
+enum TmaRingKind : int { kRingAny = 0, kRingDia = 1, kRingE16 = 2, kRingDia33 = 3, kRingDia42 = 4 };
 template <int RING>
 struct TmaRing {
-  static constexpr int kStages = RING == kRingAny ? kTmaStages : 4;
-  static constexpr int kColBytes = RING == kRingAny ? kTmaColBytes : (RING == kRingDia ? 0 : kTmaColBytes / 2);
+  // kRingDia33 / kRingDia42: DIA-only rings for three CTAs per SM (3 stages each) or four
+  // (2 stages each): more consumer warps per SM for the same bytes in flight
+  static constexpr int kStages =
+      RING == kRingAny ? kTmaStages : (RING == kRingDia33 ? 3 : (RING == kRingDia42 ? 2 : 4));
+  static constexpr int kColBytes =
+      RING == kRingAny ? kTmaColBytes
+                       : ((RING == kRingDia || RING == kRingDia33 || RING == kRingDia42) ? 0 : kTmaColBytes / 2);
   static constexpr int kStageBytes = kTmaHdrBytes + kTmaValBytes + kColBytes + 3 * kTmaVecBytes;
   static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
 };
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(kTmaThreads) sell_tma(RowKArgs a, int64_t nchu
   constexpr int NR = NRed<OP>::value;
   using EV = EpiVecs<OP>;
   using RG = TmaRing<RING>;
-  constexpr bool DIAONLY = RING == kRingDia;
+  constexpr bool DIAONLY = RING == kRingDia || RING == kRingDia33 || RING == kRingDia42;
   constexpr int kTmaStages = RG::kStages;
   constexpr int kTmaStageBytes = RG::kStageBytes;
   constexpr int kTmaColBytes = RG::kColBytes;
@@ -875,6 +880,8 @@ static void tma_launch_t(const RowKArgs& a, int grid, int64_t nchunks, int64_t n
 template <RowOp OP>
 static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_slices, int ring, cudaStream_t s) {
   if (ring == kRingDia) tma_launch_t<OP, kRingDia>(a, grid, nchunks, n_slices, s);
+  else if (ring == kRingDia33) tma_launch_t<OP, kRingDia33>(a, grid, nchunks, n_slices, s);
+  else if (ring == kRingDia42) tma_launch_t<OP, kRingDia42>(a, grid, nchunks, n_slices, s);
   else if (ring == kRingE16) tma_launch_t<OP, kRingE16>(a, grid, nchunks, n_slices, s);
   else tma_launch_t<OP, kRingAny>(a, grid, nchunks, n_slices, s);
 }
@@ -1151,14 +1158,25 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
   const bool needs_red = (op == RowOp::SpmvDot || op == RowOp::SweepDot || op == RowOp::ResidDot2);
   if (tma_ok(A, r, set)) {
     const int64_t nchunks = (A.n_units + kTmaSlices - 1) / kTmaSlices;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 2 * (int64_t)ctx->num_sms));
-    PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
     // ring layout by slice kinds (DIA slices here have <= 8 offsets, in the header)
     int dia4 = kRingAny;
     if (!env_int("PSC_NO_TMA4", 0)) {
-      if (A.n_dia == A.n_units) dia4 = kRingDia;
+      if (A.n_dia == A.n_units) {
+        // same-box A/B on A_0 of 256^3 (2x4 / 3x3 / 4x2 CTAs x stages): the sweeps and the
+        // residual are fastest at 4x2 (222 / 201 us), Sweep0 (two gathers per entry) and
+        // q = A p at 3x3 (236 / 192 us); PSC_TMA_RING=1|3|4 forces one layout
+        const int e = env_int("PSC_TMA_RING", 0);
+        if (e == 1) dia4 = kRingDia;
+        else if (e == 3) dia4 = kRingDia33;
+        else if (e == 4) dia4 = kRingDia42;
+        else dia4 = (op == RowOp::Sweep0 || op == RowOp::SpmvDot) ? kRingDia33 : kRingDia42;
+      }
       else if (A.n_dia + A.n_e16 == A.n_units) dia4 = kRingE16;
     }
+    // CTAs per SM the ring's shared memory allows
+    const int per_sm = dia4 == kRingDia33 ? 3 : (dia4 == kRingDia42 ? 4 : 2);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, per_sm * (int64_t)ctx->num_sms));
+    PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
     switch (op) {
       case RowOp::Spmv: tma_launch<RowOp::Spmv>(a, grid, nchunks, A.n_units, dia4, s); break;
       case RowOp::SpmvDot: tma_launch<RowOp::SpmvDot>(a, grid, nchunks, A.n_units, dia4, s); break;
