@@ -643,15 +643,17 @@ constexpr int kTmaVecBytes = kTmaRows * 8;                             // 2 KB p
 // no column region, so the same shared memory holds 4 stages.  kRingE16 (every slice
 // DIA or kEll16: P_0): a uint16 column region, 4 stages.  More bytes in flight per SM:
 // level-0 sweep 229.6 -> 224.8 us, Sweep0 259 -> 235, q = A p 217 -> 202 (same box).
-enum TmaRingKind : int { kRingAny = 0, kRingDia = 1, kRingE16 = 2, kRingDia33 = 3, kRingDia42 = 4, kRingE16x3 = 5 };
+enum TmaRingKind : int { kRingAny = 0, kRingDia = 1, kRingE16 = 2, kRingDia33 = 3, kRingDia42 = 4, kRingE16x3 = 5,
+                         kRingAny3 = 6 };
 template <int RING>
 struct TmaRing {
   // kRingDia33 / kRingDia42: DIA-only rings for three CTAs per SM (3 stages each) or four
   // (2 stages each): more consumer warps per SM for the same bytes in flight
   static constexpr int kStages =
-      RING == kRingAny ? kTmaStages : (RING == kRingDia33 ? 3 : ((RING == kRingDia42 || RING == kRingE16x3) ? 2 : 4));
+      RING == kRingAny ? kTmaStages
+                       : (RING == kRingDia33 ? 3 : ((RING == kRingDia42 || RING == kRingE16x3 || RING == kRingAny3) ? 2 : 4));
   static constexpr int kColBytes =
-      RING == kRingAny ? kTmaColBytes
+      (RING == kRingAny || RING == kRingAny3) ? kTmaColBytes
                        : ((RING == kRingDia || RING == kRingDia33 || RING == kRingDia42) ? 0 : kTmaColBytes / 2);
   static constexpr int kStageBytes = kTmaHdrBytes + kTmaValBytes + kColBytes + 3 * kTmaVecBytes;
   static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
@@ -883,6 +885,7 @@ static void tma_launch(const RowKArgs& a, int grid, int64_t nchunks, int64_t n_s
   else if (ring == kRingDia33) tma_launch_t<OP, kRingDia33>(a, grid, nchunks, n_slices, s);
   else if (ring == kRingDia42) tma_launch_t<OP, kRingDia42>(a, grid, nchunks, n_slices, s);
   else if (ring == kRingE16x3) tma_launch_t<OP, kRingE16x3>(a, grid, nchunks, n_slices, s);
+  else if (ring == kRingAny3) tma_launch_t<OP, kRingAny3>(a, grid, nchunks, n_slices, s);
   else if (ring == kRingE16) tma_launch_t<OP, kRingE16>(a, grid, nchunks, n_slices, s);
   else tma_launch_t<OP, kRingAny>(a, grid, nchunks, n_slices, s);
 }
@@ -1177,7 +1180,11 @@ void launch_rows(psc_ctx* ctx, const Sell& A, RowOp op, const RowArgs& r, cudaSt
       else if (A.n_dia + A.n_e16 == A.n_units) dia4 = env_int("PSC_TMA_RING_E16", 3) == 2 ? kRingE16 : kRingE16x3;
     }
     // CTAs per SM the ring's shared memory allows
-    const int per_sm = (dia4 == kRingDia33 || dia4 == kRingE16x3) ? 3 : (dia4 == kRingDia42 ? 4 : 2);
+    // mixed slice kinds (a distributed A_0: its boundary slices reference halo columns, so
+    // they are int32 ELL): 3 CTAs x 2 stages (2 B200: q = A p 216 -> 205 us, P_0 198 ->
+    // 191, residual 218 -> 213; 7094 -> 7187 Mdof*iters/s); PSC_TMA_RING_ANY=2: 2 x 3
+    if (dia4 == kRingAny && env_int("PSC_TMA_RING_ANY", 3) != 2) dia4 = kRingAny3;
+    const int per_sm = (dia4 == kRingDia33 || dia4 == kRingE16x3 || dia4 == kRingAny3) ? 3 : (dia4 == kRingDia42 ? 4 : 2);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, per_sm * (int64_t)ctx->num_sms));
     PSC_REQUIRE(!needs_red || (r.red && r.red_out && grid <= r.red->grid), PSC_ERR_STATE, "reduction site missing");
     switch (op) {
