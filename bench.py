@@ -471,6 +471,8 @@ def main():
     tkey = f"sweep_l0_{g}"
     roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+            "peak_note": "peak = measured b.copy_(a) bandwidth (half reads, half writes); the sweep's "
+                         "traffic is ~93% reads, which HBM serves faster, so frac can exceed 1",
             "frac": achieved / peak if achieved else None,
             "traffic": None if strong else load_traffic(tkey), "algorithmic_bytes_per_launch": dom_b,
             "launches_per_iteration": per_iter,
