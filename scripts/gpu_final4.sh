@@ -11,7 +11,7 @@ run() {  # N out args...
 import json; d=json.load(open('gpurun_out/${TAG}_$o.json')); p=d.get('parity') or {}
 print('  ', round(d['value'],1), round(d['ms_per_step'],2), d['config']['iters'], d['launches_per_iteration'], p.get('ok'), d['roofline']['avg_launch_us'], d['clocks']['sm_mhz'], d['clocks']['reasons'])" 2>/dev/null
 }
-timeout 2400 python -m pytest tests/test_gpu_dist.py -q > gpurun_out/${TAG}_dist4_tests.log 2>&1; echo dist_tests_rc=$?
+[ -z "$SKIP_TESTS" ] && { timeout 2400 python -m pytest tests/test_gpu_dist.py -q > gpurun_out/${TAG}_dist4_tests.log 2>&1; echo dist_tests_rc=$?; }
 tail -1 gpurun_out/${TAG}_dist4_tests.log
 run 2 bench_2gpu --steps 5 --warmup 3
 run 4 bench_4gpu --steps 5 --warmup 3
