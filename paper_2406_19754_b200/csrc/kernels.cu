@@ -2282,7 +2282,7 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
     int32_t* d_diaoff = dalloc<int32_t>((size_t)nu * kMaxDia);
     int32_t* d_e16 = dalloc<int32_t>(nu);
     // ELL slices with 16-bit column offsets (PSC_COL16=0: 32-bit columns everywhere)
-    const int allow16 = env_int("PSC_COL16", 1) ? 1 : 0;
+    int allow16 = env_int("PSC_COL16", 1) ? 1 : 0;
     // DIA slices with up to 8 diagonals (offsets in the slice header; A_0).  Wider DIA
     // slices (up to kMaxDia, offsets in the column region) are opt-in, PSC_DIA_MAX=64:
     // on the level-1 Galerkin operator of 256^3 they measured slower (175 vs 154 us per
@@ -2312,6 +2312,19 @@ void sell_from_csr(psc_ctx* ctx, int64_t n_rows, const int64_t* d_rowptr, const 
       dfree(d_tmp);
     };
     widths(allow_dia, nullptr);
+    // 16-bit column slices only in matrices the TMA kernel takes whole (every slice at most
+    // kTmaMaxW wide): elsewhere they would send the thread-per-row kernels to their wider
+    // 16-bit instantiation (P_1 of 256^3: 68 vs 64 us)
+    if (allow16 && nu > 0) {
+      std::vector<int64_t> hv(nu + 1);
+      PSC_CUDA(cudaMemcpy(hv.data(), S.ptr, sizeof(int64_t) * (nu + 1), cudaMemcpyDeviceToHost));
+      int64_t wmax = 0;
+      for (int64_t u = 0; u < nu; ++u) wmax = std::max<int64_t>(wmax, (hv[u + 1] - hv[u]) / 32);
+      if (wmax > kTmaMaxW) {
+        allow16 = 0;
+        widths(allow_dia, nullptr);
+      }
+    }
     // SELL-C-sigma, opt-in PSC_SORT=1: a matrix with no DIA slice whose
     // slices pad more than 2% is re-laid out with its rows sorted by length inside
     // 256-row windows (P_0 of 256^3: 1.36 -> 1.09 padded slots per stored value).
