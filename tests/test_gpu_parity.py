@@ -291,6 +291,10 @@ VARIANTS = [
     {"PSC_NO_FUSED_SCALE": "1", "PSC_NO_DIA": "1", "PSC_NO_TMA": "1"},
     {"PSC_COL16": "0"},
     {"PSC_COL16": "0", "PSC_NO_DIA": "1", "PSC_NO_TMA": "1"},
+    {"PSC_NO_TMA4": "1"},
+    {"PSC_TMA_RING": "1", "PSC_TMA_RING_E16": "2"},
+    {"PSC_TMA_RING": "3", "PSC_TMA_RING_ANY": "2"},
+    {"PSC_TMA_RING": "4", "PSC_NO_XPRE": "1"},
 ]
 
 
