@@ -505,6 +505,14 @@ def main():
                         "(alg = SURVEY §8(d) 12 B/nnz + 8 B/vector element; layout = as stored); levels >= 2 "
                         "are L2-resident, so their fractions of the HBM peak are not roofline claims",
                 "rows": ktab}
+    if roof["achieved"] is not None and ktab:
+        # launches per iteration of the dominant kernel as the iteration graph has them (the
+        # library's count, (pre-1)+post, also counts Sweep0 and the SweepDot)
+        dom_rows = [r for r in ktab["rows"] if r["kernel"] == "sell_tma<Sweep>" and r["level"] == 0]
+        if dom_rows and dom_n:
+            n_it = dom_rows[0]["calls_per_iter"]
+            roof["launches_per_iteration"] = n_it
+            roof["share_of_step"] = dom_s / dom_n * n_it * sum(iters) / sum(s["solve_seconds"] for s in stats)
     if roof["achieved"] is None and ktab:
         # no l1-Jacobi level-0 sweep in this cycle (AINV smoother): the kernel with the
         # largest share of the iteration, from the per-kernel table
